@@ -1,0 +1,413 @@
+"""Benchmark: exhaustive enumeration of a BASELINE lattice on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5]
+                    [--impl b200|reference]
+
+One step = one full pass of the hot path over the workload: enumerate all
+2^N configurations of the lattice into g(M, E) (K1), combine the per-GPU
+tables (one NCCL reduce when N > 1) and evaluate the config's thermodynamic
+grid from the table (K2, fp64).  The index space is sharded by
+`make_shards` (top log2(P) bits for P = 2^k), so total work is fixed as the
+GPU count grows ("scaling": "strong").
+
+Timing follows the harness contract: W untimed warm-up steps, then K timed
+steps, each bracketed by CUDA events on the launching stream, with the L2
+flushed (a 256 MiB write) between steps outside the events; max over ranks.
+`e2e` repeats the step through the public API with host buffers
+(`enumerate_shard` -> host table, host -> device -> NCCL reduce for N > 1,
+`thermo_grid` from the host table), host<->device copies inside the timed
+region.  `--impl reference` times the reference algorithm on the host cores
+(the oracle's numpy restatement of enumeration.py:167-235; the reference
+is pure Python and cannot be installed on the GPU box).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "spin configurations enumerated/sec"
+UNIT = "configs/s"
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0,
+                   help="target CPU work of the cpu_baseline sample")
+    p.add_argument("--calibrate", action="store_true", default=True)
+    p.add_argument("--extra-configs", default="c1,c2,c3,c4",
+                   help="other configs timed (value only) into extra.configs")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------
+# CPU reference (oracle port of the reference algorithm)
+# --------------------------------------------------------------------------
+
+def port_lattice(wl):
+    from oracle import port
+    s = wl.spec
+    return port.Lattice(s.rows, s.cols, s.depth, s.coupling, s.periodic,
+                        list(s.bond_signs) if s.bond_signs else None)
+
+
+def cpu_sample_size(lat, cores, seconds):
+    """Per-process index count so `cores` processes take ~`seconds`."""
+    from oracle import port
+    probe = 1 << 18
+    t0 = time.perf_counter()
+    port.enumerate_range(lat, 0, probe)
+    per = (time.perf_counter() - t0) / probe
+    n = int(seconds / per)
+    n = max(1 << 16, min(n, (1 << lat.n) // cores))
+    return n, per
+
+
+def cpu_baseline(wl, seconds):
+    from oracle import port
+    lat = port_lattice(wl)
+    cores = port.cores()
+    per_proc, _ = cpu_sample_size(lat, 1, seconds)
+    rate, wall, procs = port.sample_rate(lat, per_proc, cores)
+    proxy = "" if wl.spec.uniform else (
+        " (algorithm: the reference's walk on bond-offset masks; the "
+        "reference itself cannot express this lattice)")
+    return {
+        "value": rate, "unit": UNIT, "cores": procs, "kind": "port",
+        "sample": f"{procs} processes x {per_proc} indices of {wl.name} at "
+                  f"k*2^N/{procs}, wall {wall:.2f} s{proxy}",
+    }
+
+
+def run_reference(args, wl):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import port
+    lat = port_lattice(wl)
+    cores = port.cores()
+    # each step: all host cores on a bounded slice, ~ a few seconds
+    per_proc, _ = cpu_sample_size(lat, 1, 4.0)
+    for _ in range(args.warmup):
+        port.sample_rate(lat, max(per_proc // 8, 1 << 16), cores)
+    rates, walls = [], []
+    for _ in range(args.steps):
+        r, w, procs = port.sample_rate(lat, per_proc, cores)
+        rates.append(r)
+        walls.append(w)
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * statistics.median(walls),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "int64", "data": "synthetic (exhaustive index space)",
+        "config": {"workload": f"{wl.name}: {wl.description}",
+                   "sample_per_step": f"{cores} x {per_proc} indices"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores,
+                         "kind": "port",
+                         "sample": f"{cores} processes x {per_proc} indices "
+                                   f"per step at k*2^N/{cores}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------
+# clocks
+# --------------------------------------------------------------------------
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,"
+             "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in out.splitlines():
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+
+def run_b200(args, wl):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1110_2561_b200 as isd
+    from paper_1110_2561_b200 import _native
+    from paper_1110_2561_b200.enumeration import native_lattice
+    from paper_1110_2561_b200.workloads import canonical_ops, workloads
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    isd.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def device_step_fn(w):
+        spec = w.spec
+        lat = native_lattice(spec)
+        shard = isd.make_shards(spec, world)[rank]
+        table = torch.zeros((spec.num_spins + 1) * (spec.num_bonds + 1),
+                            dtype=torch.int64, device=dev)
+        fields = torch.tensor(w.fields, dtype=torch.float64, device=dev)
+        temps = torch.tensor(w.temps, dtype=torch.float64, device=dev)
+        out = torch.empty(len(w.fields) * len(w.temps) * 7,
+                          dtype=torch.float64, device=dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+
+        def step():
+            ev[0].record(stream)
+            nl = _native.enumerate_device(lat, shard.start_index,
+                                          shard.end_index, table.data_ptr(),
+                                          sp, accumulate=False)
+            ev[1].record(stream)
+            if world > 1:
+                dist.reduce(table, dst=0)
+            if rank == 0:
+                nl += _native.thermo_device(
+                    table.data_ptr(), spec.num_spins, spec.num_bonds,
+                    abs(spec.coupling), fields.data_ptr(), len(w.fields),
+                    temps.data_ptr(), len(w.temps), out.data_ptr(), sp)
+            ev[2].record(stream)
+            return nl
+
+        return step, ev, table, out
+
+    def time_device(w, steps, warmup):
+        step, ev, table, out = device_step_fn(w)
+        for _ in range(warmup):
+            step()
+        barrier()
+        tot, k1 = [], []
+        launches = 0
+        l0 = _native.launch_count()
+        for _ in range(steps):
+            flush.zero_()
+            barrier()
+            launches += step()
+            ev[2].synchronize()
+            tot.append(ev[0].elapsed_time(ev[2]))
+            k1.append(ev[0].elapsed_time(ev[1]))
+        barrier()
+        launches_lib = _native.launch_count() - l0
+        return tot, k1, launches_lib, table, out
+
+    # ---- headline workload -------------------------------------------------
+    cal = {}
+    if args.calibrate:
+        names = {0: "popc", 1: "lop3", 2: "iadd3x2", 3: "red_shared_spread",
+                 4: "red_shared_hashed", 5: "imad", 6: "shf"}
+        for which, name in names.items():
+            lanes, mhz = _native.calibrate(which)
+            cal[name] = {"lanes_per_clk_sm": round(lanes, 3),
+                         "sm_mhz": round(mhz, 1)}
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    tot, k1, launches, table, out = time_device(wl, args.steps, args.warmup)
+    clk = clocks.stop()
+
+    ms_step = max_over_ranks(sum(tot) / len(tot))
+    ms_k1 = max_over_ranks(sum(k1) / len(k1))
+    n_cfg = wl.spec.num_configs
+    value = n_cfg / (ms_step / 1e3)
+
+    # correctness gate on the timed result
+    ok = None
+    if rank == 0:
+        hist = isd.DoSHistogram(wl.spec, table.cpu().numpy().reshape(
+            wl.spec.num_spins + 1, wl.spec.num_bonds + 1))
+        ok = isd.verify_dos(hist).passed
+
+    # ---- e2e through the public API with host buffers ---------------------
+    def e2e_step():
+        shard = isd.make_shards(wl.spec, world)[rank]
+        part = isd.enumerate_shard(wl.spec, None, shard)
+        if world > 1:
+            t = torch.from_numpy(part.counts).to(dev)
+            dist.reduce(t, dst=0)
+            counts = t.cpu().numpy() if rank == 0 else None
+            hist = isd.DoSHistogram(wl.spec, counts) if rank == 0 else None
+        else:
+            hist = part
+        if rank == 0:
+            isd.thermo_grid(hist, wl.fields, wl.temps)
+
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    barrier()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        barrier()
+        t0 = time.perf_counter()
+        e2e_step()
+        barrier()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_step_ms = max_over_ranks(statistics.mean(e2e_ms))
+    table_bytes = (wl.spec.num_spins + 1) * (wl.spec.num_bonds + 1) * 8
+    npts = len(wl.fields) * len(wl.temps)
+    lat_bytes = 208  # sizeof(isd_lattice), passed by value to the kernels
+    h2d = lat_bytes + (table_bytes if world > 1 else 0) + \
+        (table_bytes + 8 * (len(wl.fields) + len(wl.temps)) if rank == 0 else 0)
+    d2h = table_bytes + (table_bytes if world > 1 and rank == 0 else 0) + \
+        (npts * 7 * 8 if rank == 0 else 0)
+
+    # ---- other configs (value only, same protocol, fewer steps) -----------
+    extra = {}
+    for name in [c for c in args.extra_configs.split(",") if c]:
+        w2 = workloads()[name]
+        t2, _, _, _, _ = time_device(w2, max(3, args.steps // 2), 3)
+        ms2 = max_over_ranks(sum(t2) / len(t2))
+        extra[name] = {"configs_per_s": w2.spec.num_configs / (ms2 / 1e3),
+                       "ms_per_step": ms2}
+
+    if world > 1:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+
+    # ---- roofline ------------------------------------------------------------
+    sm_count = _native.sm_count(local)
+    popc_ops, alu_ops = canonical_ops(wl.spec)
+    roof = {"bound": "int-pipe", "unit": "Gconf/s", "traffic": None}
+    mhz = clk.get("sm_mhz") or None
+    if cal and mhz:
+        p_popc = cal["popc"]["lanes_per_clk_sm"]
+        p_alu = cal["lop3"]["lanes_per_clk_sm"]
+        peak = sm_count * mhz * 1e6 * min(p_alu / alu_ops, p_popc / popc_ops)
+        ach = (n_cfg / world) / (ms_k1 / 1e3)
+        roof.update({
+            "achieved": ach / 1e9, "peak": peak / 1e9, "frac": ach / peak,
+            "formula": "n_SM * f_SM * min(P_alu/ALU_ops, P_popc/POPC_ops) "
+                       "(BASELINE.md §4), canonical ops per config "
+                       f"POPC={popc_ops} ALU={alu_ops}; P measured by K0 on "
+                       "this GPU; f_SM = median SM clock under load",
+            "kernel": "k1_hoisted", "kernel_ms": ms_k1,
+            "p_popc": p_popc, "p_alu": p_alu, "sm_count": sm_count,
+            "f_sm_mhz": mhz,
+        })
+        # the resource the hoisted kernel actually spends: one shared
+        # reduction per configuration
+        p_red = cal["red_shared_hashed"]["lanes_per_clk_sm"]
+        roof["red_shared_frac"] = ach / (sm_count * mhz * 1e6 * p_red)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic (exhaustive 2^N index space; no inputs)",
+        "config": {"workload": f"{wl.name}: {wl.description}",
+                   "n_configs": n_cfg, "thermo_points": npts,
+                   "parallelism": f"index-space shards x{world}",
+                   "l2": "flushed (256 MiB write) between timed steps",
+                   "verify_dos_passed": ok},
+        "roofline": roof,
+        "e2e": {"value": n_cfg / (e2e_step_ms / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_step_ms},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "calibration": cal,
+        "extra": {"configs": extra},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(wl, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse_args()
+    from paper_1110_2561_b200.workloads import workloads
+    wl = workloads()[args.config]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+    return run_b200(args, wl)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,163 @@
+/*
+ * isingdos_b200.h — C ABI of the B200 exact-enumeration engine.
+ *
+ * The reference (`isingdos`, /root/reference/pkg/src/isingdos) is pure
+ * Python/numpy and has no FFI; its hot path is
+ *
+ *   enumerate_shard(spec, tables, shard, batch_size)   enumeration.py:208-235
+ *     -> _classify_batch(...)                          enumeration.py:167-205
+ *     -> np.bincount accumulate                        enumeration.py:232-234
+ *   full_dos_timed / full_dos (Pool driver + root sum) enumeration.py:365-396
+ *   partition_point / thermo_sweep                     thermo.py:46-100
+ *
+ * Each entry point below replaces one of those loops; the call a
+ * maintainer would add to the reference (ctypes) is shown in
+ * INTEGRATION.md.  Conventions:
+ *   - plain pointers and sizes only; no torch / CUDA runtime types;
+ *   - every function returns 0 on success and a negative ISD_E* code on
+ *     failure, with a message in isd_last_error() (thread-local);
+ *   - host output buffers are caller-owned and fully overwritten;
+ *   - `stream` arguments are cudaStream_t passed as void* (NULL = legacy
+ *     default stream of the current device);
+ *   - the library never keeps caller pointers.
+ *
+ * Lattice description.  The reference's geometry (LatticeSpec,
+ * lattice.py:34-119, and oracle.bond_pairs, oracle.py:40-58) is compiled on
+ * the host into at most ISD_MAX_CLASSES "bond classes".  A class is a shift
+ * s and two N-bit masks: bit i of bond_mask says bond (i, i+s) exists, bit i
+ * of jneg_mask says that bond has negative sign (it is unsatisfied when the
+ * two spins are ALIGNED).  For configuration index x (bit i = spin of site i,
+ * 1 = up; lattice.py:1-13):
+ *
+ *   m_idx = popcount(x)                                   (= (M+N)/2)
+ *   e_idx = sum_c popcount(((x ^ (x >> s_c)) ^ jneg_c) & bond_c)
+ *
+ * e_idx counts unsatisfied bonds, E = |J| (2 e_idx - B): identical to the
+ * reference's column index (enumeration.py:95-121, 232-233).  Counts are
+ * written as a dense row-major uint64 table counts[m_idx][e_idx] of shape
+ * (N+1) x (B+1) — the reference's DoSHistogram.counts layout.
+ */
+#ifndef ISINGDOS_B200_H
+#define ISINGDOS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ISD_ABI_VERSION 1
+#define ISD_MAX_CLASSES 8
+#define ISD_MAX_SPINS 40   /* lattice.py:24 MAX_SPINS */
+
+/* error codes */
+#define ISD_OK 0
+#define ISD_EINVAL (-1)   /* bad argument (range, lattice, sizes)        */
+#define ISD_ECUDA (-2)    /* CUDA runtime failure                        */
+#define ISD_ENODEV (-3)   /* no CUDA device / bad device ordinal          */
+#define ISD_ENOMEM (-4)   /* device allocation failed                     */
+
+/* enumeration algorithms (isd_enumerate*.algo) */
+#define ISD_ALGO_AUTO 0       /* hoisted kernel for the aligned body, canonical head/tail */
+#define ISD_ALGO_CANONICAL 1  /* one full class-mask evaluation per configuration */
+#define ISD_ALGO_HOISTED 2    /* same as AUTO; errors if the lattice is too small */
+
+typedef struct isd_bond_class {
+  uint32_t shift;     /* partner offset s, 1 <= s < N                    */
+  uint32_t reserved;  /* must be 0                                       */
+  uint64_t bond_mask; /* bit i: bond (i, i+s) exists (i+s < N)           */
+  uint64_t jneg_mask; /* bit i: that bond is antiferro (subset of bond)  */
+} isd_bond_class;
+
+typedef struct isd_lattice {
+  uint32_t n_spins;   /* N, 1..40                                        */
+  uint32_t n_bonds;   /* B = sum_c popcount(bond_mask_c)                 */
+  uint32_t n_classes; /* 1..ISD_MAX_CLASSES                              */
+  uint32_t reserved;  /* must be 0                                       */
+  isd_bond_class classes[ISD_MAX_CLASSES];
+} isd_lattice;
+
+/* ---- enumeration (replaces enumerate_shard, enumeration.py:208-235) ---- */
+
+/* Host-buffer call: walks [start, end) on `device`, writes the exact
+ * (N+1)*(B+1) table to counts_host (zeroed first).  Synchronous.  Returns the
+ * device time of the kernels in *device_ms when non-NULL. */
+int isd_enumerate(const isd_lattice* lat, uint64_t start, uint64_t end,
+                  int device, int algo, uint64_t* counts_host,
+                  double* device_ms);
+
+/* Device-buffer call: accumulates (accumulate=1) or overwrites
+ * (accumulate=0) the table at counts_dev (device memory of the current
+ * device) on `stream`.  Asynchronous; *launches receives the number of
+ * kernels enqueued when non-NULL. */
+int isd_enumerate_async(const isd_lattice* lat, uint64_t start, uint64_t end,
+                        int algo, uint64_t* counts_dev, int accumulate,
+                        void* stream, int* launches);
+
+/* ---- thermodynamics (replaces partition_point/thermo_sweep, thermo.py:46-100)
+ * For every (field f, temperature t) pair, in field-major order
+ * (index = f*n_temps + t), writes ISD_THERMO_FIELDS doubles:
+ *   [log_z, free_energy, internal_energy, specific_heat,
+ *    mean_magnetization, susceptibility, mean_abs_magnetization]
+ * following thermo.py:65-77 (max-shifted log-sum-exp over occupied cells,
+ * central second moments).  energy_scale = |J|.  Temperatures must be > 0
+ * (validated by the caller, thermo.py:56-58). */
+#define ISD_THERMO_FIELDS 7
+
+int isd_thermo(const uint64_t* counts_host, uint32_t n_spins, uint32_t n_bonds,
+               double energy_scale, const double* fields, int n_fields,
+               const double* temps, int n_temps, int device, double* out_host,
+               double* device_ms);
+
+int isd_thermo_async(const uint64_t* counts_dev, uint32_t n_spins,
+                     uint32_t n_bonds, double energy_scale,
+                     const double* fields_dev, int n_fields,
+                     const double* temps_dev, int n_temps, double* out_dev,
+                     void* stream);
+
+/* ---- host-side plan (no GPU needed; used by the CPU tests) ----------- */
+
+/* The hoisted kernel's decomposition of the lattice.
+ * u low sites are unrolled ("copy" sites), the next l sites are the
+ * per-thread loop, the rest is the per-thread run prefix. */
+#define ISD_COPY_BITS 5
+typedef struct isd_plan_info {
+  uint32_t u, l, k;          /* k = u + l                               */
+  uint32_t stride;           /* B + 1                                   */
+  uint64_t run_mask_above_k; /* bits [k, N)                             */
+  uint64_t var_mask;         /* bits [u, k)                             */
+  int32_t  copy_degree[ISD_COPY_BITS];   /* d_p: bonds from p to sites >= u */
+  uint64_t copy_nbr1[ISD_COPY_BITS];     /* partner masks (first copy)    */
+  uint64_t copy_jneg1[ISD_COPY_BITS];    /* partner sign masks            */
+  uint64_t copy_nbr2[ISD_COPY_BITS];     /* second copy (double bonds)    */
+  uint64_t copy_jneg2[ISD_COPY_BITS];
+  int32_t  copy_table[1 << ISD_COPY_BITS]; /* KT[c] = popc(c)(B+1) + CT-CT unsat */
+} isd_plan_info;
+
+int isd_plan(const isd_lattice* lat, uint64_t n_configs_hint,
+             isd_plan_info* out);
+
+/* Validate a lattice descriptor without touching a GPU. */
+int isd_validate(const isd_lattice* lat);
+
+/* ---- calibration microbenchmarks (K0) -------------------------------- */
+/* which: 0 = POPC, 1 = LOP3, 2 = IADD3, 3 = RED.shared spread,
+ *        4 = RED.shared realistic bins, 5 = IMAD.  Writes lanes per clock
+ *        per SM to *lanes_per_clk_sm and the SM clock seen (MHz). */
+int isd_calibrate(int device, int which, double* lanes_per_clk_sm,
+                  double* sm_mhz);
+
+/* ---- misc ------------------------------------------------------------ */
+int isd_device_count(void);
+int isd_sm_count(int device);
+const char* isd_last_error(void);
+const char* isd_version(void);
+int isd_abi_version(void);
+/* Kernels launched by this process since load (all entry points). */
+uint64_t isd_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ISINGDOS_B200_H */

@@ -1,0 +1,248 @@
+"""ctypes binding of the C ABI in include/isingdos_b200.h.
+
+This is the only place Python touches the native engine.  There is no CPU
+fallback: if the library is missing the import of any compute entry point
+raises, and if no GPU is present the compute calls raise RuntimeError with
+the library's own message.
+"""
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from ._build import LIB
+
+ISD_MAX_CLASSES = 8
+ISD_COPY_BITS = 5
+ISD_THERMO_FIELDS = 7
+
+ALGO_AUTO = 0
+ALGO_CANONICAL = 1
+ALGO_HOISTED = 2
+
+EXPORTED_SYMBOLS = (
+    "isd_enumerate", "isd_enumerate_async", "isd_thermo", "isd_thermo_async",
+    "isd_plan", "isd_validate", "isd_calibrate", "isd_device_count",
+    "isd_sm_count", "isd_last_error", "isd_version", "isd_abi_version",
+    "isd_launch_count",
+)
+
+
+class BondClass(ctypes.Structure):
+    _fields_ = [("shift", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("bond_mask", ctypes.c_uint64), ("jneg_mask", ctypes.c_uint64)]
+
+
+class Lattice(ctypes.Structure):
+    _fields_ = [("n_spins", ctypes.c_uint32), ("n_bonds", ctypes.c_uint32),
+                ("n_classes", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("classes", BondClass * ISD_MAX_CLASSES)]
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("u", ctypes.c_uint32), ("l", ctypes.c_uint32), ("k", ctypes.c_uint32),
+        ("stride", ctypes.c_uint32),
+        ("run_mask_above_k", ctypes.c_uint64), ("var_mask", ctypes.c_uint64),
+        ("copy_degree", ctypes.c_int32 * ISD_COPY_BITS),
+        ("copy_nbr1", ctypes.c_uint64 * ISD_COPY_BITS),
+        ("copy_jneg1", ctypes.c_uint64 * ISD_COPY_BITS),
+        ("copy_nbr2", ctypes.c_uint64 * ISD_COPY_BITS),
+        ("copy_jneg2", ctypes.c_uint64 * ISD_COPY_BITS),
+        ("copy_table", ctypes.c_int32 * (1 << ISD_COPY_BITS)),
+    ]
+
+
+class NativeError(RuntimeError):
+    """A failure reported by the native engine (CUDA error, no device...)."""
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def library_path() -> str:
+    return os.environ.get("ISD_LIBRARY", LIB)
+
+
+def load():
+    """Load (once) and return the ctypes handle; raise if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        path = library_path()
+        if not os.path.exists(path):
+            raise ImportError(
+                f"isingdos-b200 native library not found at {path}; build it "
+                f"with `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(path)
+        u64, i32, dbl = ctypes.c_uint64, ctypes.c_int, ctypes.c_double
+        p_lat = ctypes.POINTER(Lattice)
+        p_u64 = ctypes.POINTER(ctypes.c_uint64)
+        p_dbl = ctypes.POINTER(ctypes.c_double)
+        vp = ctypes.c_void_p
+        lib.isd_enumerate.argtypes = [p_lat, u64, u64, i32, i32, p_u64, p_dbl]
+        lib.isd_enumerate_async.argtypes = [p_lat, u64, u64, i32, vp, i32, vp,
+                                            ctypes.POINTER(ctypes.c_int)]
+        lib.isd_thermo.argtypes = [p_u64, ctypes.c_uint32, ctypes.c_uint32,
+                                   dbl, p_dbl, i32, p_dbl, i32, i32, p_dbl,
+                                   p_dbl]
+        lib.isd_thermo_async.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32,
+                                         dbl, vp, i32, vp, i32, vp, vp]
+        lib.isd_plan.argtypes = [p_lat, u64, ctypes.POINTER(PlanInfo)]
+        lib.isd_validate.argtypes = [p_lat]
+        lib.isd_calibrate.argtypes = [i32, i32, p_dbl, p_dbl]
+        lib.isd_sm_count.argtypes = [i32]
+        lib.isd_last_error.restype = ctypes.c_char_p
+        lib.isd_version.restype = ctypes.c_char_p
+        lib.isd_launch_count.restype = ctypes.c_uint64
+        for name in ("isd_enumerate", "isd_enumerate_async", "isd_thermo",
+                     "isd_thermo_async", "isd_plan", "isd_validate",
+                     "isd_calibrate", "isd_device_count", "isd_sm_count",
+                     "isd_abi_version"):
+            getattr(lib, name).restype = ctypes.c_int
+        if lib.isd_abi_version() != 1:
+            raise ImportError("isingdos-b200 ABI version mismatch")
+        _lib = lib
+        return lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = load().isd_last_error().decode(errors="replace")
+        if rc == -1:
+            raise ValueError(msg)
+        raise NativeError(f"isingdos-b200 native error {rc}: {msg}")
+
+
+def make_lattice(n_spins, n_bonds, classes) -> Lattice:
+    """classes: iterable of (shift, bond_mask, jneg_mask)."""
+    classes = list(classes)
+    if not 1 <= len(classes) <= ISD_MAX_CLASSES:
+        raise ValueError(f"{len(classes)} bond classes (1..{ISD_MAX_CLASSES})")
+    lat = Lattice()
+    lat.n_spins = n_spins
+    lat.n_bonds = n_bonds
+    lat.n_classes = len(classes)
+    for i, (s, m, j) in enumerate(classes):
+        lat.classes[i].shift = s
+        lat.classes[i].bond_mask = m
+        lat.classes[i].jneg_mask = j
+    return lat
+
+
+def _default_device() -> int:
+    env = os.environ.get("ISD_DEVICE")
+    if env:
+        return int(env)
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+_device = None
+
+
+def set_device(device: int) -> None:
+    global _device
+    _device = int(device)
+
+
+def current_device() -> int:
+    return _device if _device is not None else _default_device()
+
+
+def device_count() -> int:
+    return int(load().isd_device_count())
+
+
+def enumerate_host(lat: Lattice, start: int, end: int, device=None,
+                   algo: int = ALGO_AUTO):
+    """Run the enumeration into a fresh host table; (uint64 table, device ms)."""
+    lib = load()
+    out = np.zeros((lat.n_spins + 1) * (lat.n_bonds + 1), dtype=np.uint64)
+    ms = ctypes.c_double(0.0)
+    dev = current_device() if device is None else device
+    check(lib.isd_enumerate(ctypes.byref(lat), start, end, dev, algo,
+                            out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                            ctypes.byref(ms)))
+    return out.reshape(lat.n_spins + 1, lat.n_bonds + 1), ms.value
+
+
+def enumerate_device(lat: Lattice, start: int, end: int, counts_ptr: int,
+                     stream_ptr: int, accumulate: bool = False,
+                     algo: int = ALGO_AUTO) -> int:
+    """Enqueue on a device table (raw pointer) and stream; returns launches."""
+    lib = load()
+    nl = ctypes.c_int(0)
+    check(lib.isd_enumerate_async(ctypes.byref(lat), start, end, algo,
+                                  ctypes.c_void_p(counts_ptr), int(accumulate),
+                                  ctypes.c_void_p(stream_ptr),
+                                  ctypes.byref(nl)))
+    return nl.value
+
+
+def thermo_host(counts, n_spins, n_bonds, scale, fields, temps, device=None):
+    """fp64 thermodynamics of a host table; returns (array[F, T, 7], ms)."""
+    lib = load()
+    c = np.ascontiguousarray(counts, dtype=np.uint64)
+    f = np.ascontiguousarray(fields, dtype=np.float64)
+    t = np.ascontiguousarray(temps, dtype=np.float64)
+    out = np.empty((len(f), len(t), ISD_THERMO_FIELDS), dtype=np.float64)
+    ms = ctypes.c_double(0.0)
+    dev = current_device() if device is None else device
+    pd = ctypes.POINTER(ctypes.c_double)
+    check(lib.isd_thermo(c.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                         n_spins, n_bonds, float(scale), f.ctypes.data_as(pd),
+                         len(f), t.ctypes.data_as(pd), len(t), dev,
+                         out.ctypes.data_as(pd), ctypes.byref(ms)))
+    return out, ms.value
+
+
+def thermo_device(counts_ptr, n_spins, n_bonds, scale, fields_ptr, n_fields,
+                  temps_ptr, n_temps, out_ptr, stream_ptr) -> int:
+    lib = load()
+    check(lib.isd_thermo_async(ctypes.c_void_p(counts_ptr), n_spins, n_bonds,
+                               float(scale), ctypes.c_void_p(fields_ptr),
+                               n_fields, ctypes.c_void_p(temps_ptr), n_temps,
+                               ctypes.c_void_p(out_ptr),
+                               ctypes.c_void_p(stream_ptr)))
+    return 1 if n_fields * n_temps > 0 else 0
+
+
+def plan(lat: Lattice, n_configs_hint: int) -> tuple:
+    """Host-side hoisted-kernel plan (no GPU needed): (usable, PlanInfo)."""
+    lib = load()
+    info = PlanInfo()
+    rc = lib.isd_plan(ctypes.byref(lat), n_configs_hint, ctypes.byref(info))
+    if rc < 0:
+        check(rc)
+    return rc == 0, info
+
+
+def validate(lat: Lattice) -> None:
+    check(load().isd_validate(ctypes.byref(lat)))
+
+
+def calibrate(which: int, device=None):
+    lib = load()
+    lanes = ctypes.c_double(0.0)
+    mhz = ctypes.c_double(0.0)
+    dev = current_device() if device is None else device
+    check(lib.isd_calibrate(dev, which, ctypes.byref(lanes), ctypes.byref(mhz)))
+    return lanes.value, mhz.value
+
+
+def launch_count() -> int:
+    return int(load().isd_launch_count())
+
+
+def sm_count(device=None) -> int:
+    dev = current_device() if device is None else device
+    v = load().isd_sm_count(dev)
+    if v < 0:
+        check(v)
+    return v

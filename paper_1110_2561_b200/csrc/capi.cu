@@ -1,0 +1,392 @@
+// C ABI of the B200 enumeration engine (include/isingdos_b200.h).
+//
+// Host-side orchestration only: argument validation, range splitting into
+// run-aligned bodies and unaligned head/tail pieces, per-device cached
+// streams and buffers, error strings.  All counting happens in the kernels
+// of enumerate.cu / thermo.cu; there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "isd_internal.h"
+
+namespace isd {
+
+static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+static std::mutex g_mu;
+
+uint64_t bump_launches(uint64_t n) { return g_launches += n; }
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  return fail(e == cudaErrorMemoryAllocation ? ISD_ENOMEM : ISD_ECUDA,
+              "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+static long env_long(const char* name, long dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  char* end = nullptr;
+  long x = std::strtol(v, &end, 10);
+  return (end && *end == 0) ? x : dflt;
+}
+
+uint32_t hist_words_for(uint32_t nbins) { return (nbins + 31u) & ~31u; }
+
+int hist_count_for(uint32_t hist_words) {
+  // Shared-memory budget per block for the histograms.  Three 72 KB blocks
+  // of 512 threads fill an SM's 228 KB.  Tunable for experiments.
+  const long budget = env_long("ISD_HIST_BYTES", 72 * 1024);
+  long n = budget / (long)(hist_words * 4);
+  const long cap = env_long("ISD_NHIST_MAX", 16);
+  if (n > cap) n = cap;
+  if (n < 1) n = 1;
+  return (int)n;
+}
+
+struct DevState {
+  bool init = false;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  unsigned long long* d_counts = nullptr;  // (41 x 121) max table
+  size_t d_counts_bytes = 0;
+  double* d_buf = nullptr;  // thermo fields/temps/out
+  size_t d_buf_bytes = 0;
+};
+static DevState g_dev[64];
+
+static int get_dev(int device, DevState** out) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(ISD_ENODEV, "no CUDA device available (%s)",
+                e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+  if (device < 0 || device >= ndev || device >= 64)
+    return fail(ISD_ENODEV, "device %d outside [0, %d)", device, ndev);
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  DevState& s = g_dev[device];
+  if (!s.init) {
+    e = cudaDeviceGetAttribute(&s.sm_count, cudaDevAttrMultiProcessorCount,
+                               device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+    e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+    cudaEventCreate(&s.ev0);
+    cudaEventCreate(&s.ev1);
+    s.init = true;
+  }
+  *out = &s;
+  return ISD_OK;
+}
+
+static int current_sm_count(int* sms) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  e = cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  return ISD_OK;
+}
+
+// At most 2^38 configurations per launch: with >= 148 CTAs no CTA counts
+// more than ~1.9e9 < 2^32 configurations into its u32 shared histograms.
+static constexpr uint64_t kMaxPerLaunch = 1ull << 38;
+
+static int enqueue_canonical(const isd_lattice* lat, uint64_t a, uint64_t b,
+                             unsigned long long* out, int sms,
+                             cudaStream_t st, bool small_grid, int* nl) {
+  CanonParams p;
+  fill_canon(lat, &p);
+  while (a < b) {
+    const uint64_t e = (b - a > kMaxPerLaunch) ? a + kMaxPerLaunch : b;
+    p.start = a;
+    p.end = e;
+    int r = launch_canonical(p, out, sms, st, small_grid);
+    if (r < 0) return cuda_fail((cudaError_t)(-r), "k1_canonical launch");
+    *nl += r;
+    a = e;
+  }
+  return ISD_OK;
+}
+
+static int enumerate_impl(const isd_lattice* lat, uint64_t start,
+                          uint64_t end, int algo, unsigned long long* out,
+                          int accumulate, cudaStream_t st, int* launches) {
+  char err[256];
+  int rc = validate_lattice(lat, err, sizeof err);
+  if (rc) return fail(rc, "%s", err);
+  const uint64_t total = 1ull << lat->n_spins;
+  if (!(start <= end && end <= total))
+    return fail(ISD_EINVAL, "range [%llu, %llu) invalid for 2^%u configurations",
+                (unsigned long long)start, (unsigned long long)end,
+                lat->n_spins);
+  if (algo < ISD_ALGO_AUTO || algo > ISD_ALGO_HOISTED)
+    return fail(ISD_EINVAL, "unknown algo %d", algo);
+  if (!out) return fail(ISD_EINVAL, "counts pointer is NULL");
+  const size_t bytes =
+      (size_t)(lat->n_spins + 1) * (lat->n_bonds + 1) * sizeof(uint64_t);
+  int nl = 0;
+  if (!accumulate) {
+    cudaError_t e = cudaMemsetAsync(out, 0, bytes, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  }
+  if (start == end) {
+    if (launches) *launches = 0;
+    return ISD_OK;
+  }
+  int sms = 0;
+  rc = current_sm_count(&sms);
+  if (rc) return rc;
+
+  if (algo == ISD_ALGO_CANONICAL) {
+    rc = enqueue_canonical(lat, start, end, out, sms, st, false, &nl);
+    if (launches) *launches = nl;
+    return rc;
+  }
+  isd_plan_info info;
+  const int too_small = compile_plan(lat, end - start, &info);
+  if (too_small) {
+    if (algo == ISD_ALGO_HOISTED)
+      return fail(ISD_EINVAL, "lattice of %u spins too small for the hoisted "
+                  "kernel", lat->n_spins);
+    rc = enqueue_canonical(lat, start, end, out, sms, st, true, &nl);
+    if (launches) *launches = nl;
+    return rc;
+  }
+  const uint32_t k = info.k;
+  const uint64_t r0 = (start + ((1ull << k) - 1)) >> k;
+  const uint64_t r1 = end >> k;
+  if (r0 >= r1) {
+    rc = enqueue_canonical(lat, start, end, out, sms, st, true, &nl);
+    if (launches) *launches = nl;
+    return rc;
+  }
+  // unaligned head and tail: fewer than 2^k configurations each
+  if (start < (r0 << k)) {
+    rc = enqueue_canonical(lat, start, r0 << k, out, sms, st, true, &nl);
+    if (rc) return rc;
+  }
+  HoistParams hp;
+  fill_hoist(lat, &info, &hp);
+  const uint64_t runs_per_launch = kMaxPerLaunch >> k;
+  for (uint64_t r = r0; r < r1;) {
+    const uint64_t re = (r1 - r > runs_per_launch) ? r + runs_per_launch : r1;
+    hp.run_begin = r;
+    hp.run_end = re;
+    int x = launch_hoisted(hp, out, sms, st);
+    if (x < 0) return cuda_fail((cudaError_t)(-x), "k1_hoisted launch");
+    nl += x;
+    r = re;
+  }
+  if ((r1 << k) < end) {
+    rc = enqueue_canonical(lat, r1 << k, end, out, sms, st, true, &nl);
+    if (rc) return rc;
+  }
+  if (launches) *launches = nl;
+  return ISD_OK;
+}
+
+}  // namespace isd
+
+using namespace isd;
+
+extern "C" {
+
+int isd_validate(const isd_lattice* lat) {
+  char err[256];
+  int rc = validate_lattice(lat, err, sizeof err);
+  if (rc) return fail(rc, "%s", err);
+  return ISD_OK;
+}
+
+int isd_plan(const isd_lattice* lat, uint64_t n_configs_hint,
+             isd_plan_info* out) {
+  int rc = isd_validate(lat);
+  if (rc) return rc;
+  if (!out) return fail(ISD_EINVAL, "plan pointer is NULL");
+  return compile_plan(lat, n_configs_hint, out);
+}
+
+int isd_enumerate_async(const isd_lattice* lat, uint64_t start, uint64_t end,
+                        int algo, uint64_t* counts_dev, int accumulate,
+                        void* stream, int* launches) {
+  int nl = 0;
+  int rc = enumerate_impl(lat, start, end, algo,
+                          reinterpret_cast<unsigned long long*>(counts_dev),
+                          accumulate, (cudaStream_t)stream, &nl);
+  bump_launches((uint64_t)nl);
+  if (launches) *launches = nl;
+  return rc;
+}
+
+int isd_enumerate(const isd_lattice* lat, uint64_t start, uint64_t end,
+                  int device, int algo, uint64_t* counts_host,
+                  double* device_ms) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  int rc = isd_validate(lat);
+  if (rc) return rc;
+  if (!counts_host) return fail(ISD_EINVAL, "counts pointer is NULL");
+  DevState* s = nullptr;
+  rc = get_dev(device, &s);
+  if (rc) return rc;
+  const size_t bytes =
+      (size_t)(lat->n_spins + 1) * (lat->n_bonds + 1) * sizeof(uint64_t);
+  if (s->d_counts_bytes < bytes) {
+    if (s->d_counts) cudaFree(s->d_counts);
+    s->d_counts = nullptr;
+    s->d_counts_bytes = 0;
+    cudaError_t e = cudaMalloc(&s->d_counts, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(counts)");
+    s->d_counts_bytes = bytes;
+  }
+  cudaEventRecord(s->ev0, s->stream);
+  int nl = 0;
+  rc = enumerate_impl(lat, start, end, algo, s->d_counts, 0, s->stream, &nl);
+  bump_launches((uint64_t)nl);
+  if (rc) return rc;
+  cudaEventRecord(s->ev1, s->stream);
+  cudaError_t e = cudaMemcpyAsync(counts_host, s->d_counts, bytes,
+                                  cudaMemcpyDeviceToHost, s->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(D2H)");
+  e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "enumeration kernels");
+  if (device_ms) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->ev0, s->ev1);
+    *device_ms = ms;
+  }
+  return ISD_OK;
+}
+
+int isd_thermo_async(const uint64_t* counts_dev, uint32_t n_spins,
+                     uint32_t n_bonds, double energy_scale,
+                     const double* fields_dev, int n_fields,
+                     const double* temps_dev, int n_temps, double* out_dev,
+                     void* stream) {
+  if (n_spins < 1 || n_spins > ISD_MAX_SPINS || n_bonds > 3 * ISD_MAX_SPINS)
+    return fail(ISD_EINVAL, "bad table shape N=%u B=%u", n_spins, n_bonds);
+  if (n_fields < 0 || n_temps < 0)
+    return fail(ISD_EINVAL, "negative grid size");
+  if (!(energy_scale > 0)) return fail(ISD_EINVAL, "energy_scale must be > 0");
+  if (!counts_dev || (n_fields * n_temps > 0 &&
+                      (!fields_dev || !temps_dev || !out_dev)))
+    return fail(ISD_EINVAL, "NULL buffer");
+  int r = launch_thermo(reinterpret_cast<const unsigned long long*>(counts_dev),
+                        n_spins, n_bonds, energy_scale, fields_dev, n_fields,
+                        temps_dev, n_temps, out_dev, stream);
+  if (r < 0) return cuda_fail((cudaError_t)(-r), "k2_thermo launch");
+  bump_launches((uint64_t)r);
+  return ISD_OK;
+}
+
+int isd_thermo(const uint64_t* counts_host, uint32_t n_spins, uint32_t n_bonds,
+               double energy_scale, const double* fields, int n_fields,
+               const double* temps, int n_temps, int device, double* out_host,
+               double* device_ms) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  if (n_spins < 1 || n_spins > ISD_MAX_SPINS || n_bonds > 3 * ISD_MAX_SPINS)
+    return fail(ISD_EINVAL, "bad table shape N=%u B=%u", n_spins, n_bonds);
+  if (!counts_host || !fields || !temps || !out_host)
+    return fail(ISD_EINVAL, "NULL buffer");
+  if (n_fields < 0 || n_temps < 0)
+    return fail(ISD_EINVAL, "negative grid size");
+  DevState* s = nullptr;
+  int rc = get_dev(device, &s);
+  if (rc) return rc;
+  const size_t tbytes = (size_t)(n_spins + 1) * (n_bonds + 1) * 8;
+  const size_t npts = (size_t)n_fields * n_temps;
+  const size_t dbytes = (n_fields + n_temps + npts * ISD_THERMO_FIELDS) * 8;
+  if (s->d_counts_bytes < tbytes) {
+    if (s->d_counts) cudaFree(s->d_counts);
+    s->d_counts = nullptr;
+    s->d_counts_bytes = 0;
+    cudaError_t e = cudaMalloc(&s->d_counts, tbytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(counts)");
+    s->d_counts_bytes = tbytes;
+  }
+  if (s->d_buf_bytes < dbytes) {
+    if (s->d_buf) cudaFree(s->d_buf);
+    s->d_buf = nullptr;
+    s->d_buf_bytes = 0;
+    cudaError_t e = cudaMalloc(&s->d_buf, dbytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(thermo)");
+    s->d_buf_bytes = dbytes;
+  }
+  double* d_f = s->d_buf;
+  double* d_t = d_f + n_fields;
+  double* d_o = d_t + n_temps;
+  cudaStream_t st = s->stream;
+  cudaMemcpyAsync(s->d_counts, counts_host, tbytes, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_f, fields, n_fields * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d_t, temps, n_temps * 8, cudaMemcpyHostToDevice, st);
+  cudaEventRecord(s->ev0, st);
+  rc = isd_thermo_async(reinterpret_cast<const uint64_t*>(s->d_counts),
+                        n_spins, n_bonds, energy_scale, d_f, n_fields, d_t,
+                        n_temps, d_o, st);
+  if (rc) return rc;
+  cudaEventRecord(s->ev1, st);
+  cudaError_t e = cudaMemcpyAsync(out_host, d_o, npts * ISD_THERMO_FIELDS * 8,
+                                  cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "thermo kernel");
+  if (device_ms) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, s->ev0, s->ev1);
+    *device_ms = ms;
+  }
+  return ISD_OK;
+}
+
+int isd_calibrate(int device, int which, double* lanes_per_clk_sm,
+                  double* sm_mhz) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  DevState* s = nullptr;
+  int rc = get_dev(device, &s);
+  if (rc) return rc;
+  if (which < 0 || which > 6) return fail(ISD_EINVAL, "unknown probe %d", which);
+  double lanes = 0, mhz = 0;
+  int r = run_calibration(which, s->sm_count, &lanes, &mhz);
+  if (r < 0) return cuda_fail((cudaError_t)(-r), "k0 calibration");
+  if (lanes_per_clk_sm) *lanes_per_clk_sm = lanes;
+  if (sm_mhz) *sm_mhz = mhz;
+  return ISD_OK;
+}
+
+int isd_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int isd_sm_count(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) !=
+      cudaSuccess)
+    return fail(ISD_ENODEV, "no device %d", device);
+  return v;
+}
+
+const char* isd_last_error(void) { return g_err.c_str(); }
+const char* isd_version(void) { return "isingdos-b200 0.1.0 (sm_100a)"; }
+int isd_abi_version(void) { return ISD_ABI_VERSION; }
+uint64_t isd_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

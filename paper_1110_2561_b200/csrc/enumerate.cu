@@ -1,0 +1,246 @@
+// K1 — exhaustive enumeration of Ising configurations into g(M, E) on sm_100a.
+//
+// Replaces the reference's batch loop
+//   enumerate_shard -> _classify_batch -> np.bincount
+//   (/root/reference/pkg/src/isingdos/enumeration.py:167-235)
+// with two integer kernels that share one histogram scheme:
+//
+//  * k1_canonical: one thread per configuration index (grid-stride), the
+//    full bond-class evaluation per index:
+//        m = popc(x),  e = sum_c popc(((x ^ x>>s_c) ^ jneg_c) & bond_c)
+//    Used for ranges not aligned to a run and for tiny lattices, and kept
+//    as the measured "canonical formulation" baseline.
+//
+//  * k1_hoisted: every configuration is still counted individually, but the
+//    work that does not change between neighbouring indices is hoisted:
+//    bits [k, N) are fixed per thread ("run"), bits [u, k) are the thread's
+//    loop counter, and the low u = 5 bits are 32 register copies.  Per group
+//    of 32 copies the kernel evaluates the loop-dependent bonds with
+//    LOP3/POPC over precomputed masks, derives each copy site's flip cost
+//    delta_p = d_p - 2 n_p, and then produces each copy's bin address with a
+//    single IADD3 (subset sum over the copy bits plus a per-lattice
+//    constant-bank table) followed by one shared-memory reduction.
+//
+// Counts go to shared-memory u32 histograms (one per group of warps),
+// flushed once per block into the per-GPU uint64 table with 64-bit global
+// atomics.  The host bounds the configurations per launch so no u32 counter
+// can wrap (capi.cu).
+#include <cuda_runtime.h>
+
+#include "isd_internal.h"
+
+namespace isd {
+
+__device__ __forceinline__ void red_shared_inc(uint32_t addr) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// Zero the block's histograms.
+__device__ __forceinline__ void zero_hist(uint32_t* hist, uint32_t words) {
+  uint4* h4 = reinterpret_cast<uint4*>(hist);
+  const uint32_t n4 = words / 4;
+  for (uint32_t i = threadIdx.x; i < n4; i += blockDim.x)
+    h4[i] = make_uint4(0, 0, 0, 0);
+}
+
+// Sum the block's histograms and add the nonzero bins to the global table.
+__device__ __forceinline__ void flush_hist(const uint32_t* hist,
+                                           uint32_t n_hist,
+                                           uint32_t hist_words, uint32_t nbins,
+                                           unsigned long long* out) {
+  for (uint32_t b = threadIdx.x; b < nbins; b += blockDim.x) {
+    unsigned long long s = 0;
+    for (uint32_t h = 0; h < n_hist; ++h) s += hist[h * hist_words + b];
+    if (s) atomicAdd(out + b, s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// canonical kernel
+// ---------------------------------------------------------------------------
+template <int NC, bool WIDE>
+__global__ void __launch_bounds__(kThreads)
+    k1_canonical(const __grid_constant__ CanonParams P,
+                 unsigned long long* __restrict__ out) {
+  extern __shared__ __align__(16) uint32_t hist[];
+  zero_hist(hist, P.n_hist * P.hist_words);
+  __syncthreads();
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t hbase =
+      smem_addr(hist + (warp % P.n_hist) * P.hist_words);
+  const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t x = P.start + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+       x < P.end; x += gstride) {
+    uint32_t m, e = 0;
+    if constexpr (WIDE) {
+      m = __popcll(x);
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        e += __popcll(((x ^ (x >> P.shift[c])) ^ P.jneg[c]) & P.mask[c]);
+    } else {
+      const uint32_t y = (uint32_t)x;
+      m = __popc(y);
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        e += __popc(((y ^ (y >> P.shift[c])) ^ (uint32_t)P.jneg[c]) &
+                    (uint32_t)P.mask[c]);
+    }
+    red_shared_inc(hbase + 4u * (m * P.stride + e));
+  }
+  __syncthreads();
+  flush_hist(hist, P.n_hist, P.hist_words, P.nbins, out);
+}
+
+// ---------------------------------------------------------------------------
+// hoisted kernel
+// ---------------------------------------------------------------------------
+template <int NC, bool DOUBLE>
+__global__ void __launch_bounds__(kThreads)
+    k1_hoisted(const __grid_constant__ HoistParams P,
+               unsigned long long* __restrict__ out) {
+  extern __shared__ __align__(16) uint32_t hist[];
+  zero_hist(hist, P.n_hist * P.hist_words);
+  __syncthreads();
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t hbase =
+      smem_addr(hist + (warp % P.n_hist) * P.hist_words);
+  const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+  const uint32_t nloop = 1u << P.l;
+
+  for (uint64_t r = P.run_begin + (uint64_t)blockIdx.x * blockDim.x +
+                    threadIdx.x;
+       r < P.run_end; r += gstride) {
+    // ---- per-run constants (bits [k, N) fixed) ----
+    const uint64_t xt = r << P.k;
+    int base_run = __popcll(xt) * (int)P.stride;
+    uint32_t cst[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const uint64_t sh = xt >> P.shift[c];
+      base_run += __popcll(((xt ^ sh) ^ P.jneg[c]) & P.mask[c] & P.above_k);
+      // partner word seen by the loop sites [u, k); jneg folded in
+      cst[c] = (uint32_t)sh ^ (uint32_t)P.jneg[c];
+    }
+    int npr[kCopyBits];
+#pragma unroll
+    for (int q = 0; q < kCopyBits; ++q) {
+      npr[q] = __popcll((xt ^ P.jn1[q]) & P.nm1[q] & P.above_k);
+      if constexpr (DOUBLE)
+        npr[q] += __popcll((xt ^ P.jn2[q]) & P.nm2[q] & P.above_k);
+      base_run += npr[q];
+    }
+    // ---- loop over bits [u, k) ----
+    for (uint32_t j = 0; j < nloop; ++j) {
+      const uint32_t jb = j << kCopyBits;
+      int base = base_run + __popc(j) * (int)P.stride;
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        base += __popc((jb ^ __funnelshift_rc(jb, 0u, P.shift[c]) ^ cst[c]) &
+                       P.mvar[c]);
+      int d[kCopyBits];
+#pragma unroll
+      for (int q = 0; q < kCopyBits; ++q) {
+        int nq = npr[q] + __popc((jb ^ P.jn1v[q]) & P.nm1v[q]);
+        if constexpr (DOUBLE) nq += __popc((jb ^ P.jn2v[q]) & P.nm2v[q]);
+        base += nq;
+        d[q] = 4 * (P.degree[q] - 2 * nq);
+      }
+      // ---- 32 copies: addr_c = addr_{c without top bit} + d_top + ktd[c]
+      uint32_t a[kCopies];
+      a[0] = hbase + 4u * (uint32_t)base + (uint32_t)P.ktd[0];
+      red_shared_inc(a[0]);
+#pragma unroll
+      for (int c = 1; c < kCopies; ++c) {
+        const int top = 31 - __clz(c);
+        a[c] = a[c ^ (1 << top)] + (uint32_t)d[top] + (uint32_t)P.ktd[c];
+        red_shared_inc(a[c]);
+      }
+    }
+  }
+  __syncthreads();
+  flush_hist(hist, P.n_hist, P.hist_words, P.nbins, out);
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static int blocks_for(const void* fn, size_t smem, int sm_count) {
+  int per_sm = 0;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads,
+                                                    smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  return per_sm * sm_count;
+}
+
+template <int NC, bool W>
+static int launch_canon_t(const CanonParams& p, unsigned long long* out,
+                          int sm_count, cudaStream_t st, bool small_grid) {
+  const size_t smem = (size_t)p.n_hist * p.hist_words * 4;
+  const void* fn = (const void*)k1_canonical<NC, W>;
+  int grid = blocks_for(fn, smem, sm_count);
+  const uint64_t n = p.end - p.start;
+  if (small_grid) {
+    const uint64_t need = (n + kThreads - 1) / kThreads;
+    if (need < (uint64_t)grid) grid = (int)(need ? need : 1);
+  }
+  k1_canonical<NC, W><<<grid, kThreads, smem, st>>>(p, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 1 : -(int)e;
+}
+
+int launch_canonical(const CanonParams& p, unsigned long long* out,
+                     int sm_count, void* stream, bool small_grid) {
+  cudaStream_t st = (cudaStream_t)stream;
+  // The 32-bit path is exact only when every site (and every bond) lives in
+  // the low word.
+  const bool wide = p.n_spins > 32;
+  switch (p.n_classes) {
+#define CASE(NC)                                                              \
+  case NC:                                                                    \
+    return wide ? launch_canon_t<NC, true>(p, out, sm_count, st, small_grid)  \
+                : launch_canon_t<NC, false>(p, out, sm_count, st, small_grid);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default:
+      return -(int)cudaErrorInvalidValue;
+  }
+}
+
+template <int NC, bool D>
+static int launch_hoist_t(const HoistParams& p, unsigned long long* out,
+                          int sm_count, cudaStream_t st) {
+  const size_t smem = (size_t)p.n_hist * p.hist_words * 4;
+  const void* fn = (const void*)k1_hoisted<NC, D>;
+  int grid = blocks_for(fn, smem, sm_count);
+  const uint64_t runs = p.run_end - p.run_begin;
+  const uint64_t need = (runs + kThreads - 1) / kThreads;
+  if (need < (uint64_t)grid) grid = (int)(need ? need : 1);
+  k1_hoisted<NC, D><<<grid, kThreads, smem, st>>>(p, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 1 : -(int)e;
+}
+
+int launch_hoisted(const HoistParams& p, unsigned long long* out, int sm_count,
+                   void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool dbl = p.has_double != 0;
+  switch (p.n_classes) {
+#define CASE(NC)                                                   \
+  case NC:                                                         \
+    return dbl ? launch_hoist_t<NC, true>(p, out, sm_count, st)    \
+               : launch_hoist_t<NC, false>(p, out, sm_count, st);
+    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+#undef CASE
+    default:
+      return -(int)cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace isd

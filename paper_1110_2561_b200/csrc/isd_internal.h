@@ -1,0 +1,84 @@
+// Internal declarations shared by the host plan compiler, the kernels and the
+// C ABI.  Nothing here is exported.
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+
+#include "isingdos_b200.h"
+
+namespace isd {
+
+constexpr int kCopyBits = ISD_COPY_BITS;   // u: sites unrolled in registers
+constexpr int kCopies = 1 << kCopyBits;    // 32 configurations per group
+constexpr int kMaxClasses = ISD_MAX_CLASSES;
+constexpr int kThreads = 512;              // threads per enumeration block
+
+// Parameters of the canonical kernel: one full class-mask evaluation per
+// configuration (the formulation of enumeration.py:167-205 on bit masks).
+struct CanonParams {
+  uint64_t start, end;      // [start, end) configuration indices
+  uint32_t n_classes;
+  uint32_t stride;          // B + 1 (row length of the table)
+  uint32_t nbins;           // (N+1)(B+1)
+  uint32_t hist_words;      // words per shared histogram (padded)
+  uint32_t n_hist;          // shared histograms per block
+  uint32_t n_spins;         // N (selects the 32- or 64-bit index path)
+  uint32_t shift[kMaxClasses];
+  uint64_t mask[kMaxClasses];
+  uint64_t jneg[kMaxClasses];
+};
+
+// Parameters of the hoisted kernel.  A "run" is 2^k
+// consecutive indices: bits [k, N) are fixed per thread, bits [u, k) are the
+// thread's loop counter j, and bits [0, u) are the 32 unrolled copies.
+struct HoistParams {
+  uint64_t run_begin, run_end;   // run indices (index = run << k)
+  uint64_t above_k;              // bits [k, N)
+  uint32_t k, l;                 // k = u + l
+  uint32_t n_classes;
+  uint32_t stride;               // B + 1
+  uint32_t nbins;
+  uint32_t hist_words;
+  uint32_t n_hist;
+  uint32_t has_double;           // any copy site with a doubled partner
+  uint32_t shift[kMaxClasses];
+  uint32_t mvar[kMaxClasses];    // class mask restricted to bits [u, k)
+  uint64_t mask[kMaxClasses];
+  uint64_t jneg[kMaxClasses];
+  uint64_t nm1[kCopyBits], jn1[kCopyBits];   // copy-site partner masks
+  uint64_t nm2[kCopyBits], jn2[kCopyBits];   // (second copy of a double bond)
+  uint32_t nm1v[kCopyBits], jn1v[kCopyBits]; // restricted to [u, k)
+  uint32_t nm2v[kCopyBits], jn2v[kCopyBits];
+  int32_t degree[kCopyBits];                 // d_p
+  int32_t ktd[kCopies];          // 4*(KT[c] - KT[c ^ topbit(c)]), ktd[0] = 4*KT[0]
+};
+
+// ---- host side -----------------------------------------------------------
+int validate_lattice(const isd_lattice* lat, char* err, size_t errlen);
+// Fill `info` for the hoisted decomposition.  Returns 0 if the lattice can
+// use the hoisted kernel, >0 if it is too small (canonical only).
+int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
+                 isd_plan_info* info);
+void fill_canon(const isd_lattice* lat, CanonParams* p);
+void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
+                HoistParams* p);
+
+// ---- kernel launchers (enumerate.cu / thermo.cu / calibrate.cu) ----------
+// Each returns the number of kernels launched, or a negative cudaError_t.
+int launch_canonical(const CanonParams& p, unsigned long long* out,
+                     int sm_count, void* stream, bool small_grid);
+int launch_hoisted(const HoistParams& p, unsigned long long* out,
+                   int sm_count, void* stream);
+int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
+                  uint32_t n_bonds, double scale, const double* fields,
+                  int n_fields, const double* temps, int n_temps, double* out,
+                  void* stream);
+int run_calibration(int which, int sm_count, double* lanes_per_clk_sm,
+                    double* sm_mhz);
+
+uint64_t bump_launches(uint64_t n);
+uint32_t hist_words_for(uint32_t nbins);
+int hist_count_for(uint32_t hist_words);
+
+}  // namespace isd

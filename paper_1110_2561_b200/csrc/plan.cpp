@@ -1,0 +1,198 @@
+// Host-side lattice validation and kernel-plan compiler.
+//
+// The lattice arrives as bond classes (include/isingdos_b200.h).  This file
+// turns it into the parameter blocks of the two enumeration kernels.  The
+// semantic contract is the reference's: m_idx = popcount(index) and e_idx =
+// number of unsatisfied bonds (enumeration.py:95-121, 184-204, 232-233).
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "isd_internal.h"
+
+namespace isd {
+
+static inline int popc64(uint64_t x) { return __builtin_popcountll(x); }
+
+int validate_lattice(const isd_lattice* lat, char* err, size_t errlen) {
+  if (!lat) {
+    snprintf(err, errlen, "lattice pointer is NULL");
+    return ISD_EINVAL;
+  }
+  const uint32_t n = lat->n_spins;
+  if (n < 1 || n > ISD_MAX_SPINS) {
+    snprintf(err, errlen, "n_spins=%u outside [1, %d]", n, ISD_MAX_SPINS);
+    return ISD_EINVAL;
+  }
+  if (lat->n_classes < 1 || lat->n_classes > ISD_MAX_CLASSES) {
+    snprintf(err, errlen, "n_classes=%u outside [1, %d]", lat->n_classes,
+             ISD_MAX_CLASSES);
+    return ISD_EINVAL;
+  }
+  if (lat->reserved != 0) {
+    snprintf(err, errlen, "reserved field must be 0");
+    return ISD_EINVAL;
+  }
+  uint32_t bonds = 0;
+  for (uint32_t c = 0; c < lat->n_classes; ++c) {
+    const isd_bond_class& k = lat->classes[c];
+    if (k.shift < 1 || k.shift >= n) {
+      snprintf(err, errlen, "class %u: shift %u outside [1, %u)", c, k.shift,
+               n);
+      return ISD_EINVAL;
+    }
+    if (k.reserved != 0) {
+      snprintf(err, errlen, "class %u: reserved field must be 0", c);
+      return ISD_EINVAL;
+    }
+    // bond (i, i+s) needs i + s < n
+    const uint64_t legal = (n - k.shift >= 64) ? ~0ull
+                                               : ((1ull << (n - k.shift)) - 1);
+    if (k.bond_mask & ~legal) {
+      snprintf(err, errlen, "class %u: bond_mask has partners beyond N", c);
+      return ISD_EINVAL;
+    }
+    if (k.jneg_mask & ~k.bond_mask) {
+      snprintf(err, errlen, "class %u: jneg_mask not a subset of bond_mask",
+               c);
+      return ISD_EINVAL;
+    }
+    bonds += popc64(k.bond_mask);
+  }
+  if (bonds != lat->n_bonds) {
+    snprintf(err, errlen, "n_bonds=%u but the class masks hold %u bonds",
+             lat->n_bonds, bonds);
+    return ISD_EINVAL;
+  }
+  if (bonds > 3 * ISD_MAX_SPINS) {
+    snprintf(err, errlen, "n_bonds=%u too large", bonds);
+    return ISD_EINVAL;
+  }
+  return ISD_OK;
+}
+
+// Hoisted split: u = 5 copy sites, l loop sites, the rest per-thread.  l is
+// chosen so that a full walk still has >= ~2^20 runs to spread over 148 SMs.
+int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
+                 isd_plan_info* info) {
+  std::memset(info, 0, sizeof(*info));
+  const int n = (int)lat->n_spins;
+  const int u = kCopyBits;
+  int log_configs = 0;
+  while (log_configs < 63 && (1ull << (log_configs + 1)) <= n_configs_hint)
+    ++log_configs;
+  if (log_configs > n) log_configs = n;
+  int l = log_configs - u - 20;
+  // tuning / test knob: force the loop width
+  if (const char* env = std::getenv("ISD_LOOP_BITS")) l = std::atoi(env);
+  if (l > 7) l = 7;
+  if (l < 0) l = 0;
+  const int k = u + l;
+  info->u = u;
+  info->l = l;
+  info->k = k;
+  info->stride = lat->n_bonds + 1;
+  info->run_mask_above_k = (n >= 64 ? ~0ull : ((1ull << n) - 1)) &
+                           ~((1ull << k) - 1);
+  info->var_mask = ((1ull << k) - 1) & ~((1ull << u) - 1);
+
+  // Copy-site neighbourhoods.  A bond (i, i+s) with i < u and i+s >= u is a
+  // copy/non-copy bond counted through n_p; with i+s < u it is a copy/copy
+  // bond folded into KT.  (Bonds with i >= u never touch a copy site: the
+  // upper end is above the lower one.)
+  struct CC { int p, q, neg; };
+  CC cc[ISD_MAX_CLASSES * kCopyBits];
+  int ncc = 0;
+  for (int p = 0; p < u && p < n; ++p) {
+    for (uint32_t c = 0; c < lat->n_classes; ++c) {
+      const isd_bond_class& k2 = lat->classes[c];
+      if (!((k2.bond_mask >> p) & 1)) continue;
+      const int q = p + (int)k2.shift;
+      const int neg = (int)((k2.jneg_mask >> p) & 1);
+      if (q >= u) {
+        const uint64_t bit = 1ull << q;
+        if (!(info->copy_nbr1[p] & bit)) {
+          info->copy_nbr1[p] |= bit;
+          if (neg) info->copy_jneg1[p] |= bit;
+        } else {
+          // a periodic axis of length 2 doubles the bond (lattice.py:105-107)
+          info->copy_nbr2[p] |= bit;
+          if (neg) info->copy_jneg2[p] |= bit;
+        }
+        info->copy_degree[p] += 1;
+      } else {
+        cc[ncc++] = CC{p, q, neg};
+      }
+    }
+  }
+  for (int c = 0; c < kCopies; ++c) {
+    int unsat = 0;
+    for (int i = 0; i < ncc; ++i)
+      unsat += ((c >> cc[i].p) ^ (c >> cc[i].q) ^ cc[i].neg) & 1;
+    info->copy_table[c] = __builtin_popcount((unsigned)c) * (int)info->stride +
+                          unsat;
+  }
+  // The hoisted kernel needs all copy and loop sites inside the low word and
+  // at least one run.
+  if (n < k + 1 || k > 32) return 1;
+  return 0;
+}
+
+void fill_canon(const isd_lattice* lat, CanonParams* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->n_classes = lat->n_classes;
+  p->n_spins = lat->n_spins;
+  p->stride = lat->n_bonds + 1;
+  p->nbins = (lat->n_spins + 1) * p->stride;
+  p->hist_words = hist_words_for(p->nbins);
+  p->n_hist = (uint32_t)hist_count_for(p->hist_words);
+  for (uint32_t c = 0; c < lat->n_classes; ++c) {
+    p->shift[c] = lat->classes[c].shift;
+    p->mask[c] = lat->classes[c].bond_mask;
+    p->jneg[c] = lat->classes[c].jneg_mask;
+  }
+}
+
+void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
+                HoistParams* p) {
+  std::memset(p, 0, sizeof(*p));
+  const uint32_t u = info->u, k = info->k;
+  p->k = k;
+  p->l = info->l;
+  p->above_k = info->run_mask_above_k;
+  p->n_classes = lat->n_classes;
+  p->stride = info->stride;
+  p->nbins = (lat->n_spins + 1) * p->stride;
+  p->hist_words = hist_words_for(p->nbins);
+  p->n_hist = (uint32_t)hist_count_for(p->hist_words);
+  const uint32_t var = (uint32_t)info->var_mask;
+  for (uint32_t c = 0; c < lat->n_classes; ++c) {
+    p->shift[c] = lat->classes[c].shift;
+    p->mask[c] = lat->classes[c].bond_mask;
+    p->jneg[c] = lat->classes[c].jneg_mask;
+    p->mvar[c] = (uint32_t)lat->classes[c].bond_mask & var;
+  }
+  p->has_double = 0;
+  for (uint32_t q = 0; q < u; ++q) {
+    p->nm1[q] = info->copy_nbr1[q];
+    p->jn1[q] = info->copy_jneg1[q];
+    p->nm2[q] = info->copy_nbr2[q];
+    p->jn2[q] = info->copy_jneg2[q];
+    p->nm1v[q] = (uint32_t)info->copy_nbr1[q] & var;
+    p->jn1v[q] = (uint32_t)info->copy_jneg1[q] & var;
+    p->nm2v[q] = (uint32_t)info->copy_nbr2[q] & var;
+    p->jn2v[q] = (uint32_t)info->copy_jneg2[q] & var;
+    p->degree[q] = info->copy_degree[q];
+    if (info->copy_nbr2[q]) p->has_double = 1;
+  }
+  for (int c = 0; c < kCopies; ++c) {
+    if (c == 0) {
+      p->ktd[0] = 4 * info->copy_table[0];
+    } else {
+      const int top = 31 - __builtin_clz((unsigned)c);
+      p->ktd[c] = 4 * (info->copy_table[c] - info->copy_table[c ^ (1 << top)]);
+    }
+  }
+}
+
+}  // namespace isd

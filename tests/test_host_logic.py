@@ -1,0 +1,248 @@
+"""CPU tests of the host side: lattice compiler, C-ABI library, kernel plan.
+
+No GPU: the native library is loaded and its host-only entry points
+(isd_validate, isd_plan) are exercised; the hoisted kernel's arithmetic is
+replayed in numpy from the plan the library compiles and checked against
+the oracle on every configuration.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+import paper_1110_2561_b200 as isd
+from paper_1110_2561_b200 import _native
+from paper_1110_2561_b200.enumeration import native_lattice
+from paper_1110_2561_b200.workloads import canonical_ops, workloads
+from oracle import naive, port
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+# -- library / ABI -----------------------------------------------------------
+
+def test_library_exports_every_header_symbol():
+    lib = _native.load()
+    header = open(os.path.join(ROOT, "include", "isingdos_b200.h")).read()
+    import re
+    declared = set(re.findall(r"\b(isd_[a-z_]+)\s*\(", header))
+    assert declared == set(_native.EXPORTED_SYMBOLS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.isd_abi_version() == 1
+    assert b"sm_100a" in lib.isd_version()
+
+
+def test_library_built_for_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.library_path()],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_validate_rejects_bad_lattices():
+    good = native_lattice(isd.LatticeSpec(4, 4))
+    _native.validate(good)
+    bad = _native.make_lattice(16, 31, isd.LatticeSpec(4, 4).bond_classes())
+    with pytest.raises(ValueError, match="n_bonds"):
+        _native.validate(bad)
+    bad = _native.make_lattice(16, 1, [(16, 1, 0)])
+    with pytest.raises(ValueError, match="shift"):
+        _native.validate(bad)
+    bad = _native.make_lattice(16, 1, [(4, 1 << 12, 0)])
+    with pytest.raises(ValueError, match="beyond N"):
+        _native.validate(bad)
+    bad = _native.make_lattice(16, 1, [(1, 1, 2)])
+    with pytest.raises(ValueError, match="subset"):
+        _native.validate(bad)
+    bad = _native.make_lattice(41, 1, [(1, 1, 0)])
+    with pytest.raises(ValueError, match="n_spins"):
+        _native.validate(bad)
+
+
+def test_no_gpu_means_loud_failure():
+    if _native.device_count() > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(RuntimeError):
+        isd.enumerate_shard(isd.LatticeSpec(2, 2), None,
+                            isd.make_shards(isd.LatticeSpec(2, 2), 1)[0])
+
+
+# -- lattice compiler ----------------------------------------------------------
+
+@pytest.mark.parametrize("spec,expected", [
+    (isd.LatticeSpec(5, 5), [(1, 20), (4, 5), (5, 20), (20, 5)]),
+    (isd.LatticeSpec(6, 6), [(1, 30), (5, 6), (6, 30), (30, 6)]),
+    (isd.LatticeSpec(3, 3, 4),
+     [(1, 24), (2, 12), (3, 24), (6, 12), (9, 27), (27, 9)]),
+    (isd.LatticeSpec(4, 4, boundary="free"), [(1, 12), (4, 12)]),
+    (isd.LatticeSpec(6, 6, boundary="free"), [(1, 30), (6, 30)]),
+])
+def test_bond_classes_match_survey_appendix_a(spec, expected):
+    got = [(s, bin(m).count("1")) for s, m, _ in spec.bond_classes()]
+    assert got == expected
+    assert sum(c for _, c in got) == spec.num_bonds
+
+
+LATTICES = [
+    dict(rows=2, cols=2), dict(rows=3, cols=3), dict(rows=2, cols=4),
+    dict(rows=3, cols=4, coupling=-1), dict(rows=2, cols=2, depth=2),
+    dict(rows=2, cols=3, depth=2), dict(rows=3, cols=3, boundary="free"),
+    dict(rows=4, cols=4, boundary="free"), dict(rows=2, cols=2, depth=3),
+    dict(rows=3, cols=2, depth=2, boundary="free"),
+]
+
+
+def _spec_and_oracle(kw, signed_seed=None):
+    spec = isd.LatticeSpec(**kw)
+    if signed_seed is not None:
+        spec = isd.LatticeSpec(**kw, bond_signs=isd.random_bond_signs(
+            spec, signed_seed))
+    per = spec.periodic
+    signs = list(spec.bond_signs) if spec.bond_signs else None
+    return spec, (spec.rows, spec.cols, spec.depth, spec.coupling, per, signs)
+
+
+@pytest.mark.parametrize("kw", LATTICES)
+@pytest.mark.parametrize("seed", [None, 5])
+def test_class_energy_equals_per_bond_energy(kw, seed):
+    # every index: |J|(2 e_idx - B) == -sum_b J_b s_i s_j (oracle.py:61-63)
+    spec, (r, c, d, j, per, signs) = _spec_and_oracle(kw, seed)
+    scale = abs(spec.coupling)
+    for index in range(spec.num_configs):
+        e = scale * (2 * isd.unsatisfied_bonds(spec, index) - spec.num_bonds)
+        assert e == naive.energy_of(r, c, d, index, j, per, signs)
+
+
+def test_total_energy_anchors():
+    spec = isd.LatticeSpec(4, 4)
+    assert isd.total_energy(isd.decode_config(spec, 0), spec) == -32
+    assert isd.total_energy(isd.decode_config(spec, 65535), spec) == -32
+    checker = sum(1 << spec.bit_position(r, c)
+                  for r in range(4) for c in range(4) if (r + c) % 2)
+    assert isd.total_energy(isd.decode_config(spec, checker), spec) == 32
+    free = isd.LatticeSpec(4, 4, boundary="free")
+    assert isd.total_energy(isd.decode_config(free, 0), free) == -24
+
+
+def test_latticespec_validation_messages():
+    with pytest.raises(ValueError, match="degenerate periodic axis"):
+        isd.LatticeSpec(1, 4)
+    with pytest.raises(ValueError, match="cap of 40"):
+        isd.LatticeSpec(7, 6)
+    with pytest.raises(ValueError, match="cap of 30"):
+        isd.LatticeSpec(31, 1 + 1)
+    with pytest.raises(ValueError, match="coupling"):
+        isd.LatticeSpec(2, 2, coupling=0)
+    with pytest.raises(ValueError, match="boundary"):
+        isd.LatticeSpec(2, 2, boundary="open")
+    with pytest.raises(ValueError, match="bond_signs"):
+        isd.LatticeSpec(2, 2, bond_signs=(1, -1))
+    with pytest.raises(ValueError, match="bond signs"):
+        isd.LatticeSpec(2, 2, bond_signs=(2,) * 8)
+    assert isd.LatticeSpec(4, 4, 1, 2.0).coupling == 2
+    assert isd.LatticeSpec(4, 4) == isd.LatticeSpec(4, 4, 1, 1)
+    assert isd.LatticeSpec(4, 4) != isd.LatticeSpec(4, 4, boundary="free")
+    assert isd.LatticeSpec(4, 4, boundary="free").num_bonds == 24
+    assert isd.LatticeSpec(3, 3, 4).num_bonds == 108
+
+
+def test_c4_signs_fixture_matches_convention():
+    from golden_io import load_json
+    fx = load_json("c4_bond_signs.json")
+    spec = workloads()["c4"].spec
+    assert list(spec.bond_signs) == fx["signs"]
+    assert len(fx["signs"]) == 72
+
+
+def test_canonical_ops_table():
+    w = workloads()
+    assert [canonical_ops(w[c].spec) for c in ("c1", "c2", "c3", "c4", "c5")] \
+        == [(3, 6), (5, 12), (6, 13), (10, 33), (14, 37)]
+
+
+def test_make_shards_partition():
+    spec = isd.LatticeSpec(2, 2)
+    assert [s.size for s in isd.make_shards(spec, 3)] == [6, 5, 5]
+    big = isd.LatticeSpec(6, 6)
+    s8 = isd.make_shards(big, 8)
+    assert [s.start_index >> 33 for s in s8] == list(range(8))  # top 3 bits
+    with pytest.raises(ValueError):
+        isd.make_shards(spec, 17)
+
+
+# -- hoisted-kernel plan replay ---------------------------------------------
+
+def _u(x):
+    return np.uint64(x)
+
+
+def replay_hoisted(spec, loop_bits):
+    """numpy replay of k1_hoisted's arithmetic over every index."""
+    os.environ["ISD_LOOP_BITS"] = str(loop_bits)
+    try:
+        lat = native_lattice(spec)
+        usable, info = _native.plan(lat, spec.num_configs)
+    finally:
+        del os.environ["ISD_LOOP_BITS"]
+    assert usable
+    u, l, k = info.u, info.l, info.k
+    stride = info.stride
+    classes = spec.bond_classes()
+    n = spec.num_spins
+    above_k = _u(info.run_mask_above_k)
+    var = int(info.var_mask)
+    x = np.arange(1 << n, dtype=np.uint64)
+    xt = x & above_k
+    jb = (x & _u(var)).astype(np.uint64)
+    c = (x & _u((1 << u) - 1)).astype(np.int64)
+    pc = lambda a: np.bitwise_count(a).astype(np.int64)  # noqa: E731
+    base = pc(xt) * stride
+    for s, m, jn in classes:
+        sh = xt >> _u(s)
+        base += pc(((xt ^ sh) ^ _u(jn)) & _u(m) & above_k)
+        cst = (sh & _u(0xFFFFFFFF)) ^ _u(jn & 0xFFFFFFFF)
+        jshift = (jb >> _u(s)) if s < 32 else np.zeros_like(jb)
+        base += pc((jb ^ jshift ^ cst) & _u(m & var))
+    base += pc(jb) * stride
+    bins = base.copy()
+    for q in range(u):
+        nq = pc((xt ^ _u(info.copy_jneg1[q])) & _u(info.copy_nbr1[q]) & above_k)
+        nq += pc((xt ^ _u(info.copy_jneg2[q])) & _u(info.copy_nbr2[q]) & above_k)
+        nq += pc((jb ^ _u(info.copy_jneg1[q] & var)) & _u(info.copy_nbr1[q] & var))
+        nq += pc((jb ^ _u(info.copy_jneg2[q] & var)) & _u(info.copy_nbr2[q] & var))
+        bins += nq
+        d = info.copy_degree[q] - 2 * nq
+        bins += np.where((c >> q) & 1, d, 0)
+    kt = np.array(list(info.copy_table), dtype=np.int64)
+    bins += kt[c]
+    table = np.bincount(bins, minlength=(n + 1) * stride)
+    return table.reshape(n + 1, stride)
+
+
+REPLAY = [
+    dict(rows=4, cols=4), dict(rows=3, cols=4, coupling=-1),
+    dict(rows=2, cols=2, depth=3), dict(rows=4, cols=4, boundary="free"),
+    dict(rows=2, cols=4, depth=2), dict(rows=3, cols=3, depth=2),
+    dict(rows=5, cols=3), dict(rows=2, cols=8),
+]
+
+
+@pytest.mark.parametrize("kw", REPLAY)
+@pytest.mark.parametrize("seed", [None, 11])
+@pytest.mark.parametrize("loop_bits", [0, 3, 7])
+def test_hoisted_plan_replay_matches_oracle(kw, seed, loop_bits):
+    spec, (r, c, d, j, per, signs) = _spec_and_oracle(kw, seed)
+    if spec.num_spins < 5 + loop_bits + 1:
+        pytest.skip("lattice too small for this loop width")
+    lat = port.Lattice(r, c, d, j, per, signs)
+    want = port.enumerate_range(lat, 0, 1 << lat.n)
+    got = replay_hoisted(spec, loop_bits)
+    assert np.array_equal(got, want)
+
+
+def test_plan_refuses_tiny_lattices():
+    usable, _ = _native.plan(native_lattice(isd.LatticeSpec(2, 2)), 16)
+    assert not usable

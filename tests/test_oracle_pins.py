@@ -1,0 +1,129 @@
+"""Pin the oracle to the reference before trusting it (CPU only).
+
+Every fixture compared here was produced by running the reference package
+itself (tests/golden/make_reference_goldens.py).  The naive oracle, the
+numpy port and the C oracle must reproduce them exactly; the port's
+thermodynamics must match the reference's ThermoPoints to 1e-13.
+"""
+
+import math
+import os
+
+import numpy as np
+import pytest
+
+from golden_io import (GOLDEN, csv_goldens, load_json, read_csv_table,
+                       read_json_table)
+from oracle import cref, naive, port
+
+
+def _small(name):
+    rows, cols, depth, j, table = read_csv_table(name)
+    return rows, cols, depth, j, table
+
+
+@pytest.mark.parametrize("name", [n for n in csv_goldens()
+                                  if read_csv_table(n)[4].shape[0] <= 21])
+def test_port_and_c_oracle_reproduce_reference_tables(name):
+    rows, cols, depth, j, want = _small(name)
+    lat = port.Lattice(rows, cols, depth, j)
+    assert np.array_equal(port.enumerate_range(lat, 0, 1 << lat.n), want)
+    assert np.array_equal(cref.table(rows, cols, depth, j, mode="mask",
+                                     threads=2), want)
+    if lat.n <= 16:
+        assert np.array_equal(cref.table(rows, cols, depth, j, mode="naive",
+                                         threads=2), want)
+
+
+@pytest.mark.parametrize("name", [n for n in csv_goldens()
+                                  if read_csv_table(n)[4].shape[0] <= 13])
+def test_naive_oracle_reproduces_reference_tables(name):
+    rows, cols, depth, j, want = _small(name)
+    assert np.array_equal(naive.full_dos(rows, cols, depth, j), want)
+
+
+def test_reference_4x4_golden_is_the_80_cell_table():
+    _, _, _, _, t = _small("dos_4x4x1_J1.csv")
+    assert np.count_nonzero(t) == 80 and t.sum() == 65536
+    assert t[16, 0] == 1 and t[8, 16] == 4356  # (1, M=16, E=-32), (4356, 0, 0)
+
+
+def test_port_reproduces_odd_shard_slices():
+    lat = port.Lattice(5, 5)
+    n, b = 25, 50
+    for rec in load_json("shards_5x5.json")[:4]:
+        got = port.enumerate_range(lat, rec["start"], rec["end"])
+        want = np.zeros((n + 1, b + 1), dtype=np.int64)
+        for c, m, e in rec["cells"]:
+            want[(m + n) // 2, (e + b) // 2] = c
+        assert np.array_equal(got, want)
+
+
+def test_port_reproduces_tall_column_slice():
+    rec = load_json("slice_17x2_123456_4096.json")
+    lat = port.Lattice(17, 2)
+    got = port.enumerate_range(lat, rec["start"], rec["end"])
+    n, b = 34, 68
+    want = np.zeros((n + 1, b + 1), dtype=np.int64)
+    for c, m, e in rec["cells"]:
+        want[(m + n) // 2, (e + b) // 2] = c
+    assert np.array_equal(got, want)
+
+
+def test_port_thermo_reproduces_reference_points():
+    for case in load_json("thermo_reference.json"):
+        rows, cols, depth, j, table = _small(case["dos"])
+        n = rows * cols * depth
+        b = table.shape[1] - 1
+        for p in case["points"]:
+            h, t = float(p[0]), float(p[1])
+            got = port.partition_point(table, n, b, abs(j), h, t)
+            for k in range(6):
+                want = float(p[2 + k])
+                tol = 1e-13 * max(abs(want), 1.0) if not (k == 4 and h == 0) \
+                    else 1e-13
+                assert abs(got[k] - want) <= tol, (case["dos"], h, t, k)
+
+
+def test_brute_force_log_z_agrees_with_port():
+    _, _, _, _, table = _small("dos_3x3x1_J1.csv")
+    for h, t in ((0.0, 1.0), (0.3, 2.5)):
+        bf = naive.brute_force_log_z(3, 3, 1, h, t)
+        got = port.partition_point(table, 9, 18, 1, h, t)[0]
+        assert abs(bf - got) <= 1e-11 * abs(bf)
+
+
+@pytest.mark.parametrize("fname,shape", [
+    ("c1_4x4_free.json", (17, 25)), ("c3_6x6_free.json", (37, 61)),
+    ("c4_6x6_pmJ_seed1234.json", (37, 73)),
+    ("cx_3x3x4_periodic.json", (37, 109)), ("cx_6x6_periodic.json", (37, 73)),
+])
+def test_oracle_goldens_invariants(fname, shape):
+    if not os.path.exists(os.path.join(GOLDEN, fname)):
+        pytest.skip("not generated")
+    obj, t = read_json_table(fname)
+    n = obj["n_spins"]
+    assert t.shape == shape
+    assert int(t.sum()) == 1 << n
+    assert all(int(t[m].sum()) == math.comb(n, m) for m in range(n + 1))
+    assert np.array_equal(t, t[::-1])
+    if obj["boundary"] == "free" or obj["signs"] is not None or \
+            obj["depth"] == 1:
+        e = t.sum(axis=0)  # bipartite lattices: g(E) = g(-E)
+        assert np.array_equal(e, e[::-1])
+
+
+@pytest.mark.parametrize("csv,js", [("dos_3x3x4_J1.csv", "cx_3x3x4_periodic.json"),
+                                    ("dos_6x6x1_J1.csv", "cx_6x6_periodic.json")])
+def test_c_oracle_n36_equals_reference_n36(csv, js):
+    if not (os.path.exists(os.path.join(GOLDEN, csv)) and
+            os.path.exists(os.path.join(GOLDEN, js))):
+        pytest.skip("N=36 goldens not generated")
+    assert np.array_equal(read_csv_table(csv)[4], read_json_table(js)[1])
+
+
+def test_c1_golden_three_routes():
+    if not os.path.exists(os.path.join(GOLDEN, "c1_4x4_free.json")):
+        pytest.skip("not generated")
+    _, t = read_json_table("c1_4x4_free.json")
+    assert np.array_equal(naive.full_dos(4, 4, 1, 1, periodic=False), t)
