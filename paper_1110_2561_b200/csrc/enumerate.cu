@@ -131,7 +131,6 @@ __global__ void __launch_bounds__(kThreads)
       npr[q] = __popcll((xt ^ P.jn1[q]) & P.nm1[q] & P.above_k);
       if constexpr (DOUBLE)
         npr[q] += __popcll((xt ^ P.jn2[q]) & P.nm2[q] & P.above_k);
-      base_run += npr[q];
     }
     // ---- loop over bits [u, k) ----
     for (uint32_t j = 0; j < nloop; ++j) {
