@@ -132,6 +132,15 @@ typedef struct isd_plan_info {
   uint64_t copy_nbr2[ISD_COPY_BITS];     /* second copy (double bonds)    */
   uint64_t copy_jneg2[ISD_COPY_BITS];
   int32_t  copy_table[1 << ISD_COPY_BITS]; /* KT[c] = popc(c)(B+1) + CT-CT unsat */
+  /* shared-histogram layout: word(m, e) = m*row_words + (e_halved ?
+   * (e - e_parity)/2 : e).  e is halved when every site has even degree
+   * (then e_idx always has the parity e_parity).  row_words and the lane
+   * placement are chosen on the host to minimise bank conflicts. */
+  uint32_t row_words;
+  uint32_t e_halved;
+  uint32_t e_parity;
+  uint32_t lane_shift;       /* warp lanes differ in run bits [s, s+5)  */
+  double   est_wavefronts;   /* predicted smem wavefronts per warp RED  */
 } isd_plan_info;
 
 int isd_plan(const isd_lattice* lat, uint64_t n_configs_hint,

@@ -52,6 +52,9 @@ class PlanInfo(ctypes.Structure):
         ("copy_nbr2", ctypes.c_uint64 * ISD_COPY_BITS),
         ("copy_jneg2", ctypes.c_uint64 * ISD_COPY_BITS),
         ("copy_table", ctypes.c_int32 * (1 << ISD_COPY_BITS)),
+        ("row_words", ctypes.c_uint32), ("e_halved", ctypes.c_uint32),
+        ("e_parity", ctypes.c_uint32), ("lane_shift", ctypes.c_uint32),
+        ("est_wavefronts", ctypes.c_double),
     ]
 
 

@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -106,6 +107,27 @@ static int current_sm_count(int* sms) {
   return ISD_OK;
 }
 
+// Plans are compiled once per (lattice, loop width): the layout search
+// replays a sample of warp instructions and costs tens of milliseconds.
+static std::mutex g_plan_mu;
+static std::map<std::string, std::pair<int, isd_plan_info>> g_plans;
+
+static int cached_plan(const isd_lattice* lat, uint64_t hint,
+                       isd_plan_info* info) {
+  const int l = plan_loop_bits(lat, hint);
+  std::string key(reinterpret_cast<const char*>(lat), sizeof(*lat));
+  key.push_back((char)l);
+  std::lock_guard<std::mutex> lock(g_plan_mu);
+  auto it = g_plans.find(key);
+  if (it == g_plans.end()) {
+    isd_plan_info fresh;
+    const int rc = compile_plan(lat, hint, &fresh);
+    it = g_plans.emplace(key, std::make_pair(rc, fresh)).first;
+  }
+  *info = it->second.second;
+  return it->second.first;
+}
+
 // At most 2^38 configurations per launch: with >= 148 CTAs no CTA counts
 // more than ~1.9e9 < 2^32 configurations into its u32 shared histograms.
 static constexpr uint64_t kMaxPerLaunch = 1ull << 38;
@@ -162,7 +184,7 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     return rc;
   }
   isd_plan_info info;
-  const int too_small = compile_plan(lat, end - start, &info);
+  const int too_small = cached_plan(lat, end - start, &info);
   if (too_small) {
     if (algo == ISD_ALGO_HOISTED)
       return fail(ISD_EINVAL, "lattice of %u spins too small for the hoisted "
@@ -191,6 +213,14 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     const uint64_t re = (r1 - r > runs_per_launch) ? r + runs_per_launch : r1;
     hp.run_begin = r;
     hp.run_end = re;
+    // lane placement (from the plan, or forced for experiments) needs a run
+    // count divisible by 2^(shift+5)
+    {
+      const long ls = env_long("ISD_LANE_SHIFT", (long)info.lane_shift);
+      hp.lane_shift = 0;
+      if (ls > 0 && ls < 40 && ((re - r) & ((1ull << (ls + 5)) - 1)) == 0)
+        hp.lane_shift = (uint32_t)ls;
+    }
     int x = launch_hoisted(hp, out, sms, st);
     if (x < 0) return cuda_fail((cudaError_t)(-x), "k1_hoisted launch");
     nl += x;
@@ -222,7 +252,7 @@ int isd_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   int rc = isd_validate(lat);
   if (rc) return rc;
   if (!out) return fail(ISD_EINVAL, "plan pointer is NULL");
-  return compile_plan(lat, n_configs_hint, out);
+  return cached_plan(lat, n_configs_hint, out);
 }
 
 int isd_enumerate_async(const isd_lattice* lat, uint64_t start, uint64_t end,

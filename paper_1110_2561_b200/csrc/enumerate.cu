@@ -111,17 +111,25 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
   const uint32_t nloop = 1u << P.l;
 
-  for (uint64_t r = P.run_begin + (uint64_t)blockIdx.x * blockDim.x +
-                    threadIdx.x;
-       r < P.run_end; r += gstride) {
+  const uint64_t nruns = P.run_end - P.run_begin;
+  const uint32_t ls = P.lane_shift;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+       t < nruns; t += gstride) {
+    // lane bits of t go to run bits [ls, ls+5): which five sites the 32
+    // lanes of a warp differ in (shared-memory bank spread)
+    const uint64_t hi = t >> 5;
+    const uint64_t r =
+        P.run_begin + (((hi >> ls) << (ls + 5)) | ((t & 31) << ls) |
+                       (hi & ((1ull << ls) - 1)));
     // ---- per-run constants (bits [k, N) fixed) ----
     const uint64_t xt = r << P.k;
-    int base_run = __popcll(xt) * (int)P.stride;
+    const int m_run = __popcll(xt);
+    int e_run = 0;
     uint32_t cst[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const uint64_t sh = xt >> P.shift[c];
-      base_run += __popcll(((xt ^ sh) ^ P.jneg[c]) & P.mask[c] & P.above_k);
+      e_run += __popcll(((xt ^ sh) ^ P.jneg[c]) & P.mask[c] & P.above_k);
       // partner word seen by the loop sites [u, k); jneg folded in
       cst[c] = (uint32_t)sh ^ (uint32_t)P.jneg[c];
     }
@@ -132,25 +140,29 @@ __global__ void __launch_bounds__(kThreads)
       if constexpr (DOUBLE)
         npr[q] += __popcll((xt ^ P.jn2[q]) & P.nm2[q] & P.above_k);
     }
+    // byte address of (m_run, e = 0 - parity) in this warp's histogram
+    const uint32_t a_run = hbase + (uint32_t)m_run * P.row_bytes -
+                           P.e_parity * P.e_bytes + (uint32_t)P.ktd[0];
     // ---- loop over bits [u, k) ----
     for (uint32_t j = 0; j < nloop; ++j) {
       const uint32_t jb = j << kCopyBits;
-      int base = base_run + __popc(j) * (int)P.stride;
+      int e = e_run;
 #pragma unroll
       for (int c = 0; c < NC; ++c)
-        base += __popc((jb ^ __funnelshift_rc(jb, 0u, P.shift[c]) ^ cst[c]) &
-                       P.mvar[c]);
+        e += __popc((jb ^ __funnelshift_rc(jb, 0u, P.shift[c]) ^ cst[c]) &
+                    P.mvar[c]);
       int d[kCopyBits];
 #pragma unroll
       for (int q = 0; q < kCopyBits; ++q) {
         int nq = npr[q] + __popc((jb ^ P.jn1v[q]) & P.nm1v[q]);
         if constexpr (DOUBLE) nq += __popc((jb ^ P.jn2v[q]) & P.nm2v[q]);
-        base += nq;
-        d[q] = 4 * (P.degree[q] - 2 * nq);
+        e += nq;
+        d[q] = (int)P.e_bytes * (P.degree[q] - 2 * nq);
       }
       // ---- 32 copies: addr_c = addr_{c without top bit} + d_top + ktd[c]
       uint32_t a[kCopies];
-      a[0] = hbase + 4u * (uint32_t)base + (uint32_t)P.ktd[0];
+      a[0] = a_run + (uint32_t)__popc(j) * P.row_bytes +
+             (uint32_t)e * P.e_bytes;
       red_shared_inc(a[0]);
 #pragma unroll
       for (int c = 1; c < kCopies; ++c) {
@@ -161,7 +173,20 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
   __syncthreads();
-  flush_hist(hist, P.n_hist, P.hist_words, P.nbins, out);
+  // ---- flush: word (m, e') -> table bin (m, e) ----
+  for (uint32_t bin = threadIdx.x; bin < P.nbins; bin += blockDim.x) {
+    const uint32_t m = bin / P.stride, e = bin - m * P.stride;
+    uint32_t word;
+    if (P.e_halved) {
+      if ((e ^ P.e_parity) & 1) continue;  // structurally empty
+      word = m * P.row_words + ((e - P.e_parity) >> 1);
+    } else {
+      word = m * P.row_words + e;
+    }
+    unsigned long long s = 0;
+    for (uint32_t h = 0; h < P.n_hist; ++h) s += hist[h * P.hist_words + word];
+    if (s) atomicAdd(out + bin, s);
+  }
 }
 
 // ---------------------------------------------------------------------------

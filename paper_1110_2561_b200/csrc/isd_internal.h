@@ -42,6 +42,11 @@ struct HoistParams {
   uint32_t hist_words;
   uint32_t n_hist;
   uint32_t has_double;           // any copy site with a doubled partner
+  uint32_t lane_shift;           // warp lanes take run bits [s, s+5)
+  uint32_t row_words;            // shared words per m row
+  uint32_t row_bytes;            // 4 * row_words
+  uint32_t e_bytes;              // bytes per unit of e (4, or 2 if halved)
+  uint32_t e_halved, e_parity;
   uint32_t shift[kMaxClasses];
   uint32_t mvar[kMaxClasses];    // class mask restricted to bits [u, k)
   uint64_t mask[kMaxClasses];
@@ -51,7 +56,7 @@ struct HoistParams {
   uint32_t nm1v[kCopyBits], jn1v[kCopyBits]; // restricted to [u, k)
   uint32_t nm2v[kCopyBits], jn2v[kCopyBits];
   int32_t degree[kCopyBits];                 // d_p
-  int32_t ktd[kCopies];          // 4*(KT[c] - KT[c ^ topbit(c)]), ktd[0] = 4*KT[0]
+  int32_t ktd[kCopies];          // byte offset of copy c minus copy c^topbit(c)
 };
 
 // ---- host side -----------------------------------------------------------
@@ -60,6 +65,7 @@ int validate_lattice(const isd_lattice* lat, char* err, size_t errlen);
 // use the hoisted kernel, >0 if it is too small (canonical only).
 int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
                  isd_plan_info* info);
+int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint);
 void fill_canon(const isd_lattice* lat, CanonParams* p);
 void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
                 HoistParams* p);

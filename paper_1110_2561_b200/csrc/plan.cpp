@@ -71,11 +71,110 @@ int validate_lattice(const isd_lattice* lat, char* err, size_t errlen) {
   return ISD_OK;
 }
 
+// ---- shared-histogram layout ---------------------------------------------
+// The 32 lanes of a warp reduce into one shared histogram at the same time;
+// lanes on the same word aggregate in hardware, lanes on different words of
+// the same bank serialise.  The kernel addresses word(m, e) = m*S + e' with
+// e' = e (or (e - parity)/2 when e_idx has a fixed parity, which halves the
+// footprint and doubles the banks a row touches).  S and the run bits the
+// lanes differ in are picked here by replaying a sample of warp
+// instructions: minimise the mean over instructions of the largest number
+// of distinct words falling into one bank (= wavefronts).
+
+static uint64_t rng_next(uint64_t* s) {
+  uint64_t x = *s;
+  x ^= x << 13;
+  x ^= x >> 7;
+  x ^= x << 17;
+  return *s = x;
+}
+
+static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
+  const int n = (int)lat->n_spins;
+  const int k = (int)info->k;
+  const int b = (int)lat->n_bonds;
+  int deg[64] = {0};
+  int neg = 0;
+  for (uint32_t c = 0; c < lat->n_classes; ++c) {
+    const isd_bond_class& cl = lat->classes[c];
+    for (int i = 0; i < n; ++i)
+      if ((cl.bond_mask >> i) & 1) {
+        deg[i]++;
+        deg[i + cl.shift]++;
+      }
+    neg += popc64(cl.jneg_mask);
+  }
+  bool even = true;
+  for (int i = 0; i < n; ++i) even = even && (deg[i] % 2 == 0);
+  info->e_halved = even ? 1 : 0;
+  info->e_parity = even ? (uint32_t)(neg & 1) : 0;
+  const int min_words = even ? (b - (int)info->e_parity) / 2 + 1 : b + 1;
+  info->row_words = (uint32_t)min_words;
+  info->lane_shift = 0;
+  info->est_wavefronts = 0;
+  const int run_bits = n - k;
+  if (run_bits < 5) return;
+
+  constexpr int kWarps = 24, kCand = 48;
+  static const int shifts[] = {0, 5, 10, 15};
+  double best = 1e30;
+  int m_s[32], e_s[32];
+  for (int ls : shifts) {
+    if (run_bits < ls + 5) continue;
+    double cost[kCand] = {0};
+    uint64_t seed = 0x9E3779B97F4A7C15ull ^ (uint64_t)(ls + 1);
+    const uint64_t hi_count = 1ull << (run_bits - 5);
+    for (int w = 0; w < kWarps; ++w) {
+      const uint64_t hi = rng_next(&seed) % hi_count;
+      const uint64_t j = (k > kCopyBits) ? rng_next(&seed) % (1ull << (k - kCopyBits)) : 0;
+      for (int c = 0; c < kCopies; ++c) {
+        for (int lane = 0; lane < 32; ++lane) {
+          const uint64_t r = ((hi >> ls) << (ls + 5)) | ((uint64_t)lane << ls) |
+                             (hi & ((1ull << ls) - 1));
+          const uint64_t x = (r << k) | (j << kCopyBits) | (uint64_t)c;
+          int e = 0;
+          for (uint32_t q = 0; q < lat->n_classes; ++q) {
+            const isd_bond_class& cl = lat->classes[q];
+            e += popc64(((x ^ (x >> cl.shift)) ^ cl.jneg_mask) & cl.bond_mask);
+          }
+          m_s[lane] = popc64(x);
+          e_s[lane] = even ? (e - (int)info->e_parity) / 2 : e;
+        }
+        for (int si = 0; si < kCand; ++si) {
+          const int S = min_words + si;
+          int words[32];
+          int nw = 0;
+          for (int lane = 0; lane < 32; ++lane) {
+            const int wd = m_s[lane] * S + e_s[lane];
+            bool seen = false;
+            for (int t = 0; t < nw && !seen; ++t) seen = words[t] == wd;
+            if (!seen) words[nw++] = wd;
+          }
+          int bank[32] = {0};
+          int mx = 0;
+          for (int t = 0; t < nw; ++t) {
+            const int v = ++bank[words[t] & 31];
+            if (v > mx) mx = v;
+          }
+          cost[si] += mx;
+        }
+      }
+    }
+    for (int si = 0; si < kCand; ++si) {
+      const double cst = cost[si] / (kWarps * kCopies);
+      if (cst < best - 1e-9) {
+        best = cst;
+        info->row_words = (uint32_t)(min_words + si);
+        info->lane_shift = (uint32_t)ls;
+      }
+    }
+  }
+  info->est_wavefronts = best;
+}
+
 // Hoisted split: u = 5 copy sites, l loop sites, the rest per-thread.  l is
 // chosen so that a full walk still has >= ~2^20 runs to spread over 148 SMs.
-int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
-                 isd_plan_info* info) {
-  std::memset(info, 0, sizeof(*info));
+int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint) {
   const int n = (int)lat->n_spins;
   const int u = kCopyBits;
   int log_configs = 0;
@@ -87,6 +186,15 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   if (const char* env = std::getenv("ISD_LOOP_BITS")) l = std::atoi(env);
   if (l > 7) l = 7;
   if (l < 0) l = 0;
+  return l;
+}
+
+int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
+                 isd_plan_info* info) {
+  std::memset(info, 0, sizeof(*info));
+  const int n = (int)lat->n_spins;
+  const int u = kCopyBits;
+  const int l = plan_loop_bits(lat, n_configs_hint);
   const int k = u + l;
   info->u = u;
   info->l = l;
@@ -135,6 +243,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   // The hoisted kernel needs all copy and loop sites inside the low word and
   // at least one run.
   if (n < k + 1 || k > 32) return 1;
+  choose_layout(lat, info);
   return 0;
 }
 
@@ -163,7 +272,13 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
   p->n_classes = lat->n_classes;
   p->stride = info->stride;
   p->nbins = (lat->n_spins + 1) * p->stride;
-  p->hist_words = hist_words_for(p->nbins);
+  p->row_words = info->row_words;
+  p->row_bytes = 4 * info->row_words;
+  p->e_halved = info->e_halved;
+  p->e_parity = info->e_parity;
+  p->e_bytes = info->e_halved ? 2 : 4;
+  p->lane_shift = info->lane_shift;
+  p->hist_words = hist_words_for((lat->n_spins + 1) * info->row_words);
   p->n_hist = (uint32_t)hist_count_for(p->hist_words);
   const uint32_t var = (uint32_t)info->var_mask;
   for (uint32_t c = 0; c < lat->n_classes; ++c) {
@@ -185,12 +300,19 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
     p->degree[q] = info->copy_degree[q];
     if (info->copy_nbr2[q]) p->has_double = 1;
   }
+  // copy_table[c] = popc(c)(B+1) + unsat_cc(c); split it back into the
+  // m and e parts and express the subset-sum steps in bytes
+  const int eb = (int)p->e_bytes, rb = (int)p->row_bytes;
+  auto unsat = [&](int c) {
+    return info->copy_table[c] -
+           __builtin_popcount((unsigned)c) * (int)info->stride;
+  };
   for (int c = 0; c < kCopies; ++c) {
     if (c == 0) {
-      p->ktd[0] = 4 * info->copy_table[0];
+      p->ktd[0] = eb * unsat(0);
     } else {
       const int top = 31 - __builtin_clz((unsigned)c);
-      p->ktd[c] = 4 * (info->copy_table[c] - info->copy_table[c ^ (1 << top)]);
+      p->ktd[c] = rb + eb * (unsat(c) - unsat(c ^ (1 << top)));
     }
   }
 }

@@ -1,0 +1,42 @@
+"""Run one BASELINE config's full enumeration a few times (profiling driver).
+
+    python tools/run_k1.py --config c5 --reps 3 [--algo auto|canonical]
+
+Prints device ms per walk and configs/s; exits non-zero on a wrong table
+(verify_dos).  Used under ncu: the first launches are warm-up.
+"""
+
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import paper_1110_2561_b200 as isd  # noqa: E402
+from paper_1110_2561_b200 import _native  # noqa: E402
+from paper_1110_2561_b200.enumeration import enumerate_range_timed  # noqa: E402
+from paper_1110_2561_b200.workloads import workloads  # noqa: E402
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--config", default="c5")
+    p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--algo", default="auto", choices=["auto", "canonical"])
+    a = p.parse_args()
+    algo = _native.ALGO_AUTO if a.algo == "auto" else _native.ALGO_CANONICAL
+    spec = workloads()[a.config].spec
+    for i in range(a.reps):
+        table, ms = enumerate_range_timed(spec, 0, spec.num_configs, algo=algo)
+        dos = isd.DoSHistogram(spec, table.view("int64"))
+        ok = isd.verify_dos(dos).passed
+        print(f"{a.config} rep {i}: {ms:.3f} ms, "
+              f"{spec.num_configs / ms / 1e9:.3f} Tconf/s, verify={ok}",
+              flush=True)
+        if not ok:
+            return 1
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
