@@ -120,7 +120,7 @@ int isd_thermo_async(const uint64_t* counts_dev, uint32_t n_spins,
 /* The hoisted kernel's decomposition of the lattice.
  * u low sites are unrolled ("copy" sites), the next l sites are the
  * per-thread loop, the rest is the per-thread run prefix. */
-#define ISD_COPY_BITS 5
+#define ISD_COPY_BITS 7
 typedef struct isd_plan_info {
   uint32_t u, l, k;          /* k = u + l                               */
   uint32_t stride;           /* B + 1                                   */

@@ -15,7 +15,7 @@ import numpy as np
 from ._build import LIB
 
 ISD_MAX_CLASSES = 8
-ISD_COPY_BITS = 5
+ISD_COPY_BITS = 7
 ISD_THERMO_FIELDS = 7
 
 ALGO_AUTO = 0

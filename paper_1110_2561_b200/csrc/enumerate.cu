@@ -159,16 +159,27 @@ __global__ void __launch_bounds__(kThreads)
         e += nq;
         d[q] = (int)P.e_bytes * (P.degree[q] - 2 * nq);
       }
-      // ---- 32 copies: addr_c = addr_{c without top bit} + d_top + ktd[c]
-      uint32_t a[kCopies];
-      a[0] = a_run + (uint32_t)__popc(j) * P.row_bytes +
-             (uint32_t)e * P.e_bytes;
-      red_shared_inc(a[0]);
+      // ---- 128 copies.  addr_c = addr_{c ^ topbit(c)} + d_top + ktd[c]:
+      // the low five copy bits form a subset-sum tree (live set <= 16),
+      // and each leaf immediately spawns its three siblings in bits 5, 6.
+      const uint32_t a0 = a_run + (uint32_t)__popc(j) * P.row_bytes +
+                          (uint32_t)e * P.e_bytes;
+      uint32_t a[32];
 #pragma unroll
-      for (int c = 1; c < kCopies; ++c) {
-        const int top = 31 - __clz(c);
-        a[c] = a[c ^ (1 << top)] + (uint32_t)d[top] + (uint32_t)P.ktd[c];
-        red_shared_inc(a[c]);
+      for (int cl = 0; cl < 32; ++cl) {
+        if (cl == 0) {
+          a[0] = a0;
+        } else {
+          const int top = 31 - __clz(cl);
+          a[cl] = a[cl ^ (1 << top)] + (uint32_t)d[top] + (uint32_t)P.ktd[cl];
+        }
+        red_shared_inc(a[cl]);
+        const uint32_t b1 = a[cl] + (uint32_t)d[5] + (uint32_t)P.ktd[cl + 32];
+        red_shared_inc(b1);
+        const uint32_t b2 = a[cl] + (uint32_t)d[6] + (uint32_t)P.ktd[cl + 64];
+        red_shared_inc(b2);
+        const uint32_t b3 = b1 + (uint32_t)d[6] + (uint32_t)P.ktd[cl + 96];
+        red_shared_inc(b3);
       }
     }
   }

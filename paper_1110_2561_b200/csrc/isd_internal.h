@@ -10,7 +10,10 @@
 namespace isd {
 
 constexpr int kCopyBits = ISD_COPY_BITS;   // u: sites unrolled in registers
-constexpr int kCopies = 1 << kCopyBits;    // 32 configurations per group
+constexpr int kCopies = 1 << kCopyBits;    // 128 configurations per group
+static_assert(ISD_COPY_BITS == 7, "k1_hoisted emits 32 x 4 copies");
+constexpr int kTreeBits = 5;               // copies emitted as a 32-leaf tree
+                                           // plus outer bits 5..u-1
 constexpr int kMaxClasses = ISD_MAX_CLASSES;
 constexpr int kThreads = 512;              // threads per enumeration block
 

@@ -115,7 +115,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
   const int run_bits = n - k;
   if (run_bits < 5) return;
 
-  constexpr int kWarps = 24, kCand = 48;
+  constexpr int kWarps = 8, kCand = 48;
   static const int shifts[] = {0, 5, 10, 15};
   double best = 1e30;
   int m_s[32], e_s[32];
