@@ -115,8 +115,10 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
   const int run_bits = n - k;
   if (run_bits < 5) return;
 
-  constexpr int kWarps = 8, kCand = 48;
-  static const int shifts[] = {0, 5, 10, 15};
+  // sample: many warps, a random subset of copies each (copies of one warp
+  // are strongly correlated, so breadth over warps matters more)
+  constexpr int kWarps = 64, kCopySample = 16, kCand = 40;
+  static const int shifts[] = {0, 3, 6, 9, 12, 15};
   double best = 1e30;
   int m_s[32], e_s[32];
   for (int ls : shifts) {
@@ -127,7 +129,8 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
     for (int w = 0; w < kWarps; ++w) {
       const uint64_t hi = rng_next(&seed) % hi_count;
       const uint64_t j = (k > kCopyBits) ? rng_next(&seed) % (1ull << (k - kCopyBits)) : 0;
-      for (int c = 0; c < kCopies; ++c) {
+      for (int cs = 0; cs < kCopySample; ++cs) {
+        const int c = (int)(rng_next(&seed) % kCopies);
         for (int lane = 0; lane < 32; ++lane) {
           const uint64_t r = ((hi >> ls) << (ls + 5)) | ((uint64_t)lane << ls) |
                              (hi & ((1ull << ls) - 1));
@@ -161,7 +164,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
       }
     }
     for (int si = 0; si < kCand; ++si) {
-      const double cst = cost[si] / (kWarps * kCopies);
+      const double cst = cost[si] / (kWarps * kCopySample);
       if (cst < best - 1e-9) {
         best = cst;
         info->row_words = (uint32_t)(min_words + si);
@@ -172,7 +175,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
   info->est_wavefronts = best;
 }
 
-// Hoisted split: u = 5 copy sites, l loop sites, the rest per-thread.  l is
+// Hoisted split: u = 7 copy sites, l loop sites, the rest per-thread.  l is
 // chosen so that a full walk still has >= ~2^20 runs to spread over 148 SMs.
 int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint) {
   const int n = (int)lat->n_spins;

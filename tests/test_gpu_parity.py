@@ -52,7 +52,7 @@ def test_reference_golden_tables(name, algo):
 @pytest.mark.parametrize("loop_bits", [1, 4, 7])
 def test_reference_goldens_with_forced_loop_width(name, loop_bits, monkeypatch):
     spec, want = spec_from_csv(name)
-    if spec.num_spins < 5 + loop_bits + 1:
+    if spec.num_spins < 7 + loop_bits + 1:
         pytest.skip("too small for this loop width")
     monkeypatch.setenv("ISD_LOOP_BITS", str(loop_bits))
     got = full(spec, _native.ALGO_HOISTED)

@@ -235,7 +235,7 @@ REPLAY = [
 @pytest.mark.parametrize("loop_bits", [0, 3, 7])
 def test_hoisted_plan_replay_matches_oracle(kw, seed, loop_bits):
     spec, (r, c, d, j, per, signs) = _spec_and_oracle(kw, seed)
-    if spec.num_spins < 5 + loop_bits + 1:
+    if spec.num_spins < 7 + loop_bits + 1:
         pytest.skip("lattice too small for this loop width")
     lat = port.Lattice(r, c, d, j, per, signs)
     want = port.enumerate_range(lat, 0, 1 << lat.n)
