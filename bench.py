@@ -39,7 +39,7 @@ UNIT = "configs/s"
 def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -226,10 +226,11 @@ def run_b200(args, wl):
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def device_step_fn(w):
+    def device_step_fn(w, flip=False):
         spec = w.spec
         lat = native_lattice(spec)
         shard = isd.make_shards(spec, world)[rank]
+        algo = _native.ALGO_AUTO | (_native.FLAG_FLIP_SYMMETRY if flip else 0)
         table = torch.zeros((spec.num_spins + 1) * (spec.num_bonds + 1),
                             dtype=torch.int64, device=dev)
         fields = torch.tensor(w.fields, dtype=torch.float64, device=dev)
@@ -242,7 +243,7 @@ def run_b200(args, wl):
             ev[0].record(stream)
             nl = _native.enumerate_device(lat, shard.start_index,
                                           shard.end_index, table.data_ptr(),
-                                          sp, accumulate=False)
+                                          sp, accumulate=False, algo=algo)
             ev[1].record(stream)
             if world > 1:
                 dist.reduce(table, dst=0)
@@ -256,8 +257,8 @@ def run_b200(args, wl):
 
         return step, ev, table, out
 
-    def time_device(w, steps, warmup):
-        step, ev, table, out = device_step_fn(w)
+    def time_device(w, steps, warmup, flip=False):
+        step, ev, table, out = device_step_fn(w, flip)
         for _ in range(warmup):
             step()
         barrier()
@@ -345,6 +346,16 @@ def run_b200(args, wl):
         extra[name] = {"configs_per_s": w2.spec.num_configs / (ms2 / 1e3),
                        "ms_per_step": ms2}
 
+    # flip symmetry (extension, reported separately): walk 2^(N-1), mirror
+    flip = None
+    if world == 1:
+        t3, k3, _, tab3, _ = time_device(wl, args.steps, 3, flip=True)
+        ms3 = sum(t3) / len(t3)
+        same = bool(torch.equal(tab3, table))
+        flip = {"covered_configs_per_s": n_cfg / (ms3 / 1e3),
+                "evaluated_configs_per_s": (n_cfg // 2) / (ms3 / 1e3),
+                "ms_per_step": ms3, "table_identical": same}
+
     if world > 1:
         dist.destroy_process_group()
     if rank != 0:
@@ -392,7 +403,7 @@ def run_b200(args, wl):
         "gpu_launches": launches,
         "clocks": clk,
         "calibration": cal,
-        "extra": {"configs": extra},
+        "extra": {"configs": extra, "flip_symmetry": flip},
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, args.cpu_seconds)

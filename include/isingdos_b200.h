@@ -61,6 +61,11 @@ extern "C" {
 #define ISD_ALGO_AUTO 0       /* hoisted kernel for the aligned body, canonical head/tail */
 #define ISD_ALGO_CANONICAL 1  /* one full class-mask evaluation per configuration */
 #define ISD_ALGO_HOISTED 2    /* same as AUTO; errors if the lattice is too small */
+/* OR-able flag: walk only the configurations with the top spin down and
+ * complete the table with g(M, E) = h(M, E) + h(-M, E) (global spin flip
+ * preserves E for any couplings at zero field).  Only for full walks
+ * [0, 2^N); halves the enumerated configurations (reported separately). */
+#define ISD_FLAG_FLIP_SYMMETRY 0x100
 
 typedef struct isd_bond_class {
   uint32_t shift;     /* partner offset s, 1 <= s < N                    */
@@ -93,6 +98,11 @@ int isd_enumerate(const isd_lattice* lat, uint64_t start, uint64_t end,
 int isd_enumerate_async(const isd_lattice* lat, uint64_t start, uint64_t end,
                         int algo, uint64_t* counts_dev, int accumulate,
                         void* stream, int* launches);
+
+/* In-place completion of a half walk: counts[m][e] += counts[N-m][e]
+ * pairwise (rows m and N-m both become the sum).  Device buffer, async. */
+int isd_mirror_async(uint64_t* counts_dev, uint32_t n_spins, uint32_t n_bonds,
+                     void* stream);
 
 /* ---- thermodynamics (replaces partition_point/thermo_sweep, thermo.py:46-100)
  * For every (field f, temperature t) pair, in field-major order

@@ -21,12 +21,13 @@ ISD_THERMO_FIELDS = 7
 ALGO_AUTO = 0
 ALGO_CANONICAL = 1
 ALGO_HOISTED = 2
+FLAG_FLIP_SYMMETRY = 0x100
 
 EXPORTED_SYMBOLS = (
     "isd_enumerate", "isd_enumerate_async", "isd_thermo", "isd_thermo_async",
     "isd_plan", "isd_validate", "isd_calibrate", "isd_device_count",
     "isd_sm_count", "isd_last_error", "isd_version", "isd_abi_version",
-    "isd_launch_count",
+    "isd_launch_count", "isd_mirror_async",
 )
 
 
@@ -97,6 +98,8 @@ def load():
                                    p_dbl]
         lib.isd_thermo_async.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32,
                                          dbl, vp, i32, vp, i32, vp, vp]
+        lib.isd_mirror_async.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32,
+                                         vp]
         lib.isd_plan.argtypes = [p_lat, u64, ctypes.POINTER(PlanInfo)]
         lib.isd_validate.argtypes = [p_lat]
         lib.isd_calibrate.argtypes = [i32, i32, p_dbl, p_dbl]
@@ -107,7 +110,7 @@ def load():
         for name in ("isd_enumerate", "isd_enumerate_async", "isd_thermo",
                      "isd_thermo_async", "isd_plan", "isd_validate",
                      "isd_calibrate", "isd_device_count", "isd_sm_count",
-                     "isd_abi_version"):
+                     "isd_abi_version", "isd_mirror_async"):
             getattr(lib, name).restype = ctypes.c_int
         if lib.isd_abi_version() != 1:
             raise ImportError("isingdos-b200 ABI version mismatch")

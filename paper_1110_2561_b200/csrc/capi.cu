@@ -151,7 +151,36 @@ static int enqueue_canonical(const isd_lattice* lat, uint64_t a, uint64_t b,
 
 static int enumerate_impl(const isd_lattice* lat, uint64_t start,
                           uint64_t end, int algo, unsigned long long* out,
+                          int accumulate, cudaStream_t st, int* launches);
+
+// Half walk + mirror (ISD_FLAG_FLIP_SYMMETRY).
+static int enumerate_flip(const isd_lattice* lat, uint64_t start, uint64_t end,
+                          int algo, unsigned long long* out, int accumulate,
+                          cudaStream_t st, int* launches) {
+  const uint64_t total = 1ull << lat->n_spins;
+  if (start != 0 || end != total)
+    return fail(ISD_EINVAL, "flip symmetry needs the full range [0, 2^N)");
+  if (accumulate)
+    return fail(ISD_EINVAL, "flip symmetry cannot accumulate into a table");
+  int nl = 0;
+  int rc = enumerate_impl(lat, 0, total / 2, algo & 0xff, out, 0, st, &nl);
+  if (rc) return rc;
+  int r = launch_mirror(out, lat->n_spins, lat->n_bonds, st);
+  if (r < 0) return cuda_fail((cudaError_t)(-r), "k3_mirror launch");
+  if (launches) *launches = nl + r;
+  return ISD_OK;
+}
+
+static int enumerate_impl(const isd_lattice* lat, uint64_t start,
+                          uint64_t end, int algo, unsigned long long* out,
                           int accumulate, cudaStream_t st, int* launches) {
+  if (algo & ISD_FLAG_FLIP_SYMMETRY) {
+    char err0[256];
+    int rc0 = validate_lattice(lat, err0, sizeof err0);
+    if (rc0) return fail(rc0, "%s", err0);
+    return enumerate_flip(lat, start, end, algo, out, accumulate, st,
+                          launches);
+  }
   char err[256];
   int rc = validate_lattice(lat, err, sizeof err);
   if (rc) return fail(rc, "%s", err);
@@ -303,6 +332,18 @@ int isd_enumerate(const isd_lattice* lat, uint64_t start, uint64_t end,
     cudaEventElapsedTime(&ms, s->ev0, s->ev1);
     *device_ms = ms;
   }
+  return ISD_OK;
+}
+
+int isd_mirror_async(uint64_t* counts_dev, uint32_t n_spins, uint32_t n_bonds,
+                     void* stream) {
+  if (!counts_dev || n_spins < 1 || n_spins > ISD_MAX_SPINS ||
+      n_bonds > 3 * ISD_MAX_SPINS)
+    return fail(ISD_EINVAL, "bad table N=%u B=%u", n_spins, n_bonds);
+  int r = launch_mirror(reinterpret_cast<unsigned long long*>(counts_dev),
+                        n_spins, n_bonds, stream);
+  if (r < 0) return cuda_fail((cudaError_t)(-r), "k3_mirror launch");
+  bump_launches((uint64_t)r);
   return ISD_OK;
 }
 

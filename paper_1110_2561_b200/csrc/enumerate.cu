@@ -201,6 +201,36 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------
+// flip-symmetry completion: rows m and N-m both become their sum
+// ---------------------------------------------------------------------------
+__global__ void k3_mirror(unsigned long long* __restrict__ t, uint32_t n,
+                          uint32_t stride) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t half_rows = n / 2 + 1;  // rows 0..n/2
+  if (i >= half_rows * stride) return;
+  const uint32_t m = i / stride, e = i - m * stride;
+  const uint32_t mm = n - m;
+  if (mm < m) return;
+  const unsigned long long a = t[m * stride + e];
+  if (mm == m) {
+    t[m * stride + e] = 2 * a;
+  } else {
+    const unsigned long long b = t[mm * stride + e];
+    t[m * stride + e] = a + b;
+    t[mm * stride + e] = a + b;
+  }
+}
+
+int launch_mirror(unsigned long long* t, uint32_t n, uint32_t b,
+                  void* stream) {
+  const uint32_t stride = b + 1;
+  const uint32_t work = (n / 2 + 1) * stride;
+  k3_mirror<<<(work + 255) / 256, 256, 0, (cudaStream_t)stream>>>(t, n, stride);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 1 : -(int)e;
+}
+
+// ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
 static int blocks_for(const void* fn, size_t smem, int sm_count) {

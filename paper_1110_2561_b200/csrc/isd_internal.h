@@ -79,6 +79,8 @@ int launch_canonical(const CanonParams& p, unsigned long long* out,
                      int sm_count, void* stream, bool small_grid);
 int launch_hoisted(const HoistParams& p, unsigned long long* out,
                    int sm_count, void* stream);
+int launch_mirror(unsigned long long* t, uint32_t n, uint32_t b,
+                  void* stream);
 int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
                   uint32_t n_bonds, double scale, const double* fields,
                   int n_fields, const double* temps, int n_temps, double* out,

@@ -189,6 +189,25 @@ def test_n36_canonical_equals_hoisted():
     assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_flip_symmetry_half_walk_equals_full_walk(name):
+    spec = workloads()[name].spec
+    whole = full(spec)
+    half, _ = enumerate_range_timed(
+        spec, 0, spec.num_configs,
+        algo=_native.ALGO_AUTO | _native.FLAG_FLIP_SYMMETRY)
+    assert np.array_equal(half.view(np.int64), whole)
+    dos = isd.full_dos(spec, workers=3, flip_symmetry=True)
+    assert np.array_equal(dos.counts, whole)
+
+
+def test_flip_symmetry_rejects_partial_ranges():
+    spec = isd.LatticeSpec(4, 4)
+    with pytest.raises(ValueError, match="full range"):
+        enumerate_range_timed(spec, 0, 100,
+                              algo=_native.FLAG_FLIP_SYMMETRY)
+
+
 @pytest.mark.parametrize("shards", [2, 3, 8])
 def test_shard_count_invisible_at_n36(shards):
     spec = workloads()["c5"].spec
