@@ -190,6 +190,75 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------
+# roofline
+# --------------------------------------------------------------------------
+
+def ncu_traffic(config):
+    """dram read+write bytes per launch of k1_hoisted from the committed
+    ncu --set full capture (profiles/r1_ncu_k1_hoisted_<config>.txt)."""
+    path = os.path.join(ROOT, "profiles", f"r1_ncu_k1_hoisted_{config}.txt")
+    if not os.path.exists(path):
+        return None
+    total = 0.0
+    scale = {"[byte]": 1, "[Kbyte]": 1e3, "[Mbyte]": 1e6, "[Gbyte]": 1e9}
+    for ln in open(path):
+        if "dram__bytes_read.sum [" in ln or "dram__bytes_write.sum [" in ln:
+            unit = ln.split()[1]
+            total += float(ln.split("=")[1]) * scale.get(unit, 1)
+    return total
+
+
+def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1):
+    """Two rooflines for the dominant kernel (k1_hoisted).
+
+    `roofline`: the pipe the kernel is bound by (ncu: shared-memory
+    wavefronts at 94-95% of peak).  k1_hoisted issues exactly one
+    shared-memory reduction lane per configuration, so the algorithmic work
+    is 1 RED lane per configuration and the peak is the measured
+    conflict-free RED.shared rate (K0 probe 3) x SMs x SM clock.
+
+    `roofline_int_pipe`: BASELINE.md §4's integer-pipe roofline of the
+    canonical formulation (POPC and ALU ops per
+    configuration) with the K0-measured POPC/LOP3 rates; k1_hoisted does
+    far less integer work per configuration than that formulation, so its
+    fraction exceeds 1 (k1_canonical runs at ~0.97 of it).
+    """
+    from paper_1110_2561_b200.workloads import canonical_ops
+    mhz = clk.get("sm_mhz")
+    if not cal or not mhz:
+        return ({"bound": "smem-atomic", "achieved": None, "peak": None,
+                 "unit": "Gconf/s", "frac": None, "traffic": None},
+                None)
+    f = mhz * 1e6
+    ach = cfg_per_launch / (ms_k1 / 1e3)
+    p_red = cal["red_shared_spread"]["lanes_per_clk_sm"]
+    peak_red = sm_count * f * p_red
+    roof = {
+        "bound": "smem-atomic", "achieved": ach / 1e9, "peak": peak_red / 1e9,
+        "unit": "Gconf/s", "frac": ach / peak_red,
+        "traffic": ncu_traffic(wl.name),
+        "kernel": "k1_hoisted", "kernel_ms": ms_k1,
+        "algorithmic_work": "1 RED.shared lane per configuration",
+        "peak_source": f"K0 red_shared_spread {p_red:.2f} lanes/clk/SM x "
+                       f"{sm_count} SMs x {mhz:.0f} MHz (measured, this GPU)",
+        "traffic_source": "ncu --set full, profiles/r1_ncu_k1_hoisted_*.txt",
+    }
+    popc_ops, alu_ops = canonical_ops(wl.spec)
+    p_popc = cal["popc"]["lanes_per_clk_sm"]
+    p_alu = cal["lop3"]["lanes_per_clk_sm"]
+    peak_int = sm_count * f * min(p_alu / alu_ops, p_popc / popc_ops)
+    roof_int = {
+        "bound": "int-pipe", "achieved": ach / 1e9, "peak": peak_int / 1e9,
+        "unit": "Gconf/s", "frac": ach / peak_int,
+        "formula": "n_SM * f_SM * min(P_alu/ALU_ops, P_popc/POPC_ops), "
+                   f"canonical POPC={popc_ops} ALU={alu_ops} per config "
+                   "(BASELINE.md §4, SURVEY.md §8d)",
+        "p_popc": p_popc, "p_alu": p_alu,
+    }
+    return roof, roof_int
+
+
+# --------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------
 
@@ -363,28 +432,7 @@ def run_b200(args, wl):
 
     # ---- roofline ------------------------------------------------------------
     sm_count = _native.sm_count(local)
-    popc_ops, alu_ops = canonical_ops(wl.spec)
-    roof = {"bound": "int-pipe", "unit": "Gconf/s", "traffic": None}
-    mhz = clk.get("sm_mhz") or None
-    if cal and mhz:
-        p_popc = cal["popc"]["lanes_per_clk_sm"]
-        p_alu = cal["lop3"]["lanes_per_clk_sm"]
-        peak = sm_count * mhz * 1e6 * min(p_alu / alu_ops, p_popc / popc_ops)
-        ach = (n_cfg / world) / (ms_k1 / 1e3)
-        roof.update({
-            "achieved": ach / 1e9, "peak": peak / 1e9, "frac": ach / peak,
-            "formula": "n_SM * f_SM * min(P_alu/ALU_ops, P_popc/POPC_ops) "
-                       "(BASELINE.md §4), canonical ops per config "
-                       f"POPC={popc_ops} ALU={alu_ops}; P measured by K0 on "
-                       "this GPU; f_SM = median SM clock under load",
-            "kernel": "k1_hoisted", "kernel_ms": ms_k1,
-            "p_popc": p_popc, "p_alu": p_alu, "sm_count": sm_count,
-            "f_sm_mhz": mhz,
-        })
-        # the resource the hoisted kernel actually spends: one shared
-        # reduction per configuration
-        p_red = cal["red_shared_hashed"]["lanes_per_clk_sm"]
-        roof["red_shared_frac"] = ach / (sm_count * mhz * 1e6 * p_red)
+    roof, roof_int = roofline(wl, cal, clk, sm_count, n_cfg // world, ms_k1)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -397,6 +445,7 @@ def run_b200(args, wl):
                    "l2": "flushed (256 MiB write) between timed steps",
                    "verify_dos_passed": ok},
         "roofline": roof,
+        "roofline_int_pipe": roof_int,
         "e2e": {"value": n_cfg / (e2e_step_ms / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_step_ms},

@@ -246,3 +246,33 @@ def test_hoisted_plan_replay_matches_oracle(kw, seed, loop_bits):
 def test_plan_refuses_tiny_lattices():
     usable, _ = _native.plan(native_lattice(isd.LatticeSpec(2, 2)), 16)
     assert not usable
+
+
+def _integration_stub_classes(spec):
+    # the class compiler shown in INTEGRATION.md (a reference-side binding)
+    R, C, D = spec.rows, spec.cols, spec.depth
+    dims, strides = (R, C, D), (1, R, R * C)
+    out = []
+    for a in range(3 if D > 1 else 2):
+        inner = wrap = 0
+        for l in range(D):
+            for c in range(C):
+                for r in range(R):
+                    coord = (r, c, l)[a]
+                    bit = 1 << ((l * C + c) * R + r)
+                    if coord < dims[a] - 1:
+                        inner |= bit
+                    if coord == 0:
+                        wrap |= bit
+        neg = spec.coupling < 0
+        out += [(strides[a], inner, inner if neg else 0),
+                ((dims[a] - 1) * strides[a], wrap, wrap if neg else 0)]
+    return out
+
+
+@pytest.mark.parametrize("spec", [isd.LatticeSpec(4, 4), isd.LatticeSpec(5, 5),
+                                  isd.LatticeSpec(3, 3, 4),
+                                  isd.LatticeSpec(2, 3, 2, -1),
+                                  isd.LatticeSpec(17, 2)])
+def test_integration_stub_matches_bond_classes(spec):
+    assert _integration_stub_classes(spec) == spec.bond_classes()
