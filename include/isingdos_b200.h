@@ -142,14 +142,16 @@ typedef struct isd_plan_info {
   uint64_t copy_nbr2[ISD_COPY_BITS];     /* second copy (double bonds)    */
   uint64_t copy_jneg2[ISD_COPY_BITS];
   int32_t  copy_table[1 << ISD_COPY_BITS]; /* KT[c] = popc(c)(B+1) + CT-CT unsat */
-  /* shared-histogram layout: word(m, e) = m*row_words + (e_halved ?
-   * (e - e_parity)/2 : e).  e is halved when every site has even degree
-   * (then e_idx always has the parity e_parity).  row_words and the lane
-   * placement are chosen on the host to minimise bank conflicts. */
+  /* shared-histogram layout: word(m, e) = m*row_words + e'*e_words with
+   * e' = e, or (e - e_parity)/2 when every site has even degree (then e_idx
+   * always has the parity e_parity).  The strides (m-major or e-major) and
+   * the lane placement are chosen on the host to minimise bank conflicts. */
   uint32_t row_words;
   uint32_t e_halved;
   uint32_t e_parity;
   uint32_t lane_shift;       /* warp lanes differ in run bits [s, s+5)  */
+  uint32_t e_words;
+  uint32_t hist_words;       /* words spanned by one histogram          */
   double   est_wavefronts;   /* predicted smem wavefronts per warp RED  */
 } isd_plan_info;
 
@@ -161,7 +163,9 @@ int isd_validate(const isd_lattice* lat);
 
 /* ---- calibration microbenchmarks (K0) -------------------------------- */
 /* which: 0 = POPC, 1 = LOP3, 2 = IADD3, 3 = RED.shared spread,
- *        4 = RED.shared realistic bins, 5 = IMAD.  Writes lanes per clock
+ *        4 = RED.shared realistic bins, 5 = IMAD, 6 = SHF, 7 = RED.shared
+ *        all lanes on one word, 8 = lane pairs per word (16 banks),
+ *        9 = 4 words in one bank, 10 = 8 words x 4 lanes, distinct banks.  Writes lanes per clock
  *        per SM to *lanes_per_clk_sm and the SM clock seen (MHz). */
 int isd_calibrate(int device, int which, double* lanes_per_clk_sm,
                   double* sm_mhz);

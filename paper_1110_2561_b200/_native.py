@@ -55,6 +55,7 @@ class PlanInfo(ctypes.Structure):
         ("copy_table", ctypes.c_int32 * (1 << ISD_COPY_BITS)),
         ("row_words", ctypes.c_uint32), ("e_halved", ctypes.c_uint32),
         ("e_parity", ctypes.c_uint32), ("lane_shift", ctypes.c_uint32),
+        ("e_words", ctypes.c_uint32), ("hist_words", ctypes.c_uint32),
         ("est_wavefronts", ctypes.c_double),
     ]
 

@@ -93,6 +93,45 @@ __global__ void __launch_bounds__(kCalThreads)
                        : "r"(a));
       }
       break;
+    case 7:  // RED.shared, all 32 lanes on one word (hardware aggregation)
+      for (int it = 0; it < kCalIters; ++it) {
+#pragma unroll
+        for (int i = 0; i < kChains; ++i) {
+          const uint32_t addr = sbase + 4u * (32u * ((it * kChains + i) & 255));
+          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+        }
+      }
+      break;
+    case 8:  // RED.shared, lane pairs share a word, 16 distinct banks
+      for (int it = 0; it < kCalIters; ++it) {
+#pragma unroll
+        for (int i = 0; i < kChains; ++i) {
+          const uint32_t addr =
+              sbase + 4u * ((lane >> 1) + 32u * ((it * kChains + i) & 255));
+          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+        }
+      }
+      break;
+    case 9:  // RED.shared, 4 distinct words in one bank (8 lanes each)
+      for (int it = 0; it < kCalIters; ++it) {
+#pragma unroll
+        for (int i = 0; i < kChains; ++i) {
+          const uint32_t addr =
+              sbase + 4u * (32u * ((lane >> 3) + 4u * ((it * kChains + i) & 63)));
+          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+        }
+      }
+      break;
+    case 10:  // RED.shared, 8 distinct words, distinct banks, 4 lanes each
+      for (int it = 0; it < kCalIters; ++it) {
+#pragma unroll
+        for (int i = 0; i < kChains; ++i) {
+          const uint32_t addr =
+              sbase + 4u * ((lane >> 2) * 3u + 32u * ((it * kChains + i) & 255));
+          asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+        }
+      }
+      break;
     default:
       break;
   }

@@ -190,9 +190,9 @@ __global__ void __launch_bounds__(kThreads)
     uint32_t word;
     if (P.e_halved) {
       if ((e ^ P.e_parity) & 1) continue;  // structurally empty
-      word = m * P.row_words + ((e - P.e_parity) >> 1);
+      word = m * P.row_words + ((e - P.e_parity) >> 1) * P.e_words;
     } else {
-      word = m * P.row_words + e;
+      word = m * P.row_words + e * P.e_words;
     }
     unsigned long long s = 0;
     for (uint32_t h = 0; h < P.n_hist; ++h) s += hist[h * P.hist_words + word];

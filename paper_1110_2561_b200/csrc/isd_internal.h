@@ -46,9 +46,11 @@ struct HoistParams {
   uint32_t n_hist;
   uint32_t has_double;           // any copy site with a doubled partner
   uint32_t lane_shift;           // warp lanes take run bits [s, s+5)
-  uint32_t row_words;            // shared words per m row
+  uint32_t row_words;            // word stride of m
   uint32_t row_bytes;            // 4 * row_words
-  uint32_t e_bytes;              // bytes per unit of e (4, or 2 if halved)
+  uint32_t e_words;              // word stride of e' (e or (e - parity)/2)
+  uint32_t e_bytes;              // bytes per unit of e (4 or 2 per e' word)
+  uint32_t pad2_;
   uint32_t e_halved, e_parity;
   uint32_t shift[kMaxClasses];
   uint32_t mvar[kMaxClasses];    // class mask restricted to bits [u, k)

@@ -110,6 +110,8 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
   info->e_parity = even ? (uint32_t)(neg & 1) : 0;
   const int min_words = even ? (b - (int)info->e_parity) / 2 + 1 : b + 1;
   info->row_words = (uint32_t)min_words;
+  info->e_words = 1;
+  info->hist_words = (uint32_t)((n + 1) * min_words);
   info->lane_shift = 0;
   info->est_wavefronts = 0;
   const int run_bits = n - k;
@@ -117,7 +119,16 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
 
   // sample: many warps, a random subset of copies each (copies of one warp
   // are strongly correlated, so breadth over warps matters more)
-  constexpr int kWarps = 64, kCopySample = 16, kCand = 40;
+  // candidate strides: m-major (A = S >= row length, B = 1) and e-major
+  // (A = 1, B = R >= N + 1)
+  constexpr int kWarps = 64, kCopySample = 16, kHalf = 40, kCand = 2 * kHalf;
+  int cand_a[kCand], cand_b[kCand];
+  for (int si = 0; si < kHalf; ++si) {
+    cand_a[si] = min_words + si;
+    cand_b[si] = 1;
+    cand_a[kHalf + si] = 1;
+    cand_b[kHalf + si] = n + 1 + si;
+  }
   static const int shifts[] = {0, 3, 6, 9, 12, 15};
   double best = 1e30;
   int m_s[32], e_s[32];
@@ -144,11 +155,10 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
           e_s[lane] = even ? (e - (int)info->e_parity) / 2 : e;
         }
         for (int si = 0; si < kCand; ++si) {
-          const int S = min_words + si;
           int words[32];
           int nw = 0;
           for (int lane = 0; lane < 32; ++lane) {
-            const int wd = m_s[lane] * S + e_s[lane];
+            const int wd = m_s[lane] * cand_a[si] + e_s[lane] * cand_b[si];
             bool seen = false;
             for (int t = 0; t < nw && !seen; ++t) seen = words[t] == wd;
             if (!seen) words[nw++] = wd;
@@ -167,12 +177,15 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
       const double cst = cost[si] / (kWarps * kCopySample);
       if (cst < best - 1e-9) {
         best = cst;
-        info->row_words = (uint32_t)(min_words + si);
+        info->row_words = (uint32_t)cand_a[si];
+        info->e_words = (uint32_t)cand_b[si];
         info->lane_shift = (uint32_t)ls;
       }
     }
   }
   info->est_wavefronts = best;
+  info->hist_words = (uint32_t)(n * (int)info->row_words +
+                                (min_words - 1) * (int)info->e_words + 1);
 }
 
 // Hoisted split: u = 7 copy sites, l loop sites, the rest per-thread.  l is
@@ -277,11 +290,12 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
   p->nbins = (lat->n_spins + 1) * p->stride;
   p->row_words = info->row_words;
   p->row_bytes = 4 * info->row_words;
+  p->e_words = info->e_words;
   p->e_halved = info->e_halved;
   p->e_parity = info->e_parity;
-  p->e_bytes = info->e_halved ? 2 : 4;
+  p->e_bytes = (info->e_halved ? 2 : 4) * info->e_words;
   p->lane_shift = info->lane_shift;
-  p->hist_words = hist_words_for((lat->n_spins + 1) * info->row_words);
+  p->hist_words = hist_words_for(info->hist_words);
   p->n_hist = (uint32_t)hist_count_for(p->hist_words);
   const uint32_t var = (uint32_t)info->var_mask;
   for (uint32_t c = 0; c < lat->n_classes; ++c) {

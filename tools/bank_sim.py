@@ -83,3 +83,25 @@ if __name__ == "__main__":
             for ls in (0, 5, 10, 15):
                 print(name, layout, "ls", ls, round(simulate(spec, ls=ls,
                       layout=layout, warps=150), 3), flush=True)
+
+
+def simulate_rep(spec, k, ls, S, halved, R, skew_words, warps=60, seed=3):
+    """Lanes use histogram copy (lane % R) placed skew_words*(lane%R) apart."""
+    rng = np.random.default_rng(seed)
+    n = spec.num_spins
+    run_bits = n - k
+    tot = cnt = 0
+    lanes = np.arange(32, dtype=np.int64)
+    for _ in range(warps):
+        hi = int(rng.integers(0, 1 << (run_bits - 5)))
+        r = ((hi >> ls) << (ls + 5)) | (lanes << ls) | (hi & ((1 << ls) - 1))
+        j = int(rng.integers(0, 1 << (k - 7)))
+        for c in rng.integers(0, 128, size=24):
+            x = (r.astype(np.uint64) << np.uint64(k)) | np.uint64(j << 7) | np.uint64(c)
+            m, e = bins_of(spec, x)
+            ep = (e >> 1) if halved else e
+            w = m * S + ep + (lanes % R) * skew_words
+            words = np.unique(w)
+            tot += np.bincount(words % 32, minlength=32).max()
+            cnt += 1
+    return tot / cnt
