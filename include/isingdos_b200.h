@@ -128,30 +128,37 @@ int isd_thermo_async(const uint64_t* counts_dev, uint32_t n_spins,
 /* ---- host-side plan (no GPU needed; used by the CPU tests) ----------- */
 
 /* The hoisted kernel's decomposition of the lattice.
- * u low sites are unrolled ("copy" sites), the next l sites are the
- * per-thread loop, the rest is the per-thread run prefix. */
+ * The low k index bits are split into u "copy" sites (unrolled in
+ * registers) and l loop sites (the thread's loop counter, enumerated as the
+ * subsets of loop_mask); bits [k, N) are the per-thread run prefix. */
 #define ISD_COPY_BITS 7
 typedef struct isd_plan_info {
   uint32_t u, l, k;          /* k = u + l                               */
   uint32_t stride;           /* B + 1                                   */
   uint64_t run_mask_above_k; /* bits [k, N)                             */
-  uint64_t var_mask;         /* bits [u, k)                             */
-  int32_t  copy_degree[ISD_COPY_BITS];   /* d_p: bonds from p to sites >= u */
-  uint64_t copy_nbr1[ISD_COPY_BITS];     /* partner masks (first copy)    */
+  uint64_t loop_mask;        /* the l loop sites (bits of [0, k))        */
+  int32_t  copy_site[ISD_COPY_BITS];     /* site of copy bit t            */
+  int32_t  copy_degree[ISD_COPY_BITS];   /* bonds to non-copy sites       */
+  uint64_t copy_nbr1[ISD_COPY_BITS];     /* non-copy partner masks        */
   uint64_t copy_jneg1[ISD_COPY_BITS];    /* partner sign masks            */
   uint64_t copy_nbr2[ISD_COPY_BITS];     /* second copy (double bonds)    */
   uint64_t copy_jneg2[ISD_COPY_BITS];
-  int32_t  copy_table[1 << ISD_COPY_BITS]; /* KT[c] = popc(c)(B+1) + CT-CT unsat */
-  /* shared-histogram layout: word(m, e) = m*row_words + e'*e_words with
-   * e' = e, or (e - e_parity)/2 when every site has even degree (then e_idx
-   * always has the parity e_parity).  The strides (m-major or e-major) and
-   * the lane placement are chosen on the host to minimise bank conflicts. */
-  uint32_t row_words;
-  uint32_t e_halved;
+  int32_t  copy_table[1 << ISD_COPY_BITS]; /* popc(c)(B+1) + copy-copy unsat */
+  /* Shared-histogram layout.  e_mode 0: word = m*row_words + e*e_words.
+   * e_mode 1 (every copy site has even degree): e_idx has the parity
+   * par(x) = (popc(x & odd_mask) + e_parity) & 1, constant over the 128
+   * copies of a group, and word = m*row_words + ((e - par)/2)*e_words +
+   * par*plane_words (two half-size parity planes; one plane when odd_mask
+   * is 0).  Strides and the lane placement minimise bank conflicts. */
+  uint32_t e_mode;
   uint32_t e_parity;
-  uint32_t lane_shift;       /* warp lanes differ in run bits [s, s+5)  */
+  uint64_t odd_mask;         /* sites of odd degree                     */
+  uint32_t row_words;
   uint32_t e_words;
+  uint32_t plane_words;
   uint32_t hist_words;       /* words spanned by one histogram          */
+  uint32_t lane_shift;       /* warp lanes differ in run bits [s, s+5)  */
+  uint32_t reserved;
   double   est_wavefronts;   /* predicted smem wavefronts per warp RED  */
 } isd_plan_info;
 

@@ -46,16 +46,19 @@ class PlanInfo(ctypes.Structure):
     _fields_ = [
         ("u", ctypes.c_uint32), ("l", ctypes.c_uint32), ("k", ctypes.c_uint32),
         ("stride", ctypes.c_uint32),
-        ("run_mask_above_k", ctypes.c_uint64), ("var_mask", ctypes.c_uint64),
+        ("run_mask_above_k", ctypes.c_uint64), ("loop_mask", ctypes.c_uint64),
+        ("copy_site", ctypes.c_int32 * ISD_COPY_BITS),
         ("copy_degree", ctypes.c_int32 * ISD_COPY_BITS),
         ("copy_nbr1", ctypes.c_uint64 * ISD_COPY_BITS),
         ("copy_jneg1", ctypes.c_uint64 * ISD_COPY_BITS),
         ("copy_nbr2", ctypes.c_uint64 * ISD_COPY_BITS),
         ("copy_jneg2", ctypes.c_uint64 * ISD_COPY_BITS),
         ("copy_table", ctypes.c_int32 * (1 << ISD_COPY_BITS)),
-        ("row_words", ctypes.c_uint32), ("e_halved", ctypes.c_uint32),
-        ("e_parity", ctypes.c_uint32), ("lane_shift", ctypes.c_uint32),
-        ("e_words", ctypes.c_uint32), ("hist_words", ctypes.c_uint32),
+        ("e_mode", ctypes.c_uint32), ("e_parity", ctypes.c_uint32),
+        ("odd_mask", ctypes.c_uint64),
+        ("row_words", ctypes.c_uint32), ("e_words", ctypes.c_uint32),
+        ("plane_words", ctypes.c_uint32), ("hist_words", ctypes.c_uint32),
+        ("lane_shift", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
         ("est_wavefronts", ctypes.c_double),
     ]
 

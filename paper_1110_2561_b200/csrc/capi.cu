@@ -117,6 +117,7 @@ static int cached_plan(const isd_lattice* lat, uint64_t hint,
   const int l = plan_loop_bits(lat, hint);
   std::string key(reinterpret_cast<const char*>(lat), sizeof(*lat));
   key.push_back((char)l);
+  if (const char* v = std::getenv("ISD_COPY_VARIANT")) key += v;
   std::lock_guard<std::mutex> lock(g_plan_mu);
   auto it = g_plans.find(key);
   if (it == g_plans.end()) {

@@ -140,12 +140,16 @@ __global__ void __launch_bounds__(kThreads)
       if constexpr (DOUBLE)
         npr[q] += __popcll((xt ^ P.jn2[q]) & P.nm2[q] & P.above_k);
     }
-    // byte address of (m_run, e = 0 - parity) in this warp's histogram
-    const uint32_t a_run = hbase + (uint32_t)m_run * P.row_bytes -
-                           P.e_parity * P.e_bytes + (uint32_t)P.ktd[0];
-    // ---- loop over bits [u, k) ----
-    for (uint32_t j = 0; j < nloop; ++j) {
-      const uint32_t jb = j << kCopyBits;
+    // byte address of (m_run, e = 0) in this warp's histogram; the e parity
+    // of the configurations is par_run ^ parity(loop bits & odd_mask)
+    const uint32_t a_run =
+        hbase + (uint32_t)m_run * P.row_bytes + (uint32_t)P.ktd[0];
+    const uint32_t par_run =
+        (uint32_t)(__popcll(xt & P.odd_mask) + P.e_parity) & 1u;
+    const uint32_t odd_loop = (uint32_t)P.odd_mask & P.loop_mask;
+    // ---- loop over the subsets of the loop sites ----
+    uint32_t jb = 0;
+    for (uint32_t it = 0; it < nloop; ++it) {
       int e = e_run;
 #pragma unroll
       for (int c = 0; c < NC; ++c)
@@ -159,11 +163,13 @@ __global__ void __launch_bounds__(kThreads)
         e += nq;
         d[q] = (int)P.e_bytes * (P.degree[q] - 2 * nq);
       }
+      const uint32_t par = (par_run + __popc(jb & odd_loop)) & 1u;
       // ---- 128 copies.  addr_c = addr_{c ^ topbit(c)} + d_top + ktd[c]:
       // the low five copy bits form a subset-sum tree (live set <= 16),
       // and each leaf immediately spawns its three siblings in bits 5, 6.
-      const uint32_t a0 = a_run + (uint32_t)__popc(j) * P.row_bytes +
-                          (uint32_t)e * P.e_bytes;
+      const uint32_t a0 = a_run + (uint32_t)__popc(jb) * P.row_bytes +
+                          (uint32_t)e * P.e_bytes +
+                          par * (uint32_t)P.plane_bytes;
       uint32_t a[32];
 #pragma unroll
       for (int cl = 0; cl < 32; ++cl) {
@@ -181,16 +187,19 @@ __global__ void __launch_bounds__(kThreads)
         const uint32_t b3 = b1 + (uint32_t)d[6] + (uint32_t)P.ktd[cl + 96];
         red_shared_inc(b3);
       }
+      jb = (jb - P.loop_mask) & P.loop_mask;  // next subset of the loop sites
     }
   }
   __syncthreads();
-  // ---- flush: word (m, e') -> table bin (m, e) ----
+  // ---- flush: word (m, e) -> table bin (m, e) ----
   for (uint32_t bin = threadIdx.x; bin < P.nbins; bin += blockDim.x) {
     const uint32_t m = bin / P.stride, e = bin - m * P.stride;
     uint32_t word;
-    if (P.e_halved) {
-      if ((e ^ P.e_parity) & 1) continue;  // structurally empty
-      word = m * P.row_words + ((e - P.e_parity) >> 1) * P.e_words;
+    if (P.e_mode) {
+      const uint32_t par = e & 1u;
+      if (P.odd_mask == 0 && par != P.e_parity) continue;  // structurally 0
+      word = m * P.row_words + ((e - par) >> 1) * P.e_words +
+             par * P.plane_words;
     } else {
       word = m * P.row_words + e * P.e_words;
     }

@@ -33,34 +33,38 @@ struct CanonParams {
 };
 
 // Parameters of the hoisted kernel.  A "run" is 2^k
-// consecutive indices: bits [k, N) are fixed per thread, bits [u, k) are the
-// thread's loop counter j, and bits [0, u) are the 32 unrolled copies.
+// consecutive indices: bits [k, N) are fixed per thread; inside [0, k) the
+// loop sites (loop_mask) take every subset in the thread's loop and the 7
+// copy sites are 128 register copies.
 struct HoistParams {
   uint64_t run_begin, run_end;   // run indices (index = run << k)
   uint64_t above_k;              // bits [k, N)
-  uint32_t k, l;                 // k = u + l
+  uint64_t odd_mask;             // odd-degree sites (parity planes)
+  uint32_t loop_mask;            // loop sites
+  uint32_t k, l;
   uint32_t n_classes;
   uint32_t stride;               // B + 1
   uint32_t nbins;
-  uint32_t hist_words;
+  uint32_t hist_words;           // words per shared histogram (padded)
   uint32_t n_hist;
   uint32_t has_double;           // any copy site with a doubled partner
   uint32_t lane_shift;           // warp lanes take run bits [s, s+5)
-  uint32_t row_words;            // word stride of m
+  uint32_t e_mode;               // 0 dense, 1 parity planes
+  uint32_t e_parity;             // constant part of the e parity
+  uint32_t row_words, e_words, plane_words;  // layout (words)
   uint32_t row_bytes;            // 4 * row_words
-  uint32_t e_words;              // word stride of e' (e or (e - parity)/2)
-  uint32_t e_bytes;              // bytes per unit of e (4 or 2 per e' word)
-  uint32_t pad2_;
-  uint32_t e_halved, e_parity;
+  uint32_t e_bytes;              // bytes per unit of e
+  int32_t plane_bytes;           // bytes added when the e parity is odd
   uint32_t shift[kMaxClasses];
-  uint32_t mvar[kMaxClasses];    // class mask restricted to bits [u, k)
+  uint32_t mvar[kMaxClasses];    // class bonds with lower site a loop site
+                                 // and upper site not a copy site
   uint64_t mask[kMaxClasses];
   uint64_t jneg[kMaxClasses];
   uint64_t nm1[kCopyBits], jn1[kCopyBits];   // copy-site partner masks
   uint64_t nm2[kCopyBits], jn2[kCopyBits];   // (second copy of a double bond)
-  uint32_t nm1v[kCopyBits], jn1v[kCopyBits]; // restricted to [u, k)
+  uint32_t nm1v[kCopyBits], jn1v[kCopyBits]; // restricted to loop sites
   uint32_t nm2v[kCopyBits], jn2v[kCopyBits];
-  int32_t degree[kCopyBits];                 // d_p
+  int32_t degree[kCopyBits];                 // d_q
   int32_t ktd[kCopies];          // byte offset of copy c minus copy c^topbit(c)
 };
 

@@ -74,12 +74,10 @@ int validate_lattice(const isd_lattice* lat, char* err, size_t errlen) {
 // ---- shared-histogram layout ---------------------------------------------
 // The 32 lanes of a warp reduce into one shared histogram at the same time;
 // lanes on the same word aggregate in hardware, lanes on different words of
-// the same bank serialise.  The kernel addresses word(m, e) = m*S + e' with
-// e' = e (or (e - parity)/2 when e_idx has a fixed parity, which halves the
-// footprint and doubles the banks a row touches).  S and the run bits the
-// lanes differ in are picked here by replaying a sample of warp
-// instructions: minimise the mean over instructions of the largest number
-// of distinct words falling into one bank (= wavefronts).
+// the same bank serialise (K0 probes 7-10).  The layout and the run bits the
+// lanes differ in are picked by replaying a sample of warp instructions and
+// minimising the mean over instructions of the largest number of distinct
+// words falling into one bank (= shared-memory wavefronts).
 
 static uint64_t rng_next(uint64_t* s) {
   uint64_t x = *s;
@@ -89,107 +87,133 @@ static uint64_t rng_next(uint64_t* s) {
   return *s = x;
 }
 
+static uint64_t deposit(uint64_t v, uint64_t mask) {
+  uint64_t out = 0;
+  for (int b = 0; mask; ++b) {
+    const uint64_t low = mask & (~mask + 1);
+    if ((v >> b) & 1) out |= low;
+    mask ^= low;
+  }
+  return out;
+}
+
+namespace {
+struct Bin {
+  int m, e, par;
+};
+}  // namespace
+
 static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
   const int n = (int)lat->n_spins;
   const int k = (int)info->k;
   const int b = (int)lat->n_bonds;
-  int deg[64] = {0};
-  int neg = 0;
-  for (uint32_t c = 0; c < lat->n_classes; ++c) {
-    const isd_bond_class& cl = lat->classes[c];
-    for (int i = 0; i < n; ++i)
-      if ((cl.bond_mask >> i) & 1) {
-        deg[i]++;
-        deg[i + cl.shift]++;
-      }
-    neg += popc64(cl.jneg_mask);
-  }
-  bool even = true;
-  for (int i = 0; i < n; ++i) even = even && (deg[i] % 2 == 0);
-  info->e_halved = even ? 1 : 0;
-  info->e_parity = even ? (uint32_t)(neg & 1) : 0;
-  const int min_words = even ? (b - (int)info->e_parity) / 2 + 1 : b + 1;
-  info->row_words = (uint32_t)min_words;
-  info->e_words = 1;
-  info->hist_words = (uint32_t)((n + 1) * min_words);
+  const int emax_half = b / 2;  // largest (e - par)/2
   info->lane_shift = 0;
   info->est_wavefronts = 0;
+  // candidate layouts (row_words A, e_words B, plane_words P)
+  struct Cand {
+    int a, b, p, span;
+  };
+  static Cand cand[512];
+  int nc = 0;
+  if (info->e_mode == 0) {
+    for (int t = 0; t < 40; ++t) cand[nc++] = {b + 1 + t, 1, 0, n * (b + 1 + t) + b + 1};
+    for (int t = 0; t < 40; ++t)
+      cand[nc++] = {1, n + 1 + t, 0, n + b * (n + 1 + t) + 1};
+  } else {
+    const bool planes = info->odd_mask != 0;
+    for (int t = 0; t < 24; ++t) {
+      const int a = emax_half + 1 + t;
+      const int span0 = n * a + emax_half + 1;
+      for (int q = 0; q < (planes ? 8 : 1); ++q)
+        cand[nc++] = {a, 1, planes ? span0 + 4 * q : 0,
+                      planes ? 2 * span0 + 4 * q : span0};
+    }
+    for (int t = 0; t < 24; ++t) {
+      const int bb = n + 1 + t;
+      const int span0 = n + emax_half * bb + 1;
+      for (int q = 0; q < (planes ? 8 : 1); ++q)
+        cand[nc++] = {1, bb, planes ? span0 + 4 * q : 0,
+                      planes ? 2 * span0 + 4 * q : span0};
+    }
+  }
+  // default: first candidate
+  info->row_words = (uint32_t)cand[0].a;
+  info->e_words = (uint32_t)cand[0].b;
+  info->plane_words = (uint32_t)cand[0].p;
+  info->hist_words = (uint32_t)cand[0].span;
   const int run_bits = n - k;
   if (run_bits < 5) return;
 
-  // sample: many warps, a random subset of copies each (copies of one warp
-  // are strongly correlated, so breadth over warps matters more)
-  // candidate strides: m-major (A = S >= row length, B = 1) and e-major
-  // (A = 1, B = R >= N + 1)
-  constexpr int kWarps = 64, kCopySample = 16, kHalf = 40, kCand = 2 * kHalf;
-  int cand_a[kCand], cand_b[kCand];
-  for (int si = 0; si < kHalf; ++si) {
-    cand_a[si] = min_words + si;
-    cand_b[si] = 1;
-    cand_a[kHalf + si] = 1;
-    cand_b[kHalf + si] = n + 1 + si;
-  }
+  constexpr int kWarps = 48, kCopySample = 16;
   static const int shifts[] = {0, 3, 6, 9, 12, 15};
+  static double cost[512];
   double best = 1e30;
-  int m_s[32], e_s[32];
   for (int ls : shifts) {
     if (run_bits < ls + 5) continue;
-    double cost[kCand] = {0};
+    for (int ci = 0; ci < nc; ++ci) cost[ci] = 0;
     uint64_t seed = 0x9E3779B97F4A7C15ull ^ (uint64_t)(ls + 1);
     const uint64_t hi_count = 1ull << (run_bits - 5);
     for (int w = 0; w < kWarps; ++w) {
       const uint64_t hi = rng_next(&seed) % hi_count;
-      const uint64_t j = (k > kCopyBits) ? rng_next(&seed) % (1ull << (k - kCopyBits)) : 0;
+      const uint64_t jb = deposit(rng_next(&seed), info->loop_mask);
       for (int cs = 0; cs < kCopySample; ++cs) {
-        const int c = (int)(rng_next(&seed) % kCopies);
+        uint64_t cbits = 0;
+        const uint64_t c = rng_next(&seed) % kCopies;
+        for (int t = 0; t < kCopyBits; ++t)
+          if ((c >> t) & 1) cbits |= 1ull << info->copy_site[t];
+        Bin bins[32];
+        int nb = 0;
         for (int lane = 0; lane < 32; ++lane) {
           const uint64_t r = ((hi >> ls) << (ls + 5)) | ((uint64_t)lane << ls) |
                              (hi & ((1ull << ls) - 1));
-          const uint64_t x = (r << k) | (j << kCopyBits) | (uint64_t)c;
+          const uint64_t x = (r << k) | jb | cbits;
           int e = 0;
           for (uint32_t q = 0; q < lat->n_classes; ++q) {
             const isd_bond_class& cl = lat->classes[q];
             e += popc64(((x ^ (x >> cl.shift)) ^ cl.jneg_mask) & cl.bond_mask);
           }
-          m_s[lane] = popc64(x);
-          e_s[lane] = even ? (e - (int)info->e_parity) / 2 : e;
+          Bin bn{popc64(x), e, (e & 1)};
+          bool seen = false;
+          for (int t = 0; t < nb && !seen; ++t)
+            seen = bins[t].m == bn.m && bins[t].e == bn.e;
+          if (!seen) bins[nb++] = bn;
         }
-        for (int si = 0; si < kCand; ++si) {
-          int words[32];
-          int nw = 0;
-          for (int lane = 0; lane < 32; ++lane) {
-            const int wd = m_s[lane] * cand_a[si] + e_s[lane] * cand_b[si];
-            bool seen = false;
-            for (int t = 0; t < nw && !seen; ++t) seen = words[t] == wd;
-            if (!seen) words[nw++] = wd;
-          }
+        for (int ci = 0; ci < nc; ++ci) {
           int bank[32] = {0};
           int mx = 0;
-          for (int t = 0; t < nw; ++t) {
-            const int v = ++bank[words[t] & 31];
+          for (int t = 0; t < nb; ++t) {
+            int wd;
+            if (info->e_mode == 0)
+              wd = bins[t].m * cand[ci].a + bins[t].e * cand[ci].b;
+            else
+              wd = bins[t].m * cand[ci].a +
+                   ((bins[t].e - bins[t].par) >> 1) * cand[ci].b +
+                   bins[t].par * cand[ci].p;
+            const int v = ++bank[wd & 31];
             if (v > mx) mx = v;
           }
-          cost[si] += mx;
+          cost[ci] += mx;
         }
       }
     }
-    for (int si = 0; si < kCand; ++si) {
-      const double cst = cost[si] / (kWarps * kCopySample);
+    for (int ci = 0; ci < nc; ++ci) {
+      const double cst = cost[ci] / (kWarps * kCopySample);
       if (cst < best - 1e-9) {
         best = cst;
-        info->row_words = (uint32_t)cand_a[si];
-        info->e_words = (uint32_t)cand_b[si];
+        info->row_words = (uint32_t)cand[ci].a;
+        info->e_words = (uint32_t)cand[ci].b;
+        info->plane_words = (uint32_t)cand[ci].p;
+        info->hist_words = (uint32_t)cand[ci].span;
         info->lane_shift = (uint32_t)ls;
       }
     }
   }
   info->est_wavefronts = best;
-  info->hist_words = (uint32_t)(n * (int)info->row_words +
-                                (min_words - 1) * (int)info->e_words + 1);
 }
 
-// Hoisted split: u = 7 copy sites, l loop sites, the rest per-thread.  l is
-// chosen so that a full walk still has >= ~2^20 runs to spread over 148 SMs.
+// Hoisted split: 7 copy sites and l loop sites inside the low k bits, the
+// rest per-thread.  l keeps >= ~2^20 runs in a full walk (148 SMs).
 int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint) {
   const int n = (int)lat->n_spins;
   const int u = kCopyBits;
@@ -205,6 +229,69 @@ int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint) {
   return l;
 }
 
+// Copy-site neighbourhoods for a chosen set of 7 copy sites: every bond
+// touching a copy site.  Partner also a copy site -> copy/copy bond folded
+// into KT; else the partner is counted through n_q (upward or downward).
+static void set_copy_sites(const isd_lattice* lat, isd_plan_info* info,
+                           const int* sites, uint32_t e_mode) {
+  const int n = (int)lat->n_spins;
+  const int u = kCopyBits;
+  const int k = (int)info->k;
+  for (int t = 0; t < u; ++t) {
+    info->copy_site[t] = sites[t];
+    info->copy_degree[t] = 0;
+    info->copy_nbr1[t] = info->copy_jneg1[t] = 0;
+    info->copy_nbr2[t] = info->copy_jneg2[t] = 0;
+  }
+  info->e_mode = e_mode;
+  uint64_t copy_mask = 0;
+  int slot[64];
+  for (int i = 0; i < 64; ++i) slot[i] = -1;
+  for (int t = 0; t < u; ++t) {
+    copy_mask |= 1ull << sites[t];
+    slot[sites[t]] = t;
+  }
+  info->loop_mask = ((1ull << k) - 1) & ~copy_mask;
+  struct CC { int p, q, neg; };
+  CC cc[ISD_MAX_CLASSES * kCopyBits];
+  int ncc = 0;
+  for (uint32_t c = 0; c < lat->n_classes; ++c) {
+    const isd_bond_class& cl = lat->classes[c];
+    for (int i = 0; i < n; ++i) {
+      if (!((cl.bond_mask >> i) & 1)) continue;
+      const int j = i + (int)cl.shift;
+      const int ng = (int)((cl.jneg_mask >> i) & 1);
+      const int ti = slot[i], tj = slot[j];
+      if (ti >= 0 && tj >= 0) {
+        cc[ncc++] = CC{ti, tj, ng};
+        continue;
+      }
+      for (int side = 0; side < 2; ++side) {
+        const int t = side ? tj : ti;
+        const int partner = side ? i : j;
+        if (t < 0) continue;
+        const uint64_t bit = 1ull << partner;
+        if (!(info->copy_nbr1[t] & bit)) {
+          info->copy_nbr1[t] |= bit;
+          if (ng) info->copy_jneg1[t] |= bit;
+        } else {
+          // a periodic axis of length 2 doubles the bond (lattice.py:105-107)
+          info->copy_nbr2[t] |= bit;
+          if (ng) info->copy_jneg2[t] |= bit;
+        }
+        info->copy_degree[t] += 1;
+      }
+    }
+  }
+  for (int c = 0; c < kCopies; ++c) {
+    int unsat = 0;
+    for (int i = 0; i < ncc; ++i)
+      unsat += ((c >> cc[i].p) ^ (c >> cc[i].q) ^ cc[i].neg) & 1;
+    info->copy_table[c] = __builtin_popcount((unsigned)c) * (int)info->stride +
+                          unsat;
+  }
+}
+
 int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
                  isd_plan_info* info) {
   std::memset(info, 0, sizeof(*info));
@@ -216,50 +303,66 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   info->l = l;
   info->k = k;
   info->stride = lat->n_bonds + 1;
-  info->run_mask_above_k = (n >= 64 ? ~0ull : ((1ull << n) - 1)) &
-                           ~((1ull << k) - 1);
-  info->var_mask = ((1ull << k) - 1) & ~((1ull << u) - 1);
-
-  // Copy-site neighbourhoods.  A bond (i, i+s) with i < u and i+s >= u is a
-  // copy/non-copy bond counted through n_p; with i+s < u it is a copy/copy
-  // bond folded into KT.  (Bonds with i >= u never touch a copy site: the
-  // upper end is above the lower one.)
-  struct CC { int p, q, neg; };
-  CC cc[ISD_MAX_CLASSES * kCopyBits];
-  int ncc = 0;
-  for (int p = 0; p < u && p < n; ++p) {
-    for (uint32_t c = 0; c < lat->n_classes; ++c) {
-      const isd_bond_class& k2 = lat->classes[c];
-      if (!((k2.bond_mask >> p) & 1)) continue;
-      const int q = p + (int)k2.shift;
-      const int neg = (int)((k2.jneg_mask >> p) & 1);
-      if (q >= u) {
-        const uint64_t bit = 1ull << q;
-        if (!(info->copy_nbr1[p] & bit)) {
-          info->copy_nbr1[p] |= bit;
-          if (neg) info->copy_jneg1[p] |= bit;
-        } else {
-          // a periodic axis of length 2 doubles the bond (lattice.py:105-107)
-          info->copy_nbr2[p] |= bit;
-          if (neg) info->copy_jneg2[p] |= bit;
-        }
-        info->copy_degree[p] += 1;
-      } else {
-        cc[ncc++] = CC{p, q, neg};
-      }
-    }
-  }
-  for (int c = 0; c < kCopies; ++c) {
-    int unsat = 0;
-    for (int i = 0; i < ncc; ++i)
-      unsat += ((c >> cc[i].p) ^ (c >> cc[i].q) ^ cc[i].neg) & 1;
-    info->copy_table[c] = __builtin_popcount((unsigned)c) * (int)info->stride +
-                          unsat;
-  }
   // The hoisted kernel needs all copy and loop sites inside the low word and
   // at least one run.
   if (n < k + 1 || k > 32) return 1;
-  choose_layout(lat, info);
+  info->run_mask_above_k = (n >= 64 ? ~0ull : ((1ull << n) - 1)) &
+                           ~((1ull << k) - 1);
+
+  // site degrees (with multiplicity) and the e parity structure:
+  // e_idx = sum_b (s_i ^ s_j ^ neg_b) = sum_i deg_i s_i + #neg  (mod 2)
+  int deg[64] = {0};
+  int neg = 0;
+  for (uint32_t c = 0; c < lat->n_classes; ++c) {
+    const isd_bond_class& cl = lat->classes[c];
+    for (int i = 0; i < n; ++i)
+      if ((cl.bond_mask >> i) & 1) {
+        deg[i]++;
+        deg[i + cl.shift]++;
+      }
+    neg += popc64(cl.jneg_mask);
+  }
+  uint64_t odd = 0;
+  for (int i = 0; i < n; ++i)
+    if (deg[i] & 1) odd |= 1ull << i;
+  info->odd_mask = odd;
+  info->e_parity = (uint32_t)(neg & 1);
+
+  // copy sites: (a) the even-degree sites of [0, k) when there are 7 of
+  // them (then the e parity is constant over a group's copies: e_mode 1),
+  // (b) the lowest 7 sites (e_mode 1 only if every site has even degree).
+  // Both are laid out and the one with fewer predicted wavefronts wins.
+  int even_sites[kCopyBits];
+  int ne = 0;
+  for (int i = 0; i < k && ne < u; ++i)
+    if (!((odd >> i) & 1)) even_sites[ne++] = i;
+  int low_sites[kCopyBits];
+  for (int t = 0; t < u; ++t) low_sites[t] = t;
+  isd_plan_info best_info;
+  bool have = false;
+  // test / tuning knob: ISD_COPY_VARIANT=even|low forces one variant
+  const char* force = std::getenv("ISD_COPY_VARIANT");
+  for (int variant = 0; variant < 2; ++variant) {
+    if (force && std::strcmp(force, variant ? "low" : "even") != 0) continue;
+    isd_plan_info cand = *info;
+    if (variant == 0) {
+      if (ne < u) continue;
+      set_copy_sites(lat, &cand, even_sites, 1);
+    } else {
+      const bool low_even = (odd & ((1ull << u) - 1)) == 0;
+      if (!force && low_even && ne == u &&
+          std::memcmp(even_sites, low_sites, sizeof low_sites) == 0)
+        continue;  // identical to variant 0
+      set_copy_sites(lat, &cand, low_sites, low_even ? 1 : 0);
+    }
+    choose_layout(lat, &cand);
+    if (!have || cand.est_wavefronts < best_info.est_wavefronts - 1e-9) {
+      best_info = cand;
+      have = true;
+    }
+  }
+  if (!have) return 1;  // forced variant not available for this lattice
+  *info = best_info;
   return 0;
 }
 
@@ -281,44 +384,54 @@ void fill_canon(const isd_lattice* lat, CanonParams* p) {
 void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
                 HoistParams* p) {
   std::memset(p, 0, sizeof(*p));
-  const uint32_t u = info->u, k = info->k;
-  p->k = k;
+  p->k = info->k;
   p->l = info->l;
   p->above_k = info->run_mask_above_k;
+  p->loop_mask = (uint32_t)info->loop_mask;
   p->n_classes = lat->n_classes;
   p->stride = info->stride;
   p->nbins = (lat->n_spins + 1) * p->stride;
-  p->row_words = info->row_words;
-  p->row_bytes = 4 * info->row_words;
-  p->e_words = info->e_words;
-  p->e_halved = info->e_halved;
+  p->e_mode = info->e_mode;
   p->e_parity = info->e_parity;
-  p->e_bytes = (info->e_halved ? 2 : 4) * info->e_words;
+  p->odd_mask = info->e_mode ? info->odd_mask : 0;
+  p->row_words = info->row_words;
+  p->e_words = info->e_words;
+  p->plane_words = info->plane_words;
+  p->row_bytes = 4 * info->row_words;
+  // e_mode 1: word = m*A + ((e - par)/2)*B + par*P
+  //   -> bytes = 4A m + 2B e + par (4P - 2B)
+  p->e_bytes = (info->e_mode ? 2 : 4) * info->e_words;
+  p->plane_bytes = info->e_mode ? 4 * (int)info->plane_words -
+                                      2 * (int)info->e_words
+                                : 0;
   p->lane_shift = info->lane_shift;
   p->hist_words = hist_words_for(info->hist_words);
   p->n_hist = (uint32_t)hist_count_for(p->hist_words);
-  const uint32_t var = (uint32_t)info->var_mask;
+  const uint64_t loop = info->loop_mask;
+  const uint64_t copies = ((1ull << info->k) - 1) & ~loop;
   for (uint32_t c = 0; c < lat->n_classes; ++c) {
-    p->shift[c] = lat->classes[c].shift;
-    p->mask[c] = lat->classes[c].bond_mask;
-    p->jneg[c] = lat->classes[c].jneg_mask;
-    p->mvar[c] = (uint32_t)lat->classes[c].bond_mask & var;
+    const isd_bond_class& cl = lat->classes[c];
+    p->shift[c] = cl.shift;
+    p->mask[c] = cl.bond_mask;
+    p->jneg[c] = cl.jneg_mask;
+    // lower site a loop site, upper site not a copy site
+    p->mvar[c] = (uint32_t)(cl.bond_mask & loop & ~(copies >> cl.shift));
   }
   p->has_double = 0;
-  for (uint32_t q = 0; q < u; ++q) {
+  for (int q = 0; q < kCopyBits; ++q) {
     p->nm1[q] = info->copy_nbr1[q];
     p->jn1[q] = info->copy_jneg1[q];
     p->nm2[q] = info->copy_nbr2[q];
     p->jn2[q] = info->copy_jneg2[q];
-    p->nm1v[q] = (uint32_t)info->copy_nbr1[q] & var;
-    p->jn1v[q] = (uint32_t)info->copy_jneg1[q] & var;
-    p->nm2v[q] = (uint32_t)info->copy_nbr2[q] & var;
-    p->jn2v[q] = (uint32_t)info->copy_jneg2[q] & var;
+    p->nm1v[q] = (uint32_t)(info->copy_nbr1[q] & loop);
+    p->jn1v[q] = (uint32_t)(info->copy_jneg1[q] & loop);
+    p->nm2v[q] = (uint32_t)(info->copy_nbr2[q] & loop);
+    p->jn2v[q] = (uint32_t)(info->copy_jneg2[q] & loop);
     p->degree[q] = info->copy_degree[q];
     if (info->copy_nbr2[q]) p->has_double = 1;
   }
-  // copy_table[c] = popc(c)(B+1) + unsat_cc(c); split it back into the
-  // m and e parts and express the subset-sum steps in bytes
+  // copy_table[c] = popc(c)(B+1) + unsat_cc(c); split into the m and e
+  // parts and express the subset-sum steps in bytes
   const int eb = (int)p->e_bytes, rb = (int)p->row_bytes;
   auto unsat = [&](int c) {
     return info->copy_table[c] -

@@ -173,6 +173,23 @@ def test_baseline_lattice_full_walk(name):
         assert np.array_equal(e_marg, e_marg[::-1])
 
 
+@pytest.mark.parametrize("name", ["c1", "c3", "c5"])
+@pytest.mark.parametrize("variant", ["even", "low"])
+def test_copy_site_variants(name, variant, monkeypatch):
+    # both copy-site choices (even-degree sites with parity planes, lowest
+    # sites) must give the same table; c3/c1 are the free-boundary lattices
+    # where the parity planes carry odd-degree sites
+    monkeypatch.setenv("ISD_COPY_VARIANT", variant)
+    spec = workloads()[name].spec
+    lat = __import__("paper_1110_2561_b200.enumeration",
+                     fromlist=["native_lattice"]).native_lattice(spec)
+    usable, info = _native.plan(lat, spec.num_configs)
+    if not usable:
+        pytest.skip("variant not available")
+    got = full(spec, _native.ALGO_HOISTED)
+    assert np.array_equal(got, _golden_c(name))
+
+
 def test_6x6_periodic_matches_reference_walk():
     path = os.path.join(os.path.dirname(__file__), "golden",
                         "dos_6x6x1_J1.csv")

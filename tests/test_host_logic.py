@@ -180,7 +180,14 @@ def _u(x):
 
 
 def replay_hoisted(spec, loop_bits):
-    """numpy replay of k1_hoisted's arithmetic over every index."""
+    """numpy replay of k1_hoisted's arithmetic and address layout.
+
+    Every index is decomposed exactly as the kernel does (run / loop /
+    copy sites of the plan), its histogram word is formed from the per-run,
+    per-loop and per-copy terms, and the words are read back through the
+    kernel's flush rule.  Also asserts the layout is injective on the bins
+    that occur and that the e parity formula holds.
+    """
     os.environ["ISD_LOOP_BITS"] = str(loop_bits)
     try:
         lat = native_lattice(spec)
@@ -188,38 +195,66 @@ def replay_hoisted(spec, loop_bits):
     finally:
         del os.environ["ISD_LOOP_BITS"]
     assert usable
-    u, l, k = info.u, info.l, info.k
+    u, k = info.u, info.k
     stride = info.stride
     classes = spec.bond_classes()
     n = spec.num_spins
-    above_k = _u(info.run_mask_above_k)
-    var = int(info.var_mask)
+    above_k = int(info.run_mask_above_k)
+    loop = int(info.loop_mask)
+    sites = list(info.copy_site)
+    copies = sum(1 << q for q in sites)
+    assert copies | loop == (1 << k) - 1 and copies & loop == 0
     x = np.arange(1 << n, dtype=np.uint64)
-    xt = x & above_k
-    jb = (x & _u(var)).astype(np.uint64)
-    c = (x & _u((1 << u) - 1)).astype(np.int64)
+    xt = x & _u(above_k)
+    jb = x & _u(loop)
+    c = np.zeros(x.shape, dtype=np.int64)
+    for t, q in enumerate(sites):
+        c |= ((x >> _u(q)) & _u(1)).astype(np.int64) << t
     pc = lambda a: np.bitwise_count(a).astype(np.int64)  # noqa: E731
-    base = pc(xt) * stride
-    for s, m, jn in classes:
+    m = pc(xt) + pc(jb) + pc(c.astype(np.uint64))
+    e = np.zeros(x.shape, dtype=np.int64)
+    for s, msk, jn in classes:
         sh = xt >> _u(s)
-        base += pc(((xt ^ sh) ^ _u(jn)) & _u(m) & above_k)
+        e += pc(((xt ^ sh) ^ _u(jn)) & _u(msk) & _u(above_k))
         cst = (sh & _u(0xFFFFFFFF)) ^ _u(jn & 0xFFFFFFFF)
         jshift = (jb >> _u(s)) if s < 32 else np.zeros_like(jb)
-        base += pc((jb ^ jshift ^ cst) & _u(m & var))
-    base += pc(jb) * stride
-    bins = base.copy()
-    for q in range(u):
-        nq = pc((xt ^ _u(info.copy_jneg1[q])) & _u(info.copy_nbr1[q]) & above_k)
-        nq += pc((xt ^ _u(info.copy_jneg2[q])) & _u(info.copy_nbr2[q]) & above_k)
-        nq += pc((jb ^ _u(info.copy_jneg1[q] & var)) & _u(info.copy_nbr1[q] & var))
-        nq += pc((jb ^ _u(info.copy_jneg2[q] & var)) & _u(info.copy_nbr2[q] & var))
-        bins += nq
-        d = info.copy_degree[q] - 2 * nq
-        bins += np.where((c >> q) & 1, d, 0)
+        mvar = msk & loop & ~(copies >> s)
+        e += pc((jb ^ jshift ^ cst) & _u(mvar))
+    for t in range(u):
+        nq = pc((xt ^ _u(info.copy_jneg1[t])) & _u(info.copy_nbr1[t]) & _u(above_k))
+        nq += pc((xt ^ _u(info.copy_jneg2[t])) & _u(info.copy_nbr2[t]) & _u(above_k))
+        nq += pc((jb ^ _u(info.copy_jneg1[t] & loop)) & _u(info.copy_nbr1[t] & loop))
+        nq += pc((jb ^ _u(info.copy_jneg2[t] & loop)) & _u(info.copy_nbr2[t] & loop))
+        e += nq
+        e += np.where((c >> t) & 1, info.copy_degree[t] - 2 * nq, 0)
     kt = np.array(list(info.copy_table), dtype=np.int64)
-    bins += kt[c]
-    table = np.bincount(bins, minlength=(n + 1) * stride)
-    return table.reshape(n + 1, stride)
+    e += kt[c] - stride * np.bitwise_count(c.astype(np.uint64)).astype(np.int64)
+    A, B, P = info.row_words, info.e_words, info.plane_words
+    if info.e_mode:
+        odd = int(info.odd_mask)
+        par = (pc(x & _u(odd & ~copies)) + info.e_parity) & 1
+        assert np.all((e - par) % 2 == 0), "e parity formula"
+        word = m * A + ((e - par) // 2) * B + par * P
+    else:
+        word = m * A + e * B
+    assert word.max() < info.hist_words
+    # injective on occurring bins
+    pairs = np.unique(np.stack([word, m * stride + e]), axis=1)
+    assert len(np.unique(pairs[0])) == pairs.shape[1], "layout collision"
+    hist = np.bincount(word, minlength=int(info.hist_words))
+    table = np.zeros((n + 1, stride), dtype=np.int64)
+    for mm in range(n + 1):
+        for ee in range(stride):
+            if info.e_mode:
+                p2 = ee & 1
+                if odd == 0 and p2 != info.e_parity:
+                    continue
+                w = mm * A + ((ee - p2) // 2) * B + p2 * P
+            else:
+                w = mm * A + ee * B
+            if w < len(hist):
+                table[mm, ee] = hist[w]
+    return table
 
 
 REPLAY = [
@@ -227,6 +262,8 @@ REPLAY = [
     dict(rows=2, cols=2, depth=3), dict(rows=4, cols=4, boundary="free"),
     dict(rows=2, cols=4, depth=2), dict(rows=3, cols=3, depth=2),
     dict(rows=5, cols=3), dict(rows=2, cols=8),
+    dict(rows=4, cols=3, boundary="free"), dict(rows=3, cols=5, boundary="free"),
+    dict(rows=2, cols=3, depth=2, boundary="free"),
 ]
 
 
@@ -241,6 +278,17 @@ def test_hoisted_plan_replay_matches_oracle(kw, seed, loop_bits):
     want = port.enumerate_range(lat, 0, 1 << lat.n)
     got = replay_hoisted(spec, loop_bits)
     assert np.array_equal(got, want)
+
+
+def test_plan_uses_parity_planes_for_free_lattices():
+    for name in ("c3", "c5", "c4"):
+        spec = workloads()[name].spec
+        usable, info = _native.plan(native_lattice(spec), spec.num_configs)
+        assert usable and info.e_mode == 1
+        sites = list(info.copy_site)
+        assert all(not (int(info.odd_mask) >> q) & 1 for q in sites)
+    _, info = _native.plan(native_lattice(workloads()["c3"].spec), 1 << 36)
+    assert info.odd_mask != 0 and info.plane_words > 0
 
 
 def test_plan_refuses_tiny_lattices():
