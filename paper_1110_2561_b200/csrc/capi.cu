@@ -109,24 +109,104 @@ static int current_sm_count(int* sms) {
 
 // Plans are compiled once per (lattice, loop width): the layout search
 // replays a sample of warp instructions and costs tens of milliseconds.
+// The model ranks every layout; before the first large walk the best few
+// are timed on the GPU on a 2^32-configuration slice and the fastest is
+// kept (autotune, once per process and lattice; ISD_AUTOTUNE=0 disables).
+struct PlanEntry {
+  int rc = 0;
+  isd_plan_info info;
+  std::vector<isd_plan_info> ranked;
+  bool tuned = false;
+};
 static std::mutex g_plan_mu;
-static std::map<std::string, std::pair<int, isd_plan_info>> g_plans;
+static std::map<std::string, PlanEntry> g_plans;
 
-static int cached_plan(const isd_lattice* lat, uint64_t hint,
-                       isd_plan_info* info) {
+static std::string plan_key(const isd_lattice* lat, uint64_t hint) {
   const int l = plan_loop_bits(lat, hint);
   std::string key(reinterpret_cast<const char*>(lat), sizeof(*lat));
   key.push_back((char)l);
   if (const char* v = std::getenv("ISD_COPY_VARIANT")) key += v;
+  return key;
+}
+
+static int cached_plan(const isd_lattice* lat, uint64_t hint,
+                       isd_plan_info* info) {
+  const std::string key = plan_key(lat, hint);
   std::lock_guard<std::mutex> lock(g_plan_mu);
   auto it = g_plans.find(key);
   if (it == g_plans.end()) {
-    isd_plan_info fresh;
-    const int rc = compile_plan(lat, hint, &fresh);
-    it = g_plans.emplace(key, std::make_pair(rc, fresh)).first;
+    PlanEntry fresh;
+    fresh.rc = compile_plan(lat, hint, &fresh.info, &fresh.ranked);
+    it = g_plans.emplace(key, std::move(fresh)).first;
   }
-  *info = it->second.second;
-  return it->second.first;
+  *info = it->second.info;
+  return it->second.rc;
+}
+
+static constexpr int kTuneCandidates = 6;
+static constexpr uint64_t kTuneConfigs = 1ull << 32;
+
+// Time the model's best layouts on `st` and keep the fastest.  Synchronous.
+static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
+                     int sms, cudaStream_t st, isd_plan_info* info) {
+  if (env_long("ISD_AUTOTUNE", 1) == 0) return;
+  const std::string key = plan_key(lat, hint);
+  std::vector<isd_plan_info> cands;
+  {
+    std::lock_guard<std::mutex> lock(g_plan_mu);
+    PlanEntry& pe = g_plans[key];
+    if (pe.tuned || pe.rc) {
+      *info = pe.info;
+      return;
+    }
+    pe.tuned = true;
+    for (size_t i = 0; i < pe.ranked.size() && (int)cands.size() < kTuneCandidates;
+         ++i)
+      cands.push_back(pe.ranked[i]);
+  }
+  if (cands.size() < 2) return;
+  const size_t bytes =
+      (size_t)(lat->n_spins + 1) * (lat->n_bonds + 1) * sizeof(uint64_t);
+  unsigned long long* scratch = nullptr;
+  if (cudaMalloc(&scratch, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const uint64_t runs = kTuneConfigs >> cands[0].k;
+  float best_ms = 1e30f;
+  size_t best = 0;
+  for (size_t i = 0; i < cands.size(); ++i) {
+    HoistParams hp;
+    fill_hoist(lat, &cands[i], &hp);
+    hp.run_begin = run0;
+    hp.run_end = run0 + runs;
+    hp.lane_shift = cands[i].lane_shift;
+    if ((runs & ((1ull << (hp.lane_shift + 5)) - 1)) != 0) hp.lane_shift = 0;
+    float ms = 0.f;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0, st);
+      launch_hoisted(hp, scratch, sms, st);
+      cudaEventRecord(e1, st);
+    }
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    bump_launches(2);
+    if (ms < best_ms) {
+      best_ms = ms;
+      best = i;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(scratch);
+  cudaGetLastError();
+  std::lock_guard<std::mutex> lock(g_plan_mu);
+  PlanEntry& pe = g_plans[key];
+  pe.info = cands[best];
+  *info = pe.info;
 }
 
 // At most 2^38 configurations per launch: with >= 148 CTAs no CTA counts
@@ -236,6 +316,8 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     rc = enqueue_canonical(lat, start, r0 << k, out, sms, st, true, &nl);
     if (rc) return rc;
   }
+  if (end - start >= 2 * kTuneConfigs && r1 - r0 >= (kTuneConfigs >> k))
+    autotune(lat, end - start, r0, sms, st, &info);
   HoistParams hp;
   fill_hoist(lat, &info, &hp);
   const uint64_t runs_per_launch = kMaxPerLaunch >> k;

@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <cstddef>
+#include <vector>
 
 #include "isingdos_b200.h"
 
@@ -72,8 +73,11 @@ struct HoistParams {
 int validate_lattice(const isd_lattice* lat, char* err, size_t errlen);
 // Fill `info` for the hoisted decomposition.  Returns 0 if the lattice can
 // use the hoisted kernel, >0 if it is too small (canonical only).
+// `ranked` (optional) receives every evaluated layout, best model estimate
+// first; the C ABI times the head of that list on the GPU (capi.cu).
 int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
-                 isd_plan_info* info);
+                 isd_plan_info* info,
+                 std::vector<isd_plan_info>* ranked = nullptr);
 int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint);
 void fill_canon(const isd_lattice* lat, CanonParams* p);
 void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,

@@ -6,7 +6,9 @@
 // number of unsatisfied bonds (enumeration.py:95-121, 184-204, 232-233).
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "isd_internal.h"
 
@@ -103,7 +105,8 @@ struct Bin {
 };
 }  // namespace
 
-static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
+static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
+                          std::vector<isd_plan_info>* ranked) {
   const int n = (int)lat->n_spins;
   const int k = (int)info->k;
   const int b = (int)lat->n_bonds;
@@ -143,9 +146,12 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
   info->plane_words = (uint32_t)cand[0].p;
   info->hist_words = (uint32_t)cand[0].span;
   const int run_bits = n - k;
-  if (run_bits < 5) return;
+  if (run_bits < 5) {
+    if (ranked) ranked->push_back(*info);
+    return;
+  }
 
-  constexpr int kWarps = 48, kCopySample = 16;
+  constexpr int kWarps = 160, kCopySample = 8;
   static const int shifts[] = {0, 3, 6, 9, 12, 15};
   static double cost[512];
   double best = 1e30;
@@ -199,17 +205,20 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info) {
     }
     for (int ci = 0; ci < nc; ++ci) {
       const double cst = cost[ci] / (kWarps * kCopySample);
+      isd_plan_info alt = *info;
+      alt.row_words = (uint32_t)cand[ci].a;
+      alt.e_words = (uint32_t)cand[ci].b;
+      alt.plane_words = (uint32_t)cand[ci].p;
+      alt.hist_words = (uint32_t)cand[ci].span;
+      alt.lane_shift = (uint32_t)ls;
+      alt.est_wavefronts = cst;
+      if (ranked) ranked->push_back(alt);
       if (cst < best - 1e-9) {
         best = cst;
-        info->row_words = (uint32_t)cand[ci].a;
-        info->e_words = (uint32_t)cand[ci].b;
-        info->plane_words = (uint32_t)cand[ci].p;
-        info->hist_words = (uint32_t)cand[ci].span;
-        info->lane_shift = (uint32_t)ls;
+        *info = alt;
       }
     }
   }
-  info->est_wavefronts = best;
 }
 
 // Hoisted split: 7 copy sites and l loop sites inside the low k bits, the
@@ -293,7 +302,7 @@ static void set_copy_sites(const isd_lattice* lat, isd_plan_info* info,
 }
 
 int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
-                 isd_plan_info* info) {
+                 isd_plan_info* info, std::vector<isd_plan_info>* ranked) {
   std::memset(info, 0, sizeof(*info));
   const int n = (int)lat->n_spins;
   const int u = kCopyBits;
@@ -340,6 +349,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   for (int t = 0; t < u; ++t) low_sites[t] = t;
   isd_plan_info best_info;
   bool have = false;
+  std::vector<isd_plan_info> all;
   // test / tuning knob: ISD_COPY_VARIANT=even|low forces one variant
   const char* force = std::getenv("ISD_COPY_VARIANT");
   for (int variant = 0; variant < 2; ++variant) {
@@ -355,7 +365,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
         continue;  // identical to variant 0
       set_copy_sites(lat, &cand, low_sites, low_even ? 1 : 0);
     }
-    choose_layout(lat, &cand);
+    choose_layout(lat, &cand, &all);
     if (!have || cand.est_wavefronts < best_info.est_wavefronts - 1e-9) {
       best_info = cand;
       have = true;
@@ -363,6 +373,13 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   }
   if (!have) return 1;  // forced variant not available for this lattice
   *info = best_info;
+  if (ranked) {
+    std::stable_sort(all.begin(), all.end(),
+                     [](const isd_plan_info& a, const isd_plan_info& b) {
+                       return a.est_wavefronts < b.est_wavefronts;
+                     });
+    ranked->assign(all.begin(), all.end());
+  }
   return 0;
 }
 

@@ -280,15 +280,20 @@ def test_hoisted_plan_replay_matches_oracle(kw, seed, loop_bits):
     assert np.array_equal(got, want)
 
 
-def test_plan_uses_parity_planes_for_free_lattices():
-    for name in ("c3", "c5", "c4"):
+def test_plan_copy_site_variants(monkeypatch):
+    for name in ("c5", "c4"):  # periodic: every site has even degree
         spec = workloads()[name].spec
         usable, info = _native.plan(native_lattice(spec), spec.num_configs)
-        assert usable and info.e_mode == 1
-        sites = list(info.copy_site)
-        assert all(not (int(info.odd_mask) >> q) & 1 for q in sites)
-    _, info = _native.plan(native_lattice(workloads()["c3"].spec), 1 << 36)
+        assert usable and info.e_mode == 1 and info.odd_mask == 0
+    monkeypatch.setenv("ISD_COPY_VARIANT", "even")
+    spec = workloads()["c3"].spec
+    usable, info = _native.plan(native_lattice(spec), spec.num_configs)
+    assert usable and info.e_mode == 1
     assert info.odd_mask != 0 and info.plane_words > 0
+    assert all(not (int(info.odd_mask) >> q) & 1 for q in info.copy_site)
+    monkeypatch.setenv("ISD_COPY_VARIANT", "low")
+    usable, info = _native.plan(native_lattice(spec), spec.num_configs)
+    assert usable and info.e_mode == 0 and list(info.copy_site) == list(range(7))
 
 
 def test_plan_refuses_tiny_lattices():
