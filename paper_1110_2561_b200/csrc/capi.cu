@@ -110,7 +110,7 @@ static int current_sm_count(int* sms) {
 // Plans are compiled once per (lattice, loop width): the layout search
 // replays a sample of warp instructions and costs tens of milliseconds.
 // The model ranks every layout; before the first large walk the best few
-// are timed on the GPU on a 2^30-configuration slice and the fastest is
+// are timed on the GPU on a 2^33-configuration slice (>= 4 runs per thread) and the fastest is
 // kept (autotune, once per process and lattice; ISD_AUTOTUNE=0 disables).
 struct PlanEntry {
   int rc = 0;
@@ -143,8 +143,8 @@ static int cached_plan(const isd_lattice* lat, uint64_t hint,
   return it->second.rc;
 }
 
-static constexpr int kTuneCandidates = 48;
-static constexpr uint64_t kTuneConfigs = 1ull << 30;
+static constexpr int kTuneCandidates = 24;
+static constexpr uint64_t kTuneConfigs = 1ull << 33;
 
 // Time the model's best layouts on `st` and keep the fastest.  Synchronous.
 static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
