@@ -148,7 +148,8 @@ static constexpr uint64_t kTuneConfigs = 1ull << 33;
 
 // Time the model's best layouts on `st` and keep the fastest.  Synchronous.
 static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
-                     int sms, cudaStream_t st, isd_plan_info* info) {
+                     uint64_t run1, int sms, cudaStream_t st,
+                     isd_plan_info* info) {
   if (env_long("ISD_AUTOTUNE", 1) == 0) return;
   const std::string key = plan_key(lat, hint);
   std::vector<isd_plan_info> cands;
@@ -175,16 +176,21 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  // a strided sample of the body [run0, run1): blocks of 2^(ls+5)
+  // consecutive runs (the lanes' neighbourhood, as in the real walk) spread
+  // evenly over the whole range, so every region of the index space votes
   const uint64_t runs = kTuneConfigs >> cands[0].k;
   float best_ms = 1e30f;
   size_t best = 0;
   for (size_t i = 0; i < cands.size(); ++i) {
     HoistParams hp;
     fill_hoist(lat, &cands[i], &hp);
+    const uint64_t blk = 32ull << hp.lane_shift;
+    if (runs < blk || (run1 - run0) < runs) continue;
+    const uint64_t nblk = runs / blk;
+    hp.block_stride = ((run1 - run0) / nblk) & ~(blk - 1);
     hp.run_begin = run0;
-    hp.run_end = run0 + runs;
-    hp.lane_shift = cands[i].lane_shift;
-    if ((runs & ((1ull << (hp.lane_shift + 5)) - 1)) != 0) hp.lane_shift = 0;
+    hp.run_end = run0 + nblk * blk;
     float ms = 0.f;
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0, st);
@@ -316,8 +322,8 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     rc = enqueue_canonical(lat, start, r0 << k, out, sms, st, true, &nl);
     if (rc) return rc;
   }
-  if (end - start >= 2 * kTuneConfigs && r1 - r0 >= (kTuneConfigs >> k))
-    autotune(lat, end - start, r0, sms, st, &info);
+  if (end - start >= 4 * kTuneConfigs)
+    autotune(lat, end - start, r0, r1, sms, st, &info);
   HoistParams hp;
   fill_hoist(lat, &info, &hp);
   const uint64_t runs_per_launch = kMaxPerLaunch >> k;
@@ -332,6 +338,7 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
       hp.lane_shift = 0;
       if (ls > 0 && ls < 40 && ((re - r) & ((1ull << (ls + 5)) - 1)) == 0)
         hp.lane_shift = (uint32_t)ls;
+      hp.block_stride = 32ull << hp.lane_shift;
     }
     int x = launch_hoisted(hp, out, sms, st);
     if (x < 0) return cuda_fail((cudaError_t)(-x), "k1_hoisted launch");

@@ -118,9 +118,10 @@ __global__ void __launch_bounds__(kThreads)
     // lane bits of t go to run bits [ls, ls+5): which five sites the 32
     // lanes of a warp differ in (shared-memory bank spread)
     const uint64_t hi = t >> 5;
-    const uint64_t r =
-        P.run_begin + (((hi >> ls) << (ls + 5)) | ((t & 31) << ls) |
-                       (hi & ((1ull << ls) - 1)));
+    const uint64_t perm =
+        ((hi >> ls) << (ls + 5)) | ((t & 31) << ls) | (hi & ((1ull << ls) - 1));
+    const uint64_t r = P.run_begin + (perm & ((32ull << ls) - 1)) +
+                       (perm >> (ls + 5)) * P.block_stride;
     // ---- per-run constants (bits [k, N) fixed) ----
     const uint64_t xt = r << P.k;
     const int m_run = __popcll(xt);
