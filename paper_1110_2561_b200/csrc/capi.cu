@@ -186,8 +186,9 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     HoistParams hp;
     fill_hoist(lat, &cands[i], &hp);
     const uint64_t blk = 32ull << hp.lane_shift;
-    if (runs < blk || (run1 - run0) < runs) continue;
-    const uint64_t nblk = runs / blk;
+    const uint64_t want = runs > blk ? runs : blk;
+    if (run1 - run0 < want) continue;
+    const uint64_t nblk = want / blk;
     hp.block_stride = ((run1 - run0) / nblk) & ~(blk - 1);
     hp.run_begin = run0;
     hp.run_end = run0 + nblk * blk;
@@ -200,6 +201,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     bump_launches(2);
+    ms /= (float)(nblk * blk);  // per run: samples may differ in size
     if (ms < best_ms) {
       best_ms = ms;
       best = i;
@@ -324,6 +326,17 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
   }
   if (end - start >= 4 * kTuneConfigs)
     autotune(lat, end - start, r0, r1, sms, st, &info);
+  // experiment knob: ISD_LAYOUT="A,B,P,ls" forces the histogram layout
+  if (const char* lay = std::getenv("ISD_LAYOUT")) {
+    unsigned a = 0, b = 0, pw = 0, ls = 0;
+    if (std::sscanf(lay, "%u,%u,%u,%u", &a, &b, &pw, &ls) == 4 && a && b) {
+      info.row_words = a;
+      info.e_words = b;
+      info.plane_words = pw;
+      info.lane_shift = ls;
+      info.hist_words = lat->n_spins * a + lat->n_bonds * b + pw + 1;
+    }
+  }
   HoistParams hp;
   fill_hoist(lat, &info, &hp);
   const uint64_t runs_per_launch = kMaxPerLaunch >> k;
