@@ -143,7 +143,7 @@ static int cached_plan(const isd_lattice* lat, uint64_t hint,
   return it->second.rc;
 }
 
-static constexpr int kTuneCandidates = 24;
+static constexpr int kTuneCandidates = 40;
 static constexpr uint64_t kTuneConfigs = 1ull << 33;
 
 // Time the model's best layouts on `st` and keep the fastest.  Synchronous.
