@@ -11,6 +11,21 @@ space by its top bits and combine the per-GPU tables with one NCCL reduce
 """
 
 from ._native import NativeError, current_device, set_device
+from .bench import (
+    BenchRecord,
+    ResultMismatchError,
+    emit_scaling_report,
+    parse_scaling_report,
+    run_bench,
+)
+from .dosio import (
+    DosFileError,
+    format_dos_csv,
+    format_dos_json,
+    parse_dos,
+    read_dos,
+    write_dos,
+)
 from .enumeration import (
     DEFAULT_BATCH,
     DoSHistogram,
@@ -55,6 +70,9 @@ from .thermo import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "BenchRecord", "DosFileError", "ResultMismatchError",
+    "emit_scaling_report", "format_dos_csv", "format_dos_json", "parse_dos",
+    "parse_scaling_report", "read_dos", "run_bench", "write_dos",
     "Configuration", "DEFAULT_BATCH", "DoSHistogram", "KernelTables",
     "LatticeSpec", "MAX_ROWS", "MAX_SPINS", "NativeError", "Shard",
     "TABLE_ROWS_CAP", "ThermoPoint", "VerificationReport",
