@@ -35,6 +35,20 @@ __device__ __forceinline__ void red_shared_inc(uint32_t addr) {
   asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
 }
 
+// Debug builds (-DISD_DEBUG_BOUNDS, libisingdos_b200_dbg.so) trap on any
+// histogram address outside the warp's own histogram: the bounds check that
+// stands in for compute-sanitizer, which is closed on the GPU pool.
+#ifdef ISD_DEBUG_BOUNDS
+#define ISD_CHECK_ADDR(a, lo, bytes)                                  \
+  do {                                                                \
+    if ((uint32_t)((a) - (lo)) >= (bytes) || ((a) & 3u)) __trap();    \
+  } while (0)
+#else
+#define ISD_CHECK_ADDR(a, lo, bytes) \
+  do {                               \
+  } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -89,6 +103,7 @@ __global__ void __launch_bounds__(kThreads)
         e += __popc(((y ^ (y >> P.shift[c])) ^ (uint32_t)P.jneg[c]) &
                     (uint32_t)P.mask[c]);
     }
+    ISD_CHECK_ADDR(hbase + 4u * (m * P.stride + e), hbase, 4u * P.nbins);
     red_shared_inc(hbase + 4u * (m * P.stride + e));
   }
   __syncthreads();
@@ -180,12 +195,16 @@ __global__ void __launch_bounds__(kThreads)
           const int top = 31 - __clz(cl);
           a[cl] = a[cl ^ (1 << top)] + (uint32_t)d[top] + (uint32_t)P.ktd[cl];
         }
+        ISD_CHECK_ADDR(a[cl], hbase, 4u * P.hist_words);
         red_shared_inc(a[cl]);
         const uint32_t b1 = a[cl] + (uint32_t)d[5] + (uint32_t)P.ktd[cl + 32];
+        ISD_CHECK_ADDR(b1, hbase, 4u * P.hist_words);
         red_shared_inc(b1);
         const uint32_t b2 = a[cl] + (uint32_t)d[6] + (uint32_t)P.ktd[cl + 64];
+        ISD_CHECK_ADDR(b2, hbase, 4u * P.hist_words);
         red_shared_inc(b2);
         const uint32_t b3 = b1 + (uint32_t)d[6] + (uint32_t)P.ktd[cl + 96];
+        ISD_CHECK_ADDR(b3, hbase, 4u * P.hist_words);
         red_shared_inc(b3);
       }
       jb = (jb - P.loop_mask) & P.loop_mask;  // next subset of the loop sites

@@ -321,3 +321,31 @@ def test_launch_counter_moves():
     before = _native.launch_count()
     full(isd.LatticeSpec(5, 5))
     assert _native.launch_count() > before
+
+
+def test_bounds_checked_build_runs_clean():
+    # the -DISD_DEBUG_BOUNDS library traps on any shared-histogram address
+    # outside the warp's histogram (compute-sanitizer is closed on the pool)
+    import subprocess
+    import sys
+    from paper_1110_2561_b200._build import LIB_DEBUG
+    if not os.path.exists(LIB_DEBUG):
+        pytest.skip("debug library not built")
+    env = dict(os.environ, ISD_LIBRARY=LIB_DEBUG)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import runpy; runpy.run_path(%r)\n"
+        "from paper_1110_2561_b200.workloads import workloads\n"
+        "from paper_1110_2561_b200.enumeration import enumerate_range_timed\n"
+        "import paper_1110_2561_b200 as isd\n"
+        "for n in ('c3', 'c4', 'c5'):\n"
+        "    s = workloads()[n].spec\n"
+        "    t, _ = enumerate_range_timed(s, 0, 1 << 33)\n"
+        "    assert int(t.sum()) == 1 << 33\n"
+        "print('bounds ok')\n"
+    ) % (root, os.path.join(root, "tools", "sanitize_case.py"))
+    r = subprocess.run([sys.executable, "-c", code], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "bounds ok" in r.stdout
