@@ -106,7 +106,7 @@ def run_reference(args, wl):
     lat = port_lattice(wl)
     cores = port.cores()
     # each step: all host cores on a bounded slice, ~ a few seconds
-    per_proc, _ = cpu_sample_size(lat, 1, 4.0)
+    per_proc, _ = cpu_sample_size(lat, 1, 2.0)
     for _ in range(args.warmup):
         port.sample_rate(lat, max(per_proc // 8, 1 << 16), cores)
     rates, walls = [], []
