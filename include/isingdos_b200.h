@@ -165,6 +165,11 @@ typedef struct isd_plan_info {
 int isd_plan(const isd_lattice* lat, uint64_t n_configs_hint,
              isd_plan_info* out);
 
+/* Generate and NVRTC-compile the lattice's specialised k1 kernel without
+ * loading it (no GPU needed); *cubin_bytes = its size.  For tests. */
+int isd_jit_check(const isd_lattice* lat, uint64_t n_configs_hint,
+                  uint64_t* cubin_bytes);
+
 /* Validate a lattice descriptor without touching a GPU. */
 int isd_validate(const isd_lattice* lat);
 
@@ -181,6 +186,10 @@ int isd_calibrate(int device, int which, double* lanes_per_clk_sm,
 int isd_device_count(void);
 int isd_sm_count(int device);
 const char* isd_last_error(void);
+/* Kernel path of the last enumeration on this thread: "k1_hoisted_jit"
+ * (per-lattice NVRTC specialisation, walks >= 2^35), "k1_hoisted_aot",
+ * "k1_canonical" (or an AOT note saying why the JIT was unavailable). */
+const char* isd_kernel_info(void);
 const char* isd_version(void);
 int isd_abi_version(void);
 /* Kernels launched by this process since load (all entry points). */

@@ -18,8 +18,9 @@ LIB = os.path.join(PKG, "libisingdos_b200.so")
 # ISD_LIBRARY=<path> — the stand-in for compute-sanitizer (closed on the pool)
 LIB_DEBUG = os.path.join(PKG, "libisingdos_b200_dbg.so")
 
-SOURCES = ["plan.cpp", "enumerate.cu", "thermo.cu", "calibrate.cu", "capi.cu"]
-HEADERS = ["isd_internal.h"]
+SOURCES = ["plan.cpp", "enumerate.cu", "thermo.cu", "calibrate.cu", "capi.cu",
+           "jit.cpp"]
+HEADERS = ["isd_internal.h", "k1_body.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -49,13 +50,26 @@ def up_to_date(lib: str = LIB) -> bool:
     return all(os.path.getmtime(f) <= t for f in _inputs())
 
 
+def _embed_body() -> None:
+    """csrc/k1_body_str.inc: k1_body.cuh as a C++ raw string (for NVRTC)."""
+    body = open(os.path.join(CSRC, "k1_body.cuh")).read()
+    assert ")ISDBODY\"" not in body
+    text = 'R"ISDBODY(' + body + ')ISDBODY"\n'
+    path = os.path.join(CSRC, "k1_body_str.inc")
+    if not os.path.exists(path) or open(path).read() != text:
+        with open(path, "w") as f:
+            f.write(text)
+
+
 def build(force: bool = False, verbose: bool = False,
           debug: bool = False) -> str:
     lib = LIB_DEBUG if debug else LIB
     if not force and up_to_date(lib):
         return lib
+    _embed_body()
     cmd = [nvcc_path(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"),
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", lib + ".tmp"]
+           *[os.path.join(CSRC, s) for s in SOURCES], "-ldl",
+           "-o", lib + ".tmp"]
     if debug:
         cmd.insert(1, "-DISD_DEBUG_BOUNDS")
     if verbose:

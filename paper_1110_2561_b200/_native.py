@@ -27,7 +27,8 @@ EXPORTED_SYMBOLS = (
     "isd_enumerate", "isd_enumerate_async", "isd_thermo", "isd_thermo_async",
     "isd_plan", "isd_validate", "isd_calibrate", "isd_device_count",
     "isd_sm_count", "isd_last_error", "isd_version", "isd_abi_version",
-    "isd_launch_count", "isd_mirror_async",
+    "isd_launch_count", "isd_mirror_async", "isd_kernel_info",
+    "isd_jit_check",
 )
 
 
@@ -110,6 +111,9 @@ def load():
         lib.isd_sm_count.argtypes = [i32]
         lib.isd_last_error.restype = ctypes.c_char_p
         lib.isd_version.restype = ctypes.c_char_p
+        lib.isd_kernel_info.restype = ctypes.c_char_p
+        lib.isd_jit_check.argtypes = [p_lat, u64, ctypes.POINTER(ctypes.c_uint64)]
+        lib.isd_jit_check.restype = ctypes.c_int
         lib.isd_launch_count.restype = ctypes.c_uint64
         for name in ("isd_enumerate", "isd_enumerate_async", "isd_thermo",
                      "isd_thermo_async", "isd_plan", "isd_validate",
@@ -256,3 +260,16 @@ def sm_count(device=None) -> int:
     if v < 0:
         check(v)
     return v
+
+
+def kernel_info() -> str:
+    """Kernel path of the last enumeration on this thread."""
+    return load().isd_kernel_info().decode()
+
+
+def jit_check(lat: Lattice, n_configs_hint: int) -> int:
+    """NVRTC-compile the lattice's specialised kernel (no GPU); cubin bytes."""
+    n = ctypes.c_uint64(0)
+    check(load().isd_jit_check(ctypes.byref(lat), n_configs_hint,
+                               ctypes.byref(n)))
+    return n.value

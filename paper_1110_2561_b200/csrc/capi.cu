@@ -20,6 +20,8 @@
 namespace isd {
 
 static thread_local std::string g_err;
+// which kernel path the last enumeration on this thread used
+static thread_local std::string g_kernel_info = "none";
 static std::atomic<uint64_t> g_launches{0};
 static std::mutex g_mu;
 
@@ -297,6 +299,7 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
   if (rc) return rc;
 
   if (algo == ISD_ALGO_CANONICAL) {
+    g_kernel_info = "k1_canonical";
     rc = enqueue_canonical(lat, start, end, out, sms, st, false, &nl);
     if (launches) *launches = nl;
     return rc;
@@ -340,6 +343,10 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
   HoistParams hp;
   fill_hoist(lat, &info, &hp);
   const uint64_t runs_per_launch = kMaxPerLaunch >> k;
+  // large walks use the per-lattice NVRTC specialisation (jit.cpp)
+  bool use_jit = env_long("ISD_JIT", 1) != 0 &&
+                 end - start >= 4 * kTuneConfigs;
+  g_kernel_info = use_jit ? "k1_hoisted_jit" : "k1_hoisted_aot";
   for (uint64_t r = r0; r < r1;) {
     const uint64_t re = (r1 - r > runs_per_launch) ? r + runs_per_launch : r1;
     hp.run_begin = r;
@@ -353,7 +360,17 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
         hp.lane_shift = (uint32_t)ls;
       hp.block_stride = 32ull << hp.lane_shift;
     }
-    int x = launch_hoisted(hp, out, sms, st);
+    int x = 0;
+    if (use_jit) {
+      std::string why;
+      x = launch_hoisted_jit(hp, out, sms, st, &why);
+      if (x < 0) return cuda_fail((cudaError_t)(-x), "k1_jit launch");
+      if (x == 0) {  // NVRTC unavailable: same arithmetic, AOT build
+        use_jit = false;
+        g_kernel_info = "k1_hoisted_aot (jit unavailable: " + why + ")";
+      }
+    }
+    if (!use_jit) x = launch_hoisted(hp, out, sms, st);
     if (x < 0) return cuda_fail((cudaError_t)(-x), "k1_hoisted launch");
     nl += x;
     r = re;
@@ -385,6 +402,22 @@ int isd_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   if (rc) return rc;
   if (!out) return fail(ISD_EINVAL, "plan pointer is NULL");
   return cached_plan(lat, n_configs_hint, out);
+}
+
+int isd_jit_check(const isd_lattice* lat, uint64_t n_configs_hint,
+                  uint64_t* cubin_bytes) {
+  int rc = isd_validate(lat);
+  if (rc) return rc;
+  isd_plan_info info;
+  if (cached_plan(lat, n_configs_hint, &info))
+    return fail(ISD_EINVAL, "lattice too small for the hoisted kernel");
+  HoistParams hp;
+  fill_hoist(lat, &info, &hp);
+  std::string why;
+  const int n = jit_compile_check(hp, &why);
+  if (n <= 0) return fail(ISD_ECUDA, "%s", why.c_str());
+  if (cubin_bytes) *cubin_bytes = (uint64_t)n;
+  return ISD_OK;
 }
 
 int isd_enumerate_async(const isd_lattice* lat, uint64_t start, uint64_t end,
@@ -559,6 +592,7 @@ int isd_sm_count(int device) {
 }
 
 const char* isd_last_error(void) { return g_err.c_str(); }
+const char* isd_kernel_info(void) { return g_kernel_info.c_str(); }
 const char* isd_version(void) { return "isingdos-b200 0.1.0 (sm_100a)"; }
 int isd_abi_version(void) { return ISD_ABI_VERSION; }
 uint64_t isd_launch_count(void) { return g_launches.load(); }

@@ -29,12 +29,6 @@
 
 #include "isd_internal.h"
 
-namespace isd {
-
-__device__ __forceinline__ void red_shared_inc(uint32_t addr) {
-  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
-}
-
 // Debug builds (-DISD_DEBUG_BOUNDS, libisingdos_b200_dbg.so) trap on any
 // histogram address outside the warp's own histogram: the bounds check that
 // stands in for compute-sanitizer, which is closed on the GPU pool.
@@ -48,6 +42,14 @@ __device__ __forceinline__ void red_shared_inc(uint32_t addr) {
   do {                               \
   } while (0)
 #endif
+
+#include "k1_body.cuh"
+
+namespace isd {
+
+__device__ __forceinline__ void red_shared_inc(uint32_t addr) {
+  isd_red_shared_inc(addr);
+}
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -111,122 +113,51 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---------------------------------------------------------------------------
-// hoisted kernel
+// hoisted kernel (ahead-of-time build; body in k1_body.cuh)
 // ---------------------------------------------------------------------------
+struct RuntimeTraits {
+  const HoistParams& P;
+  __device__ uint32_t k() const { return P.k; }
+  __device__ uint32_t nloop() const { return 1u << P.l; }
+  __device__ uint64_t above_k() const { return P.above_k; }
+  __device__ uint64_t odd_mask() const { return P.odd_mask; }
+  __device__ uint32_t loop_mask() const { return P.loop_mask; }
+  __device__ uint32_t e_parity() const { return P.e_parity; }
+  __device__ uint32_t e_mode() const { return P.e_mode; }
+  __device__ uint32_t row_bytes() const { return P.row_bytes; }
+  __device__ uint32_t e_bytes() const { return P.e_bytes; }
+  __device__ int32_t plane_bytes() const { return P.plane_bytes; }
+  __device__ uint32_t row_words() const { return P.row_words; }
+  __device__ uint32_t e_words() const { return P.e_words; }
+  __device__ uint32_t plane_words() const { return P.plane_words; }
+  __device__ uint32_t stride() const { return P.stride; }
+  __device__ uint32_t nbins() const { return P.nbins; }
+  __device__ uint32_t hist_words() const { return P.hist_words; }
+  __device__ uint32_t n_hist() const { return P.n_hist; }
+  __device__ uint32_t shift(int c) const { return P.shift[c]; }
+  __device__ uint64_t mask(int c) const { return P.mask[c]; }
+  __device__ uint64_t jneg(int c) const { return P.jneg[c]; }
+  __device__ uint32_t mvar(int c) const { return P.mvar[c]; }
+  __device__ uint64_t nm1(int q) const { return P.nm1[q]; }
+  __device__ uint64_t jn1(int q) const { return P.jn1[q]; }
+  __device__ uint64_t nm2(int q) const { return P.nm2[q]; }
+  __device__ uint64_t jn2(int q) const { return P.jn2[q]; }
+  __device__ uint32_t nm1v(int q) const { return P.nm1v[q]; }
+  __device__ uint32_t jn1v(int q) const { return P.jn1v[q]; }
+  __device__ uint32_t nm2v(int q) const { return P.nm2v[q]; }
+  __device__ uint32_t jn2v(int q) const { return P.jn2v[q]; }
+  __device__ int32_t degree(int q) const { return P.degree[q]; }
+  __device__ uint32_t koff(int c) const { return (uint32_t)P.koff[c]; }
+};
+
 template <int NC, bool DOUBLE>
 __global__ void __launch_bounds__(kThreads)
     k1_hoisted(const __grid_constant__ HoistParams P,
                unsigned long long* __restrict__ out) {
   extern __shared__ __align__(16) uint32_t hist[];
-  zero_hist(hist, P.n_hist * P.hist_words);
-  __syncthreads();
-  const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t hbase =
-      smem_addr(hist + (warp % P.n_hist) * P.hist_words);
-  const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
-  const uint32_t nloop = 1u << P.l;
-
-  const uint64_t nruns = P.run_end - P.run_begin;
-  const uint32_t ls = P.lane_shift;
-  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-       t < nruns; t += gstride) {
-    // lane bits of t go to run bits [ls, ls+5): which five sites the 32
-    // lanes of a warp differ in (shared-memory bank spread)
-    const uint64_t hi = t >> 5;
-    const uint64_t perm =
-        ((hi >> ls) << (ls + 5)) | ((t & 31) << ls) | (hi & ((1ull << ls) - 1));
-    const uint64_t r = P.run_begin + (perm & ((32ull << ls) - 1)) +
-                       (perm >> (ls + 5)) * P.block_stride;
-    // ---- per-run constants (bits [k, N) fixed) ----
-    const uint64_t xt = r << P.k;
-    const int m_run = __popcll(xt);
-    int e_run = 0;
-    uint32_t cst[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const uint64_t sh = xt >> P.shift[c];
-      e_run += __popcll(((xt ^ sh) ^ P.jneg[c]) & P.mask[c] & P.above_k);
-      // partner word seen by the loop sites [u, k); jneg folded in
-      cst[c] = (uint32_t)sh ^ (uint32_t)P.jneg[c];
-    }
-    int npr[kCopyBits];
-#pragma unroll
-    for (int q = 0; q < kCopyBits; ++q) {
-      npr[q] = __popcll((xt ^ P.jn1[q]) & P.nm1[q] & P.above_k);
-      if constexpr (DOUBLE)
-        npr[q] += __popcll((xt ^ P.jn2[q]) & P.nm2[q] & P.above_k);
-    }
-    // byte address of (m_run, e = 0) in this warp's histogram; the e parity
-    // of the configurations is par_run ^ parity(loop bits & odd_mask)
-    const uint32_t a_run =
-        hbase + (uint32_t)m_run * P.row_bytes + (uint32_t)P.ktd[0];
-    const uint32_t par_run =
-        (uint32_t)(__popcll(xt & P.odd_mask) + P.e_parity) & 1u;
-    const uint32_t odd_loop = (uint32_t)P.odd_mask & P.loop_mask;
-    // ---- loop over the subsets of the loop sites ----
-    uint32_t jb = 0;
-    for (uint32_t it = 0; it < nloop; ++it) {
-      int e = e_run;
-#pragma unroll
-      for (int c = 0; c < NC; ++c)
-        e += __popc((jb ^ __funnelshift_rc(jb, 0u, P.shift[c]) ^ cst[c]) &
-                    P.mvar[c]);
-      int d[kCopyBits];
-#pragma unroll
-      for (int q = 0; q < kCopyBits; ++q) {
-        int nq = npr[q] + __popc((jb ^ P.jn1v[q]) & P.nm1v[q]);
-        if constexpr (DOUBLE) nq += __popc((jb ^ P.jn2v[q]) & P.nm2v[q]);
-        e += nq;
-        d[q] = (int)P.e_bytes * (P.degree[q] - 2 * nq);
-      }
-      const uint32_t par = (par_run + __popc(jb & odd_loop)) & 1u;
-      // ---- 128 copies.  addr_c = addr_{c ^ topbit(c)} + d_top + ktd[c]:
-      // the low five copy bits form a subset-sum tree (live set <= 16),
-      // and each leaf immediately spawns its three siblings in bits 5, 6.
-      const uint32_t a0 = a_run + (uint32_t)__popc(jb) * P.row_bytes +
-                          (uint32_t)e * P.e_bytes +
-                          par * (uint32_t)P.plane_bytes;
-      uint32_t a[32];
-#pragma unroll
-      for (int cl = 0; cl < 32; ++cl) {
-        if (cl == 0) {
-          a[0] = a0;
-        } else {
-          const int top = 31 - __clz(cl);
-          a[cl] = a[cl ^ (1 << top)] + (uint32_t)d[top] + (uint32_t)P.ktd[cl];
-        }
-        ISD_CHECK_ADDR(a[cl], hbase, 4u * P.hist_words);
-        red_shared_inc(a[cl]);
-        const uint32_t b1 = a[cl] + (uint32_t)d[5] + (uint32_t)P.ktd[cl + 32];
-        ISD_CHECK_ADDR(b1, hbase, 4u * P.hist_words);
-        red_shared_inc(b1);
-        const uint32_t b2 = a[cl] + (uint32_t)d[6] + (uint32_t)P.ktd[cl + 64];
-        ISD_CHECK_ADDR(b2, hbase, 4u * P.hist_words);
-        red_shared_inc(b2);
-        const uint32_t b3 = b1 + (uint32_t)d[6] + (uint32_t)P.ktd[cl + 96];
-        ISD_CHECK_ADDR(b3, hbase, 4u * P.hist_words);
-        red_shared_inc(b3);
-      }
-      jb = (jb - P.loop_mask) & P.loop_mask;  // next subset of the loop sites
-    }
-  }
-  __syncthreads();
-  // ---- flush: word (m, e) -> table bin (m, e) ----
-  for (uint32_t bin = threadIdx.x; bin < P.nbins; bin += blockDim.x) {
-    const uint32_t m = bin / P.stride, e = bin - m * P.stride;
-    uint32_t word;
-    if (P.e_mode) {
-      const uint32_t par = e & 1u;
-      if (P.odd_mask == 0 && par != P.e_parity) continue;  // structurally 0
-      word = m * P.row_words + ((e - par) >> 1) * P.e_words +
-             par * P.plane_words;
-    } else {
-      word = m * P.row_words + e * P.e_words;
-    }
-    unsigned long long s = 0;
-    for (uint32_t h = 0; h < P.n_hist; ++h) s += hist[h * P.hist_words + word];
-    if (s) atomicAdd(out + bin, s);
-  }
+  const RuntimeTraits L{P};
+  k1_hoisted_body<NC, DOUBLE>(L, P.run_begin, P.run_end - P.run_begin,
+                              P.block_stride, P.lane_shift, hist, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <cstddef>
+#include <string>
 #include <vector>
 
 #include "isingdos_b200.h"
@@ -69,7 +70,8 @@ struct HoistParams {
   uint32_t nm1v[kCopyBits], jn1v[kCopyBits]; // restricted to loop sites
   uint32_t nm2v[kCopyBits], jn2v[kCopyBits];
   int32_t degree[kCopyBits];                 // d_q
-  int32_t ktd[kCopies];          // byte offset of copy c minus copy c^topbit(c)
+  int32_t koff[kCopies];         // constant byte offset of copy c:
+                                 // popc(c) row_bytes + e_bytes unsat_cc(c)
 };
 
 // ---- host side -----------------------------------------------------------
@@ -92,6 +94,11 @@ int launch_canonical(const CanonParams& p, unsigned long long* out,
                      int sm_count, void* stream, bool small_grid);
 int launch_hoisted(const HoistParams& p, unsigned long long* out,
                    int sm_count, void* stream);
+// NVRTC-specialised k1 (jit.cpp): 1 launched, 0 unavailable (*why), <0 error
+int launch_hoisted_jit(const HoistParams& p, unsigned long long* out,
+                       int sm_count, void* stream, std::string* why);
+// compile only (no GPU needed): cubin size, or 0 with *why
+int jit_compile_check(const HoistParams& p, std::string* why);
 int launch_mirror(unsigned long long* t, uint32_t n, uint32_t b,
                   void* stream);
 int launch_thermo(const unsigned long long* counts, uint32_t n_spins,

@@ -1,0 +1,281 @@
+// Per-lattice specialisation of the hoisted kernel with NVRTC.
+//
+// k1_body.cuh is compiled a second time at run time with every lattice
+// constant (masks, shifts, the 128-entry copy offset table, layout strides,
+// loop width) turned into a constexpr, for sm_100a.  The copy offsets then
+// fold into the shared RED's address immediate and the per-group masks into
+// LOP3 immediates, which removes the uniform-register loads the ahead-of-time
+// kernel needs.  NVRTC is loaded with dlopen; if it is
+// missing or a compile fails the caller falls back to the ahead-of-time
+// kernel (same arithmetic, same results) and isd_kernel_info() says so.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "isd_internal.h"
+
+namespace isd {
+
+static const char kBodySource[] =
+#include "k1_body_str.inc"
+    ;
+
+// ---- minimal NVRTC binding -------------------------------------------------
+typedef int nvrtcResult_t;
+typedef struct _nvrtcProgram* nvrtcProgram_t;
+struct Nvrtc {
+  bool ok = false;
+  std::string why;
+  nvrtcResult_t (*create)(nvrtcProgram_t*, const char*, const char*, int,
+                          const char* const*, const char* const*) = nullptr;
+  nvrtcResult_t (*compile)(nvrtcProgram_t, int, const char* const*) = nullptr;
+  nvrtcResult_t (*cubin_size)(nvrtcProgram_t, size_t*) = nullptr;
+  nvrtcResult_t (*cubin)(nvrtcProgram_t, char*) = nullptr;
+  nvrtcResult_t (*log_size)(nvrtcProgram_t, size_t*) = nullptr;
+  nvrtcResult_t (*log)(nvrtcProgram_t, char*) = nullptr;
+  nvrtcResult_t (*destroy)(nvrtcProgram_t*) = nullptr;
+};
+
+static Nvrtc& nvrtc() {
+  static Nvrtc n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = nullptr;
+    for (const char* name : {"libnvrtc.so.12", "libnvrtc.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
+      if (h) break;
+    }
+    if (!h) {
+      n.why = "libnvrtc not found";
+      return;
+    }
+    n.create = (decltype(n.create))dlsym(h, "nvrtcCreateProgram");
+    n.compile = (decltype(n.compile))dlsym(h, "nvrtcCompileProgram");
+    n.cubin_size = (decltype(n.cubin_size))dlsym(h, "nvrtcGetCUBINSize");
+    n.cubin = (decltype(n.cubin))dlsym(h, "nvrtcGetCUBIN");
+    n.log_size = (decltype(n.log_size))dlsym(h, "nvrtcGetProgramLogSize");
+    n.log = (decltype(n.log))dlsym(h, "nvrtcGetProgramLog");
+    n.destroy = (decltype(n.destroy))dlsym(h, "nvrtcDestroyProgram");
+    n.ok = n.create && n.compile && n.cubin_size && n.cubin && n.log_size &&
+           n.log && n.destroy;
+    if (!n.ok) n.why = "libnvrtc lacks a required symbol";
+  });
+  return n;
+}
+
+// ---- source generation -----------------------------------------------------
+template <typename V>
+static void emit_switch(std::ostringstream& o, const char* type,
+                        const char* name, const V* vals, int n,
+                        const char* suffix) {
+  o << "  __device__ __forceinline__ static " << type << " " << name
+    << "(int i) {\n    switch (i) {\n";
+  for (int i = 0; i < n; ++i)
+    o << "      case " << i << ": return " << vals[i] << suffix << ";\n";
+  o << "    }\n    return 0;\n  }\n";
+}
+
+static std::string generate(const HoistParams& P, int nc, bool dbl,
+                            bool debug_bounds) {
+  std::ostringstream o;
+  o << "typedef unsigned int uint32_t;\n"
+       "typedef unsigned long long uint64_t;\n"
+       "typedef int int32_t;\n";
+  if (debug_bounds)
+    o << "#define ISD_CHECK_ADDR(a, lo, bytes) do { if ((unsigned)((a) - "
+         "(lo)) >= (bytes) || ((a) & 3u)) __trap(); } while (0)\n";
+  o << kBodySource << "\n";
+  o << "struct JitTraits {\n";
+  auto c32 = [&](const char* name, unsigned long long v) {
+    o << "  __device__ __forceinline__ static constexpr uint32_t " << name
+      << "() { return " << v << "u; }\n";
+  };
+  auto c64 = [&](const char* name, unsigned long long v) {
+    o << "  __device__ __forceinline__ static constexpr uint64_t " << name
+      << "() { return " << v << "ull; }\n";
+  };
+  c32("k", P.k);
+  c32("nloop", 1u << P.l);
+  c64("above_k", P.above_k);
+  c64("odd_mask", P.odd_mask);
+  c32("loop_mask", P.loop_mask);
+  c32("e_parity", P.e_parity);
+  c32("e_mode", P.e_mode);
+  c32("row_bytes", P.row_bytes);
+  c32("e_bytes", P.e_bytes);
+  o << "  __device__ __forceinline__ static constexpr int32_t plane_bytes() "
+       "{ return "
+    << P.plane_bytes << "; }\n";
+  c32("row_words", P.row_words);
+  c32("e_words", P.e_words);
+  c32("plane_words", P.plane_words);
+  c32("stride", P.stride);
+  c32("nbins", P.nbins);
+  c32("hist_words", P.hist_words);
+  c32("n_hist", P.n_hist);
+  emit_switch(o, "uint32_t", "shift", P.shift, nc, "u");
+  emit_switch(o, "uint64_t", "mask", P.mask, nc, "ull");
+  emit_switch(o, "uint64_t", "jneg", P.jneg, nc, "ull");
+  emit_switch(o, "uint32_t", "mvar", P.mvar, nc, "u");
+  emit_switch(o, "uint64_t", "nm1", P.nm1, kCopyBits, "ull");
+  emit_switch(o, "uint64_t", "jn1", P.jn1, kCopyBits, "ull");
+  emit_switch(o, "uint64_t", "nm2", P.nm2, kCopyBits, "ull");
+  emit_switch(o, "uint64_t", "jn2", P.jn2, kCopyBits, "ull");
+  emit_switch(o, "uint32_t", "nm1v", P.nm1v, kCopyBits, "u");
+  emit_switch(o, "uint32_t", "jn1v", P.jn1v, kCopyBits, "u");
+  emit_switch(o, "uint32_t", "nm2v", P.nm2v, kCopyBits, "u");
+  emit_switch(o, "uint32_t", "jn2v", P.jn2v, kCopyBits, "u");
+  emit_switch(o, "int32_t", "degree", P.degree, kCopyBits, "");
+  uint32_t koff[kCopies];
+  for (int c = 0; c < kCopies; ++c) koff[c] = (uint32_t)P.koff[c];
+  emit_switch(o, "uint32_t", "koff", koff, kCopies, "u");
+  o << "};\n";
+  o << "extern \"C\" __global__ void __launch_bounds__(" << kThreads
+    << ") k1_jit(unsigned long long run_begin, unsigned long long nruns,\n"
+       "    unsigned long long block_stride, unsigned int ls,\n"
+       "    unsigned long long* __restrict__ out) {\n"
+       "  extern __shared__ __align__(16) unsigned int hist[];\n"
+       "  const JitTraits L;\n"
+       "  k1_hoisted_body<"
+    << nc << ", " << (dbl ? "true" : "false")
+    << ">(L, run_begin, nruns, block_stride, ls, hist, out);\n}\n";
+  return o.str();
+}
+
+// ---- cache -----------------------------------------------------------------
+struct JitKernel {
+  bool ok = false;
+  std::string why;
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  int grid = 0;
+};
+
+static std::mutex g_jit_mu;
+static std::map<std::string, JitKernel> g_jit;
+
+// Bytes of HoistParams that define the kernel (everything but the range).
+static std::string jit_key(const HoistParams& P, int device) {
+  HoistParams q = P;
+  q.run_begin = q.run_end = 0;
+  q.block_stride = 0;
+  q.lane_shift = 0;
+  std::string key(reinterpret_cast<const char*>(&q), sizeof q);
+  key += std::to_string(device);
+  return key;
+}
+
+// Generate and compile the specialised kernel to a cubin (host only).
+static bool compile_cubin(const HoistParams& P, std::vector<char>* cubin,
+                          std::string* why) {
+  Nvrtc& nv = nvrtc();
+  if (!nv.ok) {
+    *why = nv.why;
+    return false;
+  }
+#ifdef ISD_DEBUG_BOUNDS
+  const bool debug_bounds = true;
+#else
+  const bool debug_bounds = false;
+#endif
+  const std::string src =
+      generate(P, (int)P.n_classes, P.has_double != 0, debug_bounds);
+  nvrtcProgram_t prog = nullptr;
+  if (nv.create(&prog, src.c_str(), "k1_jit.cu", 0, nullptr, nullptr) != 0) {
+    *why = "nvrtcCreateProgram failed";
+    return false;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17",
+                        "-lineinfo"};
+  const int rc = nv.compile(prog, 3, opts);
+  if (rc != 0) {
+    size_t n = 0;
+    nv.log_size(prog, &n);
+    std::string log(n, '\0');
+    if (n) nv.log(prog, &log[0]);
+    *why = "NVRTC compile failed: " + log.substr(0, 600);
+    nv.destroy(&prog);
+    return false;
+  }
+  size_t n = 0;
+  nv.cubin_size(prog, &n);
+  cubin->resize(n);
+  nv.cubin(prog, cubin->data());
+  nv.destroy(&prog);
+  return true;
+}
+
+int jit_compile_check(const HoistParams& P, std::string* why) {
+  std::vector<char> cubin;
+  return compile_cubin(P, &cubin, why) ? (int)cubin.size() : 0;
+}
+
+static JitKernel build_kernel(const HoistParams& P, int sm_count) {
+  JitKernel jk;
+  std::vector<char> cubin;
+  if (!compile_cubin(P, &cubin, &jk.why)) return jk;
+  cudaError_t e = cudaLibraryLoadData(&jk.lib, cubin.data(), nullptr, nullptr,
+                                      0, nullptr, nullptr, 0);
+  if (e == cudaSuccess) e = cudaLibraryGetKernel(&jk.kern, jk.lib, "k1_jit");
+  const size_t smem = (size_t)P.n_hist * P.hist_words * 4;
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute((const void*)jk.kern,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+  int per_sm = 0;
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, (const void*)jk.kern, kThreads, smem);
+  if (e != cudaSuccess) {
+    jk.why = std::string("loading the JIT kernel: ") + cudaGetErrorString(e);
+    cudaGetLastError();
+    return jk;
+  }
+  jk.grid = (per_sm < 1 ? 1 : per_sm) * sm_count;
+  jk.ok = true;
+  return jk;
+}
+
+// Launch the specialised kernel for P's run range; returns 1 on success,
+// 0 if the JIT path is unavailable (caller falls back), <0 on a launch error.
+int launch_hoisted_jit(const HoistParams& P, unsigned long long* out,
+                       int sm_count, void* stream, std::string* why) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::string key = jit_key(P, dev);
+  JitKernel jk;
+  {
+    std::lock_guard<std::mutex> lock(g_jit_mu);
+    auto it = g_jit.find(key);
+    if (it == g_jit.end())
+      it = g_jit.emplace(key, build_kernel(P, sm_count)).first;
+    jk = it->second;
+  }
+  if (!jk.ok) {
+    if (why) *why = jk.why;
+    return 0;
+  }
+  unsigned long long run_begin = P.run_begin;
+  unsigned long long nruns = P.run_end - P.run_begin;
+  unsigned long long block_stride = P.block_stride;
+  unsigned int ls = P.lane_shift;
+  void* args[] = {&run_begin, &nruns, &block_stride, &ls, &out};
+  int grid = jk.grid;
+  const uint64_t need = (nruns + kThreads - 1) / kThreads;
+  if (need < (uint64_t)grid) grid = (int)(need ? need : 1);
+  const size_t smem = (size_t)P.n_hist * P.hist_words * 4;
+  cudaError_t e = cudaLaunchKernel((const void*)jk.kern, dim3(grid),
+                                   dim3(kThreads), args, smem,
+                                   (cudaStream_t)stream);
+  if (e != cudaSuccess) return -(int)e;
+  return 1;
+}
+
+}  // namespace isd

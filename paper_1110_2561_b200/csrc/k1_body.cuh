@@ -1,0 +1,156 @@
+// k1_body.cuh — body of the hoisted enumeration kernel (K1b).
+//
+// Shared, as source, by two kernels:
+//   * k1_hoisted (enumerate.cu), compiled ahead of time: the lattice
+//     constants come from a __grid_constant__ HoistParams (RuntimeTraits);
+//   * k1_jit (jit.cpp), compiled per lattice with NVRTC: the same constants
+//     are constexpr (a generated traits struct), so masks, shifts, the copy
+//     offset table and the layout strides become immediates — in particular
+//     each copy's constant offset folds into the RED's address immediate.
+// This file must stay self-contained (builtins only): jit.cpp embeds it.
+//
+// Decomposition: bits [k, N) = the thread's run; inside
+// [0, k) the loop sites take every subset, and 7 copy sites are 128
+// register copies.  Per configuration: one add and one shared RED.
+
+#ifndef ISD_K1_BODY_CUH
+#define ISD_K1_BODY_CUH
+
+#ifndef ISD_CHECK_ADDR
+#define ISD_CHECK_ADDR(a, lo, bytes) \
+  do {                               \
+  } while (0)
+#endif
+
+__device__ __forceinline__ void isd_red_shared_inc(unsigned int addr) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
+}
+
+template <int NC, bool DOUBLE, class T>
+__device__ __forceinline__ void k1_hoisted_body(
+    const T& L, unsigned long long run_begin, unsigned long long nruns,
+    unsigned long long block_stride, unsigned int ls, unsigned int* hist,
+    unsigned long long* __restrict__ out) {
+  // ---- zero the block's histograms ----
+  {
+    uint4* h4 = reinterpret_cast<uint4*>(hist);
+    const unsigned int n4 = L.n_hist() * L.hist_words() / 4;
+    for (unsigned int i = threadIdx.x; i < n4; i += blockDim.x)
+      h4[i] = make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  const unsigned int warp = threadIdx.x >> 5;
+  const unsigned int hbase = (unsigned int)__cvta_generic_to_shared(
+      hist + (warp % L.n_hist()) * L.hist_words());
+  const unsigned int hbytes = 4u * L.hist_words();
+  const unsigned long long gstride = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned int nloop = L.nloop();
+  const unsigned long long above_k = L.above_k();
+
+  for (unsigned long long t =
+           (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       t < nruns; t += gstride) {
+    // lane bits of t go to run bits [ls, ls+5): which five sites the 32
+    // lanes of a warp differ in (shared-memory bank spread); blocks of
+    // 2^(ls+5) runs are block_stride apart (contiguous in a normal walk)
+    const unsigned long long hi = t >> 5;
+    const unsigned long long perm = ((hi >> ls) << (ls + 5)) |
+                                    ((t & 31) << ls) |
+                                    (hi & ((1ull << ls) - 1));
+    const unsigned long long r = run_begin + (perm & ((32ull << ls) - 1)) +
+                                 (perm >> (ls + 5)) * block_stride;
+    // ---- per-run constants (bits [k, N) fixed) ----
+    const unsigned long long xt = r << L.k();
+    const int m_run = __popcll(xt);
+    int e_run = 0;
+    unsigned int cst[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const unsigned long long sh = xt >> L.shift(c);
+      e_run += __popcll(((xt ^ sh) ^ L.jneg(c)) & L.mask(c) & above_k);
+      // partner word seen by the loop sites; jneg folded in
+      cst[c] = (unsigned int)sh ^ (unsigned int)L.jneg(c);
+    }
+    int npr[7];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      npr[q] = __popcll((xt ^ L.jn1(q)) & L.nm1(q) & above_k);
+      if (DOUBLE) npr[q] += __popcll((xt ^ L.jn2(q)) & L.nm2(q) & above_k);
+    }
+    // byte address of (m_run, e = 0); the e parity of the configurations
+    // is par_run ^ parity(loop bits & odd_mask)
+    const unsigned int a_run = hbase + (unsigned int)m_run * L.row_bytes();
+    const unsigned int par_run =
+        (unsigned int)(__popcll(xt & L.odd_mask()) + L.e_parity()) & 1u;
+    const unsigned int odd_loop =
+        (unsigned int)L.odd_mask() & L.loop_mask();
+    // ---- loop over the subsets of the loop sites ----
+    unsigned int jb = 0;
+    for (unsigned int it = 0; it < nloop; ++it) {
+      int e = e_run;
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        e += __popc((jb ^ __funnelshift_rc(jb, 0u, L.shift(c)) ^ cst[c]) &
+                    L.mvar(c));
+      unsigned int d[7];
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {
+        int nq = npr[q] + __popc((jb ^ L.jn1v(q)) & L.nm1v(q));
+        if (DOUBLE) nq += __popc((jb ^ L.jn2v(q)) & L.nm2v(q));
+        e += nq;
+        d[q] = (unsigned int)((int)L.e_bytes() * (L.degree(q) - 2 * nq));
+      }
+      const unsigned int par = (par_run + __popc(jb & odd_loop)) & 1u;
+      // a[c] carries no per-copy constant: addr(c) = a[c] + koff(c), where
+      // koff(c) = popc(c) row_bytes + e_bytes * (copy-copy unsatisfied
+      // bonds of c) folds into the RED's address offset.  128 copies: a
+      // 32-leaf subset-sum tree over copy bits 0-4 (live set <= 16), each
+      // leaf spawning its three siblings in bits 5 and 6.
+      const unsigned int a0 = a_run + (unsigned int)__popc(jb) * L.row_bytes() +
+                              (unsigned int)e * L.e_bytes() +
+                              par * (unsigned int)L.plane_bytes();
+      unsigned int a[32];
+#pragma unroll
+      for (int cl = 0; cl < 32; ++cl) {
+        if (cl == 0) {
+          a[0] = a0;
+        } else {
+          const int top = 31 - __clz(cl);
+          a[cl] = a[cl ^ (1 << top)] + d[top];
+        }
+        const unsigned int b1 = a[cl] + d[5];
+        const unsigned int b2 = a[cl] + d[6];
+        const unsigned int b3 = b1 + d[6];
+        ISD_CHECK_ADDR(a[cl] + L.koff(cl), hbase, hbytes);
+        isd_red_shared_inc(a[cl] + L.koff(cl));
+        ISD_CHECK_ADDR(b1 + L.koff(cl + 32), hbase, hbytes);
+        isd_red_shared_inc(b1 + L.koff(cl + 32));
+        ISD_CHECK_ADDR(b2 + L.koff(cl + 64), hbase, hbytes);
+        isd_red_shared_inc(b2 + L.koff(cl + 64));
+        ISD_CHECK_ADDR(b3 + L.koff(cl + 96), hbase, hbytes);
+        isd_red_shared_inc(b3 + L.koff(cl + 96));
+      }
+      jb = (jb - L.loop_mask()) & L.loop_mask();  // next subset
+    }
+  }
+  __syncthreads();
+  // ---- flush: word (m, e) -> table bin (m, e) ----
+  for (unsigned int bin = threadIdx.x; bin < L.nbins(); bin += blockDim.x) {
+    const unsigned int m = bin / L.stride(), e = bin - m * L.stride();
+    unsigned int word;
+    if (L.e_mode()) {
+      const unsigned int par = e & 1u;
+      if (L.odd_mask() == 0 && par != L.e_parity()) continue;  // always 0
+      word = m * L.row_words() + ((e - par) >> 1) * L.e_words() +
+             par * L.plane_words();
+    } else {
+      word = m * L.row_words() + e * L.e_words();
+    }
+    unsigned long long s = 0;
+    for (unsigned int h = 0; h < L.n_hist(); ++h)
+      s += hist[h * L.hist_words() + word];
+    if (s) atomicAdd(out + bin, s);
+  }
+}
+
+#endif  // ISD_K1_BODY_CUH

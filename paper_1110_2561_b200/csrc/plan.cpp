@@ -448,20 +448,12 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
     p->degree[q] = info->copy_degree[q];
     if (info->copy_nbr2[q]) p->has_double = 1;
   }
-  // copy_table[c] = popc(c)(B+1) + unsat_cc(c); split into the m and e
-  // parts and express the subset-sum steps in bytes
+  // copy_table[c] = popc(c)(B+1) + unsat_cc(c) -> byte offset of copy c
   const int eb = (int)p->e_bytes, rb = (int)p->row_bytes;
-  auto unsat = [&](int c) {
-    return info->copy_table[c] -
-           __builtin_popcount((unsigned)c) * (int)info->stride;
-  };
   for (int c = 0; c < kCopies; ++c) {
-    if (c == 0) {
-      p->ktd[0] = eb * unsat(0);
-    } else {
-      const int top = 31 - __builtin_clz((unsigned)c);
-      p->ktd[c] = rb + eb * (unsat(c) - unsat(c ^ (1 << top)));
-    }
+    const int pc = __builtin_popcount((unsigned)c);
+    const int unsat = info->copy_table[c] - pc * (int)info->stride;
+    p->koff[c] = pc * rb + eb * unsat;
   }
 }
 

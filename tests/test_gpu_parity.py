@@ -199,6 +199,18 @@ def test_6x6_periodic_matches_reference_walk():
     assert np.array_equal(full(spec), want)
 
 
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_jit_and_aot_kernels_agree(name, monkeypatch):
+    spec = workloads()[name].spec
+    jit = full(spec)
+    assert _native.kernel_info() == "k1_hoisted_jit"
+    monkeypatch.setenv("ISD_JIT", "0")
+    aot = full(spec)
+    assert _native.kernel_info() == "k1_hoisted_aot"
+    assert np.array_equal(jit, aot)
+    assert np.array_equal(jit, _golden_c(name))
+
+
 def test_n36_canonical_equals_hoisted():
     spec = workloads()["c4"].spec
     a = full(spec, _native.ALGO_CANONICAL)

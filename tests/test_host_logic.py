@@ -329,3 +329,12 @@ def _integration_stub_classes(spec):
                                   isd.LatticeSpec(17, 2)])
 def test_integration_stub_matches_bond_classes(spec):
     assert _integration_stub_classes(spec) == spec.bond_classes()
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_jit_source_compiles_for_sm100a(name):
+    # the per-lattice specialised kernel is generated and NVRTC-compiled on
+    # the host (no GPU needed); a compile error would silently cost speed
+    spec = workloads()[name].spec
+    n = _native.jit_check(native_lattice(spec), spec.num_configs)
+    assert n > 10000
