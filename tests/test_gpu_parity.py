@@ -361,3 +361,46 @@ def test_bounds_checked_build_runs_clean():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     assert "bounds ok" in r.stdout
+
+
+# -- maximum size (N = 40, the reference's cap) : size-independent checks ---
+
+N40 = [
+    dict(rows=5, cols=8), dict(rows=4, cols=10, boundary="free"),
+    dict(rows=2, cols=4, depth=5), dict(rows=5, cols=8, seed=40),
+    dict(rows=20, cols=2, coupling=-1),
+]
+
+
+def _bipartite(spec):
+    dims = (spec.rows, spec.cols, spec.depth)
+    if not spec.periodic:
+        return True
+    return all(d % 2 == 0 for d in dims if d > 1)
+
+
+@pytest.mark.parametrize("kw", N40)
+def test_n40_full_walk_invariants(kw):
+    spec = _spec(kw)
+    assert spec.num_spins == 40
+    t = full(spec)
+    dos = isd.DoSHistogram(spec, t)
+    rep = isd.verify_dos(dos)
+    assert rep.passed, str(rep)          # 2^40 total, C(40,k) rows, M flip
+    if _bipartite(spec):
+        e = t.sum(axis=0)
+        assert np.array_equal(e, e[::-1])
+    # a slice against the oracle port, and shard-count invisibility
+    lat = _port(spec)
+    a = (1 << 39) + 987654321
+    part, _ = enumerate_range_timed(spec, a, a + (1 << 20) + 7)
+    assert np.array_equal(part.view(np.int64),
+                          port.enumerate_range(lat, a, a + (1 << 20) + 7))
+    three = sum(enumerate_range_timed(spec, s.start_index, s.end_index)[0]
+                for s in isd.make_shards(spec, 3))
+    assert np.array_equal(three.view(np.int64), t)
+
+
+def test_n40_canonical_equals_hoisted():
+    spec = _spec(dict(rows=5, cols=8, seed=7))
+    assert np.array_equal(full(spec, _native.ALGO_CANONICAL), full(spec))
