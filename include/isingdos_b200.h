@@ -187,7 +187,7 @@ int isd_device_count(void);
 int isd_sm_count(int device);
 const char* isd_last_error(void);
 /* Kernel path of the last enumeration on this thread: "k1_hoisted_jit"
- * (per-lattice NVRTC specialisation, walks >= 2^35), "k1_hoisted_aot",
+ * (per-lattice NVRTC specialisation, walks >= 2^33), "k1_hoisted_aot",
  * "k1_canonical" (or an AOT note saying why the JIT was unavailable). */
 const char* isd_kernel_info(void);
 const char* isd_version(void);

@@ -111,9 +111,10 @@ static int current_sm_count(int* sms) {
 
 // Plans are compiled once per (lattice, loop width): the layout search
 // replays a sample of warp instructions and costs tens of milliseconds.
-// The model ranks every layout; before the first large walk the best few
-// are timed on the GPU on a 2^33-configuration slice (>= 4 runs per thread) and the fastest is
-// kept (autotune, once per process and lattice; ISD_AUTOTUNE=0 disables).
+// The model ranks every layout; before the first walk of >= 2^33
+// configurations the best 40 are timed on the GPU on a strided 2^33
+// sample of the range and the fastest is kept (autotune, once per process,
+// lattice and loop width; ISD_AUTOTUNE=0 disables).
 struct PlanEntry {
   int rc = 0;
   isd_plan_info info;
@@ -327,7 +328,7 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     rc = enqueue_canonical(lat, start, r0 << k, out, sms, st, true, &nl);
     if (rc) return rc;
   }
-  if (end - start >= 4 * kTuneConfigs)
+  if (end - start >= kTuneConfigs)
     autotune(lat, end - start, r0, r1, sms, st, &info);
   // experiment knob: ISD_LAYOUT="A,B,P,ls" forces the histogram layout
   if (const char* lay = std::getenv("ISD_LAYOUT")) {
@@ -344,8 +345,7 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
   fill_hoist(lat, &info, &hp);
   const uint64_t runs_per_launch = kMaxPerLaunch >> k;
   // large walks use the per-lattice NVRTC specialisation (jit.cpp)
-  bool use_jit = env_long("ISD_JIT", 1) != 0 &&
-                 end - start >= 4 * kTuneConfigs;
+  bool use_jit = env_long("ISD_JIT", 1) != 0 && end - start >= kTuneConfigs;
   g_kernel_info = use_jit ? "k1_hoisted_jit" : "k1_hoisted_aot";
   for (uint64_t r = r0; r < r1;) {
     const uint64_t re = (r1 - r > runs_per_launch) ? r + runs_per_launch : r1;

@@ -222,7 +222,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
 }
 
 // Hoisted split: 7 copy sites and l loop sites inside the low k bits, the
-// rest per-thread.  l keeps >= ~2^20 runs in a full walk (148 SMs).
+// rest per-thread.
 int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint) {
   const int n = (int)lat->n_spins;
   const int u = kCopyBits;
@@ -230,7 +230,8 @@ int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint) {
   while (log_configs < 63 && (1ull << (log_configs + 1)) <= n_configs_hint)
     ++log_configs;
   if (log_configs > n) log_configs = n;
-  int l = log_configs - u - 20;
+  // >= 2^17 runs of 2^k configurations (>= ~3.5 per thread on 148 SMs)
+  int l = log_configs - u - 17;
   // tuning / test knob: force the loop width
   if (const char* env = std::getenv("ISD_LOOP_BITS")) l = std::atoi(env);
   if (l > 7) l = 7;

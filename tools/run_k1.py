@@ -23,15 +23,24 @@ def main():
     p.add_argument("--config", default="c5")
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--algo", default="auto", choices=["auto", "canonical"])
+    p.add_argument("--shards", type=int, default=1,
+                   help="time shard --index of make_shards(spec, shards) "
+                        "(what one rank of a multi-GPU run walks)")
+    p.add_argument("--index", type=int, default=0)
     a = p.parse_args()
     algo = _native.ALGO_AUTO if a.algo == "auto" else _native.ALGO_CANONICAL
     spec = workloads()[a.config].spec
+    sh = isd.make_shards(spec, a.shards)[a.index]
     for i in range(a.reps):
-        table, ms = enumerate_range_timed(spec, 0, spec.num_configs, algo=algo)
-        dos = isd.DoSHistogram(spec, table.view("int64"))
-        ok = isd.verify_dos(dos).passed
+        table, ms = enumerate_range_timed(spec, sh.start_index, sh.end_index,
+                                          algo=algo)
+        if a.shards == 1:
+            dos = isd.DoSHistogram(spec, table.view("int64"))
+            ok = isd.verify_dos(dos).passed
+        else:
+            ok = int(table.sum()) == sh.size
         print(f"{a.config} rep {i}: {ms:.3f} ms, "
-              f"{spec.num_configs / ms / 1e9:.3f} Tconf/s, verify={ok}",
+              f"{sh.size / ms / 1e9:.3f} Tconf/s, verify={ok}",
               flush=True)
         if not ok:
             return 1
