@@ -45,7 +45,7 @@ def main():
         if not ok:
             return 1
     from paper_1110_2561_b200.enumeration import native_lattice
-    ok, info = _native.plan(native_lattice(spec), spec.num_configs)
+    ok, info = _native.plan(native_lattice(spec), sh.size)
     print(f"  plan: mode={info.e_mode} sites={list(info.copy_site)} "
           f"A,B,P={info.row_words},{info.e_words},{info.plane_words} "
           f"lane_shift={info.lane_shift} est={info.est_wavefronts:.3f}")
