@@ -179,22 +179,27 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  // a strided sample of the body [run0, run1): blocks of 2^(ls+5)
-  // consecutive runs (the lanes' neighbourhood, as in the real walk) spread
-  // evenly over the whole range, so every region of the index space votes
+  // the sample: warps spread evenly over the body [run0, run1), each warp
+  // with the candidate's own lane placement, so every region of the index
+  // space votes and all candidates see the same spread
   const uint64_t runs = kTuneConfigs >> cands[0].k;
   float best_ms = 1e30f;
   size_t best = 0;
   for (size_t i = 0; i < cands.size(); ++i) {
     HoistParams hp;
     fill_hoist(lat, &cands[i], &hp);
+    const uint64_t body = run1 - run0;
     const uint64_t blk = 32ull << hp.lane_shift;
-    const uint64_t want = runs > blk ? runs : blk;
-    if (run1 - run0 < want) continue;
-    const uint64_t nblk = want / blk;
-    hp.block_stride = ((run1 - run0) / nblk) & ~(blk - 1);
+    if (body < blk || body < runs) continue;
+    const uint64_t warps = runs / 32;
+    const uint64_t slots = body / 32;  // warp slots in the body
+    // warp slots must stay inside whole lane blocks of the body
+    const uint64_t usable = (body / blk) * (blk / 32);
+    hp.hi_step = usable / warps;
+    if (hp.hi_step < 1) hp.hi_step = 1;
+    (void)slots;
     hp.run_begin = run0;
-    hp.run_end = run0 + nblk * blk;
+    hp.run_end = run0 + warps * 32;
     float ms = 0.f;
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(e0, st);
@@ -204,7 +209,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     bump_launches(2);
-    ms /= (float)(nblk * blk);  // per run: samples may differ in size
+    ms /= (float)(warps * 32);  // per run
     if (ms < best_ms) {
       best_ms = ms;
       best = i;
@@ -358,7 +363,7 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
       hp.lane_shift = 0;
       if (ls > 0 && ls < 40 && ((re - r) & ((1ull << (ls + 5)) - 1)) == 0)
         hp.lane_shift = (uint32_t)ls;
-      hp.block_stride = 32ull << hp.lane_shift;
+      hp.hi_step = 1;
     }
     int x = 0;
     if (use_jit) {

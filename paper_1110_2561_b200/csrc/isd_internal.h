@@ -51,9 +51,8 @@ struct HoistParams {
   uint32_t n_hist;
   uint32_t has_double;           // any copy site with a doubled partner
   uint32_t lane_shift;           // warp lanes take run bits [s, s+5)
-  uint64_t block_stride;         // runs between blocks of 2^(s+5) runs
-                                 // (2^(s+5) = contiguous; larger = a
-                                 // strided sample, used by the autotuner)
+  uint64_t hi_step;              // warp slot stride (1 = contiguous walk;
+                                 // > 1 = the autotuner's spread sample)
   uint32_t e_mode;               // 0 dense, 1 parity planes
   uint32_t e_parity;             // constant part of the e parity
   uint32_t row_words, e_words, plane_words;  // layout (words)

@@ -29,7 +29,7 @@ __device__ __forceinline__ void isd_red_shared_inc(unsigned int addr) {
 template <int NC, bool DOUBLE, class T>
 __device__ __forceinline__ void k1_hoisted_body(
     const T& L, unsigned long long run_begin, unsigned long long nruns,
-    unsigned long long block_stride, unsigned int ls, unsigned int* hist,
+    unsigned long long hi_step, unsigned int ls, unsigned int* hist,
     unsigned long long* __restrict__ out) {
   // ---- zero the block's histograms ----
   {
@@ -51,14 +51,13 @@ __device__ __forceinline__ void k1_hoisted_body(
            (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
        t < nruns; t += gstride) {
     // lane bits of t go to run bits [ls, ls+5): which five sites the 32
-    // lanes of a warp differ in (shared-memory bank spread); blocks of
-    // 2^(ls+5) runs are block_stride apart (contiguous in a normal walk)
-    const unsigned long long hi = t >> 5;
-    const unsigned long long perm = ((hi >> ls) << (ls + 5)) |
-                                    ((t & 31) << ls) |
-                                    (hi & ((1ull << ls) - 1));
-    const unsigned long long r = run_begin + (perm & ((32ull << ls) - 1)) +
-                                 (perm >> (ls + 5)) * block_stride;
+    // lanes of a warp differ in (shared-memory bank spread).  Warp w covers
+    // the warp slot w * hi_step (1 in a walk; > 1 when the autotuner times
+    // a sample of warps spread over the whole range).
+    const unsigned long long hi = (t >> 5) * hi_step;
+    const unsigned long long r = run_begin + (((hi >> ls) << (ls + 5)) |
+                                              ((t & 31) << ls) |
+                                              (hi & ((1ull << ls) - 1)));
     // ---- per-run constants (bits [k, N) fixed) ----
     const unsigned long long xt = r << L.k();
     const int m_run = __popcll(xt);

@@ -424,7 +424,7 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
                                       2 * (int)info->e_words
                                 : 0;
   p->lane_shift = info->lane_shift;
-  p->block_stride = 32ull << info->lane_shift;
+  p->hi_step = 1;
   p->hist_words = hist_words_for(info->hist_words);
   p->n_hist = (uint32_t)hist_count_for(p->hist_words);
   const uint64_t loop = info->loop_mask;
