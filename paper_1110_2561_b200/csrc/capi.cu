@@ -195,7 +195,10 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     const uint64_t slots = body / 32;  // warp slots in the body
     // warp slots must stay inside whole lane blocks of the body
     const uint64_t usable = (body / blk) * (blk / 32);
+    // odd stride: a power-of-two stride would pin the low run bits of every
+    // sampled warp to zero and bias the sample
     hp.hi_step = usable / warps;
+    if (hp.hi_step > 1 && !(hp.hi_step & 1)) hp.hi_step -= 1;
     if (hp.hi_step < 1) hp.hi_step = 1;
     (void)slots;
     hp.run_begin = run0;
