@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <string>
@@ -112,9 +113,11 @@ static int current_sm_count(int* sms) {
 // Plans are compiled once per (lattice, loop width): the layout search
 // replays a sample of warp instructions and costs tens of milliseconds.
 // The model ranks every layout; before the first walk of >= 2^33
-// configurations the best 40 are timed on the GPU on a strided 2^33
-// sample of the range and the fastest is kept (autotune, once per process,
-// lattice and loop width; ISD_AUTOTUNE=0 disables).
+// configurations the best 40 are timed on the GPU on a 2^33-configuration
+// sample of warps spread over the range, and the best 6 of those on a
+// contiguous slice of up to 2^36 configurations; the fastest is kept
+// (autotune, once per process, lattice and loop width; ISD_AUTOTUNE=0
+// disables).
 struct PlanEntry {
   int rc = 0;
   isd_plan_info info;
@@ -148,6 +151,8 @@ static int cached_plan(const isd_lattice* lat, uint64_t hint,
 
 static constexpr int kTuneCandidates = 40;
 static constexpr uint64_t kTuneConfigs = 1ull << 33;
+static constexpr size_t kTuneFinalists = 6;
+static constexpr uint64_t kTuneSliceConfigs = 1ull << 36;
 
 // Time the model's best layouts on `st` and keep the fastest.  Synchronous.
 static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
@@ -183,16 +188,14 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   // with the candidate's own lane placement, so every region of the index
   // space votes and all candidates see the same spread
   const uint64_t runs = kTuneConfigs >> cands[0].k;
-  float best_ms = 1e30f;
-  size_t best = 0;
+  const uint64_t body = run1 - run0;
+  std::vector<std::pair<float, size_t>> stage1;
   for (size_t i = 0; i < cands.size(); ++i) {
     HoistParams hp;
     fill_hoist(lat, &cands[i], &hp);
-    const uint64_t body = run1 - run0;
     const uint64_t blk = 32ull << hp.lane_shift;
     if (body < blk || body < runs) continue;
     const uint64_t warps = runs / 32;
-    const uint64_t slots = body / 32;  // warp slots in the body
     // warp slots must stay inside whole lane blocks of the body
     const uint64_t usable = (body / blk) * (blk / 32);
     // odd stride: a power-of-two stride would pin the low run bits of every
@@ -200,7 +203,6 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     hp.hi_step = usable / warps;
     if (hp.hi_step > 1 && !(hp.hi_step & 1)) hp.hi_step -= 1;
     if (hp.hi_step < 1) hp.hi_step = 1;
-    (void)slots;
     hp.run_begin = run0;
     hp.run_end = run0 + warps * 32;
     float ms = 0.f;
@@ -212,7 +214,35 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     bump_launches(2);
-    ms /= (float)(warps * 32);  // per run
+    stage1.push_back({ms / (float)(warps * 32), i});  // per run
+  }
+  // stage 2: the best few, timed as a real walk — one contiguous slice of
+  // up to 2^36 configurations from the middle of the range (the spread
+  // sample ranks the candidates but not reliably enough to pick one)
+  std::sort(stage1.begin(), stage1.end());
+  float best_ms = 1e30f;
+  size_t best = stage1.empty() ? 0 : stage1[0].second;
+  for (size_t s2 = 0; s2 < stage1.size() && s2 < kTuneFinalists; ++s2) {
+    const size_t i = stage1[s2].second;
+    HoistParams hp;
+    fill_hoist(lat, &cands[i], &hp);
+    const uint64_t blk = 32ull << hp.lane_shift;
+    uint64_t len = (kTuneSliceConfigs >> hp.k);
+    if (len > body) len = body;
+    len = (len / blk) * blk;
+    if (len == 0) continue;
+    const uint64_t off = ((body - len) / 2 / blk) * blk;
+    hp.run_begin = run0 + off;
+    hp.run_end = hp.run_begin + len;
+    hp.hi_step = 1;
+    float ms = 0.f;
+    cudaEventRecord(e0, st);
+    launch_hoisted(hp, scratch, sms, st);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    bump_launches(1);
+    ms /= (float)len;
     if (ms < best_ms) {
       best_ms = ms;
       best = i;
