@@ -196,7 +196,9 @@ class ClockSampler:
 def ncu_traffic(config):
     """dram read+write bytes per launch of k1_hoisted from the committed
     ncu --set full capture (profiles/r1_ncu_k1_hoisted_<config>.txt)."""
-    path = os.path.join(ROOT, "profiles", f"r1_ncu_k1_hoisted_{config}.txt")
+    path = os.path.join(ROOT, "profiles", f"r1_ncu_k1_jit_{config}.txt")
+    if not os.path.exists(path):
+        path = os.path.join(ROOT, "profiles", f"r1_ncu_k1_hoisted_{config}.txt")
     if not os.path.exists(path):
         return None
     total = 0.0
@@ -208,7 +210,7 @@ def ncu_traffic(config):
     return total
 
 
-def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1):
+def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1, kernel="k1"):
     """Two rooflines for the dominant kernel (k1_hoisted).
 
     `roofline`: the pipe the kernel is bound by (ncu: shared-memory
@@ -237,11 +239,11 @@ def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1):
         "bound": "smem-atomic", "achieved": ach / 1e9, "peak": peak_red / 1e9,
         "unit": "Gconf/s", "frac": ach / peak_red,
         "traffic": ncu_traffic(wl.name),
-        "kernel": "k1_hoisted", "kernel_ms": ms_k1,
+        "kernel": kernel, "kernel_ms": ms_k1,
         "algorithmic_work": "1 RED.shared lane per configuration",
         "peak_source": f"K0 red_shared_spread {p_red:.2f} lanes/clk/SM x "
                        f"{sm_count} SMs x {mhz:.0f} MHz (measured, this GPU)",
-        "traffic_source": "ncu --set full, profiles/r1_ncu_k1_hoisted_*.txt",
+        "traffic_source": "ncu --set full, profiles/r1_ncu_k1_*_<config>.txt",
     }
     popc_ops, alu_ops = canonical_ops(wl.spec)
     p_popc = cal["popc"]["lanes_per_clk_sm"]
@@ -359,6 +361,7 @@ def run_b200(args, wl):
     clocks.start()
     tot, k1, launches, table, out = time_device(wl, args.steps, args.warmup)
     clk = clocks.stop()
+    kernel_path = _native.kernel_info()
 
     ms_step = max_over_ranks(sum(tot) / len(tot))
     ms_k1 = max_over_ranks(sum(k1) / len(k1))
@@ -432,7 +435,8 @@ def run_b200(args, wl):
 
     # ---- roofline ------------------------------------------------------------
     sm_count = _native.sm_count(local)
-    roof, roof_int = roofline(wl, cal, clk, sm_count, n_cfg // world, ms_k1)
+    roof, roof_int = roofline(wl, cal, clk, sm_count, n_cfg // world, ms_k1,
+                              kernel_path)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
