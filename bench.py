@@ -277,19 +277,22 @@ def run_b200(args, wl):
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     isd.set_device(local)
-    if world > 1:
+    # ISD_BENCH_FORCE_DIST=1 runs the NCCL code path even at world size 1
+    # (how the single-GPU pool exercises the multi-GPU step)
+    use_dist = world > 1 or os.environ.get("ISD_BENCH_FORCE_DIST") == "1"
+    if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
     def max_over_ranks(x):
-        if world == 1:
+        if not use_dist:
             return x
         t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -316,7 +319,7 @@ def run_b200(args, wl):
                                           shard.end_index, table.data_ptr(),
                                           sp, accumulate=False, algo=algo)
             ev[1].record(stream)
-            if world > 1:
+            if use_dist:
                 dist.reduce(table, dst=0)
             if rank == 0:
                 nl += _native.thermo_device(
@@ -379,7 +382,7 @@ def run_b200(args, wl):
     def e2e_step():
         shard = isd.make_shards(wl.spec, world)[rank]
         part = isd.enumerate_shard(wl.spec, None, shard)
-        if world > 1:
+        if use_dist:
             t = torch.from_numpy(part.counts).to(dev)
             dist.reduce(t, dst=0)
             counts = t.cpu().numpy() if rank == 0 else None
@@ -404,9 +407,9 @@ def run_b200(args, wl):
     table_bytes = (wl.spec.num_spins + 1) * (wl.spec.num_bonds + 1) * 8
     npts = len(wl.fields) * len(wl.temps)
     lat_bytes = 208  # sizeof(isd_lattice), passed by value to the kernels
-    h2d = lat_bytes + (table_bytes if world > 1 else 0) + \
+    h2d = lat_bytes + (table_bytes if use_dist else 0) + \
         (table_bytes + 8 * (len(wl.fields) + len(wl.temps)) if rank == 0 else 0)
-    d2h = table_bytes + (table_bytes if world > 1 and rank == 0 else 0) + \
+    d2h = table_bytes + (table_bytes if use_dist and rank == 0 else 0) + \
         (npts * 7 * 8 if rank == 0 else 0)
 
     # ---- other configs (value only, same protocol, fewer steps) -----------
@@ -428,7 +431,7 @@ def run_b200(args, wl):
                 "evaluated_configs_per_s": (n_cfg // 2) / (ms3 / 1e3),
                 "ms_per_step": ms3, "table_identical": same}
 
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
     if rank != 0:
         return 0
