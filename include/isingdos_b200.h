@@ -157,8 +157,8 @@ typedef struct isd_plan_info {
   uint32_t e_words;
   uint32_t plane_words;
   uint32_t hist_words;       /* words spanned by one histogram          */
-  uint32_t lane_shift;       /* warp lanes differ in run bits [s, s+5)  */
-  uint32_t reserved;
+  uint64_t lane_mask;        /* the 5 run bits the 32 lanes of a warp
+                                differ in (bit i = run bit i)           */
   double   est_wavefronts;   /* predicted smem wavefronts per warp RED  */
 } isd_plan_info;
 

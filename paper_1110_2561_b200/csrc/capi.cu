@@ -193,7 +193,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   for (size_t i = 0; i < cands.size(); ++i) {
     HoistParams hp;
     fill_hoist(lat, &cands[i], &hp);
-    const uint64_t blk = 32ull << hp.lane_shift;
+    const uint64_t blk = 1ull << lane_span(hp.lane_mask);
     if (body < blk || body < runs) continue;
     const uint64_t warps = runs / 32;
     // warp slots must stay inside whole lane blocks of the body
@@ -226,7 +226,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     const size_t i = stage1[s2].second;
     HoistParams hp;
     fill_hoist(lat, &cands[i], &hp);
-    const uint64_t blk = 32ull << hp.lane_shift;
+    const uint64_t blk = 1ull << lane_span(hp.lane_mask);
     uint64_t len = (kTuneSliceConfigs >> hp.k);
     if (len > body) len = body;
     len = (len / blk) * blk;
@@ -368,14 +368,17 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
   }
   if (end - start >= kTuneConfigs)
     autotune(lat, end - start, r0, r1, sms, st, &info);
-  // experiment knob: ISD_LAYOUT="A,B,P,ls" forces the histogram layout
+  // experiment knob: ISD_LAYOUT="A,B,P,ls[,lanemask_hex]" forces the
+  // histogram layout and lane placement (window at ls, or the mask)
   if (const char* lay = std::getenv("ISD_LAYOUT")) {
     unsigned a = 0, b = 0, pw = 0, ls = 0;
-    if (std::sscanf(lay, "%u,%u,%u,%u", &a, &b, &pw, &ls) == 4 && a && b) {
+    unsigned long long mask = 0;
+    const int got = std::sscanf(lay, "%u,%u,%u,%u,%llx", &a, &b, &pw, &ls, &mask);
+    if (got >= 4 && a && b) {
       info.row_words = a;
       info.e_words = b;
       info.plane_words = pw;
-      info.lane_shift = ls;
+      info.lane_mask = (got == 5 && mask) ? mask : (0x1Full << ls);
       info.hist_words = lat->n_spins * a + lat->n_bonds * b + pw + 1;
     }
   }
@@ -389,15 +392,11 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     const uint64_t re = (r1 - r > runs_per_launch) ? r + runs_per_launch : r1;
     hp.run_begin = r;
     hp.run_end = re;
-    // lane placement (from the plan, or forced for experiments) needs a run
-    // count divisible by 2^(shift+5)
-    {
-      const long ls = env_long("ISD_LANE_SHIFT", (long)info.lane_shift);
-      hp.lane_shift = 0;
-      if (ls > 0 && ls < 40 && ((re - r) & ((1ull << (ls + 5)) - 1)) == 0)
-        hp.lane_shift = (uint32_t)ls;
-      hp.hi_step = 1;
-    }
+    // the plan's lane placement tiles the launch only if its run count is a
+    // multiple of 2^lane_span; otherwise lanes take the lowest 5 run bits
+    hp.lane_mask = info.lane_mask;
+    if ((re - r) & ((1ull << lane_span(hp.lane_mask)) - 1)) hp.lane_mask = 0x1F;
+    hp.hi_step = 1;
     int x = 0;
     if (use_jit) {
       std::string why;

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(kThreads)
   extern __shared__ __align__(16) uint32_t hist[];
   const RuntimeTraits L{P};
   k1_hoisted_body<NC, DOUBLE>(L, P.run_begin, P.run_end - P.run_begin,
-                              P.hi_step, P.lane_shift, hist, out);
+                              P.hi_step, P.lane_mask, hist, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -29,7 +29,8 @@ __device__ __forceinline__ void isd_red_shared_inc(unsigned int addr) {
 template <int NC, bool DOUBLE, class T>
 __device__ __forceinline__ void k1_hoisted_body(
     const T& L, unsigned long long run_begin, unsigned long long nruns,
-    unsigned long long hi_step, unsigned int ls, unsigned int* hist,
+    unsigned long long hi_step, unsigned long long lane_mask,
+    unsigned int* hist,
     unsigned long long* __restrict__ out) {
   // ---- zero the block's histograms ----
   {
@@ -46,18 +47,38 @@ __device__ __forceinline__ void k1_hoisted_body(
   const unsigned long long gstride = (unsigned long long)gridDim.x * blockDim.x;
   const unsigned int nloop = L.nloop();
   const unsigned long long above_k = L.above_k();
+  // this lane's five run bits, deposited into lane_mask
+  unsigned long long lane_dep = 0;
+  {
+    const unsigned int lane = threadIdx.x & 31;
+    unsigned long long m = lane_mask;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const unsigned long long low = m & (~m + 1);
+      if ((lane >> i) & 1) lane_dep |= low;
+      m ^= low;
+    }
+  }
 
   for (unsigned long long t =
            (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
        t < nruns; t += gstride) {
-    // lane bits of t go to run bits [ls, ls+5): which five sites the 32
-    // lanes of a warp differ in (shared-memory bank spread).  Warp w covers
-    // the warp slot w * hi_step (1 in a walk; > 1 when the autotuner times
-    // a sample of warps spread over the whole range).
-    const unsigned long long hi = (t >> 5) * hi_step;
-    const unsigned long long r = run_begin + (((hi >> ls) << (ls + 5)) |
-                                              ((t & 31) << ls) |
-                                              (hi & ((1ull << ls) - 1)));
+    // The 32 lanes of a warp differ in the five run bits of lane_mask
+    // (which sites they differ in sets the shared-memory bank spread); the
+    // warp's slot spreads over the other run bits.  Warp w takes slot
+    // w * hi_step (1 in a walk; > 1 when the autotuner times a sample of
+    // warps spread over the whole range).
+    unsigned long long hi = (t >> 5) * hi_step;
+    {
+      unsigned long long m = lane_mask;
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {  // insert a 0 at each lane bit
+        const unsigned long long low = m & (~m + 1);
+        hi = ((hi & ~(low - 1)) << 1) | (hi & (low - 1));
+        m ^= low;
+      }
+    }
+    const unsigned long long r = run_begin + (hi | lane_dep);
     // ---- per-run constants (bits [k, N) fixed) ----
     const unsigned long long xt = r << L.k();
     const int m_run = __popcll(xt);

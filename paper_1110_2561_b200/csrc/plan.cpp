@@ -105,19 +105,51 @@ struct Bin {
 };
 }  // namespace
 
+int lane_span(uint64_t lane_mask) {
+  return lane_mask ? 64 - __builtin_clzll(lane_mask) : 0;
+}
+
+// Candidate lane masks: contiguous windows of 5 run bits, plus (for large
+// walks) random 5-subsets, half of them drawn from run sites of even degree
+// (flipping those keeps the e parity of the 32 lanes equal).
+static void lane_candidates(const isd_plan_info* info, int run_bits,
+                            bool wide, std::vector<uint64_t>* out) {
+  static const int shifts[] = {0, 3, 6, 9, 12, 15};
+  for (int ls : shifts)
+    if (run_bits >= ls + 5) out->push_back(0x1Full << ls);
+  if (!wide || run_bits < 6) return;
+  std::vector<int> even, all;
+  for (int bit = 0; bit < run_bits; ++bit) {
+    all.push_back(bit);
+    if (!((info->odd_mask >> (bit + info->k)) & 1)) even.push_back(bit);
+  }
+  uint64_t seed = 0xD1B54A32D192ED03ull;
+  for (int pool = 0; pool < 2; ++pool) {
+    const std::vector<int>& src = pool == 0 ? even : all;
+    if ((int)src.size() < 5) continue;
+    for (int r = 0; r < 24; ++r) {
+      uint64_t m = 0;
+      while (__builtin_popcountll(m) < 5)
+        m |= 1ull << src[rng_next(&seed) % src.size()];
+      if (std::find(out->begin(), out->end(), m) == out->end())
+        out->push_back(m);
+    }
+  }
+}
+
 static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
-                          std::vector<isd_plan_info>* ranked) {
+                          std::vector<isd_plan_info>* ranked, bool wide) {
   const int n = (int)lat->n_spins;
   const int k = (int)info->k;
   const int b = (int)lat->n_bonds;
   const int emax_half = b / 2;  // largest (e - par)/2
-  info->lane_shift = 0;
+  info->lane_mask = 0x1F;
   info->est_wavefronts = 0;
   // candidate layouts (row_words A, e_words B, plane_words P)
   struct Cand {
     int a, b, p, span;
   };
-  static Cand cand[512];
+  static thread_local Cand cand[512];
   int nc = 0;
   if (info->e_mode == 0) {
     for (int t = 0; t < 40; ++t) cand[nc++] = {b + 1 + t, 1, 0, n * (b + 1 + t) + b + 1};
@@ -150,18 +182,20 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
     if (ranked) ranked->push_back(*info);
     return;
   }
+  std::vector<uint64_t> masks;
+  lane_candidates(info, run_bits, wide, &masks);
 
   constexpr int kWarps = 160, kCopySample = 8;
-  static const int shifts[] = {0, 3, 6, 9, 12, 15};
-  static double cost[512];
+  std::vector<double> cost(nc);
   double best = 1e30;
-  for (int ls : shifts) {
-    if (run_bits < ls + 5) continue;
-    for (int ci = 0; ci < nc; ++ci) cost[ci] = 0;
-    uint64_t seed = 0x9E3779B97F4A7C15ull ^ (uint64_t)(ls + 1);
-    const uint64_t hi_count = 1ull << (run_bits - 5);
+  for (const uint64_t lane_mask : masks) {
+    std::fill(cost.begin(), cost.end(), 0.0);
+    uint64_t seed = 0x9E3779B97F4A7C15ull ^ lane_mask;
+    const uint64_t free_mask = ((1ull << run_bits) - 1) & ~lane_mask;
+    uint64_t lane_dep[32];
+    for (int lane = 0; lane < 32; ++lane) lane_dep[lane] = deposit(lane, lane_mask);
     for (int w = 0; w < kWarps; ++w) {
-      const uint64_t hi = rng_next(&seed) % hi_count;
+      const uint64_t hi = deposit(rng_next(&seed), free_mask);
       const uint64_t jb = deposit(rng_next(&seed), info->loop_mask);
       for (int cs = 0; cs < kCopySample; ++cs) {
         uint64_t cbits = 0;
@@ -171,8 +205,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
         Bin bins[32];
         int nb = 0;
         for (int lane = 0; lane < 32; ++lane) {
-          const uint64_t r = ((hi >> ls) << (ls + 5)) | ((uint64_t)lane << ls) |
-                             (hi & ((1ull << ls) - 1));
+          const uint64_t r = hi | lane_dep[lane];
           const uint64_t x = (r << k) | jb | cbits;
           int e = 0;
           for (uint32_t q = 0; q < lat->n_classes; ++q) {
@@ -210,7 +243,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
       alt.e_words = (uint32_t)cand[ci].b;
       alt.plane_words = (uint32_t)cand[ci].p;
       alt.hist_words = (uint32_t)cand[ci].span;
-      alt.lane_shift = (uint32_t)ls;
+      alt.lane_mask = lane_mask;
       alt.est_wavefronts = cst;
       if (ranked) ranked->push_back(alt);
       if (cst < best - 1e-9) {
@@ -367,7 +400,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
         continue;  // identical to variant 0
       set_copy_sites(lat, &cand, low_sites, low_even ? 1 : 0);
     }
-    choose_layout(lat, &cand, &all);
+    choose_layout(lat, &cand, &all, n_configs_hint >= (1ull << 33));
     if (!have || cand.est_wavefronts < best_info.est_wavefronts - 1e-9) {
       best_info = cand;
       have = true;
@@ -380,6 +413,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
                      [](const isd_plan_info& a, const isd_plan_info& b) {
                        return a.est_wavefronts < b.est_wavefronts;
                      });
+    if (all.size() > 256) all.resize(256);
     ranked->assign(all.begin(), all.end());
   }
   return 0;
@@ -423,7 +457,7 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
   p->plane_bytes = info->e_mode ? 4 * (int)info->plane_words -
                                       2 * (int)info->e_words
                                 : 0;
-  p->lane_shift = info->lane_shift;
+  p->lane_mask = info->lane_mask;
   p->hi_step = 1;
   p->hist_words = hist_words_for(info->hist_words);
   p->n_hist = (uint32_t)hist_count_for(p->hist_words);

@@ -48,7 +48,7 @@ def main():
     ok, info = _native.plan(native_lattice(spec), sh.size)
     print(f"  plan: mode={info.e_mode} sites={list(info.copy_site)} "
           f"A,B,P={info.row_words},{info.e_words},{info.plane_words} "
-          f"lane_shift={info.lane_shift} est={info.est_wavefronts:.3f}")
+          f"lane_mask={info.lane_mask:#x} est={info.est_wavefronts:.3f}")
     return 0
 
 
