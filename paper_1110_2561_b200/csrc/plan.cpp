@@ -185,16 +185,20 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   std::vector<uint64_t> masks;
   lane_candidates(info, run_bits, wide, &masks);
 
-  constexpr int kWarps = 160, kCopySample = 8;
+  // Score one lane mask against every layout on `warps` sampled warp
+  // instructions x kCopySample copies; returns its best cost and, if
+  // `emit`, appends every (layout, mask) alternative to `ranked`.
+  constexpr int kWarps = 160, kScreenWarps = 40, kCopySample = 8;
   std::vector<double> cost(nc);
   double best = 1e30;
-  for (const uint64_t lane_mask : masks) {
+  isd_plan_info best_alt_ = *info;
+  auto evaluate = [&](uint64_t lane_mask, int warps, bool emit) {
     std::fill(cost.begin(), cost.end(), 0.0);
     uint64_t seed = 0x9E3779B97F4A7C15ull ^ lane_mask;
     const uint64_t free_mask = ((1ull << run_bits) - 1) & ~lane_mask;
     uint64_t lane_dep[32];
     for (int lane = 0; lane < 32; ++lane) lane_dep[lane] = deposit(lane, lane_mask);
-    for (int w = 0; w < kWarps; ++w) {
+    for (int w = 0; w < warps; ++w) {
       const uint64_t hi = deposit(rng_next(&seed), free_mask);
       const uint64_t jb = deposit(rng_next(&seed), info->loop_mask);
       for (int cs = 0; cs < kCopySample; ++cs) {
@@ -236,8 +240,11 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
         }
       }
     }
+    double mask_best = 1e30;
     for (int ci = 0; ci < nc; ++ci) {
-      const double cst = cost[ci] / (kWarps * kCopySample);
+      const double cst = cost[ci] / (warps * kCopySample);
+      mask_best = std::min(mask_best, cst);
+      if (!emit) continue;
       isd_plan_info alt = *info;
       alt.row_words = (uint32_t)cand[ci].a;
       alt.e_words = (uint32_t)cand[ci].b;
@@ -248,10 +255,22 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
       if (ranked) ranked->push_back(alt);
       if (cst < best - 1e-9) {
         best = cst;
-        *info = alt;
+        best_alt_ = alt;
       }
     }
+    return mask_best;
+  };
+  // screen every mask on a quarter of the sample, then score the best 8
+  // in full
+  std::vector<std::pair<double, uint64_t>> screen;
+  if (masks.size() > 8) {
+    for (const uint64_t m : masks) screen.push_back({evaluate(m, kScreenWarps, false), m});
+    std::sort(screen.begin(), screen.end());
+    masks.clear();
+    for (size_t i = 0; i < screen.size() && i < 8; ++i) masks.push_back(screen[i].second);
   }
+  for (const uint64_t m : masks) evaluate(m, kWarps, true);
+  if (best < 1e29) *info = best_alt_;
 }
 
 // Hoisted split: 7 copy sites and l loop sites inside the low k bits, the
