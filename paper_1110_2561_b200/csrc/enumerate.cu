@@ -13,13 +13,14 @@
 //
 //  * k1_hoisted: every configuration is still counted individually, but the
 //    work that does not change between neighbouring indices is hoisted:
-//    bits [k, N) are fixed per thread ("run"), bits [u, k) are the thread's
-//    loop counter, and the low u = 5 bits are 32 register copies.  Per group
-//    of 32 copies the kernel evaluates the loop-dependent bonds with
-//    LOP3/POPC over precomputed masks, derives each copy site's flip cost
-//    delta_p = d_p - 2 n_p, and then produces each copy's bin address with a
-//    single IADD3 (subset sum over the copy bits plus a per-lattice
-//    constant-bank table) followed by one shared-memory reduction.
+//    bits [k, N) are fixed per thread ("run"), the loop sites of [0, k) are
+//    the thread's loop, and 7 copy sites of [0, k) are 128 register copies.
+//    Per group of 128 copies the kernel evaluates the loop-dependent bonds
+//    with LOP3/POPC over precomputed masks and derives each copy site's
+//    flip cost delta_q = d_q - 2 n_q; each copy's histogram address is then
+//    one add (subset sum over the copy bits) plus a per-lattice constant
+//    offset folded into the shared-memory reduction.  The body lives in
+//    k1_body.cuh and is also compiled per lattice with NVRTC (jit.cpp).
 //
 // Counts go to shared-memory u32 histograms (one per group of warps),
 // flushed once per block into the per-GPU uint64 table with 64-bit global
