@@ -7,10 +7,13 @@
 //   U = p.H,  <M> = p.M,  C = p.(H-U)^2 / T^2,  chi = p.(M-<M>)^2 / T
 // plus the extension <|M|> = p.|M| (BASELINE configs 2 and 5).
 //
-// One CTA per (h, T) point.  Each thread walks a fixed strided subset of the
-// table and the partial sums are combined by a fixed shared-memory tree, so
-// a point's result does not depend on which other points share the launch
-// (thermo_sweep(...)[0] == partition_point(...) exactly, test_thermo.py:85-87).
+// One warp per (h, T) point, eight points per CTA.  The CTA first compacts
+// the occupied cells of the table into shared memory, in table order (a
+// block prefix scan), so every warp walks the same cell list; each lane
+// takes a fixed strided subset and the partials meet in a fixed xor-shuffle
+// tree.  A point's result therefore does not depend on which other points
+// share the launch (thermo_sweep(...)[0] == partition_point(...) exactly,
+// test_thermo.py:85-87).
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -18,116 +21,133 @@
 
 namespace isd {
 
-constexpr int kThermoThreads = 256;
+constexpr int kThermoThreads = 256;                 // 8 warps = 8 points
+constexpr int kThermoPoints = kThermoThreads / 32;
+constexpr int kMaxBins = (ISD_MAX_SPINS + 1) * (3 * ISD_MAX_SPINS + 1);
 
-template <int K>
-__device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
-  // red: K * kThermoThreads doubles
+struct Cell {
+  double g;  // count (exact in fp64 below 2^53)
+  float m;   // M = 2 m_idx - N
+  int e;     // 2 e_idx - B (E = e * |J|)
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
-  for (int i = 0; i < K; ++i) red[i * kThermoThreads + threadIdx.x] = v[i];
-  __syncthreads();
-  for (int w = kThermoThreads / 2; w > 0; w >>= 1) {
-    if ((int)threadIdx.x < w) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
-      for (int i = 0; i < K; ++i)
-        red[i * kThermoThreads + threadIdx.x] +=
-            red[i * kThermoThreads + threadIdx.x + w];
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < K; ++i) v[i] = red[i * kThermoThreads];
-  __syncthreads();
+  for (int o = 16; o > 0; o >>= 1)
+    v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
 }
 
 __global__ void __launch_bounds__(kThermoThreads)
     k2_thermo(const unsigned long long* __restrict__ counts, uint32_t n,
               uint32_t b, double scale, const double* __restrict__ fields,
-              const double* __restrict__ temps, int n_temps,
+              const double* __restrict__ temps, int n_temps, int n_points,
               double* __restrict__ out) {
-  __shared__ double red[3 * kThermoThreads];
-  const int point = blockIdx.x;
-  const double h = fields[point / n_temps];
-  const double t = temps[point % n_temps];
+  extern __shared__ __align__(16) unsigned char smem[];
+  Cell* cells = reinterpret_cast<Cell*>(smem);
+  __shared__ int scan[kThermoThreads];
+  __shared__ int n_cells;
   const uint32_t stride = b + 1;
   const uint32_t nbins = (n + 1) * stride;
 
-  // pass 1: shift = max x over occupied cells
-  double xmax = -INFINITY;
-  for (uint32_t i = threadIdx.x; i < nbins; i += kThermoThreads) {
-    if (counts[i] == 0) continue;
-    const double m = (double)(2 * (int)(i / stride) - (int)n);
-    const double e = (double)(2 * (int)(i % stride) - (int)b) * scale;
-    const double en = e - h * m;
-    const double x = -en / t;
-    xmax = fmax(xmax, x);
-  }
-  red[threadIdx.x] = xmax;
+  // ---- compact the occupied cells, in table order ----
+  const uint32_t per = (nbins + kThermoThreads - 1) / kThermoThreads;
+  const uint32_t lo = threadIdx.x * per;
+  const uint32_t hi = min(lo + per, nbins);
+  int mine = 0;
+  for (uint32_t i = lo; i < hi; ++i) mine += counts[i] != 0;
+  scan[threadIdx.x] = mine;
   __syncthreads();
-  for (int w = kThermoThreads / 2; w > 0; w >>= 1) {
-    if ((int)threadIdx.x < w)
-      red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+  for (int o = 1; o < kThermoThreads; o <<= 1) {  // inclusive scan
+    const int v = (int)threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
+    __syncthreads();
+    scan[threadIdx.x] += v;
     __syncthreads();
   }
-  const double shift = red[0];
+  int pos = scan[threadIdx.x] - mine;
+  for (uint32_t i = lo; i < hi; ++i) {
+    const unsigned long long g = counts[i];
+    if (!g) continue;
+    const int mi = (int)(i / stride), ei = (int)(i - mi * stride);
+    cells[pos].g = (double)g;
+    cells[pos].m = (float)(2 * mi - (int)n);
+    cells[pos].e = 2 * ei - (int)b;
+    ++pos;
+  }
+  if (threadIdx.x == kThermoThreads - 1) n_cells = scan[threadIdx.x];
   __syncthreads();
+  const int nc = n_cells;
+
+  const int point = blockIdx.x * kThermoPoints + (threadIdx.x >> 5);
+  if (point >= n_points) return;
+  const int lane = threadIdx.x & 31;
+  const double h = fields[point / n_temps];
+  const double t = temps[point % n_temps];
+
+  // pass 1: shift = max x over occupied cells
+  double xmax = -INFINITY;
+  for (int i = lane; i < nc; i += 32) {
+    const double m = (double)cells[i].m;
+    const double e = (double)cells[i].e * scale;
+    const double en = e - h * m;
+    xmax = fmax(xmax, -en / t);
+  }
+  const double shift = warp_max(xmax);
 
   // pass 2: s = sum g exp(x - shift)
-  double v1[1] = {0.0};
-  for (uint32_t i = threadIdx.x; i < nbins; i += kThermoThreads) {
-    const unsigned long long g = counts[i];
-    if (g == 0) continue;
-    const double m = (double)(2 * (int)(i / stride) - (int)n);
-    const double e = (double)(2 * (int)(i % stride) - (int)b) * scale;
+  double s = 0.0;
+  for (int i = lane; i < nc; i += 32) {
+    const double m = (double)cells[i].m;
+    const double e = (double)cells[i].e * scale;
     const double en = e - h * m;
-    const double x = -en / t;
-    v1[0] += (double)g * exp(x - shift);
+    s += cells[i].g * exp(-en / t - shift);
   }
-  block_sum<1>(v1, red);
-  const double s = v1[0];
+  s = warp_sum(s);
 
   // pass 3: first moments
-  double v3[3] = {0.0, 0.0, 0.0};
-  for (uint32_t i = threadIdx.x; i < nbins; i += kThermoThreads) {
-    const unsigned long long g = counts[i];
-    if (g == 0) continue;
-    const double m = (double)(2 * (int)(i / stride) - (int)n);
-    const double e = (double)(2 * (int)(i % stride) - (int)b) * scale;
+  double u = 0.0, mean_m = 0.0, mean_abs = 0.0;
+  for (int i = lane; i < nc; i += 32) {
+    const double m = (double)cells[i].m;
+    const double e = (double)cells[i].e * scale;
     const double en = e - h * m;
-    const double x = -en / t;
-    const double p = ((double)g * exp(x - shift)) / s;
-    v3[0] += p * en;
-    v3[1] += p * m;
-    v3[2] += p * fabs(m);
+    const double p = (cells[i].g * exp(-en / t - shift)) / s;
+    u += p * en;
+    mean_m += p * m;
+    mean_abs += p * fabs(m);
   }
-  block_sum<3>(v3, red);
-  const double u = v3[0], mean_m = v3[1], mean_abs = v3[2];
+  u = warp_sum(u);
+  mean_m = warp_sum(mean_m);
+  mean_abs = warp_sum(mean_abs);
 
   // pass 4: central second moments
-  double v2[2] = {0.0, 0.0};
-  for (uint32_t i = threadIdx.x; i < nbins; i += kThermoThreads) {
-    const unsigned long long g = counts[i];
-    if (g == 0) continue;
-    const double m = (double)(2 * (int)(i / stride) - (int)n);
-    const double e = (double)(2 * (int)(i % stride) - (int)b) * scale;
+  double ve = 0.0, vm = 0.0;
+  for (int i = lane; i < nc; i += 32) {
+    const double m = (double)cells[i].m;
+    const double e = (double)cells[i].e * scale;
     const double en = e - h * m;
-    const double x = -en / t;
-    const double p = ((double)g * exp(x - shift)) / s;
+    const double p = (cells[i].g * exp(-en / t - shift)) / s;
     const double de = en - u, dm = m - mean_m;
-    v2[0] += p * (de * de);
-    v2[1] += p * (dm * dm);
+    ve += p * (de * de);
+    vm += p * (dm * dm);
   }
-  block_sum<2>(v2, red);
+  ve = warp_sum(ve);
+  vm = warp_sum(vm);
 
-  if (threadIdx.x == 0) {
+  if (lane == 0) {
     const double log_z = shift + log(s);
     double* o = out + (size_t)point * ISD_THERMO_FIELDS;
     o[0] = log_z;
     o[1] = -t * log_z;
     o[2] = u;
-    o[3] = v2[0] / (t * t);
+    o[3] = ve / (t * t);
     o[4] = mean_m;
-    o[5] = v2[1] / t;
+    o[5] = vm / t;
     o[6] = mean_abs;
   }
 }
@@ -138,8 +158,13 @@ int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
                   void* stream) {
   const int points = n_fields * n_temps;
   if (points <= 0) return 0;
-  k2_thermo<<<points, kThermoThreads, 0, (cudaStream_t)stream>>>(
-      counts, n_spins, n_bonds, scale, fields, temps, n_temps, out);
+  const size_t smem = sizeof(Cell) * (size_t)(n_spins + 1) * (n_bonds + 1);
+  static_assert(sizeof(Cell) * kMaxBins <= 227 * 1024, "cell list fits");
+  cudaFuncSetAttribute((const void*)k2_thermo,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = (points + kThermoPoints - 1) / kThermoPoints;
+  k2_thermo<<<grid, kThermoThreads, smem, (cudaStream_t)stream>>>(
+      counts, n_spins, n_bonds, scale, fields, temps, n_temps, points, out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 1 : -(int)e;
 }
