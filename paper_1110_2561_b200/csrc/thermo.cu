@@ -7,7 +7,7 @@
 //   U = p.H,  <M> = p.M,  C = p.(H-U)^2 / T^2,  chi = p.(M-<M>)^2 / T
 // plus the extension <|M|> = p.|M| (BASELINE configs 2 and 5).
 //
-// One warp per (h, T) point, eight points per CTA.  The CTA first compacts
+// One warp per (h, T) point, four points per CTA.  The CTA first compacts
 // the occupied cells of the table into shared memory, in table order (a
 // block prefix scan), so every warp walks the same cell list; each lane
 // takes a fixed strided subset and the partials meet in a fixed xor-shuffle
@@ -21,7 +21,7 @@
 
 namespace isd {
 
-constexpr int kThermoThreads = 256;                 // 8 warps = 8 points
+constexpr int kThermoThreads = 128;                 // 4 warps = 4 points
 constexpr int kThermoPoints = kThermoThreads / 32;
 constexpr int kMaxBins = (ISD_MAX_SPINS + 1) * (3 * ISD_MAX_SPINS + 1);
 
@@ -100,15 +100,22 @@ __global__ void __launch_bounds__(kThermoThreads)
   }
   const double shift = warp_max(xmax);
 
-  // pass 2: s = sum g exp(x - shift)
-  double s = 0.0;
-  for (int i = lane; i < nc; i += 32) {
-    const double m = (double)cells[i].m;
-    const double e = (double)cells[i].e * scale;
-    const double en = e - h * m;
-    s += cells[i].g * exp(-en / t - shift);
+  // pass 2: s = sum g exp(x - shift).  Two accumulators per lane (cells
+  // i and i + 32 of each 64-cell stripe) for ILP; fixed combination order.
+  double s0 = 0.0, s1 = 0.0;
+  for (int i = lane; i < nc; i += 64) {
+    {
+      const double m = (double)cells[i].m;
+      const double e = (double)cells[i].e * scale;
+      s0 += cells[i].g * exp(-(e - h * m) / t - shift);
+    }
+    if (i + 32 < nc) {
+      const double m = (double)cells[i + 32].m;
+      const double e = (double)cells[i + 32].e * scale;
+      s1 += cells[i + 32].g * exp(-(e - h * m) / t - shift);
+    }
   }
-  s = warp_sum(s);
+  const double s = warp_sum(s0 + s1);
 
   // pass 3: first moments
   double u = 0.0, mean_m = 0.0, mean_abs = 0.0;
