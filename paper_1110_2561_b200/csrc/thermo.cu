@@ -7,9 +7,9 @@
 //   U = p.H,  <M> = p.M,  C = p.(H-U)^2 / T^2,  chi = p.(M-<M>)^2 / T
 // plus the extension <|M|> = p.|M| (BASELINE configs 2 and 5).
 //
-// One warp per (h, T) point, four points per CTA.  The CTA first compacts
-// the occupied cells of the table into shared memory, in table order (warp
-// ballots + a CTA prefix per chunk), so every warp walks the same cell list; each lane
+// One warp per (h, T) point, eight points per CTA.  The CTA first compacts
+// the occupied cells of the table into shared memory, in table order (a
+// block prefix scan), so every warp walks the same cell list; each lane
 // takes a fixed strided subset and the partials meet in a fixed xor-shuffle
 // tree.  A point's result therefore does not depend on which other points
 // share the launch (thermo_sweep(...)[0] == partition_point(...) exactly,
@@ -21,7 +21,7 @@
 
 namespace isd {
 
-constexpr int kThermoThreads = 128;                 // 4 warps = 4 points
+constexpr int kThermoThreads = 256;                 // 8 warps = 8 points
 constexpr int kThermoPoints = kThermoThreads / 32;
 constexpr int kMaxBins = (ISD_MAX_SPINS + 1) * (3 * ISD_MAX_SPINS + 1);
 
@@ -51,34 +51,38 @@ __global__ void __launch_bounds__(kThermoThreads)
               double* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem[];
   Cell* cells = reinterpret_cast<Cell*>(smem);
+  __shared__ int scan[kThermoThreads];
+  __shared__ int n_cells;
   const uint32_t stride = b + 1;
   const uint32_t nbins = (n + 1) * stride;
 
   // ---- compact the occupied cells, in table order ----
-  // chunks of kThermoThreads bins: coalesced loads, warp ballots for the
-  // in-warp prefix, per-warp totals for the CTA prefix
-  __shared__ int warp_tot[kThermoPoints];
-  const int lane_id = threadIdx.x & 31, warp_id = threadIdx.x >> 5;
-  int base = 0;
-  for (uint32_t c0 = 0; c0 < nbins; c0 += kThermoThreads) {
-    const uint32_t i = c0 + threadIdx.x;
-    const unsigned long long g = i < nbins ? counts[i] : 0ull;
-    const unsigned int ball = __ballot_sync(0xffffffffu, g != 0);
-    if (lane_id == 0) warp_tot[warp_id] = __popc(ball);
+  const uint32_t per = (nbins + kThermoThreads - 1) / kThermoThreads;
+  const uint32_t lo = threadIdx.x * per;
+  const uint32_t hi = min(lo + per, nbins);
+  int mine = 0;
+  for (uint32_t i = lo; i < hi; ++i) mine += counts[i] != 0;
+  scan[threadIdx.x] = mine;
+  __syncthreads();
+  for (int o = 1; o < kThermoThreads; o <<= 1) {  // inclusive scan
+    const int v = (int)threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
     __syncthreads();
-    int before = base;
-    for (int w = 0; w < warp_id; ++w) before += warp_tot[w];
-    if (g) {
-      const int pos = before + __popc(ball & ((1u << lane_id) - 1));
-      const int mi = (int)(i / stride), ei = (int)(i - mi * stride);
-      cells[pos].g = (double)g;
-      cells[pos].m = (float)(2 * mi - (int)n);
-      cells[pos].e = 2 * ei - (int)b;
-    }
-    for (int w = 0; w < kThermoPoints; ++w) base += warp_tot[w];
+    scan[threadIdx.x] += v;
     __syncthreads();
   }
-  const int nc = base;
+  int pos = scan[threadIdx.x] - mine;
+  for (uint32_t i = lo; i < hi; ++i) {
+    const unsigned long long g = counts[i];
+    if (!g) continue;
+    const int mi = (int)(i / stride), ei = (int)(i - mi * stride);
+    cells[pos].g = (double)g;
+    cells[pos].m = (float)(2 * mi - (int)n);
+    cells[pos].e = 2 * ei - (int)b;
+    ++pos;
+  }
+  if (threadIdx.x == kThermoThreads - 1) n_cells = scan[threadIdx.x];
+  __syncthreads();
+  const int nc = n_cells;
 
   const int point = blockIdx.x * kThermoPoints + (threadIdx.x >> 5);
   if (point >= n_points) return;
@@ -96,22 +100,15 @@ __global__ void __launch_bounds__(kThermoThreads)
   }
   const double shift = warp_max(xmax);
 
-  // pass 2: s = sum g exp(x - shift).  Two accumulators per lane (cells
-  // i and i + 32 of each 64-cell stripe) for ILP; fixed combination order.
-  double s0 = 0.0, s1 = 0.0;
-  for (int i = lane; i < nc; i += 64) {
-    {
-      const double m = (double)cells[i].m;
-      const double e = (double)cells[i].e * scale;
-      s0 += cells[i].g * exp(-(e - h * m) / t - shift);
-    }
-    if (i + 32 < nc) {
-      const double m = (double)cells[i + 32].m;
-      const double e = (double)cells[i + 32].e * scale;
-      s1 += cells[i + 32].g * exp(-(e - h * m) / t - shift);
-    }
+  // pass 2: s = sum g exp(x - shift)
+  double s = 0.0;
+  for (int i = lane; i < nc; i += 32) {
+    const double m = (double)cells[i].m;
+    const double e = (double)cells[i].e * scale;
+    const double en = e - h * m;
+    s += cells[i].g * exp(-en / t - shift);
   }
-  const double s = warp_sum(s0 + s1);
+  s = warp_sum(s);
 
   // pass 3: first moments
   double u = 0.0, mean_m = 0.0, mean_abs = 0.0;
