@@ -391,34 +391,68 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   info->odd_mask = odd;
   info->e_parity = (uint32_t)(neg & 1);
 
-  // copy sites: (a) the even-degree sites of [0, k) when there are 7 of
-  // them (then the e parity is constant over a group's copies: e_mode 1),
-  // (b) the lowest 7 sites (e_mode 1 only if every site has even degree).
-  // Both are laid out and the one with fewer predicted wavefronts wins.
-  int even_sites[kCopyBits];
-  int ne = 0;
-  for (int i = 0; i < k && ne < u; ++i)
-    if (!((odd >> i) & 1)) even_sites[ne++] = i;
-  int low_sites[kCopyBits];
-  for (int t = 0; t < u; ++t) low_sites[t] = t;
+  // copy sites, three candidate sets (each laid out; the one with fewer
+  // predicted wavefronts wins, and the autotuner re-times the best):
+  //   even   the first 7 even-degree sites of [0, k) — the e parity is then
+  //          constant over a group's copies (e_mode 1);
+  //   low    the lowest 7 sites (e_mode 1 only if every site is even);
+  //   spread (large walks) greedily mutually non-adjacent sites, even
+  //          degree first — fewer copy-copy bonds, different delta mix.
+  auto adjacent = [&](int a, int c) {
+    for (uint32_t q = 0; q < lat->n_classes; ++q) {
+      const isd_bond_class& cl = lat->classes[q];
+      const int lo2 = a < c ? a : c, hi2 = a < c ? c : a;
+      if (hi2 - lo2 == (int)cl.shift && ((cl.bond_mask >> lo2) & 1)) return true;
+    }
+    return false;
+  };
+  std::vector<std::vector<int>> sets;
+  std::vector<const char*> names;
+  {
+    std::vector<int> even;
+    for (int i = 0; i < k && (int)even.size() < u; ++i)
+      if (!((odd >> i) & 1)) even.push_back(i);
+    if ((int)even.size() == u) {
+      sets.push_back(even);
+      names.push_back("even");
+    }
+    std::vector<int> low;
+    for (int t = 0; t < u; ++t) low.push_back(t);
+    if (sets.empty() || low != sets[0]) {
+      sets.push_back(low);
+      names.push_back("low");
+    }
+    if (n_configs_hint >= (1ull << 33)) {
+      std::vector<int> spread;
+      for (int pass = 0; pass < 3 && (int)spread.size() < u; ++pass)
+        for (int i = 0; i < k && (int)spread.size() < u; ++i) {
+          if (std::find(spread.begin(), spread.end(), i) != spread.end())
+            continue;
+          const bool even_ok = !((odd >> i) & 1) || pass == 2;
+          bool free_ok = true;
+          for (int j : spread) free_ok = free_ok && !adjacent(i, j);
+          if (even_ok && (free_ok || pass == 2)) spread.push_back(i);
+        }
+      std::sort(spread.begin(), spread.end());
+      bool dup = false;
+      for (const auto& st : sets) dup = dup || st == spread;
+      if (!dup) {
+        sets.push_back(spread);
+        names.push_back("spread");
+      }
+    }
+  }
   isd_plan_info best_info;
   bool have = false;
   std::vector<isd_plan_info> all;
-  // test / tuning knob: ISD_COPY_VARIANT=even|low forces one variant
+  // test / tuning knob: ISD_COPY_VARIANT=even|low|spread forces one set
   const char* force = std::getenv("ISD_COPY_VARIANT");
-  for (int variant = 0; variant < 2; ++variant) {
-    if (force && std::strcmp(force, variant ? "low" : "even") != 0) continue;
+  for (size_t v = 0; v < sets.size(); ++v) {
+    if (force && std::strcmp(force, names[v]) != 0) continue;
     isd_plan_info cand = *info;
-    if (variant == 0) {
-      if (ne < u) continue;
-      set_copy_sites(lat, &cand, even_sites, 1);
-    } else {
-      const bool low_even = (odd & ((1ull << u) - 1)) == 0;
-      if (!force && low_even && ne == u &&
-          std::memcmp(even_sites, low_sites, sizeof low_sites) == 0)
-        continue;  // identical to variant 0
-      set_copy_sites(lat, &cand, low_sites, low_even ? 1 : 0);
-    }
+    bool all_even = true;
+    for (int site : sets[v]) all_even = all_even && !((odd >> site) & 1);
+    set_copy_sites(lat, &cand, sets[v].data(), all_even ? 1 : 0);
     choose_layout(lat, &cand, &all, n_configs_hint >= (1ull << 33));
     if (!have || cand.est_wavefronts < best_info.est_wavefronts - 1e-9) {
       best_info = cand;
