@@ -418,7 +418,9 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
     }
     std::vector<int> low;
     for (int t = 0; t < u; ++t) low.push_back(t);
-    if (sets.empty() || low != sets[0]) {
+    const char* forced = std::getenv("ISD_COPY_VARIANT");
+    const bool force_low = forced && std::strcmp(forced, "low") == 0;
+    if (sets.empty() || low != sets[0] || force_low) {
       sets.push_back(low);
       names.push_back("low");
     }
