@@ -177,7 +177,9 @@ int isd_validate(const isd_lattice* lat);
 /* which: 0 = POPC, 1 = LOP3, 2 = IADD3, 3 = RED.shared spread,
  *        4 = RED.shared realistic bins, 5 = IMAD, 6 = SHF, 7 = RED.shared
  *        all lanes on one word, 8 = lane pairs per word (16 banks),
- *        9 = 4 words in one bank, 10 = 8 words x 4 lanes, distinct banks.  Writes lanes per clock
+ *        9 = 4 words in one bank, 10 = 8 words x 4 lanes, distinct banks,
+ *        11 = all lanes one word with values 1 / 65536 (16-bit halves),
+ *        12 = lane pairs per word with values 1 / 65536.  Writes lanes per clock
  *        per SM to *lanes_per_clk_sm and the SM clock seen (MHz). */
 int isd_calibrate(int device, int which, double* lanes_per_clk_sm,
                   double* sm_mhz);

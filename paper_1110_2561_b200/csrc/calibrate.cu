@@ -132,6 +132,29 @@ __global__ void __launch_bounds__(kCalThreads)
         }
       }
       break;
+    case 11:  // RED.shared.add, all lanes one word, value 1 or 65536
+      for (int it = 0; it < kCalIters; ++it) {
+#pragma unroll
+        for (int i = 0; i < kChains; ++i) {
+          const uint32_t addr = sbase + 4u * (32u * ((it * kChains + i) & 255));
+          const uint32_t val = (lane & 1) ? 65536u : 1u;
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(val)
+                       : "memory");
+        }
+      }
+      break;
+    case 12:  // RED.shared.add, lane pairs per word (16 banks), values 1/65536
+      for (int it = 0; it < kCalIters; ++it) {
+#pragma unroll
+        for (int i = 0; i < kChains; ++i) {
+          const uint32_t addr =
+              sbase + 4u * ((lane >> 1) + 32u * ((it * kChains + i) & 255));
+          const uint32_t val = (lane & 1) ? 65536u : 1u;
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(val)
+                       : "memory");
+        }
+      }
+      break;
     default:
       break;
   }

@@ -605,7 +605,7 @@ int isd_calibrate(int device, int which, double* lanes_per_clk_sm,
   DevState* s = nullptr;
   int rc = get_dev(device, &s);
   if (rc) return rc;
-  if (which < 0 || which > 10) return fail(ISD_EINVAL, "unknown probe %d", which);
+  if (which < 0 || which > 12) return fail(ISD_EINVAL, "unknown probe %d", which);
   double lanes = 0, mhz = 0;
   int r = run_calibration(which, s->sm_count, &lanes, &mhz);
   if (r < 0) return cuda_fail((cudaError_t)(-r), "k0 calibration");

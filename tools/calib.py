@@ -7,7 +7,8 @@ from paper_1110_2561_b200 import _native  # noqa: E402
 
 NAMES = ["popc", "lop3", "iadd x2", "red spread", "red hashed 4033", "imad",
          "shf", "red 1 word", "red 2 lanes/word", "red 4 words 1 bank",
-         "red 8 words x4 lanes"]
+         "red 8 words x4 lanes", "red 1 word, vals 1|2^16",
+         "red 2 lanes/word, vals 1|2^16"]
 for i, n in enumerate(NAMES):
     lanes, mhz = _native.calibrate(i)
     print(f"{i:2d} {n:22s} {lanes:8.3f} lanes/clk/SM  ({mhz:.0f} MHz)")
