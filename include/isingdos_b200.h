@@ -157,8 +157,11 @@ typedef struct isd_plan_info {
   uint32_t e_words;
   uint32_t plane_words;
   uint32_t hist_words;       /* words spanned by one histogram          */
-  uint64_t lane_mask;        /* the 5 run bits the 32 lanes of a warp
-                                differ in (bit i = run bit i)           */
+  uint64_t lane_mask;        /* the 5 pivot run bits of the lanes       */
+  uint64_t lane_vec[5];      /* lane bit i flips the run bits lane_vec[i]
+                                (its pivot, plus an optional adjacent
+                                site: a "domino"); lane L's run is the
+                                slot's run XOR the vectors of L's bits  */
   double   est_wavefronts;   /* predicted smem wavefronts per warp RED  */
 } isd_plan_info;
 

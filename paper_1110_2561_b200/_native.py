@@ -59,7 +59,7 @@ class PlanInfo(ctypes.Structure):
         ("odd_mask", ctypes.c_uint64),
         ("row_words", ctypes.c_uint32), ("e_words", ctypes.c_uint32),
         ("plane_words", ctypes.c_uint32), ("hist_words", ctypes.c_uint32),
-        ("lane_mask", ctypes.c_uint64),
+        ("lane_mask", ctypes.c_uint64), ("lane_vec", ctypes.c_uint64 * 5),
         ("est_wavefronts", ctypes.c_double),
     ]
 

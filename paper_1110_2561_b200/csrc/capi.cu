@@ -193,7 +193,9 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   for (size_t i = 0; i < cands.size(); ++i) {
     HoistParams hp;
     fill_hoist(lat, &cands[i], &hp);
-    const uint64_t blk = 1ull << lane_span(hp.lane_mask);
+    uint64_t span_bits = hp.lane_mask;
+    for (int v = 0; v < 5; ++v) span_bits |= hp.lane_vec[v];
+    const uint64_t blk = 1ull << lane_span(span_bits);
     if (body < blk || body < runs) continue;
     const uint64_t warps = runs / 32;
     // warp slots must stay inside whole lane blocks of the body
@@ -226,7 +228,9 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     const size_t i = stage1[s2].second;
     HoistParams hp;
     fill_hoist(lat, &cands[i], &hp);
-    const uint64_t blk = 1ull << lane_span(hp.lane_mask);
+    uint64_t span_bits = hp.lane_mask;
+    for (int v = 0; v < 5; ++v) span_bits |= hp.lane_vec[v];
+    const uint64_t blk = 1ull << lane_span(span_bits);
     uint64_t len = (kTuneSliceConfigs >> hp.k);
     if (len > body) len = body;
     len = (len / blk) * blk;
@@ -379,6 +383,11 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
       info.e_words = b;
       info.plane_words = pw;
       info.lane_mask = (got == 5 && mask) ? mask : (0x1Full << ls);
+      uint64_t m = info.lane_mask;
+      for (int v = 0; v < 5; ++v) {
+        info.lane_vec[v] = m & (~m + 1);
+        m ^= info.lane_vec[v];
+      }
       info.hist_words = lat->n_spins * a + lat->n_bonds * b + pw + 1;
     }
   }
@@ -395,7 +404,11 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     // the plan's lane placement tiles the launch only if its run count is a
     // multiple of 2^lane_span; otherwise lanes take the lowest 5 run bits
     hp.lane_mask = info.lane_mask;
-    if ((re - r) & ((1ull << lane_span(hp.lane_mask)) - 1)) hp.lane_mask = 0x1F;
+    for (int v = 0; v < 5; ++v) hp.lane_vec[v] = info.lane_vec[v];
+    uint64_t span_bits = hp.lane_mask;
+    for (int v = 0; v < 5; ++v) span_bits |= hp.lane_vec[v];
+    if ((re - r) & ((1ull << lane_span(span_bits)) - 1))
+      default_lanes(&hp.lane_mask, hp.lane_vec);
     hp.hi_step = 1;
     int x = 0;
     if (use_jit) {

@@ -157,8 +157,11 @@ __global__ void __launch_bounds__(kThreads)
                unsigned long long* __restrict__ out) {
   extern __shared__ __align__(16) uint32_t hist[];
   const RuntimeTraits L{P};
+  IsdLanes lanes;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) lanes.v[i] = P.lane_vec[i];
   k1_hoisted_body<NC, DOUBLE>(L, P.run_begin, P.run_end - P.run_begin,
-                              P.hi_step, P.lane_mask, hist, out);
+                              P.hi_step, P.lane_mask, lanes, hist, out);
 }
 
 // ---------------------------------------------------------------------------

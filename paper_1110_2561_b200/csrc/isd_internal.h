@@ -51,7 +51,8 @@ struct HoistParams {
   uint32_t n_hist;
   uint32_t has_double;           // any copy site with a doubled partner
   uint32_t pad3_;
-  uint64_t lane_mask;            // the 5 run bits warp lanes differ in
+  uint64_t lane_mask;            // the 5 pivot run bits of the lanes
+  uint64_t lane_vec[5];          // run bits flipped by lane bit i
   uint64_t hi_step;              // warp slot stride (1 = contiguous walk;
                                  // > 1 = the autotuner's spread sample)
   uint32_t e_mode;               // 0 dense, 1 parity planes
@@ -86,6 +87,8 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
 // run-bit count spanned by a lane mask (runs of a walk must be a multiple
 // of 2^lane_span(mask) for that placement to tile the walk)
 int lane_span(uint64_t lane_mask);
+// lanes taking the 5 lowest run bits (valid for any launch)
+void default_lanes(uint64_t* lane_mask, uint64_t* lane_vec);
 int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint);
 void fill_canon(const isd_lattice* lat, CanonParams* p);
 void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,

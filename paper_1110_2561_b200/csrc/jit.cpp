@@ -140,12 +140,13 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
   o << "extern \"C\" __global__ void __launch_bounds__(" << kThreads
     << ") k1_jit(unsigned long long run_begin, unsigned long long nruns,\n"
        "    unsigned long long hi_step, unsigned long long lane_mask,\n"
+       "    const IsdLanes lanes,\n"
        "    unsigned long long* __restrict__ out) {\n"
        "  extern __shared__ __align__(16) unsigned int hist[];\n"
        "  const JitTraits L;\n"
        "  k1_hoisted_body<"
     << nc << ", " << (dbl ? "true" : "false")
-    << ">(L, run_begin, nruns, hi_step, lane_mask, hist, out);\n}\n";
+    << ">(L, run_begin, nruns, hi_step, lane_mask, lanes, hist, out);\n}\n";
   return o.str();
 }
 
@@ -167,6 +168,7 @@ static std::string jit_key(const HoistParams& P, int device) {
   q.run_begin = q.run_end = 0;
   q.hi_step = 0;
   q.lane_mask = 0;
+  for (int i = 0; i < 5; ++i) q.lane_vec[i] = 0;
   std::string key(reinterpret_cast<const char*>(&q), sizeof q);
   key += std::to_string(device);
   return key;
@@ -266,7 +268,11 @@ int launch_hoisted_jit(const HoistParams& P, unsigned long long* out,
   unsigned long long nruns = P.run_end - P.run_begin;
   unsigned long long hi_step = P.hi_step;
   unsigned long long lane_mask = P.lane_mask;
-  void* args[] = {&run_begin, &nruns, &hi_step, &lane_mask, &out};
+  struct {
+    unsigned long long v[5];
+  } lanes;
+  for (int i = 0; i < 5; ++i) lanes.v[i] = P.lane_vec[i];
+  void* args[] = {&run_begin, &nruns, &hi_step, &lane_mask, &lanes, &out};
   int grid = jk.grid;
   const uint64_t need = (nruns + kThreads - 1) / kThreads;
   if (need < (uint64_t)grid) grid = (int)(need ? need : 1);

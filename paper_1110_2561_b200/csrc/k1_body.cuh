@@ -22,6 +22,11 @@
   } while (0)
 #endif
 
+// lane bit i of a warp flips the run bits v[i] (pivot + optional partner)
+struct IsdLanes {
+  unsigned long long v[5];
+};
+
 __device__ __forceinline__ void isd_red_shared_inc(unsigned int addr) {
   asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
 }
@@ -30,7 +35,7 @@ template <int NC, bool DOUBLE, class T>
 __device__ __forceinline__ void k1_hoisted_body(
     const T& L, unsigned long long run_begin, unsigned long long nruns,
     unsigned long long hi_step, unsigned long long lane_mask,
-    unsigned int* hist,
+    const IsdLanes lanes, unsigned int* hist,
     unsigned long long* __restrict__ out) {
   // ---- zero the block's histograms ----
   {
@@ -47,25 +52,22 @@ __device__ __forceinline__ void k1_hoisted_body(
   const unsigned long long gstride = (unsigned long long)gridDim.x * blockDim.x;
   const unsigned int nloop = L.nloop();
   const unsigned long long above_k = L.above_k();
-  // this lane's five run bits, deposited into lane_mask
+  // this lane's run-bit pattern: XOR of the vectors of its set lane bits
   unsigned long long lane_dep = 0;
   {
     const unsigned int lane = threadIdx.x & 31;
-    unsigned long long m = lane_mask;
 #pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      const unsigned long long low = m & (~m + 1);
-      if ((lane >> i) & 1) lane_dep |= low;
-      m ^= low;
-    }
+    for (int i = 0; i < 5; ++i)
+      if ((lane >> i) & 1) lane_dep ^= lanes.v[i];
   }
 
   for (unsigned long long t =
            (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
        t < nruns; t += gstride) {
-    // The 32 lanes of a warp differ in the five run bits of lane_mask
-    // (which sites they differ in sets the shared-memory bank spread); the
-    // warp's slot spreads over the other run bits.  Warp w takes slot
+    // The 32 lanes of a warp differ by XORs of five run-bit vectors, each
+    // with its own pivot bit (lane_mask): which sites they differ in sets
+    // the shared-memory bank spread.  The warp's slot spreads over the
+    // non-pivot run bits, so (slot, lane) -> run is a bijection.  Warp w takes slot
     // w * hi_step (1 in a walk; > 1 when the autotuner times a sample of
     // warps spread over the whole range).
     unsigned long long hi = (t >> 5) * hi_step;
@@ -78,7 +80,7 @@ __device__ __forceinline__ void k1_hoisted_body(
         m ^= low;
       }
     }
-    const unsigned long long r = run_begin + (hi | lane_dep);
+    const unsigned long long r = run_begin + (hi ^ lane_dep);
     // ---- per-run constants (bits [k, N) fixed) ----
     const unsigned long long xt = r << L.k();
     const int m_run = __popcll(xt);

@@ -109,20 +109,51 @@ int lane_span(uint64_t lane_mask) {
   return lane_mask ? 64 - __builtin_clzll(lane_mask) : 0;
 }
 
-// Candidate lane masks: contiguous windows of 5 run bits, plus (for large
-// walks) random 5-subsets, half of them drawn from run sites of even degree
-// (flipping those keeps the e parity of the 32 lanes equal).
-static void lane_candidates(const isd_plan_info* info, int run_bits,
-                            bool wide, std::vector<uint64_t>* out) {
+void default_lanes(uint64_t* lane_mask, uint64_t* lane_vec) {
+  *lane_mask = 0x1F;
+  for (int i = 0; i < 5; ++i) lane_vec[i] = 1ull << i;
+}
+
+namespace {
+struct Lanes {
+  uint64_t mask;    // pivots
+  uint64_t vec[5];  // lane bit i flips these run bits (pivot i included)
+};
+}  // namespace
+
+static Lanes lanes_from_mask(uint64_t mask) {
+  Lanes L{mask, {0, 0, 0, 0, 0}};
+  uint64_t m = mask;
+  for (int i = 0; i < 5; ++i) {
+    L.vec[i] = m & (~m + 1);
+    m ^= L.vec[i];
+  }
+  return L;
+}
+
+// Candidate lane patterns: contiguous windows of 5 run bits, plus (for
+// large walks) random 5-subsets — half of them from even-degree sites,
+// whose flips keep the lanes' e parity equal — and random "dominoes": each
+// lane bit flips its pivot site together with one adjacent run site (lanes
+// then differ by pairs of neighbours, which keeps their (m, e) bins closer
+// together: fewer distinct words per RED, fewer bank conflicts).
+static void lane_candidates(const isd_lattice* lat, const isd_plan_info* info,
+                            int run_bits, bool wide, std::vector<Lanes>* out) {
   static const int shifts[] = {0, 3, 6, 9, 12, 15};
   for (int ls : shifts)
-    if (run_bits >= ls + 5) out->push_back(0x1Full << ls);
+    if (run_bits >= ls + 5) out->push_back(lanes_from_mask(0x1Full << ls));
   if (!wide || run_bits < 6) return;
+  const int k = (int)info->k;
   std::vector<int> even, all;
   for (int bit = 0; bit < run_bits; ++bit) {
     all.push_back(bit);
-    if (!((info->odd_mask >> (bit + info->k)) & 1)) even.push_back(bit);
+    if (!((info->odd_mask >> (bit + k)) & 1)) even.push_back(bit);
   }
+  auto seen = [&](uint64_t mask, const uint64_t* vec) {
+    for (const Lanes& L : *out)
+      if (L.mask == mask && std::equal(L.vec, L.vec + 5, vec)) return true;
+    return false;
+  };
   uint64_t seed = 0xD1B54A32D192ED03ull;
   for (int pool = 0; pool < 2; ++pool) {
     const std::vector<int>& src = pool == 0 ? even : all;
@@ -131,9 +162,34 @@ static void lane_candidates(const isd_plan_info* info, int run_bits,
       uint64_t m = 0;
       while (__builtin_popcountll(m) < 5)
         m |= 1ull << src[rng_next(&seed) % src.size()];
-      if (std::find(out->begin(), out->end(), m) == out->end())
-        out->push_back(m);
+      const Lanes L = lanes_from_mask(m);
+      if (!seen(L.mask, L.vec)) out->push_back(L);
     }
+  }
+  // run-bit adjacency
+  std::vector<std::vector<int>> nbr(run_bits);
+  for (uint32_t q = 0; q < lat->n_classes; ++q) {
+    const isd_bond_class& cl = lat->classes[q];
+    for (int i = k; i + (int)cl.shift < (int)lat->n_spins; ++i)
+      if ((cl.bond_mask >> i) & 1) {
+        const int a = i - k, c = i + (int)cl.shift - k;
+        nbr[a].push_back(c);
+        nbr[c].push_back(a);
+      }
+  }
+  for (int r = 0; r < 32; ++r) {
+    Lanes L = lanes_from_mask(0);
+    uint64_t m = 0;
+    while (__builtin_popcountll(m) < 5) m |= 1ull << (rng_next(&seed) % run_bits);
+    L = lanes_from_mask(m);
+    for (int i = 0; i < 5; ++i) {
+      const int p = __builtin_ctzll(L.vec[i]);
+      std::vector<int> cand;
+      for (int q : nbr[p])
+        if (!((m >> q) & 1)) cand.push_back(q);
+      if (!cand.empty()) L.vec[i] |= 1ull << cand[rng_next(&seed) % cand.size()];
+    }
+    if (!seen(L.mask, L.vec)) out->push_back(L);
   }
 }
 
@@ -143,7 +199,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   const int k = (int)info->k;
   const int b = (int)lat->n_bonds;
   const int emax_half = b / 2;  // largest (e - par)/2
-  info->lane_mask = 0x1F;
+  default_lanes(&info->lane_mask, info->lane_vec);
   info->est_wavefronts = 0;
   // candidate layouts (row_words A, e_words B, plane_words P)
   struct Cand {
@@ -182,8 +238,8 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
     if (ranked) ranked->push_back(*info);
     return;
   }
-  std::vector<uint64_t> masks;
-  lane_candidates(info, run_bits, wide, &masks);
+  std::vector<Lanes> masks;
+  lane_candidates(lat, info, run_bits, wide, &masks);
 
   // Score one lane mask against every layout on `warps` sampled warp
   // instructions x kCopySample copies; returns its best cost and, if
@@ -192,12 +248,17 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   std::vector<double> cost(nc);
   double best = 1e30;
   isd_plan_info best_alt_ = *info;
-  auto evaluate = [&](uint64_t lane_mask, int warps, bool emit) {
+  auto evaluate = [&](const Lanes& LN, int warps, bool emit) {
     std::fill(cost.begin(), cost.end(), 0.0);
-    uint64_t seed = 0x9E3779B97F4A7C15ull ^ lane_mask;
+    const uint64_t lane_mask = LN.mask;
+    uint64_t seed = 0x9E3779B97F4A7C15ull ^ lane_mask ^ (LN.vec[0] << 7);
     const uint64_t free_mask = ((1ull << run_bits) - 1) & ~lane_mask;
     uint64_t lane_dep[32];
-    for (int lane = 0; lane < 32; ++lane) lane_dep[lane] = deposit(lane, lane_mask);
+    for (int lane = 0; lane < 32; ++lane) {
+      lane_dep[lane] = 0;
+      for (int i = 0; i < 5; ++i)
+        if ((lane >> i) & 1) lane_dep[lane] ^= LN.vec[i];
+    }
     for (int w = 0; w < warps; ++w) {
       const uint64_t hi = deposit(rng_next(&seed), free_mask);
       const uint64_t jb = deposit(rng_next(&seed), info->loop_mask);
@@ -209,7 +270,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
         Bin bins[32];
         int nb = 0;
         for (int lane = 0; lane < 32; ++lane) {
-          const uint64_t r = hi | lane_dep[lane];
+          const uint64_t r = hi ^ lane_dep[lane];
           const uint64_t x = (r << k) | jb | cbits;
           int e = 0;
           for (uint32_t q = 0; q < lat->n_classes; ++q) {
@@ -251,6 +312,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
       alt.plane_words = (uint32_t)cand[ci].p;
       alt.hist_words = (uint32_t)cand[ci].span;
       alt.lane_mask = lane_mask;
+      for (int i = 0; i < 5; ++i) alt.lane_vec[i] = LN.vec[i];
       alt.est_wavefronts = cst;
       if (ranked) ranked->push_back(alt);
       if (cst < best - 1e-9) {
@@ -262,14 +324,17 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   };
   // screen every mask on a quarter of the sample, then score the best 8
   // in full
-  std::vector<std::pair<double, uint64_t>> screen;
   if (masks.size() > 8) {
-    for (const uint64_t m : masks) screen.push_back({evaluate(m, kScreenWarps, false), m});
+    std::vector<std::pair<double, size_t>> screen;
+    for (size_t i = 0; i < masks.size(); ++i)
+      screen.push_back({evaluate(masks[i], kScreenWarps, false), i});
     std::sort(screen.begin(), screen.end());
-    masks.clear();
-    for (size_t i = 0; i < screen.size() && i < 8; ++i) masks.push_back(screen[i].second);
+    std::vector<Lanes> keep;
+    for (size_t i = 0; i < screen.size() && i < 8; ++i)
+      keep.push_back(masks[screen[i].second]);
+    masks.swap(keep);
   }
-  for (const uint64_t m : masks) evaluate(m, kWarps, true);
+  for (const Lanes& m : masks) evaluate(m, kWarps, true);
   if (best < 1e29) *info = best_alt_;
 }
 
@@ -513,6 +578,7 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
                                       2 * (int)info->e_words
                                 : 0;
   p->lane_mask = info->lane_mask;
+  for (int i = 0; i < 5; ++i) p->lane_vec[i] = info->lane_vec[i];
   p->hi_step = 1;
   p->hist_words = hist_words_for(info->hist_words);
   p->n_hist = (uint32_t)hist_count_for(p->hist_words);
