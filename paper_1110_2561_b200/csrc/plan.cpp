@@ -131,6 +131,22 @@ static Lanes lanes_from_mask(uint64_t mask) {
   return L;
 }
 
+// Adjacency between run bits (run bit b = site b + k).
+static std::vector<std::vector<int>> run_neighbors(const isd_lattice* lat,
+                                                   int k, int run_bits) {
+  std::vector<std::vector<int>> nbr(run_bits);
+  for (uint32_t q = 0; q < lat->n_classes; ++q) {
+    const isd_bond_class& cl = lat->classes[q];
+    for (int i = k; i + (int)cl.shift < (int)lat->n_spins; ++i)
+      if ((cl.bond_mask >> i) & 1) {
+        const int a = i - k, c = i + (int)cl.shift - k;
+        nbr[a].push_back(c);
+        nbr[c].push_back(a);
+      }
+  }
+  return nbr;
+}
+
 // Candidate lane patterns: contiguous windows of 5 run bits, plus (for
 // large walks) random 5-subsets — half of them from even-degree sites,
 // whose flips keep the lanes' e parity equal — and random "dominoes": each
@@ -166,17 +182,7 @@ static void lane_candidates(const isd_lattice* lat, const isd_plan_info* info,
       if (!seen(L.mask, L.vec)) out->push_back(L);
     }
   }
-  // run-bit adjacency
-  std::vector<std::vector<int>> nbr(run_bits);
-  for (uint32_t q = 0; q < lat->n_classes; ++q) {
-    const isd_bond_class& cl = lat->classes[q];
-    for (int i = k; i + (int)cl.shift < (int)lat->n_spins; ++i)
-      if ((cl.bond_mask >> i) & 1) {
-        const int a = i - k, c = i + (int)cl.shift - k;
-        nbr[a].push_back(c);
-        nbr[c].push_back(a);
-      }
-  }
+  const std::vector<std::vector<int>> nbr = run_neighbors(lat, k, run_bits);
   for (int r = 0; r < 32; ++r) {
     Lanes L = lanes_from_mask(0);
     uint64_t m = 0;
@@ -251,7 +257,9 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   auto evaluate = [&](const Lanes& LN, int warps, bool emit) {
     std::fill(cost.begin(), cost.end(), 0.0);
     const uint64_t lane_mask = LN.mask;
-    uint64_t seed = 0x9E3779B97F4A7C15ull ^ lane_mask ^ (LN.vec[0] << 7);
+    // the same random stream for every candidate (common random numbers:
+    // differences between candidates are then not sampling noise)
+    uint64_t seed = 0x9E3779B97F4A7C15ull;
     const uint64_t free_mask = ((1ull << run_bits) - 1) & ~lane_mask;
     uint64_t lane_dep[32];
     for (int lane = 0; lane < 32; ++lane) {
@@ -333,6 +341,46 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
     for (size_t i = 0; i < screen.size() && i < 8; ++i)
       keep.push_back(masks[screen[i].second]);
     masks.swap(keep);
+  }
+  // large walks: hill-climb the best three patterns (re-pivot a lane bit,
+  // or give / move / drop its domino partner), scored on the screen sample
+  if (wide && run_bits >= 8) {
+    const std::vector<std::vector<int>> nbr = run_neighbors(lat, k, run_bits);
+    uint64_t seed = 0x2545F4914F6CDD1Dull;
+    const size_t n_start = std::min<size_t>(3, masks.size());
+    for (size_t si = 0; si < n_start; ++si) {
+      Lanes cur = masks[si];
+      double cur_cost = evaluate(cur, kScreenWarps, false);
+      for (int step = 0; step < 40; ++step) {
+        Lanes q = cur;
+        const int i = (int)(rng_next(&seed) % 5);
+        uint64_t partners = 0;
+        for (int v = 0; v < 5; ++v) partners |= q.vec[v] & ~q.mask;
+        const int piv = __builtin_ctzll(q.vec[i] & q.mask);
+        if (rng_next(&seed) & 1) {  // re-pivot (drops the partner)
+          const int nb = (int)(rng_next(&seed) % run_bits);
+          if (((q.mask | partners) >> nb) & 1) continue;
+          q.mask = (q.mask & ~(1ull << piv)) | (1ull << nb);
+          q.vec[i] = 1ull << nb;
+        } else {  // partner: new random neighbour of the pivot, or none
+          std::vector<int> cand;
+          for (int c : nbr[piv])
+            if (!((q.mask >> c) & 1)) cand.push_back(c);
+          const size_t pick = rng_next(&seed) % (cand.size() + 1);
+          q.vec[i] = 1ull << piv;
+          if (pick < cand.size()) q.vec[i] |= 1ull << cand[pick];
+        }
+        const double c = evaluate(q, kScreenWarps, false);
+        if (c < cur_cost) {
+          cur = q;
+          cur_cost = c;
+        }
+      }
+      bool dup = false;
+      for (const Lanes& m : masks)
+        dup = dup || (m.mask == cur.mask && std::equal(m.vec, m.vec + 5, cur.vec));
+      if (!dup) masks.push_back(cur);
+    }
   }
   for (const Lanes& m : masks) evaluate(m, kWarps, true);
   if (best < 1e29) *info = best_alt_;
