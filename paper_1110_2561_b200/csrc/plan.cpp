@@ -200,7 +200,8 @@ static void lane_candidates(const isd_lattice* lat, const isd_plan_info* info,
 }
 
 static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
-                          std::vector<isd_plan_info>* ranked, bool wide) {
+                          std::vector<isd_plan_info>* ranked, bool wide,
+                          int walk_bits) {
   const int n = (int)lat->n_spins;
   const int k = (int)info->k;
   const int b = (int)lat->n_bonds;
@@ -239,7 +240,9 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   info->e_words = (uint32_t)cand[0].b;
   info->plane_words = (uint32_t)cand[0].p;
   info->hist_words = (uint32_t)cand[0].span;
-  const int run_bits = n - k;
+  // run bits a walk of 2^walk_bits configurations actually varies (a shard
+  // fixes the top ones): lane patterns must stay inside them to tile it
+  const int run_bits = std::min(n, walk_bits) - k;
   if (run_bits < 5) {
     if (ranked) ranked->push_back(*info);
     return;
@@ -568,7 +571,11 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
     bool all_even = true;
     for (int site : sets[v]) all_even = all_even && !((odd >> site) & 1);
     set_copy_sites(lat, &cand, sets[v].data(), all_even ? 1 : 0);
-    choose_layout(lat, &cand, &all, n_configs_hint >= (1ull << 33));
+    int walk_bits = 0;
+    while (walk_bits < 63 && (1ull << (walk_bits + 1)) <= n_configs_hint)
+      ++walk_bits;
+    choose_layout(lat, &cand, &all, n_configs_hint >= (1ull << 33),
+                  walk_bits);
     if (!have || cand.est_wavefronts < best_info.est_wavefronts - 1e-9) {
       best_info = cand;
       have = true;
