@@ -140,6 +140,7 @@ static std::vector<std::vector<int>> run_neighbors(const isd_lattice* lat,
     for (int i = k; i + (int)cl.shift < (int)lat->n_spins; ++i)
       if ((cl.bond_mask >> i) & 1) {
         const int a = i - k, c = i + (int)cl.shift - k;
+        if (a >= run_bits || c >= run_bits) continue;
         nbr[a].push_back(c);
         nbr[c].push_back(a);
       }

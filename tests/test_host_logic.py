@@ -338,3 +338,23 @@ def test_jit_source_compiles_for_sm100a(name):
     spec = workloads()[name].spec
     n = _native.jit_check(native_lattice(spec), spec.num_configs)
     assert n > 10000
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+@pytest.mark.parametrize("log_hint", [33, 34, 36])
+def test_lane_patterns_tile_the_walk(name, log_hint):
+    # every lane vector has its own pivot, and all of them stay inside the
+    # run bits a walk of 2^log_hint configurations varies (shards of an
+    # 8-GPU run use log_hint = 33)
+    spec = workloads()[name].spec
+    usable, info = _native.plan(native_lattice(spec), 1 << log_hint)
+    assert usable
+    mask = int(info.lane_mask)
+    vecs = [int(v) for v in info.lane_vec]
+    assert bin(mask).count("1") == 5
+    assert sorted(v & mask for v in vecs) == sorted(1 << b for b in range(64)
+                                                   if (mask >> b) & 1)
+    span = 0
+    for v in vecs + [mask]:
+        span = max(span, v.bit_length())
+    assert span <= log_hint - info.k
