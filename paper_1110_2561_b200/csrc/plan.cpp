@@ -16,6 +16,11 @@ namespace isd {
 
 static inline int popc64(uint64_t x) { return __builtin_popcountll(x); }
 
+static long env_int(const char* name, long dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atol(v) : dflt;
+}
+
 int validate_lattice(const isd_lattice* lat, char* err, size_t errlen) {
   if (!lat) {
     snprintf(err, errlen, "lattice pointer is NULL");
@@ -255,6 +260,8 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   // instructions x kCopySample copies; returns its best cost and, if
   // `emit`, appends every (layout, mask) alternative to `ranked`.
   constexpr int kWarps = 160, kScreenWarps = 40, kCopySample = 8;
+  const int kClimbSteps = (int)env_int("ISD_CLIMB_STEPS", 40);
+  const size_t kClimbStarts = (size_t)env_int("ISD_CLIMB_STARTS", 3);
   std::vector<double> cost(nc);
   double best = 1e30;
   isd_plan_info best_alt_ = *info;
@@ -351,11 +358,11 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   if (wide && run_bits >= 8) {
     const std::vector<std::vector<int>> nbr = run_neighbors(lat, k, run_bits);
     uint64_t seed = 0x2545F4914F6CDD1Dull;
-    const size_t n_start = std::min<size_t>(3, masks.size());
+    const size_t n_start = std::min<size_t>(kClimbStarts, masks.size());
     for (size_t si = 0; si < n_start; ++si) {
       Lanes cur = masks[si];
       double cur_cost = evaluate(cur, kScreenWarps, false);
-      for (int step = 0; step < 40; ++step) {
+      for (int step = 0; step < kClimbSteps; ++step) {
         Lanes q = cur;
         const int i = (int)(rng_next(&seed) % 5);
         uint64_t partners = 0;
