@@ -24,7 +24,6 @@ static thread_local std::string g_err;
 // which kernel path the last enumeration on this thread used
 static thread_local std::string g_kernel_info = "none";
 static std::atomic<uint64_t> g_launches{0};
-static std::mutex g_mu;
 
 uint64_t bump_launches(uint64_t n) { return g_launches += n; }
 
@@ -65,6 +64,7 @@ int hist_count_for(uint32_t hist_words) {
 }
 
 struct DevState {
+  std::mutex mu;  // serialises host-buffer calls on this device only
   bool init = false;
   int sm_count = 0;
   cudaStream_t stream = nullptr;
@@ -76,7 +76,11 @@ struct DevState {
 };
 static DevState g_dev[64];
 
-static int get_dev(int device, DevState** out) {
+// Select `device` on this thread, initialise its state once, and lock it:
+// host-buffer calls on different devices run concurrently (one host thread
+// per GPU in full_dos_timed), calls on one device are serialised.
+static int get_dev(int device, DevState** out,
+                   std::unique_lock<std::mutex>* lock) {
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0)
@@ -87,6 +91,7 @@ static int get_dev(int device, DevState** out) {
   e = cudaSetDevice(device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
   DevState& s = g_dev[device];
+  *lock = std::unique_lock<std::mutex>(s.mu);
   if (!s.init) {
     e = cudaDeviceGetAttribute(&s.sm_count, cudaDevAttrMultiProcessorCount,
                                device);
@@ -485,12 +490,12 @@ int isd_enumerate_async(const isd_lattice* lat, uint64_t start, uint64_t end,
 int isd_enumerate(const isd_lattice* lat, uint64_t start, uint64_t end,
                   int device, int algo, uint64_t* counts_host,
                   double* device_ms) {
-  std::lock_guard<std::mutex> lock(g_mu);
   int rc = isd_validate(lat);
   if (rc) return rc;
   if (!counts_host) return fail(ISD_EINVAL, "counts pointer is NULL");
   DevState* s = nullptr;
-  rc = get_dev(device, &s);
+  std::unique_lock<std::mutex> lock;
+  rc = get_dev(device, &s, &lock);
   if (rc) return rc;
   const size_t bytes =
       (size_t)(lat->n_spins + 1) * (lat->n_bonds + 1) * sizeof(uint64_t);
@@ -558,7 +563,6 @@ int isd_thermo(const uint64_t* counts_host, uint32_t n_spins, uint32_t n_bonds,
                double energy_scale, const double* fields, int n_fields,
                const double* temps, int n_temps, int device, double* out_host,
                double* device_ms) {
-  std::lock_guard<std::mutex> lock(g_mu);
   if (n_spins < 1 || n_spins > ISD_MAX_SPINS || n_bonds > 3 * ISD_MAX_SPINS)
     return fail(ISD_EINVAL, "bad table shape N=%u B=%u", n_spins, n_bonds);
   if (!counts_host || !fields || !temps || !out_host)
@@ -566,7 +570,8 @@ int isd_thermo(const uint64_t* counts_host, uint32_t n_spins, uint32_t n_bonds,
   if (n_fields < 0 || n_temps < 0)
     return fail(ISD_EINVAL, "negative grid size");
   DevState* s = nullptr;
-  int rc = get_dev(device, &s);
+  std::unique_lock<std::mutex> lock;
+  int rc = get_dev(device, &s, &lock);
   if (rc) return rc;
   const size_t tbytes = (size_t)(n_spins + 1) * (n_bonds + 1) * 8;
   const size_t npts = (size_t)n_fields * n_temps;
@@ -614,9 +619,9 @@ int isd_thermo(const uint64_t* counts_host, uint32_t n_spins, uint32_t n_bonds,
 
 int isd_calibrate(int device, int which, double* lanes_per_clk_sm,
                   double* sm_mhz) {
-  std::lock_guard<std::mutex> lock(g_mu);
   DevState* s = nullptr;
-  int rc = get_dev(device, &s);
+  std::unique_lock<std::mutex> lock;
+  int rc = get_dev(device, &s, &lock);
   if (rc) return rc;
   if (which < 0 || which > 12) return fail(ISD_EINVAL, "unknown probe %d", which);
   double lanes = 0, mhz = 0;
