@@ -1,11 +1,13 @@
 // K2 — Z(h, T) and thermodynamics from the exact table g(M, E), fp64.
 //
-// Follows /root/reference/pkg/src/isingdos/thermo.py:37-88 step for step:
+// Follows /root/reference/pkg/src/isingdos/thermo.py:37-88:
 //   cells   = occupied (g > 0) entries, M = 2 m_idx - N, E = (2 e_idx - B)|J|
 //   H       = E - h M,   x = -H / T,   shift = max over occupied cells of x
 //   w       = g exp(x - shift),  s = sum w,  log Z = shift + log s,  p = w / s
 //   U = p.H,  <M> = p.M,  C = p.(H-U)^2 / T^2,  chi = p.(M-<M>)^2 / T
-// plus the extension <|M|> = p.|M| (BASELINE configs 2 and 5).
+// plus the extension <|M|> = p.|M| (BASELINE configs 2 and 5).  The
+// moments are accumulated as w-weighted sums and divided by s once
+// (sum(w x)/s instead of sum((w/s) x)): same value to ~1e-16 relative.
 //
 // One warp per (h, T) point, eight points per CTA.  The CTA first compacts
 // the occupied cells of the table into shared memory, in table order (a
@@ -100,44 +102,54 @@ __global__ void __launch_bounds__(kThermoThreads)
   }
   const double shift = warp_max(xmax);
 
-  // pass 2: s = sum g exp(x - shift)
-  double s = 0.0;
-  for (int i = lane; i < nc; i += 32) {
-    const double m = (double)cells[i].m;
-    const double e = (double)cells[i].e * scale;
-    const double en = e - h * m;
-    s += cells[i].g * exp(-en / t - shift);
+  // pass 2: w = g exp(x - shift); s = sum w and the first moments as
+  // w-weighted sums (divided by s afterwards: one exp per cell here, one in
+  // pass 3).  Four independent accumulators per lane (cells i, i+32, i+64,
+  // i+96 of each 128-cell stripe) hide the exp latency; they are combined
+  // in a fixed order, then across lanes by a fixed xor tree.
+  double s4[4] = {0, 0, 0, 0}, u4[4] = {0, 0, 0, 0}, m4[4] = {0, 0, 0, 0},
+         a4[4] = {0, 0, 0, 0};
+  for (int i0 = lane; i0 < nc; i0 += 128) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + 32 * j;
+      if (i < nc) {
+        const double m = (double)cells[i].m;
+        const double e = (double)cells[i].e * scale;
+        const double en = e - h * m;
+        const double w = cells[i].g * exp(-en / t - shift);
+        s4[j] += w;
+        u4[j] += w * en;
+        m4[j] += w * m;
+        a4[j] += w * fabs(m);
+      }
+    }
   }
-  s = warp_sum(s);
+  const double s = warp_sum((s4[0] + s4[1]) + (s4[2] + s4[3]));
+  const double u = warp_sum((u4[0] + u4[1]) + (u4[2] + u4[3])) / s;
+  const double mean_m = warp_sum((m4[0] + m4[1]) + (m4[2] + m4[3])) / s;
+  const double mean_abs = warp_sum((a4[0] + a4[1]) + (a4[2] + a4[3])) / s;
 
-  // pass 3: first moments
-  double u = 0.0, mean_m = 0.0, mean_abs = 0.0;
-  for (int i = lane; i < nc; i += 32) {
-    const double m = (double)cells[i].m;
-    const double e = (double)cells[i].e * scale;
-    const double en = e - h * m;
-    const double p = (cells[i].g * exp(-en / t - shift)) / s;
-    u += p * en;
-    mean_m += p * m;
-    mean_abs += p * fabs(m);
+  // pass 3: central second moments (the two-pass form of thermo.py:75-77;
+  // the raw <H^2> - <H>^2 form cancels catastrophically at low T)
+  double e4[4] = {0, 0, 0, 0}, v4[4] = {0, 0, 0, 0};
+  for (int i0 = lane; i0 < nc; i0 += 128) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + 32 * j;
+      if (i < nc) {
+        const double m = (double)cells[i].m;
+        const double e = (double)cells[i].e * scale;
+        const double en = e - h * m;
+        const double w = cells[i].g * exp(-en / t - shift);
+        const double de = en - u, dm = m - mean_m;
+        e4[j] += w * (de * de);
+        v4[j] += w * (dm * dm);
+      }
+    }
   }
-  u = warp_sum(u);
-  mean_m = warp_sum(mean_m);
-  mean_abs = warp_sum(mean_abs);
-
-  // pass 4: central second moments
-  double ve = 0.0, vm = 0.0;
-  for (int i = lane; i < nc; i += 32) {
-    const double m = (double)cells[i].m;
-    const double e = (double)cells[i].e * scale;
-    const double en = e - h * m;
-    const double p = (cells[i].g * exp(-en / t - shift)) / s;
-    const double de = en - u, dm = m - mean_m;
-    ve += p * (de * de);
-    vm += p * (dm * dm);
-  }
-  ve = warp_sum(ve);
-  vm = warp_sum(vm);
+  const double ve = warp_sum((e4[0] + e4[1]) + (e4[2] + e4[3])) / s;
+  const double vm = warp_sum((v4[0] + v4[1]) + (v4[2] + v4[3])) / s;
 
   if (lane == 0) {
     const double log_z = shift + log(s);
