@@ -59,18 +59,11 @@ __global__ void __launch_bounds__(kThermoThreads)
   const uint32_t nbins = (n + 1) * stride;
 
   // ---- compact the occupied cells, in table order ----
-  // stage the table in shared memory with coalesced loads, then scan
-  // contiguous per-thread chunks of it
-  unsigned long long* tab =
-      reinterpret_cast<unsigned long long*>(smem + sizeof(Cell) * nbins);
-  for (uint32_t i = threadIdx.x; i < nbins; i += kThermoThreads)
-    tab[i] = counts[i];
-  __syncthreads();
   const uint32_t per = (nbins + kThermoThreads - 1) / kThermoThreads;
   const uint32_t lo = threadIdx.x * per;
   const uint32_t hi = min(lo + per, nbins);
   int mine = 0;
-  for (uint32_t i = lo; i < hi; ++i) mine += tab[i] != 0;
+  for (uint32_t i = lo; i < hi; ++i) mine += counts[i] != 0;
   scan[threadIdx.x] = mine;
   __syncthreads();
   for (int o = 1; o < kThermoThreads; o <<= 1) {  // inclusive scan
@@ -81,7 +74,7 @@ __global__ void __launch_bounds__(kThermoThreads)
   }
   int pos = scan[threadIdx.x] - mine;
   for (uint32_t i = lo; i < hi; ++i) {
-    const unsigned long long g = tab[i];
+    const unsigned long long g = counts[i];
     if (!g) continue;
     const int mi = (int)(i / stride), ei = (int)(i - mi * stride);
     cells[pos].g = (double)g;
@@ -177,10 +170,8 @@ int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
                   void* stream) {
   const int points = n_fields * n_temps;
   if (points <= 0) return 0;
-  const size_t bins = (size_t)(n_spins + 1) * (n_bonds + 1);
-  const size_t smem = (sizeof(Cell) + sizeof(unsigned long long)) * bins;
-  static_assert((sizeof(Cell) + 8) * kMaxBins <= 227 * 1024,
-                "cell list + staged table fit in shared memory");
+  const size_t smem = sizeof(Cell) * (size_t)(n_spins + 1) * (n_bonds + 1);
+  static_assert(sizeof(Cell) * kMaxBins <= 227 * 1024, "cell list fits");
   cudaFuncSetAttribute((const void*)k2_thermo,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = (points + kThermoPoints - 1) / kThermoPoints;
