@@ -1,5 +1,5 @@
 #!/bin/bash
-# ground truth: full-walk time for forced layouts (A,B,P,lane_shift)
+# ground truth: full-walk time for forced layouts (A,B,P,window shift)
 for cfg in ${CFGS:-c5 c4 c3}; do
   case $cfg in
     c5) lays="55,1,0,0 58,1,0,15 58,1,0,6 59,1,0,6 70,1,0,12 70,1,0,6 69,1,0,15 1,38,0,0 1,51,0,3 1,45,0,9";;
