@@ -369,6 +369,8 @@ N40 = [
     dict(rows=5, cols=8), dict(rows=4, cols=10, boundary="free"),
     dict(rows=2, cols=4, depth=5), dict(rows=5, cols=8, seed=40),
     dict(rows=20, cols=2, coupling=-1),
+    # length-2 periodic axes: double bonds through the JIT kernel
+    dict(rows=2, cols=20), dict(rows=2, cols=2, depth=10, seed=3),
 ]
 
 
@@ -404,3 +406,14 @@ def test_n40_full_walk_invariants(kw):
 def test_n40_canonical_equals_hoisted():
     spec = _spec(dict(rows=5, cols=8, seed=7))
     assert np.array_equal(full(spec, _native.ALGO_CANONICAL), full(spec))
+
+
+@pytest.mark.parametrize("kw", [dict(rows=2, cols=17), dict(rows=2, cols=2,
+                                                           depth=9, seed=5)])
+def test_double_bond_lattices_jit_vs_aot(kw, monkeypatch):
+    spec = _spec(kw)
+    jit = full(spec)
+    assert _native.kernel_info() == "k1_hoisted_jit"
+    monkeypatch.setenv("ISD_JIT", "0")
+    assert np.array_equal(full(spec), jit)
+    assert isd.verify_dos(isd.DoSHistogram(spec, jit)).passed
