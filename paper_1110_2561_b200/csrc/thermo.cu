@@ -9,7 +9,7 @@
 // moments are accumulated as w-weighted sums and divided by s once
 // (sum(w x)/s instead of sum((w/s) x)): same value to ~1e-16 relative.
 //
-// One warp per (h, T) point, eight points per CTA.  The CTA first compacts
+// A team of four warps per (h, T) point, two points per CTA.  The CTA first compacts
 // the occupied cells of the table into shared memory, in table order (a
 // block prefix scan), so every warp walks the same cell list; each lane
 // takes a fixed strided subset and the partials meet in a fixed xor-shuffle
@@ -23,8 +23,10 @@
 
 namespace isd {
 
-constexpr int kThermoThreads = 256;                 // 8 warps = 8 points
-constexpr int kThermoPoints = kThermoThreads / 32;
+constexpr int kThermoThreads = 256;                 // 8 warps
+constexpr int kTeam = 4;                            // warps per point
+constexpr int kTeamLanes = 32 * kTeam;
+constexpr int kThermoPoints = kThermoThreads / kTeamLanes;  // 2 per CTA
 constexpr int kMaxBins = (ISD_MAX_SPINS + 1) * (3 * ISD_MAX_SPINS + 1);
 
 struct Cell {
@@ -86,72 +88,91 @@ __global__ void __launch_bounds__(kThermoThreads)
   __syncthreads();
   const int nc = n_cells;
 
-  const int point = blockIdx.x * kThermoPoints + (threadIdx.x >> 5);
-  if (point >= n_points) return;
-  const int lane = threadIdx.x & 31;
+  // a team of kTeam warps per point; partial results of the team's warps
+  // meet in shared memory in a fixed order (deterministic)
+  __shared__ double part[kThermoThreads / 32][4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int team = warp / kTeam, tw = warp % kTeam;
+  const int tl = tw * 32 + lane;  // lane within the team
+  const int point_raw = blockIdx.x * kThermoPoints + team;
+  const int point = point_raw < n_points ? point_raw : n_points - 1;
   const double h = fields[point / n_temps];
   const double t = temps[point % n_temps];
+  auto team_sum = [&](double v, int slot) {
+    v = warp_sum(v);
+    if (lane == 0) part[warp][slot] = v;
+    __syncthreads();
+    double r = 0.0;
+#pragma unroll
+    for (int w = 0; w < kTeam; ++w) r += part[team * kTeam + w][slot];
+    return r;
+  };
 
   // pass 1: shift = max x over occupied cells
   double xmax = -INFINITY;
-  for (int i = lane; i < nc; i += 32) {
+  for (int i = tl; i < nc; i += kTeamLanes) {
     const double m = (double)cells[i].m;
     const double e = (double)cells[i].e * scale;
     const double en = e - h * m;
     xmax = fmax(xmax, -en / t);
   }
-  const double shift = warp_max(xmax);
+  xmax = warp_max(xmax);
+  if (lane == 0) part[warp][0] = xmax;
+  __syncthreads();
+  double shift = part[team * kTeam][0];
+#pragma unroll
+  for (int w = 1; w < kTeam; ++w) shift = fmax(shift, part[team * kTeam + w][0]);
+  __syncthreads();
 
   // pass 2: w = g exp(x - shift); s = sum w and the first moments as
   // w-weighted sums (divided by s afterwards: one exp per cell here, one in
-  // pass 3).  Four independent accumulators per lane (cells i, i+32, i+64,
-  // i+96 of each 128-cell stripe) hide the exp latency; they are combined
-  // in a fixed order, then across lanes by a fixed xor tree.
-  double s4[4] = {0, 0, 0, 0}, u4[4] = {0, 0, 0, 0}, m4[4] = {0, 0, 0, 0},
-         a4[4] = {0, 0, 0, 0};
-  for (int i0 = lane; i0 < nc; i0 += 128) {
+  // pass 3).  Two independent accumulators per lane hide the exp latency;
+  // they are combined in a fixed order, then across lanes and warps.
+  double s2[2] = {0, 0}, u2[2] = {0, 0}, m2[2] = {0, 0}, a2[2] = {0, 0};
+  for (int i0 = tl; i0 < nc; i0 += 2 * kTeamLanes) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = i0 + 32 * j;
+    for (int j = 0; j < 2; ++j) {
+      const int i = i0 + kTeamLanes * j;
       if (i < nc) {
         const double m = (double)cells[i].m;
         const double e = (double)cells[i].e * scale;
         const double en = e - h * m;
         const double w = cells[i].g * exp(-en / t - shift);
-        s4[j] += w;
-        u4[j] += w * en;
-        m4[j] += w * m;
-        a4[j] += w * fabs(m);
+        s2[j] += w;
+        u2[j] += w * en;
+        m2[j] += w * m;
+        a2[j] += w * fabs(m);
       }
     }
   }
-  const double s = warp_sum((s4[0] + s4[1]) + (s4[2] + s4[3]));
-  const double u = warp_sum((u4[0] + u4[1]) + (u4[2] + u4[3])) / s;
-  const double mean_m = warp_sum((m4[0] + m4[1]) + (m4[2] + m4[3])) / s;
-  const double mean_abs = warp_sum((a4[0] + a4[1]) + (a4[2] + a4[3])) / s;
+  const double s = team_sum(s2[0] + s2[1], 0);
+  const double u = team_sum(u2[0] + u2[1], 1) / s;
+  const double mean_m = team_sum(m2[0] + m2[1], 2) / s;
+  const double mean_abs = team_sum(a2[0] + a2[1], 3) / s;
+  __syncthreads();
 
   // pass 3: central second moments (the two-pass form of thermo.py:75-77;
   // the raw <H^2> - <H>^2 form cancels catastrophically at low T)
-  double e4[4] = {0, 0, 0, 0}, v4[4] = {0, 0, 0, 0};
-  for (int i0 = lane; i0 < nc; i0 += 128) {
+  double e2[2] = {0, 0}, v2[2] = {0, 0};
+  for (int i0 = tl; i0 < nc; i0 += 2 * kTeamLanes) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = i0 + 32 * j;
+    for (int j = 0; j < 2; ++j) {
+      const int i = i0 + kTeamLanes * j;
       if (i < nc) {
         const double m = (double)cells[i].m;
         const double e = (double)cells[i].e * scale;
         const double en = e - h * m;
         const double w = cells[i].g * exp(-en / t - shift);
         const double de = en - u, dm = m - mean_m;
-        e4[j] += w * (de * de);
-        v4[j] += w * (dm * dm);
+        e2[j] += w * (de * de);
+        v2[j] += w * (dm * dm);
       }
     }
   }
-  const double ve = warp_sum((e4[0] + e4[1]) + (e4[2] + e4[3])) / s;
-  const double vm = warp_sum((v4[0] + v4[1]) + (v4[2] + v4[3])) / s;
+  const double ve = team_sum(e2[0] + e2[1], 0) / s;
+  const double vm = team_sum(v2[0] + v2[1], 1) / s;
 
-  if (lane == 0) {
+  if (tl == 0 && point_raw < n_points) {
     const double log_z = shift + log(s);
     double* o = out + (size_t)point * ISD_THERMO_FIELDS;
     o[0] = log_z;
