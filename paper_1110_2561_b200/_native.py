@@ -224,7 +224,7 @@ def thermo_device(counts_ptr, n_spins, n_bonds, scale, fields_ptr, n_fields,
                                n_fields, ctypes.c_void_p(temps_ptr), n_temps,
                                ctypes.c_void_p(out_ptr),
                                ctypes.c_void_p(stream_ptr)))
-    return 1 if n_fields * n_temps > 0 else 0
+    return 2 if n_fields * n_temps > 0 else 0  # K2a compaction + K2b
 
 
 def plan(lat: Lattice, n_configs_hint: int) -> tuple:

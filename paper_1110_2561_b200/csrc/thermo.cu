@@ -9,9 +9,9 @@
 // moments are accumulated as w-weighted sums and divided by s once
 // (sum(w x)/s instead of sum((w/s) x)): same value to ~1e-16 relative.
 //
-// A team of four warps per (h, T) point, two points per CTA.  The CTA first compacts
-// the occupied cells of the table into shared memory, in table order (a
-// block prefix scan), so every warp walks the same cell list; each lane
+// K2a compacts the occupied cells of the table once, in table order (a
+// block prefix scan); K2b gives each (h, T) point a team of four warps that
+// walk the same cell list; each lane
 // takes a fixed strided subset and the partials meet in a fixed xor-shuffle
 // tree.  A point's result therefore does not depend on which other points
 // share the launch (thermo_sweep(...)[0] == partition_point(...) exactly,
@@ -48,27 +48,28 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-__global__ void __launch_bounds__(kThermoThreads)
-    k2_thermo(const unsigned long long* __restrict__ counts, uint32_t n,
-              uint32_t b, double scale, const double* __restrict__ fields,
-              const double* __restrict__ temps, int n_temps, int n_points,
-              double* __restrict__ out) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  Cell* cells = reinterpret_cast<Cell*>(smem);
-  __shared__ int scan[kThermoThreads];
-  __shared__ int n_cells;
+// K2a: compact the occupied cells of the table, in table order, into a
+// scratch list (one CTA: coalesced loads into shared memory, block scan).
+constexpr int kCompactThreads = 1024;
+
+__global__ void __launch_bounds__(kCompactThreads)
+    k2_compact(const unsigned long long* __restrict__ counts, uint32_t n,
+               uint32_t b, Cell* __restrict__ cells, int* __restrict__ n_cells) {
+  __shared__ unsigned long long tab[kMaxBins];
+  __shared__ int scan[kCompactThreads];
   const uint32_t stride = b + 1;
   const uint32_t nbins = (n + 1) * stride;
-
-  // ---- compact the occupied cells, in table order ----
-  const uint32_t per = (nbins + kThermoThreads - 1) / kThermoThreads;
+  for (uint32_t i = threadIdx.x; i < nbins; i += kCompactThreads)
+    tab[i] = counts[i];
+  __syncthreads();
+  const uint32_t per = (nbins + kCompactThreads - 1) / kCompactThreads;
   const uint32_t lo = threadIdx.x * per;
   const uint32_t hi = min(lo + per, nbins);
   int mine = 0;
-  for (uint32_t i = lo; i < hi; ++i) mine += counts[i] != 0;
+  for (uint32_t i = lo; i < hi; ++i) mine += tab[i] != 0;
   scan[threadIdx.x] = mine;
   __syncthreads();
-  for (int o = 1; o < kThermoThreads; o <<= 1) {  // inclusive scan
+  for (int o = 1; o < kCompactThreads; o <<= 1) {  // inclusive scan
     const int v = (int)threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
     __syncthreads();
     scan[threadIdx.x] += v;
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(kThermoThreads)
   }
   int pos = scan[threadIdx.x] - mine;
   for (uint32_t i = lo; i < hi; ++i) {
-    const unsigned long long g = counts[i];
+    const unsigned long long g = tab[i];
     if (!g) continue;
     const int mi = (int)(i / stride), ei = (int)(i - mi * stride);
     cells[pos].g = (double)g;
@@ -84,10 +85,16 @@ __global__ void __launch_bounds__(kThermoThreads)
     cells[pos].e = 2 * ei - (int)b;
     ++pos;
   }
-  if (threadIdx.x == kThermoThreads - 1) n_cells = scan[threadIdx.x];
-  __syncthreads();
-  const int nc = n_cells;
+  if (threadIdx.x == kCompactThreads - 1) *n_cells = scan[threadIdx.x];
+}
 
+// K2b: the observables, a team of kTeam warps per (h, T) point.
+__global__ void __launch_bounds__(kThermoThreads)
+    k2_thermo(const Cell* __restrict__ cells, const int* __restrict__ n_cells,
+              double scale, const double* __restrict__ fields,
+              const double* __restrict__ temps, int n_temps, int n_points,
+              double* __restrict__ out) {
+  const int nc = *n_cells;
   // a team of kTeam warps per point; partial results of the team's warps
   // meet in shared memory in a fixed order (deterministic)
   __shared__ double part[kThermoThreads / 32][4];
@@ -191,15 +198,23 @@ int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
                   void* stream) {
   const int points = n_fields * n_temps;
   if (points <= 0) return 0;
-  const size_t smem = sizeof(Cell) * (size_t)(n_spins + 1) * (n_bonds + 1);
-  static_assert(sizeof(Cell) * kMaxBins <= 227 * 1024, "cell list fits");
-  cudaFuncSetAttribute((const void*)k2_thermo,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bins = (size_t)(n_spins + 1) * (n_bonds + 1);
+  // stream-ordered scratch: safe for concurrent calls on different streams
+  void* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, sizeof(Cell) * bins + 16, st);
+  if (e != cudaSuccess) return -(int)e;
+  Cell* cells = reinterpret_cast<Cell*>(scratch);
+  int* n_cells = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) +
+                                        sizeof(Cell) * bins);
+  k2_compact<<<1, kCompactThreads, 0, st>>>(counts, n_spins, n_bonds, cells,
+                                            n_cells);
   const int grid = (points + kThermoPoints - 1) / kThermoPoints;
-  k2_thermo<<<grid, kThermoThreads, smem, (cudaStream_t)stream>>>(
-      counts, n_spins, n_bonds, scale, fields, temps, n_temps, points, out);
-  cudaError_t e = cudaGetLastError();
-  return e == cudaSuccess ? 1 : -(int)e;
+  k2_thermo<<<grid, kThermoThreads, 0, st>>>(cells, n_cells, scale, fields,
+                                             temps, n_temps, points, out);
+  e = cudaGetLastError();
+  cudaFreeAsync(scratch, st);
+  return e == cudaSuccess ? 2 : -(int)e;
 }
 
 }  // namespace isd
