@@ -49,43 +49,59 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 // K2a: compact the occupied cells of the table, in table order, into a
-// scratch list (one CTA: coalesced loads into shared memory, block scan).
+// scratch list (one CTA, <= 5 bins per thread, shuffle scans).
 constexpr int kCompactThreads = 1024;
+static_assert(kMaxBins <= 5 * kCompactThreads, "<= 5 bins per thread");
 
 __global__ void __launch_bounds__(kCompactThreads)
     k2_compact(const unsigned long long* __restrict__ counts, uint32_t n,
                uint32_t b, Cell* __restrict__ cells, int* __restrict__ n_cells) {
-  __shared__ unsigned long long tab[kMaxBins];
-  __shared__ int scan[kCompactThreads];
+  __shared__ int warp_tot[kCompactThreads / 32];
   const uint32_t stride = b + 1;
   const uint32_t nbins = (n + 1) * stride;
-  for (uint32_t i = threadIdx.x; i < nbins; i += kCompactThreads)
-    tab[i] = counts[i];
-  __syncthreads();
-  const uint32_t per = (nbins + kCompactThreads - 1) / kCompactThreads;
+  const uint32_t per = (nbins + kCompactThreads - 1) / kCompactThreads;  // <= 5
   const uint32_t lo = threadIdx.x * per;
-  const uint32_t hi = min(lo + per, nbins);
+  unsigned long long g[5];
   int mine = 0;
-  for (uint32_t i = lo; i < hi; ++i) mine += tab[i] != 0;
-  scan[threadIdx.x] = mine;
-  __syncthreads();
-  for (int o = 1; o < kCompactThreads; o <<= 1) {  // inclusive scan
-    const int v = (int)threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
-    __syncthreads();
-    scan[threadIdx.x] += v;
-    __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    const uint32_t i = lo + j;
+    g[j] = (j < (int)per && i < nbins) ? counts[i] : 0ull;
+    mine += g[j] != 0;
   }
-  int pos = scan[threadIdx.x] - mine;
-  for (uint32_t i = lo; i < hi; ++i) {
-    const unsigned long long g = tab[i];
-    if (!g) continue;
+  // exclusive prefix of `mine` over the CTA: warp shuffle scan, then the
+  // warp totals scanned by warp 0
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int t = warp_tot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += v;
+    }
+    warp_tot[lane] = t;  // inclusive over warps
+  }
+  __syncthreads();
+  int pos = (warp ? warp_tot[warp - 1] : 0) + incl - mine;
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    if (!g[j]) continue;
+    const uint32_t i = lo + j;
     const int mi = (int)(i / stride), ei = (int)(i - mi * stride);
-    cells[pos].g = (double)g;
+    cells[pos].g = (double)g[j];
     cells[pos].m = (float)(2 * mi - (int)n);
     cells[pos].e = 2 * ei - (int)b;
     ++pos;
   }
-  if (threadIdx.x == kCompactThreads - 1) *n_cells = scan[threadIdx.x];
+  if (threadIdx.x == kCompactThreads - 1) *n_cells = warp_tot[31];
 }
 
 // K2b: the observables, a team of kTeam warps per (h, T) point.
