@@ -216,7 +216,21 @@ int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
   if (points <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t bins = (size_t)(n_spins + 1) * (n_bonds + 1);
-  // stream-ordered scratch: safe for concurrent calls on different streams
+  // stream-ordered scratch: safe for concurrent calls on different streams.
+  // Keep freed blocks in the device's default pool (threshold 64 MiB) so a
+  // steady stream of calls does not go back to the driver every time.
+  static bool pool_ready[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && !pool_ready[dev]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = 64ull << 20;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    pool_ready[dev] = true;
+  }
   void* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&scratch, sizeof(Cell) * bins + 16, st);
   if (e != cudaSuccess) return -(int)e;
