@@ -417,3 +417,16 @@ def test_double_bond_lattices_jit_vs_aot(kw, monkeypatch):
     monkeypatch.setenv("ISD_JIT", "0")
     assert np.array_equal(full(spec), jit)
     assert isd.verify_dos(isd.DoSHistogram(spec, jit)).passed
+
+
+def test_thermo_call_overhead_stays_small():
+    # guards the K2 scratch path: a per-call pool release once cost ~10 ms
+    import time
+    wl = workloads()["c5"]
+    dos = isd.DoSHistogram(wl.spec, _golden_c("c5"))
+    isd.thermo_grid(dos, wl.fields, wl.temps)
+    t0 = time.perf_counter()
+    for _ in range(20):
+        isd.thermo_grid(dos, wl.fields, wl.temps)
+    per_call = (time.perf_counter() - t0) / 20
+    assert per_call < 2e-3, per_call
