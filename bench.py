@@ -73,7 +73,7 @@ def port_lattice(wl):
 def cpu_sample_size(lat, cores, seconds):
     """Per-process index count so `cores` processes take ~`seconds`."""
     from oracle import port
-    probe = 1 << 18
+    probe = min(1 << 18, 1 << lat.n)
     t0 = time.perf_counter()
     port.enumerate_range(lat, 0, probe)
     per = (time.perf_counter() - t0) / probe
