@@ -1,19 +1,26 @@
 """Scaling harness over shard counts.
 
-Mirrors /root/reference/pkg/src/isingdos/bench.py: min-of-repeats wall
-time per shard count, a hard identity check of every run against the
-1-shard result (`ResultMismatchError`), and the same CSV report
-(`rows,cols,depth,N,workers,wall_seconds,speedup`).  Here a "worker" is a
-shard mapped onto the visible GPUs by `full_dos_timed`; records add the
-configurations/s and the per-shard device time.  `full_dos_timed` is looked
-up as a module global, as in the reference (bench.py:10, 52, 59), so tests
-can substitute it.
+Same contract as the reference harness (/root/reference/pkg/src/isingdos/
+bench.py:29-95): for each shard count the fastest of `repeats` complete
+walks is kept, every walk must reproduce the single-shard table exactly or
+`ResultMismatchError` is raised, and the report is the CSV
+``rows,cols,depth,N,workers,wall_seconds,speedup`` sorted by (N, workers)
+with floats written losslessly.  On this engine a "worker" is one shard of
+`full_dos_timed` spread over the visible GPUs, and each record also carries
+the configurations/s of its best walk.  `full_dos_timed` is resolved as a
+module global at call time (as the reference does) so tests can patch it.
 """
 
 from dataclasses import dataclass, field
 
 from .enumeration import full_dos_timed
 from .lattice import LatticeSpec
+
+REPORT_HEADER = "rows,cols,depth,N,workers,wall_seconds,speedup"
+# report column -> parser, in column order
+_REPORT_COLUMNS = (("rows", int), ("cols", int), ("depth", int), ("N", int),
+                   ("workers", int), ("wall_seconds", float),
+                   ("speedup", float))
 
 
 class ResultMismatchError(RuntimeError):
@@ -30,60 +37,68 @@ class BenchRecord:
     configs_per_second: float = 0.0
 
 
-def run_bench(spec: LatticeSpec, worker_counts, repeats: int = 3):
-    counts = list(worker_counts)
+def _check_arguments(counts: list, repeats: int) -> None:
     if not counts:
         raise ValueError("worker_counts must be nonempty")
-    if any(not isinstance(p, int) or p < 1 for p in counts):
+    bad = [p for p in counts if not isinstance(p, int) or p < 1]
+    if bad:
         raise ValueError(f"worker counts must be positive integers: {counts}")
     if repeats < 1:
         raise ValueError(f"repeats must be >= 1, got {repeats}")
-    reference, ref_wall, _ = full_dos_timed(spec, workers=1)
+
+
+def _fastest_walk(spec: LatticeSpec, shards: int, repeats: int, expected):
+    """Best (wall, per-shard times) of `repeats` verified walks."""
+    trials = []
+    for _ in range(repeats):
+        table, wall, per_shard = full_dos_timed(spec, workers=shards)
+        if table != expected:
+            raise ResultMismatchError(
+                f"{shards}-worker run disagrees with the 1-worker result "
+                f"on {spec.rows}x{spec.cols}x{spec.depth}")
+        trials.append((wall, per_shard))
+    return min(trials, key=lambda t: t[0])
+
+
+def run_bench(spec: LatticeSpec, worker_counts, repeats: int = 3):
+    counts = list(worker_counts)
+    _check_arguments(counts, repeats)
+    expected, single_wall, _ = full_dos_timed(spec, workers=1)
     records = []
-    for p in counts:
-        best_wall = best_per = None
-        for _ in range(repeats):
-            hist, wall, per_worker = full_dos_timed(spec, workers=p)
-            if hist != reference:
-                raise ResultMismatchError(
-                    f"{p}-worker run disagrees with the 1-worker result "
-                    f"on {spec.rows}x{spec.cols}x{spec.depth}")
-            if best_wall is None or wall < best_wall:
-                best_wall, best_per = wall, per_worker
-        records.append(BenchRecord(
-            spec=spec, num_workers=p, wall_seconds=best_wall,
-            per_worker_seconds=best_per,
-            configs_per_second=spec.num_configs / best_wall))
-    baseline = next((r.wall_seconds for r in records if r.num_workers == 1),
-                    ref_wall)
+    for shards in counts:
+        wall, per_shard = _fastest_walk(spec, shards, repeats, expected)
+        records.append(BenchRecord(spec, shards, wall, per_shard,
+                                   configs_per_second=spec.num_configs / wall))
+    # speed-ups are relative to the measured 1-shard point when the sweep
+    # has one, else to the verification walk
+    ones = [r.wall_seconds for r in records if r.num_workers == 1]
+    base = ones[0] if ones else single_wall
     for r in records:
-        r.speedup_vs_one = baseline / r.wall_seconds
+        r.speedup_vs_one = base / r.wall_seconds
     return records
 
 
-REPORT_HEADER = "rows,cols,depth,N,workers,wall_seconds,speedup"
-
-
 def emit_scaling_report(records) -> str:
-    records = list(records)
-    if not records:
+    ordered = sorted(records, key=lambda r: (r.spec.num_spins, r.num_workers))
+    if not ordered:
         raise ValueError("no records to report")
-    rows = [REPORT_HEADER]
-    for r in sorted(records, key=lambda r: (r.spec.num_spins, r.num_workers)):
-        s = r.spec
-        rows.append(f"{s.rows},{s.cols},{s.depth},{s.num_spins},"
-                    f"{r.num_workers},{r.wall_seconds!r},{r.speedup_vs_one!r}")
-    return "\n".join(rows) + "\n"
+    body = []
+    for r in ordered:
+        fields = (r.spec.rows, r.spec.cols, r.spec.depth, r.spec.num_spins,
+                  r.num_workers, repr(r.wall_seconds), repr(r.speedup_vs_one))
+        body.append(",".join(str(f) for f in fields))
+    return "\n".join([REPORT_HEADER] + body) + "\n"
 
 
 def parse_scaling_report(text: str) -> list[dict]:
-    lines = [ln for ln in text.splitlines() if ln.strip()]
-    if not lines or lines[0] != REPORT_HEADER:
+    rows = [ln for ln in text.splitlines() if ln.strip()]
+    if not rows or rows[0] != REPORT_HEADER:
         raise ValueError(f"expected header {REPORT_HEADER!r}")
-    out = []
-    for ln in lines[1:]:
-        rows, cols, depth, n, workers, wall, speedup = ln.split(",")
-        out.append({"rows": int(rows), "cols": int(cols), "depth": int(depth),
-                    "N": int(n), "workers": int(workers),
-                    "wall_seconds": float(wall), "speedup": float(speedup)})
-    return out
+    parsed = []
+    for row in rows[1:]:
+        cells = row.split(",")
+        if len(cells) != len(_REPORT_COLUMNS):
+            raise ValueError(f"malformed report row {row!r}")
+        parsed.append({name: cast(cell) for (name, cast), cell
+                       in zip(_REPORT_COLUMNS, cells)})
+    return parsed

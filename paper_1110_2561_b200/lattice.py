@@ -41,6 +41,36 @@ TABLE_ROWS_CAP = 16
 BOUNDARIES = ("periodic", "free")
 
 
+def _check_geometry(rows, cols, depth) -> None:
+    """The reference's geometry rules and messages (lattice.py:50-70)."""
+    for label, value in (("rows", rows), ("cols", cols), ("depth", depth)):
+        if isinstance(value, bool) or not isinstance(value, int):
+            raise ValueError(f"{label} must be an integer, got {value!r}")
+    if min(rows, cols) < 2:
+        raise ValueError("degenerate periodic axis: rows and cols must be "
+                         f">= 2, got rows={rows} cols={cols}")
+    if depth < 1:
+        raise ValueError(f"depth must be >= 1, got {depth}")
+    if rows > MAX_ROWS:
+        raise ValueError(f"rows={rows} exceeds the cap of {MAX_ROWS}")
+    spins = rows * cols * depth
+    if spins > MAX_SPINS:
+        raise ValueError(f"{spins} spins exceeds the cap of {MAX_SPINS} "
+                         "(2^N must fit a 64-bit index with headroom)")
+
+
+def _check_signs(signs, n_bonds: int) -> tuple:
+    signs = tuple(signs)
+    if len(signs) != n_bonds:
+        raise ValueError(f"bond_signs has {len(signs)} entries, lattice has "
+                         f"{n_bonds} bonds")
+    bad = next((x for x in signs if isinstance(x, bool) or x not in (1, -1)),
+               None)
+    if bad is not None:
+        raise ValueError(f"bond signs must be +1 or -1, got {bad!r}")
+    return tuple(int(x) for x in signs)
+
+
 @dataclass(frozen=True)
 class LatticeSpec:
     """Geometry and couplings of a finite Ising lattice.
@@ -61,44 +91,19 @@ class LatticeSpec:
     bond_signs: tuple | None = field(default=None, kw_only=True)
 
     def __post_init__(self):
-        for name in ("rows", "cols", "depth"):
-            v = getattr(self, name)
-            if not isinstance(v, int) or isinstance(v, bool):
-                raise ValueError(f"{name} must be an integer, got {v!r}")
-        if self.rows < 2 or self.cols < 2:
-            raise ValueError(
-                f"degenerate periodic axis: rows and cols must be >= 2, "
-                f"got rows={self.rows} cols={self.cols}"
-            )
-        if self.depth < 1:
-            raise ValueError(f"depth must be >= 1, got {self.depth}")
-        if self.rows > MAX_ROWS:
-            raise ValueError(f"rows={self.rows} exceeds the cap of {MAX_ROWS}")
-        n = self.rows * self.cols * self.depth
-        if n > MAX_SPINS:
-            raise ValueError(
-                f"{n} spins exceeds the cap of {MAX_SPINS} "
-                f"(2^N must fit a 64-bit index with headroom)"
-            )
-        if self.coupling == 0:
-            raise ValueError("coupling J must be nonzero")
+        _check_geometry(self.rows, self.cols, self.depth)
         j = self.coupling
+        if j == 0:
+            raise ValueError("coupling J must be nonzero")
         if isinstance(j, float) and j.is_integer():
+            # integral J stays an int so energies remain exact integers
             object.__setattr__(self, "coupling", int(j))
         if self.boundary not in BOUNDARIES:
             raise ValueError(
                 f"boundary must be one of {BOUNDARIES}, got {self.boundary!r}")
         if self.bond_signs is not None:
-            signs = tuple(self.bond_signs)
-            if len(signs) != self.num_bonds:
-                raise ValueError(
-                    f"bond_signs has {len(signs)} entries, lattice has "
-                    f"{self.num_bonds} bonds")
-            for s in signs:
-                if isinstance(s, bool) or s not in (1, -1):
-                    raise ValueError(f"bond signs must be +1 or -1, got {s!r}")
             object.__setattr__(self, "bond_signs",
-                               tuple(int(s) for s in signs))
+                               _check_signs(self.bond_signs, self.num_bonds))
 
     # -- derived sizes (lattice.py:77-100) ---------------------------------
 
@@ -136,25 +141,26 @@ class LatticeSpec:
         return self.periodic and self.bond_signs is None
 
     def word_neighbor_pairs(self) -> list[tuple[int, int]]:
-        """Inter-word bond pairs along cols (and layers in 3D).
+        """Inter-word bond pairs: the col axis, then (3D) the layer axis.
 
-        Same order as lattice.py:102-119; free boundaries omit the wrap
-        pairs.  A periodic axis of length 2 lists both orders (double bond).
+        Order of lattice.py:102-119; free boundaries leave out the wrap
+        pairs, and a periodic axis of length 2 lists both orders of the
+        same two words (its double bond).
         """
-        pairs = []
-        for layer in range(self.depth):
-            base = layer * self.cols
-            for c in range(self.cols):
-                if self.periodic or c + 1 < self.cols:
-                    pairs.append((base + c, base + (c + 1) % self.cols))
-        if self.depth > 1:
-            for layer in range(self.depth):
-                for c in range(self.cols):
-                    if self.periodic or layer + 1 < self.depth:
-                        pairs.append((layer * self.cols + c,
-                                      ((layer + 1) % self.depth) * self.cols
-                                      + c))
-        return pairs
+        cols, depth = self.cols, self.depth
+
+        def word(c, layer):
+            return layer * cols + c
+
+        col_pairs = [(word(c, layer), word((c + 1) % cols, layer))
+                     for layer in range(depth) for c in range(cols)
+                     if self.periodic or c < cols - 1]
+        if depth == 1:
+            return col_pairs
+        layer_pairs = [(word(c, layer), word(c, (layer + 1) % depth))
+                       for layer in range(depth) for c in range(cols)
+                       if self.periodic or layer < depth - 1]
+        return col_pairs + layer_pairs
 
     # -- bond geometry ------------------------------------------------------
 
@@ -236,25 +242,24 @@ class Configuration:
 
 def decode_config(spec: LatticeSpec, index: int) -> Configuration:
     """Split an index into its column bit-words (lattice.py:130-137)."""
-    if not 0 <= index < spec.num_configs:
+    if index < 0 or index >= spec.num_configs:
         raise ValueError(f"index {index} outside [0, 2^{spec.num_spins})")
-    mask = spec.word_mask
-    words = tuple((index >> (w * spec.rows)) & mask
-                  for w in range(spec.num_words))
-    return Configuration(index=index, words=words)
+    h, mask = spec.rows, spec.word_mask
+    return Configuration(index, tuple((index >> shift) & mask for shift
+                                      in range(0, h * spec.num_words, h)))
 
 
 def encode_words(spec: LatticeSpec, words) -> int:
     """Inverse of decode_config (lattice.py:140-148)."""
     if len(words) != spec.num_words:
         raise ValueError(f"expected {spec.num_words} words, got {len(words)}")
-    index = 0
-    for w, word in enumerate(words):
-        if not 0 <= word <= spec.word_mask:
+    packed = 0
+    for word in reversed(words):
+        if word < 0 or word > spec.word_mask:
             raise ValueError(
                 f"word {word:#x} has stray bits above row {spec.rows}")
-        index |= word << (w * spec.rows)
-    return index
+        packed = (packed << spec.rows) | word
+    return packed
 
 
 @dataclass(frozen=True, eq=False)
@@ -332,17 +337,17 @@ def total_energy(config: Configuration, spec: LatticeSpec,
         unit = 2 * e_idx - spec.num_bonds
         scale = abs(spec.coupling)
         return unit if scale == 1 else scale * unit
-    words = config.words
-    if tables is not None:
-        aligned = sum(aligned_column_bonds(w, tables) for w in words)
-        aligned += sum(aligned_row_bonds(words[a], words[b], tables)
-                       for a, b in spec.word_neighbor_pairs())
+    words, pairs = config.words, spec.word_neighbor_pairs()
+    if tables is None:
+        # direct bit counting (columns taller than the table cap)
+        h = spec.rows
+        misaligned = sum(popcount(w ^ circular_shift(w, h)) for w in words)
+        misaligned += sum(popcount(words[a] ^ words[b]) for a, b in pairs)
+        aligned = h * (len(words) + len(pairs)) - misaligned
     else:
-        rows = spec.rows
-        aligned = sum(rows - popcount(w ^ circular_shift(w, rows))
-                      for w in words)
-        aligned += sum(rows - popcount(words[a] ^ words[b])
-                       for a, b in spec.word_neighbor_pairs())
+        aligned = (sum(aligned_column_bonds(w, tables) for w in words) +
+                   sum(aligned_row_bonds(words[a], words[b], tables)
+                       for a, b in pairs))
     return -spec.coupling * (2 * aligned - spec.num_bonds)
 
 
