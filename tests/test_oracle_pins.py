@@ -141,3 +141,36 @@ def test_unpinned_n36_goldens_agree_across_two_formulations(mask_json,
         pytest.skip("naive-route golden not generated")
     assert np.array_equal(read_json_table(mask_json)[1],
                           read_json_table(naive_json)[1])
+
+
+def _random_small_lattices(seed, count):
+    import random
+    rng = random.Random(seed)
+    out = []
+    while len(out) < count:
+        rows, cols, depth = rng.randint(2, 5), rng.randint(2, 5), \
+            rng.choice((1, 1, 2, 3))
+        n = rows * cols * depth
+        if n > 12:
+            continue
+        periodic = rng.random() < 0.5
+        j = rng.choice((1, -1, 0.5, -2.5))
+        nb = len(naive.bond_pairs(rows, cols, depth, periodic))
+        signs = naive.random_signs(nb, rng.randrange(1000)) \
+            if rng.random() < 0.5 else None
+        out.append((rows, cols, depth, j, periodic, signs))
+    return out
+
+
+@pytest.mark.parametrize("case", _random_small_lattices(77, 16))
+def test_three_oracles_agree_on_random_small_lattices(case):
+    # the per-bond naive loops, the numpy bond-mask port and the C walk
+    # (both of its modes) are independent restatements; they must agree on
+    # every geometry the GPU fuzz tests draw from
+    rows, cols, depth, j, periodic, signs = case
+    want = naive.full_dos(rows, cols, depth, j, periodic, signs)
+    lat = port.Lattice(rows, cols, depth, j, periodic, signs)
+    assert np.array_equal(port.enumerate_range(lat, 0, 1 << lat.n), want)
+    for mode in ("mask", "naive"):
+        assert np.array_equal(cref.table(rows, cols, depth, j, periodic, signs,
+                                         mode=mode, threads=2), want)
