@@ -210,14 +210,17 @@ def ncu_traffic(config):
     return total
 
 
-def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1, kernel="k1"):
+def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1, kernel="k1",
+             cfg_per_red=1):
     """Two rooflines for the dominant kernel (k1_hoisted).
 
     `roofline`: the pipe the kernel is bound by (ncu: shared-memory
-    wavefronts at 94-95% of peak).  k1_hoisted issues exactly one
-    shared-memory reduction lane per configuration, so the algorithmic work
-    is 1 RED lane per configuration and the peak is the measured
-    conflict-free RED.shared rate (K0 probe 3) x SMs x SM clock.
+    wavefronts at 94-97% of peak).  k1_hoisted issues one shared-memory
+    reduction lane per `cfg_per_red` configurations — 1 with unpaired
+    copies, 2 with paired copies (one RED counts a configuration and its
+    partner with copy site 6 flipped, isd_plan_info.pair_mode) — so the
+    peak is the measured conflict-free RED.shared rate (K0 probe 3) x SMs x
+    SM clock x cfg_per_red.
 
     `roofline_int_pipe`: BASELINE.md §4's integer-pipe roofline of the
     canonical formulation (POPC and ALU ops per
@@ -234,15 +237,19 @@ def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1, kernel="k1"):
     f = mhz * 1e6
     ach = cfg_per_launch / (ms_k1 / 1e3)
     p_red = cal["red_shared_spread"]["lanes_per_clk_sm"]
-    peak_red = sm_count * f * p_red
+    peak_red = sm_count * f * p_red * cfg_per_red
     roof = {
         "bound": "smem-atomic", "achieved": ach / 1e9, "peak": peak_red / 1e9,
         "unit": "Gconf/s", "frac": ach / peak_red,
         "traffic": ncu_traffic(wl.name),
         "kernel": kernel, "kernel_ms": ms_k1,
-        "algorithmic_work": "1 RED.shared lane per configuration",
+        "algorithmic_work": ("1 RED.shared lane per configuration"
+                             if cfg_per_red == 1 else
+                             f"1 RED.shared lane per {cfg_per_red} "
+                             "configurations (paired copies)"),
         "peak_source": f"K0 red_shared_spread {p_red:.2f} lanes/clk/SM x "
-                       f"{sm_count} SMs x {mhz:.0f} MHz (measured, this GPU)",
+                       f"{sm_count} SMs x {mhz:.0f} MHz x {cfg_per_red} "
+                       "configurations/lane (measured, this GPU)",
         "traffic_source": "ncu --set full, profiles/r1_ncu_k1_*_<config>.txt",
     }
     popc_ops, alu_ops = canonical_ops(wl.spec)
@@ -438,8 +445,16 @@ def run_b200(args, wl):
 
     # ---- roofline ------------------------------------------------------------
     sm_count = _native.sm_count(local)
+    # the plan the walk ran with (autotuned; cached per lattice and size)
+    from paper_1110_2561_b200.enumeration import native_lattice as _nl
+    _, plan = _native.plan(_nl(wl.spec), n_cfg // world)
     roof, roof_int = roofline(wl, cal, clk, sm_count, n_cfg // world, ms_k1,
-                              kernel_path)
+                              kernel_path, 2 if plan.pair_mode else 1)
+    roof["plan"] = {"pair_mode": int(plan.pair_mode),
+                    "copy_sites": list(plan.copy_site),
+                    "loop_bits": int(plan.l),
+                    "hist_words": int(plan.hist_words),
+                    "model_wavefronts_per_red": round(plan.est_wavefronts, 4)}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

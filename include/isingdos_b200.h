@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define ISD_ABI_VERSION 1
+#define ISD_ABI_VERSION 2
 #define ISD_MAX_CLASSES 8
 #define ISD_MAX_SPINS 40   /* lattice.py:24 MAX_SPINS */
 
@@ -163,6 +163,18 @@ typedef struct isd_plan_info {
                                 site: a "domino"); lane L's run is the
                                 slot's run XOR the vectors of L's bits  */
   double   est_wavefronts;   /* predicted smem wavefronts per warp RED  */
+  /* Paired copies (pair_mode 1): copy bit 6's site q is not a register copy
+   * of its own.  One RED counts the configuration with q down AND its
+   * partner with q up: it lands in pattern plane p = (bonds of q
+   * unsatisfied while q is down), word = base word + p*pair_words, and the
+   * flush credits the partner to (m + 1, e + pair_degree - 2p).  Halves the
+   * shared-memory REDs per configuration at the cost of pair_degree + 1
+   * planes of base_words words each. */
+  uint32_t pair_mode;
+  int32_t  pair_degree;      /* degree of copy site 6 (all bonds)       */
+  uint32_t pair_words;       /* stride between pattern planes (words)   */
+  uint32_t base_words;       /* words of the unpaired layout            */
+  double   est_per_config;   /* est_wavefronts / configurations per RED */
 } isd_plan_info;
 
 int isd_plan(const isd_lattice* lat, uint64_t n_configs_hint,

@@ -61,6 +61,9 @@ class PlanInfo(ctypes.Structure):
         ("plane_words", ctypes.c_uint32), ("hist_words", ctypes.c_uint32),
         ("lane_mask", ctypes.c_uint64), ("lane_vec", ctypes.c_uint64 * 5),
         ("est_wavefronts", ctypes.c_double),
+        ("pair_mode", ctypes.c_uint32), ("pair_degree", ctypes.c_int32),
+        ("pair_words", ctypes.c_uint32), ("base_words", ctypes.c_uint32),
+        ("est_per_config", ctypes.c_double),
     ]
 
 
@@ -120,7 +123,7 @@ def load():
                      "isd_calibrate", "isd_device_count", "isd_sm_count",
                      "isd_abi_version", "isd_mirror_async"):
             getattr(lib, name).restype = ctypes.c_int
-        if lib.isd_abi_version() != 1:
+        if lib.isd_abi_version() != 2:
             raise ImportError("isingdos-b200 ABI version mismatch")
         _lib = lib
         return lib

@@ -137,6 +137,7 @@ static std::string plan_key(const isd_lattice* lat, uint64_t hint) {
   std::string key(reinterpret_cast<const char*>(lat), sizeof(*lat));
   key.push_back((char)l);
   if (const char* v = std::getenv("ISD_COPY_VARIANT")) key += v;
+  if (const char* v = std::getenv("ISD_PAIR")) key += std::string("|pair") + v;
   return key;
 }
 
@@ -394,6 +395,8 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
         m ^= info.lane_vec[v];
       }
       info.hist_words = lat->n_spins * a + lat->n_bonds * b + pw + 1;
+      info.base_words = info.hist_words;
+      info.pair_mode = 0;  // the knob describes an unpaired layout
     }
   }
   HoistParams hp;

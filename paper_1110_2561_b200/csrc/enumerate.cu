@@ -149,9 +149,12 @@ struct RuntimeTraits {
   __device__ uint32_t jn2v(int q) const { return P.jn2v[q]; }
   __device__ int32_t degree(int q) const { return P.degree[q]; }
   __device__ uint32_t koff(int c) const { return (uint32_t)P.koff[c]; }
+  __device__ uint32_t pair_bytes() const { return P.pair_bytes; }
+  __device__ uint32_t pair_words() const { return P.pair_words; }
+  __device__ int32_t pair_deg() const { return P.pair_deg; }
 };
 
-template <int NC, bool DOUBLE>
+template <int NC, bool DOUBLE, bool PAIR>
 __global__ void __launch_bounds__(kThreads)
     k1_hoisted(const __grid_constant__ HoistParams P,
                unsigned long long* __restrict__ out) {
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(kThreads)
   IsdLanes lanes;
 #pragma unroll
   for (int i = 0; i < 5; ++i) lanes.v[i] = P.lane_vec[i];
-  k1_hoisted_body<NC, DOUBLE>(L, P.run_begin, P.run_end - P.run_begin,
+  k1_hoisted_body<NC, DOUBLE, PAIR>(L, P.run_begin, P.run_end - P.run_begin,
                               P.hi_step, P.lane_mask, lanes, hist, out);
 }
 
@@ -242,16 +245,16 @@ int launch_canonical(const CanonParams& p, unsigned long long* out,
   }
 }
 
-template <int NC, bool D>
+template <int NC, bool D, bool PR>
 static int launch_hoist_t(const HoistParams& p, unsigned long long* out,
                           int sm_count, cudaStream_t st) {
   const size_t smem = (size_t)p.n_hist * p.hist_words * 4;
-  const void* fn = (const void*)k1_hoisted<NC, D>;
+  const void* fn = (const void*)k1_hoisted<NC, D, PR>;
   int grid = blocks_for(fn, smem, sm_count);
   const uint64_t runs = p.run_end - p.run_begin;
   const uint64_t need = (runs + kThreads - 1) / kThreads;
   if (need < (uint64_t)grid) grid = (int)(need ? need : 1);
-  k1_hoisted<NC, D><<<grid, kThreads, smem, st>>>(p, out);
+  k1_hoisted<NC, D, PR><<<grid, kThreads, smem, st>>>(p, out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 1 : -(int)e;
 }
@@ -260,11 +263,15 @@ int launch_hoisted(const HoistParams& p, unsigned long long* out, int sm_count,
                    void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const bool dbl = p.has_double != 0;
+  const bool pr = p.pair != 0;
   switch (p.n_classes) {
-#define CASE(NC)                                                   \
-  case NC:                                                         \
-    return dbl ? launch_hoist_t<NC, true>(p, out, sm_count, st)    \
-               : launch_hoist_t<NC, false>(p, out, sm_count, st);
+#define CASE(NC)                                                              \
+  case NC:                                                                    \
+    if (pr)                                                                   \
+      return dbl ? launch_hoist_t<NC, true, true>(p, out, sm_count, st)       \
+                 : launch_hoist_t<NC, false, true>(p, out, sm_count, st);     \
+    return dbl ? launch_hoist_t<NC, true, false>(p, out, sm_count, st)        \
+               : launch_hoist_t<NC, false, false>(p, out, sm_count, st);
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
     default:

@@ -73,7 +73,18 @@ struct HoistParams {
   int32_t degree[kCopyBits];                 // d_q
   int32_t koff[kCopies];         // constant byte offset of copy c:
                                  // popc(c) row_bytes + e_bytes unsat_cc(c)
+                                 // (+ pair_bytes u_q(c) for paired copies)
+  // paired copies (isd_plan_info.pair_mode): copy bit 6 is counted through
+  // pattern planes instead of register copies
+  uint32_t pair;                 // 0 / 1
+  uint32_t pair_bytes;           // 4 * pair_words
+  uint32_t pair_words;           // stride between pattern planes
+  int32_t pair_deg;              // D: degree of copy site 6
 };
+
+// Largest paired histogram (words): two CTAs of 512 threads must still fit
+// an SM's shared memory.
+constexpr uint32_t kMaxPairWords = 28000;
 
 // ---- host side -----------------------------------------------------------
 int validate_lattice(const isd_lattice* lat, char* err, size_t errlen);

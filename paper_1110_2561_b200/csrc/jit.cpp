@@ -136,6 +136,11 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
   uint32_t koff[kCopies];
   for (int c = 0; c < kCopies; ++c) koff[c] = (uint32_t)P.koff[c];
   emit_switch(o, "uint32_t", "koff", koff, kCopies, "u");
+  c32("pair_bytes", P.pair_bytes);
+  c32("pair_words", P.pair_words);
+  o << "  __device__ __forceinline__ static constexpr int32_t pair_deg() "
+       "{ return "
+    << P.pair_deg << "; }\n";
   o << "};\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << kThreads
     << ") k1_jit(unsigned long long run_begin, unsigned long long nruns,\n"
@@ -145,8 +150,8 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
        "  extern __shared__ __align__(16) unsigned int hist[];\n"
        "  const JitTraits L;\n"
        "  k1_hoisted_body<"
-    << nc << ", " << (dbl ? "true" : "false")
-    << ">(L, run_begin, nruns, hi_step, lane_mask, lanes, hist, out);\n}\n";
+    << nc << ", " << (dbl ? "true" : "false") << ", "
+    << (P.pair ? "true" : "false") << ">(L, run_begin, nruns, hi_step, lane_mask, lanes, hist, out);\n}\n";
   return o.str();
 }
 

@@ -31,7 +31,23 @@ __device__ __forceinline__ void isd_red_shared_inc(unsigned int addr) {
   asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
 }
 
-template <int NC, bool DOUBLE, class T>
+// word of bin (m, e) in the unpaired layout
+template <class T>
+__device__ __forceinline__ unsigned int isd_bin_word(const T& L, unsigned int m,
+                                                     unsigned int e) {
+  if (L.e_mode()) {
+    const unsigned int par = e & 1u;
+    return m * L.row_words() + ((e - par) >> 1) * L.e_words() +
+           par * L.plane_words();
+  }
+  return m * L.row_words() + e * L.e_words();
+}
+
+// PAIR: copy bit 6 is not unrolled; one RED counts the configuration with
+// that site down and its partner with it up, in pattern plane p (= the
+// site's unsatisfied bonds while down), and the flush credits the partner
+// to (m + 1, e + D - 2p).
+template <int NC, bool DOUBLE, bool PAIR, class T>
 __device__ __forceinline__ void k1_hoisted_body(
     const T& L, unsigned long long run_begin, unsigned long long nruns,
     unsigned long long hi_step, unsigned long long lane_mask,
@@ -115,12 +131,14 @@ __device__ __forceinline__ void k1_hoisted_body(
         e += __popc((jb ^ __funnelshift_rc(jb, 0u, L.shift(c)) ^ cst[c]) &
                     L.mvar(c));
       unsigned int d[7];
+      unsigned int pair_off = 0;
 #pragma unroll
       for (int q = 0; q < 7; ++q) {
         int nq = npr[q] + __popc((jb ^ L.jn1v(q)) & L.nm1v(q));
         if (DOUBLE) nq += __popc((jb ^ L.jn2v(q)) & L.nm2v(q));
         e += nq;
         d[q] = (unsigned int)((int)L.e_bytes() * (L.degree(q) - 2 * nq));
+        if (PAIR && q == 6) pair_off = (unsigned int)nq * L.pair_bytes();
       }
       const unsigned int par = (par_run + __popc(jb & odd_loop)) & 1u;
       // a[c] carries no per-copy constant: addr(c) = a[c] + koff(c), where
@@ -130,7 +148,7 @@ __device__ __forceinline__ void k1_hoisted_body(
       // leaf spawning its three siblings in bits 5 and 6.
       const unsigned int a0 = a_run + (unsigned int)__popc(jb) * L.row_bytes() +
                               (unsigned int)e * L.e_bytes() +
-                              par * (unsigned int)L.plane_bytes();
+                              par * (unsigned int)L.plane_bytes() + pair_off;
       unsigned int a[32];
 #pragma unroll
       for (int cl = 0; cl < 32; ++cl) {
@@ -141,16 +159,18 @@ __device__ __forceinline__ void k1_hoisted_body(
           a[cl] = a[cl ^ (1 << top)] + d[top];
         }
         const unsigned int b1 = a[cl] + d[5];
-        const unsigned int b2 = a[cl] + d[6];
-        const unsigned int b3 = b1 + d[6];
         ISD_CHECK_ADDR(a[cl] + L.koff(cl), hbase, hbytes);
         isd_red_shared_inc(a[cl] + L.koff(cl));
         ISD_CHECK_ADDR(b1 + L.koff(cl + 32), hbase, hbytes);
         isd_red_shared_inc(b1 + L.koff(cl + 32));
-        ISD_CHECK_ADDR(b2 + L.koff(cl + 64), hbase, hbytes);
-        isd_red_shared_inc(b2 + L.koff(cl + 64));
-        ISD_CHECK_ADDR(b3 + L.koff(cl + 96), hbase, hbytes);
-        isd_red_shared_inc(b3 + L.koff(cl + 96));
+        if (!PAIR) {
+          const unsigned int b2 = a[cl] + d[6];
+          const unsigned int b3 = b1 + d[6];
+          ISD_CHECK_ADDR(b2 + L.koff(cl + 64), hbase, hbytes);
+          isd_red_shared_inc(b2 + L.koff(cl + 64));
+          ISD_CHECK_ADDR(b3 + L.koff(cl + 96), hbase, hbytes);
+          isd_red_shared_inc(b3 + L.koff(cl + 96));
+        }
       }
       jb = (jb - L.loop_mask()) & L.loop_mask();  // next subset
     }
@@ -159,18 +179,29 @@ __device__ __forceinline__ void k1_hoisted_body(
   // ---- flush: word (m, e) -> table bin (m, e) ----
   for (unsigned int bin = threadIdx.x; bin < L.nbins(); bin += blockDim.x) {
     const unsigned int m = bin / L.stride(), e = bin - m * L.stride();
-    unsigned int word;
-    if (L.e_mode()) {
-      const unsigned int par = e & 1u;
-      if (L.odd_mask() == 0 && par != L.e_parity()) continue;  // always 0
-      word = m * L.row_words() + ((e - par) >> 1) * L.e_words() +
-             par * L.plane_words();
-    } else {
-      word = m * L.row_words() + e * L.e_words();
-    }
+    // single parity plane: bins of the other parity are always 0 (and
+    // their words alias)
+    if (L.e_mode() && L.odd_mask() == 0 && (e & 1u) != L.e_parity()) continue;
+    const unsigned int word = isd_bin_word(L, m, e);
     unsigned long long s = 0;
-    for (unsigned int h = 0; h < L.n_hist(); ++h)
-      s += hist[h * L.hist_words() + word];
+    for (unsigned int h = 0; h < L.n_hist(); ++h) {
+      const unsigned int* hh = hist + h * L.hist_words();
+      if constexpr (PAIR) {
+        // the paired site down: this bin, every pattern plane
+        for (int p = 0; p <= L.pair_deg(); ++p)
+          s += hh[word + p * L.pair_words()];
+        // the paired site up: partners of (m - 1, e - D + 2p) in plane p
+        if (m > 0)
+          for (int p = 0; p <= L.pair_deg(); ++p) {
+            const int es = (int)e - L.pair_deg() + 2 * p;
+            if (es < 0 || es >= (int)L.stride()) continue;
+            s += hh[isd_bin_word(L, m - 1, (unsigned int)es) +
+                    p * L.pair_words()];
+          }
+      } else {
+        s += hh[word];
+      }
+    }
     if (s) atomicAdd(out + bin, s);
   }
 }

@@ -205,6 +205,33 @@ static void lane_candidates(const isd_lattice* lat, const isd_plan_info* info,
   }
 }
 
+static int site_degree(const isd_lattice* lat, int site) {
+  int d = 0;
+  for (uint32_t q = 0; q < lat->n_classes; ++q) {
+    const isd_bond_class& cl = lat->classes[q];
+    d += (int)((cl.bond_mask >> site) & 1);
+    if (site >= (int)cl.shift) d += (int)((cl.bond_mask >> (site - cl.shift)) & 1);
+  }
+  return d;
+}
+
+static int energy_of(const isd_lattice* lat, uint64_t x) {
+  int e = 0;
+  for (uint32_t q = 0; q < lat->n_classes; ++q) {
+    const isd_bond_class& cl = lat->classes[q];
+    e += popc64(((x ^ (x >> cl.shift)) ^ cl.jneg_mask) & cl.bond_mask);
+  }
+  return e;
+}
+
+// ISD_PAIR: unset = let the model / autotuner choose, 0 = unpaired layouts
+// only, 1 = paired layouts only (when one fits shared memory)
+static int pair_policy() {
+  const char* v = std::getenv("ISD_PAIR");
+  if (!v || !*v) return -1;
+  return std::atoi(v) ? 1 : 0;
+}
+
 static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
                           std::vector<isd_plan_info>* ranked, bool wide,
                           int walk_bits) {
@@ -214,38 +241,79 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   const int emax_half = b / 2;  // largest (e - par)/2
   default_lanes(&info->lane_mask, info->lane_vec);
   info->est_wavefronts = 0;
-  // candidate layouts (row_words A, e_words B, plane_words P)
+  info->est_per_config = 0;
+  info->pair_mode = 0;
+  const int pair_site = info->copy_site[kCopyBits - 1];
+  const int pair_deg = site_degree(lat, pair_site);
+  info->pair_degree = pair_deg;
+  // candidate layouts (row_words A, e_words B, plane_words P; paired: plane
+  // stride S over pair_deg + 1 pattern planes)
   struct Cand {
-    int a, b, p, span;
+    int a, b, p, span, pair, s, total;
   };
-  static thread_local Cand cand[512];
-  int nc = 0;
+  static thread_local std::vector<Cand> cand;
+  cand.clear();
   if (info->e_mode == 0) {
-    for (int t = 0; t < 40; ++t) cand[nc++] = {b + 1 + t, 1, 0, n * (b + 1 + t) + b + 1};
     for (int t = 0; t < 40; ++t)
-      cand[nc++] = {1, n + 1 + t, 0, n + b * (n + 1 + t) + 1};
+      cand.push_back({b + 1 + t, 1, 0, n * (b + 1 + t) + b + 1, 0, 0, 0});
+    for (int t = 0; t < 40; ++t)
+      cand.push_back({1, n + 1 + t, 0, n + b * (n + 1 + t) + 1, 0, 0, 0});
   } else {
     const bool planes = info->odd_mask != 0;
     for (int t = 0; t < 24; ++t) {
       const int a = emax_half + 1 + t;
       const int span0 = n * a + emax_half + 1;
       for (int q = 0; q < (planes ? 8 : 1); ++q)
-        cand[nc++] = {a, 1, planes ? span0 + 4 * q : 0,
-                      planes ? 2 * span0 + 4 * q : span0};
+        cand.push_back({a, 1, planes ? span0 + 4 * q : 0,
+                        planes ? 2 * span0 + 4 * q : span0, 0, 0, 0});
     }
     for (int t = 0; t < 24; ++t) {
       const int bb = n + 1 + t;
       const int span0 = n + emax_half * bb + 1;
       for (int q = 0; q < (planes ? 8 : 1); ++q)
-        cand[nc++] = {1, bb, planes ? span0 + 4 * q : 0,
-                      planes ? 2 * span0 + 4 * q : span0};
+        cand.push_back({1, bb, planes ? span0 + 4 * q : 0,
+                        planes ? 2 * span0 + 4 * q : span0, 0, 0, 0});
     }
   }
+  const int policy = pair_policy();
+  {
+    const size_t n_base = cand.size();
+    for (size_t ci = 0; ci < n_base; ++ci) {
+      cand[ci].total = cand[ci].span;
+      // plane strides: odd residues mod 32 put lanes that differ only in
+      // the pattern on different banks
+      // (every other plane offset: the pattern planes spread the banks)
+      if (cand[ci].p && ((2 * cand[ci].p - cand[ci].span) / 4) % 2) continue;
+      for (int r : {1, 9}) {
+        const int s = ((cand[ci].span + 31) & ~31) + r;
+        const int total = cand[ci].span + pair_deg * s;
+        if (total > (int)kMaxPairWords) continue;
+        Cand c = cand[ci];
+        c.pair = 1;
+        c.s = s;
+        c.total = total;
+        cand.push_back(c);
+      }
+    }
+    if (policy >= 0) {
+      std::vector<Cand> keep;
+      for (const Cand& c : cand)
+        if (c.pair == policy) keep.push_back(c);
+      if (!keep.empty()) cand.swap(keep);
+    }
+  }
+  const int nc = (int)cand.size();
+  auto apply = [&](isd_plan_info* dst, const Cand& c) {
+    dst->row_words = (uint32_t)c.a;
+    dst->e_words = (uint32_t)c.b;
+    dst->plane_words = (uint32_t)c.p;
+    dst->base_words = (uint32_t)c.span;
+    dst->hist_words = (uint32_t)c.total;
+    dst->pair_mode = (uint32_t)c.pair;
+    dst->pair_words = (uint32_t)c.s;
+  };
   // default: first candidate
-  info->row_words = (uint32_t)cand[0].a;
-  info->e_words = (uint32_t)cand[0].b;
-  info->plane_words = (uint32_t)cand[0].p;
-  info->hist_words = (uint32_t)cand[0].span;
+  apply(info, cand[0]);
   // run bits a walk of 2^walk_bits configurations actually varies (a shard
   // fixes the top ones): lane patterns must stay inside them to tile it
   const int run_bits = std::min(n, walk_bits) - k;
@@ -257,11 +325,13 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   lane_candidates(lat, info, run_bits, wide, &masks);
 
   // Score one lane mask against every layout on `warps` sampled warp
-  // instructions x kCopySample copies; returns its best cost and, if
-  // `emit`, appends every (layout, mask) alternative to `ranked`.
+  // instructions x kCopySample copies; returns its best cost per
+  // configuration and, if `emit`, appends every (layout, mask) alternative
+  // to `ranked`.
   constexpr int kWarps = 160, kScreenWarps = 40, kCopySample = 8;
   const int kClimbSteps = (int)env_int("ISD_CLIMB_STEPS", 40);
   const size_t kClimbStarts = (size_t)env_int("ISD_CLIMB_STARTS", 3);
+  const uint64_t pair_bit = 1ull << pair_site;
   std::vector<double> cost(nc);
   double best = 1e30;
   isd_plan_info best_alt_ = *info;
@@ -286,33 +356,46 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
         const uint64_t c = rng_next(&seed) % kCopies;
         for (int t = 0; t < kCopyBits; ++t)
           if ((c >> t) & 1) cbits |= 1ull << info->copy_site[t];
-        Bin bins[32];
-        int nb = 0;
+        // distinct bins of the warp instruction: unpaired (m, e) and paired
+        // (m, e, pattern) of the configuration with the paired site down
+        Bin bins[32], pbins[32];
+        int pat[32];
+        int nb = 0, npb = 0;
         for (int lane = 0; lane < 32; ++lane) {
           const uint64_t r = hi ^ lane_dep[lane];
           const uint64_t x = (r << k) | jb | cbits;
-          int e = 0;
-          for (uint32_t q = 0; q < lat->n_classes; ++q) {
-            const isd_bond_class& cl = lat->classes[q];
-            e += popc64(((x ^ (x >> cl.shift)) ^ cl.jneg_mask) & cl.bond_mask);
-          }
+          const int e = energy_of(lat, x);
           Bin bn{popc64(x), e, (e & 1)};
           bool seen = false;
           for (int t = 0; t < nb && !seen; ++t)
             seen = bins[t].m == bn.m && bins[t].e == bn.e;
           if (!seen) bins[nb++] = bn;
+          const uint64_t x0 = x & ~pair_bit;
+          const int e0 = energy_of(lat, x0);
+          const int pt = (pair_deg - (energy_of(lat, x0 | pair_bit) - e0)) / 2;
+          Bin pb{popc64(x0), e0, (e0 & 1)};
+          seen = false;
+          for (int t = 0; t < npb && !seen; ++t)
+            seen = pbins[t].m == pb.m && pbins[t].e == pb.e && pat[t] == pt;
+          if (!seen) {
+            pat[npb] = pt;
+            pbins[npb++] = pb;
+          }
         }
         for (int ci = 0; ci < nc; ++ci) {
+          const Cand& cd = cand[ci];
+          const Bin* bb = cd.pair ? pbins : bins;
+          const int cnt = cd.pair ? npb : nb;
           int bank[32] = {0};
           int mx = 0;
-          for (int t = 0; t < nb; ++t) {
+          for (int t = 0; t < cnt; ++t) {
             int wd;
             if (info->e_mode == 0)
-              wd = bins[t].m * cand[ci].a + bins[t].e * cand[ci].b;
+              wd = bb[t].m * cd.a + bb[t].e * cd.b;
             else
-              wd = bins[t].m * cand[ci].a +
-                   ((bins[t].e - bins[t].par) >> 1) * cand[ci].b +
-                   bins[t].par * cand[ci].p;
+              wd = bb[t].m * cd.a + ((bb[t].e - bb[t].par) >> 1) * cd.b +
+                   bb[t].par * cd.p;
+            if (cd.pair) wd += pat[t] * cd.s;
             const int v = ++bank[wd & 31];
             if (v > mx) mx = v;
           }
@@ -322,20 +405,19 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
     }
     double mask_best = 1e30;
     for (int ci = 0; ci < nc; ++ci) {
-      const double cst = cost[ci] / (warps * kCopySample);
-      mask_best = std::min(mask_best, cst);
+      const double per_red = cost[ci] / (warps * kCopySample);
+      const double per_cfg = per_red / (cand[ci].pair ? 2.0 : 1.0);
+      mask_best = std::min(mask_best, per_cfg);
       if (!emit) continue;
       isd_plan_info alt = *info;
-      alt.row_words = (uint32_t)cand[ci].a;
-      alt.e_words = (uint32_t)cand[ci].b;
-      alt.plane_words = (uint32_t)cand[ci].p;
-      alt.hist_words = (uint32_t)cand[ci].span;
+      apply(&alt, cand[ci]);
       alt.lane_mask = lane_mask;
       for (int i = 0; i < 5; ++i) alt.lane_vec[i] = LN.vec[i];
-      alt.est_wavefronts = cst;
+      alt.est_wavefronts = per_red;
+      alt.est_per_config = per_cfg;
       if (ranked) ranked->push_back(alt);
-      if (cst < best - 1e-9) {
-        best = cst;
+      if (per_cfg < best - 1e-9) {
+        best = per_cfg;
         best_alt_ = alt;
       }
     }
@@ -584,7 +666,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
       ++walk_bits;
     choose_layout(lat, &cand, &all, n_configs_hint >= (1ull << 33),
                   walk_bits);
-    if (!have || cand.est_wavefronts < best_info.est_wavefronts - 1e-9) {
+    if (!have || cand.est_per_config < best_info.est_per_config - 1e-9) {
       best_info = cand;
       have = true;
     }
@@ -594,7 +676,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   if (ranked) {
     std::stable_sort(all.begin(), all.end(),
                      [](const isd_plan_info& a, const isd_plan_info& b) {
-                       return a.est_wavefronts < b.est_wavefronts;
+                       return a.est_per_config < b.est_per_config;
                      });
     if (all.size() > 256) all.resize(256);
     ranked->assign(all.begin(), all.end());
@@ -670,10 +752,26 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
   }
   // copy_table[c] = popc(c)(B+1) + unsat_cc(c) -> byte offset of copy c
   const int eb = (int)p->e_bytes, rb = (int)p->row_bytes;
-  for (int c = 0; c < kCopies; ++c) {
-    const int pc = __builtin_popcount((unsigned)c);
-    const int unsat = info->copy_table[c] - pc * (int)info->stride;
-    p->koff[c] = pc * rb + eb * unsat;
+  auto unsat_cc = [&](int c) {
+    return info->copy_table[c] -
+           __builtin_popcount((unsigned)c) * (int)info->stride;
+  };
+  for (int c = 0; c < kCopies; ++c)
+    p->koff[c] = __builtin_popcount((unsigned)c) * rb + eb * unsat_cc(c);
+  p->pair = info->pair_mode;
+  p->pair_words = info->pair_words;
+  p->pair_bytes = 4 * info->pair_words;
+  p->pair_deg = info->pair_degree;
+  if (info->pair_mode) {
+    // copy c with the paired site (copy bit 6) down lands in pattern plane
+    // n_6 + u(c), u(c) = its bonds to copy sites of c left unsatisfied:
+    // flipping it changes unsat_cc by (copy-copy degree) - 2 u(c)
+    const int top = 1 << (kCopyBits - 1);
+    const int cc_deg = info->pair_degree - info->copy_degree[kCopyBits - 1];
+    for (int c = 0; c < top; ++c) {
+      const int u = (cc_deg - (unsat_cc(c | top) - unsat_cc(c))) / 2;
+      p->koff[c] += (int)p->pair_bytes * u;
+    }
   }
 }
 

@@ -31,7 +31,7 @@ def test_library_exports_every_header_symbol():
     assert declared == set(_native.EXPORTED_SYMBOLS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.isd_abi_version() == 1
+    assert lib.isd_abi_version() == 2
     assert b"sm_100a" in lib.isd_version()
 
 
@@ -179,7 +179,7 @@ def _u(x):
     return np.uint64(x)
 
 
-def replay_hoisted(spec, loop_bits):
+def replay_hoisted(spec, loop_bits, pair=None):
     """numpy replay of k1_hoisted's arithmetic and address layout.
 
     Every index is decomposed exactly as the kernel does (run / loop /
@@ -189,12 +189,17 @@ def replay_hoisted(spec, loop_bits):
     that occur and that the e parity formula holds.
     """
     os.environ["ISD_LOOP_BITS"] = str(loop_bits)
+    if pair is not None:
+        os.environ["ISD_PAIR"] = str(pair)
     try:
         lat = native_lattice(spec)
         usable, info = _native.plan(lat, spec.num_configs)
     finally:
         del os.environ["ISD_LOOP_BITS"]
+        os.environ.pop("ISD_PAIR", None)
     assert usable
+    if pair is not None:
+        assert info.pair_mode == pair
     u, k = info.u, info.k
     stride = info.stride
     classes = spec.bond_classes()
@@ -220,6 +225,7 @@ def replay_hoisted(spec, loop_bits):
         jshift = (jb >> _u(s)) if s < 32 else np.zeros_like(jb)
         mvar = msk & loop & ~(copies >> s)
         e += pc((jb ^ jshift ^ cst) & _u(mvar))
+    n_pair = None
     for t in range(u):
         nq = pc((xt ^ _u(info.copy_jneg1[t])) & _u(info.copy_nbr1[t]) & _u(above_k))
         nq += pc((xt ^ _u(info.copy_jneg2[t])) & _u(info.copy_nbr2[t]) & _u(above_k))
@@ -227,6 +233,8 @@ def replay_hoisted(spec, loop_bits):
         nq += pc((jb ^ _u(info.copy_jneg2[t] & loop)) & _u(info.copy_nbr2[t] & loop))
         e += nq
         e += np.where((c >> t) & 1, info.copy_degree[t] - 2 * nq, 0)
+        if t == u - 1:
+            n_pair = nq
     kt = np.array(list(info.copy_table), dtype=np.int64)
     e += kt[c] - stride * np.bitwise_count(c.astype(np.uint64)).astype(np.int64)
     A, B, P = info.row_words, info.e_words, info.plane_words
@@ -237,23 +245,43 @@ def replay_hoisted(spec, loop_bits):
         word = m * A + ((e - par) // 2) * B + par * P
     else:
         word = m * A + e * B
+    key = m * stride + e
+    if info.pair_mode:
+        # paired copies: only configurations with copy bit 6 down issue a
+        # RED, into pattern plane n_6 + u(c) (u from the copy table)
+        top = 1 << (u - 1)
+        down = (c & top) == 0
+        cc_deg = info.pair_degree - info.copy_degree[u - 1]
+        u_c = (cc_deg - (kt[c | top] - kt[c & ~top] - stride)) // 2
+        pat = n_pair + u_c
+        assert pat[down].min() >= 0 and pat[down].max() <= info.pair_degree
+        word = (word + pat * info.pair_words)[down]
+        key = (key * (info.pair_degree + 1) + pat)[down]
     assert word.max() < info.hist_words
     # injective on occurring bins
-    pairs = np.unique(np.stack([word, m * stride + e]), axis=1)
+    pairs = np.unique(np.stack([word, key]), axis=1)
     assert len(np.unique(pairs[0])) == pairs.shape[1], "layout collision"
     hist = np.bincount(word, minlength=int(info.hist_words))
+
+    def bin_word(mm, ee):
+        if info.e_mode:
+            p2 = ee & 1
+            return mm * A + ((ee - p2) // 2) * B + p2 * P
+        return mm * A + ee * B
+
     table = np.zeros((n + 1, stride), dtype=np.int64)
+    planes = info.pair_degree + 1 if info.pair_mode else 1
     for mm in range(n + 1):
         for ee in range(stride):
-            if info.e_mode:
-                p2 = ee & 1
-                if odd == 0 and p2 != info.e_parity:
-                    continue
-                w = mm * A + ((ee - p2) // 2) * B + p2 * P
-            else:
-                w = mm * A + ee * B
-            if w < len(hist):
-                table[mm, ee] = hist[w]
+            if info.e_mode and odd == 0 and (ee & 1) != info.e_parity:
+                continue
+            tot = 0
+            for p in range(planes):
+                tot += hist[bin_word(mm, ee) + p * info.pair_words]
+                es = ee - info.pair_degree + 2 * p
+                if info.pair_mode and mm > 0 and 0 <= es < stride:
+                    tot += hist[bin_word(mm - 1, es) + p * info.pair_words]
+            table[mm, ee] = tot
     return table
 
 
@@ -270,13 +298,14 @@ REPLAY = [
 @pytest.mark.parametrize("kw", REPLAY)
 @pytest.mark.parametrize("seed", [None, 11])
 @pytest.mark.parametrize("loop_bits", [0, 3, 7])
-def test_hoisted_plan_replay_matches_oracle(kw, seed, loop_bits):
+@pytest.mark.parametrize("pair", [0, 1])
+def test_hoisted_plan_replay_matches_oracle(kw, seed, loop_bits, pair):
     spec, (r, c, d, j, per, signs) = _spec_and_oracle(kw, seed)
     if spec.num_spins < 7 + loop_bits + 1:
         pytest.skip("lattice too small for this loop width")
     lat = port.Lattice(r, c, d, j, per, signs)
     want = port.enumerate_range(lat, 0, 1 << lat.n)
-    got = replay_hoisted(spec, loop_bits)
+    got = replay_hoisted(spec, loop_bits, pair)
     assert np.array_equal(got, want)
 
 
