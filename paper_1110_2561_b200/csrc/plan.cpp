@@ -234,7 +234,7 @@ static int pair_policy() {
 
 static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
                           std::vector<isd_plan_info>* ranked, bool wide,
-                          int walk_bits) {
+                          int walk_bits, bool climb) {
   const int n = (int)lat->n_spins;
   const int k = (int)info->k;
   const int b = (int)lat->n_bonds;
@@ -333,6 +333,9 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   const size_t kClimbStarts = (size_t)env_int("ISD_CLIMB_STARTS", 3);
   const uint64_t pair_bit = 1ull << pair_site;
   std::vector<double> cost(nc);
+  // candidates scored by evaluate (the hill climb narrows this to the
+  // start pattern's best layouts)
+  std::vector<char> active(nc, 1);
   double best = 1e30;
   isd_plan_info best_alt_ = *info;
   auto evaluate = [&](const Lanes& LN, int warps, bool emit) {
@@ -383,6 +386,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
           }
         }
         for (int ci = 0; ci < nc; ++ci) {
+          if (!active[ci]) continue;
           const Cand& cd = cand[ci];
           const Bin* bb = cd.pair ? pbins : bins;
           const int cnt = cd.pair ? npb : nb;
@@ -405,6 +409,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
     }
     double mask_best = 1e30;
     for (int ci = 0; ci < nc; ++ci) {
+      if (!active[ci]) continue;
       const double per_red = cost[ci] / (warps * kCopySample);
       const double per_cfg = per_red / (cand[ci].pair ? 2.0 : 1.0);
       mask_best = std::min(mask_best, per_cfg);
@@ -426,9 +431,13 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   // screen every mask on a quarter of the sample, then score the best 8
   // in full
   if (masks.size() > 8) {
+    // (on every third layout: ranks the lane patterns, not the layouts)
+    if (nc > 96)
+      for (int ci = 0; ci < nc; ++ci) active[ci] = ci % 3 == 0;
     std::vector<std::pair<double, size_t>> screen;
     for (size_t i = 0; i < masks.size(); ++i)
       screen.push_back({evaluate(masks[i], kScreenWarps, false), i});
+    std::fill(active.begin(), active.end(), 1);
     std::sort(screen.begin(), screen.end());
     std::vector<Lanes> keep;
     for (size_t i = 0; i < screen.size() && i < 8; ++i)
@@ -437,12 +446,23 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   }
   // large walks: hill-climb the best three patterns (re-pivot a lane bit,
   // or give / move / drop its domino partner), scored on the screen sample
-  if (wide && run_bits >= 8) {
+  if (climb && wide && run_bits >= 8) {
     const std::vector<std::vector<int>> nbr = run_neighbors(lat, k, run_bits);
     uint64_t seed = 0x2545F4914F6CDD1Dull;
     const size_t n_start = std::min<size_t>(kClimbStarts, masks.size());
     for (size_t si = 0; si < n_start; ++si) {
       Lanes cur = masks[si];
+      std::fill(active.begin(), active.end(), 1);
+      evaluate(cur, kScreenWarps, false);
+      {
+        std::vector<std::pair<double, int>> order;
+        for (int ci = 0; ci < nc; ++ci)
+          order.push_back({cost[ci] / (cand[ci].pair ? 2.0 : 1.0), ci});
+        std::sort(order.begin(), order.end());
+        std::fill(active.begin(), active.end(), 0);
+        for (size_t i = 0; i < order.size() && i < 24; ++i)
+          active[order[i].second] = 1;
+      }
       double cur_cost = evaluate(cur, kScreenWarps, false);
       for (int step = 0; step < kClimbSteps; ++step) {
         Lanes q = cur;
@@ -474,6 +494,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
         dup = dup || (m.mask == cur.mask && std::equal(m.vec, m.vec + 5, cur.vec));
       if (!dup) masks.push_back(cur);
     }
+    std::fill(active.begin(), active.end(), 1);
   }
   for (const Lanes& m : masks) evaluate(m, kWarps, true);
   if (best < 1e29) *info = best_alt_;
@@ -653,24 +674,28 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   isd_plan_info best_info;
   bool have = false;
   std::vector<isd_plan_info> all;
-  // test / tuning knob: ISD_COPY_VARIANT=even|low|spread forces one set
-  const char* force = std::getenv("ISD_COPY_VARIANT");
-  for (size_t v = 0; v < sets.size(); ++v) {
-    if (force && std::strcmp(force, names[v]) != 0) continue;
+  int walk_bits = 0;
+  while (walk_bits < 63 && (1ull << (walk_bits + 1)) <= n_configs_hint)
+    ++walk_bits;
+  const bool wide = n_configs_hint >= (1ull << 33);
+  auto try_variant = [&](size_t v, bool climb) {
     isd_plan_info cand = *info;
     bool all_even = true;
     for (int site : sets[v]) all_even = all_even && !((odd >> site) & 1);
     set_copy_sites(lat, &cand, sets[v].data(), all_even ? 1 : 0);
-    int walk_bits = 0;
-    while (walk_bits < 63 && (1ull << (walk_bits + 1)) <= n_configs_hint)
-      ++walk_bits;
-    choose_layout(lat, &cand, &all, n_configs_hint >= (1ull << 33),
-                  walk_bits);
+    choose_layout(lat, &cand, &all, wide, walk_bits, climb);
     if (!have || cand.est_per_config < best_info.est_per_config - 1e-9) {
       best_info = cand;
       have = true;
     }
-  }
+  };
+  // test / tuning knob: ISD_COPY_VARIANT=even|low|spread forces one set
+  const char* force = std::getenv("ISD_COPY_VARIANT");
+  // (large walks also hill-climb each set's lane patterns; the model's
+  // estimates are only good to a few percent, so every set keeps its best
+  // climbed candidates in the list the GPU autotuner times)
+  for (size_t v = 0; v < sets.size(); ++v)
+    if (!force || std::strcmp(force, names[v]) == 0) try_variant(v, wide);
   if (!have) return 1;  // forced variant not available for this lattice
   *info = best_info;
   if (ranked) {

@@ -173,6 +173,21 @@ def test_baseline_lattice_full_walk(name):
         assert np.array_equal(e_marg, e_marg[::-1])
 
 
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_paired_and_unpaired_copies(name, pair, monkeypatch):
+    # ISD_PAIR forces the copy-site-6 pairing on (one RED per configuration
+    # pair, pattern planes) or off; both kernels must give the golden table
+    # (the autotuner then times only layouts of that kind)
+    monkeypatch.setenv("ISD_PAIR", pair)
+    spec = workloads()[name].spec
+    _, info = _native.plan(__import__(
+        "paper_1110_2561_b200.enumeration",
+        fromlist=["native_lattice"]).native_lattice(spec), spec.num_configs)
+    assert info.pair_mode == int(pair)
+    assert np.array_equal(full(spec), _golden_c(name))
+
+
 @pytest.mark.parametrize("name", ["c1", "c3", "c5"])
 @pytest.mark.parametrize("variant", ["even", "low"])
 def test_copy_site_variants(name, variant, monkeypatch):
