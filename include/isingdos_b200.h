@@ -163,16 +163,21 @@ typedef struct isd_plan_info {
                                 site: a "domino"); lane L's run is the
                                 slot's run XOR the vectors of L's bits  */
   double   est_wavefronts;   /* predicted smem wavefronts per warp RED  */
-  /* Paired copies (pair_mode 1): copy bit 6's site q is not a register copy
-   * of its own.  One RED counts the configuration with q down AND its
-   * partner with q up: it lands in pattern plane p = (bonds of q
-   * unsatisfied while q is down), word = base word + p*pair_words, and the
-   * flush credits the partner to (m + 1, e + pair_degree - 2p).  Halves the
-   * shared-memory REDs per configuration at the cost of pair_degree + 1
-   * planes of base_words words each. */
-  uint32_t pair_mode;
-  int32_t  pair_degree;      /* degree of copy site 6 (all bonds)       */
-  uint32_t pair_words;       /* stride between pattern planes (words)   */
+  /* Paired copies.  pair_mode 1: copy bit 6's site q is not a register
+   * copy of its own; one RED counts the configuration with q down AND its
+   * partner with q up: it lands in pattern plane p = (bonds of q left
+   * unsatisfied while q is down), word = base word + p*pair_words[0], and
+   * the flush credits the partner to (m + 1, e + pair_degree[0] - 2p).
+   * pair_mode 2 pairs copy bit 5 the same way on top (index 1 of the
+   * arrays): one RED counts four configurations; the one with both sites
+   * up lands at (m + 2, e + D0 - 2p0 + D1 - 2p1 + pair_both).  Each pairing
+   * halves the shared-memory REDs per configuration and multiplies the
+   * histogram by D + 1 planes of base_words words. */
+  uint32_t pair_mode;        /* 0, 1 or 2                               */
+  int32_t  pair_degree[2];   /* degree D of the paired sites (bit 6, 5) */
+  uint32_t pair_words[2];    /* pattern-plane strides (bit 6, bit 5)    */
+  int32_t  pair_both;        /* mode 2: e change of flipping both sites
+                                beyond the sum of the single flips      */
   uint32_t base_words;       /* words of the unpaired layout            */
   double   est_per_config;   /* est_wavefronts / configurations per RED */
 } isd_plan_info;

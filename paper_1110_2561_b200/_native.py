@@ -61,8 +61,9 @@ class PlanInfo(ctypes.Structure):
         ("plane_words", ctypes.c_uint32), ("hist_words", ctypes.c_uint32),
         ("lane_mask", ctypes.c_uint64), ("lane_vec", ctypes.c_uint64 * 5),
         ("est_wavefronts", ctypes.c_double),
-        ("pair_mode", ctypes.c_uint32), ("pair_degree", ctypes.c_int32),
-        ("pair_words", ctypes.c_uint32), ("base_words", ctypes.c_uint32),
+        ("pair_mode", ctypes.c_uint32), ("pair_degree", ctypes.c_int32 * 2),
+        ("pair_words", ctypes.c_uint32 * 2), ("pair_both", ctypes.c_int32),
+        ("base_words", ctypes.c_uint32),
         ("est_per_config", ctypes.c_double),
     ]
 

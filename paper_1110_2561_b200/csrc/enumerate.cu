@@ -149,12 +149,13 @@ struct RuntimeTraits {
   __device__ uint32_t jn2v(int q) const { return P.jn2v[q]; }
   __device__ int32_t degree(int q) const { return P.degree[q]; }
   __device__ uint32_t koff(int c) const { return (uint32_t)P.koff[c]; }
-  __device__ uint32_t pair_bytes() const { return P.pair_bytes; }
-  __device__ uint32_t pair_words() const { return P.pair_words; }
-  __device__ int32_t pair_deg() const { return P.pair_deg; }
+  __device__ uint32_t pair_bytes(int i) const { return P.pair_bytes[i]; }
+  __device__ uint32_t pair_words(int i) const { return P.pair_words[i]; }
+  __device__ int32_t pair_deg(int i) const { return P.pair_deg[i]; }
+  __device__ int32_t pair_both() const { return P.pair_both; }
 };
 
-template <int NC, bool DOUBLE, bool PAIR>
+template <int NC, bool DOUBLE, int PAIR>
 __global__ void __launch_bounds__(kThreads)
     k1_hoisted(const __grid_constant__ HoistParams P,
                unsigned long long* __restrict__ out) {
@@ -245,7 +246,7 @@ int launch_canonical(const CanonParams& p, unsigned long long* out,
   }
 }
 
-template <int NC, bool D, bool PR>
+template <int NC, bool D, int PR>
 static int launch_hoist_t(const HoistParams& p, unsigned long long* out,
                           int sm_count, cudaStream_t st) {
   const size_t smem = (size_t)p.n_hist * p.hist_words * 4;
@@ -263,17 +264,15 @@ int launch_hoisted(const HoistParams& p, unsigned long long* out, int sm_count,
                    void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const bool dbl = p.has_double != 0;
-  const bool pr = p.pair != 0;
-  switch (p.n_classes) {
-#define CASE(NC)                                                              \
-  case NC:                                                                    \
-    if (pr)                                                                   \
-      return dbl ? launch_hoist_t<NC, true, true>(p, out, sm_count, st)       \
-                 : launch_hoist_t<NC, false, true>(p, out, sm_count, st);     \
-    return dbl ? launch_hoist_t<NC, true, false>(p, out, sm_count, st)        \
-               : launch_hoist_t<NC, false, false>(p, out, sm_count, st);
+  switch (p.n_classes * 3 + (p.pair > 2 ? 0 : p.pair)) {
+#define CASE1(NC, PR)                                                  \
+  case NC * 3 + PR:                                                    \
+    return dbl ? launch_hoist_t<NC, true, PR>(p, out, sm_count, st)    \
+               : launch_hoist_t<NC, false, PR>(p, out, sm_count, st);
+#define CASE(NC) CASE1(NC, 0) CASE1(NC, 1) CASE1(NC, 2)
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
+#undef CASE1
     default:
       return -(int)cudaErrorInvalidValue;
   }

@@ -74,17 +74,20 @@ struct HoistParams {
   int32_t koff[kCopies];         // constant byte offset of copy c:
                                  // popc(c) row_bytes + e_bytes unsat_cc(c)
                                  // (+ pair_bytes u_q(c) for paired copies)
-  // paired copies (isd_plan_info.pair_mode): copy bit 6 is counted through
-  // pattern planes instead of register copies
-  uint32_t pair;                 // 0 / 1
-  uint32_t pair_bytes;           // 4 * pair_words
-  uint32_t pair_words;           // stride between pattern planes
-  int32_t pair_deg;              // D: degree of copy site 6
+  // paired copies (isd_plan_info.pair_mode): copy bit 6 (index 0) and, in
+  // mode 2, copy bit 5 (index 1) are counted through pattern planes
+  // instead of register copies
+  uint32_t pair;                 // 0, 1, 2
+  uint32_t pair_bytes[2];        // 4 * pair_words
+  uint32_t pair_words[2];        // stride between pattern planes
+  int32_t pair_deg[2];           // D: degree of the paired site
+  int32_t pair_both;             // mode 2: extra e change of the double flip
 };
 
-// Largest paired histogram (words): two CTAs of 512 threads must still fit
-// an SM's shared memory.
+// Largest paired histogram (words): two CTAs of 512 threads per SM fit
+// 28 K words each; up to 56 K words runs one CTA per SM (mode 2 only).
 constexpr uint32_t kMaxPairWords = 28000;
+constexpr uint32_t kMaxPair2Words = 56000;
 
 // ---- host side -----------------------------------------------------------
 int validate_lattice(const isd_lattice* lat, char* err, size_t errlen);

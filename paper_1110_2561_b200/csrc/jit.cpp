@@ -75,8 +75,8 @@ template <typename V>
 static void emit_switch(std::ostringstream& o, const char* type,
                         const char* name, const V* vals, int n,
                         const char* suffix) {
-  o << "  __device__ __forceinline__ static " << type << " " << name
-    << "(int i) {\n    switch (i) {\n";
+  o << "  __device__ __forceinline__ static constexpr " << type << " "
+    << name << "(int i) {\n    switch (i) {\n";
   for (int i = 0; i < n; ++i)
     o << "      case " << i << ": return " << vals[i] << suffix << ";\n";
   o << "    }\n    return 0;\n  }\n";
@@ -136,11 +136,12 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
   uint32_t koff[kCopies];
   for (int c = 0; c < kCopies; ++c) koff[c] = (uint32_t)P.koff[c];
   emit_switch(o, "uint32_t", "koff", koff, kCopies, "u");
-  c32("pair_bytes", P.pair_bytes);
-  c32("pair_words", P.pair_words);
-  o << "  __device__ __forceinline__ static constexpr int32_t pair_deg() "
+  emit_switch(o, "uint32_t", "pair_bytes", P.pair_bytes, 2, "u");
+  emit_switch(o, "uint32_t", "pair_words", P.pair_words, 2, "u");
+  emit_switch(o, "int32_t", "pair_deg", P.pair_deg, 2, "");
+  o << "  __device__ __forceinline__ static constexpr int32_t pair_both() "
        "{ return "
-    << P.pair_deg << "; }\n";
+    << P.pair_both << "; }\n";
   o << "};\n";
   o << "extern \"C\" __global__ void __launch_bounds__(" << kThreads
     << ") k1_jit(unsigned long long run_begin, unsigned long long nruns,\n"
@@ -151,7 +152,7 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
        "  const JitTraits L;\n"
        "  k1_hoisted_body<"
     << nc << ", " << (dbl ? "true" : "false") << ", "
-    << (P.pair ? "true" : "false") << ">(L, run_begin, nruns, hi_step, lane_mask, lanes, hist, out);\n}\n";
+    << P.pair << ">(L, run_begin, nruns, hi_step, lane_mask, lanes, hist, out);\n}\n";
   return o.str();
 }
 

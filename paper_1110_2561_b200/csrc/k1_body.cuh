@@ -43,11 +43,12 @@ __device__ __forceinline__ unsigned int isd_bin_word(const T& L, unsigned int m,
   return m * L.row_words() + e * L.e_words();
 }
 
-// PAIR: copy bit 6 is not unrolled; one RED counts the configuration with
-// that site down and its partner with it up, in pattern plane p (= the
+// PAIR 1: copy bit 6 is not unrolled; one RED counts the configuration
+// with that site down and its partner with it up, in pattern plane p (= the
 // site's unsatisfied bonds while down), and the flush credits the partner
-// to (m + 1, e + D - 2p).
-template <int NC, bool DOUBLE, bool PAIR, class T>
+// to (m + 1, e + D - 2p).  PAIR 2: copy bit 5 as well (4 configurations per
+// RED, planes p0 (bit 6) x p1 (bit 5)).
+template <int NC, bool DOUBLE, int PAIR, class T>
 __device__ __forceinline__ void k1_hoisted_body(
     const T& L, unsigned long long run_begin, unsigned long long nruns,
     unsigned long long hi_step, unsigned long long lane_mask,
@@ -138,7 +139,8 @@ __device__ __forceinline__ void k1_hoisted_body(
         if (DOUBLE) nq += __popc((jb ^ L.jn2v(q)) & L.nm2v(q));
         e += nq;
         d[q] = (unsigned int)((int)L.e_bytes() * (L.degree(q) - 2 * nq));
-        if (PAIR && q == 6) pair_off = (unsigned int)nq * L.pair_bytes();
+        if (PAIR >= 1 && q == 6) pair_off += (unsigned int)nq * L.pair_bytes(0);
+        if (PAIR >= 2 && q == 5) pair_off += (unsigned int)nq * L.pair_bytes(1);
       }
       const unsigned int par = (par_run + __popc(jb & odd_loop)) & 1u;
       // a[c] carries no per-copy constant: addr(c) = a[c] + koff(c), where
@@ -158,12 +160,14 @@ __device__ __forceinline__ void k1_hoisted_body(
           const int top = 31 - __clz(cl);
           a[cl] = a[cl ^ (1 << top)] + d[top];
         }
-        const unsigned int b1 = a[cl] + d[5];
         ISD_CHECK_ADDR(a[cl] + L.koff(cl), hbase, hbytes);
         isd_red_shared_inc(a[cl] + L.koff(cl));
-        ISD_CHECK_ADDR(b1 + L.koff(cl + 32), hbase, hbytes);
-        isd_red_shared_inc(b1 + L.koff(cl + 32));
-        if (!PAIR) {
+        const unsigned int b1 = a[cl] + d[5];
+        if (PAIR <= 1) {
+          ISD_CHECK_ADDR(b1 + L.koff(cl + 32), hbase, hbytes);
+          isd_red_shared_inc(b1 + L.koff(cl + 32));
+        }
+        if (PAIR == 0) {
           const unsigned int b2 = a[cl] + d[6];
           const unsigned int b3 = b1 + d[6];
           ISD_CHECK_ADDR(b2 + L.koff(cl + 64), hbase, hbytes);
@@ -186,20 +190,37 @@ __device__ __forceinline__ void k1_hoisted_body(
     unsigned long long s = 0;
     for (unsigned int h = 0; h < L.n_hist(); ++h) {
       const unsigned int* hh = hist + h * L.hist_words();
-      if constexpr (PAIR) {
-        // the paired site down: this bin, every pattern plane
-        for (int p = 0; p <= L.pair_deg(); ++p)
-          s += hh[word + p * L.pair_words()];
-        // the paired site up: partners of (m - 1, e - D + 2p) in plane p
-        if (m > 0)
-          for (int p = 0; p <= L.pair_deg(); ++p) {
-            const int es = (int)e - L.pair_deg() + 2 * p;
-            if (es < 0 || es >= (int)L.stride()) continue;
-            s += hh[isd_bin_word(L, m - 1, (unsigned int)es) +
-                    p * L.pair_words()];
-          }
-      } else {
+      if constexpr (PAIR == 0) {
         s += hh[word];
+      } else if constexpr (PAIR == 1) {
+        const int D0 = L.pair_deg(0);
+        for (int p = 0; p <= D0; ++p) {
+          const unsigned int plane = p * L.pair_words(0);
+          // the paired site down: this bin
+          s += hh[word + plane];
+          // the paired site up: partner of (m - 1, e - D + 2p)
+          const int es = (int)e - D0 + 2 * p;
+          if (m > 0 && es >= 0 && es < (int)L.stride())
+            s += hh[isd_bin_word(L, m - 1, (unsigned int)es) + plane];
+        }
+      } else {
+        const int D0 = L.pair_deg(0), D1 = L.pair_deg(1);
+        for (int p1 = 0; p1 <= D1; ++p1)
+          for (int p0 = 0; p0 <= D0; ++p0) {
+            const unsigned int plane = p0 * L.pair_words(0) +
+                                       p1 * L.pair_words(1);
+            const int f0 = D0 - 2 * p0, f1 = D1 - 2 * p1;
+            s += hh[word + plane];  // both paired sites down
+            if (m == 0) continue;
+            const int e0 = (int)e - f0, e1 = (int)e - f1;
+            if (e0 >= 0 && e0 < (int)L.stride())  // bit-6 site up
+              s += hh[isd_bin_word(L, m - 1, (unsigned int)e0) + plane];
+            if (e1 >= 0 && e1 < (int)L.stride())  // bit-5 site up
+              s += hh[isd_bin_word(L, m - 1, (unsigned int)e1) + plane];
+            const int e2 = (int)e - f0 - f1 - L.pair_both();
+            if (m >= 2 && e2 >= 0 && e2 < (int)L.stride())  // both up
+              s += hh[isd_bin_word(L, m - 2, (unsigned int)e2) + plane];
+          }
       }
     }
     if (s) atomicAdd(out + bin, s);

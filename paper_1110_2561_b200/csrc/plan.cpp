@@ -215,6 +215,20 @@ static int site_degree(const isd_lattice* lat, int site) {
   return d;
 }
 
+// e change of flipping sites a and b (both down -> both up) beyond the sum
+// of the two single flips: each a-b bond is counted by both single flips as
+// changing, but flips back: -2 (1 - 2 neg) per bond
+static int both_flip_term(const isd_lattice* lat, int a, int b) {
+  int t = 0;
+  const int lo = a < b ? a : b, hi = a < b ? b : a;
+  for (uint32_t q = 0; q < lat->n_classes; ++q) {
+    const isd_bond_class& cl = lat->classes[q];
+    if (hi - lo == (int)cl.shift && ((cl.bond_mask >> lo) & 1))
+      t -= 2 * (1 - 2 * (int)((cl.jneg_mask >> lo) & 1));
+  }
+  return t;
+}
+
 static int energy_of(const isd_lattice* lat, uint64_t x) {
   int e = 0;
   for (uint32_t q = 0; q < lat->n_classes; ++q) {
@@ -224,12 +238,13 @@ static int energy_of(const isd_lattice* lat, uint64_t x) {
   return e;
 }
 
-// ISD_PAIR: unset = let the model / autotuner choose, 0 = unpaired layouts
-// only, 1 = paired layouts only (when one fits shared memory)
+// ISD_PAIR: unset = let the model / autotuner choose; 0, 1 or 2 = layouts
+// of that pairing mode only (when one fits shared memory)
 static int pair_policy() {
   const char* v = std::getenv("ISD_PAIR");
   if (!v || !*v) return -1;
-  return std::atoi(v) ? 1 : 0;
+  const int m = std::atoi(v);
+  return m < 0 ? 0 : (m > 2 ? 2 : m);
 }
 
 static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
@@ -243,21 +258,25 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   info->est_wavefronts = 0;
   info->est_per_config = 0;
   info->pair_mode = 0;
-  const int pair_site = info->copy_site[kCopyBits - 1];
-  const int pair_deg = site_degree(lat, pair_site);
-  info->pair_degree = pair_deg;
+  // paired sites: copy bit 6 (index 0) and, for mode 2, copy bit 5
+  const int psite[2] = {info->copy_site[kCopyBits - 1],
+                        info->copy_site[kCopyBits - 2]};
+  const int pdeg[2] = {site_degree(lat, psite[0]), site_degree(lat, psite[1])};
+  info->pair_degree[0] = pdeg[0];
+  info->pair_degree[1] = pdeg[1];
+  info->pair_both = both_flip_term(lat, psite[0], psite[1]);
   // candidate layouts (row_words A, e_words B, plane_words P; paired: plane
-  // stride S over pair_deg + 1 pattern planes)
+  // strides s0 (bit 6) and s1 (bit 5) over the pattern planes)
   struct Cand {
-    int a, b, p, span, pair, s, total;
+    int a, b, p, span, pair, s0, s1, total;
   };
   static thread_local std::vector<Cand> cand;
   cand.clear();
   if (info->e_mode == 0) {
     for (int t = 0; t < 40; ++t)
-      cand.push_back({b + 1 + t, 1, 0, n * (b + 1 + t) + b + 1, 0, 0, 0});
+      cand.push_back({b + 1 + t, 1, 0, n * (b + 1 + t) + b + 1, 0, 0, 0, 0});
     for (int t = 0; t < 40; ++t)
-      cand.push_back({1, n + 1 + t, 0, n + b * (n + 1 + t) + 1, 0, 0, 0});
+      cand.push_back({1, n + 1 + t, 0, n + b * (n + 1 + t) + 1, 0, 0, 0, 0});
   } else {
     const bool planes = info->odd_mask != 0;
     for (int t = 0; t < 24; ++t) {
@@ -265,34 +284,38 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
       const int span0 = n * a + emax_half + 1;
       for (int q = 0; q < (planes ? 8 : 1); ++q)
         cand.push_back({a, 1, planes ? span0 + 4 * q : 0,
-                        planes ? 2 * span0 + 4 * q : span0, 0, 0, 0});
+                        planes ? 2 * span0 + 4 * q : span0, 0, 0, 0, 0});
     }
     for (int t = 0; t < 24; ++t) {
       const int bb = n + 1 + t;
       const int span0 = n + emax_half * bb + 1;
       for (int q = 0; q < (planes ? 8 : 1); ++q)
         cand.push_back({1, bb, planes ? span0 + 4 * q : 0,
-                        planes ? 2 * span0 + 4 * q : span0, 0, 0, 0});
+                        planes ? 2 * span0 + 4 * q : span0, 0, 0, 0, 0});
     }
   }
   const int policy = pair_policy();
   {
     const size_t n_base = cand.size();
     for (size_t ci = 0; ci < n_base; ++ci) {
-      cand[ci].total = cand[ci].span;
-      // plane strides: odd residues mod 32 put lanes that differ only in
-      // the pattern on different banks
+      Cand c = cand[ci];
+      cand[ci].total = c.span;
       // (every other plane offset: the pattern planes spread the banks)
-      if (cand[ci].p && ((2 * cand[ci].p - cand[ci].span) / 4) % 2) continue;
+      if (c.p && ((2 * c.p - c.span) / 4) % 2) continue;
+      // plane strides: odd residues mod 32 put lanes that differ only in
+      // the patterns on different banks (mode 2: p0 + (D0 + 1) p1 times an
+      // odd residue: distinct banks while (D0 + 1)(D1 + 1) <= 32)
       for (int r : {1, 9}) {
-        const int s = ((cand[ci].span + 31) & ~31) + r;
-        const int total = cand[ci].span + pair_deg * s;
-        if (total > (int)kMaxPairWords) continue;
-        Cand c = cand[ci];
+        c.s0 = ((c.span + 31) & ~31) + r;
         c.pair = 1;
-        c.s = s;
-        c.total = total;
-        cand.push_back(c);
+        c.s1 = 0;
+        c.total = c.span + pdeg[0] * c.s0;
+        if (c.total <= (int)kMaxPairWords) cand.push_back(c);
+        c.pair = 2;
+        const int end0 = c.span + pdeg[0] * c.s0;
+        c.s1 = ((end0 + 31) & ~31) + (r * (pdeg[0] + 1)) % 32;
+        c.total = end0 + pdeg[1] * c.s1;
+        if (c.total <= (int)kMaxPair2Words) cand.push_back(c);
       }
     }
     if (policy >= 0) {
@@ -310,7 +333,8 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
     dst->base_words = (uint32_t)c.span;
     dst->hist_words = (uint32_t)c.total;
     dst->pair_mode = (uint32_t)c.pair;
-    dst->pair_words = (uint32_t)c.s;
+    dst->pair_words[0] = (uint32_t)c.s0;
+    dst->pair_words[1] = (uint32_t)c.s1;
   };
   // default: first candidate
   apply(info, cand[0]);
@@ -331,7 +355,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   constexpr int kWarps = 160, kScreenWarps = 40, kCopySample = 8;
   const int kClimbSteps = (int)env_int("ISD_CLIMB_STEPS", 40);
   const size_t kClimbStarts = (size_t)env_int("ISD_CLIMB_STARTS", 3);
-  const uint64_t pair_bit = 1ull << pair_site;
+  const uint64_t pbit[2] = {1ull << psite[0], 1ull << psite[1]};
   std::vector<double> cost(nc);
   // candidates scored by evaluate (the hill climb narrows this to the
   // start pattern's best layouts)
@@ -359,37 +383,42 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
         const uint64_t c = rng_next(&seed) % kCopies;
         for (int t = 0; t < kCopyBits; ++t)
           if ((c >> t) & 1) cbits |= 1ull << info->copy_site[t];
-        // distinct bins of the warp instruction: unpaired (m, e) and paired
-        // (m, e, pattern) of the configuration with the paired site down
-        Bin bins[32], pbins[32];
-        int pat[32];
-        int nb = 0, npb = 0;
+        // distinct bins of the warp instruction for each pairing mode:
+        // unpaired (m, e); mode 1 (m, e, p0) of the configuration with the
+        // bit-6 site down; mode 2 (m, e, p0, p1) with both sites down
+        Bin bins[3][32];
+        int pat[3][32];
+        int nb[3] = {0, 0, 0};
         for (int lane = 0; lane < 32; ++lane) {
           const uint64_t r = hi ^ lane_dep[lane];
           const uint64_t x = (r << k) | jb | cbits;
-          const int e = energy_of(lat, x);
-          Bin bn{popc64(x), e, (e & 1)};
-          bool seen = false;
-          for (int t = 0; t < nb && !seen; ++t)
-            seen = bins[t].m == bn.m && bins[t].e == bn.e;
-          if (!seen) bins[nb++] = bn;
-          const uint64_t x0 = x & ~pair_bit;
-          const int e0 = energy_of(lat, x0);
-          const int pt = (pair_deg - (energy_of(lat, x0 | pair_bit) - e0)) / 2;
-          Bin pb{popc64(x0), e0, (e0 & 1)};
-          seen = false;
-          for (int t = 0; t < npb && !seen; ++t)
-            seen = pbins[t].m == pb.m && pbins[t].e == pb.e && pat[t] == pt;
-          if (!seen) {
-            pat[npb] = pt;
-            pbins[npb++] = pb;
+          for (int mode = 0; mode < 3; ++mode) {
+            const uint64_t xs = mode == 0 ? x
+                                : mode == 1 ? x & ~pbit[0]
+                                            : x & ~(pbit[0] | pbit[1]);
+            const int e = energy_of(lat, xs);
+            int pt = 0;
+            if (mode >= 1)
+              pt = (pdeg[0] - (energy_of(lat, xs | pbit[0]) - e)) / 2;
+            if (mode == 2)
+              pt += 64 * ((pdeg[1] - (energy_of(lat, xs | pbit[1]) - e)) / 2);
+            const Bin bn{popc64(xs), e, e & 1};
+            bool seen = false;
+            for (int t = 0; t < nb[mode] && !seen; ++t)
+              seen = bins[mode][t].m == bn.m && bins[mode][t].e == bn.e &&
+                     pat[mode][t] == pt;
+            if (!seen) {
+              pat[mode][nb[mode]] = pt;
+              bins[mode][nb[mode]++] = bn;
+            }
           }
         }
         for (int ci = 0; ci < nc; ++ci) {
           if (!active[ci]) continue;
           const Cand& cd = cand[ci];
-          const Bin* bb = cd.pair ? pbins : bins;
-          const int cnt = cd.pair ? npb : nb;
+          const Bin* bb = bins[cd.pair];
+          const int* pp = pat[cd.pair];
+          const int cnt = nb[cd.pair];
           int bank[32] = {0};
           int mx = 0;
           for (int t = 0; t < cnt; ++t) {
@@ -399,7 +428,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
             else
               wd = bb[t].m * cd.a + ((bb[t].e - bb[t].par) >> 1) * cd.b +
                    bb[t].par * cd.p;
-            if (cd.pair) wd += pat[t] * cd.s;
+            wd += (pp[t] & 63) * cd.s0 + (pp[t] >> 6) * cd.s1;
             const int v = ++bank[wd & 31];
             if (v > mx) mx = v;
           }
@@ -411,7 +440,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
     for (int ci = 0; ci < nc; ++ci) {
       if (!active[ci]) continue;
       const double per_red = cost[ci] / (warps * kCopySample);
-      const double per_cfg = per_red / (cand[ci].pair ? 2.0 : 1.0);
+      const double per_cfg = per_red / (double)(1 << cand[ci].pair);
       mask_best = std::min(mask_best, per_cfg);
       if (!emit) continue;
       isd_plan_info alt = *info;
@@ -457,7 +486,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
       {
         std::vector<std::pair<double, int>> order;
         for (int ci = 0; ci < nc; ++ci)
-          order.push_back({cost[ci] / (cand[ci].pair ? 2.0 : 1.0), ci});
+          order.push_back({cost[ci] / (double)(1 << cand[ci].pair), ci});
         std::sort(order.begin(), order.end());
         std::fill(active.begin(), active.end(), 0);
         for (size_t i = 0; i < order.size() && i < 24; ++i)
@@ -678,6 +707,11 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   while (walk_bits < 63 && (1ull << (walk_bits + 1)) <= n_configs_hint)
     ++walk_bits;
   const bool wide = n_configs_hint >= (1ull << 33);
+  // the paired slots (6, then 5) take the set's lowest-degree sites: fewer
+  // pattern planes
+  for (auto& st : sets)
+    std::stable_sort(st.begin(), st.end(),
+                     [&](int x, int y) { return deg[x] > deg[y]; });
   auto try_variant = [&](size_t v, bool climb) {
     isd_plan_info cand = *info;
     bool all_even = true;
@@ -699,12 +733,20 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   if (!have) return 1;  // forced variant not available for this lattice
   *info = best_info;
   if (ranked) {
+    // best first within each pairing mode, the modes interleaved (the model
+    // cannot see occupancy or the issue cost of fewer REDs per loop
+    // subset, so the GPU autotuner must time every mode)
     std::stable_sort(all.begin(), all.end(),
                      [](const isd_plan_info& a, const isd_plan_info& b) {
                        return a.est_per_config < b.est_per_config;
                      });
-    if (all.size() > 256) all.resize(256);
-    ranked->assign(all.begin(), all.end());
+    std::vector<isd_plan_info> by_mode[3], mixed;
+    for (const isd_plan_info& x : all) by_mode[x.pair_mode % 3].push_back(x);
+    for (size_t i = 0; mixed.size() < all.size(); ++i)
+      for (int mode : {2, 1, 0})
+        if (i < by_mode[mode].size()) mixed.push_back(by_mode[mode][i]);
+    if (mixed.size() > 256) mixed.resize(256);
+    ranked->assign(mixed.begin(), mixed.end());
   }
   return 0;
 }
@@ -784,18 +826,24 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
   for (int c = 0; c < kCopies; ++c)
     p->koff[c] = __builtin_popcount((unsigned)c) * rb + eb * unsat_cc(c);
   p->pair = info->pair_mode;
-  p->pair_words = info->pair_words;
-  p->pair_bytes = 4 * info->pair_words;
-  p->pair_deg = info->pair_degree;
-  if (info->pair_mode) {
-    // copy c with the paired site (copy bit 6) down lands in pattern plane
-    // n_6 + u(c), u(c) = its bonds to copy sites of c left unsatisfied:
-    // flipping it changes unsat_cc by (copy-copy degree) - 2 u(c)
-    const int top = 1 << (kCopyBits - 1);
-    const int cc_deg = info->pair_degree - info->copy_degree[kCopyBits - 1];
-    for (int c = 0; c < top; ++c) {
-      const int u = (cc_deg - (unsat_cc(c | top) - unsat_cc(c))) / 2;
-      p->koff[c] += (int)p->pair_bytes * u;
+  p->pair_both = info->pair_both;
+  for (int i = 0; i < 2; ++i) {
+    p->pair_words[i] = info->pair_words[i];
+    p->pair_bytes[i] = 4 * info->pair_words[i];
+    p->pair_deg[i] = info->pair_degree[i];
+  }
+  // a paired site's RED lands in pattern plane n + u(c): u(c) = its bonds
+  // to the copy sites of c left unsatisfied while it is down (the other
+  // paired site down too); flipping it changes unsat_cc by (its copy-copy
+  // degree) - 2 u(c)
+  for (uint32_t i = 0; i < info->pair_mode; ++i) {
+    const int slot = kCopyBits - 1 - (int)i;
+    const int bit = 1 << slot;
+    const int cc_deg = info->pair_degree[i] - info->copy_degree[slot];
+    const int live = 1 << (kCopyBits - (int)info->pair_mode);
+    for (int c = 0; c < live; ++c) {
+      const int u = (cc_deg - (unsat_cc(c | bit) - unsat_cc(c))) / 2;
+      p->koff[c] += (int)p->pair_bytes[i] * u;
     }
   }
 }
