@@ -216,11 +216,12 @@ def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1, kernel="k1",
 
     `roofline`: the pipe the kernel is bound by (ncu: shared-memory
     wavefronts at 94-97% of peak).  k1_hoisted issues one shared-memory
-    reduction lane per `cfg_per_red` configurations — 1 with unpaired
-    copies, 2 with paired copies (one RED counts a configuration and its
-    partner with copy site 6 flipped, isd_plan_info.pair_mode) — so the
-    peak is the measured conflict-free RED.shared rate (K0 probe 3) x SMs x
-    SM clock x cfg_per_red.
+    reduction lane per `cfg_per_red` = 2^pair_mode configurations — 1 with
+    unpaired copies, 2 with copy bit 6 paired (one RED counts a
+    configuration and its partner with that site flipped), 4 with bits 5
+    and 6 paired (isd_plan_info.pair_mode) — so the peak is the measured
+    conflict-free RED.shared rate (K0 probe 3) x SMs x SM clock x
+    cfg_per_red.
 
     `roofline_int_pipe`: BASELINE.md §4's integer-pipe roofline of the
     canonical formulation (POPC and ALU ops per
@@ -425,8 +426,11 @@ def run_b200(args, wl):
         w2 = workloads()[name]
         t2, _, _, _, _ = time_device(w2, max(3, args.steps // 2), 3)
         ms2 = max_over_ranks(sum(t2) / len(t2))
+        from paper_1110_2561_b200.enumeration import native_lattice as _nl2
+        _, plan2 = _native.plan(_nl2(w2.spec), w2.spec.num_configs // world)
         extra[name] = {"configs_per_s": w2.spec.num_configs / (ms2 / 1e3),
-                       "ms_per_step": ms2}
+                       "ms_per_step": ms2,
+                       "configs_per_red_lane": 1 << plan2.pair_mode}
 
     # flip symmetry (extension, reported separately): walk 2^(N-1), mirror
     flip = None
@@ -449,7 +453,7 @@ def run_b200(args, wl):
     from paper_1110_2561_b200.enumeration import native_lattice as _nl
     _, plan = _native.plan(_nl(wl.spec), n_cfg // world)
     roof, roof_int = roofline(wl, cal, clk, sm_count, n_cfg // world, ms_k1,
-                              kernel_path, 2 if plan.pair_mode else 1)
+                              kernel_path, 1 << plan.pair_mode)
     roof["plan"] = {"pair_mode": int(plan.pair_mode),
                     "copy_sites": list(plan.copy_site),
                     "loop_bits": int(plan.l),

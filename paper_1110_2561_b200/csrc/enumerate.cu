@@ -155,8 +155,10 @@ struct RuntimeTraits {
   __device__ int32_t pair_both() const { return P.pair_both; }
 };
 
+// (mode-2 histograms can be too large for two blocks per SM: those kernels
+// may run 1024-thread blocks, which caps them at 64 registers)
 template <int NC, bool DOUBLE, int PAIR>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(PAIR == 2 ? kWideThreads : kThreads)
     k1_hoisted(const __grid_constant__ HoistParams P,
                unsigned long long* __restrict__ out) {
   extern __shared__ __align__(16) uint32_t hist[];
@@ -246,16 +248,42 @@ int launch_canonical(const CanonParams& p, unsigned long long* out,
   }
 }
 
+// Threads per block of the hoisted kernel: 512, or 1024 when a histogram
+// this large leaves room for one block per SM (twice the warps to hide the
+// issue latency).  The grid is one wave of resident blocks.
+int hoisted_block(const void* fn, size_t smem, int sm_count, bool may_widen,
+                  int* grid) {
+  int threads = kThreads;
+  int per_sm = 0;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads,
+                                                    smem) != cudaSuccess)
+    per_sm = 1;
+  if (per_sm <= 1 && may_widen) {
+    int wide = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wide, fn, kWideThreads,
+                                                      smem) == cudaSuccess &&
+        wide >= 1)
+      threads = kWideThreads;
+  }
+  if (per_sm < 1) per_sm = 1;
+  cudaGetLastError();
+  *grid = per_sm * sm_count;
+  return threads;
+}
+
 template <int NC, bool D, int PR>
 static int launch_hoist_t(const HoistParams& p, unsigned long long* out,
                           int sm_count, cudaStream_t st) {
   const size_t smem = (size_t)p.n_hist * p.hist_words * 4;
   const void* fn = (const void*)k1_hoisted<NC, D, PR>;
-  int grid = blocks_for(fn, smem, sm_count);
+  int grid = 0;
+  const int threads = hoisted_block(fn, smem, sm_count, PR == 2, &grid);
   const uint64_t runs = p.run_end - p.run_begin;
-  const uint64_t need = (runs + kThreads - 1) / kThreads;
+  const uint64_t need = (runs + threads - 1) / threads;
   if (need < (uint64_t)grid) grid = (int)(need ? need : 1);
-  k1_hoisted<NC, D, PR><<<grid, kThreads, smem, st>>>(p, out);
+  k1_hoisted<NC, D, PR><<<grid, threads, smem, st>>>(p, out);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 1 : -(int)e;
 }

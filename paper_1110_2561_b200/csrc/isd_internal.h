@@ -18,6 +18,8 @@ constexpr int kTreeBits = 5;               // copies emitted as a 32-leaf tree
                                            // plus outer bits 5..u-1
 constexpr int kMaxClasses = ISD_MAX_CLASSES;
 constexpr int kThreads = 512;              // threads per enumeration block
+constexpr int kWideThreads = 1024;         // ... when only one block fits an
+                                           // SM (large paired histograms)
 
 // Parameters of the canonical kernel: one full class-mask evaluation per
 // configuration (the formulation of enumeration.py:167-205 on bit masks).
@@ -114,6 +116,9 @@ int launch_canonical(const CanonParams& p, unsigned long long* out,
                      int sm_count, void* stream, bool small_grid);
 int launch_hoisted(const HoistParams& p, unsigned long long* out,
                    int sm_count, void* stream);
+// threads per block (512 or 1024) and grid for a hoisted kernel
+int hoisted_block(const void* fn, size_t smem, int sm_count, bool may_widen,
+                  int* grid);
 // NVRTC-specialised k1 (jit.cpp): 1 launched, 0 unavailable (*why), <0 error
 int launch_hoisted_jit(const HoistParams& p, unsigned long long* out,
                        int sm_count, void* stream, std::string* why);

@@ -143,7 +143,8 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
        "{ return "
     << P.pair_both << "; }\n";
   o << "};\n";
-  o << "extern \"C\" __global__ void __launch_bounds__(" << kThreads
+  o << "extern \"C\" __global__ void __launch_bounds__("
+    << (P.pair == 2 ? kWideThreads : kThreads)
     << ") k1_jit(unsigned long long run_begin, unsigned long long nruns,\n"
        "    unsigned long long hi_step, unsigned long long lane_mask,\n"
        "    const IsdLanes lanes,\n"
@@ -163,6 +164,7 @@ struct JitKernel {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
   int grid = 0;
+  int threads = kThreads;
 };
 
 static std::mutex g_jit_mu;
@@ -233,20 +235,13 @@ static JitKernel build_kernel(const HoistParams& P, int sm_count) {
                                       0, nullptr, nullptr, 0);
   if (e == cudaSuccess) e = cudaLibraryGetKernel(&jk.kern, jk.lib, "k1_jit");
   const size_t smem = (size_t)P.n_hist * P.hist_words * 4;
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute((const void*)jk.kern,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-  int per_sm = 0;
-  if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, (const void*)jk.kern, kThreads, smem);
   if (e != cudaSuccess) {
     jk.why = std::string("loading the JIT kernel: ") + cudaGetErrorString(e);
     cudaGetLastError();
     return jk;
   }
-  jk.grid = (per_sm < 1 ? 1 : per_sm) * sm_count;
+  jk.threads = hoisted_block((const void*)jk.kern, smem, sm_count,
+                             P.pair == 2, &jk.grid);
   jk.ok = true;
   return jk;
 }
@@ -280,11 +275,11 @@ int launch_hoisted_jit(const HoistParams& P, unsigned long long* out,
   for (int i = 0; i < 5; ++i) lanes.v[i] = P.lane_vec[i];
   void* args[] = {&run_begin, &nruns, &hi_step, &lane_mask, &lanes, &out};
   int grid = jk.grid;
-  const uint64_t need = (nruns + kThreads - 1) / kThreads;
+  const uint64_t need = (nruns + jk.threads - 1) / jk.threads;
   if (need < (uint64_t)grid) grid = (int)(need ? need : 1);
   const size_t smem = (size_t)P.n_hist * P.hist_words * 4;
   cudaError_t e = cudaLaunchKernel((const void*)jk.kern, dim3(grid),
-                                   dim3(kThreads), args, smem,
+                                   dim3(jk.threads), args, smem,
                                    (cudaStream_t)stream);
   if (e != cudaSuccess) return -(int)e;
   return 1;
