@@ -403,7 +403,9 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
   fill_hoist(lat, &info, &hp);
   const uint64_t runs_per_launch = kMaxPerLaunch >> k;
   // large walks use the per-lattice NVRTC specialisation (jit.cpp)
-  bool use_jit = env_long("ISD_JIT", 1) != 0 && end - start >= kTuneConfigs;
+  // (ISD_JIT=0: never; ISD_JIT=2: for every hoisted walk — tests)
+  const long jit_mode = env_long("ISD_JIT", 1);
+  bool use_jit = jit_mode != 0 && (end - start >= kTuneConfigs || jit_mode == 2);
   g_kernel_info = use_jit ? "k1_hoisted_jit" : "k1_hoisted_aot";
   for (uint64_t r = r0; r < r1;) {
     const uint64_t re = (r1 - r > runs_per_launch) ? r + runs_per_launch : r1;

@@ -153,6 +153,22 @@ struct RuntimeTraits {
   __device__ uint32_t pair_words(int i) const { return P.pair_words[i]; }
   __device__ int32_t pair_deg(int i) const { return P.pair_deg[i]; }
   __device__ int32_t pair_both() const { return P.pair_both; }
+  // no Gray sites in the ahead-of-time build (the stubs are never called)
+  __host__ __device__ static constexpr int gray() { return 0; }
+  __device__ uint32_t g_mask() const { return 0; }
+  __device__ uint32_t g_bit(int) const { return 0; }
+  __device__ uint64_t g_nm1(int) const { return 0; }
+  __device__ uint64_t g_jn1(int) const { return 0; }
+  __device__ uint64_t g_nm2(int) const { return 0; }
+  __device__ uint64_t g_jn2(int) const { return 0; }
+  __device__ uint32_t g_nm1v(int) const { return 0; }
+  __device__ uint32_t g_jn1v(int) const { return 0; }
+  __device__ uint32_t g_nm2v(int) const { return 0; }
+  __device__ uint32_t g_jn2v(int) const { return 0; }
+  __device__ int32_t g_deg(int) const { return 0; }
+  __device__ int32_t g_csum(int) const { return 0; }
+  __device__ int32_t g_odd(int) const { return 0; }
+  __device__ int32_t g_cdelta(int, int) const { return 0; }
 };
 
 // (mode-2 histograms can be too large for two blocks per SM: those kernels

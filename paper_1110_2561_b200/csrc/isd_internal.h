@@ -84,6 +84,19 @@ struct HoistParams {
   uint32_t pair_words[2];        // stride between pattern planes
   int32_t pair_deg[2];           // D: degree of the paired site
   int32_t pair_both;             // mode 2: extra e change of the double flip
+  // Gray sites (NVRTC build only; the AOT kernel walks every loop subset
+  // from scratch): the `gray` lowest loop sites are flipped one at a time
+  // inside an iteration.  Per site: its loop bit, its bonds to non-copy
+  // sites (masks as for the copy sites; v = restricted to loop bits), their
+  // count, and the shift of each copy site's unsatisfied count when it
+  // flips up (cdelta, csum = their sum).
+  uint32_t gray;
+  uint32_t g_mask;
+  uint32_t g_bit[2];
+  uint64_t g_nm1[2], g_jn1[2], g_nm2[2], g_jn2[2];
+  uint32_t g_nm1v[2], g_jn1v[2], g_nm2v[2], g_jn2v[2];
+  int32_t g_deg[2], g_csum[2], g_odd[2];
+  int32_t g_cdelta[2][kCopyBits];
 };
 
 // Largest paired histogram (words): two CTAs of 512 threads per SM fit

@@ -12,6 +12,7 @@
 #include <dlfcn.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -142,6 +143,29 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
   o << "  __device__ __forceinline__ static constexpr int32_t pair_both() "
        "{ return "
     << P.pair_both << "; }\n";
+  // Gray sites
+  o << "  __host__ __device__ static constexpr int gray() { return " << P.gray
+    << "; }\n";
+  c32("g_mask", P.g_mask);
+  emit_switch(o, "uint32_t", "g_bit", P.g_bit, 2, "u");
+  emit_switch(o, "uint64_t", "g_nm1", P.g_nm1, 2, "ull");
+  emit_switch(o, "uint64_t", "g_jn1", P.g_jn1, 2, "ull");
+  emit_switch(o, "uint64_t", "g_nm2", P.g_nm2, 2, "ull");
+  emit_switch(o, "uint64_t", "g_jn2", P.g_jn2, 2, "ull");
+  emit_switch(o, "uint32_t", "g_nm1v", P.g_nm1v, 2, "u");
+  emit_switch(o, "uint32_t", "g_jn1v", P.g_jn1v, 2, "u");
+  emit_switch(o, "uint32_t", "g_nm2v", P.g_nm2v, 2, "u");
+  emit_switch(o, "uint32_t", "g_jn2v", P.g_jn2v, 2, "u");
+  emit_switch(o, "int32_t", "g_deg", P.g_deg, 2, "");
+  emit_switch(o, "int32_t", "g_csum", P.g_csum, 2, "");
+  emit_switch(o, "int32_t", "g_odd", P.g_odd, 2, "");
+  o << "  __device__ __forceinline__ static constexpr int32_t g_cdelta(int g, "
+       "int q) {\n";
+  for (int g = 0; g < 2; ++g)
+    for (int q = 0; q < kCopyBits; ++q)
+      o << "    if (g == " << g << " && q == " << q << ") return "
+        << P.g_cdelta[g][q] << ";\n";
+  o << "    return 0;\n  }\n";
   o << "};\n";
   o << "extern \"C\" __global__ void __launch_bounds__("
     << (P.pair == 2 ? kWideThreads : kThreads)
@@ -219,6 +243,13 @@ static bool compile_cubin(const HoistParams& P, std::vector<char>* cubin,
   cubin->resize(n);
   nv.cubin(prog, cubin->data());
   nv.destroy(&prog);
+  // inspection knob: ISD_JIT_DUMP=<path> writes the cubin (cuobjdump -sass)
+  if (const char* dump = std::getenv("ISD_JIT_DUMP")) {
+    if (FILE* f = std::fopen(dump, "wb")) {
+      std::fwrite(cubin->data(), 1, cubin->size(), f);
+      std::fclose(f);
+    }
+  }
   return true;
 }
 

@@ -123,9 +123,20 @@ __device__ __forceinline__ void k1_hoisted_body(
         (unsigned int)(__popcll(xt & L.odd_mask()) + L.e_parity()) & 1u;
     const unsigned int odd_loop =
         (unsigned int)L.odd_mask() & L.loop_mask();
+    // Gray sites (JIT builds): the G lowest loop sites are walked in Gray
+    // order inside one iteration, each step one site flip updated from its
+    // neighbours; their run-site partners are counted once per run
+    constexpr int G = T::gray();
+    int gpr[G > 0 ? G : 1];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      gpr[g] = __popcll((xt ^ L.g_jn1(g)) & L.g_nm1(g) & above_k);
+      if (DOUBLE) gpr[g] += __popcll((xt ^ L.g_jn2(g)) & L.g_nm2(g) & above_k);
+    }
     // ---- loop over the subsets of the loop sites ----
+    const unsigned int outer = L.loop_mask() & ~L.g_mask();
     unsigned int jb = 0;
-    for (unsigned int it = 0; it < nloop; ++it) {
+    for (unsigned int it = 0; it < (nloop >> G); ++it) {
       int e = e_run;
 #pragma unroll
       for (int c = 0; c < NC; ++c)
@@ -142,41 +153,78 @@ __device__ __forceinline__ void k1_hoisted_body(
         if (PAIR >= 1 && q == 6) pair_off += (unsigned int)nq * L.pair_bytes(0);
         if (PAIR >= 2 && q == 5) pair_off += (unsigned int)nq * L.pair_bytes(1);
       }
-      const unsigned int par = (par_run + __popc(jb & odd_loop)) & 1u;
+      unsigned int par = (par_run + __popc(jb & odd_loop)) & 1u;
       // a[c] carries no per-copy constant: addr(c) = a[c] + koff(c), where
       // koff(c) = popc(c) row_bytes + e_bytes * (copy-copy unsatisfied
       // bonds of c) folds into the RED's address offset.  128 copies: a
       // 32-leaf subset-sum tree over copy bits 0-4 (live set <= 16), each
-      // leaf spawning its three siblings in bits 5 and 6.
-      const unsigned int a0 = a_run + (unsigned int)__popc(jb) * L.row_bytes() +
-                              (unsigned int)e * L.e_bytes() +
-                              par * (unsigned int)L.plane_bytes() + pair_off;
-      unsigned int a[32];
+      // leaf spawning its siblings in bits 5 and 6 (paired bits: none).
+      auto emit = [&]() {
+        const unsigned int a0 = a_run + (unsigned int)__popc(jb) * L.row_bytes() +
+                                (unsigned int)e * L.e_bytes() +
+                                par * (unsigned int)L.plane_bytes() + pair_off;
+        unsigned int a[32];
 #pragma unroll
-      for (int cl = 0; cl < 32; ++cl) {
-        if (cl == 0) {
-          a[0] = a0;
-        } else {
-          const int top = 31 - __clz(cl);
-          a[cl] = a[cl ^ (1 << top)] + d[top];
+        for (int cl = 0; cl < 32; ++cl) {
+          if (cl == 0) {
+            a[0] = a0;
+          } else {
+            const int top = 31 - __clz(cl);
+            a[cl] = a[cl ^ (1 << top)] + d[top];
+          }
+          ISD_CHECK_ADDR(a[cl] + L.koff(cl), hbase, hbytes);
+          isd_red_shared_inc(a[cl] + L.koff(cl));
+          const unsigned int b1 = a[cl] + d[5];
+          if (PAIR <= 1) {
+            ISD_CHECK_ADDR(b1 + L.koff(cl + 32), hbase, hbytes);
+            isd_red_shared_inc(b1 + L.koff(cl + 32));
+          }
+          if (PAIR == 0) {
+            const unsigned int b2 = a[cl] + d[6];
+            const unsigned int b3 = b1 + d[6];
+            ISD_CHECK_ADDR(b2 + L.koff(cl + 64), hbase, hbytes);
+            isd_red_shared_inc(b2 + L.koff(cl + 64));
+            ISD_CHECK_ADDR(b3 + L.koff(cl + 96), hbase, hbytes);
+            isd_red_shared_inc(b3 + L.koff(cl + 96));
+          }
         }
-        ISD_CHECK_ADDR(a[cl] + L.koff(cl), hbase, hbytes);
-        isd_red_shared_inc(a[cl] + L.koff(cl));
-        const unsigned int b1 = a[cl] + d[5];
-        if (PAIR <= 1) {
-          ISD_CHECK_ADDR(b1 + L.koff(cl + 32), hbase, hbytes);
-          isd_red_shared_inc(b1 + L.koff(cl + 32));
-        }
-        if (PAIR == 0) {
-          const unsigned int b2 = a[cl] + d[6];
-          const unsigned int b3 = b1 + d[6];
-          ISD_CHECK_ADDR(b2 + L.koff(cl + 64), hbase, hbytes);
-          isd_red_shared_inc(b2 + L.koff(cl + 64));
-          ISD_CHECK_ADDR(b3 + L.koff(cl + 96), hbase, hbytes);
-          isd_red_shared_inc(b3 + L.koff(cl + 96));
-        }
+      };
+      // flip Gray site g (up or down) in the current subset: its bonds to
+      // non-copy sites change e by +-(D_g - 2 n_g), n_g from the current
+      // neighbours; its bonds to copy sites shift those sites' unsatisfied
+      // counts by the per-lattice g_cdelta (and e, d, the pattern planes)
+      auto flip = [&](int g, bool up) {
+        int ng = gpr[g] + __popc((jb ^ L.g_jn1v(g)) & L.g_nm1v(g));
+        if (DOUBLE) ng += __popc((jb ^ L.g_jn2v(g)) & L.g_nm2v(g));
+        const int sg = up ? 1 : -1;
+        e += sg * (L.g_deg(g) - 2 * ng + L.g_csum(g));
+#pragma unroll
+        for (int q = 0; q < 7; ++q)
+          if (L.g_cdelta(g, q) != 0) {
+            d[q] -= (unsigned int)(sg * 2 * (int)L.e_bytes() * L.g_cdelta(g, q));
+            if (PAIR >= 1 && q == 6)
+              pair_off += (unsigned int)(sg * L.g_cdelta(g, q) *
+                                         (int)L.pair_bytes(0));
+            if (PAIR >= 2 && q == 5)
+              pair_off += (unsigned int)(sg * L.g_cdelta(g, q) *
+                                         (int)L.pair_bytes(1));
+          }
+        if (L.g_odd(g)) par ^= 1u;
+        jb ^= L.g_bit(g);
+      };
+      emit();
+      if constexpr (G == 1) {
+        flip(0, true);
+        emit();
+      } else if constexpr (G == 2) {
+        flip(0, true);
+        emit();
+        flip(1, true);
+        emit();
+        flip(0, false);
+        emit();
       }
-      jb = (jb - L.loop_mask()) & L.loop_mask();  // next subset
+      jb = ((jb & outer) - outer) & outer;  // next subset (Gray sites clear)
     }
   }
   __syncthreads();

@@ -832,6 +832,53 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
     p->pair_bytes[i] = 4 * info->pair_words[i];
     p->pair_deg[i] = info->pair_degree[i];
   }
+  // Gray sites: the lowest min(2, l) loop sites (ISD_GRAY=0|1|2 caps it)
+  {
+    long g = env_int("ISD_GRAY", 2);
+    if (g < 0) g = 0;
+    if (g > 2) g = 2;
+    if (g > (long)info->l) g = (long)info->l;
+    p->gray = (uint32_t)g;
+    int slot_of[64];
+    for (int i = 0; i < 64; ++i) slot_of[i] = -1;
+    for (int t = 0; t < kCopyBits; ++t) slot_of[info->copy_site[t]] = t;
+    uint64_t rest = loop;
+    for (uint32_t gi = 0; gi < p->gray; ++gi) {
+      const int j = __builtin_ctzll(rest);
+      rest &= rest - 1;
+      p->g_bit[gi] = 1u << j;
+      p->g_mask |= 1u << j;
+      p->g_odd[gi] = info->e_mode ? (int)((info->odd_mask >> j) & 1) : 0;
+      for (uint32_t c = 0; c < lat->n_classes; ++c) {
+        const isd_bond_class& cl = lat->classes[c];
+        for (int side = 0; side < 2; ++side) {
+          // bond (i, i + s) with j at either end
+          const int i = side ? j - (int)cl.shift : j;
+          if (i < 0 || !((cl.bond_mask >> i) & 1)) continue;
+          const int partner = side ? i : i + (int)cl.shift;
+          const int neg = (int)((cl.jneg_mask >> i) & 1);
+          if (slot_of[partner] >= 0) {
+            p->g_cdelta[gi][slot_of[partner]] += 1 - 2 * neg;
+            p->g_csum[gi] += 1 - 2 * neg;
+            continue;
+          }
+          const uint64_t bit = 1ull << partner;
+          if (!(p->g_nm1[gi] & bit)) {
+            p->g_nm1[gi] |= bit;
+            if (neg) p->g_jn1[gi] |= bit;
+          } else {  // a periodic axis of length 2: the doubled bond
+            p->g_nm2[gi] |= bit;
+            if (neg) p->g_jn2[gi] |= bit;
+          }
+          p->g_deg[gi] += 1;
+        }
+      }
+      p->g_nm1v[gi] = (uint32_t)(p->g_nm1[gi] & loop);
+      p->g_jn1v[gi] = (uint32_t)(p->g_jn1[gi] & loop);
+      p->g_nm2v[gi] = (uint32_t)(p->g_nm2[gi] & loop);
+      p->g_jn2v[gi] = (uint32_t)(p->g_jn2[gi] & loop);
+    }
+  }
   // a paired site's RED lands in pattern plane n + u(c): u(c) = its bonds
   // to the copy sites of c left unsatisfied while it is down (the other
   // paired site down too); flipping it changes unsat_cc by (its copy-copy

@@ -77,3 +77,28 @@ def test_slices_match_c_oracle(spec):
         table, _ = enumerate_range_timed(spec, start, start + size)
         assert np.array_equal(table.view(np.int64),
                               oracle_table(spec, start, start + size)), start
+
+
+# The NVRTC-specialised kernel (normally only for walks >= 2^33) walks the
+# lowest 1-2 loop sites in Gray order, updating e and the copy-site counts
+# per flip; force it (ISD_JIT=2), a loop width, each Gray level and each
+# pairing mode on lattices of every kind, against the C oracle.
+JIT_SPECS = [s for s in WHOLE if s.num_spins >= 14][:8]
+
+
+@pytest.mark.parametrize("gray", ["1", "2"])
+@pytest.mark.parametrize("pair", ["0", "1", "2"])
+@pytest.mark.parametrize("spec", JIT_SPECS, ids=repr)
+def test_jit_gray_walk_matches_c_oracle(spec, pair, gray, monkeypatch):
+    monkeypatch.setenv("ISD_JIT", "2")
+    monkeypatch.setenv("ISD_LOOP_BITS", "4")
+    monkeypatch.setenv("ISD_GRAY", gray)
+    monkeypatch.setenv("ISD_PAIR", pair)
+    got = isd.full_dos(spec)
+    assert _native_kernel_path().startswith("k1_hoisted_jit")
+    assert np.array_equal(got.counts, oracle_table(spec))
+
+
+def _native_kernel_path():
+    from paper_1110_2561_b200 import _native
+    return _native.kernel_info()

@@ -369,10 +369,13 @@ def test_bounds_checked_build_runs_clean():
         "from paper_1110_2561_b200.workloads import workloads\n"
         "from paper_1110_2561_b200.enumeration import enumerate_range_timed\n"
         "import paper_1110_2561_b200 as isd\n"
-        "for n in ('c3', 'c4', 'c5'):\n"
-        "    s = workloads()[n].spec\n"
-        "    t, _ = enumerate_range_timed(s, 0, 1 << 33)\n"
-        "    assert int(t.sum()) == 1 << 33\n"
+        "import os\n"
+        "for pm in ('0', '1', '2'):\n"
+        "    os.environ['ISD_PAIR'] = pm\n"
+        "    for n in ('c3', 'c4', 'c5'):\n"
+        "        s = workloads()[n].spec\n"
+        "        t, _ = enumerate_range_timed(s, 0, 1 << 33)\n"
+        "        assert int(t.sum()) == 1 << 33\n"
         "print('bounds ok')\n"
     ) % (root, os.path.join(root, "tools", "sanitize_case.py"))
     r = subprocess.run([sys.executable, "-c", code], env=env,
