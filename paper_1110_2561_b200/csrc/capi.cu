@@ -71,10 +71,29 @@ struct DevState {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   unsigned long long* d_counts = nullptr;  // (41 x 121) max table
   size_t d_counts_bytes = 0;
-  double* d_buf = nullptr;  // thermo fields/temps/out
+  double* d_buf = nullptr;  // thermo table/fields/temps/out
   size_t d_buf_bytes = 0;
+  void* h_stage = nullptr;  // pinned staging for the host-buffer calls
+  size_t h_stage_bytes = 0;
 };
 static DevState g_dev[64];
+
+// Pinned host staging of at least `bytes` (grown on demand): host-buffer
+// calls copy through it so their transfers are true async DMA, not the
+// driver's pageable bounce path.
+static int stage_buffer(DevState* s, size_t bytes, void** out) {
+  if (s->h_stage_bytes < bytes) {
+    if (s->h_stage) cudaFreeHost(s->h_stage);
+    s->h_stage = nullptr;
+    s->h_stage_bytes = 0;
+    const size_t want = bytes < 65536 ? 65536 : bytes;
+    cudaError_t e = cudaHostAlloc(&s->h_stage, want, cudaHostAllocDefault);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaHostAlloc(staging)");
+    s->h_stage_bytes = want;
+  }
+  *out = s->h_stage;
+  return ISD_OK;
+}
 
 // Select `device` on this thread, initialise its state once, and lock it:
 // host-buffer calls on different devices run concurrently (one host thread
@@ -518,11 +537,15 @@ int isd_enumerate(const isd_lattice* lat, uint64_t start, uint64_t end,
   bump_launches((uint64_t)nl);
   if (rc) return rc;
   cudaEventRecord(s->ev1, s->stream);
-  cudaError_t e = cudaMemcpyAsync(counts_host, s->d_counts, bytes,
+  void* stage = nullptr;
+  rc = stage_buffer(s, bytes, &stage);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(stage, s->d_counts, bytes,
                                   cudaMemcpyDeviceToHost, s->stream);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(D2H)");
   e = cudaStreamSynchronize(s->stream);
   if (e != cudaSuccess) return cuda_fail(e, "enumeration kernels");
+  std::memcpy(counts_host, stage, bytes);
   if (device_ms) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, s->ev0, s->ev1);
@@ -578,42 +601,43 @@ int isd_thermo(const uint64_t* counts_host, uint32_t n_spins, uint32_t n_bonds,
   std::unique_lock<std::mutex> lock;
   int rc = get_dev(device, &s, &lock);
   if (rc) return rc;
+  // one block, host and device alike: [table | fields | temps | results]
   const size_t tbytes = (size_t)(n_spins + 1) * (n_bonds + 1) * 8;
   const size_t npts = (size_t)n_fields * n_temps;
-  const size_t dbytes = (n_fields + n_temps + npts * ISD_THERMO_FIELDS) * 8;
-  if (s->d_counts_bytes < tbytes) {
-    if (s->d_counts) cudaFree(s->d_counts);
-    s->d_counts = nullptr;
-    s->d_counts_bytes = 0;
-    cudaError_t e = cudaMalloc(&s->d_counts, tbytes);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(counts)");
-    s->d_counts_bytes = tbytes;
-  }
-  if (s->d_buf_bytes < dbytes) {
+  const size_t in_bytes = tbytes + (size_t)(n_fields + n_temps) * 8;
+  const size_t out_bytes = npts * ISD_THERMO_FIELDS * 8;
+  if (s->d_buf_bytes < in_bytes + out_bytes) {
     if (s->d_buf) cudaFree(s->d_buf);
     s->d_buf = nullptr;
     s->d_buf_bytes = 0;
-    cudaError_t e = cudaMalloc(&s->d_buf, dbytes);
+    cudaError_t e = cudaMalloc(&s->d_buf, in_bytes + out_bytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(thermo)");
-    s->d_buf_bytes = dbytes;
+    s->d_buf_bytes = in_bytes + out_bytes;
   }
-  double* d_f = s->d_buf;
-  double* d_t = d_f + n_fields;
-  double* d_o = d_t + n_temps;
+  void* stage = nullptr;
+  rc = stage_buffer(s, in_bytes + out_bytes, &stage);
+  if (rc) return rc;
+  char* h = static_cast<char*>(stage);
+  std::memcpy(h, counts_host, tbytes);
+  std::memcpy(h + tbytes, fields, (size_t)n_fields * 8);
+  std::memcpy(h + tbytes + (size_t)n_fields * 8, temps, (size_t)n_temps * 8);
+  char* d = reinterpret_cast<char*>(s->d_buf);
+  const uint64_t* d_c = reinterpret_cast<const uint64_t*>(d);
+  const double* d_f = reinterpret_cast<const double*>(d + tbytes);
+  const double* d_t = d_f + n_fields;
+  double* d_o = reinterpret_cast<double*>(d + in_bytes);
   cudaStream_t st = s->stream;
-  cudaMemcpyAsync(s->d_counts, counts_host, tbytes, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d_f, fields, n_fields * 8, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d_t, temps, n_temps * 8, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d, h, in_bytes, cudaMemcpyHostToDevice, st);
   cudaEventRecord(s->ev0, st);
-  rc = isd_thermo_async(reinterpret_cast<const uint64_t*>(s->d_counts),
-                        n_spins, n_bonds, energy_scale, d_f, n_fields, d_t,
-                        n_temps, d_o, st);
+  rc = isd_thermo_async(d_c, n_spins, n_bonds, energy_scale, d_f, n_fields,
+                        d_t, n_temps, d_o, st);
   if (rc) return rc;
   cudaEventRecord(s->ev1, st);
-  cudaError_t e = cudaMemcpyAsync(out_host, d_o, npts * ISD_THERMO_FIELDS * 8,
+  cudaError_t e = cudaMemcpyAsync(h + in_bytes, d_o, out_bytes,
                                   cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return cuda_fail(e, "thermo kernel");
+  std::memcpy(out_host, h + in_bytes, out_bytes);
   if (device_ms) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, s->ev0, s->ev1);

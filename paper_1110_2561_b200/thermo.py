@@ -50,9 +50,9 @@ def thermo_grid(dos: DoSHistogram, fields, temps, *, device=None):
     log_z, free_energy, internal_energy, specific_heat, mean_magnetization,
     susceptibility, mean_abs_magnetization.
     """
-    fields = [float(h) for h in fields]
-    temps = [float(t) for t in temps]
-    if any(not t > 0 for t in temps):
+    fields = np.asarray(fields, dtype=np.float64).reshape(-1)
+    temps = np.asarray(temps, dtype=np.float64).reshape(-1)
+    if not np.all(temps > 0):  # (NaN fails too)
         raise ValueError("all temperatures must be > 0")
     _check_complete(dos)
     spec = dos.spec
