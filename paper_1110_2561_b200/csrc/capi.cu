@@ -245,7 +245,11 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   }
   // stage 2: the best few, timed as a real walk — one contiguous slice of
   // up to 2^36 configurations from the middle of the range (the spread
-  // sample ranks the candidates but not reliably enough to pick one)
+  // sample ranks the candidates but not reliably enough to pick one), with
+  // the kernel the walk will use: the NVRTC build when it is available
+  // (its Gray-order loop changes the instruction mix), compiled once per
+  // finalist and cached for the walk
+  const bool jit_ok = env_long("ISD_JIT", 1) != 0;
   std::sort(stage1.begin(), stage1.end());
   float best_ms = 1e30f;
   size_t best = stage1.empty() ? 0 : stage1[0].second;
@@ -265,8 +269,20 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     hp.run_end = hp.run_begin + len;
     hp.hi_step = 1;
     float ms = 0.f;
+    // (warm the finalist's kernel first: the JIT compile is not timed)
+    int x = 0;
+    if (jit_ok) {
+      std::string why;
+      HoistParams warm = hp;
+      warm.run_end = warm.run_begin + blk;
+      x = launch_hoisted_jit(warm, scratch, sms, st, &why);
+      if (x > 0) bump_launches(1);
+    }
     cudaEventRecord(e0, st);
-    launch_hoisted(hp, scratch, sms, st);
+    if (x > 0)
+      launch_hoisted_jit(hp, scratch, sms, st, nullptr);
+    else
+      launch_hoisted(hp, scratch, sms, st);
     cudaEventRecord(e1, st);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
