@@ -194,7 +194,8 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
       return;
     }
     pe.tuned = true;
-    for (size_t i = 0; i < pe.ranked.size() && (int)cands.size() < kTuneCandidates;
+    const int n_cand = (int)env_long("ISD_TUNE_CANDIDATES", kTuneCandidates);
+    for (size_t i = 0; i < pe.ranked.size() && (int)cands.size() < n_cand;
          ++i)
       cands.push_back(pe.ranked[i]);
   }
@@ -253,7 +254,8 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   std::sort(stage1.begin(), stage1.end());
   float best_ms = 1e30f;
   size_t best = stage1.empty() ? 0 : stage1[0].second;
-  for (size_t s2 = 0; s2 < stage1.size() && s2 < kTuneFinalists; ++s2) {
+  const size_t n_final = (size_t)env_long("ISD_TUNE_FINALISTS", kTuneFinalists);
+  for (size_t s2 = 0; s2 < stage1.size() && s2 < n_final; ++s2) {
     const size_t i = stage1[s2].second;
     HoistParams hp;
     fill_hoist(lat, &cands[i], &hp);

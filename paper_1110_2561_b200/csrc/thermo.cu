@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <mutex>
+
 #include "isd_internal.h"
 
 namespace isd {
@@ -219,18 +221,18 @@ int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
   // stream-ordered scratch: safe for concurrent calls on different streams.
   // Keep freed blocks in the device's default pool (threshold 64 MiB) so a
   // steady stream of calls does not go back to the driver every time.
-  static bool pool_ready[64] = {false};
+  static std::once_flag pool_ready[64];
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 64 && !pool_ready[dev]) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = 64ull << 20;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    cudaGetLastError();
-    pool_ready[dev] = true;
-  }
+  if (dev < 64)
+    std::call_once(pool_ready[dev], [dev] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = 64ull << 20;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      cudaGetLastError();
+    });
   void* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&scratch, sizeof(Cell) * bins + 16, st);
   if (e != cudaSuccess) return -(int)e;
