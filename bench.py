@@ -49,6 +49,8 @@ def parse_args():
     p.add_argument("--calibrate", action="store_true", default=True)
     p.add_argument("--extra-configs", default="c1,c2,c3,c4",
                    help="other configs timed (value only) into extra.configs")
+    p.add_argument("--no-graph", action="store_true",
+                   help="time eager steps instead of CUDA-graph replays")
     return p.parse_args()
 
 
@@ -321,25 +323,46 @@ def run_b200(args, wl):
                           dtype=torch.float64, device=dev)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 
-        def step():
-            ev[0].record(stream)
+        def work(st, after_k1=None):
+            # one step's GPU work on stream `st`: K1 over this rank's shard
+            # (+ memset of the table), the NCCL reduce, K2 on rank 0
             nl = _native.enumerate_device(lat, shard.start_index,
                                           shard.end_index, table.data_ptr(),
-                                          sp, accumulate=False, algo=algo)
-            ev[1].record(stream)
+                                          st, accumulate=False, algo=algo)
+            if after_k1 is not None:
+                after_k1()
             if use_dist:
                 dist.reduce(table, dst=0)
             if rank == 0:
                 nl += _native.thermo_device(
                     table.data_ptr(), spec.num_spins, spec.num_bonds,
                     abs(spec.coupling), fields.data_ptr(), len(w.fields),
-                    temps.data_ptr(), len(w.temps), out.data_ptr(), sp)
+                    temps.data_ptr(), len(w.temps), out.data_ptr(), st)
+            return nl
+
+        def step():
+            ev[0].record(stream)
+            nl = work(sp, lambda: ev[1].record(stream))
             ev[2].record(stream)
             return nl
 
+        def k1_only(st):
+            return _native.enumerate_device(lat, shard.start_index,
+                                            shard.end_index, table.data_ptr(),
+                                            st, accumulate=False, algo=algo)
+
+        step.work = work
+        step.k1_only = k1_only
         return step, ev, table, out
 
-    def time_device(w, steps, warmup, flip=False):
+    graph_info = {"mode": "eager"}
+
+    def time_device(w, steps, warmup, flip=False, graph=False):
+        """Per-step device ms (events on the launching stream), K1 ms, our
+        kernel launches in the timed region, and the result buffers.  With
+        `graph`, the timed steps replay a CUDA graph of one step (captured
+        after the eager warm-up and K1 timing); K1 ms comes from the eager
+        steps, the step time from the replays."""
         step, ev, table, out = device_step_fn(w, flip)
         for _ in range(warmup):
             step()
@@ -356,7 +379,42 @@ def run_b200(args, wl):
             k1.append(ev[0].elapsed_time(ev[1]))
         barrier()
         launches_lib = _native.launch_count() - l0
-        return tot, k1, launches_lib, table, out
+        if not graph:
+            return tot, k1, launches_lib, table, out
+        try:
+            g = torch.cuda.CUDAGraph()
+            g1 = torch.cuda.CUDAGraph()  # K1 alone (+ its table memset)
+            cap = torch.cuda.Stream(dev)
+            cap.wait_stream(stream)
+            torch.cuda.synchronize(dev)
+            with torch.cuda.graph(g, stream=cap):
+                per_step = step.work(cap.cuda_stream)
+            with torch.cuda.graph(g1, stream=cap):
+                step.k1_only(cap.cuda_stream)
+            g.replay()  # warm replays
+            g1.replay()
+            barrier()
+            gtot, gk1 = [], []
+            for graph_, acc in ((g1, gk1), (g, gtot)):
+                for _ in range(steps):
+                    flush.zero_()
+                    barrier()
+                    ev[0].record(stream)
+                    graph_.replay()
+                    ev[2].record(stream)
+                    ev[2].synchronize()
+                    acc.append(ev[0].elapsed_time(ev[2]))
+            barrier()
+            graph_info.update(mode="cuda-graph replay", nodes_per_step=per_step,
+                              eager_ms_per_step=sum(tot) / len(tot),
+                              eager_k1_ms=sum(k1) / len(k1))
+            return gtot, gk1, per_step * steps, table, out
+        except Exception as exc:  # capture unsupported here: eager numbers
+            print(f"[bench] CUDA graph capture failed ({exc}); eager steps",
+                  file=sys.stderr)
+            graph_info.update(mode="eager (graph capture failed)")
+            torch.cuda.synchronize(dev)
+            return tot, k1, launches_lib, table, out
 
     # ---- headline workload -------------------------------------------------
     cal = {}
@@ -370,7 +428,8 @@ def run_b200(args, wl):
 
     clocks = ClockSampler(local)
     clocks.start()
-    tot, k1, launches, table, out = time_device(wl, args.steps, args.warmup)
+    tot, k1, launches, table, out = time_device(wl, args.steps, args.warmup,
+                                                graph=not args.no_graph)
     clk = clocks.stop()
     kernel_path = _native.kernel_info()
 
@@ -469,6 +528,7 @@ def run_b200(args, wl):
                    "n_configs": n_cfg, "thermo_points": npts,
                    "parallelism": f"index-space shards x{world}",
                    "l2": "flushed (256 MiB write) between timed steps",
+                   "step": graph_info,
                    "verify_dos_passed": ok},
         "roofline": roof,
         "roofline_int_pipe": roof_int,
