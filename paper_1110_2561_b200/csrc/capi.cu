@@ -215,14 +215,14 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   // space votes and all candidates see the same spread
   const uint64_t runs = kTuneConfigs >> cands[0].k;
   const uint64_t body = run1 - run0;
-  std::vector<std::pair<float, size_t>> stage1;
-  for (size_t i = 0; i < cands.size(); ++i) {
+  // per-run ms of a candidate on the spread sample (< 0: not applicable)
+  auto time_spread = [&](const isd_plan_info& cand) -> float {
     HoistParams hp;
-    fill_hoist(lat, &cands[i], &hp);
+    fill_hoist(lat, &cand, &hp);
     uint64_t span_bits = hp.lane_mask;
     for (int v = 0; v < 5; ++v) span_bits |= hp.lane_vec[v];
     const uint64_t blk = 1ull << lane_span(span_bits);
-    if (body < blk || body < runs) continue;
+    if (body < blk || body < runs) return -1.f;
     const uint64_t warps = runs / 32;
     // warp slots must stay inside whole lane blocks of the body
     const uint64_t usable = (body / blk) * (blk / 32);
@@ -242,7 +242,35 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     bump_launches(2);
-    stage1.push_back({ms / (float)(warps * 32), i});  // per run
+    return ms / (float)(warps * 32);
+  };
+  std::vector<std::pair<float, size_t>> stage1;
+  for (size_t i = 0; i < cands.size(); ++i) {
+    const float t = time_spread(cands[i]);
+    if (t >= 0.f) stage1.push_back({t, i});
+  }
+  std::sort(stage1.begin(), stage1.end());
+  // optional GPU hill climb of the best candidate's lane pattern, scored on
+  // the same spread sample (ISD_GPU_CLIMB = steps); the result joins the
+  // finalists
+  const long climb = env_long("ISD_GPU_CLIMB", 0);
+  if (climb > 0 && !stage1.empty()) {
+    isd_plan_info cur = cands[stage1[0].second];
+    float cur_t = stage1[0].first;
+    int run_bits = 0;
+    while (run_bits < 63 && (2ull << run_bits) <= body) ++run_bits;
+    uint64_t seed = 0x6A09E667F3BCC909ull;
+    for (long step = 0; step < climb; ++step) {
+      isd_plan_info q = cur;
+      if (!mutate_lanes(lat, run_bits, &seed, &q)) continue;
+      const float t = time_spread(q);
+      if (t >= 0.f && t < cur_t * 0.999f) {
+        cur = q;
+        cur_t = t;
+      }
+    }
+    cands.push_back(cur);
+    stage1.insert(stage1.begin(), {cur_t, cands.size() - 1});
   }
   // stage 2: the best few, timed as a real walk — one contiguous slice of
   // up to 2^36 configurations from the middle of the range (the spread
@@ -251,7 +279,6 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   // (its Gray-order loop changes the instruction mix), compiled once per
   // finalist and cached for the walk
   const bool jit_ok = env_long("ISD_JIT", 1) != 0;
-  std::sort(stage1.begin(), stage1.end());
   float best_ms = 1e30f;
   size_t best = stage1.empty() ? 0 : stage1[0].second;
   const size_t n_final = (size_t)env_long("ISD_TUNE_FINALISTS", kTuneFinalists);

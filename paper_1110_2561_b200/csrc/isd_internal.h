@@ -119,6 +119,9 @@ int lane_span(uint64_t lane_mask);
 // lanes taking the 5 lowest run bits (valid for any launch)
 void default_lanes(uint64_t* lane_mask, uint64_t* lane_vec);
 int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint);
+// one random move of the plan's lane pattern within `run_bits` run bits
+bool mutate_lanes(const isd_lattice* lat, int run_bits, uint64_t* seed,
+                  isd_plan_info* info);
 void fill_canon(const isd_lattice* lat, CanonParams* p);
 void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
                 HoistParams* p);

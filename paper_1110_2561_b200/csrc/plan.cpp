@@ -153,6 +153,43 @@ static std::vector<std::vector<int>> run_neighbors(const isd_lattice* lat,
   return nbr;
 }
 
+// One random move of a plan's lane pattern inside the low `run_bits` run
+// bits (the autotuner's GPU hill climb): re-pivot a lane bit (dropping its
+// partner), or give it a new random neighbour partner, or none.  Returns
+// false when the draw is not a valid pattern.
+bool mutate_lanes(const isd_lattice* lat, int run_bits, uint64_t* seed,
+                  isd_plan_info* info) {
+  const int k = (int)info->k;
+  if (run_bits < 6) return false;
+  uint64_t pivots = info->lane_mask, partners = 0;
+  for (int v = 0; v < 5; ++v) partners |= info->lane_vec[v] & ~pivots;
+  const int i = (int)(rng_next(seed) % 5);
+  const uint64_t piv_bit = info->lane_vec[i] & pivots;
+  if (!piv_bit) return false;
+  const int piv = __builtin_ctzll(piv_bit);
+  if (rng_next(seed) & 1) {
+    const int nb = (int)(rng_next(seed) % run_bits);
+    if (((pivots | partners) >> nb) & 1) return false;
+    info->lane_mask = (pivots & ~piv_bit) | (1ull << nb);
+    info->lane_vec[i] = 1ull << nb;
+  } else {
+    const std::vector<std::vector<int>> nbr = run_neighbors(lat, k, run_bits);
+    std::vector<int> cand;
+    for (int c : nbr[piv])
+      if (!((pivots >> c) & 1) && !((partners >> c) & 1)) cand.push_back(c);
+    const size_t pick = rng_next(seed) % (cand.size() + 1);
+    info->lane_vec[i] = piv_bit;
+    if (pick < cand.size()) info->lane_vec[i] |= 1ull << cand[pick];
+  }
+  // the lane vectors must stay a triangular (pivoted) basis: pivots are
+  // the lowest bit... any pivot works as long as no vector holds another's
+  // pivot
+  for (int v = 0; v < 5; ++v)
+    if (__builtin_popcountll(info->lane_vec[v] & info->lane_mask) != 1)
+      return false;
+  return true;
+}
+
 // Candidate lane patterns: contiguous windows of 5 run bits, plus (for
 // large walks) random 5-subsets — half of them from even-degree sites,
 // whose flips keep the lanes' e parity equal — and random "dominoes": each
