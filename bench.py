@@ -198,10 +198,16 @@ class ClockSampler:
 def ncu_traffic(config):
     """dram read+write bytes per launch of k1_hoisted from the committed
     ncu --set full capture (profiles/r1_ncu_k1_hoisted_<config>.txt)."""
-    path = os.path.join(ROOT, "profiles", f"r1_ncu_k1_jit_{config}.txt")
-    if not os.path.exists(path):
-        path = os.path.join(ROOT, "profiles", f"r1_ncu_k1_hoisted_{config}.txt")
-    if not os.path.exists(path):
+    # newest capture of the kernel the walk runs first
+    for name in (f"r1_ncu_k1_jit_gray_{config}.txt",
+                 f"r1_ncu_k1_jit_pair2_{config}.txt",
+                 f"r1_ncu_k1_jit_pair_{config}.txt",
+                 f"r1_ncu_k1_jit_{config}.txt",
+                 f"r1_ncu_k1_hoisted_{config}.txt"):
+        path = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(path):
+            break
+    else:
         return None
     total = 0.0
     scale = {"[byte]": 1, "[Kbyte]": 1e3, "[Mbyte]": 1e6, "[Gbyte]": 1e9}
