@@ -11,6 +11,14 @@ space by its top bits and combine the per-GPU tables with one NCCL reduce
 """
 
 from ._native import NativeError, current_device, set_device
+from .crosscheck import (
+    ORACLE_MAX_SPINS,
+    brute_force_log_z,
+    decode_spins,
+    oracle_energy,
+    oracle_full_dos,
+    oracle_magnetization,
+)
 from .bench import (
     BenchRecord,
     ResultMismatchError,
@@ -82,5 +90,6 @@ __all__ = [
     "gpu_count", "make_shards", "merge", "partition_point", "popcount",
     "random_bond_signs", "set_device", "spin_excess", "temperature_grid",
     "thermo_grid", "thermo_sweep", "total_energy", "unsatisfied_bonds",
-    "verify_dos",
+    "verify_dos", "ORACLE_MAX_SPINS", "brute_force_log_z", "decode_spins",
+    "oracle_energy", "oracle_full_dos", "oracle_magnetization",
 ]

@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 import paper_1110_2561_b200 as isd
+import paper_1110_2561_b200.crosscheck  # noqa: F401  (isd.crosscheck)
 from golden_io import read_csv_table
 
 
@@ -217,3 +218,79 @@ def test_specific_heat_has_one_peak():
     assert 0 < peak < len(c) - 1
     assert all(c[i] <= c[i + 1] + 1e-12 for i in range(peak - 5))
     assert all(c[i] >= c[i + 1] - 1e-12 for i in range(peak + 5, len(c) - 1))
+
+
+# -- cross-check API (the reference's oracle.py names) ----------------------
+
+def test_crosscheck_scalar_helpers_match_naive_oracle():
+    from oracle import naive
+    rng = random.Random(5)
+    for dims, kw in [((3, 4, 1), {}), ((2, 2, 3), {}), ((2, 3, 1), {}),
+                     ((4, 4, 1), dict(boundary="free")), ((3, 3, 2), {})]:
+        for j in (1, -2.5, 0.5):
+            spec = isd.LatticeSpec(*dims, j, **kw)
+            assert len(isd.crosscheck.bond_pairs(spec)) == spec.num_bonds
+            for x in rng.sample(range(spec.num_configs), 40):
+                spins = isd.decode_spins(spec, x)
+                assert len(spins) == spec.num_spins
+                assert isd.oracle_energy(spins, spec) == naive.energy_of(
+                    *dims, x, j, spec.periodic)
+                assert isd.oracle_energy(spins, spec) == isd.total_energy(
+                    isd.decode_config(spec, x), spec)
+                assert isd.oracle_magnetization(spins) == isd.spin_excess(
+                    isd.decode_config(spec, x), spec)
+
+
+def test_crosscheck_signed_energy_matches_unsatisfied_bonds():
+    base = isd.LatticeSpec(3, 4)
+    spec = isd.LatticeSpec(3, 4, bond_signs=isd.random_bond_signs(base, 9))
+    for x in range(0, spec.num_configs, 97):
+        e_idx = isd.unsatisfied_bonds(spec, x)
+        assert isd.oracle_energy(isd.decode_spins(spec, x), spec) == \
+            2 * e_idx - spec.num_bonds
+
+
+def test_crosscheck_caps_and_validation():
+    big = isd.LatticeSpec(5, 5)
+    with pytest.raises(ValueError, match="oracle cap of 24"):
+        isd.oracle_full_dos(big)
+    with pytest.raises(ValueError, match="oracle cap"):
+        isd.brute_force_log_z(big, 0.0, 1.0)
+    with pytest.raises(ValueError, match="temperature"):
+        isd.brute_force_log_z(isd.LatticeSpec(2, 2), 0.0, 0.0)
+    with pytest.raises(ValueError):
+        isd.decode_spins(isd.LatticeSpec(2, 2), 16)
+    assert isd.ORACLE_MAX_SPINS == 24
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["dos_2x2x1_J1.csv", "dos_3x3x1_J1.csv",
+                                  "dos_4x4x1_J1.csv", "dos_2x2x2_J1.csv"])
+def test_crosscheck_route_reproduces_reference_tables(name):
+    rows, cols, depth, j, table = read_csv_table(name)
+    spec = isd.LatticeSpec(rows, cols, depth, j)
+    got = isd.oracle_full_dos(spec)
+    assert np.array_equal(got.counts, table)
+    assert got == isd.full_dos(spec)
+
+
+@pytest.mark.gpu
+def test_brute_force_log_z_matches_partition_point():
+    for dims, kw in [((4, 4), {}), ((3, 4), dict(coupling=-1)),
+                     ((4, 4), dict(boundary="free"))]:
+        spec = isd.LatticeSpec(*dims, **kw)
+        dos = isd.full_dos(spec)
+        for h, t in ((0.0, 1.0), (0.3, 2.5), (-0.2, 4.0)):
+            bf = isd.brute_force_log_z(spec, h, t)
+            lz = isd.partition_point(dos, h, t).log_z
+            assert abs(bf - lz) <= 1e-12 * abs(lz)
+
+
+@pytest.mark.gpu
+def test_cli_oracle_check(capsys):
+    from paper_1110_2561_b200.cli import main
+    assert main(["oracle-check", "--rows", "3", "--cols", "4"]) == 0
+    assert "OK: bit-kernel and naive engines agree on all 4096" in \
+        capsys.readouterr().out
+    assert main(["oracle-check", "--rows", "5", "--cols", "5"]) == 1
+    assert "oracle cap" in capsys.readouterr().err
