@@ -179,6 +179,14 @@ typedef struct isd_plan_info {
   int32_t  pair_both;        /* mode 2: e change of flipping both sites
                                 beyond the sum of the single flips      */
   uint32_t base_words;       /* words of the unpaired layout            */
+  /* Banded tables (band_rows > 0, pairing mode 2 only): the table holds
+   * band_rows rows of m relative to a base row, and a launch is split into
+   * work items of run slots ordered by popcount, each item's runs spanning
+   * at most band_span + 5 + l + u - 2 rows — so a mode-2 table that could
+   * not hold all N + 1 rows fits shared memory.  Lanes are then single
+   * run sites (lane_vec[i] == pivot i). */
+  uint32_t band_rows;
+  uint32_t band_span;
   double   est_per_config;   /* est_wavefronts / configurations per RED */
 } isd_plan_info;
 

@@ -64,6 +64,7 @@ class PlanInfo(ctypes.Structure):
         ("pair_mode", ctypes.c_uint32), ("pair_degree", ctypes.c_int32 * 2),
         ("pair_words", ctypes.c_uint32 * 2), ("pair_both", ctypes.c_int32),
         ("base_words", ctypes.c_uint32),
+        ("band_rows", ctypes.c_uint32), ("band_span", ctypes.c_uint32),
         ("est_per_config", ctypes.c_double),
     ]
 

@@ -174,14 +174,101 @@ static int cached_plan(const isd_lattice* lat, uint64_t hint,
   return it->second.rc;
 }
 
+// ---- banded launches ------------------------------------------------------
+// A banded plan needs an aligned power-of-two run range: its work items
+// cover the free run bits in popcount order.
+static int log2_exact(uint64_t x) {
+  return (x && !(x & (x - 1))) ? 63 - __builtin_clzll(x) : -1;
+}
+
+static bool band_ok(const isd_plan_info& info, uint64_t start, uint64_t end) {
+  if (!info.band_rows) return false;
+  const uint64_t unit = 1ull << info.k;
+  if (start % unit || end % unit || end <= start) return false;
+  const int rb = log2_exact((end - start) >> info.k);
+  uint64_t span_bits = info.lane_mask;
+  for (int v = 0; v < 5; ++v) span_bits |= info.lane_vec[v];
+  return rb >= 6 && lane_span(span_bits) <= rb;
+}
+
+// Work items of a launch over 2^F slots (popcount order): ~n_target items of
+// equal size, cut so that each spans at most kBandSpan + 1 popcount classes.
+static std::vector<BandItem> build_band_items(int F, int n_target) {
+  std::vector<uint64_t> cum(F + 2, 0);  // cum[q] = slots of popcount < q
+  uint64_t c = 1;
+  for (int q = 0; q <= F; ++q) {
+    cum[q + 1] = cum[q] + c;
+    c = c * (uint64_t)(F - q) / (uint64_t)(q + 1);
+  }
+  const uint64_t total = cum[F + 1];
+  const uint64_t size = (total + n_target - 1) / n_target;
+  std::vector<BandItem> items;
+  uint64_t g = 0;
+  int q = 0;
+  while (g < total) {
+    while (cum[q + 1] <= g) ++q;
+    const int q_last = std::min(F, q + kBandSpan);
+    uint64_t g1 = std::min(g + (size ? size : 1), cum[q_last + 1]);
+    items.push_back(BandItem{g, g1, (unsigned)q, 0u});
+    g = g1;
+  }
+  return items;
+}
+
+static std::mutex g_items_mu;
+static std::map<std::string, std::pair<BandItem*, uint32_t>> g_items;
+
+// Device work items for 2^F slots (uploaded once per device and size).
+static int band_items(int F, int n_target, BandItem** ptr, uint32_t* count) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::string key = std::to_string(dev) + ":" + std::to_string(F) +
+                          ":" + std::to_string(n_target);
+  std::lock_guard<std::mutex> lock(g_items_mu);
+  auto it = g_items.find(key);
+  if (it == g_items.end()) {
+    const std::vector<BandItem> host = build_band_items(F, n_target);
+    BandItem* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, host.size() * sizeof(BandItem));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(d, host.data(), host.size() * sizeof(BandItem),
+                     cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "band work items");
+    it = g_items.emplace(key, std::make_pair(d, (uint32_t)host.size())).first;
+  }
+  *ptr = it->second.first;
+  *count = it->second.second;
+  return ISD_OK;
+}
+
+// Fill the banded-launch fields of hp for its run range [run_begin, run_end).
+static int set_band_launch(HoistParams* hp, int sms) {
+  hp->band_free_bits = 0;
+  hp->band_items = 0;
+  hp->band_n_items = 0;
+  if (!hp->band_rows) return ISD_OK;
+  const int rb = log2_exact(hp->run_end - hp->run_begin);
+  if (rb < 6) return fail(ISD_EINVAL, "banded launch needs 2^r runs");
+  BandItem* items = nullptr;
+  uint32_t count = 0;
+  const int rc = band_items(rb - 5, 2 * sms, &items, &count);
+  if (rc) return rc;
+  hp->band_free_bits = (uint32_t)(rb - 5);
+  hp->band_items = (uint64_t)(uintptr_t)items;
+  hp->band_n_items = count;
+  return ISD_OK;
+}
+
 static constexpr int kTuneCandidates = 40;
 static constexpr uint64_t kTuneConfigs = 1ull << 33;
 static constexpr size_t kTuneFinalists = 6;
 static constexpr uint64_t kTuneSliceConfigs = 1ull << 36;
 
 // Time the model's best layouts on `st` and keep the fastest.  Synchronous.
-static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
-                     uint64_t run1, int sms, cudaStream_t st,
+// Candidates may differ in loop width (banded plans use a shorter loop), so
+// each is timed on its own run range of [start, end).
+static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
+                     uint64_t end, int sms, cudaStream_t st,
                      isd_plan_info* info) {
   if (env_long("ISD_AUTOTUNE", 1) == 0) return;
   const std::string key = plan_key(lat, hint);
@@ -197,7 +284,8 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     const int n_cand = (int)env_long("ISD_TUNE_CANDIDATES", kTuneCandidates);
     for (size_t i = 0; i < pe.ranked.size() && (int)cands.size() < n_cand;
          ++i)
-      cands.push_back(pe.ranked[i]);
+      if (!pe.ranked[i].band_rows || band_ok(pe.ranked[i], start, end))
+        cands.push_back(pe.ranked[i]);
   }
   if (cands.size() < 2) return;
   const size_t bytes =
@@ -210,15 +298,22 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  // the sample: warps spread evenly over the body [run0, run1), each warp
-  // with the candidate's own lane placement, so every region of the index
-  // space votes and all candidates see the same spread
-  const uint64_t runs = kTuneConfigs >> cands[0].k;
-  const uint64_t body = run1 - run0;
-  // per-run ms of a candidate on the spread sample (< 0: not applicable)
+  // run range [r0, r1) of [start, end) for a loop width of k bits
+  auto run_range = [&](uint32_t k, uint64_t* r0, uint64_t* r1) {
+    *r0 = (start + ((1ull << k) - 1)) >> k;
+    *r1 = end >> k;
+  };
+  // Stage 1 (unbanded candidates): per-run ms on a sample of warps spread
+  // evenly over the body, each warp with the candidate's own lane
+  // placement, so every region of the index space votes and all
+  // candidates see the same spread (< 0: not applicable)
   auto time_spread = [&](const isd_plan_info& cand) -> float {
     HoistParams hp;
     fill_hoist(lat, &cand, &hp);
+    uint64_t run0, run1;
+    run_range(cand.k, &run0, &run1);
+    const uint64_t body = run1 > run0 ? run1 - run0 : 0;
+    const uint64_t runs = kTuneConfigs >> cand.k;
     uint64_t span_bits = hp.lane_mask;
     for (int v = 0; v < 5; ++v) span_bits |= hp.lane_vec[v];
     const uint64_t blk = 1ull << lane_span(span_bits);
@@ -242,10 +337,15 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     bump_launches(2);
-    return ms / (float)(warps * 32);
+    return ms / (float)(warps * 32) / (float)(1ull << cand.k);  // per config
   };
   std::vector<std::pair<float, size_t>> stage1;
+  std::vector<size_t> banded;
   for (size_t i = 0; i < cands.size(); ++i) {
+    if (cands[i].band_rows) {
+      banded.push_back(i);  // needs whole work items: straight to stage 2
+      continue;
+    }
     const float t = time_spread(cands[i]);
     if (t >= 0.f) stage1.push_back({t, i});
   }
@@ -257,8 +357,10 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   if (climb > 0 && !stage1.empty()) {
     isd_plan_info cur = cands[stage1[0].second];
     float cur_t = stage1[0].first;
+    uint64_t run0, run1;
+    run_range(cur.k, &run0, &run1);
     int run_bits = 0;
-    while (run_bits < 63 && (2ull << run_bits) <= body) ++run_bits;
+    while (run_bits < 63 && (2ull << run_bits) <= run1 - run0) ++run_bits;
     uint64_t seed = 0x6A09E667F3BCC909ull;
     for (long step = 0; step < climb; ++step) {
       isd_plan_info q = cur;
@@ -273,37 +375,51 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     stage1.insert(stage1.begin(), {cur_t, cands.size() - 1});
   }
   // stage 2: the best few, timed as a real walk — one contiguous slice of
-  // up to 2^36 configurations from the middle of the range (the spread
-  // sample ranks the candidates but not reliably enough to pick one), with
-  // the kernel the walk will use: the NVRTC build when it is available
-  // (its Gray-order loop changes the instruction mix), compiled once per
-  // finalist and cached for the walk
+  // up to 2^36 configurations (the spread sample ranks the candidates but
+  // not reliably enough to pick one), with the kernel the walk will use:
+  // the NVRTC build when it is available (its Gray-order loop changes the
+  // instruction mix), compiled once per finalist and cached for the walk.
+  // The model's best banded candidates join the finalists.
   const bool jit_ok = env_long("ISD_JIT", 1) != 0;
-  float best_ms = 1e30f;
-  size_t best = stage1.empty() ? 0 : stage1[0].second;
+  std::vector<size_t> finalists;
   const size_t n_final = (size_t)env_long("ISD_TUNE_FINALISTS", kTuneFinalists);
-  for (size_t s2 = 0; s2 < stage1.size() && s2 < n_final; ++s2) {
-    const size_t i = stage1[s2].second;
+  for (size_t s2 = 0; s2 < stage1.size() && s2 < n_final; ++s2)
+    finalists.push_back(stage1[s2].second);
+  for (size_t b = 0; b < banded.size() && b < 3; ++b)
+    finalists.push_back(banded[b]);
+  float best_ms = 1e30f;
+  size_t best = finalists.empty() ? 0 : finalists[0];
+  for (size_t i : finalists) {
     HoistParams hp;
     fill_hoist(lat, &cands[i], &hp);
+    uint64_t run0, run1;
+    run_range(cands[i].k, &run0, &run1);
+    const uint64_t body = run1 - run0;
     uint64_t span_bits = hp.lane_mask;
     for (int v = 0; v < 5; ++v) span_bits |= hp.lane_vec[v];
     const uint64_t blk = 1ull << lane_span(span_bits);
     uint64_t len = (kTuneSliceConfigs >> hp.k);
     if (len > body) len = body;
-    len = (len / blk) * blk;
+    uint64_t off;
+    if (hp.band_rows) {  // an aligned power-of-two slice: whole items
+      while (len & (len - 1)) len &= len - 1;
+      off = 0;
+    } else {
+      len = (len / blk) * blk;
+      off = ((body - len) / 2 / blk) * blk;
+    }
     if (len == 0) continue;
-    const uint64_t off = ((body - len) / 2 / blk) * blk;
     hp.run_begin = run0 + off;
     hp.run_end = hp.run_begin + len;
     hp.hi_step = 1;
+    if (set_band_launch(&hp, sms)) continue;
     float ms = 0.f;
     // (warm the finalist's kernel first: the JIT compile is not timed)
     int x = 0;
     if (jit_ok) {
       std::string why;
       HoistParams warm = hp;
-      warm.run_end = warm.run_begin + blk;
+      if (!warm.band_rows) warm.run_end = warm.run_begin + blk;
       x = launch_hoisted_jit(warm, scratch, sms, st, &why);
       if (x > 0) bump_launches(1);
     }
@@ -316,7 +432,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
     bump_launches(1);
-    ms /= (float)len;
+    ms /= (float)len * (float)(1ull << hp.k);  // per configuration
     if (ms < best_ms) {
       best_ms = ms;
       best = i;
@@ -330,6 +446,22 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t run0,
   PlanEntry& pe = g_plans[key];
   pe.info = cands[best];
   *info = pe.info;
+}
+
+// The best plan the model found without a banded table (banded plans need
+// an aligned power-of-two range).
+static bool unbanded_plan(const isd_lattice* lat, uint64_t hint,
+                          isd_plan_info* info) {
+  std::lock_guard<std::mutex> lock(g_plan_mu);
+  auto it = g_plans.find(plan_key(lat, hint));
+  if (it == g_plans.end()) return false;
+  const isd_plan_info* best = nullptr;
+  for (const isd_plan_info& x : it->second.ranked)
+    if (!x.band_rows && (!best || x.est_per_config < best->est_per_config))
+      best = &x;
+  if (!best) return false;
+  *info = *best;
+  return true;
 }
 
 // At most 2^38 configurations per launch: with >= 148 CTAs no CTA counts
@@ -427,6 +559,12 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     if (launches) *launches = nl;
     return rc;
   }
+  if (end - start >= kTuneConfigs)
+    autotune(lat, end - start, start, end, sms, st, &info);
+  // a banded plan runs only on an aligned power-of-two range
+  if (info.band_rows && !band_ok(info, start, end) &&
+      !unbanded_plan(lat, end - start, &info))
+    return fail(ISD_EINVAL, "no unbanded plan for an unaligned range");
   const uint32_t k = info.k;
   const uint64_t r0 = (start + ((1ull << k) - 1)) >> k;
   const uint64_t r1 = end >> k;
@@ -440,8 +578,6 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     rc = enqueue_canonical(lat, start, r0 << k, out, sms, st, true, &nl);
     if (rc) return rc;
   }
-  if (end - start >= kTuneConfigs)
-    autotune(lat, end - start, r0, r1, sms, st, &info);
   // experiment knob: ISD_LAYOUT="A,B,P,ls[,lanemask_hex]" forces the
   // histogram layout and lane placement (window at ls, or the mask)
   if (const char* lay = std::getenv("ISD_LAYOUT")) {
@@ -461,6 +597,7 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
       info.hist_words = lat->n_spins * a + lat->n_bonds * b + pw + 1;
       info.base_words = info.hist_words;
       info.pair_mode = 0;  // the knob describes an unpaired layout
+      info.band_rows = 0;
     }
   }
   HoistParams hp;
@@ -484,6 +621,8 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     if ((re - r) & ((1ull << lane_span(span_bits)) - 1))
       default_lanes(&hp.lane_mask, hp.lane_vec);
     hp.hi_step = 1;
+    rc = set_band_launch(&hp, sms);
+    if (rc) return rc;
     int x = 0;
     if (use_jit) {
       std::string why;

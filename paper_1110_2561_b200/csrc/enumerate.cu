@@ -154,6 +154,7 @@ struct RuntimeTraits {
   __device__ int32_t pair_deg(int i) const { return P.pair_deg[i]; }
   __device__ int32_t pair_both() const { return P.pair_both; }
   // no Gray sites in the ahead-of-time build (the stubs are never called)
+  __device__ uint32_t band_rows() const { return P.band_rows; }
   __host__ __device__ static constexpr int gray() { return 0; }
   __device__ uint32_t g_mask() const { return 0; }
   __device__ uint32_t g_bit(int) const { return 0; }
@@ -182,8 +183,10 @@ __global__ void __launch_bounds__(PAIR == 2 ? kWideThreads : kThreads)
   IsdLanes lanes;
 #pragma unroll
   for (int i = 0; i < 5; ++i) lanes.v[i] = P.lane_vec[i];
-  k1_hoisted_body<NC, DOUBLE, PAIR>(L, P.run_begin, P.run_end - P.run_begin,
-                              P.hi_step, P.lane_mask, lanes, hist, out);
+  k1_hoisted_body<NC, DOUBLE, PAIR>(
+      L, P.run_begin, P.run_end - P.run_begin, P.hi_step, P.lane_mask, lanes,
+      reinterpret_cast<const IsdBandItem*>(P.band_items), P.band_n_items,
+      (int)P.band_free_bits, hist, out);
 }
 
 // ---------------------------------------------------------------------------

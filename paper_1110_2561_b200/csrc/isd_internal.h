@@ -97,12 +97,31 @@ struct HoistParams {
   uint32_t g_nm1v[2], g_jn1v[2], g_nm2v[2], g_jn2v[2];
   int32_t g_deg[2], g_csum[2], g_odd[2];
   int32_t g_cdelta[2][kCopyBits];
+  // banded tables (isd_plan_info.band_rows): rows of the table, and for a
+  // launch its work items (device array of BandItem) and free run bits
+  uint32_t band_rows;
+  uint32_t band_free_bits;
+  uint32_t band_n_items;
+  uint32_t pad4_;
+  uint64_t band_items;
 };
 
 // Largest paired histogram (words): two CTAs of 512 threads per SM fit
 // 28 K words each; up to 56 K words runs one CTA per SM (mode 2 only).
 constexpr uint32_t kMaxPairWords = 28000;
 constexpr uint32_t kMaxPair2Words = 56000;
+// Banded mode-2 tables may use a block's whole shared memory (227 KB).
+constexpr uint32_t kMaxBandWords = 57600;
+// Work items of a banded launch span at most this many popcount classes
+// of their free run bits (+1: the rows of one item = kBandSpan + 5 lane
+// bits + l loop bits + (u - 2) copy bits + 1).
+constexpr int kBandSpan = 2;
+// one work item of a banded launch: slots [g0, g1) of the popcount-ordered
+// free run bits, whose popcounts are >= q0
+struct BandItem {
+  unsigned long long g0, g1;
+  unsigned int q0, pad;
+};
 
 // ---- host side -----------------------------------------------------------
 int validate_lattice(const isd_lattice* lat, char* err, size_t errlen);

@@ -143,6 +143,7 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
   o << "  __device__ __forceinline__ static constexpr int32_t pair_both() "
        "{ return "
     << P.pair_both << "; }\n";
+  c32("band_rows", P.band_rows);
   // Gray sites
   o << "  __host__ __device__ static constexpr int gray() { return " << P.gray
     << "; }\n";
@@ -171,13 +172,15 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
     << (P.pair == 2 ? kWideThreads : kThreads)
     << ") k1_jit(unsigned long long run_begin, unsigned long long nruns,\n"
        "    unsigned long long hi_step, unsigned long long lane_mask,\n"
-       "    const IsdLanes lanes,\n"
+       "    const IsdLanes lanes, const IsdBandItem* items,\n"
+       "    unsigned int n_items, int free_bits,\n"
        "    unsigned long long* __restrict__ out) {\n"
        "  extern __shared__ __align__(16) unsigned int hist[];\n"
        "  const JitTraits L;\n"
        "  k1_hoisted_body<"
     << nc << ", " << (dbl ? "true" : "false") << ", "
-    << P.pair << ">(L, run_begin, nruns, hi_step, lane_mask, lanes, hist, out);\n}\n";
+    << P.pair << ">(L, run_begin, nruns, hi_step, lane_mask, lanes, items,\n"
+       "      n_items, free_bits, hist, out);\n}\n";
   return o.str();
 }
 
@@ -201,6 +204,8 @@ static std::string jit_key(const HoistParams& P, int device) {
   q.hi_step = 0;
   q.lane_mask = 0;
   for (int i = 0; i < 5; ++i) q.lane_vec[i] = 0;
+  q.band_free_bits = q.band_n_items = 0;  // launch arguments, not constants
+  q.band_items = 0;
   std::string key(reinterpret_cast<const char*>(&q), sizeof q);
   key += std::to_string(device);
   return key;
@@ -304,7 +309,11 @@ int launch_hoisted_jit(const HoistParams& P, unsigned long long* out,
     unsigned long long v[5];
   } lanes;
   for (int i = 0; i < 5; ++i) lanes.v[i] = P.lane_vec[i];
-  void* args[] = {&run_begin, &nruns, &hi_step, &lane_mask, &lanes, &out};
+  const void* items = reinterpret_cast<const void*>(P.band_items);
+  unsigned int n_items = P.band_n_items;
+  int free_bits = (int)P.band_free_bits;
+  void* args[] = {&run_begin, &nruns, &hi_step, &lane_mask, &lanes,
+                  &items,     &n_items, &free_bits, &out};
   int grid = jk.grid;
   const uint64_t need = (nruns + jk.threads - 1) / jk.threads;
   if (need < (uint64_t)grid) grid = (int)(need ? need : 1);

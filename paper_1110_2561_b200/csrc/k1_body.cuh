@@ -31,6 +31,55 @@ __device__ __forceinline__ void isd_red_shared_inc(unsigned int addr) {
   asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory");
 }
 
+// A banded launch's work item (mirrors isd::BandItem): slots [g0, g1) of the
+// free run bits in popcount order, popcounts >= q0.
+struct IsdBandItem {
+  unsigned long long g0, g1;
+  unsigned int q0, pad;
+};
+
+// The g-th F-bit number in (popcount, value) order; *q = its popcount.
+__device__ __forceinline__ unsigned long long isd_unrank(unsigned long long g,
+                                                         int F, int* q) {
+  unsigned long long c = 1;  // C(F, q): size of popcount class q
+  int qq = 0;
+  while (g >= c && qq < F) {
+    g -= c;
+    c = c * (unsigned long long)(F - qq) / (unsigned long long)(qq + 1);
+    ++qq;
+  }
+  *q = qq;
+  // colex rank g among the F-bit numbers of popcount qq: the highest set
+  // bit is the largest b with C(b, qq) <= g, and so on down
+  unsigned long long cb = F ? c * (unsigned long long)(F - qq) / F : 0;
+  unsigned long long v = 0;
+  for (int bit = F - 1; bit >= 0 && qq > 0; --bit) {  // cb = C(bit, qq)
+    if (g >= cb) {
+      v |= 1ull << bit;
+      g -= cb;
+      cb = bit ? cb * (unsigned long long)qq / bit : 0;  // C(bit-1, qq-1)
+      --qq;
+    } else {
+      cb = bit ? cb * (unsigned long long)(bit - qq) / bit : 0;  // C(bit-1, qq)
+    }
+  }
+  return v;
+}
+
+// the next F-bit number in (popcount, value) order
+__device__ __forceinline__ unsigned long long isd_next_slot(
+    unsigned long long v, int F, int* q) {
+  if (v != 0) {
+    const unsigned long long low = v & (~v + 1);
+    const unsigned long long up = v + low;
+    const unsigned long long nv =
+        (((up ^ v) >> 2) >> (__ffsll((long long)low) - 1)) | up;
+    if (!(nv >> F)) return nv;  // same popcount
+  }
+  *q += 1;  // first (smallest) number of the next popcount class
+  return (1ull << *q) - 1;
+}
+
 // word of bin (m, e) in the unpaired layout
 template <class T>
 __device__ __forceinline__ unsigned int isd_bin_word(const T& L, unsigned int m,
@@ -48,20 +97,24 @@ __device__ __forceinline__ unsigned int isd_bin_word(const T& L, unsigned int m,
 // site's unsatisfied bonds while down), and the flush credits the partner
 // to (m + 1, e + D - 2p).  PAIR 2: copy bit 5 as well (4 configurations per
 // RED, planes p0 (bit 6) x p1 (bit 5)).
+//
+// Banded tables (L.band_rows() > 0, mode 2): the table holds band_rows rows
+// of m relative to a work item's base row; the launch walks work items
+// (slots of the free run bits in popcount order, `items`), each zeroed,
+// walked and flushed in turn.
 template <int NC, bool DOUBLE, int PAIR, class T>
 __device__ __forceinline__ void k1_hoisted_body(
     const T& L, unsigned long long run_begin, unsigned long long nruns,
     unsigned long long hi_step, unsigned long long lane_mask,
-    const IsdLanes lanes, unsigned int* hist,
+    const IsdLanes lanes, const IsdBandItem* __restrict__ items,
+    unsigned int n_items, int free_bits, unsigned int* hist,
     unsigned long long* __restrict__ out) {
-  // ---- zero the block's histograms ----
-  {
+  auto zero_hist = [&]() {
     uint4* h4 = reinterpret_cast<uint4*>(hist);
     const unsigned int n4 = L.n_hist() * L.hist_words() / 4;
     for (unsigned int i = threadIdx.x; i < n4; i += blockDim.x)
       h4[i] = make_uint4(0, 0, 0, 0);
-  }
-  __syncthreads();
+  };
   const unsigned int warp = threadIdx.x >> 5;
   const unsigned int hbase = (unsigned int)__cvta_generic_to_shared(
       hist + (warp % L.n_hist()) * L.hist_words());
@@ -78,26 +131,20 @@ __device__ __forceinline__ void k1_hoisted_body(
       if ((lane >> i) & 1) lane_dep ^= lanes.v[i];
   }
 
-  for (unsigned long long t =
-           (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-       t < nruns; t += gstride) {
-    // The 32 lanes of a warp differ by XORs of five run-bit vectors, each
-    // with its own pivot bit (lane_mask): which sites they differ in sets
-    // the shared-memory bank spread.  The warp's slot spreads over the
-    // non-pivot run bits, so (slot, lane) -> run is a bijection.  Warp w takes slot
-    // w * hi_step (1 in a walk; > 1 when the autotuner times a sample of
-    // warps spread over the whole range).
-    unsigned long long hi = (t >> 5) * hi_step;
-    {
-      unsigned long long m = lane_mask;
+  // slot (warp-uniform run bits) -> run: insert a 0 at each lane pivot,
+  // then XOR in the lane's pattern
+  auto slot_run = [&](unsigned long long hi) {
+    unsigned long long m = lane_mask;
 #pragma unroll
-      for (int i = 0; i < 5; ++i) {  // insert a 0 at each lane bit
-        const unsigned long long low = m & (~m + 1);
-        hi = ((hi & ~(low - 1)) << 1) | (hi & (low - 1));
-        m ^= low;
-      }
+    for (int i = 0; i < 5; ++i) {  // insert a 0 at each lane bit
+      const unsigned long long low = m & (~m + 1);
+      hi = ((hi & ~(low - 1)) << 1) | (hi & (low - 1));
+      m ^= low;
     }
-    const unsigned long long r = run_begin + (hi ^ lane_dep);
+    return run_begin + (hi ^ lane_dep);
+  };
+  // ---- one run: bits [k, N) fixed; table rows are m - row_off ----
+  auto run_body = [&](unsigned long long r, unsigned int row_off) {
     // ---- per-run constants (bits [k, N) fixed) ----
     const unsigned long long xt = r << L.k();
     const int m_run = __popcll(xt);
@@ -118,7 +165,8 @@ __device__ __forceinline__ void k1_hoisted_body(
     }
     // byte address of (m_run, e = 0); the e parity of the configurations
     // is par_run ^ parity(loop bits & odd_mask)
-    const unsigned int a_run = hbase + (unsigned int)m_run * L.row_bytes();
+    const unsigned int a_run =
+        hbase + (unsigned int)(m_run - (int)row_off) * L.row_bytes();
     const unsigned int par_run =
         (unsigned int)(__popcll(xt & L.odd_mask()) + L.e_parity()) & 1u;
     const unsigned int odd_loop =
@@ -226,52 +274,100 @@ __device__ __forceinline__ void k1_hoisted_body(
       }
       jb = ((jb & outer) - outer) & outer;  // next subset (Gray sites clear)
     }
-  }
-  __syncthreads();
-  // ---- flush: word (m, e) -> table bin (m, e) ----
-  for (unsigned int bin = threadIdx.x; bin < L.nbins(); bin += blockDim.x) {
-    const unsigned int m = bin / L.stride(), e = bin - m * L.stride();
-    // single parity plane: bins of the other parity are always 0 (and
-    // their words alias)
-    if (L.e_mode() && L.odd_mask() == 0 && (e & 1u) != L.e_parity()) continue;
-    const unsigned int word = isd_bin_word(L, m, e);
-    unsigned long long s = 0;
-    for (unsigned int h = 0; h < L.n_hist(); ++h) {
-      const unsigned int* hh = hist + h * L.hist_words();
-      if constexpr (PAIR == 0) {
-        s += hh[word];
-      } else if constexpr (PAIR == 1) {
-        const int D0 = L.pair_deg(0);
-        for (int p = 0; p <= D0; ++p) {
-          const unsigned int plane = p * L.pair_words(0);
-          // the paired site down: this bin
-          s += hh[word + plane];
-          // the paired site up: partner of (m - 1, e - D + 2p)
-          const int es = (int)e - D0 + 2 * p;
-          if (m > 0 && es >= 0 && es < (int)L.stride())
-            s += hh[isd_bin_word(L, m - 1, (unsigned int)es) + plane];
-        }
-      } else {
-        const int D0 = L.pair_deg(0), D1 = L.pair_deg(1);
-        for (int p1 = 0; p1 <= D1; ++p1)
-          for (int p0 = 0; p0 <= D0; ++p0) {
-            const unsigned int plane = p0 * L.pair_words(0) +
-                                       p1 * L.pair_words(1);
-            const int f0 = D0 - 2 * p0, f1 = D1 - 2 * p1;
-            s += hh[word + plane];  // both paired sites down
-            if (m == 0) continue;
-            const int e0 = (int)e - f0, e1 = (int)e - f1;
-            if (e0 >= 0 && e0 < (int)L.stride())  // bit-6 site up
-              s += hh[isd_bin_word(L, m - 1, (unsigned int)e0) + plane];
-            if (e1 >= 0 && e1 < (int)L.stride())  // bit-5 site up
-              s += hh[isd_bin_word(L, m - 1, (unsigned int)e1) + plane];
-            const int e2 = (int)e - f0 - f1 - L.pair_both();
-            if (m >= 2 && e2 >= 0 && e2 < (int)L.stride())  // both up
-              s += hh[isd_bin_word(L, m - 2, (unsigned int)e2) + plane];
+  };
+  // ---- flush: table rows [0, rows) at absolute row row_off -> bins ----
+  auto flush = [&](unsigned int row_off, unsigned int rows) {
+    const unsigned int m_lo = row_off;
+    unsigned int m_hi = row_off + rows + (PAIR > 0 ? PAIR : 0);  // exclusive
+    if (m_hi > L.nbins() / L.stride()) m_hi = L.nbins() / L.stride();
+    const unsigned int b_lo = m_lo * L.stride(), b_hi = m_hi * L.stride();
+    for (unsigned int bin = b_lo + threadIdx.x; bin < b_hi; bin += blockDim.x) {
+      const unsigned int m = bin / L.stride(), e = bin - m * L.stride();
+      // single parity plane: bins of the other parity are always 0 (and
+      // their words alias)
+      if (L.e_mode() && L.odd_mask() == 0 && (e & 1u) != L.e_parity()) continue;
+      const int row = (int)(m - row_off);  // table row of this bin
+      unsigned long long s = 0;
+      for (unsigned int h = 0; h < L.n_hist(); ++h) {
+        const unsigned int* hh = hist + h * L.hist_words();
+        // (row r, energy e) of the table, if it exists
+        auto at = [&](int r, int ee, unsigned int plane) -> unsigned int {
+          if (r < 0 || r >= (int)rows || ee < 0 || ee >= (int)L.stride())
+            return 0u;
+          return hh[isd_bin_word(L, (unsigned int)r, (unsigned int)ee) + plane];
+        };
+        if constexpr (PAIR == 0) {
+          s += at(row, (int)e, 0);
+        } else if constexpr (PAIR == 1) {
+          const int D0 = L.pair_deg(0);
+          for (int p = 0; p <= D0; ++p) {
+            const unsigned int plane = p * L.pair_words(0);
+            s += at(row, (int)e, plane);                   // paired site down
+            s += at(row - 1, (int)e - D0 + 2 * p, plane);  // ... up: partner
           }
+        } else {
+          const int D0 = L.pair_deg(0), D1 = L.pair_deg(1);
+          for (int p1 = 0; p1 <= D1; ++p1)
+            for (int p0 = 0; p0 <= D0; ++p0) {
+              const unsigned int plane = p0 * L.pair_words(0) +
+                                         p1 * L.pair_words(1);
+              const int f0 = D0 - 2 * p0, f1 = D1 - 2 * p1;
+              s += at(row, (int)e, plane);           // both paired sites down
+              s += at(row - 1, (int)e - f0, plane);  // bit-6 site up
+              s += at(row - 1, (int)e - f1, plane);  // bit-5 site up
+              s += at(row - 2, (int)e - f0 - f1 - L.pair_both(), plane);
+            }
+        }
       }
+      if (s) atomicAdd(out + bin, s);
     }
-    if (s) atomicAdd(out + bin, s);
+  };
+
+  if (L.band_rows() == 0) {
+    // ---- grid-stride walk over the runs; one table for all rows ----
+    zero_hist();
+    __syncthreads();
+    for (unsigned long long t =
+             (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+         t < nruns; t += gstride) {
+      // The 32 lanes of a warp differ by XORs of five run-bit vectors, each
+      // with its own pivot bit (lane_mask): which sites they differ in sets
+      // the shared-memory bank spread.  The warp's slot spreads over the
+      // non-pivot run bits, so (slot, lane) -> run is a bijection.  Warp w
+      // takes slot w * hi_step (1 in a walk; > 1 when the autotuner times a
+      // sample of warps spread over the whole range).
+      run_body(slot_run((t >> 5) * hi_step), 0u);
+    }
+    __syncthreads();
+    flush(0u, L.nbins() / L.stride());
+  } else {
+    // ---- banded: work items of slots in popcount order ----
+    const unsigned int warps = blockDim.x >> 5;
+    const unsigned int base_popc =
+        (unsigned int)__popcll(run_begin << L.k());
+    for (unsigned int it = blockIdx.x; it < n_items; it += gridDim.x) {
+      const IsdBandItem item = items[it];
+      zero_hist();
+      __syncthreads();
+      const unsigned int row_off = base_popc + item.q0;
+      // this warp's contiguous share of the item's slots
+      const unsigned long long n_slots = item.g1 - item.g0;
+      const unsigned long long per = (n_slots + warps - 1) / warps;
+      unsigned long long g = item.g0 + (unsigned long long)warp * per;
+      unsigned long long g_end = g + per;
+      if (g_end > item.g1) g_end = item.g1;
+      if (g < g_end) {
+        int q = 0;
+        unsigned long long v = isd_unrank(g, free_bits, &q);
+        for (; g < g_end; ++g) {
+          run_body(slot_run(v), row_off);
+          v = isd_next_slot(v, free_bits, &q);
+        }
+      }
+      __syncthreads();
+      flush(row_off, L.band_rows());
+      __syncthreads();
+    }
   }
 }
 

@@ -197,7 +197,8 @@ bool mutate_lanes(const isd_lattice* lat, int run_bits, uint64_t* seed,
 // then differ by pairs of neighbours, which keeps their (m, e) bins closer
 // together: fewer distinct words per RED, fewer bank conflicts).
 static void lane_candidates(const isd_lattice* lat, const isd_plan_info* info,
-                            int run_bits, bool wide, std::vector<Lanes>* out) {
+                            int run_bits, bool wide, bool single_site,
+                            std::vector<Lanes>* out) {
   static const int shifts[] = {0, 3, 6, 9, 12, 15};
   for (int ls : shifts)
     if (run_bits >= ls + 5) out->push_back(lanes_from_mask(0x1Full << ls));
@@ -225,6 +226,7 @@ static void lane_candidates(const isd_lattice* lat, const isd_plan_info* info,
       if (!seen(L.mask, L.vec)) out->push_back(L);
     }
   }
+  if (single_site) return;  // banded tables: lanes flip single sites only
   const std::vector<std::vector<int>> nbr = run_neighbors(lat, k, run_bits);
   for (int r = 0; r < 32; ++r) {
     Lanes L = lanes_from_mask(0);
@@ -286,8 +288,10 @@ static int pair_policy() {
 
 static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
                           std::vector<isd_plan_info>* ranked, bool wide,
-                          int walk_bits, bool climb) {
-  const int n = (int)lat->n_spins;
+                          int walk_bits, bool climb, int band_rows = 0) {
+  // table rows: all N + 1 values of m, or a band of them
+  const int n = band_rows ? band_rows - 1 : (int)lat->n_spins;
+  const int n_spins = (int)lat->n_spins;
   const int k = (int)info->k;
   const int b = (int)lat->n_bonds;
   const int emax_half = b / 2;  // largest (e - par)/2
@@ -295,6 +299,8 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   info->est_wavefronts = 0;
   info->est_per_config = 0;
   info->pair_mode = 0;
+  info->band_rows = (uint32_t)band_rows;
+  info->band_span = band_rows ? (uint32_t)kBandSpan : 0;
   // paired sites: copy bit 6 (index 0) and, for mode 2, copy bit 5
   const int psite[2] = {info->copy_site[kCopyBits - 1],
                         info->copy_site[kCopyBits - 2]};
@@ -352,10 +358,21 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
         const int end0 = c.span + pdeg[0] * c.s0;
         c.s1 = ((end0 + 31) & ~31) + (r * (pdeg[0] + 1)) % 32;
         c.total = end0 + pdeg[1] * c.s1;
-        if (c.total <= (int)kMaxPair2Words) cand.push_back(c);
+        if (c.total <= (int)(band_rows ? kMaxBandWords : kMaxPair2Words))
+          cand.push_back(c);
       }
     }
-    if (policy >= 0) {
+    if (band_rows) {  // banded tables exist for mode 2 only
+      std::vector<Cand> keep;
+      for (const Cand& c : cand)
+        if (c.pair == 2) keep.push_back(c);
+      cand.swap(keep);
+      if (cand.empty()) {
+        info->est_per_config = 1e30;
+        return;
+      }
+    }
+    if (policy >= 0 && !band_rows) {
       std::vector<Cand> keep;
       for (const Cand& c : cand)
         if (c.pair == policy) keep.push_back(c);
@@ -377,13 +394,13 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   apply(info, cand[0]);
   // run bits a walk of 2^walk_bits configurations actually varies (a shard
   // fixes the top ones): lane patterns must stay inside them to tile it
-  const int run_bits = std::min(n, walk_bits) - k;
+  const int run_bits = std::min(n_spins, walk_bits) - k;
   if (run_bits < 5) {
     if (ranked) ranked->push_back(*info);
     return;
   }
   std::vector<Lanes> masks;
-  lane_candidates(lat, info, run_bits, wide, &masks);
+  lane_candidates(lat, info, run_bits, wide, band_rows > 0, &masks);
 
   // Score one lane mask against every layout on `warps` sampled warp
   // instructions x kCopySample copies; returns its best cost per
@@ -536,7 +553,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
         uint64_t partners = 0;
         for (int v = 0; v < 5; ++v) partners |= q.vec[v] & ~q.mask;
         const int piv = __builtin_ctzll(q.vec[i] & q.mask);
-        if (rng_next(&seed) & 1) {  // re-pivot (drops the partner)
+        if (band_rows || (rng_next(&seed) & 1)) {  // re-pivot (drops the partner)
           const int nb = (int)(rng_next(&seed) % run_bits);
           if (((q.mask | partners) >> nb) & 1) continue;
           q.mask = (q.mask & ~(1ull << piv)) | (1ull << nb);
@@ -699,28 +716,28 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
     }
     return false;
   };
-  std::vector<std::vector<int>> sets;
-  std::vector<const char*> names;
-  {
+  // copy-site sets of the low kk bits
+  auto build_sets = [&](int kk, std::vector<std::vector<int>>* sets,
+                        std::vector<const char*>* names) {
     std::vector<int> even;
-    for (int i = 0; i < k && (int)even.size() < u; ++i)
+    for (int i = 0; i < kk && (int)even.size() < u; ++i)
       if (!((odd >> i) & 1)) even.push_back(i);
     if ((int)even.size() == u) {
-      sets.push_back(even);
-      names.push_back("even");
+      sets->push_back(even);
+      names->push_back("even");
     }
     std::vector<int> low;
     for (int t = 0; t < u; ++t) low.push_back(t);
     const char* forced = std::getenv("ISD_COPY_VARIANT");
     const bool force_low = forced && std::strcmp(forced, "low") == 0;
-    if (sets.empty() || low != sets[0] || force_low) {
-      sets.push_back(low);
-      names.push_back("low");
+    if (sets->empty() || low != (*sets)[0] || force_low) {
+      sets->push_back(low);
+      names->push_back("low");
     }
     if (n_configs_hint >= (1ull << 33)) {
       std::vector<int> spread;
       for (int pass = 0; pass < 3 && (int)spread.size() < u; ++pass)
-        for (int i = 0; i < k && (int)spread.size() < u; ++i) {
+        for (int i = 0; i < kk && (int)spread.size() < u; ++i) {
           if (std::find(spread.begin(), spread.end(), i) != spread.end())
             continue;
           const bool even_ok = !((odd >> i) & 1) || pass == 2;
@@ -730,13 +747,21 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
         }
       std::sort(spread.begin(), spread.end());
       bool dup = false;
-      for (const auto& st : sets) dup = dup || st == spread;
+      for (const auto& st : *sets) dup = dup || st == spread;
       if (!dup) {
-        sets.push_back(spread);
-        names.push_back("spread");
+        sets->push_back(spread);
+        names->push_back("spread");
       }
     }
-  }
+    // the paired slots (6, then 5) take the set's lowest-degree sites:
+    // fewer pattern planes
+    for (auto& st : *sets)
+      std::stable_sort(st.begin(), st.end(),
+                       [&](int x, int y) { return deg[x] > deg[y]; });
+  };
+  std::vector<std::vector<int>> sets;
+  std::vector<const char*> names;
+  build_sets(k, &sets, &names);
   isd_plan_info best_info;
   bool have = false;
   std::vector<isd_plan_info> all;
@@ -744,29 +769,54 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   while (walk_bits < 63 && (1ull << (walk_bits + 1)) <= n_configs_hint)
     ++walk_bits;
   const bool wide = n_configs_hint >= (1ull << 33);
-  // the paired slots (6, then 5) take the set's lowest-degree sites: fewer
-  // pattern planes
-  for (auto& st : sets)
-    std::stable_sort(st.begin(), st.end(),
-                     [&](int x, int y) { return deg[x] > deg[y]; });
-  auto try_variant = [&](size_t v, bool climb) {
-    isd_plan_info cand = *info;
+  auto try_variant = [&](const isd_plan_info& base, const std::vector<int>& set,
+                         bool climb, int band_rows) {
+    isd_plan_info cand = base;
     bool all_even = true;
-    for (int site : sets[v]) all_even = all_even && !((odd >> site) & 1);
-    set_copy_sites(lat, &cand, sets[v].data(), all_even ? 1 : 0);
-    choose_layout(lat, &cand, &all, wide, walk_bits, climb);
+    for (int site : set) all_even = all_even && !((odd >> site) & 1);
+    set_copy_sites(lat, &cand, set.data(), all_even ? 1 : 0);
+    choose_layout(lat, &cand, &all, wide, walk_bits, climb, band_rows);
+    if (cand.est_per_config >= 1e29) return;  // no layout of that kind
     if (!have || cand.est_per_config < best_info.est_per_config - 1e-9) {
       best_info = cand;
       have = true;
     }
   };
-  // test / tuning knob: ISD_COPY_VARIANT=even|low|spread forces one set
-  const char* force = std::getenv("ISD_COPY_VARIANT");
   // (large walks also hill-climb each set's lane patterns; the model's
   // estimates are only good to a few percent, so every set keeps its best
   // climbed candidates in the list the GPU autotuner times)
-  for (size_t v = 0; v < sets.size(); ++v)
-    if (!force || std::strcmp(force, names[v]) == 0) try_variant(v, wide);
+  // test / tuning knob: ISD_COPY_VARIANT=even|low|spread forces one set
+  const char* force = std::getenv("ISD_COPY_VARIANT");
+  const long band_knob = env_int("ISD_BAND", -1);  // 0 never, 1 always
+  if (band_knob != 1)
+    for (size_t v = 0; v < sets.size(); ++v)
+      if (!force || std::strcmp(force, names[v]) == 0)
+        try_variant(*info, sets[v], wide, 0);
+  // Banded mode 2: when no unbanded mode-2 table fits (c5: 49 planes of all
+  // 37 rows), a power-of-two walk can still run mode 2 with a table of
+  // band_rows rows per work item; a shorter loop (l = 5) keeps the band
+  // narrow.  Requires an aligned power-of-two range (checked at launch).
+  const int policy = pair_policy();
+  const bool pow2 = n_configs_hint && !(n_configs_hint & (n_configs_hint - 1));
+  if (band_knob != 0 && pow2 && (policy < 0 || policy == 2) &&
+      (band_knob == 1 || (wide && (!have || best_info.pair_mode < 2)))) {
+    const int lb = (int)std::min<long>(env_int("ISD_BAND_LOOP_BITS", 5), l);
+    const int kb = u + lb;
+    const int rows = kBandSpan + 5 + lb + (u - 2) + 1;
+    if (walk_bits - kb - 5 >= 1 && kb <= 32 && rows <= n + 1) {
+      isd_plan_info base = *info;
+      base.l = (uint32_t)lb;
+      base.k = (uint32_t)kb;
+      base.run_mask_above_k = (n >= 64 ? ~0ull : ((1ull << n) - 1)) &
+                              ~((1ull << kb) - 1);
+      std::vector<std::vector<int>> bsets;
+      std::vector<const char*> bnames;
+      build_sets(kb, &bsets, &bnames);
+      for (size_t v = 0; v < bsets.size(); ++v)
+        if (!force || std::strcmp(force, bnames[v]) == 0)
+          try_variant(base, bsets[v], wide, rows);
+    }
+  }
   if (!have) return 1;  // forced variant not available for this lattice
   *info = best_info;
   if (ranked) {
@@ -777,10 +827,14 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
                      [](const isd_plan_info& a, const isd_plan_info& b) {
                        return a.est_per_config < b.est_per_config;
                      });
-    std::vector<isd_plan_info> by_mode[3], mixed;
-    for (const isd_plan_info& x : all) by_mode[x.pair_mode % 3].push_back(x);
-    for (size_t i = 0; mixed.size() < all.size(); ++i)
-      for (int mode : {2, 1, 0})
+    std::vector<isd_plan_info> by_mode[4], mixed;
+    for (const isd_plan_info& x : all)
+      if (x.est_per_config < 1e29)
+        by_mode[x.band_rows ? 3 : x.pair_mode % 3].push_back(x);
+    size_t total = 0;
+    for (const auto& g : by_mode) total += g.size();
+    for (size_t i = 0; mixed.size() < total; ++i)
+      for (int mode : {3, 2, 1, 0})
         if (i < by_mode[mode].size()) mixed.push_back(by_mode[mode][i]);
     if (mixed.size() > 256) mixed.resize(256);
     ranked->assign(mixed.begin(), mixed.end());
@@ -862,6 +916,7 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
   };
   for (int c = 0; c < kCopies; ++c)
     p->koff[c] = __builtin_popcount((unsigned)c) * rb + eb * unsat_cc(c);
+  p->band_rows = info->band_rows;
   p->pair = info->pair_mode;
   p->pair_both = info->pair_both;
   for (int i = 0; i < 2; ++i) {

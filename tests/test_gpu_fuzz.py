@@ -102,3 +102,23 @@ def test_jit_gray_walk_matches_c_oracle(spec, pair, gray, monkeypatch):
 def _native_kernel_path():
     from paper_1110_2561_b200 import _native
     return _native.kernel_info()
+
+
+# Banded mode-2 tables (c5's layout: rows of m relative to each work
+# item's base, work items of run slots in popcount order): forced on small
+# lattices through both kernel builds, against the C oracle.
+@pytest.mark.parametrize("jit", ["0", "2"])
+@pytest.mark.parametrize("loop_bits", ["1", "3"])
+@pytest.mark.parametrize("spec", JIT_SPECS, ids=repr)
+def test_banded_walk_matches_c_oracle(spec, loop_bits, jit, monkeypatch):
+    from paper_1110_2561_b200 import _native
+    from paper_1110_2561_b200.enumeration import native_lattice
+    monkeypatch.setenv("ISD_BAND", "1")
+    monkeypatch.setenv("ISD_BAND_LOOP_BITS", loop_bits)
+    monkeypatch.setenv("ISD_JIT", jit)
+    monkeypatch.setenv("ISD_LOOP_BITS", loop_bits)
+    _, info = _native.plan(native_lattice(spec), spec.num_configs)
+    if not info.band_rows or spec.num_spins - info.k < 6:
+        pytest.skip("no banded plan for this lattice")
+    got = isd.full_dos(spec)
+    assert np.array_equal(got.counts, oracle_table(spec))

@@ -179,7 +179,32 @@ def _u(x):
     return np.uint64(x)
 
 
-def replay_hoisted(spec, loop_bits, pair=None):
+def _band_items(F, n_target, span=2):
+    """The host's work-item split of 2^F slots (capi.cu build_band_items)."""
+    from math import comb
+    cum = [0]
+    for q in range(F + 1):
+        cum.append(cum[-1] + comb(F, q))
+    total = cum[-1]
+    size = max(1, -(-total // n_target))
+    items, g, q = [], 0, 0
+    while g < total:
+        while cum[q + 1] <= g:
+            q += 1
+        g1 = min(g + size, cum[min(F, q + span) + 1])
+        items.append((g, g1, q))
+        g = g1
+    return items, cum
+
+
+def _slot_rank(v, F, cum):
+    """Index of F-bit v in (popcount, value) order."""
+    from math import comb
+    bits = [b for b in range(F) if (v >> b) & 1]
+    return cum[len(bits)] + sum(comb(b, i + 1) for i, b in enumerate(bits))
+
+
+def replay_hoisted(spec, loop_bits, pair=None, band_items=None):
     """numpy replay of k1_hoisted's arithmetic and address layout.
 
     Every index is decomposed exactly as the kernel does (run / loop /
@@ -191,12 +216,18 @@ def replay_hoisted(spec, loop_bits, pair=None):
     os.environ["ISD_LOOP_BITS"] = str(loop_bits)
     if pair is not None:
         os.environ["ISD_PAIR"] = str(pair)
+    if band_items is not None:  # force a banded mode-2 plan
+        os.environ.update(ISD_BAND="1", ISD_PAIR="2",
+                          ISD_BAND_LOOP_BITS=str(loop_bits))
     try:
         lat = native_lattice(spec)
         usable, info = _native.plan(lat, spec.num_configs)
     finally:
-        del os.environ["ISD_LOOP_BITS"]
-        os.environ.pop("ISD_PAIR", None)
+        for key in ("ISD_LOOP_BITS", "ISD_PAIR", "ISD_BAND",
+                    "ISD_BAND_LOOP_BITS"):
+            os.environ.pop(key, None)
+    if band_items is not None and not info.band_rows:
+        return None  # no banded layout for this lattice
     assert usable
     if pair is not None:
         assert info.pair_mode == pair
@@ -237,8 +268,8 @@ def replay_hoisted(spec, loop_bits, pair=None):
     kt = np.array(list(info.copy_table), dtype=np.int64)
     e += kt[c] - stride * np.bitwise_count(c.astype(np.uint64)).astype(np.int64)
     A, B, P = info.row_words, info.e_words, info.plane_words
+    odd = int(info.odd_mask)
     if info.e_mode:
-        odd = int(info.odd_mask)
         par = (pc(x & _u(odd & ~copies)) + info.e_parity) & 1
         assert np.all((e - par) % 2 == 0), "e parity formula"
         word = m * A + ((e - par) // 2) * B + par * P
@@ -259,8 +290,33 @@ def replay_hoisted(spec, loop_bits, pair=None):
         word = word + pat * info.pair_words[i]
         key = key * (info.pair_degree[i] + 1) + pat
         assert pat[down].min() >= 0 and pat[down].max() <= info.pair_degree[i]
+    if info.band_rows:
+        # banded: each run's slot (its non-pivot run bits) falls in a work
+        # item whose base row q0 the table rows are relative to
+        run = (x >> _u(k)).astype(np.int64)
+        rb = n - k
+        pivots = int(info.lane_mask)
+        assert all((int(v) & pivots) == int(v) for v in info.lane_vec)
+        free = [b for b in range(rb) if not (pivots >> b) & 1]
+        F = len(free)
+        items, cum = _band_items(F, band_items)
+        starts = np.array([it[0] for it in items], dtype=np.int64)
+        vals = np.zeros(run.shape, dtype=np.int64)
+        for j, b in enumerate(free):
+            vals |= ((run >> b) & 1) << j
+        uniq, inv = np.unique(vals, return_inverse=True)
+        gidx = np.array([_slot_rank(int(v), F, cum) for v in uniq])[inv]
+        item_of = np.searchsorted(starts, gidx, side="right") - 1
+        q0 = np.array([it[2] for it in items], dtype=np.int64)[item_of]
+        row = m - q0
+        assert row.min() >= 0 and row[down].max() < info.band_rows
+        word = word - q0 * A
+        key = key + 0
     word, key = word[down], key[down]
     assert word.max() < info.hist_words
+    if info.band_rows:
+        return _banded_table(info, spec, word, key, item_of[down],
+                             q0[down], len(items), odd, A, B, P)
     # injective on occurring bins
     pairs = np.unique(np.stack([word, key]), axis=1)
     assert len(np.unique(pairs[0])) == pairs.shape[1], "layout collision"
@@ -297,6 +353,47 @@ def replay_hoisted(spec, loop_bits, pair=None):
     return table
 
 
+def _banded_table(info, spec, word, key, item, q0, n_items, odd, A, B, P):
+    """Per-item tables and the kernel's banded mode-2 flush rule."""
+    n, stride = spec.num_spins, info.stride
+    D, S = list(info.pair_degree), list(info.pair_words)
+    R = info.band_rows
+
+    def bin_word(rr, ee):
+        if info.e_mode:
+            p2 = ee & 1
+            return rr * A + ((ee - p2) // 2) * B + p2 * P
+        return rr * A + ee * B
+
+    table = np.zeros((n + 1, stride), dtype=np.int64)
+    for it in range(n_items):
+        sel = item == it
+        if not sel.any():
+            continue
+        w, kk = word[sel], key[sel]
+        pairs = np.unique(np.stack([w, kk]), axis=1)
+        assert len(np.unique(pairs[0])) == pairs.shape[1], "layout collision"
+        hist = np.bincount(w, minlength=int(info.hist_words))
+        base = int(q0[sel][0])
+        assert (q0[sel] == base).all()
+        for mm in range(base, min(n, base + R + 1) + 1):
+            for ee in range(stride):
+                if info.e_mode and odd == 0 and (ee & 1) != info.e_parity:
+                    continue
+                tot = 0
+                for p1 in range(D[1] + 1):
+                    for p0 in range(D[0] + 1):
+                        plane = p0 * S[0] + p1 * S[1]
+                        f0, f1 = D[0] - 2 * p0, D[1] - 2 * p1
+                        for dr, de in ((0, 0), (1, f0), (1, f1),
+                                       (2, f0 + f1 + info.pair_both)):
+                            rr, se = mm - base - dr, ee - de
+                            if 0 <= rr < R and 0 <= se < stride:
+                                tot += hist[bin_word(rr, se) + plane]
+                table[mm, ee] += tot
+    return table
+
+
 REPLAY = [
     dict(rows=4, cols=4), dict(rows=3, cols=4, coupling=-1),
     dict(rows=2, cols=2, depth=3), dict(rows=4, cols=4, boundary="free"),
@@ -319,6 +416,25 @@ def test_hoisted_plan_replay_matches_oracle(kw, seed, loop_bits, pair):
     want = port.enumerate_range(lat, 0, 1 << lat.n)
     got = replay_hoisted(spec, loop_bits, pair)
     assert np.array_equal(got, want)
+
+
+BAND_REPLAY = [dict(rows=4, cols=4), dict(rows=2, cols=3, depth=3),
+               dict(rows=5, cols=4), dict(rows=4, cols=5, boundary="free"),
+               dict(rows=3, cols=3, depth=2)]
+
+
+@pytest.mark.parametrize("kw", BAND_REPLAY)
+@pytest.mark.parametrize("seed", [None, 11])
+@pytest.mark.parametrize("n_items", [3, 17])
+def test_banded_plan_replay_matches_oracle(kw, seed, n_items):
+    # banded mode 2: per-item tables of band_rows rows, the kernel's slot
+    # order and item split replayed, flushed per item, against the oracle
+    spec, (r, c, d, j, per, signs) = _spec_and_oracle(kw, seed)
+    got = replay_hoisted(spec, 1, band_items=n_items)
+    if got is None:
+        pytest.skip("no banded layout")
+    lat = port.Lattice(r, c, d, j, per, signs)
+    assert np.array_equal(got, port.enumerate_range(lat, 0, 1 << lat.n))
 
 
 def test_plan_copy_site_variants(monkeypatch):

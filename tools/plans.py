@@ -7,4 +7,4 @@ from paper_1110_2561_b200.enumeration import native_lattice
 for k,w in workloads().items():
     t=time.time()
     ok,p=_native.plan(native_lattice(w.spec), w.spec.num_configs)
-    print(k, ok, f"{time.time()-t:.2f}s", {f:getattr(p,f) for f in ('l','e_mode','row_words','e_words','plane_words','hist_words','base_words','pair_mode','pair_both')}, list(p.pair_degree), list(p.pair_words), f"est={p.est_wavefronts:.3f} per_cfg={p.est_per_config:.3f}", list(p.copy_site))
+    print(k, ok, f"{time.time()-t:.2f}s", {f:getattr(p,f) for f in ('l','e_mode','row_words','e_words','plane_words','hist_words','base_words','pair_mode','pair_both','band_rows')}, list(p.pair_degree), list(p.pair_words), f"est={p.est_wavefronts:.3f} per_cfg={p.est_per_config:.3f}", list(p.copy_site))
