@@ -227,7 +227,13 @@ static int band_items(int F, int n_target, BandItem** ptr, uint32_t* count) {
   std::lock_guard<std::mutex> lock(g_items_mu);
   auto it = g_items.find(key);
   if (it == g_items.end()) {
-    const std::vector<BandItem> host = build_band_items(F, n_target);
+    // the class-boundary cuts add a few small items: shrink the target so
+    // the count stays a whole number of waves (blocks get equal work)
+    std::vector<BandItem> host = build_band_items(F, n_target);
+    for (int goal = n_target; (int)host.size() > n_target && goal > 1;) {
+      goal -= (int)host.size() - n_target;
+      host = build_band_items(F, goal < 1 ? 1 : goal);
+    }
     BandItem* d = nullptr;
     cudaError_t e = cudaMalloc(&d, host.size() * sizeof(BandItem));
     if (e == cudaSuccess)
@@ -251,7 +257,13 @@ static int set_band_launch(HoistParams* hp, int sms) {
   if (rb < 6) return fail(ISD_EINVAL, "banded launch needs 2^r runs");
   BandItem* items = nullptr;
   uint32_t count = 0;
-  const int rc = band_items(rb - 5, 2 * sms, &items, &count);
+  // two items per block once an item has >= 1024 slots (more blocks
+  // finish together), else one (each item costs a flush of the table)
+  const int F = rb - 5;
+  const int per_sm = (int)env_long(
+      "ISD_BAND_ITEMS_PER_SM", ((1ull << F) / (2ull * sms) >= 1024) ? 2 : 1);
+  const int rc = band_items(F, (per_sm < 1 ? 1 : per_sm) * sms, &items,
+                            &count);
   if (rc) return rc;
   hp->band_free_bits = (uint32_t)(rb - 5);
   hp->band_items = (uint64_t)(uintptr_t)items;
