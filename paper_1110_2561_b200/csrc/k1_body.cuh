@@ -287,35 +287,52 @@ __device__ __forceinline__ void k1_hoisted_body(
       // their words alias)
       if (L.e_mode() && L.odd_mask() == 0 && (e & 1u) != L.e_parity()) continue;
       const int row = (int)(m - row_off);  // table row of this bin
+      // words are linear in the row and, for the even shifts the pairing
+      // makes, in e: word(r - dr, e - de) = word(r, e) - dr A - de_words(de)
+      const int gw = (int)isd_bin_word(L, 0u, e);
+      auto de_words = [&](int de) {
+        return L.e_mode() ? (de >> 1) * (int)L.e_words() : de * (int)L.e_words();
+      };
+      auto row_ok = [&](int r) { return r >= 0 && r < (int)rows; };
+      auto e_ok = [&](int ee) { return ee >= 0 && ee < (int)L.stride(); };
+      const int A = (int)L.row_words();
       unsigned long long s = 0;
       for (unsigned int h = 0; h < L.n_hist(); ++h) {
         const unsigned int* hh = hist + h * L.hist_words();
-        // (row r, energy e) of the table, if it exists
-        auto at = [&](int r, int ee, unsigned int plane) -> unsigned int {
-          if (r < 0 || r >= (int)rows || ee < 0 || ee >= (int)L.stride())
-            return 0u;
-          return hh[isd_bin_word(L, (unsigned int)r, (unsigned int)ee) + plane];
-        };
         if constexpr (PAIR == 0) {
-          s += at(row, (int)e, 0);
+          if (row_ok(row)) s += hh[row * A + gw];
         } else if constexpr (PAIR == 1) {
           const int D0 = L.pair_deg(0);
+          const bool ok0 = row_ok(row), ok1 = row_ok(row - 1);
+          const int w0 = row * A + gw, w1 = w0 - A;
+#pragma unroll
           for (int p = 0; p <= D0; ++p) {
-            const unsigned int plane = p * L.pair_words(0);
-            s += at(row, (int)e, plane);                   // paired site down
-            s += at(row - 1, (int)e - D0 + 2 * p, plane);  // ... up: partner
+            const int plane = p * (int)L.pair_words(0);
+            const int f = D0 - 2 * p;
+            if (ok0) s += hh[w0 + plane];  // paired site down
+            if (ok1 && e_ok((int)e - f))   // ... up: the partner
+              s += hh[w1 + plane - de_words(f)];
           }
         } else {
           const int D0 = L.pair_deg(0), D1 = L.pair_deg(1);
+          const bool ok0 = row_ok(row), ok1 = row_ok(row - 1),
+                     ok2 = row_ok(row - 2);
+          const int w0 = row * A + gw, w1 = w0 - A, w2 = w0 - 2 * A;
+#pragma unroll
           for (int p1 = 0; p1 <= D1; ++p1)
+#pragma unroll
             for (int p0 = 0; p0 <= D0; ++p0) {
-              const unsigned int plane = p0 * L.pair_words(0) +
-                                         p1 * L.pair_words(1);
+              const int plane = p0 * (int)L.pair_words(0) +
+                                p1 * (int)L.pair_words(1);
               const int f0 = D0 - 2 * p0, f1 = D1 - 2 * p1;
-              s += at(row, (int)e, plane);           // both paired sites down
-              s += at(row - 1, (int)e - f0, plane);  // bit-6 site up
-              s += at(row - 1, (int)e - f1, plane);  // bit-5 site up
-              s += at(row - 2, (int)e - f0 - f1 - L.pair_both(), plane);
+              const int f2 = f0 + f1 + L.pair_both();
+              if (ok0) s += hh[w0 + plane];  // both paired sites down
+              if (ok1 && e_ok((int)e - f0))  // bit-6 site up
+                s += hh[w1 + plane - de_words(f0)];
+              if (ok1 && e_ok((int)e - f1))  // bit-5 site up
+                s += hh[w1 + plane - de_words(f1)];
+              if (ok2 && e_ok((int)e - f2))  // both up
+                s += hh[w2 + plane - de_words(f2)];
             }
         }
       }
