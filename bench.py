@@ -199,7 +199,8 @@ def ncu_traffic(config):
     """dram read+write bytes per launch of k1_hoisted from the committed
     ncu --set full capture (profiles/r1_ncu_k1_hoisted_<config>.txt)."""
     # newest capture of the kernel the walk runs first
-    for name in (f"r1_ncu_k1_jit_gray_{config}.txt",
+    for name in (f"r1_ncu_k1_jit_band_{config}.txt",
+                 f"r1_ncu_k1_jit_gray_{config}.txt",
                  f"r1_ncu_k1_jit_pair2_{config}.txt",
                  f"r1_ncu_k1_jit_pair_{config}.txt",
                  f"r1_ncu_k1_jit_{config}.txt",
