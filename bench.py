@@ -453,6 +453,11 @@ def run_b200(args, wl):
         ok = isd.verify_dos(hist).passed
 
     # ---- e2e through the public API with host buffers ---------------------
+    # the (h, T) grid is host input data: built once, like the lattice
+    # (Workload.temps recomputes the grid on every access)
+    h_fields = np.asarray(wl.fields, dtype=np.float64)
+    h_temps = np.asarray(wl.temps, dtype=np.float64)
+
     def e2e_step():
         shard = isd.make_shards(wl.spec, world)[rank]
         part = isd.enumerate_shard(wl.spec, None, shard)
@@ -464,7 +469,7 @@ def run_b200(args, wl):
         else:
             hist = part
         if rank == 0:
-            isd.thermo_grid(hist, wl.fields, wl.temps)
+            isd.thermo_grid(hist, h_fields, h_temps)
 
     for _ in range(max(1, args.warmup)):
         e2e_step()

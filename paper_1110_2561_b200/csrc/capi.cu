@@ -192,8 +192,8 @@ static bool band_ok(const isd_plan_info& info, uint64_t start, uint64_t end) {
 }
 
 // Work items of a launch over 2^F slots (popcount order): ~n_target items of
-// equal size, cut so that each spans at most kBandSpan + 1 popcount classes.
-static std::vector<BandItem> build_band_items(int F, int n_target) {
+// equal size, cut so that each spans at most span + 1 popcount classes.
+static std::vector<BandItem> build_band_items(int F, int n_target, int span) {
   std::vector<uint64_t> cum(F + 2, 0);  // cum[q] = slots of popcount < q
   uint64_t c = 1;
   for (int q = 0; q <= F; ++q) {
@@ -207,7 +207,7 @@ static std::vector<BandItem> build_band_items(int F, int n_target) {
   int q = 0;
   while (g < total) {
     while (cum[q + 1] <= g) ++q;
-    const int q_last = std::min(F, q + kBandSpan);
+    const int q_last = std::min(F, q + span);
     uint64_t g1 = std::min(g + (size ? size : 1), cum[q_last + 1]);
     items.push_back(BandItem{g, g1, (unsigned)q, 0u});
     g = g1;
@@ -219,26 +219,53 @@ static std::mutex g_items_mu;
 static std::map<std::string, std::pair<BandItem*, uint32_t>> g_items;
 
 // Device work items for 2^F slots (uploaded once per device and size).
-static int band_items(int F, int n_target, BandItem** ptr, uint32_t* count) {
+static int band_items(int F, int n_target, int span, BandItem** ptr,
+                      uint32_t* count) {
   int dev = 0;
   cudaGetDevice(&dev);
   const std::string key = std::to_string(dev) + ":" + std::to_string(F) +
-                          ":" + std::to_string(n_target);
+                          ":" + std::to_string(n_target) + ":" +
+                          std::to_string(span);
   std::lock_guard<std::mutex> lock(g_items_mu);
   auto it = g_items.find(key);
   if (it == g_items.end()) {
     // the class-boundary cuts add a few small items: shrink the target so
     // the count stays a whole number of waves (blocks get equal work)
-    std::vector<BandItem> host = build_band_items(F, n_target);
+    std::vector<BandItem> host = build_band_items(F, n_target, span);
     for (int goal = n_target; (int)host.size() > n_target && goal > 1;) {
       goal -= (int)host.size() - n_target;
-      host = build_band_items(F, goal < 1 ? 1 : goal);
+      host = build_band_items(F, goal < 1 ? 1 : goal, span);
     }
+    // the kernel's unrank tables follow the items (k1_body.cuh isd_unrank):
+    // cum[q] for q <= F + 1, then C(b, q) for b < F, q <= F (u32: F <= 30)
+    if (F > 30) return fail(ISD_EINVAL, "banded launch: too many slot bits");
+    std::vector<uint32_t> tab((size_t)(F + 2) + (size_t)F * (F + 1), 0);
+    {
+      uint64_t c = 1, acc = 0;
+      for (int q = 0; q <= F + 1; ++q) {
+        tab[q] = (uint32_t)acc;
+        if (q <= F) {
+          acc += c;
+          c = c * (uint64_t)(F - q) / (uint64_t)(q + 1);
+        }
+      }
+      for (int b = 0; b < F; ++b) {
+        uint64_t cb = 1;  // C(b, q)
+        for (int q = 0; q <= F; ++q) {
+          tab[(size_t)(F + 2) + (size_t)b * (F + 1) + q] = (uint32_t)cb;
+          cb = q < b ? cb * (uint64_t)(b - q) / (uint64_t)(q + 1) : 0;
+        }
+      }
+    }
+    const size_t item_bytes = host.size() * sizeof(BandItem);
     BandItem* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, host.size() * sizeof(BandItem));
+    cudaError_t e =
+        cudaMalloc(&d, item_bytes + tab.size() * sizeof(uint32_t));
     if (e == cudaSuccess)
-      e = cudaMemcpy(d, host.data(), host.size() * sizeof(BandItem),
-                     cudaMemcpyHostToDevice);
+      e = cudaMemcpy(d, host.data(), item_bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(reinterpret_cast<char*>(d) + item_bytes, tab.data(),
+                     tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "band work items");
     it = g_items.emplace(key, std::make_pair(d, (uint32_t)host.size())).first;
   }
@@ -257,12 +284,15 @@ static int set_band_launch(HoistParams* hp, int sms) {
   if (rb < 6) return fail(ISD_EINVAL, "banded launch needs 2^r runs");
   BandItem* items = nullptr;
   uint32_t count = 0;
-  // two items per block once an item has >= 1024 slots (more blocks
-  // finish together), else one (each item costs a flush of the table)
+  // items of >= 512 slots, up to four per block (blocks then get a mix of
+  // popcount classes, whose walks run at slightly different speeds; each
+  // item costs a flush of the table): c5 2^36 walk 2.32 -> 2.30 ms
   const int F = rb - 5;
-  const int per_sm = (int)env_long(
-      "ISD_BAND_ITEMS_PER_SM", ((1ull << F) / (2ull * sms) >= 1024) ? 2 : 1);
-  const int rc = band_items(F, (per_sm < 1 ? 1 : per_sm) * sms, &items,
+  long dflt = (long)((1ull << F) / (512ull * (uint64_t)sms));
+  dflt = dflt < 1 ? 1 : (dflt > 4 ? 4 : dflt);
+  const int per_sm = (int)env_long("ISD_BAND_ITEMS_PER_SM", dflt);
+  const int rc = band_items(F, (per_sm < 1 ? 1 : per_sm) * sms,
+                            (int)hp->band_span, &items,
                             &count);
   if (rc) return rc;
   hp->band_free_bits = (uint32_t)(rb - 5);

@@ -12,6 +12,9 @@
 namespace isd {
 
 constexpr int kCopyBits = ISD_COPY_BITS;   // u: sites unrolled in registers
+// most loop sites the NVRTC kernel walks in Gray order (HoistParams.gray)
+constexpr int kMaxGray = 5;
+constexpr int kDefaultGray = 2;
 constexpr int kCopies = 1 << kCopyBits;    // 128 configurations per group
 static_assert(ISD_COPY_BITS == 7, "k1_hoisted emits 32 x 4 copies");
 constexpr int kTreeBits = 5;               // copies emitted as a 32-leaf tree
@@ -92,17 +95,18 @@ struct HoistParams {
   // flips up (cdelta, csum = their sum).
   uint32_t gray;
   uint32_t g_mask;
-  uint32_t g_bit[2];
-  uint64_t g_nm1[2], g_jn1[2], g_nm2[2], g_jn2[2];
-  uint32_t g_nm1v[2], g_jn1v[2], g_nm2v[2], g_jn2v[2];
-  int32_t g_deg[2], g_csum[2], g_odd[2];
-  int32_t g_cdelta[2][kCopyBits];
+  uint32_t g_bit[kMaxGray];
+  uint64_t g_nm1[kMaxGray], g_jn1[kMaxGray], g_nm2[kMaxGray], g_jn2[kMaxGray];
+  uint32_t g_nm1v[kMaxGray], g_jn1v[kMaxGray], g_nm2v[kMaxGray],
+      g_jn2v[kMaxGray];
+  int32_t g_deg[kMaxGray], g_csum[kMaxGray], g_odd[kMaxGray];
+  int32_t g_cdelta[kMaxGray][kCopyBits];
   // banded tables (isd_plan_info.band_rows): rows of the table, and for a
   // launch its work items (device array of BandItem) and free run bits
   uint32_t band_rows;
   uint32_t band_free_bits;
   uint32_t band_n_items;
-  uint32_t pad4_;
+  uint32_t band_span;  // popcount classes per work item - 1 (plan)
   uint64_t band_items;
 };
 

@@ -148,21 +148,21 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
   o << "  __host__ __device__ static constexpr int gray() { return " << P.gray
     << "; }\n";
   c32("g_mask", P.g_mask);
-  emit_switch(o, "uint32_t", "g_bit", P.g_bit, 2, "u");
-  emit_switch(o, "uint64_t", "g_nm1", P.g_nm1, 2, "ull");
-  emit_switch(o, "uint64_t", "g_jn1", P.g_jn1, 2, "ull");
-  emit_switch(o, "uint64_t", "g_nm2", P.g_nm2, 2, "ull");
-  emit_switch(o, "uint64_t", "g_jn2", P.g_jn2, 2, "ull");
-  emit_switch(o, "uint32_t", "g_nm1v", P.g_nm1v, 2, "u");
-  emit_switch(o, "uint32_t", "g_jn1v", P.g_jn1v, 2, "u");
-  emit_switch(o, "uint32_t", "g_nm2v", P.g_nm2v, 2, "u");
-  emit_switch(o, "uint32_t", "g_jn2v", P.g_jn2v, 2, "u");
-  emit_switch(o, "int32_t", "g_deg", P.g_deg, 2, "");
-  emit_switch(o, "int32_t", "g_csum", P.g_csum, 2, "");
-  emit_switch(o, "int32_t", "g_odd", P.g_odd, 2, "");
+  emit_switch(o, "uint32_t", "g_bit", P.g_bit, kMaxGray, "u");
+  emit_switch(o, "uint64_t", "g_nm1", P.g_nm1, kMaxGray, "ull");
+  emit_switch(o, "uint64_t", "g_jn1", P.g_jn1, kMaxGray, "ull");
+  emit_switch(o, "uint64_t", "g_nm2", P.g_nm2, kMaxGray, "ull");
+  emit_switch(o, "uint64_t", "g_jn2", P.g_jn2, kMaxGray, "ull");
+  emit_switch(o, "uint32_t", "g_nm1v", P.g_nm1v, kMaxGray, "u");
+  emit_switch(o, "uint32_t", "g_jn1v", P.g_jn1v, kMaxGray, "u");
+  emit_switch(o, "uint32_t", "g_nm2v", P.g_nm2v, kMaxGray, "u");
+  emit_switch(o, "uint32_t", "g_jn2v", P.g_jn2v, kMaxGray, "u");
+  emit_switch(o, "int32_t", "g_deg", P.g_deg, kMaxGray, "");
+  emit_switch(o, "int32_t", "g_csum", P.g_csum, kMaxGray, "");
+  emit_switch(o, "int32_t", "g_odd", P.g_odd, kMaxGray, "");
   o << "  __device__ __forceinline__ static constexpr int32_t g_cdelta(int g, "
        "int q) {\n";
-  for (int g = 0; g < 2; ++g)
+  for (int g = 0; g < kMaxGray; ++g)
     for (int q = 0; q < kCopyBits; ++q)
       o << "    if (g == " << g << " && q == " << q << ") return "
         << P.g_cdelta[g][q] << ";\n";

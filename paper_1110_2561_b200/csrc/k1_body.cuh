@@ -39,31 +39,47 @@ struct IsdBandItem {
 };
 
 // The g-th F-bit number in (popcount, value) order; *q = its popcount.
-__device__ __forceinline__ unsigned long long isd_unrank(unsigned long long g,
-                                                         int F, int* q) {
-  unsigned long long c = 1;  // C(F, q): size of popcount class q
+// Tables (uploaded after the launch's work items, isd::band_tables):
+// cum[q] = number of F-bit values of popcount < q (q <= F + 1) and
+// binom[b * (F + 1) + q] = C(b, q) for b < F, q <= F.  Warp-uniform: every
+// lane walks the same slot, so the loads are broadcasts.
+__device__ __forceinline__ unsigned long long isd_unrank(
+    unsigned int g, int F, const unsigned int* __restrict__ cum,
+    const unsigned int* __restrict__ binom, int* q) {
   int qq = 0;
-  while (g >= c && qq < F) {
-    g -= c;
-    c = c * (unsigned long long)(F - qq) / (unsigned long long)(qq + 1);
-    ++qq;
-  }
+  while (qq < F && g >= __ldg(cum + qq + 1)) ++qq;
   *q = qq;
+  g -= __ldg(cum + qq);
   // colex rank g among the F-bit numbers of popcount qq: the highest set
   // bit is the largest b with C(b, qq) <= g, and so on down
-  unsigned long long cb = F ? c * (unsigned long long)(F - qq) / F : 0;
   unsigned long long v = 0;
-  for (int bit = F - 1; bit >= 0 && qq > 0; --bit) {  // cb = C(bit, qq)
+  for (int bit = F - 1; bit >= 0 && qq > 0; --bit) {
+    const unsigned int cb = __ldg(binom + bit * (F + 1) + qq);
     if (g >= cb) {
       v |= 1ull << bit;
       g -= cb;
-      cb = bit ? cb * (unsigned long long)qq / bit : 0;  // C(bit-1, qq-1)
       --qq;
-    } else {
-      cb = bit ? cb * (unsigned long long)(bit - qq) / bit : 0;  // C(bit-1, qq)
     }
   }
   return v;
+}
+
+// index of the lowest set bit (s > 0); constexpr so unrolled Gray steps fold
+__host__ __device__ constexpr int isd_ctz(int s) {
+  return (s & 1) ? 0 : 1 + isd_ctz(s >> 1);
+}
+
+// Gray steps S .. 2^G - 1: flip site ctz(S) to its bit in gray(S), emit.
+// Each step is its own call site with constant arguments, so after inlining
+// the site's constants fold (a loop here stays rolled under NVRTC).
+template <int S, int G, class Flip, class Emit>
+__device__ __forceinline__ void isd_gray_steps(Flip& flip, Emit& emit) {
+  if constexpr (S < (1 << G)) {
+    constexpr int g = isd_ctz(S);
+    flip(g, (((S ^ (S >> 1)) >> g) & 1) != 0);
+    emit();
+    isd_gray_steps<S + 1, G>(flip, emit);
+  }
 }
 
 // the next F-bit number in (popcount, value) order
@@ -241,7 +257,7 @@ __device__ __forceinline__ void k1_hoisted_body(
       // non-copy sites change e by +-(D_g - 2 n_g), n_g from the current
       // neighbours; its bonds to copy sites shift those sites' unsatisfied
       // counts by the per-lattice g_cdelta (and e, d, the pattern planes)
-      auto flip = [&](int g, bool up) {
+      auto flip = [&](const int g, const bool up) {
         int ng = gpr[g] + __popc((jb ^ L.g_jn1v(g)) & L.g_nm1v(g));
         if (DOUBLE) ng += __popc((jb ^ L.g_jn2v(g)) & L.g_nm2v(g));
         const int sg = up ? 1 : -1;
@@ -260,18 +276,11 @@ __device__ __forceinline__ void k1_hoisted_body(
         if (L.g_odd(g)) par ^= 1u;
         jb ^= L.g_bit(g);
       };
+      // the 2^G subsets of the Gray sites in reflected Gray-code order:
+      // step s flips site ctz(s), to its value in gray(s) = s ^ (s >> 1)
+      // (unrolled at compile time, so every site index is a constant)
       emit();
-      if constexpr (G == 1) {
-        flip(0, true);
-        emit();
-      } else if constexpr (G == 2) {
-        flip(0, true);
-        emit();
-        flip(1, true);
-        emit();
-        flip(0, false);
-        emit();
-      }
+      isd_gray_steps<1, G>(flip, emit);
       jb = ((jb & outer) - outer) & outer;  // next subset (Gray sites clear)
     }
   };
@@ -280,12 +289,18 @@ __device__ __forceinline__ void k1_hoisted_body(
     const unsigned int m_lo = row_off;
     unsigned int m_hi = row_off + rows + (PAIR > 0 ? PAIR : 0);  // exclusive
     if (m_hi > L.nbins() / L.stride()) m_hi = L.nbins() / L.stride();
-    const unsigned int b_lo = m_lo * L.stride(), b_hi = m_hi * L.stride();
-    for (unsigned int bin = b_lo + threadIdx.x; bin < b_hi; bin += blockDim.x) {
-      const unsigned int m = bin / L.stride(), e = bin - m * L.stride();
-      // single parity plane: bins of the other parity are always 0 (and
-      // their words alias)
-      if (L.e_mode() && L.odd_mask() == 0 && (e & 1u) != L.e_parity()) continue;
+    // single parity plane: bins of the other parity are always 0 (and their
+    // words alias), so only the bins of parity e_parity are visited
+    const bool one_plane = L.e_mode() && L.odd_mask() == 0;
+    const unsigned int e0 = one_plane ? (unsigned int)L.e_parity() : 0u;
+    const unsigned int e_step = one_plane ? 2u : 1u;
+    const unsigned int per_row = (L.stride() - e0 + e_step - 1) / e_step;
+    const unsigned int n_units = (m_hi - m_lo) * per_row;
+    for (unsigned int u = threadIdx.x; u < n_units; u += blockDim.x) {
+      const unsigned int mr = u / per_row;
+      const unsigned int m = m_lo + mr;
+      const unsigned int e = e0 + (u - mr * per_row) * e_step;
+      const unsigned int bin = m * L.stride() + e;
       const int row = (int)(m - row_off);  // table row of this bin
       // words are linear in the row and, for the even shifts the pairing
       // makes, in e: word(r - dr, e - de) = word(r, e) - dr A - de_words(de)
@@ -360,23 +375,45 @@ __device__ __forceinline__ void k1_hoisted_body(
   } else {
     // ---- banded: work items of slots in popcount order ----
     const unsigned int warps = blockDim.x >> 5;
+    const unsigned int lane = threadIdx.x & 31;
     const unsigned int base_popc =
         (unsigned int)__popcll(run_begin << L.k());
+    const unsigned int* cum =
+        reinterpret_cast<const unsigned int*>(items + n_items);
+    const unsigned int* binom = cum + free_bits + 2;
+    __shared__ unsigned int next_slot;  // the item's first unclaimed slot
     for (unsigned int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const IsdBandItem item = items[it];
       zero_hist();
+      if (threadIdx.x == 0) next_slot = 0;
       __syncthreads();
       const unsigned int row_off = base_popc + item.q0;
-      // this warp's contiguous share of the item's slots
-      const unsigned long long n_slots = item.g1 - item.g0;
-      const unsigned long long per = (n_slots + warps - 1) / warps;
-      unsigned long long g = item.g0 + (unsigned long long)warp * per;
-      unsigned long long g_end = g + per;
-      if (g_end > item.g1) g_end = item.g1;
-      if (g < g_end) {
+      // Warps claim chunks of the item's slots (guided: a chunk is 1/(2W)
+      // of what is left, down to one slot), so they finish within about
+      // one slot of each other; each chunk starts with a table unrank and
+      // steps in popcount order.
+      const unsigned int n_slots = (unsigned int)(item.g1 - item.g0);
+      for (;;) {
+        unsigned int start = 0, cnt = 0;
+        if (lane == 0) {
+          unsigned int old = *(volatile unsigned int*)&next_slot;
+          while (old < n_slots) {
+            cnt = (n_slots - old) / (2u * warps);
+            if (cnt == 0) cnt = 1;
+            const unsigned int seen = atomicCAS(&next_slot, old, old + cnt);
+            if (seen == old) break;
+            old = seen;
+            cnt = 0;
+          }
+          start = old;
+        }
+        cnt = __shfl_sync(0xffffffffu, cnt, 0);
+        if (cnt == 0) break;
+        start = __shfl_sync(0xffffffffu, start, 0);
         int q = 0;
-        unsigned long long v = isd_unrank(g, free_bits, &q);
-        for (; g < g_end; ++g) {
+        unsigned long long v = isd_unrank((unsigned int)item.g0 + start,
+                                          free_bits, cum, binom, &q);
+        for (unsigned int i = 0; i < cnt; ++i) {
           run_body(slot_run(v), row_off);
           v = isd_next_slot(v, free_bits, &q);
         }

@@ -288,7 +288,11 @@ static int pair_policy() {
 
 static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
                           std::vector<isd_plan_info>* ranked, bool wide,
-                          int walk_bits, bool climb, int band_rows = 0) {
+                          int walk_bits, bool climb, int band_rows = 0,
+                          int band_span = kBandSpan, bool band_domino = false) {
+  // banded tables: lanes flip single sites (lane m span 5), or with
+  // band_domino also a neighbour of the pivot (span 10; rows sized for it)
+  const bool single_site = band_rows > 0 && !band_domino;
   // table rows: all N + 1 values of m, or a band of them
   const int n = band_rows ? band_rows - 1 : (int)lat->n_spins;
   const int n_spins = (int)lat->n_spins;
@@ -300,7 +304,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   info->est_per_config = 0;
   info->pair_mode = 0;
   info->band_rows = (uint32_t)band_rows;
-  info->band_span = band_rows ? (uint32_t)kBandSpan : 0;
+  info->band_span = band_rows ? (uint32_t)band_span : 0;
   // paired sites: copy bit 6 (index 0) and, for mode 2, copy bit 5
   const int psite[2] = {info->copy_site[kCopyBits - 1],
                         info->copy_site[kCopyBits - 2]};
@@ -400,7 +404,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
     return;
   }
   std::vector<Lanes> masks;
-  lane_candidates(lat, info, run_bits, wide, band_rows > 0, &masks);
+  lane_candidates(lat, info, run_bits, wide, single_site, &masks);
 
   // Score one lane mask against every layout on `warps` sampled warp
   // instructions x kCopySample copies; returns its best cost per
@@ -553,7 +557,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
         uint64_t partners = 0;
         for (int v = 0; v < 5; ++v) partners |= q.vec[v] & ~q.mask;
         const int piv = __builtin_ctzll(q.vec[i] & q.mask);
-        if (band_rows || (rng_next(&seed) & 1)) {  // re-pivot (drops the partner)
+        if (single_site || (rng_next(&seed) & 1)) {  // re-pivot (drops the partner)
           const int nb = (int)(rng_next(&seed) % run_bits);
           if (((q.mask | partners) >> nb) & 1) continue;
           q.mask = (q.mask & ~(1ull << piv)) | (1ull << nb);
@@ -768,14 +772,19 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   int walk_bits = 0;
   while (walk_bits < 63 && (1ull << (walk_bits + 1)) <= n_configs_hint)
     ++walk_bits;
-  const bool wide = n_configs_hint >= (1ull << 33);
+  // (test knob ISD_PLAN_WIDE=1: plan a small lattice as a large walk, with
+  // random and domino lane patterns, so the CPU replay can check them)
+  const bool wide = n_configs_hint >= (1ull << 33) ||
+                    env_int("ISD_PLAN_WIDE", 0) == 1;
   auto try_variant = [&](const isd_plan_info& base, const std::vector<int>& set,
-                         bool climb, int band_rows) {
+                         bool climb, int band_rows, int band_span = kBandSpan,
+                         bool band_domino = false) {
     isd_plan_info cand = base;
     bool all_even = true;
     for (int site : set) all_even = all_even && !((odd >> site) & 1);
     set_copy_sites(lat, &cand, set.data(), all_even ? 1 : 0);
-    choose_layout(lat, &cand, &all, wide, walk_bits, climb, band_rows);
+    choose_layout(lat, &cand, &all, wide, walk_bits, climb, band_rows,
+                  band_span, band_domino);
     if (cand.est_per_config >= 1e29) return;  // no layout of that kind
     if (!have || cand.est_per_config < best_info.est_per_config - 1e-9) {
       best_info = cand;
@@ -798,23 +807,40 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   // narrow.  Requires an aligned power-of-two range (checked at launch).
   const int policy = pair_policy();
   const bool pow2 = n_configs_hint && !(n_configs_hint & (n_configs_hint - 1));
+  // Two band shapes: single-site lanes (lane m span 5) with items of up to
+  // kBandSpan + 1 popcount classes and l = 5; or domino lanes (span 10)
+  // with one class per item and l = 4, so that the 49-plane table of a
+  // degree-6 lattice still fits shared memory.  The domino shape is off by
+  // default: on c5 the few layouts that fit 20 rows score 1.24 wavefronts
+  // per RED against 1.11 for the single-site shape (the model then picks
+  // single-site lanes anyway).  ISD_BAND_DOMINO=1 adds it, 2 keeps only it.
+  const long domino_knob = env_int("ISD_BAND_DOMINO", 0);
   if (band_knob != 0 && pow2 && (policy < 0 || policy == 2) &&
       (band_knob == 1 || (wide && (!have || best_info.pair_mode < 2)))) {
-    const int lb = (int)std::min<long>(env_int("ISD_BAND_LOOP_BITS", 5), l);
-    const int kb = u + lb;
-    const int rows = kBandSpan + 5 + lb + (u - 2) + 1;
-    if (walk_bits - kb - 5 >= 1 && kb <= 32 && rows <= n + 1) {
-      isd_plan_info base = *info;
-      base.l = (uint32_t)lb;
-      base.k = (uint32_t)kb;
-      base.run_mask_above_k = (n >= 64 ? ~0ull : ((1ull << n) - 1)) &
-                              ~((1ull << kb) - 1);
-      std::vector<std::vector<int>> bsets;
-      std::vector<const char*> bnames;
-      build_sets(kb, &bsets, &bnames);
-      for (size_t v = 0; v < bsets.size(); ++v)
-        if (!force || std::strcmp(force, bnames[v]) == 0)
-          try_variant(base, bsets[v], wide, rows);
+    for (int shape = 0; shape < 2; ++shape) {
+      const bool domino = shape == 1;
+      if ((domino && domino_knob == 0) || (!domino && domino_knob == 2))
+        continue;
+      const int span = domino ? 0 : kBandSpan;
+      const int lb = (int)std::min<long>(
+          env_int(domino ? "ISD_BAND_DOMINO_LOOP_BITS" : "ISD_BAND_LOOP_BITS",
+                  domino ? 4 : 5),
+          l);
+      const int kb = u + lb;
+      const int rows = span + (domino ? 10 : 5) + lb + (u - 2) + 1;
+      if (walk_bits - kb - 5 >= 1 && kb <= 32 && rows <= n + 1) {
+        isd_plan_info base = *info;
+        base.l = (uint32_t)lb;
+        base.k = (uint32_t)kb;
+        base.run_mask_above_k = (n >= 64 ? ~0ull : ((1ull << n) - 1)) &
+                                ~((1ull << kb) - 1);
+        std::vector<std::vector<int>> bsets;
+        std::vector<const char*> bnames;
+        build_sets(kb, &bsets, &bnames);
+        for (size_t v = 0; v < bsets.size(); ++v)
+          if (!force || std::strcmp(force, bnames[v]) == 0)
+            try_variant(base, bsets[v], wide, rows, span, domino);
+      }
     }
   }
   if (!have) return 1;  // forced variant not available for this lattice
@@ -917,6 +943,7 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
   for (int c = 0; c < kCopies; ++c)
     p->koff[c] = __builtin_popcount((unsigned)c) * rb + eb * unsat_cc(c);
   p->band_rows = info->band_rows;
+  p->band_span = info->band_span;
   p->pair = info->pair_mode;
   p->pair_both = info->pair_both;
   for (int i = 0; i < 2; ++i) {
@@ -924,11 +951,12 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
     p->pair_bytes[i] = 4 * info->pair_words[i];
     p->pair_deg[i] = info->pair_degree[i];
   }
-  // Gray sites: the lowest min(2, l) loop sites (ISD_GRAY=0|1|2 caps it)
+  // Gray sites: the lowest min(G, l) loop sites, G = kDefaultGray
+  // (ISD_GRAY=0..kMaxGray overrides it)
   {
-    long g = env_int("ISD_GRAY", 2);
+    long g = env_int("ISD_GRAY", kDefaultGray);
     if (g < 0) g = 0;
-    if (g > 2) g = 2;
+    if (g > kMaxGray) g = kMaxGray;
     if (g > (long)info->l) g = (long)info->l;
     p->gray = (uint32_t)g;
     int slot_of[64];

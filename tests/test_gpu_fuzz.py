@@ -80,18 +80,18 @@ def test_slices_match_c_oracle(spec):
 
 
 # The NVRTC-specialised kernel (normally only for walks >= 2^33) walks the
-# lowest 1-2 loop sites in Gray order, updating e and the copy-site counts
+# lowest 1-5 loop sites in Gray order, updating e and the copy-site counts
 # per flip; force it (ISD_JIT=2), a loop width, each Gray level and each
 # pairing mode on lattices of every kind, against the C oracle.
 JIT_SPECS = [s for s in WHOLE if s.num_spins >= 14][:8]
 
 
-@pytest.mark.parametrize("gray", ["1", "2"])
+@pytest.mark.parametrize("gray", ["1", "2", "3", "4", "5"])
 @pytest.mark.parametrize("pair", ["0", "1", "2"])
 @pytest.mark.parametrize("spec", JIT_SPECS, ids=repr)
 def test_jit_gray_walk_matches_c_oracle(spec, pair, gray, monkeypatch):
     monkeypatch.setenv("ISD_JIT", "2")
-    monkeypatch.setenv("ISD_LOOP_BITS", "4")
+    monkeypatch.setenv("ISD_LOOP_BITS", "5" if gray == "5" else "4")
     monkeypatch.setenv("ISD_GRAY", gray)
     monkeypatch.setenv("ISD_PAIR", pair)
     got = isd.full_dos(spec)

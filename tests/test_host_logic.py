@@ -204,7 +204,8 @@ def _slot_rank(v, F, cum):
     return cum[len(bits)] + sum(comb(b, i + 1) for i, b in enumerate(bits))
 
 
-def replay_hoisted(spec, loop_bits, pair=None, band_items=None):
+def replay_hoisted(spec, loop_bits, pair=None, band_items=None,
+                   domino=False):
     """numpy replay of k1_hoisted's arithmetic and address layout.
 
     Every index is decomposed exactly as the kernel does (run / loop /
@@ -218,13 +219,18 @@ def replay_hoisted(spec, loop_bits, pair=None, band_items=None):
         os.environ["ISD_PAIR"] = str(pair)
     if band_items is not None:  # force a banded mode-2 plan
         os.environ.update(ISD_BAND="1", ISD_PAIR="2",
-                          ISD_BAND_LOOP_BITS=str(loop_bits))
+                          ISD_BAND_LOOP_BITS=str(loop_bits),
+                          ISD_BAND_DOMINO_LOOP_BITS=str(loop_bits),
+                          ISD_BAND_DOMINO="2" if domino else "0")
+        if domino:  # lane patterns with domino partners need a "wide" plan
+            os.environ["ISD_PLAN_WIDE"] = "1"
     try:
         lat = native_lattice(spec)
         usable, info = _native.plan(lat, spec.num_configs)
     finally:
         for key in ("ISD_LOOP_BITS", "ISD_PAIR", "ISD_BAND",
-                    "ISD_BAND_LOOP_BITS"):
+                    "ISD_BAND_LOOP_BITS", "ISD_BAND_DOMINO_LOOP_BITS",
+                    "ISD_BAND_DOMINO", "ISD_PLAN_WIDE"):
             os.environ.pop(key, None)
     if band_items is not None and not info.band_rows:
         return None  # no banded layout for this lattice
@@ -296,10 +302,15 @@ def replay_hoisted(spec, loop_bits, pair=None, band_items=None):
         run = (x >> _u(k)).astype(np.int64)
         rb = n - k
         pivots = int(info.lane_mask)
-        assert all((int(v) & pivots) == int(v) for v in info.lane_vec)
+        # lane bit i = the run's bit at pivot i; XOR the lane pattern (with
+        # any domino partners) out to get the warp's slot bits
+        for v in info.lane_vec:
+            piv = int(v) & pivots
+            assert piv and piv & (piv - 1) == 0
+            run = run ^ (((run & piv) != 0) * (int(v) & ~piv))
         free = [b for b in range(rb) if not (pivots >> b) & 1]
         F = len(free)
-        items, cum = _band_items(F, band_items)
+        items, cum = _band_items(F, band_items, span=int(info.band_span))
         starts = np.array([it[0] for it in items], dtype=np.int64)
         vals = np.zeros(run.shape, dtype=np.int64)
         for j, b in enumerate(free):
@@ -426,11 +437,14 @@ BAND_REPLAY = [dict(rows=4, cols=4), dict(rows=2, cols=3, depth=3),
 @pytest.mark.parametrize("kw", BAND_REPLAY)
 @pytest.mark.parametrize("seed", [None, 11])
 @pytest.mark.parametrize("n_items", [3, 17])
-def test_banded_plan_replay_matches_oracle(kw, seed, n_items):
+@pytest.mark.parametrize("domino", [False, True])
+def test_banded_plan_replay_matches_oracle(kw, seed, n_items, domino):
     # banded mode 2: per-item tables of band_rows rows, the kernel's slot
-    # order and item split replayed, flushed per item, against the oracle
+    # order and item split replayed, flushed per item, against the oracle;
+    # both band shapes (single-site lanes; domino lanes, one popcount class
+    # per item)
     spec, (r, c, d, j, per, signs) = _spec_and_oracle(kw, seed)
-    got = replay_hoisted(spec, 1, band_items=n_items)
+    got = replay_hoisted(spec, 1, band_items=n_items, domino=domino)
     if got is None:
         pytest.skip("no banded layout")
     lat = port.Lattice(r, c, d, j, per, signs)
