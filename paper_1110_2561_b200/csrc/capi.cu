@@ -236,36 +236,13 @@ static int band_items(int F, int n_target, int span, BandItem** ptr,
       goal -= (int)host.size() - n_target;
       host = build_band_items(F, goal < 1 ? 1 : goal, span);
     }
-    // the kernel's unrank tables follow the items (k1_body.cuh isd_unrank):
-    // cum[q] for q <= F + 1, then C(b, q) for b < F, q <= F (u32: F <= 30)
-    if (F > 30) return fail(ISD_EINVAL, "banded launch: too many slot bits");
-    std::vector<uint32_t> tab((size_t)(F + 2) + (size_t)F * (F + 1), 0);
-    {
-      uint64_t c = 1, acc = 0;
-      for (int q = 0; q <= F + 1; ++q) {
-        tab[q] = (uint32_t)acc;
-        if (q <= F) {
-          acc += c;
-          c = c * (uint64_t)(F - q) / (uint64_t)(q + 1);
-        }
-      }
-      for (int b = 0; b < F; ++b) {
-        uint64_t cb = 1;  // C(b, q)
-        for (int q = 0; q <= F; ++q) {
-          tab[(size_t)(F + 2) + (size_t)b * (F + 1) + q] = (uint32_t)cb;
-          cb = q < b ? cb * (uint64_t)(b - q) / (uint64_t)(q + 1) : 0;
-        }
-      }
-    }
+    // the kernel's register unrank is exact in u32 up to F = 23
+    if (F > 23) return fail(ISD_EINVAL, "banded launch: too many slot bits");
     const size_t item_bytes = host.size() * sizeof(BandItem);
     BandItem* d = nullptr;
-    cudaError_t e =
-        cudaMalloc(&d, item_bytes + tab.size() * sizeof(uint32_t));
+    cudaError_t e = cudaMalloc(&d, item_bytes);
     if (e == cudaSuccess)
       e = cudaMemcpy(d, host.data(), item_bytes, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-      e = cudaMemcpy(reinterpret_cast<char*>(d) + item_bytes, tab.data(),
-                     tab.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "band work items");
     it = g_items.emplace(key, std::make_pair(d, (uint32_t)host.size())).first;
   }
@@ -274,11 +251,42 @@ static int band_items(int F, int n_target, int span, BandItem** ptr,
   return ISD_OK;
 }
 
-// Fill the banded-launch fields of hp for its run range [run_begin, run_end).
-static int set_band_launch(HoistParams* hp, int sms) {
+// Per-device ring of item-claim counters: each banded launch takes the next
+// slot and zeroes it on its own stream first, so launches in flight on
+// different streams never share a counter (64 slots).
+static std::mutex g_claim_mu;
+static std::map<int, uint32_t*> g_claim_ring;
+static std::atomic<uint32_t> g_claim_next{0};
+constexpr uint32_t kClaimSlots = 64;
+
+static int claim_counter(cudaStream_t st, uint32_t** out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  uint32_t* ring = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(g_claim_mu);
+    auto it = g_claim_ring.find(dev);
+    if (it == g_claim_ring.end()) {
+      cudaError_t e = cudaMalloc(&ring, kClaimSlots * 32);  // 32 B apart
+      if (e != cudaSuccess) return cuda_fail(e, "band claim counters");
+      it = g_claim_ring.emplace(dev, ring).first;
+    }
+    ring = it->second;
+  }
+  uint32_t* slot = ring + 8 * (g_claim_next.fetch_add(1) % kClaimSlots);
+  cudaError_t e = cudaMemsetAsync(slot, 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) return cuda_fail(e, "band claim counter reset");
+  *out = slot;
+  return ISD_OK;
+}
+
+// Fill the banded-launch fields of hp for its run range [run_begin, run_end)
+// (and zero its claim counter on st).
+static int set_band_launch(HoistParams* hp, int sms, cudaStream_t st) {
   hp->band_free_bits = 0;
   hp->band_items = 0;
   hp->band_n_items = 0;
+  hp->band_claim = 0;
   if (!hp->band_rows) return ISD_OK;
   const int rb = log2_exact(hp->run_end - hp->run_begin);
   if (rb < 6) return fail(ISD_EINVAL, "banded launch needs 2^r runs");
@@ -298,6 +306,14 @@ static int set_band_launch(HoistParams* hp, int sms) {
   hp->band_free_bits = (uint32_t)(rb - 5);
   hp->band_items = (uint64_t)(uintptr_t)items;
   hp->band_n_items = count;
+  // ISD_BAND_DYNAMIC=1: blocks claim items from a counter (measured no
+  // faster than the static round-robin over items in slot order)
+  if (env_long("ISD_BAND_DYNAMIC", 0) != 0) {
+    uint32_t* slot = nullptr;
+    const int rc2 = claim_counter(st, &slot);
+    if (rc2) return rc2;
+    hp->band_claim = (uint64_t)(uintptr_t)slot;
+  }
   return ISD_OK;
 }
 
@@ -454,7 +470,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
     hp.run_begin = run0 + off;
     hp.run_end = hp.run_begin + len;
     hp.hi_step = 1;
-    if (set_band_launch(&hp, sms)) continue;
+    if (set_band_launch(&hp, sms, st)) continue;
     float ms = 0.f;
     // (warm the finalist's kernel first: the JIT compile is not timed)
     int x = 0;
@@ -663,7 +679,7 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     if ((re - r) & ((1ull << lane_span(span_bits)) - 1))
       default_lanes(&hp.lane_mask, hp.lane_vec);
     hp.hi_step = 1;
-    rc = set_band_launch(&hp, sms);
+    rc = set_band_launch(&hp, sms, st);
     if (rc) return rc;
     int x = 0;
     if (use_jit) {

@@ -108,6 +108,9 @@ struct HoistParams {
   uint32_t band_n_items;
   uint32_t band_span;  // popcount classes per work item - 1 (plan)
   uint64_t band_items;
+  // banded launches: a zeroed u32 counter the blocks claim items from
+  // (dynamic scheduling; 0 = static round-robin)
+  uint64_t band_claim;
 };
 
 // Largest paired histogram (words): two CTAs of 512 threads per SM fit

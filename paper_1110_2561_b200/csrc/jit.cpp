@@ -89,6 +89,7 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
   o << "typedef unsigned int uint32_t;\n"
        "typedef unsigned long long uint64_t;\n"
        "typedef int int32_t;\n";
+  if (std::getenv("ISD_PROBE")) o << "#define ISD_PROBE 1\n";
   if (debug_bounds)
     o << "#define ISD_CHECK_ADDR(a, lo, bytes) do { if ((unsigned)((a) - "
          "(lo)) >= (bytes) || ((a) & 3u)) __trap(); } while (0)\n";
@@ -173,14 +174,14 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
     << ") k1_jit(unsigned long long run_begin, unsigned long long nruns,\n"
        "    unsigned long long hi_step, unsigned long long lane_mask,\n"
        "    const IsdLanes lanes, const IsdBandItem* items,\n"
-       "    unsigned int n_items, int free_bits,\n"
+       "    unsigned int n_items, int free_bits, unsigned int* claim,\n"
        "    unsigned long long* __restrict__ out) {\n"
        "  extern __shared__ __align__(16) unsigned int hist[];\n"
        "  const JitTraits L;\n"
        "  k1_hoisted_body<"
     << nc << ", " << (dbl ? "true" : "false") << ", "
     << P.pair << ">(L, run_begin, nruns, hi_step, lane_mask, lanes, items,\n"
-       "      n_items, free_bits, hist, out);\n}\n";
+       "      n_items, free_bits, claim, hist, out);\n}\n";
   return o.str();
 }
 
@@ -206,6 +207,7 @@ static std::string jit_key(const HoistParams& P, int device) {
   for (int i = 0; i < 5; ++i) q.lane_vec[i] = 0;
   q.band_free_bits = q.band_n_items = 0;  // launch arguments, not constants
   q.band_items = 0;
+  q.band_claim = 0;
   std::string key(reinterpret_cast<const char*>(&q), sizeof q);
   key += std::to_string(device);
   return key;
@@ -312,8 +314,9 @@ int launch_hoisted_jit(const HoistParams& P, unsigned long long* out,
   const void* items = reinterpret_cast<const void*>(P.band_items);
   unsigned int n_items = P.band_n_items;
   int free_bits = (int)P.band_free_bits;
-  void* args[] = {&run_begin, &nruns, &hi_step, &lane_mask, &lanes,
-                  &items,     &n_items, &free_bits, &out};
+  void* claim = reinterpret_cast<void*>(P.band_claim);
+  void* args[] = {&run_begin, &nruns,   &hi_step,   &lane_mask, &lanes,
+                  &items,     &n_items, &free_bits, &claim,     &out};
   int grid = jk.grid;
   const uint64_t need = (nruns + jk.threads - 1) / jk.threads;
   if (need < (uint64_t)grid) grid = (int)(need ? need : 1);

@@ -38,23 +38,32 @@ struct IsdBandItem {
   unsigned int q0, pad;
 };
 
-// The g-th F-bit number in (popcount, value) order; *q = its popcount.
-// Tables (uploaded after the launch's work items, isd::band_tables):
-// cum[q] = number of F-bit values of popcount < q (q <= F + 1) and
-// binom[b * (F + 1) + q] = C(b, q) for b < F, q <= F.  Warp-uniform: every
-// lane walks the same slot, so the loads are broadcasts.
-__device__ __forceinline__ unsigned long long isd_unrank(
-    unsigned int g, int F, const unsigned int* __restrict__ cum,
-    const unsigned int* __restrict__ binom, int* q) {
+// Binomial coefficients C(n, k), n, k < 24, in constant memory: the unrank
+// below reads them with warp-uniform indices (constant-cache broadcasts).
+struct IsdBinom {
+  unsigned int c[24][24];
+};
+__host__ __device__ constexpr IsdBinom isd_make_binom() {
+  IsdBinom b{};
+  for (int n = 0; n < 24; ++n)
+    for (int k = 0; k < 24; ++k)
+      b.c[n][k] = k == 0 ? 1u : (n == 0 ? 0u : b.c[n - 1][k - 1] + b.c[n - 1][k]);
+  return b;
+}
+__constant__ IsdBinom isd_binom = isd_make_binom();
+
+// The g-th F-bit number in (popcount, value) order; *q = its popcount
+// (F <= 23, checked by the host).  Warp-uniform.
+__device__ __forceinline__ unsigned long long isd_unrank(unsigned int g, int F,
+                                                         int* q) {
   int qq = 0;
-  while (qq < F && g >= __ldg(cum + qq + 1)) ++qq;
+  while (qq < F && g >= isd_binom.c[F][qq]) g -= isd_binom.c[F][qq++];
   *q = qq;
-  g -= __ldg(cum + qq);
   // colex rank g among the F-bit numbers of popcount qq: the highest set
   // bit is the largest b with C(b, qq) <= g, and so on down
   unsigned long long v = 0;
   for (int bit = F - 1; bit >= 0 && qq > 0; --bit) {
-    const unsigned int cb = __ldg(binom + bit * (F + 1) + qq);
+    const unsigned int cb = isd_binom.c[bit][qq];
     if (g >= cb) {
       v |= 1ull << bit;
       g -= cb;
@@ -123,8 +132,8 @@ __device__ __forceinline__ void k1_hoisted_body(
     const T& L, unsigned long long run_begin, unsigned long long nruns,
     unsigned long long hi_step, unsigned long long lane_mask,
     const IsdLanes lanes, const IsdBandItem* __restrict__ items,
-    unsigned int n_items, int free_bits, unsigned int* hist,
-    unsigned long long* __restrict__ out) {
+    unsigned int n_items, int free_bits, unsigned int* claim,
+    unsigned int* hist, unsigned long long* __restrict__ out) {
   auto zero_hist = [&]() {
     uint4* h4 = reinterpret_cast<uint4*>(hist);
     const unsigned int n4 = L.n_hist() * L.hist_words() / 4;
@@ -285,6 +294,9 @@ __device__ __forceinline__ void k1_hoisted_body(
     }
   };
   // ---- flush: table rows [0, rows) at absolute row row_off -> bins ----
+#ifdef ISD_PROBE
+  long long probe_t1 = 0;  // (probe build) end of the flush's stage 1
+#endif
   auto flush = [&](unsigned int row_off, unsigned int rows) {
     const unsigned int m_lo = row_off;
     unsigned int m_hi = row_off + rows + (PAIR > 0 ? PAIR : 0);  // exclusive
@@ -296,62 +308,126 @@ __device__ __forceinline__ void k1_hoisted_body(
     const unsigned int e_step = one_plane ? 2u : 1u;
     const unsigned int per_row = (L.stride() - e0 + e_step - 1) / e_step;
     const unsigned int n_units = (m_hi - m_lo) * per_row;
-    for (unsigned int u = threadIdx.x; u < n_units; u += blockDim.x) {
-      const unsigned int mr = u / per_row;
-      const unsigned int m = m_lo + mr;
-      const unsigned int e = e0 + (u - mr * per_row) * e_step;
-      const unsigned int bin = m * L.stride() + e;
-      const int row = (int)(m - row_off);  // table row of this bin
-      // words are linear in the row and, for the even shifts the pairing
-      // makes, in e: word(r - dr, e - de) = word(r, e) - dr A - de_words(de)
-      const int gw = (int)isd_bin_word(L, 0u, e);
-      auto de_words = [&](int de) {
-        return L.e_mode() ? (de >> 1) * (int)L.e_words() : de * (int)L.e_words();
-      };
-      auto row_ok = [&](int r) { return r >= 0 && r < (int)rows; };
-      auto e_ok = [&](int ee) { return ee >= 0 && ee < (int)L.stride(); };
-      const int A = (int)L.row_words();
-      unsigned long long s = 0;
-      for (unsigned int h = 0; h < L.n_hist(); ++h) {
-        const unsigned int* hh = hist + h * L.hist_words();
-        if constexpr (PAIR == 0) {
-          if (row_ok(row)) s += hh[row * A + gw];
-        } else if constexpr (PAIR == 1) {
-          const int D0 = L.pair_deg(0);
-          const bool ok0 = row_ok(row), ok1 = row_ok(row - 1);
-          const int w0 = row * A + gw, w1 = w0 - A;
+    // words are linear in the row and, for the even shifts the pairing
+    // makes, in e: word(r - dr, e - de) = word(r, e) - dr A - de_words(de)
+    auto de_words = [&](int de) {
+      return L.e_mode() ? (de >> 1) * (int)L.e_words() : de * (int)L.e_words();
+    };
+    auto row_ok = [&](int r) { return r >= 0 && r < (int)rows; };
+    auto e_ok = [&](int ee) { return ee >= 0 && ee < (int)L.stride(); };
+    const int A = (int)L.row_words();
+    if constexpr (PAIR == 2) {
+      // Separable two-stage flush.  A bin (m, e) collects, over the pattern
+      // planes (p0, p1), its own word and its three partners':
+      //   H[r, e] + H[r-1, e-f0] + H[r-1, e-f1] + H[r-2, e-f0-f1-t]
+      // (r = m - row_off, f_i = D_i - 2 p_i).  Stage 1 folds p0 per
+      // (r, e, p1): X = sum_p0 H[r, e], Y = sum_p0 H[r, e - f0], written in
+      // place over the words of p0 = 0 and 1 (a warp owns a whole (r, p1)
+      // slice, so only the warp syncs); stage 2 then needs 4 words per p1:
+      //   X[r, e] + Y[r-1, e] + X[r-1, e-f1] + Y[r-2, e-f1-t].
+      // 14 (D0 + 1) + 4 (D1 + 1) words per bin instead of 4 (D0+1)(D1+1).
+      const int D0 = L.pair_deg(0), D1 = L.pair_deg(1);
+      const int S0 = (int)L.pair_words(0), S1 = (int)L.pair_words(1);
+      const int y_off = D0 >= 1 ? S0 : 0;  // D0 = 0: Y = X
+      const unsigned int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+      const unsigned int slices = rows * (unsigned int)(D1 + 1);
+      constexpr int kE = 4;  // e units per lane (per_row <= 128)
+      for (unsigned int g = warp; g < slices * L.n_hist(); g += nwarps) {
+        unsigned int* hh = hist + (g / slices) * L.hist_words();
+        const unsigned int sl = g % slices;
+        const int r = (int)(sl / (unsigned int)(D1 + 1));
+        const int p1 = (int)(sl % (unsigned int)(D1 + 1));
+        unsigned int xs[kE], ys[kE];
+        int base[kE];
 #pragma unroll
-          for (int p = 0; p <= D0; ++p) {
-            const int plane = p * (int)L.pair_words(0);
-            const int f = D0 - 2 * p;
-            if (ok0) s += hh[w0 + plane];  // paired site down
-            if (ok1 && e_ok((int)e - f))   // ... up: the partner
-              s += hh[w1 + plane - de_words(f)];
-          }
-        } else {
-          const int D0 = L.pair_deg(0), D1 = L.pair_deg(1);
-          const bool ok0 = row_ok(row), ok1 = row_ok(row - 1),
-                     ok2 = row_ok(row - 2);
-          const int w0 = row * A + gw, w1 = w0 - A, w2 = w0 - 2 * A;
-#pragma unroll
-          for (int p1 = 0; p1 <= D1; ++p1)
+        for (int j = 0; j < kE; ++j) {
+          const unsigned int u = lane + 32u * j;
+          xs[j] = ys[j] = 0u;
+          base[j] = 0;
+          if (u < per_row) {
+            const unsigned int e = e0 + u * e_step;
+            base[j] = r * A + (int)isd_bin_word(L, 0u, e) + p1 * S1;
 #pragma unroll
             for (int p0 = 0; p0 <= D0; ++p0) {
-              const int plane = p0 * (int)L.pair_words(0) +
-                                p1 * (int)L.pair_words(1);
-              const int f0 = D0 - 2 * p0, f1 = D1 - 2 * p1;
-              const int f2 = f0 + f1 + L.pair_both();
-              if (ok0) s += hh[w0 + plane];  // both paired sites down
-              if (ok1 && e_ok((int)e - f0))  // bit-6 site up
-                s += hh[w1 + plane - de_words(f0)];
-              if (ok1 && e_ok((int)e - f1))  // bit-5 site up
-                s += hh[w1 + plane - de_words(f1)];
-              if (ok2 && e_ok((int)e - f2))  // both up
-                s += hh[w2 + plane - de_words(f2)];
+              const int f0 = D0 - 2 * p0;
+              xs[j] += hh[base[j] + p0 * S0];
+              if (e_ok((int)e - f0)) ys[j] += hh[base[j] + p0 * S0 - de_words(f0)];
             }
+          }
         }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < kE; ++j)
+          if (lane + 32u * j < per_row) {
+            hh[base[j]] = xs[j];
+            hh[base[j] + y_off] = ys[j];
+          }
+        __syncwarp();
       }
-      if (s) atomicAdd(out + bin, s);
+      __syncthreads();
+#ifdef ISD_PROBE
+      probe_t1 = clock64();
+#endif
+      // (each block starts at its own offset: blocks flushing at the same
+      // time then add into different lines of the global table)
+      const unsigned int rot = (blockIdx.x * 97u) % n_units;
+      for (unsigned int v = threadIdx.x; v < n_units; v += blockDim.x) {
+        const unsigned int u = v + rot < n_units ? v + rot : v + rot - n_units;
+        const unsigned int mr = u / per_row;
+        const unsigned int m = m_lo + mr;
+        const unsigned int e = e0 + (u - mr * per_row) * e_step;
+        const int row = (int)(m - row_off);
+        const int gw = (int)isd_bin_word(L, 0u, e);
+        const bool ok0 = row_ok(row), ok1 = row_ok(row - 1),
+                   ok2 = row_ok(row - 2);
+        unsigned long long s = 0;
+        for (unsigned int h = 0; h < L.n_hist(); ++h) {
+          const unsigned int* hh = hist + h * L.hist_words();
+          unsigned int s32 = 0;  // < 2^32: an item holds < 2^32 configurations
+#pragma unroll
+          for (int p1 = 0; p1 <= D1; ++p1) {
+            const int f1 = D1 - 2 * p1, ft = f1 + L.pair_both();
+            const int w0 = row * A + gw + p1 * S1;
+            if (ok0) s32 += hh[w0];                             // X[r, e]
+            if (ok1) s32 += hh[w0 - A + y_off];                 // Y[r-1, e]
+            if (ok1 && e_ok((int)e - f1))
+              s32 += hh[w0 - A - de_words(f1)];                 // X[r-1, e-f1]
+            if (ok2 && e_ok((int)e - ft))
+              s32 += hh[w0 - 2 * A - de_words(ft) + y_off];     // Y[r-2, ..]
+          }
+          s += s32;
+        }
+        if (s) atomicAdd(out + m * L.stride() + e, s);
+      }
+    } else {
+      for (unsigned int u = threadIdx.x; u < n_units; u += blockDim.x) {
+        const unsigned int mr = u / per_row;
+        const unsigned int m = m_lo + mr;
+        const unsigned int e = e0 + (u - mr * per_row) * e_step;
+        const unsigned int bin = m * L.stride() + e;
+        const int row = (int)(m - row_off);  // table row of this bin
+        const int gw = (int)isd_bin_word(L, 0u, e);
+        unsigned long long s = 0;
+        for (unsigned int h = 0; h < L.n_hist(); ++h) {
+          const unsigned int* hh = hist + h * L.hist_words();
+          if constexpr (PAIR == 0) {
+            if (row_ok(row)) s += hh[row * A + gw];
+          } else {
+            const int D0 = L.pair_deg(0);
+            const bool ok0 = row_ok(row), ok1 = row_ok(row - 1);
+            const int w0 = row * A + gw, w1 = w0 - A;
+#pragma unroll
+            for (int p = 0; p <= D0; ++p) {
+              const int plane = p * (int)L.pair_words(0);
+              const int f = D0 - 2 * p;
+              if (ok0) s += hh[w0 + plane];  // paired site down
+              if (ok1 && e_ok((int)e - f))   // ... up: the partner
+                s += hh[w1 + plane - de_words(f)];
+            }
+          }
+        }
+        if (s) atomicAdd(out + bin, s);
+      }
     }
   };
 
@@ -378,49 +454,95 @@ __device__ __forceinline__ void k1_hoisted_body(
     const unsigned int lane = threadIdx.x & 31;
     const unsigned int base_popc =
         (unsigned int)__popcll(run_begin << L.k());
-    const unsigned int* cum =
-        reinterpret_cast<const unsigned int*>(items + n_items);
-    const unsigned int* binom = cum + free_bits + 2;
     __shared__ unsigned int next_slot;  // the item's first unclaimed slot
-    for (unsigned int it = blockIdx.x; it < n_items; it += gridDim.x) {
-      const IsdBandItem item = items[it];
+    __shared__ unsigned int cur_item;
+    // Blocks claim items from a zeroed counter (dynamic scheduling), or
+    // without one take every gridDim-th item.
+    for (unsigned int k = 0;; ++k) {
+      if (threadIdx.x == 0) {
+        const unsigned int c =
+            claim ? atomicAdd(claim, 1u) : blockIdx.x + k * gridDim.x;
+        cur_item = c;
+        // warp w's first chunk is [w c0, (w + 1) c0) (no claim, no wait);
+        // the rest is claimed from next_slot
+        if (c < n_items) {
+          const unsigned int n = (unsigned int)(items[c].g1 - items[c].g0);
+          unsigned int c0 = n / (2u * warps);
+          c0 = c0 ? c0 : 1u;
+          next_slot = n < warps * c0 ? n : warps * c0;
+        }
+      }
       zero_hist();
-      if (threadIdx.x == 0) next_slot = 0;
       __syncthreads();
+      const unsigned int it = cur_item;
+      if (it >= n_items) break;
+      const IsdBandItem item = items[it];
+#ifdef ISD_PROBE
+      const long long t_item = clock64();
+      long long t_first = 0;
+#endif
       const unsigned int row_off = base_popc + item.q0;
-      // Warps claim chunks of the item's slots (guided: a chunk is 1/(2W)
-      // of what is left, down to one slot), so they finish within about
-      // one slot of each other; each chunk starts with a table unrank and
+      // Warps then claim chunks of the item's slots (guided: a chunk is
+      // 1/(2W) of what is left, down to one slot), so they finish within
+      // about one slot of each other; each chunk starts with an unrank and
       // steps in popcount order.
       const unsigned int n_slots = (unsigned int)(item.g1 - item.g0);
-      for (;;) {
+      unsigned int c0 = n_slots / (2u * warps);
+      c0 = c0 ? c0 : 1u;
+      for (bool first = true;; first = false) {
         unsigned int start = 0, cnt = 0;
-        if (lane == 0) {
-          unsigned int old = *(volatile unsigned int*)&next_slot;
-          while (old < n_slots) {
-            cnt = (n_slots - old) / (2u * warps);
-            if (cnt == 0) cnt = 1;
-            const unsigned int seen = atomicCAS(&next_slot, old, old + cnt);
-            if (seen == old) break;
-            old = seen;
-            cnt = 0;
+        if (first) {
+          start = warp * c0;
+          cnt = start < n_slots ? min(c0, n_slots - start) : 0u;
+          if (cnt == 0) continue;
+        } else {
+          if (lane == 0) {
+            unsigned int old = *(volatile unsigned int*)&next_slot;
+            while (old < n_slots) {
+              cnt = (n_slots - old) / (2u * warps);
+              if (cnt == 0) cnt = 1;
+              const unsigned int seen = atomicCAS(&next_slot, old, old + cnt);
+              if (seen == old) break;
+              old = seen;
+              cnt = 0;
+            }
+            start = old;
           }
-          start = old;
+          cnt = __shfl_sync(0xffffffffu, cnt, 0);
+          if (cnt == 0) break;
+          start = __shfl_sync(0xffffffffu, start, 0);
         }
-        cnt = __shfl_sync(0xffffffffu, cnt, 0);
-        if (cnt == 0) break;
-        start = __shfl_sync(0xffffffffu, start, 0);
         int q = 0;
-        unsigned long long v = isd_unrank((unsigned int)item.g0 + start,
-                                          free_bits, cum, binom, &q);
+        unsigned long long v =
+            isd_unrank((unsigned int)item.g0 + start, free_bits, &q);
+#ifdef ISD_PROBE
+        if (t_first == 0) t_first = clock64();
+#endif
         for (unsigned int i = 0; i < cnt; ++i) {
           run_body(slot_run(v), row_off);
           v = isd_next_slot(v, free_bits, &q);
         }
       }
+#ifdef ISD_PROBE
+      const long long t_done = clock64();  // this warp's walk ends
+#endif
       __syncthreads();
+#ifdef ISD_PROBE
+      const long long t_walk = clock64();
+#endif
       flush(row_off, L.band_rows());
       __syncthreads();
+#ifdef ISD_PROBE
+      // (probe build) per item: first chunk start, this warp's end, last
+      // warp's end, flush end, relative to the item start (SM cycles)
+      if ((threadIdx.x & 31) == 0 && blockIdx.x < 4 &&
+          (warp == 0 || warp == 31))
+        printf("ISDPROBE blk %u item %u q0 %u slots %u warp %u first %lld "
+               "done %lld walk %lld stage1 %lld flush %lld\n", blockIdx.x, it,
+               item.q0, (unsigned)(item.g1 - item.g0), warp,
+               t_first - t_item, t_done - t_item, t_walk - t_item,
+               probe_t1 - t_item, clock64() - t_item);
+#endif
     }
   }
 }

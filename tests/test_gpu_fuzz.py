@@ -14,6 +14,7 @@ The oracle side builds its bond list from the naive oracle's geometry
 Bit-exact equality is required.
 """
 
+import os
 import random
 
 import numpy as np
@@ -90,6 +91,14 @@ JIT_SPECS = [s for s in WHOLE if s.num_spins >= 14][:8]
 @pytest.mark.parametrize("pair", ["0", "1", "2"])
 @pytest.mark.parametrize("spec", JIT_SPECS, ids=repr)
 def test_jit_gray_walk_matches_c_oracle(spec, pair, gray, monkeypatch):
+    # Gray widths 3-5 unroll 2^G copies of the RED tree: on 4 lattices, not
+    # unpaired beyond G = 3 (4096 REDs of code), and not through the
+    # bounds-checked build (its NVRTC compile of G = 5 takes minutes)
+    if int(gray) >= 3:
+        if JIT_SPECS.index(spec) >= 4 or (pair == "0" and int(gray) >= 4):
+            pytest.skip("Gray width >= 3: a subset of the lattices and modes")
+        if os.environ.get("ISD_LIBRARY", "").endswith("_dbg.so"):
+            pytest.skip("Gray width >= 3 runs through the release build")
     monkeypatch.setenv("ISD_JIT", "2")
     monkeypatch.setenv("ISD_LOOP_BITS", "5" if gray == "5" else "4")
     monkeypatch.setenv("ISD_GRAY", gray)
