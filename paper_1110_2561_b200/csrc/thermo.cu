@@ -29,6 +29,7 @@ constexpr int kThermoThreads = 256;                 // 8 warps
 constexpr int kTeam = 4;                            // warps per point
 constexpr int kTeamLanes = 32 * kTeam;
 constexpr int kThermoPoints = kThermoThreads / kTeamLanes;  // 2 per CTA
+constexpr int kKeep = 12;  // w of a lane's first 12 cells kept for pass 3
 constexpr int kMaxBins = (ISD_MAX_SPINS + 1) * (3 * ISD_MAX_SPINS + 1);
 
 struct Cell {
@@ -43,10 +44,10 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-__device__ __forceinline__ double warp_max(double v) {
+__device__ __forceinline__ double warp_min(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1)
-    v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
@@ -133,36 +134,60 @@ __global__ void __launch_bounds__(kThermoThreads)
     return r;
   };
 
-  // pass 1: shift = max x over occupied cells
-  double xmax = -INFINITY;
+  // pass 1: shift = max over occupied cells of x = -H / T.  Division by
+  // T > 0 is monotone, so that max is exactly -H_min / T: one division per
+  // point instead of one per cell.
+  double hmin = INFINITY;
   for (int i = tl; i < nc; i += kTeamLanes) {
     const double m = (double)cells[i].m;
     const double e = (double)cells[i].e * scale;
-    const double en = e - h * m;
-    xmax = fmax(xmax, -en / t);
+    hmin = fmin(hmin, e - h * m);
   }
-  xmax = warp_max(xmax);
-  if (lane == 0) part[warp][0] = xmax;
+  hmin = warp_min(hmin);
+  if (lane == 0) part[warp][0] = hmin;
   __syncthreads();
-  double shift = part[team * kTeam][0];
+  double hlo = part[team * kTeam][0];
 #pragma unroll
-  for (int w = 1; w < kTeam; ++w) shift = fmax(shift, part[team * kTeam + w][0]);
+  for (int w = 1; w < kTeam; ++w) hlo = fmin(hlo, part[team * kTeam + w][0]);
+  const double shift = -hlo / t;
   __syncthreads();
 
   // pass 2: w = g exp(x - shift); s = sum w and the first moments as
-  // w-weighted sums (divided by s afterwards: one exp per cell here, one in
-  // pass 3).  Two independent accumulators per lane hide the exp latency;
-  // they are combined in a fixed order, then across lanes and warps.
+  // w-weighted sums (divided by s afterwards).  A lane keeps the w of its
+  // first kKeep cells in registers for pass 3 (the rest are recomputed).
+  // Two independent accumulators per lane hide the exp latency; they are
+  // combined in a fixed order, then across lanes and warps.
+  double wk[kKeep];
   double s2[2] = {0, 0}, u2[2] = {0, 0}, m2[2] = {0, 0}, a2[2] = {0, 0};
-  for (int i0 = tl; i0 < nc; i0 += 2 * kTeamLanes) {
+  auto weight = [&](int i, double* en_out, double* m_out) {
+    const double m = (double)cells[i].m;
+    const double e = (double)cells[i].e * scale;
+    const double en = e - h * m;
+    *en_out = en;
+    *m_out = m;
+    return cells[i].g * exp(-en / t - shift);
+  };
+#pragma unroll
+  for (int j = 0; j < kKeep; ++j) {
+    const int i = tl + kTeamLanes * j;
+    wk[j] = 0.0;
+    if (i < nc) {
+      double en, m;
+      const double w = weight(i, &en, &m);
+      wk[j] = w;
+      s2[j & 1] += w;
+      u2[j & 1] += w * en;
+      m2[j & 1] += w * m;
+      a2[j & 1] += w * fabs(m);
+    }
+  }
+  for (int i0 = tl + kTeamLanes * kKeep; i0 < nc; i0 += 2 * kTeamLanes) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int i = i0 + kTeamLanes * j;
       if (i < nc) {
-        const double m = (double)cells[i].m;
-        const double e = (double)cells[i].e * scale;
-        const double en = e - h * m;
-        const double w = cells[i].g * exp(-en / t - shift);
+        double en, m;
+        const double w = weight(i, &en, &m);
         s2[j] += w;
         u2[j] += w * en;
         m2[j] += w * m;
@@ -179,15 +204,24 @@ __global__ void __launch_bounds__(kThermoThreads)
   // pass 3: central second moments (the two-pass form of thermo.py:75-77;
   // the raw <H^2> - <H>^2 form cancels catastrophically at low T)
   double e2[2] = {0, 0}, v2[2] = {0, 0};
-  for (int i0 = tl; i0 < nc; i0 += 2 * kTeamLanes) {
+#pragma unroll
+  for (int j = 0; j < kKeep; ++j) {
+    const int i = tl + kTeamLanes * j;
+    if (i < nc) {
+      const double m = (double)cells[i].m;
+      const double en = (double)cells[i].e * scale - h * m;
+      const double de = en - u, dm = m - mean_m;
+      e2[j & 1] += wk[j] * (de * de);
+      v2[j & 1] += wk[j] * (dm * dm);
+    }
+  }
+  for (int i0 = tl + kTeamLanes * kKeep; i0 < nc; i0 += 2 * kTeamLanes) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int i = i0 + kTeamLanes * j;
       if (i < nc) {
-        const double m = (double)cells[i].m;
-        const double e = (double)cells[i].e * scale;
-        const double en = e - h * m;
-        const double w = cells[i].g * exp(-en / t - shift);
+        double en, m;
+        const double w = weight(i, &en, &m);
         const double de = en - u, dm = m - mean_m;
         e2[j] += w * (de * de);
         v2[j] += w * (dm * dm);

@@ -1,5 +1,5 @@
-# full GPU check after the banded-launch changes, then evidence: bench line,
-# K1 launch list under ncu, ncu --set full of the c5 walk kernel
+# full GPU check, then evidence: bench line, launch list, ncu of the c5 walk
+# kernel, of one 8-way shard and of K2
 mkdir -p gpurun_out
 bash tools/gpu_checks.sh > gpurun_out/checks_v.log 2>&1; echo "checks exit=$?" >> gpurun_out/checks_v.log
 grep -E "passed|failed|smoke|exit" gpurun_out/checks_v.log
@@ -9,6 +9,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/r1v_launches_bench_c5.csv python bench.py --steps 3 --warmup 3 \
   --no-cpu-baseline --extra-configs "" > gpurun_out/ncu_launch_v.log 2>&1
 ISD_AUTOTUNE=0 ncu --set full --clock-control none --import-source on -k regex:k1_jit -c 1 -f \
-  -o gpurun_out/r1_k1_jit_band3_c5 python tools/run_k1.py --config c5 --reps 1 \
+  -o gpurun_out/r1_k1_jit_band4_c5 python tools/run_k1.py --config c5 --reps 1 \
   > gpurun_out/ncu_v_c5.log 2>&1
-tail -c 1200 gpurun_out/bench_r1v.json
+ISD_AUTOTUNE=0 ncu --set full --clock-control none --import-source on -k regex:k1_jit -c 1 -f \
+  -o gpurun_out/r1_k1_jit_shard8b_c5 python tools/run_k1.py --config c5 --shards 8 --index 3 --reps 1 \
+  > gpurun_out/ncu_v_shard.log 2>&1
+for i in 0 3 7; do python tools/run_k1.py --config c5 --shards 8 --index $i --reps 4 2>&1 | tail -2 | head -1; done
+tail -c 1500 gpurun_out/bench_r1v.json
