@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -192,8 +193,12 @@ static bool band_ok(const isd_plan_info& info, uint64_t start, uint64_t end) {
 }
 
 // Work items of a launch over 2^F slots (popcount order): ~n_target items of
-// equal size, cut so that each spans at most span + 1 popcount classes.
-static std::vector<BandItem> build_band_items(int F, int n_target, int span) {
+// equal cost, cut so that each spans at most span + 1 popcount classes.  The
+// slots are cut into w.size() equal segments and a slot of segment j costs
+// w[j] (expected wavefronts per RED, band_slot_cost; empty w: equal costs),
+// so items where the lanes' bins spread over more banks hold fewer slots.
+static std::vector<BandItem> build_band_items(int F, int n_target, int span,
+                                              const std::vector<double>& w) {
   std::vector<uint64_t> cum(F + 2, 0);  // cum[q] = slots of popcount < q
   uint64_t c = 1;
   for (int q = 0; q <= F; ++q) {
@@ -201,16 +206,30 @@ static std::vector<BandItem> build_band_items(int F, int n_target, int span) {
     c = c * (uint64_t)(F - q) / (uint64_t)(q + 1);
   }
   const uint64_t total = cum[F + 1];
-  const uint64_t size = (total + n_target - 1) / n_target;
+  const uint64_t n_seg = w.empty() ? 1 : (uint64_t)w.size();
+  auto seg_lo = [&](uint64_t j) { return total * j / n_seg; };
+  double total_w = 0;
+  for (uint64_t j = 0; j < n_seg; ++j)
+    total_w += (double)(seg_lo(j + 1) - seg_lo(j)) * (w.empty() ? 1.0 : w[j]);
+  const double target = total_w / (n_target > 0 ? n_target : 1);
   std::vector<BandItem> items;
-  uint64_t g = 0;
+  uint64_t g = 0, j = 0;
   int q = 0;
   while (g < total) {
     while (cum[q + 1] <= g) ++q;
-    const int q_last = std::min(F, q + span);
-    uint64_t g1 = std::min(g + (size ? size : 1), cum[q_last + 1]);
-    items.push_back(BandItem{g, g1, (unsigned)q, 0u});
-    g = g1;
+    const uint64_t limit = cum[std::min(F, q + span) + 1];
+    const uint64_t g0 = g;
+    double budget = target;
+    while (g < limit && budget > 0) {
+      while (seg_lo(j + 1) <= g) ++j;
+      const double wj = w.empty() ? 1.0 : std::max(w[j], 1e-3);
+      const uint64_t room = std::min(limit, seg_lo(j + 1)) - g;
+      uint64_t take = (uint64_t)std::ceil(budget / wj - 1e-9);
+      take = std::max<uint64_t>(1, std::min(take, room));
+      g += take;
+      budget -= (double)take * wj;
+    }
+    items.push_back(BandItem{g0, g, (unsigned)q, 0u});
   }
   return items;
 }
@@ -218,26 +237,37 @@ static std::vector<BandItem> build_band_items(int F, int n_target, int span) {
 static std::mutex g_items_mu;
 static std::map<std::string, std::pair<BandItem*, uint32_t>> g_items;
 
-// Device work items for 2^F slots (uploaded once per device and size).
-static int band_items(int F, int n_target, int span, BandItem** ptr,
-                      uint32_t* count) {
+// Device work items for 2^F slots (uploaded once per device, size and cost
+// curve; `cost_key` identifies w).
+static int band_items(int F, int n_target, int span,
+                      const std::vector<double>& w, const std::string& cost_key,
+                      BandItem** ptr, uint32_t* count) {
   int dev = 0;
   cudaGetDevice(&dev);
   const std::string key = std::to_string(dev) + ":" + std::to_string(F) +
                           ":" + std::to_string(n_target) + ":" +
-                          std::to_string(span);
+                          std::to_string(span) + ":" + cost_key;
   std::lock_guard<std::mutex> lock(g_items_mu);
   auto it = g_items.find(key);
   if (it == g_items.end()) {
-    // the class-boundary cuts add a few small items: shrink the target so
-    // the count stays a whole number of waves (blocks get equal work)
-    std::vector<BandItem> host = build_band_items(F, n_target, span);
-    for (int goal = n_target; (int)host.size() > n_target && goal > 1;) {
-      goal -= (int)host.size() - n_target;
-      host = build_band_items(F, goal < 1 ? 1 : goal, span);
-    }
     // the kernel's register unrank is exact in u32 up to F = 23
     if (F > 23) return fail(ISD_EINVAL, "banded launch: too many slot bits");
+    // the class-boundary cuts add a few small items: shrink the target so
+    // the count stays a whole number of waves (blocks get equal work)
+    std::vector<BandItem> host = build_band_items(F, n_target, span, w);
+    for (int goal = n_target; (int)host.size() > n_target && goal > 1;) {
+      goal -= (int)host.size() - n_target;
+      host = build_band_items(F, goal < 1 ? 1 : goal, span, w);
+    }
+    // the items must tile [0, 2^F) in order
+    uint64_t next = 0;
+    for (const BandItem& x : host) {
+      if (x.g0 != next || x.g1 <= x.g0)
+        return fail(ISD_EINVAL, "band work items do not tile the slots");
+      next = x.g1;
+    }
+    if (next != (1ull << F))
+      return fail(ISD_EINVAL, "band work items do not tile the slots");
     const size_t item_bytes = host.size() * sizeof(BandItem);
     BandItem* d = nullptr;
     cudaError_t e = cudaMalloc(&d, item_bytes);
@@ -249,6 +279,70 @@ static int band_items(int F, int n_target, int span, BandItem** ptr,
   *ptr = it->second.first;
   *count = it->second.second;
   return ISD_OK;
+}
+
+// Cost curve of a banded launch (cached: same lattice, plan, lanes and run
+// base give the same curve).  ISD_BAND_WEIGHTS=0: equal costs.
+static std::mutex g_cost_mu;
+// key -> (curve, short name of the curve for the items cache)
+static std::map<std::string, std::pair<std::vector<double>, std::string>>
+    g_cost;
+
+static void band_costs(const isd_lattice* lat, const isd_plan_info& info,
+                       const HoistParams& hp, int run_bits,
+                       const std::vector<double>** w, std::string* key) {
+  *w = nullptr;
+  key->clear();
+  if (env_long("ISD_BAND_WEIGHTS", 1) == 0) return;
+  // (explicit fields: the structs' padding is not initialised)
+  std::string k;
+  auto add = [&](unsigned long long v) { k += std::to_string(v) + ","; };
+  add(lat->n_spins);
+  for (uint32_t c = 0; c < lat->n_classes; ++c) {
+    add(lat->classes[c].shift);
+    add(lat->classes[c].bond_mask);
+    add(lat->classes[c].jneg_mask);
+  }
+  add(info.k);
+  add(info.loop_mask);
+  add(info.e_mode);
+  add(info.row_words);
+  add(info.e_words);
+  add(info.plane_words);
+  for (int i = 0; i < 2; ++i) {
+    add(info.pair_words[i]);
+    add(info.pair_degree[i]);
+  }
+  for (int t = 0; t < kCopyBits; ++t) add(info.copy_site[t]);
+  add(hp.lane_mask);
+  for (int v = 0; v < 5; ++v) add(hp.lane_vec[v]);
+  add(hp.run_begin);
+  add((unsigned long long)run_bits);
+  {
+    std::lock_guard<std::mutex> lock(g_cost_mu);
+    auto it = g_cost.find(k);
+    if (it == g_cost.end()) {
+      std::vector<double> c;
+      // ~16 segments per item of a four-items-per-block launch, 64
+      // samples each (c5: ~0.3 s once per process and plan)
+      const int F = run_bits - 5;
+      const int n_seg = (int)std::min<uint64_t>(1ull << F, 16ull * 4 * 148);
+      band_slot_cost(lat, info, hp.run_begin, hp.lane_mask, hp.lane_vec,
+                     run_bits, n_seg, 64, &c);
+      // the items cache names the curve by a hash of its rounded values
+      uint64_t h = 1469598103934665603ull;
+      for (double x : c) {
+        h ^= (uint64_t)std::llround(x * 1e4);
+        h *= 1099511628211ull;
+      }
+      std::string name = "w" + std::to_string(h) + ":" +
+                         std::to_string(c.size());
+      it = g_cost.emplace(k, std::make_pair(std::move(c), std::move(name)))
+               .first;
+    }
+    *w = &it->second.first;  // (map nodes are stable)
+    *key = it->second.second;
+  }
 }
 
 // Per-device ring of item-claim counters: each banded launch takes the next
@@ -282,7 +376,9 @@ static int claim_counter(cudaStream_t st, uint32_t** out) {
 
 // Fill the banded-launch fields of hp for its run range [run_begin, run_end)
 // (and zero its claim counter on st).
-static int set_band_launch(HoistParams* hp, int sms, cudaStream_t st) {
+static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
+                           HoistParams* hp, int sms, cudaStream_t st,
+                           bool weighted = true) {
   hp->band_free_bits = 0;
   hp->band_items = 0;
   hp->band_n_items = 0;
@@ -292,16 +388,25 @@ static int set_band_launch(HoistParams* hp, int sms, cudaStream_t st) {
   if (rb < 6) return fail(ISD_EINVAL, "banded launch needs 2^r runs");
   BandItem* items = nullptr;
   uint32_t count = 0;
-  // items of >= 512 slots, up to four per block (blocks then get a mix of
-  // popcount classes, whose walks run at slightly different speeds; each
-  // item costs a flush of the table): c5 2^36 walk 2.32 -> 2.30 ms
+  // One item per block: items are cut to equal modelled cost
+  // (band_slot_cost), so blocks finish together without the extra flushes
+  // of several items per block.  Measured on c5: 2^36 walk 2.253 ms with
+  // four equal-size items per block -> 2.201 ms with one cost-weighted
+  // item; 2^33 shards 0.33-0.38 -> 0.30-0.33 ms.  Without weights
+  // (ISD_BAND_WEIGHTS=0) up to four items per block of >= 512 slots mix
+  // popcount classes instead.
   const int F = rb - 5;
   long dflt = (long)((1ull << F) / (512ull * (uint64_t)sms));
   dflt = dflt < 1 ? 1 : (dflt > 4 ? 4 : dflt);
+  if (weighted && env_long("ISD_BAND_WEIGHTS", 1) != 0) dflt = 1;
   const int per_sm = (int)env_long("ISD_BAND_ITEMS_PER_SM", dflt);
+  const std::vector<double>* w = nullptr;
+  std::string cost_key;
+  if (weighted) band_costs(lat, info, *hp, rb, &w, &cost_key);
+  static const std::vector<double> equal;
   const int rc = band_items(F, (per_sm < 1 ? 1 : per_sm) * sms,
-                            (int)hp->band_span, &items,
-                            &count);
+                            (int)hp->band_span, w ? *w : equal, cost_key,
+                            &items, &count);
   if (rc) return rc;
   hp->band_free_bits = (uint32_t)(rb - 5);
   hp->band_items = (uint64_t)(uintptr_t)items;
@@ -470,7 +575,9 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
     hp.run_begin = run0 + off;
     hp.run_end = hp.run_begin + len;
     hp.hi_step = 1;
-    if (set_band_launch(&hp, sms, st)) continue;
+    // (equal-size items: the autotuner compares plans, the cost-weighted
+    // cut is computed once for the winner)
+    if (set_band_launch(lat, cands[i], &hp, sms, st, false)) continue;
     float ms = 0.f;
     // (warm the finalist's kernel first: the JIT compile is not timed)
     int x = 0;
@@ -679,7 +786,7 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     if ((re - r) & ((1ull << lane_span(span_bits)) - 1))
       default_lanes(&hp.lane_mask, hp.lane_vec);
     hp.hi_step = 1;
-    rc = set_band_launch(&hp, sms, st);
+    rc = set_band_launch(lat, info, &hp, sms, st);
     if (rc) return rc;
     int x = 0;
     if (use_jit) {

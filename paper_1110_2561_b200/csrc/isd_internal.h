@@ -149,6 +149,12 @@ int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint);
 bool mutate_lanes(const isd_lattice* lat, int run_bits, uint64_t* seed,
                   isd_plan_info* info);
 void fill_canon(const isd_lattice* lat, CanonParams* p);
+// expected shared wavefronts per RED of a banded launch per segment of its
+// slot order (the cost of an item, plan.cpp)
+void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
+                    uint64_t run_begin, uint64_t lane_mask,
+                    const uint64_t* lane_vec, int run_bits, int n_seg,
+                    int samples, std::vector<double>* cost);
 void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
                 HoistParams* p);
 

@@ -535,8 +535,7 @@ __device__ __forceinline__ void k1_hoisted_body(
 #ifdef ISD_PROBE
       // (probe build) per item: first chunk start, this warp's end, last
       // warp's end, flush end, relative to the item start (SM cycles)
-      if ((threadIdx.x & 31) == 0 && blockIdx.x < 4 &&
-          (warp == 0 || warp == 31))
+      if (threadIdx.x == 0)
         printf("ISDPROBE blk %u item %u q0 %u slots %u warp %u first %lld "
                "done %lld walk %lld stage1 %lld flush %lld\n", blockIdx.x, it,
                item.q0, (unsigned)(item.g1 - item.g0), warp,

@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <cstring>
 #include <vector>
+#include <atomic>
+#include <thread>
 
 #include "isd_internal.h"
 
@@ -1013,6 +1015,118 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
       p->koff[c] += (int)p->pair_bytes[i] * u;
     }
   }
+}
+
+}  // namespace isd
+
+namespace isd {
+
+// Expected shared-memory wavefronts per RED of a banded mode-2 launch, per
+// segment of its slots: the 2^F values of the F non-pivot run bits in
+// (popcount, colex) order — the kernel's slot order — cut into n_seg equal
+// ranges.  The walk is wavefront-bound (ncu: pipe ~95% busy), so this is
+// its cost per slot up to a constant: measured cycles per slot / (1024 x
+// this) stayed within ~2% over the c5 walk (ISD_PROBE).  Items cut to equal
+// total cost then finish together.  Cost varies with the popcount class
+// (how far the lanes' bins spread) and, within a class, with which sites
+// are up, hence segments rather than classes.  Fixed seed: the same plan
+// gives the same cuts.  Per segment, `samples` warp REDs of a random slot
+// in it, loop subset and unpaired copy: the 32 lanes' words (m, e, pattern
+// planes) counted per bank.
+void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
+                    uint64_t run_begin, uint64_t lane_mask,
+                    const uint64_t* lane_vec, int run_bits, int n_seg,
+                    int samples, std::vector<double>* cost) {
+  const int k = (int)info.k;
+  const uint64_t free_mask =
+      ((run_bits >= 64) ? ~0ull : ((1ull << run_bits) - 1)) & ~lane_mask;
+  const int F = popc64(free_mask);
+  const uint64_t total = 1ull << F;
+  if (n_seg < 1) n_seg = 1;
+  if ((uint64_t)n_seg > total) n_seg = (int)total;
+  cost->assign((size_t)n_seg, 1.0);
+  // binomials C(n, j), n, j <= F
+  std::vector<uint64_t> C((size_t)(F + 1) * (F + 1), 0);
+  for (int n = 0; n <= F; ++n)
+    for (int j = 0; j <= n; ++j)
+      C[(size_t)n * (F + 1) + j] =
+          (j == 0 || j == n) ? 1
+                             : C[(size_t)(n - 1) * (F + 1) + j - 1] +
+                                   C[(size_t)(n - 1) * (F + 1) + j];
+  auto binom = [&](int n, int j) -> uint64_t {
+    return (j < 0 || j > n) ? 0 : C[(size_t)n * (F + 1) + j];
+  };
+  auto unrank = [&](uint64_t g) {  // k1_body.cuh isd_unrank
+    int q = 0;
+    while (q < F && g >= binom(F, q)) g -= binom(F, q++);
+    uint64_t v = 0;
+    for (int bit = F - 1; bit >= 0 && q > 0; --bit)
+      if (g >= binom(bit, q)) {
+        v |= 1ull << bit;
+        g -= binom(bit, q--);
+      }
+    return v;
+  };
+  uint64_t dep[32];
+  for (int lane = 0; lane < 32; ++lane) {
+    dep[lane] = 0;
+    for (int i = 0; i < 5; ++i)
+      if ((lane >> i) & 1) dep[lane] ^= lane_vec[i];
+  }
+  const uint64_t p0bit = 1ull << info.copy_site[kCopyBits - 1];
+  const uint64_t p1bit = 1ull << info.copy_site[kCopyBits - 2];
+  const int d0 = (int)info.pair_degree[0], d1 = (int)info.pair_degree[1];
+  const int unpaired = kCopyBits - 2;
+  // segments are independent (each with its own seed): spread them over
+  // the host's cores
+  auto run_segment = [&](int sg) {
+    uint64_t seed = 0x5851F42D4C957F2Dull ^ (0x9E3779B97F4A7C15ull * (sg + 1));
+    const uint64_t g0 = total * (uint64_t)sg / (uint64_t)n_seg;
+    const uint64_t g1 = total * (uint64_t)(sg + 1) / (uint64_t)n_seg;
+    double tot = 0;
+    for (int s = 0; s < samples; ++s) {
+      const uint64_t slot =
+          deposit(unrank(g0 + rng_next(&seed) % (g1 - g0)), free_mask);
+      const uint64_t jb = deposit(rng_next(&seed), info.loop_mask);
+      uint64_t cb = 0;
+      const uint64_t c = rng_next(&seed);
+      for (int t = 0; t < unpaired; ++t)
+        if ((c >> t) & 1) cb |= 1ull << info.copy_site[t];
+      int64_t words[32];
+      for (int lane = 0; lane < 32; ++lane) {
+        const uint64_t run = run_begin + (slot ^ dep[lane]);
+        const uint64_t x = (run << k) | jb | cb;  // paired sites down
+        const int e = energy_of(lat, x);
+        const int p0 = (d0 - (energy_of(lat, x | p0bit) - e)) / 2;
+        const int p1 = (d1 - (energy_of(lat, x | p1bit) - e)) / 2;
+        const int eh = info.e_mode ? (e - (e & 1)) / 2 : e;
+        const int par = info.e_mode ? (e & 1) : 0;
+        words[lane] = (int64_t)popc64(x) * info.row_words +
+                      (int64_t)eh * info.e_words + par * info.plane_words +
+                      (int64_t)p0 * info.pair_words[0] +
+                      (int64_t)p1 * info.pair_words[1];
+      }
+      std::sort(words, words + 32);
+      int per_bank[32] = {0};
+      int worst = 0;
+      for (int i = 0; i < 32; ++i)
+        if (i == 0 || words[i] != words[i - 1]) {
+          const int b = (int)(((words[i] % 32) + 32) % 32);
+          worst = std::max(worst, ++per_bank[b]);
+        }
+      tot += worst;
+    }
+    (*cost)[(size_t)sg] = tot / samples;
+  };
+  unsigned nt = std::thread::hardware_concurrency();
+  nt = nt < 1 ? 1 : (nt > 32 ? 32 : nt);
+  std::atomic<int> next{0};
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < nt; ++t)
+    pool.emplace_back([&] {
+      for (int sg; (sg = next.fetch_add(1)) < n_seg;) run_segment(sg);
+    });
+  for (auto& th : pool) th.join();
 }
 
 }  // namespace isd
