@@ -152,23 +152,27 @@ struct PlanEntry {
 static std::mutex g_plan_mu;
 static std::map<std::string, PlanEntry> g_plans;
 
-static std::string plan_key(const isd_lattice* lat, uint64_t hint) {
+// top: the configuration bits a walk holds fixed (a shard of an aligned
+// power-of-two split: its start), which the layout model includes
+static std::string plan_key(const isd_lattice* lat, uint64_t hint,
+                            uint64_t top = 0) {
   const int l = plan_loop_bits(lat, hint);
   std::string key(reinterpret_cast<const char*>(lat), sizeof(*lat));
   key.push_back((char)l);
+  key += "|top" + std::to_string(top);
   if (const char* v = std::getenv("ISD_COPY_VARIANT")) key += v;
   if (const char* v = std::getenv("ISD_PAIR")) key += std::string("|pair") + v;
   return key;
 }
 
 static int cached_plan(const isd_lattice* lat, uint64_t hint,
-                       isd_plan_info* info) {
-  const std::string key = plan_key(lat, hint);
+                       isd_plan_info* info, uint64_t top = 0) {
+  const std::string key = plan_key(lat, hint, top);
   std::lock_guard<std::mutex> lock(g_plan_mu);
   auto it = g_plans.find(key);
   if (it == g_plans.end()) {
     PlanEntry fresh;
-    fresh.rc = compile_plan(lat, hint, &fresh.info, &fresh.ranked);
+    fresh.rc = compile_plan(lat, hint, &fresh.info, &fresh.ranked, top);
     it = g_plans.emplace(key, std::move(fresh)).first;
   }
   *info = it->second.info;
@@ -432,9 +436,9 @@ static constexpr uint64_t kTuneSliceConfigs = 1ull << 36;
 // each is timed on its own run range of [start, end).
 static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
                      uint64_t end, int sms, cudaStream_t st,
-                     isd_plan_info* info) {
+                     isd_plan_info* info, uint64_t top) {
   if (env_long("ISD_AUTOTUNE", 1) == 0) return;
-  const std::string key = plan_key(lat, hint);
+  const std::string key = plan_key(lat, hint, top);
   std::vector<isd_plan_info> cands;
   {
     std::lock_guard<std::mutex> lock(g_plan_mu);
@@ -616,9 +620,9 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
 // The best plan the model found without a banded table (banded plans need
 // an aligned power-of-two range).
 static bool unbanded_plan(const isd_lattice* lat, uint64_t hint,
-                          isd_plan_info* info) {
+                          isd_plan_info* info, uint64_t top) {
   std::lock_guard<std::mutex> lock(g_plan_mu);
-  auto it = g_plans.find(plan_key(lat, hint));
+  auto it = g_plans.find(plan_key(lat, hint, top));
   if (it == g_plans.end()) return false;
   const isd_plan_info* best = nullptr;
   for (const isd_plan_info& x : it->second.ranked)
@@ -715,7 +719,14 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     return rc;
   }
   isd_plan_info info;
-  const int too_small = cached_plan(lat, end - start, &info);
+  // an aligned power-of-two range (a shard) holds its top bits fixed:
+  // the layout model sees them (ISD_PLAN_TOP=0: plan as for shard 0)
+  const uint64_t len = end - start;
+  const uint64_t top = (!(len & (len - 1)) && start % len == 0 &&
+                        env_long("ISD_PLAN_TOP", 1) != 0)
+                           ? start
+                           : 0;
+  const int too_small = cached_plan(lat, len, &info, top);
   if (too_small) {
     if (algo == ISD_ALGO_HOISTED)
       return fail(ISD_EINVAL, "lattice of %u spins too small for the hoisted "
@@ -725,10 +736,10 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     return rc;
   }
   if (end - start >= kTuneConfigs)
-    autotune(lat, end - start, start, end, sms, st, &info);
+    autotune(lat, end - start, start, end, sms, st, &info, top);
   // a banded plan runs only on an aligned power-of-two range
   if (info.band_rows && !band_ok(info, start, end) &&
-      !unbanded_plan(lat, end - start, &info))
+      !unbanded_plan(lat, end - start, &info, top))
     return fail(ISD_EINVAL, "no unbanded plan for an unaligned range");
   const uint32_t k = info.k;
   const uint64_t r0 = (start + ((1ull << k) - 1)) >> k;

@@ -136,9 +136,12 @@ int validate_lattice(const isd_lattice* lat, char* err, size_t errlen);
 // use the hoisted kernel, >0 if it is too small (canonical only).
 // `ranked` (optional) receives every evaluated layout, best model estimate
 // first; the C ABI times the head of that list on the GPU (capi.cu).
+// `top`: configuration bits the walk holds fixed (a shard's start), seen by
+// the layout model.
 int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
                  isd_plan_info* info,
-                 std::vector<isd_plan_info>* ranked = nullptr);
+                 std::vector<isd_plan_info>* ranked = nullptr,
+                 uint64_t top = 0);
 // run-bit count spanned by a lane mask (runs of a walk must be a multiple
 // of 2^lane_span(mask) for that placement to tile the walk)
 int lane_span(uint64_t lane_mask);

@@ -291,7 +291,8 @@ static int pair_policy() {
 static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
                           std::vector<isd_plan_info>* ranked, bool wide,
                           int walk_bits, bool climb, int band_rows = 0,
-                          int band_span = kBandSpan, bool band_domino = false) {
+                          int band_span = kBandSpan, bool band_domino = false,
+                          uint64_t top = 0) {
   // banded tables: lanes flip single sites (lane m span 5), or with
   // band_domino also a neighbour of the pivot (span 10; rows sized for it)
   const bool single_site = band_rows > 0 && !band_domino;
@@ -451,7 +452,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
         int nb[3] = {0, 0, 0};
         for (int lane = 0; lane < 32; ++lane) {
           const uint64_t r = hi ^ lane_dep[lane];
-          const uint64_t x = (r << k) | jb | cbits;
+          const uint64_t x = (r << k) | jb | cbits | top;
           for (int mode = 0; mode < 3; ++mode) {
             const uint64_t xs = mode == 0 ? x
                                 : mode == 1 ? x & ~pbit[0]
@@ -672,7 +673,8 @@ static void set_copy_sites(const isd_lattice* lat, isd_plan_info* info,
 }
 
 int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
-                 isd_plan_info* info, std::vector<isd_plan_info>* ranked) {
+                 isd_plan_info* info, std::vector<isd_plan_info>* ranked,
+                 uint64_t top) {
   std::memset(info, 0, sizeof(*info));
   const int n = (int)lat->n_spins;
   const int u = kCopyBits;
@@ -786,7 +788,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
     for (int site : set) all_even = all_even && !((odd >> site) & 1);
     set_copy_sites(lat, &cand, set.data(), all_even ? 1 : 0);
     choose_layout(lat, &cand, &all, wide, walk_bits, climb, band_rows,
-                  band_span, band_domino);
+                  band_span, band_domino, top);
     if (cand.est_per_config >= 1e29) return;  // no layout of that kind
     if (!have || cand.est_per_config < best_info.est_per_config - 1e-9) {
       best_info = cand;
