@@ -825,7 +825,8 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
       const bool domino = shape == 1;
       if ((domino && domino_knob == 0) || (!domino && domino_knob == 2))
         continue;
-      const int span = domino ? 0 : kBandSpan;
+      const int span =
+          domino ? 0 : (int)env_int("ISD_BAND_SPAN", kBandSpan);  // (knob)
       const int lb = (int)std::min<long>(
           env_int(domino ? "ISD_BAND_DOMINO_LOOP_BITS" : "ISD_BAND_LOOP_BITS",
                   domino ? 4 : 5),
