@@ -202,7 +202,9 @@ static bool band_ok(const isd_plan_info& info, uint64_t start, uint64_t end) {
 // w[j] (expected wavefronts per RED, band_slot_cost; empty w: equal costs),
 // so items where the lanes' bins spread over more banks hold fewer slots.
 static std::vector<BandItem> build_band_items(int F, int n_target, int span,
-                                              const std::vector<double>& w) {
+                                              const std::vector<double>& w,
+                                              double flush_units, bool* exact) {
+  *exact = false;
   std::vector<uint64_t> cum(F + 2, 0);  // cum[q] = slots of popcount < q
   uint64_t c = 1;
   for (int q = 0; q <= F; ++q) {
@@ -212,29 +214,91 @@ static std::vector<BandItem> build_band_items(int F, int n_target, int span,
   const uint64_t total = cum[F + 1];
   const uint64_t n_seg = w.empty() ? 1 : (uint64_t)w.size();
   auto seg_lo = [&](uint64_t j) { return total * j / n_seg; };
-  double total_w = 0;
-  for (uint64_t j = 0; j < n_seg; ++j)
-    total_w += (double)(seg_lo(j + 1) - seg_lo(j)) * (w.empty() ? 1.0 : w[j]);
-  const double target = total_w / (n_target > 0 ? n_target : 1);
-  std::vector<BandItem> items;
-  uint64_t g = 0, j = 0;
-  int q = 0;
-  while (g < total) {
-    while (cum[q + 1] <= g) ++q;
-    const uint64_t limit = cum[std::min(F, q + span) + 1];
-    const uint64_t g0 = g;
-    double budget = target;
-    while (g < limit && budget > 0) {
-      while (seg_lo(j + 1) <= g) ++j;
-      const double wj = w.empty() ? 1.0 : std::max(w[j], 1e-3);
-      const uint64_t room = std::min(limit, seg_lo(j + 1)) - g;
-      uint64_t take = (uint64_t)std::ceil(budget / wj - 1e-9);
-      take = std::max<uint64_t>(1, std::min(take, room));
-      g += take;
-      budget -= (double)take * wj;
+  auto wseg = [&](uint64_t j) { return w.empty() ? 1.0 : std::max(w[j], 1e-3); };
+  // cost of the slots [a, b)
+  auto cost = [&](uint64_t a, uint64_t b) {
+    double x = 0;
+    for (uint64_t j = a * n_seg / total; j < n_seg && seg_lo(j) < b; ++j) {
+      const uint64_t lo = std::max(a, seg_lo(j)), hi = std::min(b, seg_lo(j + 1));
+      if (hi > lo) x += (double)(hi - lo) * wseg(j);
     }
-    items.push_back(BandItem{g0, g, (unsigned)q, 0u});
+    return x;
+  };
+  // cut [g, end) into items: item k gets budget target(k) (the last one
+  // runs to `end`), each capped at span + 1 popcount classes
+  auto cut = [&](uint64_t g, uint64_t end, int n_items, auto target,
+                 std::vector<BandItem>* out) {
+    uint64_t j = g * n_seg / total;
+    int q = 0;
+    for (int k = 0; g < end; ++k) {
+      while (cum[q + 1] <= g) ++q;
+      const uint64_t limit = std::min(end, cum[std::min(F, q + span) + 1]);
+      const uint64_t g0 = g;
+      double budget = k >= n_items - 1 ? 1e300 : target(k);
+      while (g < limit && budget > 0) {
+        while (seg_lo(j + 1) <= g) ++j;
+        const double wj = wseg(j);
+        const uint64_t room = std::min(limit, seg_lo(j + 1)) - g;
+        uint64_t take = budget > 1e200 ? room
+                                       : (uint64_t)std::ceil(budget / wj - 1e-9);
+        take = std::max<uint64_t>(1, std::min(take, room));
+        g += take;
+        budget -= (double)take * wj;
+      }
+      out->push_back(BandItem{g0, g, (unsigned)q, 0u});
+    }
+  };
+  const double total_w = cost(0, total);
+  const double T = total_w / (n_target > 0 ? n_target : 1);
+  std::vector<BandItem> plain;
+  cut(0, total, 1 << 30, [&](int) { return T; }, &plain);
+  // The extreme popcount classes [0, cum[span + 1]) and [cum[F - span],
+  // 2^F) hold few slots, and an item may not reach past them: alone they
+  // would leave their blocks idle.  They become second items of blocks 0
+  // and 1, whose first items are shortened by their cost plus a flush
+  // (flush_units: ~20 K SM cycles in slot-walk units, ISD_PROBE), and the
+  // rest is cut into exactly n_target items of equal cost (block b walks
+  // item b).
+  const uint64_t lo_end = cum[std::min(F, span) + 1];
+  const uint64_t hi_start = cum[std::max(0, F - span)];
+  if (n_target < 3 || hi_start <= lo_end) {
+    *exact = (int)plain.size() == n_target;
+    return plain;
   }
+  const double c_lo = cost(0, lo_end), c_hi = cost(hi_start, total);
+  const bool s_lo = c_lo < 0.5 * T, s_hi = c_hi < 0.5 * T;
+  if (!s_lo && !s_hi) {
+    *exact = (int)plain.size() == n_target;
+    return plain;
+  }
+  const double f = flush_units;
+  std::vector<BandItem> smalls;
+  std::vector<double> small_cost;
+  if (s_lo) {
+    smalls.push_back(BandItem{0, lo_end, 0u, 0u});
+    small_cost.push_back(c_lo);
+  }
+  if (s_hi) {
+    smalls.push_back(BandItem{hi_start, total, (unsigned)(F - span), 0u});
+    small_cost.push_back(c_hi);
+  }
+  const uint64_t mid_lo = s_lo ? lo_end : 0, mid_hi = s_hi ? hi_start : total;
+  double T2 = cost(mid_lo, mid_hi);
+  for (double x : small_cost) T2 += x + f;
+  T2 /= n_target;
+  std::vector<BandItem> items;
+  cut(mid_lo, mid_hi, n_target,
+      [&](int k) {
+        return k < (int)small_cost.size() ? T2 - small_cost[(size_t)k] - f
+                                          : T2;
+      },
+      &items);
+  if ((int)items.size() != n_target) {
+    *exact = (int)plain.size() == n_target;
+    return plain;
+  }
+  items.insert(items.end(), smalls.begin(), smalls.end());
+  *exact = true;
   return items;
 }
 
@@ -245,12 +309,13 @@ static std::map<std::string, std::pair<BandItem*, uint32_t>> g_items;
 // curve; `cost_key` identifies w).
 static int band_items(int F, int n_target, int span,
                       const std::vector<double>& w, const std::string& cost_key,
-                      BandItem** ptr, uint32_t* count) {
+                      double flush_units, BandItem** ptr, uint32_t* count) {
   int dev = 0;
   cudaGetDevice(&dev);
   const std::string key = std::to_string(dev) + ":" + std::to_string(F) +
                           ":" + std::to_string(n_target) + ":" +
-                          std::to_string(span) + ":" + cost_key;
+                          std::to_string(span) + ":" + cost_key + ":" +
+                          std::to_string((int)flush_units);
   std::lock_guard<std::mutex> lock(g_items_mu);
   auto it = g_items.find(key);
   if (it == g_items.end()) {
@@ -258,20 +323,46 @@ static int band_items(int F, int n_target, int span,
     if (F > 23) return fail(ISD_EINVAL, "banded launch: too many slot bits");
     // the class-boundary cuts add a few small items: shrink the target so
     // the count stays a whole number of waves (blocks get equal work)
-    std::vector<BandItem> host = build_band_items(F, n_target, span, w);
-    for (int goal = n_target; (int)host.size() > n_target && goal > 1;) {
+    // (exact: n_target items, block b walks item b, plus the small items
+    // of the extreme classes as second items of blocks 0 and 1; otherwise
+    // the target is shrunk until the count is a whole number of waves)
+    bool exact = false;
+    std::vector<BandItem> host =
+        build_band_items(F, n_target, span, w, flush_units, &exact);
+    for (int goal = n_target; !exact && (int)host.size() > n_target && goal > 1;) {
       goal -= (int)host.size() - n_target;
-      host = build_band_items(F, goal < 1 ? 1 : goal, span, w);
+      bool ignored = false;
+      host = build_band_items(F, goal < 1 ? 1 : goal, span, w, flush_units,
+                              &ignored);
     }
-    // the items must tile [0, 2^F) in order
-    uint64_t next = 0;
-    for (const BandItem& x : host) {
-      if (x.g0 != next || x.g1 <= x.g0)
+    // the items must tile [0, 2^F) (listed in any order), each within
+    // span + 1 popcount classes of its q0
+    {
+      std::vector<BandItem> r(host);
+      std::sort(r.begin(), r.end(), [](const BandItem& a, const BandItem& b) {
+        return a.g0 < b.g0;
+      });
+      std::vector<uint64_t> cum(F + 2, 0);
+      uint64_t c = 1;
+      for (int q = 0; q <= F; ++q) {
+        cum[q + 1] = cum[q] + c;
+        c = c * (uint64_t)(F - q) / (uint64_t)(q + 1);
+      }
+      auto cls = [&](uint64_t g) {
+        int q = 0;
+        while (cum[q + 1] <= g) ++q;
+        return q;
+      };
+      uint64_t next = 0;
+      for (const BandItem& x : r) {
+        if (x.g0 != next || x.g1 <= x.g0 || cls(x.g0) != (int)x.q0 ||
+            cls(x.g1 - 1) > (int)x.q0 + span)
+          return fail(ISD_EINVAL, "band work items do not tile the slots");
+        next = x.g1;
+      }
+      if (next != (1ull << F))
         return fail(ISD_EINVAL, "band work items do not tile the slots");
-      next = x.g1;
     }
-    if (next != (1ull << F))
-      return fail(ISD_EINVAL, "band work items do not tile the slots");
     const size_t item_bytes = host.size() * sizeof(BandItem);
     BandItem* d = nullptr;
     cudaError_t e = cudaMalloc(&d, item_bytes);
@@ -408,9 +499,12 @@ static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
   std::string cost_key;
   if (weighted) band_costs(lat, info, *hp, rb, &w, &cost_key);
   static const std::vector<double> equal;
+  // a flush (~20 K SM cycles) in units of one slot's walk at one wavefront
+  // per RED (a slot = 32 lanes x 2^l loop subsets x 32 REDs / 32 lanes)
+  const double flush_units = 20000.0 / (double)(32u << hp->l);
   const int rc = band_items(F, (per_sm < 1 ? 1 : per_sm) * sms,
                             (int)hp->band_span, w ? *w : equal, cost_key,
-                            &items, &count);
+                            flush_units, &items, &count);
   if (rc) return rc;
   hp->band_free_bits = (uint32_t)(rb - 5);
   hp->band_items = (uint64_t)(uintptr_t)items;
