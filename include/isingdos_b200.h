@@ -201,6 +201,18 @@ int isd_jit_check(const isd_lattice* lat, uint64_t n_configs_hint,
 /* Validate a lattice descriptor without touching a GPU. */
 int isd_validate(const isd_lattice* lat);
 
+/* The host's work-item split of a banded launch over 2^free_bits slots (no
+ * GPU needed; for tests): n_target items of equal cost under the per-slot
+ * costs seg_cost[0 .. n_seg) (the slots cut into n_seg equal segments in
+ * popcount order; n_seg = 0: equal costs), each spanning at most span + 1
+ * popcount classes, plus the small items of the extreme classes.  Writes
+ * (g0, g1, q0) per item to out (3 x max_items) and the count to *n_items;
+ * *exact = 1 when item b is block b's first item. */
+int isd_band_items(uint32_t free_bits, uint32_t n_target, uint32_t span,
+                   const double* seg_cost, uint32_t n_seg, double flush_units,
+                   uint64_t* out, uint32_t max_items, uint32_t* n_items,
+                   int* exact);
+
 /* ---- calibration microbenchmarks (K0) -------------------------------- */
 /* which: 0 = POPC, 1 = LOP3, 2 = IADD3, 3 = RED.shared spread,
  *        4 = RED.shared realistic bins, 5 = IMAD, 6 = SHF, 7 = RED.shared

@@ -28,7 +28,7 @@ EXPORTED_SYMBOLS = (
     "isd_plan", "isd_validate", "isd_calibrate", "isd_device_count",
     "isd_sm_count", "isd_last_error", "isd_version", "isd_abi_version",
     "isd_launch_count", "isd_mirror_async", "isd_kernel_info",
-    "isd_jit_check",
+    "isd_jit_check", "isd_band_items",
 )
 
 
@@ -119,6 +119,11 @@ def load():
         lib.isd_kernel_info.restype = ctypes.c_char_p
         lib.isd_jit_check.argtypes = [p_lat, u64, ctypes.POINTER(ctypes.c_uint64)]
         lib.isd_jit_check.restype = ctypes.c_int
+        lib.isd_band_items.argtypes = [
+            ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, vp,
+            ctypes.c_uint32, dbl, vp, ctypes.c_uint32,
+            ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int)]
+        lib.isd_band_items.restype = ctypes.c_int
         lib.isd_launch_count.restype = ctypes.c_uint64
         for name in ("isd_enumerate", "isd_enumerate_async", "isd_thermo",
                      "isd_thermo_async", "isd_plan", "isd_validate",
@@ -276,3 +281,22 @@ def jit_check(lat: Lattice, n_configs_hint: int) -> int:
     check(load().isd_jit_check(ctypes.byref(lat), n_configs_hint,
                                ctypes.byref(n)))
     return n.value
+
+
+def band_items(free_bits: int, n_target: int, span: int, seg_cost=None,
+               flush_units: float = 20.0):
+    """The host's work-item split of a banded launch (no GPU; for tests):
+    (array[n, 3] of (g0, g1, q0), exact)."""
+    lib = load()
+    w = (np.ascontiguousarray(seg_cost, dtype=np.float64)
+         if seg_cost is not None else np.zeros(0))
+    cap = 4 * n_target + 64
+    out = np.zeros(3 * cap, dtype=np.uint64)
+    n = ctypes.c_uint32(0)
+    ex = ctypes.c_int(0)
+    check(lib.isd_band_items(free_bits, n_target, span,
+                             w.ctypes.data if len(w) else None, len(w),
+                             float(flush_units), out.ctypes.data, cap,
+                             ctypes.byref(n), ctypes.byref(ex)))
+    return out[:3 * n.value].reshape(-1, 3).astype(np.int64), bool(ex.value)
+

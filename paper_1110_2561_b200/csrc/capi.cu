@@ -196,112 +196,6 @@ static bool band_ok(const isd_plan_info& info, uint64_t start, uint64_t end) {
   return rb >= 6 && lane_span(span_bits) <= rb;
 }
 
-// Work items of a launch over 2^F slots (popcount order): ~n_target items of
-// equal cost, cut so that each spans at most span + 1 popcount classes.  The
-// slots are cut into w.size() equal segments and a slot of segment j costs
-// w[j] (expected wavefronts per RED, band_slot_cost; empty w: equal costs),
-// so items where the lanes' bins spread over more banks hold fewer slots.
-static std::vector<BandItem> build_band_items(int F, int n_target, int span,
-                                              const std::vector<double>& w,
-                                              double flush_units, bool* exact) {
-  *exact = false;
-  std::vector<uint64_t> cum(F + 2, 0);  // cum[q] = slots of popcount < q
-  uint64_t c = 1;
-  for (int q = 0; q <= F; ++q) {
-    cum[q + 1] = cum[q] + c;
-    c = c * (uint64_t)(F - q) / (uint64_t)(q + 1);
-  }
-  const uint64_t total = cum[F + 1];
-  const uint64_t n_seg = w.empty() ? 1 : (uint64_t)w.size();
-  auto seg_lo = [&](uint64_t j) { return total * j / n_seg; };
-  auto wseg = [&](uint64_t j) { return w.empty() ? 1.0 : std::max(w[j], 1e-3); };
-  // cost of the slots [a, b)
-  auto cost = [&](uint64_t a, uint64_t b) {
-    double x = 0;
-    for (uint64_t j = a * n_seg / total; j < n_seg && seg_lo(j) < b; ++j) {
-      const uint64_t lo = std::max(a, seg_lo(j)), hi = std::min(b, seg_lo(j + 1));
-      if (hi > lo) x += (double)(hi - lo) * wseg(j);
-    }
-    return x;
-  };
-  // cut [g, end) into items: item k gets budget target(k) (the last one
-  // runs to `end`), each capped at span + 1 popcount classes
-  auto cut = [&](uint64_t g, uint64_t end, int n_items, auto target,
-                 std::vector<BandItem>* out) {
-    uint64_t j = g * n_seg / total;
-    int q = 0;
-    for (int k = 0; g < end; ++k) {
-      while (cum[q + 1] <= g) ++q;
-      const uint64_t limit = std::min(end, cum[std::min(F, q + span) + 1]);
-      const uint64_t g0 = g;
-      double budget = k >= n_items - 1 ? 1e300 : target(k);
-      while (g < limit && budget > 0) {
-        while (seg_lo(j + 1) <= g) ++j;
-        const double wj = wseg(j);
-        const uint64_t room = std::min(limit, seg_lo(j + 1)) - g;
-        uint64_t take = budget > 1e200 ? room
-                                       : (uint64_t)std::ceil(budget / wj - 1e-9);
-        take = std::max<uint64_t>(1, std::min(take, room));
-        g += take;
-        budget -= (double)take * wj;
-      }
-      out->push_back(BandItem{g0, g, (unsigned)q, 0u});
-    }
-  };
-  const double total_w = cost(0, total);
-  const double T = total_w / (n_target > 0 ? n_target : 1);
-  std::vector<BandItem> plain;
-  cut(0, total, 1 << 30, [&](int) { return T; }, &plain);
-  // The extreme popcount classes [0, cum[span + 1]) and [cum[F - span],
-  // 2^F) hold few slots, and an item may not reach past them: alone they
-  // would leave their blocks idle.  They become second items of blocks 0
-  // and 1, whose first items are shortened by their cost plus a flush
-  // (flush_units: ~20 K SM cycles in slot-walk units, ISD_PROBE), and the
-  // rest is cut into exactly n_target items of equal cost (block b walks
-  // item b).
-  const uint64_t lo_end = cum[std::min(F, span) + 1];
-  const uint64_t hi_start = cum[std::max(0, F - span)];
-  if (n_target < 3 || hi_start <= lo_end) {
-    *exact = (int)plain.size() == n_target;
-    return plain;
-  }
-  const double c_lo = cost(0, lo_end), c_hi = cost(hi_start, total);
-  const bool s_lo = c_lo < 0.5 * T, s_hi = c_hi < 0.5 * T;
-  if (!s_lo && !s_hi) {
-    *exact = (int)plain.size() == n_target;
-    return plain;
-  }
-  const double f = flush_units;
-  std::vector<BandItem> smalls;
-  std::vector<double> small_cost;
-  if (s_lo) {
-    smalls.push_back(BandItem{0, lo_end, 0u, 0u});
-    small_cost.push_back(c_lo);
-  }
-  if (s_hi) {
-    smalls.push_back(BandItem{hi_start, total, (unsigned)(F - span), 0u});
-    small_cost.push_back(c_hi);
-  }
-  const uint64_t mid_lo = s_lo ? lo_end : 0, mid_hi = s_hi ? hi_start : total;
-  double T2 = cost(mid_lo, mid_hi);
-  for (double x : small_cost) T2 += x + f;
-  T2 /= n_target;
-  std::vector<BandItem> items;
-  cut(mid_lo, mid_hi, n_target,
-      [&](int k) {
-        return k < (int)small_cost.size() ? T2 - small_cost[(size_t)k] - f
-                                          : T2;
-      },
-      &items);
-  if ((int)items.size() != n_target) {
-    *exact = (int)plain.size() == n_target;
-    return plain;
-  }
-  items.insert(items.end(), smalls.begin(), smalls.end());
-  *exact = true;
-  return items;
-}
-
 static std::mutex g_items_mu;
 static std::map<std::string, std::pair<BandItem*, uint32_t>> g_items;
 
@@ -328,12 +222,12 @@ static int band_items(int F, int n_target, int span,
     // the target is shrunk until the count is a whole number of waves)
     bool exact = false;
     std::vector<BandItem> host =
-        build_band_items(F, n_target, span, w, flush_units, &exact);
+        band_work_items(F, n_target, span, w, flush_units, &exact);
     for (int goal = n_target; !exact && (int)host.size() > n_target && goal > 1;) {
       goal -= (int)host.size() - n_target;
       bool ignored = false;
-      host = build_band_items(F, goal < 1 ? 1 : goal, span, w, flush_units,
-                              &ignored);
+      host = band_work_items(F, goal < 1 ? 1 : goal, span, w, flush_units,
+                             &ignored);
     }
     // the items must tile [0, 2^F) (listed in any order), each within
     // span + 1 popcount classes of its q0
@@ -935,6 +829,29 @@ int isd_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   if (rc) return rc;
   if (!out) return fail(ISD_EINVAL, "plan pointer is NULL");
   return cached_plan(lat, n_configs_hint, out);
+}
+
+int isd_band_items(uint32_t free_bits, uint32_t n_target, uint32_t span,
+                   const double* seg_cost, uint32_t n_seg, double flush_units,
+                   uint64_t* out, uint32_t max_items, uint32_t* n_items,
+                   int* exact) {
+  if (free_bits < 1 || free_bits > 23 || n_target < 1 || span > 8 ||
+      (n_seg && !seg_cost) || !out || !n_items || !exact)
+    return fail(ISD_EINVAL, "bad band item arguments");
+  std::vector<double> w;
+  if (n_seg) w.assign(seg_cost, seg_cost + n_seg);
+  bool ex = false;
+  const std::vector<BandItem> items = band_work_items(
+      (int)free_bits, (int)n_target, (int)span, w, flush_units, &ex);
+  if (items.size() > max_items) return fail(ISD_EINVAL, "out too small");
+  for (size_t i = 0; i < items.size(); ++i) {
+    out[3 * i] = items[i].g0;
+    out[3 * i + 1] = items[i].g1;
+    out[3 * i + 2] = items[i].q0;
+  }
+  *n_items = (uint32_t)items.size();
+  *exact = ex ? 1 : 0;
+  return ISD_OK;
 }
 
 int isd_jit_check(const isd_lattice* lat, uint64_t n_configs_hint,

@@ -152,6 +152,10 @@ int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint);
 bool mutate_lanes(const isd_lattice* lat, int run_bits, uint64_t* seed,
                   isd_plan_info* info);
 void fill_canon(const isd_lattice* lat, CanonParams* p);
+// work items of a banded launch over 2^F slots (plan.cpp; see there)
+std::vector<BandItem> band_work_items(int F, int n_target, int span,
+                                      const std::vector<double>& w,
+                                      double flush_units, bool* exact);
 // expected shared wavefronts per RED of a banded launch per segment of its
 // slot order (the cost of an item, plan.cpp)
 void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,

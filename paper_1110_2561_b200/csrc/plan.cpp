@@ -4,6 +4,7 @@
 // turns it into the parameter blocks of the two enumeration kernels.  The
 // semantic contract is the reference's: m_idx = popcount(index) and e_idx =
 // number of unsatisfied bonds (enumeration.py:95-121, 184-204, 232-233).
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -1130,6 +1131,114 @@ void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
       for (int sg; (sg = next.fetch_add(1)) < n_seg;) run_segment(sg);
     });
   for (auto& th : pool) th.join();
+}
+
+// Work items of a launch over 2^F slots (popcount order): ~n_target items of
+// equal cost, cut so that each spans at most span + 1 popcount classes.  The
+// slots are cut into w.size() equal segments and a slot of segment j costs
+// w[j] (expected wavefronts per RED, band_slot_cost; empty w: equal costs),
+// so items where the lanes' bins spread over more banks hold fewer slots.
+std::vector<BandItem> band_work_items(int F, int n_target, int span,
+                                      const std::vector<double>& w,
+                                      double flush_units, bool* exact) {
+  *exact = false;
+  std::vector<uint64_t> cum(F + 2, 0);  // cum[q] = slots of popcount < q
+  uint64_t c = 1;
+  for (int q = 0; q <= F; ++q) {
+    cum[q + 1] = cum[q] + c;
+    c = c * (uint64_t)(F - q) / (uint64_t)(q + 1);
+  }
+  const uint64_t total = cum[F + 1];
+  const uint64_t n_seg = w.empty() ? 1 : (uint64_t)w.size();
+  auto seg_lo = [&](uint64_t j) { return total * j / n_seg; };
+  auto wseg = [&](uint64_t j) { return w.empty() ? 1.0 : std::max(w[j], 1e-3); };
+  // cost of the slots [a, b)
+  auto cost = [&](uint64_t a, uint64_t b) {
+    double x = 0;
+    for (uint64_t j = a * n_seg / total; j < n_seg && seg_lo(j) < b; ++j) {
+      const uint64_t lo = std::max(a, seg_lo(j)), hi = std::min(b, seg_lo(j + 1));
+      if (hi > lo) x += (double)(hi - lo) * wseg(j);
+    }
+    return x;
+  };
+  // cut [g, end) into items: item k gets budget target(k) (the last one
+  // runs to `end`), each capped at span + 1 popcount classes
+  auto cut = [&](uint64_t g, uint64_t end, int n_items, auto target,
+                 std::vector<BandItem>* out) {
+    uint64_t j = g * n_seg / total;
+    int q = 0;
+    double carry = 0;  // overshoot of the previous item (whole slots)
+    for (int k = 0; g < end; ++k) {
+      while (cum[q + 1] <= g) ++q;
+      const uint64_t limit = std::min(end, cum[std::min(F, q + span) + 1]);
+      const uint64_t g0 = g;
+      double budget = k >= n_items - 1 ? 1e300 : target(k) + carry;
+      while (g < limit && budget > 0) {
+        while (seg_lo(j + 1) <= g) ++j;
+        const double wj = wseg(j);
+        const uint64_t room = std::min(limit, seg_lo(j + 1)) - g;
+        uint64_t take = budget > 1e200 ? room
+                                       : (uint64_t)std::ceil(budget / wj - 1e-9);
+        take = std::max<uint64_t>(1, std::min(take, room));
+        g += take;
+        budget -= (double)take * wj;
+      }
+      carry = budget < 0 && budget > -1e200 ? budget : 0;
+      out->push_back(BandItem{g0, g, (unsigned)q, 0u});
+    }
+  };
+  const double total_w = cost(0, total);
+  const double T = total_w / (n_target > 0 ? n_target : 1);
+  std::vector<BandItem> plain;
+  cut(0, total, 1 << 30, [&](int) { return T; }, &plain);
+  // The extreme popcount classes [0, cum[span + 1]) and [cum[F - span],
+  // 2^F) hold few slots, and an item may not reach past them: alone they
+  // would leave their blocks idle.  They become second items of blocks 0
+  // and 1, whose first items are shortened by their cost plus a flush
+  // (flush_units: ~20 K SM cycles in slot-walk units, ISD_PROBE), and the
+  // rest is cut into exactly n_target items of equal cost (block b walks
+  // item b).
+  const uint64_t lo_end = cum[std::min(F, span) + 1];
+  const uint64_t hi_start = cum[std::max(0, F - span)];
+  if (n_target < 3 || hi_start <= lo_end) {
+    *exact = (int)plain.size() == n_target;
+    return plain;
+  }
+  const double c_lo = cost(0, lo_end), c_hi = cost(hi_start, total);
+  const bool s_lo = c_lo < 0.5 * T, s_hi = c_hi < 0.5 * T;
+  if (!s_lo && !s_hi) {
+    *exact = (int)plain.size() == n_target;
+    return plain;
+  }
+  const double f = flush_units;
+  std::vector<BandItem> smalls;
+  std::vector<double> small_cost;
+  if (s_lo) {
+    smalls.push_back(BandItem{0, lo_end, 0u, 0u});
+    small_cost.push_back(c_lo);
+  }
+  if (s_hi) {
+    smalls.push_back(BandItem{hi_start, total, (unsigned)(F - span), 0u});
+    small_cost.push_back(c_hi);
+  }
+  const uint64_t mid_lo = s_lo ? lo_end : 0, mid_hi = s_hi ? hi_start : total;
+  double T2 = cost(mid_lo, mid_hi);
+  for (double x : small_cost) T2 += x + f;
+  T2 /= n_target;
+  std::vector<BandItem> items;
+  cut(mid_lo, mid_hi, n_target,
+      [&](int k) {
+        return k < (int)small_cost.size() ? T2 - small_cost[(size_t)k] - f
+                                          : T2;
+      },
+      &items);
+  if ((int)items.size() != n_target) {
+    *exact = (int)plain.size() == n_target;
+    return plain;
+  }
+  items.insert(items.end(), smalls.begin(), smalls.end());
+  *exact = true;
+  return items;
 }
 
 }  // namespace isd

@@ -530,3 +530,45 @@ def test_lane_patterns_tile_the_walk(name, log_hint):
     for v in vecs + [mask]:
         span = max(span, v.bit_length())
     assert span <= log_hint - info.k
+
+
+# The host's work-item split of banded launches (capi.cu -> plan.cpp
+# band_work_items, exported as isd_band_items for this test): items tile the
+# slot order, stay within span + 1 popcount classes, and with the small
+# items of the extreme classes added to blocks 0 and 1 every block gets the
+# same cost.
+@pytest.mark.parametrize("F,n_target", [(19, 148), (16, 148), (12, 37),
+                                        (8, 7)])
+@pytest.mark.parametrize("weighted", [False, True])
+def test_band_items_tile_and_balance(F, n_target, weighted):
+    from bisect import bisect_right
+    from math import comb
+    rng = np.random.default_rng(F * 1000 + n_target)
+    n_seg = min(1 << F, 2048) if weighted else 0
+    w = 1.0 + 0.8 * rng.random(n_seg) if weighted else None
+    flush = 20.0
+    items, exact = _native.band_items(F, n_target, 2, w, flush)
+    cum = [0]
+    for q in range(F + 1):
+        cum.append(cum[-1] + comb(F, q))
+    cls = lambda g: bisect_right(cum, g) - 1  # noqa: E731
+    r = items[np.argsort(items[:, 0])]
+    assert r[0, 0] == 0 and r[-1, 1] == 1 << F
+    assert np.array_equal(r[1:, 0], r[:-1, 1]) and np.all(r[:, 1] > r[:, 0])
+    for g0, g1, q0 in items:
+        assert cls(g0) == q0 and cls(g1 - 1) <= q0 + 2
+
+    total = 1 << F
+    seg = np.arange(total) * max(n_seg, 1) // total
+    per_slot = w[seg] if weighted else np.ones(total)
+    csum = np.concatenate([[0.0], np.cumsum(per_slot)])
+    cost = [csum[g1] - csum[g0] for g0, g1, _ in items]
+    if not exact:
+        assert F <= 12  # class caps bind on small walks: plain split
+        return
+    block = np.array(cost[:n_target])
+    for i, c in enumerate(cost[n_target:]):
+        block[i] += c + flush  # a second item costs its walk and a flush
+    assert len(items) >= n_target
+    assert block.max() <= 1.01 * block.mean() + 2 * per_slot.max()
+    assert block.min() >= 0.99 * block.mean() - 2 * per_slot.max()
