@@ -1173,7 +1173,8 @@ std::vector<BandItem> band_work_items(int F, int n_target, int span,
       const uint64_t limit = std::min(end, cum[std::min(F, q + span) + 1]);
       const uint64_t g0 = g;
       double budget = k >= n_items - 1 ? 1e300 : target(k) + carry;
-      while (g < limit && budget > 0) {
+      // (every item takes at least one slot)
+      for (bool first = true; g < limit && (first || budget > 0); first = false) {
         while (seg_lo(j + 1) <= g) ++j;
         const double wj = wseg(j);
         const uint64_t room = std::min(limit, seg_lo(j + 1)) - g;
@@ -1225,6 +1226,13 @@ std::vector<BandItem> band_work_items(int F, int n_target, int span,
   double T2 = cost(mid_lo, mid_hi);
   for (double x : small_cost) T2 += x + f;
   T2 /= n_target;
+  // (a block's first item must keep at least half its share; otherwise,
+  // e.g. on tiny walks where a flush outweighs an item, the plain split)
+  for (double x : small_cost)
+    if (T2 - x - f < 0.5 * T2) {
+      *exact = (int)plain.size() == n_target;
+      return plain;
+    }
   std::vector<BandItem> items;
   cut(mid_lo, mid_hi, n_target,
       [&](int k) {

@@ -572,3 +572,28 @@ def test_band_items_tile_and_balance(F, n_target, weighted):
     assert len(items) >= n_target
     assert block.max() <= 1.01 * block.mean() + 2 * per_slot.max()
     assert block.min() >= 0.99 * block.mean() - 2 * per_slot.max()
+
+
+def test_band_items_valid_for_every_walk_size():
+    # tiny walks (a flush outweighs an item) through full-size ones, every
+    # block count, flush cost and cost curve: always a tiling of the slot
+    # order with non-empty items inside their class span
+    from bisect import bisect_right
+    from math import comb
+    for F in range(1, 20):
+        cum = [0]
+        for q in range(F + 1):
+            cum.append(cum[-1] + comb(F, q))
+        for nt in (1, 3, 7, 148):
+            for flush in (0.0, 78.0, 312.0, 5000.0):
+                for weighted in (False, True):
+                    w = (np.linspace(1, 2, min(1 << F, 9472)) if weighted
+                         else None)
+                    items, _ = _native.band_items(F, nt, 2, w, flush)
+                    r = items[np.argsort(items[:, 0])]
+                    assert r[0, 0] == 0 and r[-1, 1] == 1 << F
+                    assert np.array_equal(r[1:, 0], r[:-1, 1])
+                    assert np.all(r[:, 1] > r[:, 0])
+                    for g0, g1, q0 in items:
+                        assert bisect_right(cum, g0) - 1 == q0
+                        assert bisect_right(cum, g1 - 1) - 1 <= q0 + 2
