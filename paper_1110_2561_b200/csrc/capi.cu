@@ -580,15 +580,22 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
       x = launch_hoisted_jit(warm, scratch, sms, st, &why);
       if (x > 0) bump_launches(1);
     }
-    cudaEventRecord(e0, st);
-    if (x > 0)
-      launch_hoisted_jit(hp, scratch, sms, st, nullptr);
-    else
-      launch_hoisted(hp, scratch, sms, st);
-    cudaEventRecord(e1, st);
-    cudaEventSynchronize(e1);
-    cudaEventElapsedTime(&ms, e0, e1);
-    bump_launches(1);
+    // best of two timed launches: one noisy timing picked a plan ~9%
+    // slower on c4 once (31.1 vs 33.9e12 configs/s)
+    ms = 1e30f;
+    for (int rep = 0; rep < 2; ++rep) {
+      float t = 0.f;
+      cudaEventRecord(e0, st);
+      if (x > 0)
+        launch_hoisted_jit(hp, scratch, sms, st, nullptr);
+      else
+        launch_hoisted(hp, scratch, sms, st);
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&t, e0, e1);
+      bump_launches(1);
+      ms = std::min(ms, t);
+    }
     ms /= (float)len * (float)(1ull << hp.k);  // per configuration
     if (ms < best_ms) {
       best_ms = ms;
