@@ -224,6 +224,26 @@ int isd_band_items(uint32_t free_bits, uint32_t n_target, uint32_t span,
 int isd_calibrate(int device, int which, double* lanes_per_clk_sm,
                   double* sm_mhz);
 
+/* ---- tuning knobs ------------------------------------------------------
+ * Process-wide overrides of planning and launch choices (loop width,
+ * pairing mode, banded tables, autotuning, the JIT, ...), for the tests and
+ * the experiment scripts.  The library never reads the environment: a knob
+ * changes behaviour only when set here.  value NULL or "" unsets it; an
+ * unknown name is ISD_EINVAL.  Plans are cached per knob set. */
+int isd_set_knob(const char* name, const char* value);
+int isd_clear_knobs(void);
+
+/* ---- on-disk cache ------------------------------------------------------
+ * Autotuned plans (walks of >= 2^33 configurations), band cost curves and
+ * NVRTC cubins are kept in a directory cache so that a new process skips
+ * the layout model, the GPU autotune and the compiles (and runs the same
+ * plan as the process that tuned it).  `dirs` is a ':'-separated list: the
+ * first directory is written (created if missing), the rest are read-only
+ * seeds.  NULL or "" disables the cache (the default).  Entries are keyed
+ * by isd_build_id(), the device name and SM count. */
+int isd_set_cache_dirs(const char* dirs);
+const char* isd_build_id(void);
+
 /* ---- misc ------------------------------------------------------------ */
 int isd_device_count(void);
 int isd_sm_count(int device);

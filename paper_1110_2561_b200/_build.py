@@ -19,7 +19,7 @@ LIB = os.path.join(PKG, "libisingdos_b200.so")
 LIB_DEBUG = os.path.join(PKG, "libisingdos_b200_dbg.so")
 
 SOURCES = ["plan.cpp", "enumerate.cu", "thermo.cu", "calibrate.cu", "capi.cu",
-           "jit.cpp"]
+           "jit.cpp", "knobs.cpp", "cache.cpp"]
 HEADERS = ["isd_internal.h", "k1_body.cuh"]
 
 NVCC_FLAGS = [
@@ -67,14 +67,38 @@ def build(force: bool = False, verbose: bool = False,
     if not force and up_to_date(lib):
         return lib
     _embed_body()
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"),
-           *[os.path.join(CSRC, s) for s in SOURCES], "-ldl",
-           "-o", lib + ".tmp"]
-    if debug:
-        cmd.insert(1, "-DISD_DEBUG_BOUNDS")
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), flush=True)
+    # one nvcc per source, in parallel, then one link
+    tag = "dbg" if debug else "rel"
+    objdir = os.path.join(PKG, "_obj", tag)
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    extra = (["-DISD_DEBUG_BOUNDS"] if debug else []) + \
+        (["-Xptxas=-v"] if verbose else [])
+
+    # the on-disk plan / cubin cache keys carry a hash of the sources, so a
+    # rebuilt library never reads another build's entries
+    import hashlib
+    h = hashlib.sha256()
+    for f in _inputs():
+        h.update(os.path.basename(f).encode())
+        h.update(open(f, "rb").read())
+    extra.append(f"-DISD_BUILD_ID=\"{h.hexdigest()[:16]}{'-dbg' if debug else ''}\"")
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        cmd = [nvcc_path(), *extra, *compile_flags, "-I",
+               os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src),
+               "-o", obj]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
+    cmd = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a",
+           "-shared", *objs, "-ldl", "-o", lib + ".tmp"]
     subprocess.run(cmd, check=True)
     os.replace(lib + ".tmp", lib)
     return lib

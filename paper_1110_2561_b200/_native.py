@@ -6,6 +6,7 @@ raises, and if no GPU is present the compute calls raise RuntimeError with
 the library's own message.
 """
 
+import contextlib
 import ctypes
 import os
 import threading
@@ -28,7 +29,8 @@ EXPORTED_SYMBOLS = (
     "isd_plan", "isd_validate", "isd_calibrate", "isd_device_count",
     "isd_sm_count", "isd_last_error", "isd_version", "isd_abi_version",
     "isd_launch_count", "isd_mirror_async", "isd_kernel_info",
-    "isd_jit_check", "isd_band_items",
+    "isd_jit_check", "isd_band_items", "isd_set_knob", "isd_clear_knobs",
+    "isd_set_cache_dirs", "isd_build_id",
 )
 
 
@@ -125,6 +127,12 @@ def load():
             ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_int)]
         lib.isd_band_items.restype = ctypes.c_int
         lib.isd_launch_count.restype = ctypes.c_uint64
+        lib.isd_set_knob.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
+        lib.isd_set_knob.restype = ctypes.c_int
+        lib.isd_clear_knobs.restype = ctypes.c_int
+        lib.isd_set_cache_dirs.argtypes = [ctypes.c_char_p]
+        lib.isd_set_cache_dirs.restype = ctypes.c_int
+        lib.isd_build_id.restype = ctypes.c_char_p
         for name in ("isd_enumerate", "isd_enumerate_async", "isd_thermo",
                      "isd_thermo_async", "isd_plan", "isd_validate",
                      "isd_calibrate", "isd_device_count", "isd_sm_count",
@@ -132,8 +140,33 @@ def load():
             getattr(lib, name).restype = ctypes.c_int
         if lib.isd_abi_version() != 2:
             raise ImportError("isingdos-b200 ABI version mismatch")
+        lib.isd_set_cache_dirs(default_cache_dir().encode())
         _lib = lib
         return lib
+
+
+def default_cache_dir() -> str:
+    """Where tuned plans and NVRTC cubins persist between processes:
+    $XDG_CACHE_HOME/isingdos_b200 (default ~/.cache/isingdos_b200)."""
+    base = os.environ.get("XDG_CACHE_HOME") or os.path.join(
+        os.path.expanduser("~"), ".cache")
+    return os.path.join(base, "isingdos_b200")
+
+
+def set_cache_dirs(dirs) -> None:
+    """Set the engine's plan / cubin cache: a path, a list of paths (the
+    first is written, the rest are read-only seeds), or None to disable."""
+    if dirs is None:
+        text = ""
+    elif isinstance(dirs, str):
+        text = dirs
+    else:
+        text = ":".join(dirs)
+    check(load().isd_set_cache_dirs(text.encode()))
+
+
+def build_id() -> str:
+    return load().isd_build_id().decode()
 
 
 def check(rc: int) -> None:
@@ -142,6 +175,33 @@ def check(rc: int) -> None:
         if rc == -1:
             raise ValueError(msg)
         raise NativeError(f"isingdos-b200 native error {rc}: {msg}")
+
+
+def set_knob(name: str, value=None) -> None:
+    """Set (or with None unset) one tuning knob of the engine.
+
+    Knobs force planning and launch choices (loop width, pairing mode,
+    banded tables, autotuning, the JIT...) for the tests and tools/; the
+    library never reads them from the environment (include/isingdos_b200.h).
+    """
+    v = None if value is None else str(value).encode()
+    check(load().isd_set_knob(name.encode(), v))
+
+
+def clear_knobs() -> None:
+    load().isd_clear_knobs()
+
+
+@contextlib.contextmanager
+def knobs(**values):
+    """Set knobs for the duration of a block: `with knobs(ISD_JIT=2): ...`."""
+    for k, v in values.items():
+        set_knob(k, v)
+    try:
+        yield
+    finally:
+        for k in values:
+            set_knob(k, None)
 
 
 def make_lattice(n_spins, n_bonds, classes) -> Lattice:

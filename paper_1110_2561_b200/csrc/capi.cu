@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -43,22 +44,15 @@ static int cuda_fail(cudaError_t e, const char* what) {
               "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
 
-static long env_long(const char* name, long dflt) {
-  const char* v = std::getenv(name);
-  if (!v || !*v) return dflt;
-  char* end = nullptr;
-  long x = std::strtol(v, &end, 10);
-  return (end && *end == 0) ? x : dflt;
-}
 
 uint32_t hist_words_for(uint32_t nbins) { return (nbins + 31u) & ~31u; }
 
 int hist_count_for(uint32_t hist_words) {
   // Shared-memory budget per block for the histograms.  Three 72 KB blocks
   // of 512 threads fill an SM's 228 KB.  Tunable for experiments.
-  const long budget = env_long("ISD_HIST_BYTES", 72 * 1024);
+  const long budget = knob_long("ISD_HIST_BYTES", 72 * 1024);
   long n = budget / (long)(hist_words * 4);
-  const long cap = env_long("ISD_NHIST_MAX", 16);
+  const long cap = knob_long("ISD_NHIST_MAX", 16);
   if (n > cap) n = cap;
   if (n < 1) n = 1;
   return (int)n;
@@ -126,14 +120,52 @@ static int get_dev(int device, DevState** out,
   return ISD_OK;
 }
 
+// SMs the enumeration grids are sized for: the device's, or fewer under the
+// ISD_GRID_SMS test knob (which stands in for a small partition of a GPU,
+// e.g. a MIG slice or a green context).
 static int current_sm_count(int* sms) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   e = cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetAttribute");
+  const long cap = knob_long("ISD_GRID_SMS", 0);
+  if (cap > 0 && cap < *sms) *sms = (int)cap;
   return ISD_OK;
 }
+
+// Configurations per launch.  Every grid has at least one block per SM and
+// a block's u32 shared counters see at most the configurations its block
+// counts (one RED lane adds 1 for 1, 2 or 4 configurations), so with
+// launches of at most 2^31 configurations per SM of the grid no counter can
+// wrap, even for a work item twice the mean (banded launches cut one item
+// per block, of equal modelled cost).  A power of two, so that a banded
+// launch chunk stays an aligned power-of-two range.  148 SMs: 2^38.
+static uint64_t launch_cap(int sms) {
+  uint64_t p = 1;
+  while (p * 2 <= (uint64_t)(sms < 1 ? 1 : sms)) p *= 2;
+  return p << 31;
+}
+
+// Restores the calling thread's current device on scope exit.  The library
+// shares the primary context with its caller (e.g. torch); a call on device
+// k must not leave the caller's thread switched to k.
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      prev = -1;
+      cudaGetLastError();
+    }
+  }
+  ~DeviceGuard() {
+    int now = -1;
+    if (prev >= 0 && cudaGetDevice(&now) == cudaSuccess && now != prev)
+      cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
 
 // Plans are compiled once per (lattice, loop width): the layout search
 // replays a sample of warp instructions and costs tens of milliseconds.
@@ -160,8 +192,7 @@ static std::string plan_key(const isd_lattice* lat, uint64_t hint,
   std::string key(reinterpret_cast<const char*>(lat), sizeof(*lat));
   key.push_back((char)l);
   key += "|top" + std::to_string(top);
-  if (const char* v = std::getenv("ISD_COPY_VARIANT")) key += v;
-  if (const char* v = std::getenv("ISD_PAIR")) key += std::string("|pair") + v;
+  key += knob_signature();
   return key;
 }
 
@@ -282,7 +313,7 @@ static void band_costs(const isd_lattice* lat, const isd_plan_info& info,
                        const std::vector<double>** w, std::string* key) {
   *w = nullptr;
   key->clear();
-  if (env_long("ISD_BAND_WEIGHTS", 1) == 0) return;
+  if (knob_long("ISD_BAND_WEIGHTS", 1) == 0) return;
   // (explicit fields: the structs' padding is not initialised)
   std::string k;
   auto add = [&](unsigned long long v) { k += std::to_string(v) + ","; };
@@ -342,7 +373,7 @@ static std::map<int, uint32_t*> g_claim_ring;
 static std::atomic<uint32_t> g_claim_next{0};
 constexpr uint32_t kClaimSlots = 64;
 
-static int claim_counter(cudaStream_t st, uint32_t** out) {
+static int claim_counter(uint32_t** out) {
   int dev = 0;
   cudaGetDevice(&dev);
   uint32_t* ring = nullptr;
@@ -356,18 +387,15 @@ static int claim_counter(cudaStream_t st, uint32_t** out) {
     }
     ring = it->second;
   }
-  uint32_t* slot = ring + 8 * (g_claim_next.fetch_add(1) % kClaimSlots);
-  cudaError_t e = cudaMemsetAsync(slot, 0, sizeof(uint32_t), st);
-  if (e != cudaSuccess) return cuda_fail(e, "band claim counter reset");
-  *out = slot;
+  // (the launch zeroes it on its own stream first)
+  *out = ring + 8 * (g_claim_next.fetch_add(1) % kClaimSlots);
   return ISD_OK;
 }
 
 // Fill the banded-launch fields of hp for its run range [run_begin, run_end)
-// (and zero its claim counter on st).
+// (a dynamic-claim counter must be zeroed on the launch's stream first).
 static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
-                           HoistParams* hp, int sms, cudaStream_t st,
-                           bool weighted = true) {
+                           HoistParams* hp, int sms, bool weighted = true) {
   hp->band_free_bits = 0;
   hp->band_items = 0;
   hp->band_n_items = 0;
@@ -387,8 +415,8 @@ static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
   const int F = rb - 5;
   long dflt = (long)((1ull << F) / (512ull * (uint64_t)sms));
   dflt = dflt < 1 ? 1 : (dflt > 4 ? 4 : dflt);
-  if (weighted && env_long("ISD_BAND_WEIGHTS", 1) != 0) dflt = 1;
-  const int per_sm = (int)env_long("ISD_BAND_ITEMS_PER_SM", dflt);
+  if (weighted && knob_long("ISD_BAND_WEIGHTS", 1) != 0) dflt = 1;
+  const int per_sm = (int)knob_long("ISD_BAND_ITEMS_PER_SM", dflt);
   const std::vector<double>* w = nullptr;
   std::string cost_key;
   if (weighted) band_costs(lat, info, *hp, rb, &w, &cost_key);
@@ -405,9 +433,9 @@ static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
   hp->band_n_items = count;
   // ISD_BAND_DYNAMIC=1: blocks claim items from a counter (measured no
   // faster than the static round-robin over items in slot order)
-  if (env_long("ISD_BAND_DYNAMIC", 0) != 0) {
+  if (knob_long("ISD_BAND_DYNAMIC", 0) != 0) {
     uint32_t* slot = nullptr;
-    const int rc2 = claim_counter(st, &slot);
+    const int rc2 = claim_counter(&slot);
     if (rc2) return rc2;
     hp->band_claim = (uint64_t)(uintptr_t)slot;
   }
@@ -423,9 +451,9 @@ static constexpr uint64_t kTuneSliceConfigs = 1ull << 36;
 // Candidates may differ in loop width (banded plans use a shorter loop), so
 // each is timed on its own run range of [start, end).
 static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
-                     uint64_t end, int sms, cudaStream_t st,
-                     isd_plan_info* info, uint64_t top) {
-  if (env_long("ISD_AUTOTUNE", 1) == 0) return;
+                     uint64_t end, int sms, isd_plan_info* info,
+                     uint64_t top) {
+  if (knob_long("ISD_AUTOTUNE", 1) == 0) return;
   const std::string key = plan_key(lat, hint, top);
   std::vector<isd_plan_info> cands;
   {
@@ -436,18 +464,26 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
       return;
     }
     pe.tuned = true;
-    const int n_cand = (int)env_long("ISD_TUNE_CANDIDATES", kTuneCandidates);
+    const int n_cand = (int)knob_long("ISD_TUNE_CANDIDATES", kTuneCandidates);
     for (size_t i = 0; i < pe.ranked.size() && (int)cands.size() < n_cand;
          ++i)
       if (!pe.ranked[i].band_rows || band_ok(pe.ranked[i], start, end))
         cands.push_back(pe.ranked[i]);
   }
   if (cands.size() < 2) return;
+  // tuning runs on a private stream (never the caller's, which may be
+  // capturing a graph or carry unrelated work); it is synchronous
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
   const size_t bytes =
       (size_t)(lat->n_spins + 1) * (lat->n_bonds + 1) * sizeof(uint64_t);
   unsigned long long* scratch = nullptr;
   if (cudaMalloc(&scratch, bytes) != cudaSuccess) {
     cudaGetLastError();
+    cudaStreamDestroy(st);
     return;
   }
   cudaEvent_t e0, e1;
@@ -508,7 +544,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
   // optional GPU hill climb of the best candidate's lane pattern, scored on
   // the same spread sample (ISD_GPU_CLIMB = steps); the result joins the
   // finalists
-  const long climb = env_long("ISD_GPU_CLIMB", 0);
+  const long climb = knob_long("ISD_GPU_CLIMB", 0);
   if (climb > 0 && !stage1.empty()) {
     isd_plan_info cur = cands[stage1[0].second];
     float cur_t = stage1[0].first;
@@ -535,13 +571,24 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
   // the NVRTC build when it is available (its Gray-order loop changes the
   // instruction mix), compiled once per finalist and cached for the walk.
   // The model's best banded candidates join the finalists.
-  const bool jit_ok = env_long("ISD_JIT", 1) != 0;
+  const bool jit_ok = knob_long("ISD_JIT", 1) != 0;
   std::vector<size_t> finalists;
-  const size_t n_final = (size_t)env_long("ISD_TUNE_FINALISTS", kTuneFinalists);
+  const size_t n_final = (size_t)knob_long("ISD_TUNE_FINALISTS", kTuneFinalists);
   for (size_t s2 = 0; s2 < stage1.size() && s2 < n_final; ++s2)
     finalists.push_back(stage1[s2].second);
   for (size_t b = 0; b < banded.size() && b < 3; ++b)
     finalists.push_back(banded[b]);
+  // the finalists' NVRTC kernels compile concurrently (or come from the
+  // cubin cache) before the first is timed
+  if (jit_ok) {
+    std::vector<HoistParams> ps;
+    for (size_t i : finalists) {
+      HoistParams hp;
+      fill_hoist(lat, &cands[i], &hp);
+      ps.push_back(hp);
+    }
+    jit_prefetch(ps);
+  }
   float best_ms = 1e30f;
   size_t best = finalists.empty() ? 0 : finalists[0];
   for (size_t i : finalists) {
@@ -569,7 +616,11 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
     hp.hi_step = 1;
     // (equal-size items: the autotuner compares plans, the cost-weighted
     // cut is computed once for the winner)
-    if (set_band_launch(lat, cands[i], &hp, sms, st, false)) continue;
+    if (set_band_launch(lat, cands[i], &hp, sms, false)) continue;
+    if (hp.band_claim &&
+        cudaMemsetAsync(reinterpret_cast<void*>(hp.band_claim), 0,
+                        sizeof(uint32_t), st) != cudaSuccess)
+      continue;
     float ms = 0.f;
     // (warm the finalist's kernel first: the JIT compile is not timed)
     int x = 0;
@@ -605,6 +656,8 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(scratch);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
   cudaGetLastError();
   std::lock_guard<std::mutex> lock(g_plan_mu);
   PlanEntry& pe = g_plans[key];
@@ -628,62 +681,184 @@ static bool unbanded_plan(const isd_lattice* lat, uint64_t hint,
   return true;
 }
 
-// At most 2^38 configurations per launch: with >= 148 CTAs no CTA counts
-// more than ~1.9e9 < 2^32 configurations into its u32 shared histograms.
-static constexpr uint64_t kMaxPerLaunch = 1ull << 38;
-
-static int enqueue_canonical(const isd_lattice* lat, uint64_t a, uint64_t b,
-                             unsigned long long* out, int sms,
-                             cudaStream_t st, bool small_grid, int* nl) {
-  CanonParams p;
-  fill_canon(lat, &p);
-  while (a < b) {
-    const uint64_t e = (b - a > kMaxPerLaunch) ? a + kMaxPerLaunch : b;
-    p.start = a;
-    p.end = e;
-    int r = launch_canonical(p, out, sms, st, small_grid);
-    if (r < 0) return cuda_fail((cudaError_t)(-r), "k1_canonical launch");
-    *nl += r;
-    a = e;
+// Identity of the current device for the plan cache: its name, SM count
+// (as the grids are sized) and compute capability.
+static std::string device_identity(int sms) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static std::mutex mu;
+  static std::map<int, std::string> names;
+  std::string name;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = names.find(dev);
+    if (it == names.end()) {
+      cudaDeviceProp prop;
+      std::string n = "?";
+      if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess)
+        n = std::string(prop.name) + "|cc" + std::to_string(prop.major) +
+            std::to_string(prop.minor) + "|sm" +
+            std::to_string(prop.multiProcessorCount);
+      cudaGetLastError();
+      it = names.emplace(dev, n).first;
+    }
+    name = it->second;
   }
+  return name + "|grid" + std::to_string(sms);
+}
+
+// The plan of a walk over [start, end) (aligned power-of-two ranges hold
+// their top bits fixed: `top` is their start).  Small walks take the host
+// model's plan.  Walks of >= 2^33 configurations take the autotuned plan:
+// from this process's memory, else from the disk cache (cache.cpp), else
+// the model's candidates are timed now and the winner is written to the
+// cache.  Tuning is skipped (the model's plan is used, not remembered as
+// tuned) when `capturing`: a stream being captured into a graph cannot run
+// the synchronous timing launches.  Returns 0, or > 0 when the lattice is
+// too small for the hoisted kernel, or < 0 on error.
+static int walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
+                     int sms, bool capturing, isd_plan_info* info,
+                     uint64_t* top_out) {
+  const uint64_t len = end - start;
+  const uint64_t top = (!(len & (len - 1)) && start % len == 0 &&
+                        knob_long("ISD_PLAN_TOP", 1) != 0)
+                           ? start
+                           : 0;
+  *top_out = top;
+  const bool large = len >= kTuneConfigs;
+  const std::string key = plan_key(lat, len, top);
+  {
+    std::lock_guard<std::mutex> lock(g_plan_mu);
+    auto it = g_plans.find(key);
+    if (it != g_plans.end() && (it->second.tuned || it->second.rc || !large)) {
+      *info = it->second.info;
+      return it->second.rc;
+    }
+  }
+  const bool tune = large && knob_long("ISD_AUTOTUNE", 1) != 0;
+  const std::string dkey = key + "|" + device_identity(sms) + "|span" +
+                           std::to_string(end - start);
+  if (tune) {
+    std::string blob;
+    if (cache_get("plan", dkey, &blob) && blob.size() >= 4) {
+      uint32_t n = 0;
+      std::memcpy(&n, blob.data(), 4);
+      if (n >= 1 && n <= 2 && blob.size() == 4 + n * sizeof(isd_plan_info)) {
+        PlanEntry pe;
+        std::memcpy(&pe.info, blob.data() + 4, sizeof(isd_plan_info));
+        for (uint32_t i = 1; i < n; ++i) {
+          isd_plan_info x;
+          std::memcpy(&x, blob.data() + 4 + i * sizeof(isd_plan_info),
+                      sizeof x);
+          pe.ranked.push_back(x);
+        }
+        pe.tuned = true;
+        std::lock_guard<std::mutex> lock(g_plan_mu);
+        auto it = g_plans.find(key);
+        if (it == g_plans.end() || !it->second.tuned)
+          g_plans[key] = std::move(pe);
+        *info = g_plans[key].info;
+        return 0;
+      }
+    }
+  }
+  const int rc = cached_plan(lat, len, info, top);
+  if (rc || !tune || capturing) return rc;
+  autotune(lat, len, start, end, sms, info, top);
+  // remember the winner (and the best unbanded plan, for unaligned ranges)
+  std::string blob(4, '\0');
+  uint32_t n = 1;
+  blob.append(reinterpret_cast<const char*>(info), sizeof *info);
+  isd_plan_info ub;
+  {
+    std::lock_guard<std::mutex> lock(g_plan_mu);
+    const isd_plan_info* best = nullptr;
+    for (const isd_plan_info& x : g_plans[key].ranked)
+      if (!x.band_rows && (!best || x.est_per_config < best->est_per_config))
+        best = &x;
+    if (best) {
+      ub = *best;
+      ++n;
+    }
+  }
+  if (n == 2) blob.append(reinterpret_cast<const char*>(&ub), sizeof ub);
+  std::memcpy(&blob[0], &n, 4);
+  cache_put("plan", dkey, blob);
+  return 0;
+}
+
+// ---- walks as lists of stream operations ----------------------------------
+// A walk is prepared first — validation, plan (and a first large walk's
+// autotune), band work items, NVRTC kernels, all host-side and synchronous —
+// into a list of operations, which are then issued back to back on a stream.
+// So a caller's timing events around the issue see only device work, and
+// several devices' walks can be prepared before any of them starts.
+struct Op {
+  const char* what;
+  std::function<int(cudaStream_t)> fn;  // launches (>= 0) or -cudaError_t
+};
+
+static int issue_ops(const std::vector<Op>& ops, cudaStream_t st,
+                     int* launches) {
+  int nl = 0;
+  for (const Op& op : ops) {
+    const int r = op.fn(st);
+    if (r < 0) return cuda_fail((cudaError_t)(-r), op.what);
+    nl += r;
+  }
+  if (launches) *launches = nl;
   return ISD_OK;
 }
 
-static int enumerate_impl(const isd_lattice* lat, uint64_t start,
-                          uint64_t end, int algo, unsigned long long* out,
-                          int accumulate, cudaStream_t st, int* launches);
+static void prepare_canonical(const isd_lattice* lat, uint64_t a, uint64_t b,
+                              unsigned long long* out, int sms,
+                              bool small_grid, std::vector<Op>* ops) {
+  CanonParams p;
+  fill_canon(lat, &p);
+  const uint64_t cap = launch_cap(sms);
+  while (a < b) {
+    const uint64_t e = (b - a > cap) ? a + cap : b;
+    p.start = a;
+    p.end = e;
+    ops->push_back({"k1_canonical launch", [p, out, sms, small_grid](
+                                               cudaStream_t st) {
+                      return launch_canonical(p, out, sms, st, small_grid);
+                    }});
+    a = e;
+  }
+}
+
+static int prepare_walk(const isd_lattice* lat, uint64_t start, uint64_t end,
+                        int algo, unsigned long long* out, int accumulate,
+                        bool capturing, std::vector<Op>* ops);
 
 // Half walk + mirror (ISD_FLAG_FLIP_SYMMETRY).
-static int enumerate_flip(const isd_lattice* lat, uint64_t start, uint64_t end,
-                          int algo, unsigned long long* out, int accumulate,
-                          cudaStream_t st, int* launches) {
+static int prepare_flip(const isd_lattice* lat, uint64_t start, uint64_t end,
+                        int algo, unsigned long long* out, int accumulate,
+                        bool capturing, std::vector<Op>* ops) {
   const uint64_t total = 1ull << lat->n_spins;
   if (start != 0 || end != total)
     return fail(ISD_EINVAL, "flip symmetry needs the full range [0, 2^N)");
   if (accumulate)
     return fail(ISD_EINVAL, "flip symmetry cannot accumulate into a table");
-  int nl = 0;
-  int rc = enumerate_impl(lat, 0, total / 2, algo & 0xff, out, 0, st, &nl);
+  int rc = prepare_walk(lat, 0, total / 2, algo & 0xff, out, 0, capturing, ops);
   if (rc) return rc;
-  int r = launch_mirror(out, lat->n_spins, lat->n_bonds, st);
-  if (r < 0) return cuda_fail((cudaError_t)(-r), "k3_mirror launch");
-  if (launches) *launches = nl + r;
+  const uint32_t n = lat->n_spins, b = lat->n_bonds;
+  ops->push_back({"k3_mirror launch", [out, n, b](cudaStream_t st) {
+                    return launch_mirror(out, n, b, st);
+                  }});
   return ISD_OK;
 }
 
-static int enumerate_impl(const isd_lattice* lat, uint64_t start,
-                          uint64_t end, int algo, unsigned long long* out,
-                          int accumulate, cudaStream_t st, int* launches) {
-  if (algo & ISD_FLAG_FLIP_SYMMETRY) {
-    char err0[256];
-    int rc0 = validate_lattice(lat, err0, sizeof err0);
-    if (rc0) return fail(rc0, "%s", err0);
-    return enumerate_flip(lat, start, end, algo, out, accumulate, st,
-                          launches);
-  }
+static int prepare_walk(const isd_lattice* lat, uint64_t start, uint64_t end,
+                        int algo, unsigned long long* out, int accumulate,
+                        bool capturing, std::vector<Op>* ops) {
   char err[256];
   int rc = validate_lattice(lat, err, sizeof err);
   if (rc) return fail(rc, "%s", err);
+  if (algo & ISD_FLAG_FLIP_SYMMETRY)
+    return prepare_flip(lat, start, end, algo, out, accumulate, capturing,
+                        ops);
   const uint64_t total = 1ull << lat->n_spins;
   if (!(start <= end && end <= total))
     return fail(ISD_EINVAL, "range [%llu, %llu) invalid for 2^%u configurations",
@@ -694,44 +869,36 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
   if (!out) return fail(ISD_EINVAL, "counts pointer is NULL");
   const size_t bytes =
       (size_t)(lat->n_spins + 1) * (lat->n_bonds + 1) * sizeof(uint64_t);
-  int nl = 0;
-  if (!accumulate) {
-    cudaError_t e = cudaMemsetAsync(out, 0, bytes, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
-  }
-  if (start == end) {
-    if (launches) *launches = 0;
-    return ISD_OK;
-  }
+  if (!accumulate)
+    ops->push_back({"cudaMemsetAsync", [out, bytes](cudaStream_t st) {
+                      const cudaError_t e = cudaMemsetAsync(out, 0, bytes, st);
+                      return e == cudaSuccess ? 0 : -(int)e;
+                    }});
+  if (start == end) return ISD_OK;
   int sms = 0;
   rc = current_sm_count(&sms);
   if (rc) return rc;
 
   if (algo == ISD_ALGO_CANONICAL) {
     g_kernel_info = "k1_canonical";
-    rc = enqueue_canonical(lat, start, end, out, sms, st, false, &nl);
-    if (launches) *launches = nl;
-    return rc;
+    prepare_canonical(lat, start, end, out, sms, false, ops);
+    return ISD_OK;
   }
   isd_plan_info info;
   // an aligned power-of-two range (a shard) holds its top bits fixed:
   // the layout model sees them (ISD_PLAN_TOP=0: plan as for shard 0)
-  const uint64_t len = end - start;
-  const uint64_t top = (!(len & (len - 1)) && start % len == 0 &&
-                        env_long("ISD_PLAN_TOP", 1) != 0)
-                           ? start
-                           : 0;
-  const int too_small = cached_plan(lat, len, &info, top);
+  uint64_t top = 0;
+  const int too_small =
+      walk_plan(lat, start, end, sms, capturing, &info, &top);
+  if (too_small < 0) return too_small;
   if (too_small) {
     if (algo == ISD_ALGO_HOISTED)
       return fail(ISD_EINVAL, "lattice of %u spins too small for the hoisted "
                   "kernel", lat->n_spins);
-    rc = enqueue_canonical(lat, start, end, out, sms, st, true, &nl);
-    if (launches) *launches = nl;
-    return rc;
+    g_kernel_info = "k1_canonical";
+    prepare_canonical(lat, start, end, out, sms, true, ops);
+    return ISD_OK;
   }
-  if (end - start >= kTuneConfigs)
-    autotune(lat, end - start, start, end, sms, st, &info, top);
   // a banded plan runs only on an aligned power-of-two range
   if (info.band_rows && !band_ok(info, start, end) &&
       !unbanded_plan(lat, end - start, &info, top))
@@ -740,18 +907,18 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
   const uint64_t r0 = (start + ((1ull << k) - 1)) >> k;
   const uint64_t r1 = end >> k;
   if (r0 >= r1) {
-    rc = enqueue_canonical(lat, start, end, out, sms, st, true, &nl);
-    if (launches) *launches = nl;
-    return rc;
+    g_kernel_info = "k1_canonical";
+    prepare_canonical(lat, start, end, out, sms, true, ops);
+    return ISD_OK;
   }
   // unaligned head and tail: fewer than 2^k configurations each
-  if (start < (r0 << k)) {
-    rc = enqueue_canonical(lat, start, r0 << k, out, sms, st, true, &nl);
-    if (rc) return rc;
-  }
+  if (start < (r0 << k))
+    prepare_canonical(lat, start, r0 << k, out, sms, true, ops);
   // experiment knob: ISD_LAYOUT="A,B,P,ls[,lanemask_hex]" forces the
   // histogram layout and lane placement (window at ls, or the mask)
-  if (const char* lay = std::getenv("ISD_LAYOUT")) {
+  std::string lay_s;
+  if (knob_str("ISD_LAYOUT", &lay_s) && !lay_s.empty()) {
+    const char* lay = lay_s.c_str();
     unsigned a = 0, b = 0, pw = 0, ls = 0;
     unsigned long long mask = 0;
     const int got = std::sscanf(lay, "%u,%u,%u,%u,%llx", &a, &b, &pw, &ls, &mask);
@@ -773,12 +940,22 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
   }
   HoistParams hp;
   fill_hoist(lat, &info, &hp);
-  const uint64_t runs_per_launch = kMaxPerLaunch >> k;
+  const uint64_t runs_per_launch = launch_cap(sms) >> k;
   // large walks use the per-lattice NVRTC specialisation (jit.cpp)
   // (ISD_JIT=0: never; ISD_JIT=2: for every hoisted walk — tests)
-  const long jit_mode = env_long("ISD_JIT", 1);
+  const long jit_mode = knob_long("ISD_JIT", 1);
   bool use_jit = jit_mode != 0 && (end - start >= kTuneConfigs || jit_mode == 2);
-  g_kernel_info = use_jit ? "k1_hoisted_jit" : "k1_hoisted_aot";
+  if (use_jit) {
+    std::string why;
+    if (!jit_ready(hp, &why)) {  // NVRTC unavailable: same arithmetic, AOT
+      use_jit = false;
+      g_kernel_info = "k1_hoisted_aot (jit unavailable: " + why + ")";
+    } else {
+      g_kernel_info = "k1_hoisted_jit";
+    }
+  } else {
+    g_kernel_info = "k1_hoisted_aot";
+  }
   for (uint64_t r = r0; r < r1;) {
     const uint64_t re = (r1 - r > runs_per_launch) ? r + runs_per_launch : r1;
     hp.run_begin = r;
@@ -792,29 +969,52 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
     if ((re - r) & ((1ull << lane_span(span_bits)) - 1))
       default_lanes(&hp.lane_mask, hp.lane_vec);
     hp.hi_step = 1;
-    rc = set_band_launch(lat, info, &hp, sms, st);
+    rc = set_band_launch(lat, info, &hp, sms);
     if (rc) return rc;
-    int x = 0;
-    if (use_jit) {
-      std::string why;
-      x = launch_hoisted_jit(hp, out, sms, st, &why);
-      if (x < 0) return cuda_fail((cudaError_t)(-x), "k1_jit launch");
-      if (x == 0) {  // NVRTC unavailable: same arithmetic, AOT build
-        use_jit = false;
-        g_kernel_info = "k1_hoisted_aot (jit unavailable: " + why + ")";
-      }
+    if (hp.band_claim) {  // (dynamic item claims: zero the counter first)
+      void* claim = reinterpret_cast<void*>(hp.band_claim);
+      ops->push_back({"band claim counter reset", [claim](cudaStream_t st) {
+                        const cudaError_t e =
+                            cudaMemsetAsync(claim, 0, sizeof(uint32_t), st);
+                        return e == cudaSuccess ? 0 : -(int)e;
+                      }});
     }
-    if (!use_jit) x = launch_hoisted(hp, out, sms, st);
-    if (x < 0) return cuda_fail((cudaError_t)(-x), "k1_hoisted launch");
-    nl += x;
+    if (use_jit)
+      ops->push_back({"k1_jit launch", [hp, out, sms](cudaStream_t st) {
+                        const int x =
+                            launch_hoisted_jit(hp, out, sms, st, nullptr);
+                        // (0: the kernel vanished after jit_ready said yes)
+                        return x == 0 ? -(int)cudaErrorInvalidDeviceFunction
+                                      : x;
+                      }});
+    else
+      ops->push_back({"k1_hoisted launch", [hp, out, sms](cudaStream_t st) {
+                        return launch_hoisted(hp, out, sms, st);
+                      }});
     r = re;
   }
-  if ((r1 << k) < end) {
-    rc = enqueue_canonical(lat, r1 << k, end, out, sms, st, true, &nl);
-    if (rc) return rc;
-  }
-  if (launches) *launches = nl;
+  if ((r1 << k) < end)
+    prepare_canonical(lat, r1 << k, end, out, sms, true, ops);
   return ISD_OK;
+}
+
+static bool stream_capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cap != cudaStreamCaptureStatusNone;
+}
+
+static int enumerate_impl(const isd_lattice* lat, uint64_t start,
+                          uint64_t end, int algo, unsigned long long* out,
+                          int accumulate, cudaStream_t st, int* launches) {
+  std::vector<Op> ops;
+  const int rc = prepare_walk(lat, start, end, algo, out, accumulate,
+                              stream_capturing(st), &ops);
+  if (rc) return rc;
+  return issue_ops(ops, st, launches);
 }
 
 }  // namespace isd
@@ -895,6 +1095,7 @@ int isd_enumerate(const isd_lattice* lat, uint64_t start, uint64_t end,
   int rc = isd_validate(lat);
   if (rc) return rc;
   if (!counts_host) return fail(ISD_EINVAL, "counts pointer is NULL");
+  DeviceGuard guard;
   DevState* s = nullptr;
   std::unique_lock<std::mutex> lock;
   rc = get_dev(device, &s, &lock);
@@ -909,9 +1110,14 @@ int isd_enumerate(const isd_lattice* lat, uint64_t start, uint64_t end,
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(counts)");
     s->d_counts_bytes = bytes;
   }
+  // host-side preparation (plan, a first large walk's autotune, work
+  // items, NVRTC kernels) happens before the timed region
+  std::vector<Op> ops;
+  rc = prepare_walk(lat, start, end, algo, s->d_counts, 0, false, &ops);
+  if (rc) return rc;
   cudaEventRecord(s->ev0, s->stream);
   int nl = 0;
-  rc = enumerate_impl(lat, start, end, algo, s->d_counts, 0, s->stream, &nl);
+  rc = issue_ops(ops, s->stream, &nl);
   bump_launches((uint64_t)nl);
   if (rc) return rc;
   cudaEventRecord(s->ev1, s->stream);
@@ -975,6 +1181,7 @@ int isd_thermo(const uint64_t* counts_host, uint32_t n_spins, uint32_t n_bonds,
     return fail(ISD_EINVAL, "NULL buffer");
   if (n_fields < 0 || n_temps < 0)
     return fail(ISD_EINVAL, "negative grid size");
+  DeviceGuard guard;
   DevState* s = nullptr;
   std::unique_lock<std::mutex> lock;
   int rc = get_dev(device, &s, &lock);
@@ -1026,6 +1233,7 @@ int isd_thermo(const uint64_t* counts_host, uint32_t n_spins, uint32_t n_bonds,
 
 int isd_calibrate(int device, int which, double* lanes_per_clk_sm,
                   double* sm_mhz) {
+  DeviceGuard guard;
   DevState* s = nullptr;
   std::unique_lock<std::mutex> lock;
   int rc = get_dev(device, &s, &lock);
@@ -1052,6 +1260,24 @@ int isd_sm_count(int device) {
     return fail(ISD_ENODEV, "no device %d", device);
   return v;
 }
+
+int isd_set_knob(const char* name, const char* value) {
+  if (!name || !knob_known(name))
+    return fail(ISD_EINVAL, "unknown knob %s", name ? name : "(null)");
+  return set_knob(name, value);
+}
+
+int isd_clear_knobs(void) {
+  clear_knobs();
+  return ISD_OK;
+}
+
+int isd_set_cache_dirs(const char* dirs) {
+  set_cache_dirs(dirs ? dirs : "");
+  return ISD_OK;
+}
+
+const char* isd_build_id(void) { return build_id(); }
 
 const char* isd_last_error(void) { return g_err.c_str(); }
 const char* isd_kernel_info(void) { return g_kernel_info.c_str(); }

@@ -179,6 +179,11 @@ int launch_hoisted_jit(const HoistParams& p, unsigned long long* out,
                        int sm_count, void* stream, std::string* why);
 // compile only (no GPU needed): cubin size, or 0 with *why
 int jit_compile_check(const HoistParams& p, std::string* why);
+// load P's kernel on the current device (compiling it if needed): 1 ready,
+// 0 unavailable (*why)
+int jit_ready(const HoistParams& p, std::string* why);
+// compile (or fetch from the caches) several kernels' cubins concurrently
+void jit_prefetch(const std::vector<HoistParams>& ps);
 int launch_mirror(unsigned long long* t, uint32_t n, uint32_t b,
                   void* stream);
 int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
@@ -189,6 +194,23 @@ int run_calibration(int which, int sm_count, double* lanes_per_clk_sm,
                     double* sm_mhz);
 
 uint64_t bump_launches(uint64_t n);
+
+// ---- tuning knobs (knobs.cpp): set only through isd_set_knob() ----------
+bool knob_known(const char* name);
+bool knob_str(const char* name, std::string* out);
+long knob_long(const char* name, long dflt);
+std::string knob_signature();  // every knob that is set, for cache keys
+int set_knob(const char* name, const char* value);
+void clear_knobs();
+
+// ---- on-disk cache (cache.cpp) -------------------------------------------
+const char* build_id();
+void set_cache_dirs(const std::string& colon_list);  // first one is written
+std::string cache_dirs();
+bool cache_get(const std::string& kind, const std::string& key,
+               std::string* blob);
+void cache_put(const std::string& kind, const std::string& key,
+               const std::string& blob);
 uint32_t hist_words_for(uint32_t nbins);
 int hist_count_for(uint32_t hist_words);
 

@@ -14,8 +14,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -89,7 +91,7 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
   o << "typedef unsigned int uint32_t;\n"
        "typedef unsigned long long uint64_t;\n"
        "typedef int int32_t;\n";
-  if (std::getenv("ISD_PROBE")) o << "#define ISD_PROBE 1\n";
+  if (knob_long("ISD_PROBE", 0)) o << "#define ISD_PROBE 1\n";
   if (debug_bounds)
     o << "#define ISD_CHECK_ADDR(a, lo, bytes) do { if ((unsigned)((a) - "
          "(lo)) >= (bytes) || ((a) & 3u)) __trap(); } while (0)\n";
@@ -186,19 +188,160 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
 }
 
 // ---- cache -----------------------------------------------------------------
+// Two levels, both filled without holding a lock across a compile (so the
+// host threads of different GPUs, and the autotuner's finalists, compile in
+// parallel): cubins by generated source (memory, then the disk cache of
+// cache.cpp), and loaded kernels by (source, device).
 struct JitKernel {
   bool ok = false;
   std::string why;
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
-  int grid = 0;
+  int per_sm = 0;  // resident blocks per SM (grid = per_sm x SMs)
   int threads = kThreads;
 };
 
-static std::mutex g_jit_mu;
-static std::map<std::string, JitKernel> g_jit;
+struct Cubin {
+  bool ok = false;
+  std::string why;
+  std::string bytes;
+};
 
-// Bytes of HoistParams that define the kernel (everything but the range).
+static std::mutex g_jit_mu;
+static std::map<std::string, std::shared_future<Cubin>> g_cubins;
+static std::map<std::string, std::shared_future<JitKernel>> g_jit;
+
+static const char* const kNvrtcOpts[] = {"--gpu-architecture=sm_100a",
+                                         "-std=c++17", "-lineinfo"};
+
+// The specialised kernel's source (it holds every lattice constant, so it
+// identifies the kernel).
+static std::string jit_source(const HoistParams& P) {
+#ifdef ISD_DEBUG_BOUNDS
+  const bool debug_bounds = true;
+#else
+  const bool debug_bounds = false;
+#endif
+  return generate(P, (int)P.n_classes, P.has_double != 0, debug_bounds);
+}
+
+// NVRTC compile of one source (host only).
+static Cubin compile_source(const std::string& src) {
+  Cubin out;
+  Nvrtc& nv = nvrtc();
+  if (!nv.ok) {
+    out.why = nv.why;
+    return out;
+  }
+  nvrtcProgram_t prog = nullptr;
+  if (nv.create(&prog, src.c_str(), "k1_jit.cu", 0, nullptr, nullptr) != 0) {
+    out.why = "nvrtcCreateProgram failed";
+    return out;
+  }
+  const int rc = nv.compile(prog, 3, kNvrtcOpts);
+  if (rc != 0) {
+    size_t n = 0;
+    nv.log_size(prog, &n);
+    std::string log(n, '\0');
+    if (n) nv.log(prog, &log[0]);
+    out.why = "NVRTC compile failed: " + log.substr(0, 600);
+    nv.destroy(&prog);
+    return out;
+  }
+  size_t n = 0;
+  nv.cubin_size(prog, &n);
+  out.bytes.resize(n);
+  nv.cubin(prog, &out.bytes[0]);
+  nv.destroy(&prog);
+  out.ok = true;
+  return out;
+}
+
+// The cubin of P's kernel: memoised per process, then the disk cache, then
+// NVRTC.  Concurrent callers of one source share a single compile.
+static Cubin get_cubin(const HoistParams& P) {
+  const std::string src = jit_source(P);
+  std::string key = src;
+  for (const char* o : kNvrtcOpts) key += std::string("|") + o;
+  std::shared_future<Cubin> fut;
+  std::promise<Cubin> prom;
+  bool mine = false;
+  {
+    std::lock_guard<std::mutex> lock(g_jit_mu);
+    auto it = g_cubins.find(key);
+    if (it == g_cubins.end()) {
+      fut = prom.get_future().share();
+      g_cubins.emplace(key, fut);
+      mine = true;
+    } else {
+      fut = it->second;
+    }
+  }
+  if (mine) {
+    Cubin c;
+    if (cache_get("cubin", key, &c.bytes) && !c.bytes.empty()) {
+      c.ok = true;
+    } else {
+      c = compile_source(src);
+      if (c.ok) cache_put("cubin", key, c.bytes);
+    }
+    prom.set_value(std::move(c));
+  }
+  Cubin c = fut.get();
+  // inspection knob: ISD_JIT_DUMP=<path> writes the cubin (cuobjdump -sass)
+  std::string dump;
+  if (c.ok && knob_str("ISD_JIT_DUMP", &dump) && !dump.empty()) {
+    if (FILE* f = std::fopen(dump.c_str(), "wb")) {
+      std::fwrite(c.bytes.data(), 1, c.bytes.size(), f);
+      std::fclose(f);
+    }
+  }
+  return c;
+}
+
+int jit_compile_check(const HoistParams& P, std::string* why) {
+  const std::string src = jit_source(P);
+  Cubin c = compile_source(src);
+  if (!c.ok) {
+    *why = c.why;
+    return 0;
+  }
+  return (int)c.bytes.size();
+}
+
+// Compile (or fetch) the cubins of several kernels concurrently: the
+// autotuner's finalists are known before any of them is timed.
+void jit_prefetch(const std::vector<HoistParams>& ps) {
+  if (!nvrtc().ok || ps.empty()) return;
+  std::vector<std::thread> pool;
+  for (const HoistParams& p : ps) pool.emplace_back([p] { get_cubin(p); });
+  for (std::thread& t : pool) t.join();
+}
+
+static JitKernel build_kernel(const HoistParams& P) {
+  JitKernel jk;
+  Cubin cubin = get_cubin(P);
+  if (!cubin.ok) {
+    jk.why = cubin.why;
+    return jk;
+  }
+  cudaError_t e = cudaLibraryLoadData(&jk.lib, cubin.bytes.data(), nullptr,
+                                      nullptr, 0, nullptr, nullptr, 0);
+  if (e == cudaSuccess) e = cudaLibraryGetKernel(&jk.kern, jk.lib, "k1_jit");
+  const size_t smem = (size_t)P.n_hist * P.hist_words * 4;
+  if (e != cudaSuccess) {
+    jk.why = std::string("loading the JIT kernel: ") + cudaGetErrorString(e);
+    cudaGetLastError();
+    return jk;
+  }
+  jk.threads = hoisted_block((const void*)jk.kern, smem, 1, P.pair == 2,
+                             &jk.per_sm);
+  jk.ok = true;
+  return jk;
+}
+
+// Bytes of HoistParams that define the kernel (everything but the launch
+// arguments), plus the device: the key of a loaded kernel.
 static std::string jit_key(const HoistParams& P, int device) {
   HoistParams q = P;
   q.run_begin = q.run_end = 0;
@@ -210,95 +353,44 @@ static std::string jit_key(const HoistParams& P, int device) {
   q.band_claim = 0;
   std::string key(reinterpret_cast<const char*>(&q), sizeof q);
   key += std::to_string(device);
+  key += knob_long("ISD_PROBE", 0) ? "|probe" : "";
   return key;
 }
 
-// Generate and compile the specialised kernel to a cubin (host only).
-static bool compile_cubin(const HoistParams& P, std::vector<char>* cubin,
-                          std::string* why) {
-  Nvrtc& nv = nvrtc();
-  if (!nv.ok) {
-    *why = nv.why;
-    return false;
-  }
-#ifdef ISD_DEBUG_BOUNDS
-  const bool debug_bounds = true;
-#else
-  const bool debug_bounds = false;
-#endif
-  const std::string src =
-      generate(P, (int)P.n_classes, P.has_double != 0, debug_bounds);
-  nvrtcProgram_t prog = nullptr;
-  if (nv.create(&prog, src.c_str(), "k1_jit.cu", 0, nullptr, nullptr) != 0) {
-    *why = "nvrtcCreateProgram failed";
-    return false;
-  }
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17",
-                        "-lineinfo"};
-  const int rc = nv.compile(prog, 3, opts);
-  if (rc != 0) {
-    size_t n = 0;
-    nv.log_size(prog, &n);
-    std::string log(n, '\0');
-    if (n) nv.log(prog, &log[0]);
-    *why = "NVRTC compile failed: " + log.substr(0, 600);
-    nv.destroy(&prog);
-    return false;
-  }
-  size_t n = 0;
-  nv.cubin_size(prog, &n);
-  cubin->resize(n);
-  nv.cubin(prog, cubin->data());
-  nv.destroy(&prog);
-  // inspection knob: ISD_JIT_DUMP=<path> writes the cubin (cuobjdump -sass)
-  if (const char* dump = std::getenv("ISD_JIT_DUMP")) {
-    if (FILE* f = std::fopen(dump, "wb")) {
-      std::fwrite(cubin->data(), 1, cubin->size(), f);
-      std::fclose(f);
+// The loaded kernel of P on the current device (built once per process).
+static JitKernel get_kernel(const HoistParams& P) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::string key = jit_key(P, dev);
+  std::shared_future<JitKernel> fut;
+  std::promise<JitKernel> prom;
+  bool mine = false;
+  {
+    std::lock_guard<std::mutex> lock(g_jit_mu);
+    auto it = g_jit.find(key);
+    if (it == g_jit.end()) {
+      fut = prom.get_future().share();
+      g_jit.emplace(key, fut);
+      mine = true;
+    } else {
+      fut = it->second;
     }
   }
-  return true;
+  if (mine) prom.set_value(build_kernel(P));
+  return fut.get();
 }
 
-int jit_compile_check(const HoistParams& P, std::string* why) {
-  std::vector<char> cubin;
-  return compile_cubin(P, &cubin, why) ? (int)cubin.size() : 0;
-}
-
-static JitKernel build_kernel(const HoistParams& P, int sm_count) {
-  JitKernel jk;
-  std::vector<char> cubin;
-  if (!compile_cubin(P, &cubin, &jk.why)) return jk;
-  cudaError_t e = cudaLibraryLoadData(&jk.lib, cubin.data(), nullptr, nullptr,
-                                      0, nullptr, nullptr, 0);
-  if (e == cudaSuccess) e = cudaLibraryGetKernel(&jk.kern, jk.lib, "k1_jit");
-  const size_t smem = (size_t)P.n_hist * P.hist_words * 4;
-  if (e != cudaSuccess) {
-    jk.why = std::string("loading the JIT kernel: ") + cudaGetErrorString(e);
-    cudaGetLastError();
-    return jk;
-  }
-  jk.threads = hoisted_block((const void*)jk.kern, smem, sm_count,
-                             P.pair == 2, &jk.grid);
-  jk.ok = true;
-  return jk;
+int jit_ready(const HoistParams& P, std::string* why) {
+  const JitKernel jk = get_kernel(P);
+  if (!jk.ok && why) *why = jk.why;
+  return jk.ok ? 1 : 0;
 }
 
 // Launch the specialised kernel for P's run range; returns 1 on success,
 // 0 if the JIT path is unavailable (caller falls back), <0 on a launch error.
 int launch_hoisted_jit(const HoistParams& P, unsigned long long* out,
                        int sm_count, void* stream, std::string* why) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const std::string key = jit_key(P, dev);
-  JitKernel jk;
-  {
-    std::lock_guard<std::mutex> lock(g_jit_mu);
-    auto it = g_jit.find(key);
-    if (it == g_jit.end())
-      it = g_jit.emplace(key, build_kernel(P, sm_count)).first;
-    jk = it->second;
-  }
+  const JitKernel jk = get_kernel(P);
   if (!jk.ok) {
     if (why) *why = jk.why;
     return 0;
@@ -317,7 +409,7 @@ int launch_hoisted_jit(const HoistParams& P, unsigned long long* out,
   void* claim = reinterpret_cast<void*>(P.band_claim);
   void* args[] = {&run_begin, &nruns,   &hi_step,   &lane_mask, &lanes,
                   &items,     &n_items, &free_bits, &claim,     &out};
-  int grid = jk.grid;
+  int grid = jk.per_sm * sm_count;
   const uint64_t need = (nruns + jk.threads - 1) / jk.threads;
   if (need < (uint64_t)grid) grid = (int)(need ? need : 1);
   const size_t smem = (size_t)P.n_hist * P.hist_words * 4;

@@ -19,10 +19,6 @@ namespace isd {
 
 static inline int popc64(uint64_t x) { return __builtin_popcountll(x); }
 
-static long env_int(const char* name, long dflt) {
-  const char* v = std::getenv(name);
-  return (v && *v) ? std::atol(v) : dflt;
-}
 
 int validate_lattice(const isd_lattice* lat, char* err, size_t errlen) {
   if (!lat) {
@@ -283,9 +279,9 @@ static int energy_of(const isd_lattice* lat, uint64_t x) {
 // ISD_PAIR: unset = let the model / autotuner choose; 0, 1 or 2 = layouts
 // of that pairing mode only (when one fits shared memory)
 static int pair_policy() {
-  const char* v = std::getenv("ISD_PAIR");
-  if (!v || !*v) return -1;
-  const int m = std::atoi(v);
+  std::string v;
+  if (!knob_str("ISD_PAIR", &v) || v.empty()) return -1;
+  const int m = std::atoi(v.c_str());
   return m < 0 ? 0 : (m > 2 ? 2 : m);
 }
 
@@ -415,8 +411,8 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   // configuration and, if `emit`, appends every (layout, mask) alternative
   // to `ranked`.
   constexpr int kWarps = 160, kScreenWarps = 40, kCopySample = 8;
-  const int kClimbSteps = (int)env_int("ISD_CLIMB_STEPS", 40);
-  const size_t kClimbStarts = (size_t)env_int("ISD_CLIMB_STARTS", 3);
+  const int kClimbSteps = (int)knob_long("ISD_CLIMB_STEPS", 40);
+  const size_t kClimbStarts = (size_t)knob_long("ISD_CLIMB_STARTS", 3);
   const uint64_t pbit[2] = {1ull << psite[0], 1ull << psite[1]};
   std::vector<double> cost(nc);
   // candidates scored by evaluate (the hill climb narrows this to the
@@ -604,7 +600,7 @@ int plan_loop_bits(const isd_lattice* lat, uint64_t n_configs_hint) {
   // grid-stride tail costs < 4% (at ~3.5 runs per thread it cost ~13%)
   int l = log_configs - u - 22;
   // tuning / test knob: force the loop width
-  if (const char* env = std::getenv("ISD_LOOP_BITS")) l = std::atoi(env);
+  l = (int)knob_long("ISD_LOOP_BITS", l);
   if (l > 7) l = 7;
   if (l < 0) l = 0;
   return l;
@@ -737,8 +733,9 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
     }
     std::vector<int> low;
     for (int t = 0; t < u; ++t) low.push_back(t);
-    const char* forced = std::getenv("ISD_COPY_VARIANT");
-    const bool force_low = forced && std::strcmp(forced, "low") == 0;
+    std::string forced;
+    const bool force_low =
+        knob_str("ISD_COPY_VARIANT", &forced) && forced == "low";
     if (sets->empty() || low != (*sets)[0] || force_low) {
       sets->push_back(low);
       names->push_back("low");
@@ -780,7 +777,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   // (test knob ISD_PLAN_WIDE=1: plan a small lattice as a large walk, with
   // random and domino lane patterns, so the CPU replay can check them)
   const bool wide = n_configs_hint >= (1ull << 33) ||
-                    env_int("ISD_PLAN_WIDE", 0) == 1;
+                    knob_long("ISD_PLAN_WIDE", 0) == 1;
   auto try_variant = [&](const isd_plan_info& base, const std::vector<int>& set,
                          bool climb, int band_rows, int band_span = kBandSpan,
                          bool band_domino = false) {
@@ -800,8 +797,12 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   // estimates are only good to a few percent, so every set keeps its best
   // climbed candidates in the list the GPU autotuner times)
   // test / tuning knob: ISD_COPY_VARIANT=even|low|spread forces one set
-  const char* force = std::getenv("ISD_COPY_VARIANT");
-  const long band_knob = env_int("ISD_BAND", -1);  // 0 never, 1 always
+  std::string force_s;
+  const char* force =
+      knob_str("ISD_COPY_VARIANT", &force_s) && !force_s.empty()
+          ? force_s.c_str()
+          : nullptr;
+  const long band_knob = knob_long("ISD_BAND", -1);  // 0 never, 1 always
   if (band_knob != 1)
     for (size_t v = 0; v < sets.size(); ++v)
       if (!force || std::strcmp(force, names[v]) == 0)
@@ -819,7 +820,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   // default: on c5 the few layouts that fit 20 rows score 1.24 wavefronts
   // per RED against 1.11 for the single-site shape (the model then picks
   // single-site lanes anyway).  ISD_BAND_DOMINO=1 adds it, 2 keeps only it.
-  const long domino_knob = env_int("ISD_BAND_DOMINO", 0);
+  const long domino_knob = knob_long("ISD_BAND_DOMINO", 0);
   if (band_knob != 0 && pow2 && (policy < 0 || policy == 2) &&
       (band_knob == 1 || (wide && (!have || best_info.pair_mode < 2)))) {
     for (int shape = 0; shape < 2; ++shape) {
@@ -827,9 +828,9 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
       if ((domino && domino_knob == 0) || (!domino && domino_knob == 2))
         continue;
       const int span =
-          domino ? 0 : (int)env_int("ISD_BAND_SPAN", kBandSpan);  // (knob)
+          domino ? 0 : (int)knob_long("ISD_BAND_SPAN", kBandSpan);  // (knob)
       const int lb = (int)std::min<long>(
-          env_int(domino ? "ISD_BAND_DOMINO_LOOP_BITS" : "ISD_BAND_LOOP_BITS",
+          knob_long(domino ? "ISD_BAND_DOMINO_LOOP_BITS" : "ISD_BAND_LOOP_BITS",
                   domino ? 4 : 5),
           l);
       const int kb = u + lb;
@@ -960,7 +961,7 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
   // Gray sites: the lowest min(G, l) loop sites, G = kDefaultGray
   // (ISD_GRAY=0..kMaxGray overrides it)
   {
-    long g = env_int("ISD_GRAY", kDefaultGray);
+    long g = knob_long("ISD_GRAY", kDefaultGray);
     if (g < 0) g = 0;
     if (g > kMaxGray) g = kMaxGray;
     if (g > (long)info->l) g = (long)info->l;

@@ -18,3 +18,13 @@ def pytest_configure(config):
 @pytest.fixture(scope="session")
 def golden_dir():
     return GOLDEN
+
+
+@pytest.fixture(autouse=True)
+def _reset_knobs():
+    """Tests force kernel variants through the engine's tuning knobs
+    (`_native.set_knob`); none may leak into the next test."""
+    yield
+    from paper_1110_2561_b200 import _native
+    if _native._lib is not None:
+        _native.clear_knobs()

@@ -21,6 +21,7 @@ import numpy as np
 import pytest
 
 import paper_1110_2561_b200 as isd
+from paper_1110_2561_b200 import _native
 from paper_1110_2561_b200.enumeration import enumerate_range_timed
 from oracle import cref
 
@@ -99,10 +100,10 @@ def test_jit_gray_walk_matches_c_oracle(spec, pair, gray, monkeypatch):
             pytest.skip("Gray width >= 3: a subset of the lattices and modes")
         if os.environ.get("ISD_LIBRARY", "").endswith("_dbg.so"):
             pytest.skip("Gray width >= 3 runs through the release build")
-    monkeypatch.setenv("ISD_JIT", "2")
-    monkeypatch.setenv("ISD_LOOP_BITS", "5" if gray == "5" else "4")
-    monkeypatch.setenv("ISD_GRAY", gray)
-    monkeypatch.setenv("ISD_PAIR", pair)
+    _native.set_knob("ISD_JIT", "2")
+    _native.set_knob("ISD_LOOP_BITS", "5" if gray == "5" else "4")
+    _native.set_knob("ISD_GRAY", gray)
+    _native.set_knob("ISD_PAIR", pair)
     got = isd.full_dos(spec)
     assert _native_kernel_path().startswith("k1_hoisted_jit")
     assert np.array_equal(got.counts, oracle_table(spec))
@@ -122,10 +123,10 @@ def _native_kernel_path():
 def test_banded_walk_matches_c_oracle(spec, loop_bits, jit, monkeypatch):
     from paper_1110_2561_b200 import _native
     from paper_1110_2561_b200.enumeration import native_lattice
-    monkeypatch.setenv("ISD_BAND", "1")
-    monkeypatch.setenv("ISD_BAND_LOOP_BITS", loop_bits)
-    monkeypatch.setenv("ISD_JIT", jit)
-    monkeypatch.setenv("ISD_LOOP_BITS", loop_bits)
+    _native.set_knob("ISD_BAND", "1")
+    _native.set_knob("ISD_BAND_LOOP_BITS", loop_bits)
+    _native.set_knob("ISD_JIT", jit)
+    _native.set_knob("ISD_LOOP_BITS", loop_bits)
     _, info = _native.plan(native_lattice(spec), spec.num_configs)
     if not info.band_rows or spec.num_spins - info.k < 6:
         pytest.skip("no banded plan for this lattice")

@@ -54,7 +54,7 @@ def test_reference_goldens_with_forced_loop_width(name, loop_bits, monkeypatch):
     spec, want = spec_from_csv(name)
     if spec.num_spins < 7 + loop_bits + 1:
         pytest.skip("too small for this loop width")
-    monkeypatch.setenv("ISD_LOOP_BITS", str(loop_bits))
+    _native.set_knob("ISD_LOOP_BITS", str(loop_bits))
     got = full(spec, _native.ALGO_HOISTED)
     assert np.array_equal(got, want)
 
@@ -180,7 +180,7 @@ def test_paired_and_unpaired_copies(name, pair, monkeypatch):
     # bit 6 paired (2 configurations per RED), 2 = bits 6 and 5 (4 per RED);
     # every mode must give the golden table (the autotuner then times only
     # layouts of that mode)
-    monkeypatch.setenv("ISD_PAIR", pair)
+    _native.set_knob("ISD_PAIR", pair)
     spec = workloads()[name].spec
     _, info = _native.plan(__import__(
         "paper_1110_2561_b200.enumeration",
@@ -197,7 +197,7 @@ def test_copy_site_variants(name, variant, monkeypatch):
     # both copy-site choices (even-degree sites with parity planes, lowest
     # sites) must give the same table; c3/c1 are the free-boundary lattices
     # where the parity planes carry odd-degree sites
-    monkeypatch.setenv("ISD_COPY_VARIANT", variant)
+    _native.set_knob("ISD_COPY_VARIANT", variant)
     spec = workloads()[name].spec
     lat = __import__("paper_1110_2561_b200.enumeration",
                      fromlist=["native_lattice"]).native_lattice(spec)
@@ -222,7 +222,7 @@ def test_jit_and_aot_kernels_agree(name, monkeypatch):
     spec = workloads()[name].spec
     jit = full(spec)
     assert _native.kernel_info() == "k1_hoisted_jit"
-    monkeypatch.setenv("ISD_JIT", "0")
+    _native.set_knob("ISD_JIT", "0")
     aot = full(spec)
     assert _native.kernel_info() == "k1_hoisted_aot"
     assert np.array_equal(jit, aot)
@@ -369,9 +369,9 @@ def test_bounds_checked_build_runs_clean():
         "from paper_1110_2561_b200.workloads import workloads\n"
         "from paper_1110_2561_b200.enumeration import enumerate_range_timed\n"
         "import paper_1110_2561_b200 as isd\n"
-        "import os\n"
+        "from paper_1110_2561_b200 import _native\n"
         "for pm in ('0', '1', '2'):\n"
-        "    os.environ['ISD_PAIR'] = pm\n"
+        "    _native.set_knob('ISD_PAIR', pm)\n"
         "    for n in ('c3', 'c4', 'c5'):\n"
         "        s = workloads()[n].spec\n"
         "        t, _ = enumerate_range_timed(s, 0, 1 << 33)\n"
@@ -435,7 +435,7 @@ def test_double_bond_lattices_jit_vs_aot(kw, monkeypatch):
     spec = _spec(kw)
     jit = full(spec)
     assert _native.kernel_info() == "k1_hoisted_jit"
-    monkeypatch.setenv("ISD_JIT", "0")
+    _native.set_knob("ISD_JIT", "0")
     assert np.array_equal(full(spec), jit)
     assert isd.verify_dos(isd.DoSHistogram(spec, jit)).passed
 

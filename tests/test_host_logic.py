@@ -214,24 +214,18 @@ def replay_hoisted(spec, loop_bits, pair=None, band_items=None,
     kernel's flush rule.  Also asserts the layout is injective on the bins
     that occur and that the e parity formula holds.
     """
-    os.environ["ISD_LOOP_BITS"] = str(loop_bits)
+    knobs = {"ISD_LOOP_BITS": loop_bits}
     if pair is not None:
-        os.environ["ISD_PAIR"] = str(pair)
+        knobs["ISD_PAIR"] = pair
     if band_items is not None:  # force a banded mode-2 plan
-        os.environ.update(ISD_BAND="1", ISD_PAIR="2",
-                          ISD_BAND_LOOP_BITS=str(loop_bits),
-                          ISD_BAND_DOMINO_LOOP_BITS=str(loop_bits),
-                          ISD_BAND_DOMINO="2" if domino else "0")
+        knobs.update(ISD_BAND=1, ISD_PAIR=2, ISD_BAND_LOOP_BITS=loop_bits,
+                     ISD_BAND_DOMINO_LOOP_BITS=loop_bits,
+                     ISD_BAND_DOMINO=2 if domino else 0)
         if domino:  # lane patterns with domino partners need a "wide" plan
-            os.environ["ISD_PLAN_WIDE"] = "1"
-    try:
+            knobs["ISD_PLAN_WIDE"] = 1
+    with _native.knobs(**knobs):
         lat = native_lattice(spec)
         usable, info = _native.plan(lat, spec.num_configs)
-    finally:
-        for key in ("ISD_LOOP_BITS", "ISD_PAIR", "ISD_BAND",
-                    "ISD_BAND_LOOP_BITS", "ISD_BAND_DOMINO_LOOP_BITS",
-                    "ISD_BAND_DOMINO", "ISD_PLAN_WIDE"):
-            os.environ.pop(key, None)
     if band_items is not None and not info.band_rows:
         return None  # no banded layout for this lattice
     assert usable
@@ -456,13 +450,13 @@ def test_plan_copy_site_variants(monkeypatch):
         spec = workloads()[name].spec
         usable, info = _native.plan(native_lattice(spec), spec.num_configs)
         assert usable and info.e_mode == 1 and info.odd_mask == 0
-    monkeypatch.setenv("ISD_COPY_VARIANT", "even")
+    _native.set_knob("ISD_COPY_VARIANT", "even")
     spec = workloads()["c3"].spec
     usable, info = _native.plan(native_lattice(spec), spec.num_configs)
     assert usable and info.e_mode == 1
     assert info.odd_mask != 0 and info.plane_words > 0
     assert all(not (int(info.odd_mask) >> q) & 1 for q in info.copy_site)
-    monkeypatch.setenv("ISD_COPY_VARIANT", "low")
+    _native.set_knob("ISD_COPY_VARIANT", "low")
     usable, info = _native.plan(native_lattice(spec), spec.num_configs)
     assert usable and info.e_mode == 0
     assert sorted(info.copy_site) == list(range(7))

@@ -12,6 +12,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_1110_2561_b200 as isd  # noqa: E402
 from paper_1110_2561_b200.workloads import workloads  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))  # noqa: E402
+import knobs_env  # noqa: E402
+knobs_env.apply()
 
 
 def main():

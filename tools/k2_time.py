@@ -14,6 +14,9 @@ import torch  # noqa: E402
 import paper_1110_2561_b200 as isd  # noqa: E402
 from paper_1110_2561_b200 import _native  # noqa: E402
 from paper_1110_2561_b200.workloads import workloads  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))  # noqa: E402
+import knobs_env  # noqa: E402
+knobs_env.apply()
 
 
 def main():

@@ -4,6 +4,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1110_2561_b200 import _native
 from paper_1110_2561_b200.workloads import workloads
 from paper_1110_2561_b200.enumeration import native_lattice
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))  # noqa: E402
+import knobs_env  # noqa: E402
+knobs_env.apply()
 for k,w in workloads().items():
     t=time.time()
     ok,p=_native.plan(native_lattice(w.spec), w.spec.num_configs)
