@@ -51,6 +51,13 @@ def parse_args():
                    help="other configs timed (value only) into extra.configs")
     p.add_argument("--no-graph", action="store_true",
                    help="time eager steps instead of CUDA-graph replays")
+    p.add_argument("--knob", action="append", default=[],
+                   metavar="NAME=VALUE",
+                   help="set an engine tuning knob (experiments)")
+    p.add_argument("--no-shard-emulation", action="store_true",
+                   help="skip extra.shard_emulation (P-way shard timings)")
+    p.add_argument("--no-cold", action="store_true",
+                   help="skip extra.cold_start (fresh-process timings)")
     return p.parse_args()
 
 
@@ -195,28 +202,36 @@ class ClockSampler:
 # roofline
 # --------------------------------------------------------------------------
 
-def ncu_traffic(config):
-    """dram read+write bytes per launch of k1_hoisted from the committed
-    ncu --set full capture (profiles/r1_ncu_k1_hoisted_<config>.txt)."""
-    # newest capture of the kernel the walk runs first
-    for name in (f"r1_ncu_k1_jit_band_{config}.txt",
-                 f"r1_ncu_k1_jit_gray_{config}.txt",
-                 f"r1_ncu_k1_jit_pair2_{config}.txt",
-                 f"r1_ncu_k1_jit_pair_{config}.txt",
-                 f"r1_ncu_k1_jit_{config}.txt",
-                 f"r1_ncu_k1_hoisted_{config}.txt"):
-        path = os.path.join(ROOT, "profiles", name)
-        if os.path.exists(path):
-            break
-    else:
-        return None
-    total = 0.0
-    scale = {"[byte]": 1, "[Kbyte]": 1e3, "[Mbyte]": 1e6, "[Gbyte]": 1e9}
+# The ncu --set full capture of the walk kernel on the code this bench runs
+# (profiles/README.md): dram bytes per launch and its duration.  Used only
+# when the capture's kernel time is within 10% of the one measured here;
+# otherwise traffic is reported as null.
+NCU_CAPTURE = "r2_ncu_k1_jit_{config}.txt"
+
+
+def ncu_traffic(config, kernel_ms):
+    path = os.path.join(ROOT, "profiles", NCU_CAPTURE.format(config=config))
+    if not os.path.exists(path):
+        return None, None
+    total, dur_ms = 0.0, None
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}
     for ln in open(path):
-        if "dram__bytes_read.sum [" in ln or "dram__bytes_write.sum [" in ln:
-            unit = ln.split()[1]
-            total += float(ln.split("=")[1]) * scale.get(unit, 1)
-    return total
+        parts = ln.split()
+        if len(parts) < 3:
+            continue
+        unit = parts[1].strip("[]")
+        if parts[0] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            total += float(parts[-1].replace(",", "")) * scale.get(unit, 1)
+        elif parts[0] == "gpu__time_duration.sum":
+            dur_ms = float(parts[-1].replace(",", "")) * tscale.get(unit, 1)
+    src = {"file": f"profiles/{os.path.basename(path)}",
+           "capture_kernel_ms": dur_ms}
+    if dur_ms is None or total == 0 or \
+            abs(dur_ms - kernel_ms) > 0.1 * kernel_ms:
+        src["note"] = "capture does not match this kernel's time: traffic null"
+        return None, src
+    return total, src
 
 
 def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1, kernel="k1",
@@ -248,10 +263,11 @@ def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1, kernel="k1",
     ach = cfg_per_launch / (ms_k1 / 1e3)
     p_red = cal["red_shared_spread"]["lanes_per_clk_sm"]
     peak_red = sm_count * f * p_red * cfg_per_red
+    traffic, traffic_src = ncu_traffic(wl.name, ms_k1)
     roof = {
         "bound": "smem-atomic", "achieved": ach / 1e9, "peak": peak_red / 1e9,
         "unit": "Gconf/s", "frac": ach / peak_red,
-        "traffic": ncu_traffic(wl.name),
+        "traffic": traffic,
         "kernel": kernel, "kernel_ms": ms_k1,
         "algorithmic_work": ("1 RED.shared lane per configuration"
                              if cfg_per_red == 1 else
@@ -260,21 +276,159 @@ def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1, kernel="k1",
         "peak_source": f"K0 red_shared_spread {p_red:.2f} lanes/clk/SM x "
                        f"{sm_count} SMs x {mhz:.0f} MHz x {cfg_per_red} "
                        "configurations/lane (measured, this GPU)",
-        "traffic_source": "ncu --set full, profiles/r1_ncu_k1_*_<config>.txt",
+        "traffic_source": traffic_src,
     }
     popc_ops, alu_ops = canonical_ops(wl.spec)
     p_popc = cal["popc"]["lanes_per_clk_sm"]
     p_alu = cal["lop3"]["lanes_per_clk_sm"]
     peak_int = sm_count * f * min(p_alu / alu_ops, p_popc / popc_ops)
+    # not a utilisation: the hoisted kernel does far less integer work per
+    # configuration than the canonical formulation this bound counts
     roof_int = {
-        "bound": "int-pipe", "achieved": ach / 1e9, "peak": peak_int / 1e9,
-        "unit": "Gconf/s", "frac": ach / peak_int,
+        "bound": "int-pipe (canonical formulation)", "achieved": ach / 1e9,
+        "peak": peak_int / 1e9, "unit": "Gconf/s",
+        "speedup_vs_canonical_int_roofline": ach / peak_int,
         "formula": "n_SM * f_SM * min(P_alu/ALU_ops, P_popc/POPC_ops), "
                    f"canonical POPC={popc_ops} ALU={alu_ops} per config "
                    "(BASELINE.md §4, SURVEY.md §8d)",
         "p_popc": p_popc, "p_alu": p_alu,
     }
     return roof, roof_int
+
+
+# --------------------------------------------------------------------------
+# multi-GPU projection from one GPU, and cold start
+# --------------------------------------------------------------------------
+
+# NVLink read latency of the root's gather (peer loads of P tables inside
+# K2a), which a one-GPU emulation cannot see: a conservative allowance
+NVLINK_GATHER_ALLOWANCE_MS = 0.003
+
+
+def shard_emulation(wl, ms_step_1, dev, reps):
+    """Every shard of a P-way split (P = 2, 4, 8) timed on this GPU through
+    the engine's multi-device entry (all shards listed on device 0: each is
+    walked and event-timed alone, exactly as one rank of a P-GPU run walks
+    it), plus the root's tail — the fused peer gather of P tables + K2 on the
+    workload's grid, replayed as a CUDA graph.  Projected P-GPU step = the
+    slowest shard + the tail (+ an NVLink allowance); projected efficiency
+    = one-GPU step / (P x projected step)."""
+    import statistics as st_
+    import torch
+    from paper_1110_2561_b200 import _native
+    from paper_1110_2561_b200.enumeration import native_lattice
+    import paper_1110_2561_b200 as isd
+    spec = wl.spec
+    lat = native_lattice(spec)
+    nb = (spec.num_spins + 1) * (spec.num_bonds + 1)
+    fields = torch.tensor(wl.fields, dtype=torch.float64, device=dev)
+    temps = torch.tensor(wl.temps, dtype=torch.float64, device=dev)
+    out = torch.empty(len(wl.fields) * len(wl.temps) * 7, dtype=torch.float64,
+                      device=dev)
+    total = torch.empty(nb, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    res = {"method": "isd_enumerate_multi with every shard on this GPU "
+                     "(each shard walked and event-timed alone); tail = "
+                     "isd_thermo_gather_async over P tables + K2, CUDA-graph "
+                     f"replay; + {NVLINK_GATHER_ALLOWANCE_MS * 1e3:.0f} us "
+                     "NVLink allowance",
+           "one_gpu_step_ms": ms_step_1}
+    for P in (2, 4, 8):
+        _native.enumerate_multi(lat, 0, spec.num_configs, [0] * P)  # warm
+        runs = [_native.enumerate_multi(lat, 0, spec.num_configs, [0] * P)
+                for _ in range(reps)]
+        per_shard = [st_.median(r[1][i] for r in runs) for i in range(P)]
+        # the root's tail on real shard tables
+        tabs = []
+        for sh in isd.make_shards(spec, P):
+            t = torch.zeros(nb, dtype=torch.int64, device=dev)
+            _native.enumerate_device(lat, sh.start_index, sh.end_index,
+                                     t.data_ptr(), stream.cuda_stream)
+            tabs.append(t)
+        ptrs = [t.data_ptr() for t in tabs]
+
+        def tail(st):
+            _native.thermo_gather_device(
+                ptrs, total.data_ptr(), spec.num_spins, spec.num_bonds,
+                abs(spec.coupling), fields.data_ptr(), len(wl.fields),
+                temps.data_ptr(), len(wl.temps), out.data_ptr(), st)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        with torch.cuda.graph(g, stream=cap):
+            tail(cap.cuda_stream)
+        for _ in range(3):
+            g.replay()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        n_rep = 50
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(n_rep):
+            g.replay()
+        e1.record(stream)
+        e1.synchronize()
+        tail_ms = e0.elapsed_time(e1) / n_rep
+        ok = bool(torch.equal(total, sum(tabs)))
+        step = max(per_shard) + tail_ms + NVLINK_GATHER_ALLOWANCE_MS
+        res[f"P{P}"] = {
+            "shard_ms": per_shard, "max_shard_ms": max(per_shard),
+            "min_shard_ms": min(per_shard), "tail_ms": tail_ms,
+            "projected_step_ms": step,
+            "projected_configs_per_s": spec.num_configs / (step / 1e3),
+            "projected_efficiency": ms_step_1 / (P * step),
+            "gather_sum_exact": ok}
+    return res
+
+
+COLD_SCRIPT = r"""
+import json, sys, time
+sys.path.insert(0, sys.argv[1])
+t0 = time.perf_counter()
+import paper_1110_2561_b200 as isd
+from paper_1110_2561_b200 import _native
+from paper_1110_2561_b200.enumeration import native_lattice
+from paper_1110_2561_b200.workloads import workloads
+_native.set_cache_dirs(sys.argv[2] or None)
+t1 = time.perf_counter()
+isd.full_dos(isd.LatticeSpec(2, 2))          # CUDA context + library load
+t2 = time.perf_counter()
+spec = workloads()[sys.argv[3]].spec
+dos = isd.full_dos(spec)                     # the first walk of the lattice
+t3 = time.perf_counter()
+isd.full_dos(spec)
+t4 = time.perf_counter()
+_, plan = _native.walk_plan(native_lattice(spec), 0, spec.num_configs, 0)
+print(json.dumps({"import_s": t1 - t0, "context_s": t2 - t1,
+                  "first_walk_ms": (t3 - t2) * 1e3,
+                  "second_walk_ms": (t4 - t3) * 1e3,
+                  "verify": isd.verify_dos(dos).passed,
+                  "plan": _native.plan_fingerprint(plan)}))
+"""
+
+
+def cold_start(wl):
+    """The first full_dos of the workload in a fresh process (after its
+    CUDA context is up), without the plan / cubin cache (an empty cache
+    directory: layout model, GPU autotune and NVRTC compiles all run) and
+    with it (a second fresh process reading what the first wrote)."""
+    import tempfile
+    res = {}
+    with tempfile.TemporaryDirectory() as d:
+        cache = os.path.join(d, "cache")
+        for name in ("no_cache", "cached"):
+            r = subprocess.run([sys.executable, "-c", COLD_SCRIPT, ROOT, cache,
+                                wl.name], capture_output=True, text=True,
+                               timeout=600)
+            if r.returncode != 0:
+                res[name] = {"error": r.stderr[-400:]}
+                continue
+            res[name] = json.loads(r.stdout.strip().splitlines()[-1])
+    a, b = res.get("no_cache", {}), res.get("cached", {})
+    res["same_plan_across_processes"] = \
+        a.get("plan") is not None and a.get("plan") == b.get("plan")
+    return res
 
 
 # --------------------------------------------------------------------------
@@ -294,6 +448,9 @@ def run_b200(args, wl):
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     isd.set_device(local)
+    for kv in args.knob:
+        name, _, value = kv.partition("=")
+        _native.set_knob(name, value)
     # ISD_BENCH_FORCE_DIST=1 runs the NCCL code path even at world size 1
     # (how the single-GPU pool exercises the multi-GPU step)
     use_dist = world > 1 or os.environ.get("ISD_BENCH_FORCE_DIST") == "1"
@@ -513,6 +670,13 @@ def run_b200(args, wl):
                 "evaluated_configs_per_s": (n_cfg // 2) / (ms3 / 1e3),
                 "ms_per_step": ms3, "table_identical": same}
 
+    emulation = None
+    if world == 1 and not args.no_shard_emulation:
+        emulation = shard_emulation(wl, ms_step, dev, max(3, args.steps // 4))
+    cold = None
+    if world == 1 and not args.no_cold:
+        cold = cold_start(wl)
+
     if use_dist:
         dist.destroy_process_group()
     if rank != 0:
@@ -522,14 +686,17 @@ def run_b200(args, wl):
     sm_count = _native.sm_count(local)
     # the plan the walk ran with (autotuned; cached per lattice and size)
     from paper_1110_2561_b200.enumeration import native_lattice as _nl
-    _, plan = _native.plan(_nl(wl.spec), n_cfg // world)
+    shard0 = isd.make_shards(wl.spec, world)[0]
+    _, plan = _native.walk_plan(_nl(wl.spec), shard0.start_index,
+                                shard0.end_index, local)
     roof, roof_int = roofline(wl, cal, clk, sm_count, n_cfg // world, ms_k1,
                               kernel_path, 1 << plan.pair_mode)
     roof["plan"] = {"pair_mode": int(plan.pair_mode),
                     "copy_sites": list(plan.copy_site),
                     "loop_bits": int(plan.l),
                     "hist_words": int(plan.hist_words),
-                    "model_wavefronts_per_red": round(plan.est_wavefronts, 4)}
+                    "model_wavefronts_per_red": round(plan.est_wavefronts, 4),
+                    "fingerprint": _native.plan_fingerprint(plan)}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -550,7 +717,8 @@ def run_b200(args, wl):
         "gpu_launches": launches,
         "clocks": clk,
         "calibration": cal,
-        "extra": {"configs": extra, "flip_symmetry": flip},
+        "extra": {"configs": extra, "flip_symmetry": flip,
+                  "shard_emulation": emulation, "cold_start": cold},
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(wl, args.cpu_seconds)

@@ -99,6 +99,26 @@ int isd_enumerate_async(const isd_lattice* lat, uint64_t start, uint64_t end,
                         int algo, uint64_t* counts_dev, int accumulate,
                         void* stream, int* launches);
 
+/* Multi-device walk (replaces full_dos_timed's Pool of shard workers and
+ * its root-side sum, enumeration.py:365-390).  Splits [start, end) into
+ * n_shards contiguous shards with the reference's partition (make_shards,
+ * enumeration.py:44-63; for n_shards = 2^k over an aligned power-of-two
+ * range: the top k index bits) and walks shard i on device devs[i].  A
+ * device may be listed several times: its shards then run one after another
+ * on its stream (so on one GPU every shard of a P-way split is timed on its
+ * own).  The tables are combined on the device: the root devs[0] reads every
+ * device's table over NVLink peer access (or a device-to-device copy where
+ * peer access is unavailable) in one kernel.  Writes the exact table to
+ * counts_host, shard i's device time to shard_ms[i] (NULL: not wanted) and
+ * the root's span — from its start event, which every device waits on, to
+ * the combined table — to *total_ms.  ISD_FLAG_FLIP_SYMMETRY: the shards
+ * split the top-spin-down half of the full range and the root completes
+ * the table.  Synchronous. */
+int isd_enumerate_multi(const isd_lattice* lat, uint64_t start, uint64_t end,
+                        int n_shards, const int* devs, int algo,
+                        uint64_t* counts_host, double* shard_ms,
+                        double* total_ms);
+
 /* In-place completion of a half walk: counts[m][e] += counts[N-m][e]
  * pairwise (rows m and N-m both become the sum).  Device buffer, async. */
 int isd_mirror_async(uint64_t* counts_dev, uint32_t n_spins, uint32_t n_bonds,
@@ -124,6 +144,21 @@ int isd_thermo_async(const uint64_t* counts_dev, uint32_t n_spins,
                      const double* fields_dev, int n_fields,
                      const double* temps_dev, int n_temps, double* out_dev,
                      void* stream);
+
+/* The fused combine + thermodynamics of a multi-GPU step: the tables
+ * tables_dev[0 .. n_tables) (device pointers readable from the current
+ * device: its own, peer-mapped NVLink memory, or CUDA IPC mappings of other
+ * processes' tables) are summed inside K2's compaction kernel, the sum is
+ * written to sum_dev (may be NULL when a grid is given) and the grid is
+ * evaluated from it, as isd_thermo_async.  With an empty grid only the sum
+ * is formed (one gather kernel).  n_tables <= 32.  Asynchronous on
+ * `stream`. */
+int isd_thermo_gather_async(const uint64_t* const* tables_dev, int n_tables,
+                            uint64_t* sum_dev, uint32_t n_spins,
+                            uint32_t n_bonds, double energy_scale,
+                            const double* fields_dev, int n_fields,
+                            const double* temps_dev, int n_temps,
+                            double* out_dev, void* stream);
 
 /* ---- host-side plan (no GPU needed; used by the CPU tests) ----------- */
 
@@ -192,6 +227,13 @@ typedef struct isd_plan_info {
 
 int isd_plan(const isd_lattice* lat, uint64_t n_configs_hint,
              isd_plan_info* out);
+
+/* The plan a walk of [start, end) on `device` actually runs with: the
+ * host model's for small walks, the autotuned one (from memory, the disk
+ * cache, or tuned now) for walks of >= 2^33 configurations.  Returns 0, or
+ * > 0 when the lattice is too small for the hoisted kernel. */
+int isd_walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
+                  int device, isd_plan_info* out);
 
 /* Generate and NVRTC-compile the lattice's specialised k1 kernel without
  * loading it (no GPU needed); *cubin_bytes = its size.  For tests. */

@@ -30,7 +30,8 @@ EXPORTED_SYMBOLS = (
     "isd_sm_count", "isd_last_error", "isd_version", "isd_abi_version",
     "isd_launch_count", "isd_mirror_async", "isd_kernel_info",
     "isd_jit_check", "isd_band_items", "isd_set_knob", "isd_clear_knobs",
-    "isd_set_cache_dirs", "isd_build_id",
+    "isd_set_cache_dirs", "isd_build_id", "isd_enumerate_multi",
+    "isd_thermo_gather_async", "isd_walk_plan",
 )
 
 
@@ -130,6 +131,16 @@ def load():
         lib.isd_set_knob.argtypes = [ctypes.c_char_p, ctypes.c_char_p]
         lib.isd_set_knob.restype = ctypes.c_int
         lib.isd_clear_knobs.restype = ctypes.c_int
+        lib.isd_enumerate_multi.argtypes = [p_lat, u64, u64, i32, vp, i32,
+                                            vp, vp, p_dbl]
+        lib.isd_enumerate_multi.restype = ctypes.c_int
+        lib.isd_thermo_gather_async.argtypes = [
+            vp, i32, vp, ctypes.c_uint32, ctypes.c_uint32, dbl, vp, i32, vp,
+            i32, vp, vp]
+        lib.isd_thermo_gather_async.restype = ctypes.c_int
+        lib.isd_walk_plan.argtypes = [p_lat, u64, u64, i32,
+                                      ctypes.POINTER(PlanInfo)]
+        lib.isd_walk_plan.restype = ctypes.c_int
         lib.isd_set_cache_dirs.argtypes = [ctypes.c_char_p]
         lib.isd_set_cache_dirs.restype = ctypes.c_int
         lib.isd_build_id.restype = ctypes.c_char_p
@@ -256,6 +267,40 @@ def enumerate_host(lat: Lattice, start: int, end: int, device=None,
     return out.reshape(lat.n_spins + 1, lat.n_bonds + 1), ms.value
 
 
+def enumerate_multi(lat: Lattice, start: int, end: int, devices,
+                    algo: int = ALGO_AUTO):
+    """Walk [start, end) as len(devices) shards, shard i on devices[i]
+    (the reference's partition), tables combined on devices[0] by a peer
+    gather kernel.  Returns (uint64 table, per-shard device ms, root ms)."""
+    lib = load()
+    devs = np.ascontiguousarray(devices, dtype=np.int32)
+    if devs.ndim != 1 or len(devs) < 1:
+        raise ValueError("need at least one device")
+    out = np.zeros((lat.n_spins + 1) * (lat.n_bonds + 1), dtype=np.uint64)
+    shard_ms = np.zeros(len(devs), dtype=np.float64)
+    total = ctypes.c_double(0.0)
+    check(lib.isd_enumerate_multi(ctypes.byref(lat), start, end, len(devs),
+                                  devs.ctypes.data, algo, out.ctypes.data,
+                                  shard_ms.ctypes.data, ctypes.byref(total)))
+    return (out.reshape(lat.n_spins + 1, lat.n_bonds + 1), shard_ms.tolist(),
+            total.value)
+
+
+def thermo_gather_device(table_ptrs, sum_ptr, n_spins, n_bonds, scale,
+                         fields_ptr, n_fields, temps_ptr, n_temps, out_ptr,
+                         stream_ptr) -> int:
+    """Fused sum of several device tables + K2 (isd_thermo_gather_async);
+    returns the kernels launched."""
+    lib = load()
+    ptrs = (ctypes.c_void_p * len(table_ptrs))(*table_ptrs)
+    check(lib.isd_thermo_gather_async(
+        ptrs, len(table_ptrs), ctypes.c_void_p(sum_ptr or None), n_spins,
+        n_bonds, float(scale), ctypes.c_void_p(fields_ptr or None), n_fields,
+        ctypes.c_void_p(temps_ptr or None), n_temps,
+        ctypes.c_void_p(out_ptr or None), ctypes.c_void_p(stream_ptr)))
+    return 2 if n_fields * n_temps > 0 else 1
+
+
 def enumerate_device(lat: Lattice, start: int, end: int, counts_ptr: int,
                      stream_ptr: int, accumulate: bool = False,
                      algo: int = ALGO_AUTO) -> int:
@@ -303,6 +348,25 @@ def plan(lat: Lattice, n_configs_hint: int) -> tuple:
     if rc < 0:
         check(rc)
     return rc == 0, info
+
+
+def walk_plan(lat: Lattice, start: int, end: int, device=None) -> tuple:
+    """The plan a walk of [start, end) runs with on `device` (autotuned for
+    walks of >= 2^33 configurations): (usable, PlanInfo)."""
+    lib = load()
+    info = PlanInfo()
+    dev = current_device() if device is None else device
+    rc = lib.isd_walk_plan(ctypes.byref(lat), start, end, dev,
+                           ctypes.byref(info))
+    if rc < 0:
+        check(rc)
+    return rc == 0, info
+
+
+def plan_fingerprint(info: PlanInfo) -> str:
+    """Short stable digest of a plan (to compare plans across processes)."""
+    import hashlib
+    return hashlib.sha256(bytes(info)).hexdigest()[:16]
 
 
 def validate(lat: Lattice) -> None:

@@ -17,6 +17,8 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "isd_internal.h"
 
@@ -70,8 +72,28 @@ struct DevState {
   size_t d_buf_bytes = 0;
   void* h_stage = nullptr;  // pinned staging for the host-buffer calls
   size_t h_stage_bytes = 0;
+  // multi-device walks: the combined table (root), and local copies of
+  // tables of devices this one has no peer access to
+  unsigned long long* d_sum = nullptr;
+  size_t d_sum_bytes = 0;
+  unsigned long long* d_copies = nullptr;
+  size_t d_copies_bytes = 0;
 };
 static DevState g_dev[64];
+
+// (Re)allocate a device buffer of at least `bytes` on the current device.
+template <class T>
+static int ensure_buffer(T** ptr, size_t* have, size_t bytes,
+                         const char* what) {
+  if (*have >= bytes) return ISD_OK;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *have = 0;
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  *have = bytes;
+  return ISD_OK;
+}
 
 // Pinned host staging of at least `bytes` (grown on demand): host-buffer
 // calls copy through it so their transfers are true async DMA, not the
@@ -344,11 +366,22 @@ static void band_costs(const isd_lattice* lat, const isd_plan_info& info,
     if (it == g_cost.end()) {
       std::vector<double> c;
       // ~16 segments per item of a four-items-per-block launch, 64
-      // samples each (c5: ~0.3 s once per process and plan)
+      // samples each (c5: ~0.3 s once per process and plan; then from the
+      // disk cache)
       const int F = run_bits - 5;
       const int n_seg = (int)std::min<uint64_t>(1ull << F, 16ull * 4 * 148);
-      band_slot_cost(lat, info, hp.run_begin, hp.lane_mask, hp.lane_vec,
-                     run_bits, n_seg, 64, &c);
+      std::string blob;
+      if (cache_get("cost", k, &blob) && !blob.empty() &&
+          blob.size() % sizeof(double) == 0) {
+        c.resize(blob.size() / sizeof(double));
+        std::memcpy(c.data(), blob.data(), blob.size());
+      } else {
+        band_slot_cost(lat, info, hp.run_begin, hp.lane_mask, hp.lane_vec,
+                       run_bits, n_seg, 64, &c);
+        cache_put("cost", k,
+                  std::string(reinterpret_cast<const char*>(c.data()),
+                              c.size() * sizeof(double)));
+      }
       // the items cache names the curve by a hash of its rounded values
       uint64_t h = 1469598103934665603ull;
       for (double x : c) {
@@ -1017,6 +1050,253 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
   return issue_ops(ops, st, launches);
 }
 
+// ---- multi-device walks ----------------------------------------------------
+// One process drives several GPUs (enumeration.py:365-390's Pool and root sum,
+// PAPER.md:98-115's MPI reduce): each device walks its shards into its own
+// table on its own stream; the root device then reads every table over
+// NVLink (peer access) inside one kernel that forms the combined table — K4,
+// or K2a when thermodynamics follow (launch_thermo_set) — so no host sum and
+// no separate reduce launch.  Where peer access is unavailable the root
+// copies that table first (cudaMemcpyPeerAsync, still device to device).
+
+// Peer access from `root` to `dev` (enabled once per pair): true when the
+// root's kernels may read dev's memory directly.
+static bool peer_access(int root, int dev) {
+  if (root == dev) return true;
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, bool> known;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = known.find({root, dev});
+  if (it != known.end()) return it->second;
+  int can = 0;
+  bool ok = false;
+  if (cudaDeviceCanAccessPeer(&can, root, dev) == cudaSuccess && can) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(root);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(dev, 0);
+    ok = e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled;
+    cudaGetLastError();
+    cudaSetDevice(cur);
+  }
+  cudaGetLastError();
+  known[{root, dev}] = ok;
+  return ok;
+}
+
+// The reference's partition of [start, end) into n contiguous shards
+// (make_shards, enumeration.py:44-63: the first (end - start) mod n shards
+// are one longer; for n = 2^k over an aligned power-of-two range they are
+// the top-k-bit prefixes).
+static void split_range(uint64_t start, uint64_t end, int n,
+                        std::vector<uint64_t>* edge) {
+  const uint64_t len = end - start, q = len / (uint64_t)n,
+                 r = len % (uint64_t)n;
+  edge->resize(n + 1);
+  for (int i = 0; i <= n; ++i)
+    (*edge)[i] = start + (uint64_t)i * q + std::min<uint64_t>((uint64_t)i, r);
+}
+
+static int enumerate_multi(const isd_lattice* lat, uint64_t start,
+                           uint64_t end, int n_shards, const int* devs,
+                           int algo, uint64_t* counts_host, double* shard_ms,
+                           double* total_ms) {
+  char err[256];
+  int rc = validate_lattice(lat, err, sizeof err);
+  if (rc) return fail(rc, "%s", err);
+  if (n_shards < 1 || !devs)
+    return fail(ISD_EINVAL, "need n_shards >= 1 and a device list");
+  if (!counts_host) return fail(ISD_EINVAL, "counts pointer is NULL");
+  const uint64_t total = 1ull << lat->n_spins;
+  if (!(start <= end && end <= total))
+    return fail(ISD_EINVAL, "range [%llu, %llu) invalid for 2^%u configurations",
+                (unsigned long long)start, (unsigned long long)end,
+                lat->n_spins);
+  const bool flip = (algo & ISD_FLAG_FLIP_SYMMETRY) != 0;
+  uint64_t wstart = start, wend = end;
+  if (flip) {  // shards of the top-spin-down half, mirrored on the root
+    if (start != 0 || end != total)
+      return fail(ISD_EINVAL, "flip symmetry needs the full range [0, 2^N)");
+    wend = total / 2;
+  }
+  if ((uint64_t)n_shards > std::max<uint64_t>(wend - wstart, 1))
+    return fail(ISD_EINVAL, "%d shards for %llu configurations", n_shards,
+                (unsigned long long)(wend - wstart));
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(ISD_ENODEV, "no CUDA device available (%s)",
+                e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+  std::vector<int> uniq;  // distinct devices, root (devs[0]) first
+  for (int i = 0; i < n_shards; ++i) {
+    if (devs[i] < 0 || devs[i] >= ndev || devs[i] >= 64)
+      return fail(ISD_ENODEV, "device %d outside [0, %d)", devs[i], ndev);
+    if (std::find(uniq.begin(), uniq.end(), devs[i]) == uniq.end())
+      uniq.push_back(devs[i]);
+  }
+  if ((int)uniq.size() > kMaxTables)
+    return fail(ISD_EINVAL, "more than %d distinct devices", kMaxTables);
+  const int root = devs[0];
+  DeviceGuard guard;
+  // lock every device involved, in ascending order (no lock-order cycles
+  // with concurrent multi-device calls)
+  std::vector<int> order(uniq);
+  std::sort(order.begin(), order.end());
+  std::vector<std::unique_lock<std::mutex>> locks(order.size());
+  for (size_t j = 0; j < order.size(); ++j) {
+    DevState* s = nullptr;
+    rc = get_dev(order[j], &s, &locks[j]);
+    if (rc) return rc;
+  }
+  const size_t bytes =
+      (size_t)(lat->n_spins + 1) * (lat->n_bonds + 1) * sizeof(uint64_t);
+  for (int d : uniq) {
+    cudaSetDevice(d);
+    DevState& s = g_dev[d];
+    rc = ensure_buffer(&s.d_counts, &s.d_counts_bytes, bytes,
+                       "cudaMalloc(counts)");
+    if (rc) return rc;
+  }
+  cudaSetDevice(root);
+  DevState& R = g_dev[root];
+  rc = ensure_buffer(&R.d_sum, &R.d_sum_bytes, bytes, "cudaMalloc(sum)");
+  if (rc) return rc;
+  rc = ensure_buffer(&R.d_copies, &R.d_copies_bytes, bytes * uniq.size(),
+                     "cudaMalloc(table copies)");
+  if (rc) return rc;
+  std::vector<uint64_t> edge;
+  split_range(wstart, wend, n_shards, &edge);
+
+  // 1. prepare every shard's walk, one host thread per device (plans, a
+  // first large walk's autotune and NVRTC compiles run concurrently)
+  std::vector<std::vector<Op>> ops(n_shards);
+  std::vector<int> prc(uniq.size(), 0);
+  std::vector<std::string> perr(uniq.size()), kinfo(uniq.size());
+  auto prepare_dev = [&](size_t j) {
+    const int d = uniq[j];
+    cudaSetDevice(d);
+    bool first = true;
+    for (int i = 0; i < n_shards && !prc[j]; ++i) {
+      if (devs[i] != d) continue;
+      prc[j] = prepare_walk(lat, edge[i], edge[i + 1], algo & 0xff,
+                            g_dev[d].d_counts, first ? 0 : 1, false, &ops[i]);
+      first = false;
+      if (prc[j]) perr[j] = g_err;
+    }
+    kinfo[j] = g_kernel_info;
+  };
+  if (uniq.size() == 1) {
+    prepare_dev(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (size_t j = 0; j < uniq.size(); ++j) pool.emplace_back(prepare_dev, j);
+    for (std::thread& t : pool) t.join();
+  }
+  for (size_t j = 0; j < uniq.size(); ++j)
+    if (prc[j]) return fail(prc[j], "%s", perr[j].c_str());
+  g_kernel_info = kinfo[0];
+
+  // 2. issue: every device starts after the root's start event; each
+  // shard is bracketed by its own events on its device's stream
+  std::vector<cudaEvent_t> es(n_shards), ee(n_shards), done(uniq.size());
+  auto destroy_events = [&]() {
+    for (int i = 0; i < n_shards; ++i) {
+      if (es[i]) cudaEventDestroy(es[i]);
+      if (ee[i]) cudaEventDestroy(ee[i]);
+    }
+    for (cudaEvent_t x : done)
+      if (x) cudaEventDestroy(x);
+  };
+  std::fill(es.begin(), es.end(), nullptr);
+  std::fill(ee.begin(), ee.end(), nullptr);
+  std::fill(done.begin(), done.end(), nullptr);
+  cudaSetDevice(root);
+  cudaEventRecord(R.ev0, R.stream);
+  int nl = 0;
+  for (size_t j = 0; j < uniq.size(); ++j) {
+    const int d = uniq[j];
+    cudaSetDevice(d);
+    cudaStream_t st = g_dev[d].stream;
+    if (d != root) cudaStreamWaitEvent(st, R.ev0, 0);
+    for (int i = 0; i < n_shards; ++i) {
+      if (devs[i] != d) continue;
+      cudaEventCreate(&es[i]);
+      cudaEventCreate(&ee[i]);
+      cudaEventRecord(es[i], st);
+      int x = 0;
+      rc = issue_ops(ops[i], st, &x);
+      nl += x;
+      if (rc) {
+        destroy_events();
+        return rc;
+      }
+      cudaEventRecord(ee[i], st);
+    }
+    cudaEventCreateWithFlags(&done[j], cudaEventDisableTiming);
+    cudaEventRecord(done[j], st);
+  }
+  // 3. combine on the root: one kernel reads every device's table
+  cudaSetDevice(root);
+  TableSet tabs;
+  tabs.n = (int)uniq.size();
+  for (size_t j = 0; j < uniq.size(); ++j) {
+    const int d = uniq[j];
+    if (d != root) cudaStreamWaitEvent(R.stream, done[j], 0);
+    if (peer_access(root, d)) {
+      tabs.t[j] = g_dev[d].d_counts;
+    } else {
+      unsigned long long* copy = R.d_copies + j * (bytes / 8);
+      e = cudaMemcpyPeerAsync(copy, root, g_dev[d].d_counts, d, bytes,
+                              R.stream);
+      if (e != cudaSuccess) {
+        destroy_events();
+        return cuda_fail(e, "cudaMemcpyPeerAsync");
+      }
+      tabs.t[j] = copy;
+    }
+  }
+  int r = launch_gather(tabs, R.d_sum, lat->n_spins, lat->n_bonds, R.stream);
+  if (r >= 0 && flip) {
+    const int r2 = launch_mirror(R.d_sum, lat->n_spins, lat->n_bonds, R.stream);
+    r = r2 < 0 ? r2 : r + r2;
+  }
+  if (r < 0) {
+    destroy_events();
+    return cuda_fail((cudaError_t)(-r), "k4_gather launch");
+  }
+  nl += r;
+  bump_launches((uint64_t)nl);
+  cudaEventRecord(R.ev1, R.stream);
+  void* stage = nullptr;
+  rc = stage_buffer(&R, bytes, &stage);
+  if (rc) {
+    destroy_events();
+    return rc;
+  }
+  e = cudaMemcpyAsync(stage, R.d_sum, bytes, cudaMemcpyDeviceToHost,
+                      R.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(R.stream);
+  if (e != cudaSuccess) {
+    destroy_events();
+    return cuda_fail(e, "multi-device enumeration");
+  }
+  std::memcpy(counts_host, stage, bytes);
+  for (int i = 0; i < n_shards; ++i) {
+    float ms = 0.f;
+    cudaSetDevice(devs[i]);
+    cudaEventElapsedTime(&ms, es[i], ee[i]);
+    if (shard_ms) shard_ms[i] = ms;
+  }
+  cudaSetDevice(root);
+  if (total_ms) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, R.ev0, R.ev1);
+    *total_ms = ms;
+  }
+  destroy_events();
+  return ISD_OK;
+}
+
 }  // namespace isd
 
 using namespace isd;
@@ -1036,6 +1316,32 @@ int isd_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   if (rc) return rc;
   if (!out) return fail(ISD_EINVAL, "plan pointer is NULL");
   return cached_plan(lat, n_configs_hint, out);
+}
+
+int isd_walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
+                  int device, isd_plan_info* out) {
+  int rc = isd_validate(lat);
+  if (rc) return rc;
+  if (!out) return fail(ISD_EINVAL, "plan pointer is NULL");
+  if (!(start < end && end <= (1ull << lat->n_spins)))
+    return fail(ISD_EINVAL, "range [%llu, %llu) invalid for 2^%u configurations",
+                (unsigned long long)start, (unsigned long long)end,
+                lat->n_spins);
+  DeviceGuard guard;
+  DevState* s = nullptr;
+  std::unique_lock<std::mutex> lock;
+  rc = get_dev(device, &s, &lock);
+  if (rc) return rc;
+  int sms = 0;
+  rc = current_sm_count(&sms);
+  if (rc) return rc;
+  uint64_t top = 0;
+  rc = walk_plan(lat, start, end, sms, false, out, &top);
+  if (rc) return rc;
+  if (out->band_rows && !band_ok(*out, start, end) &&
+      !unbanded_plan(lat, end - start, out, top))
+    return fail(ISD_EINVAL, "no unbanded plan for an unaligned range");
+  return ISD_OK;
 }
 
 int isd_band_items(uint32_t free_bits, uint32_t n_target, uint32_t span,
@@ -1135,6 +1441,44 @@ int isd_enumerate(const isd_lattice* lat, uint64_t start, uint64_t end,
     cudaEventElapsedTime(&ms, s->ev0, s->ev1);
     *device_ms = ms;
   }
+  return ISD_OK;
+}
+
+int isd_enumerate_multi(const isd_lattice* lat, uint64_t start, uint64_t end,
+                        int n_shards, const int* devs, int algo,
+                        uint64_t* counts_host, double* shard_ms,
+                        double* total_ms) {
+  return enumerate_multi(lat, start, end, n_shards, devs, algo, counts_host,
+                         shard_ms, total_ms);
+}
+
+int isd_thermo_gather_async(const uint64_t* const* tables_dev, int n_tables,
+                            uint64_t* sum_dev, uint32_t n_spins,
+                            uint32_t n_bonds, double energy_scale,
+                            const double* fields_dev, int n_fields,
+                            const double* temps_dev, int n_temps,
+                            double* out_dev, void* stream) {
+  if (n_spins < 1 || n_spins > ISD_MAX_SPINS || n_bonds > 3 * ISD_MAX_SPINS)
+    return fail(ISD_EINVAL, "bad table shape N=%u B=%u", n_spins, n_bonds);
+  if (n_tables < 1 || n_tables > kMaxTables || !tables_dev)
+    return fail(ISD_EINVAL, "need 1..%d tables", kMaxTables);
+  if (n_fields < 0 || n_temps < 0)
+    return fail(ISD_EINVAL, "negative grid size");
+  if (!(energy_scale > 0)) return fail(ISD_EINVAL, "energy_scale must be > 0");
+  const bool grid = n_fields * n_temps > 0;
+  if ((grid && (!fields_dev || !temps_dev || !out_dev)) || (!grid && !sum_dev))
+    return fail(ISD_EINVAL, "NULL buffer");
+  TableSet tabs;
+  tabs.n = n_tables;
+  for (int i = 0; i < n_tables; ++i) {
+    if (!tables_dev[i]) return fail(ISD_EINVAL, "NULL table %d", i);
+    tabs.t[i] = reinterpret_cast<const unsigned long long*>(tables_dev[i]);
+  }
+  const int r = launch_thermo_set(
+      tabs, reinterpret_cast<unsigned long long*>(sum_dev), n_spins, n_bonds,
+      energy_scale, fields_dev, n_fields, temps_dev, n_temps, out_dev, stream);
+  if (r < 0) return cuda_fail((cudaError_t)(-r), "k2 gather launch");
+  bump_launches((uint64_t)r);
   return ISD_OK;
 }
 

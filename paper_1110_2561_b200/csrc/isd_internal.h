@@ -186,6 +186,21 @@ int jit_ready(const HoistParams& p, std::string* why);
 void jit_prefetch(const std::vector<HoistParams>& ps);
 int launch_mirror(unsigned long long* t, uint32_t n, uint32_t b,
                   void* stream);
+// the per-device tables of a multi-GPU walk, as seen from the root device
+// (peer pointers, or local copies where peer access is unavailable)
+constexpr int kMaxTables = 32;
+struct TableSet {
+  const unsigned long long* t[kMaxTables];
+  int n;
+};
+int launch_gather(const TableSet& tabs, unsigned long long* sum,
+                  uint32_t n_spins, uint32_t n_bonds, void* stream);
+// K2 over the sum of a table set (K2a also writes that sum when `sum` is
+// set; with an empty grid only the sum is formed, by K4)
+int launch_thermo_set(const TableSet& tabs, unsigned long long* sum,
+                      uint32_t n_spins, uint32_t n_bonds, double scale,
+                      const double* fields, int n_fields, const double* temps,
+                      int n_temps, double* out, void* stream);
 int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
                   uint32_t n_bonds, double scale, const double* fields,
                   int n_fields, const double* temps, int n_temps, double* out,

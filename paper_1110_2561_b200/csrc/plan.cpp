@@ -11,6 +11,7 @@
 #include <cstring>
 #include <vector>
 #include <atomic>
+#include <functional>
 #include <thread>
 
 #include "isd_internal.h"
@@ -778,20 +779,51 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   // random and domino lane patterns, so the CPU replay can check them)
   const bool wide = n_configs_hint >= (1ull << 33) ||
                     knob_long("ISD_PLAN_WIDE", 0) == 1;
+  // Each (copy-site set, band shape) variant is searched independently, so
+  // a batch of them runs on parallel host threads (the layout search of a
+  // large walk is seconds of CPU); results merge in submission order, so
+  // the plan does not depend on the thread count.
+  struct Variant {
+    isd_plan_info base;
+    std::vector<int> set;
+    bool climb;
+    int band_rows, band_span;
+    bool band_domino;
+    isd_plan_info out;
+    std::vector<isd_plan_info> all;
+  };
+  std::vector<Variant> batch;
   auto try_variant = [&](const isd_plan_info& base, const std::vector<int>& set,
                          bool climb, int band_rows, int band_span = kBandSpan,
                          bool band_domino = false) {
-    isd_plan_info cand = base;
-    bool all_even = true;
-    for (int site : set) all_even = all_even && !((odd >> site) & 1);
-    set_copy_sites(lat, &cand, set.data(), all_even ? 1 : 0);
-    choose_layout(lat, &cand, &all, wide, walk_bits, climb, band_rows,
-                  band_span, band_domino, top);
-    if (cand.est_per_config >= 1e29) return;  // no layout of that kind
-    if (!have || cand.est_per_config < best_info.est_per_config - 1e-9) {
-      best_info = cand;
-      have = true;
+    batch.push_back({base, set, climb, band_rows, band_span, band_domino,
+                     base, {}});
+  };
+  auto run_batch = [&]() {
+    auto one = [&](Variant& v) {
+      v.out = v.base;
+      bool all_even = true;
+      for (int site : v.set) all_even = all_even && !((odd >> site) & 1);
+      set_copy_sites(lat, &v.out, v.set.data(), all_even ? 1 : 0);
+      choose_layout(lat, &v.out, &v.all, wide, walk_bits, v.climb,
+                    v.band_rows, v.band_span, v.band_domino, top);
+    };
+    if (batch.size() == 1) {
+      one(batch[0]);
+    } else {
+      std::vector<std::thread> pool;
+      for (Variant& v : batch) pool.emplace_back(one, std::ref(v));
+      for (std::thread& t : pool) t.join();
     }
+    for (Variant& v : batch) {
+      all.insert(all.end(), v.all.begin(), v.all.end());
+      if (v.out.est_per_config >= 1e29) continue;  // no layout of that kind
+      if (!have || v.out.est_per_config < best_info.est_per_config - 1e-9) {
+        best_info = v.out;
+        have = true;
+      }
+    }
+    batch.clear();
   };
   // (large walks also hill-climb each set's lane patterns; the model's
   // estimates are only good to a few percent, so every set keeps its best
@@ -807,6 +839,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
     for (size_t v = 0; v < sets.size(); ++v)
       if (!force || std::strcmp(force, names[v]) == 0)
         try_variant(*info, sets[v], wide, 0);
+  run_batch();
   // Banded mode 2: when no unbanded mode-2 table fits (c5: 49 planes of all
   // 37 rows), a power-of-two walk can still run mode 2 with a table of
   // band_rows rows per work item; a shorter loop (l = 5) keeps the band
@@ -849,6 +882,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
             try_variant(base, bsets[v], wide, rows, span, domino);
       }
     }
+    run_batch();
   }
   if (!have) return 1;  // forced variant not available for this lattice
   *info = best_info;

@@ -56,9 +56,14 @@ __device__ __forceinline__ double warp_min(double v) {
 constexpr int kCompactThreads = 1024;
 static_assert(kMaxBins <= 5 * kCompactThreads, "<= 5 bins per thread");
 
+// K2a sums its input over up to kMaxTables tables (the per-device tables of
+// a multi-GPU walk, read over NVLink peer access) and, when `sum` is set,
+// writes the combined table there: the cross-device reduce is fused into the
+// compaction the thermodynamics needs anyway.
 __global__ void __launch_bounds__(kCompactThreads)
-    k2_compact(const unsigned long long* __restrict__ counts, uint32_t n,
-               uint32_t b, Cell* __restrict__ cells, int* __restrict__ n_cells) {
+    k2_compact(const TableSet tabs, unsigned long long* __restrict__ sum,
+               uint32_t n, uint32_t b, Cell* __restrict__ cells,
+               int* __restrict__ n_cells) {
   __shared__ int warp_tot[kCompactThreads / 32];
   const uint32_t stride = b + 1;
   const uint32_t nbins = (n + 1) * stride;
@@ -69,7 +74,11 @@ __global__ void __launch_bounds__(kCompactThreads)
 #pragma unroll
   for (int j = 0; j < 5; ++j) {
     const uint32_t i = lo + j;
-    g[j] = (j < (int)per && i < nbins) ? counts[i] : 0ull;
+    g[j] = 0ull;
+    if (j < (int)per && i < nbins) {
+      for (int t = 0; t < tabs.n; ++t) g[j] += tabs.t[t][i];
+      if (sum) sum[i] = g[j];
+    }
     mine += g[j] != 0;
   }
   // exclusive prefix of `mine` over the CTA: warp shuffle scan, then the
@@ -244,12 +253,47 @@ __global__ void __launch_bounds__(kThermoThreads)
   }
 }
 
+// K4: the combined table of several devices' tables (peer reads over
+// NVLink), for a multi-GPU walk that is not followed by K2.
+__global__ void __launch_bounds__(256)
+    k4_gather(const TableSet tabs, unsigned long long* __restrict__ sum,
+              uint32_t nbins) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nbins) return;
+  unsigned long long g = 0;
+  for (int t = 0; t < tabs.n; ++t) g += tabs.t[t][i];
+  sum[i] = g;
+}
+
+int launch_gather(const TableSet& tabs, unsigned long long* sum,
+                  uint32_t n_spins, uint32_t n_bonds, void* stream) {
+  const uint32_t nbins = (n_spins + 1) * (n_bonds + 1);
+  k4_gather<<<(nbins + 255) / 256, 256, 0, (cudaStream_t)stream>>>(tabs, sum,
+                                                                   nbins);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 1 : -(int)e;
+}
+
 int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
                   uint32_t n_bonds, double scale, const double* fields,
                   int n_fields, const double* temps, int n_temps, double* out,
                   void* stream) {
+  TableSet one;
+  one.n = 1;
+  one.t[0] = counts;
+  return launch_thermo_set(one, nullptr, n_spins, n_bonds, scale, fields,
+                           n_fields, temps, n_temps, out, stream);
+}
+
+int launch_thermo_set(const TableSet& tabs, unsigned long long* sum,
+                      uint32_t n_spins, uint32_t n_bonds, double scale,
+                      const double* fields, int n_fields, const double* temps,
+                      int n_temps, double* out, void* stream) {
   const int points = n_fields * n_temps;
-  if (points <= 0) return 0;
+  if (points <= 0) {
+    if (sum) return launch_gather(tabs, sum, n_spins, n_bonds, stream);
+    return 0;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   const size_t bins = (size_t)(n_spins + 1) * (n_bonds + 1);
   // stream-ordered scratch: safe for concurrent calls on different streams.
@@ -273,8 +317,8 @@ int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
   Cell* cells = reinterpret_cast<Cell*>(scratch);
   int* n_cells = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) +
                                         sizeof(Cell) * bins);
-  k2_compact<<<1, kCompactThreads, 0, st>>>(counts, n_spins, n_bonds, cells,
-                                            n_cells);
+  k2_compact<<<1, kCompactThreads, 0, st>>>(tabs, sum, n_spins, n_bonds,
+                                            cells, n_cells);
   const int grid = (points + kThermoPoints - 1) / kThermoPoints;
   k2_thermo<<<grid, kThermoThreads, 0, st>>>(cells, n_cells, scale, fields,
                                              temps, n_temps, points, out);

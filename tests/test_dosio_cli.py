@@ -226,6 +226,41 @@ def test_run_bench_on_gpu():
 
 
 @pytest.mark.gpu
+def test_run_bench_extended_record_and_report(tmp_path, capsys):
+    spec = isd.LatticeSpec(3, 3, 4)  # c5: the hoisted kernel's roofline
+    recs = bench_mod.run_bench(spec, [1, 2], repeats=1, roofline=True)
+    for r in recs:
+        assert r.num_gpus == 1
+        assert 0.3 < r.roofline_fraction < 1.05, r.roofline_fraction
+        assert 500 < r.sm_clock_mhz < 3000
+    rows = bench_mod.parse_scaling_report(bench_mod.emit_extended_report(recs))
+    assert [row["workers"] for row in rows] == [1, 2]
+    assert rows[0]["roofline_fraction"] == recs[0].roofline_fraction
+    # the CLI flag
+    assert main(["bench", "--rows", "3", "--cols", "3", "--workers", "1,2",
+                 "--repeats", "1", "--extended"]) == 0
+    out = capsys.readouterr().out
+    assert out.splitlines()[0] == bench_mod.EXTENDED_HEADER
+
+
+def test_extended_report_round_trip_without_gpu():
+    spec = isd.LatticeSpec(2, 2)
+    recs = [bench_mod.BenchRecord(spec, 1, 0.5, [0.5], 1.0, 32.0, 1, 0.9,
+                                  1965.0),
+            bench_mod.BenchRecord(spec, 2, 0.25, [0.2, 0.25], 2.0, 64.0, 1)]
+    text = bench_mod.emit_extended_report(recs)
+    assert text.splitlines()[0] == (
+        "rows,cols,depth,N,workers,wall_seconds,speedup,"
+        "gpus,configs_per_second,roofline_fraction,sm_mhz")
+    rows = bench_mod.parse_scaling_report(text)
+    assert rows[0]["roofline_fraction"] == 0.9 and rows[0]["sm_mhz"] == 1965.0
+    assert rows[1]["roofline_fraction"] is None and rows[1]["sm_mhz"] is None
+    # the reference report is unchanged
+    assert bench_mod.emit_scaling_report(recs).splitlines()[0] == \
+        bench_mod.REPORT_HEADER
+
+
+@pytest.mark.gpu
 def test_console_module_runs(tmp_path):
     out = tmp_path / "d.csv"
     r = subprocess.run([sys.executable, "-m", "paper_1110_2561_b200.cli", "dos",
