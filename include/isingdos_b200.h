@@ -235,6 +235,13 @@ int isd_plan(const isd_lattice* lat, uint64_t n_configs_hint,
 int isd_walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
                   int device, isd_plan_info* out);
 
+/* Install `plan` as the plan of walks of [start, end)'s size and top
+ * bits in this process (replacing the tuned one; not written to the disk
+ * cache).  For tools and tests that time one plan on several ranges; the
+ * plan must come from isd_plan / isd_walk_plan of the same lattice. */
+int isd_set_walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
+                      const isd_plan_info* plan);
+
 /* Generate and NVRTC-compile the lattice's specialised k1 kernel without
  * loading it (no GPU needed); *cubin_bytes = its size.  For tests. */
 int isd_jit_check(const isd_lattice* lat, uint64_t n_configs_hint,

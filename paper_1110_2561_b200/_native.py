@@ -31,7 +31,7 @@ EXPORTED_SYMBOLS = (
     "isd_launch_count", "isd_mirror_async", "isd_kernel_info",
     "isd_jit_check", "isd_band_items", "isd_set_knob", "isd_clear_knobs",
     "isd_set_cache_dirs", "isd_build_id", "isd_enumerate_multi",
-    "isd_thermo_gather_async", "isd_walk_plan",
+    "isd_thermo_gather_async", "isd_walk_plan", "isd_set_walk_plan",
 )
 
 
@@ -141,6 +141,9 @@ def load():
         lib.isd_walk_plan.argtypes = [p_lat, u64, u64, i32,
                                       ctypes.POINTER(PlanInfo)]
         lib.isd_walk_plan.restype = ctypes.c_int
+        lib.isd_set_walk_plan.argtypes = [p_lat, u64, u64,
+                                          ctypes.POINTER(PlanInfo)]
+        lib.isd_set_walk_plan.restype = ctypes.c_int
         lib.isd_set_cache_dirs.argtypes = [ctypes.c_char_p]
         lib.isd_set_cache_dirs.restype = ctypes.c_int
         lib.isd_build_id.restype = ctypes.c_char_p
@@ -361,6 +364,12 @@ def walk_plan(lat: Lattice, start: int, end: int, device=None) -> tuple:
     if rc < 0:
         check(rc)
     return rc == 0, info
+
+
+def set_walk_plan(lat: Lattice, start: int, end: int, info: PlanInfo) -> None:
+    """Use `info` for walks of [start, end)'s size and top bits (tools)."""
+    check(load().isd_set_walk_plan(ctypes.byref(lat), start, end,
+                                   ctypes.byref(info)))
 
 
 def plan_fingerprint(info: PlanInfo) -> str:

@@ -1344,6 +1344,34 @@ int isd_walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
   return ISD_OK;
 }
 
+int isd_set_walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
+                      const isd_plan_info* plan) {
+  int rc = isd_validate(lat);
+  if (rc) return rc;
+  if (!plan) return fail(ISD_EINVAL, "plan pointer is NULL");
+  if (!(start < end && end <= (1ull << lat->n_spins)))
+    return fail(ISD_EINVAL, "range [%llu, %llu) invalid for 2^%u configurations",
+                (unsigned long long)start, (unsigned long long)end,
+                lat->n_spins);
+  if (plan->u != ISD_COPY_BITS || plan->k != plan->u + plan->l ||
+      plan->k > lat->n_spins || plan->pair_mode > 2 ||
+      (size_t)plan->hist_words * 4 > 227 * 1024)
+    return fail(ISD_EINVAL, "not a hoisted-kernel plan of this lattice");
+  const uint64_t len = end - start;
+  const uint64_t top = (!(len & (len - 1)) && start % len == 0 &&
+                        knob_long("ISD_PLAN_TOP", 1) != 0)
+                           ? start
+                           : 0;
+  isd_plan_info model;
+  rc = cached_plan(lat, len, &model, top);  // (ranked list for fallbacks)
+  if (rc) return fail(ISD_EINVAL, "lattice too small for the hoisted kernel");
+  std::lock_guard<std::mutex> lock(g_plan_mu);
+  PlanEntry& pe = g_plans[plan_key(lat, len, top)];
+  pe.info = *plan;
+  pe.tuned = true;
+  return ISD_OK;
+}
+
 int isd_band_items(uint32_t free_bits, uint32_t n_target, uint32_t span,
                    const double* seg_cost, uint32_t n_seg, double flush_units,
                    uint64_t* out, uint32_t max_items, uint32_t* n_items,

@@ -10,10 +10,9 @@
 // (sum(w x)/s instead of sum((w/s) x)): same value to ~1e-16 relative.
 //
 // K2a compacts the occupied cells of the table once, in table order (a
-// block prefix scan); K2b gives each (h, T) point a team of four warps that
-// walk the same cell list; each lane
-// takes a fixed strided subset and the partials meet in a fixed xor-shuffle
-// tree.  A point's result therefore does not depend on which other points
+// block prefix scan); K2b gives each (h, T) point one CTA that walks the
+// cell list; each lane takes a fixed strided subset and the partials meet
+// in a fixed xor-shuffle tree.  A point's result therefore does not depend on which other points
 // share the launch (thermo_sweep(...)[0] == partition_point(...) exactly,
 // test_thermo.py:85-87).
 #include <cuda_runtime.h>
@@ -25,11 +24,8 @@
 
 namespace isd {
 
-constexpr int kThermoThreads = 256;                 // 8 warps
-constexpr int kTeam = 4;                            // warps per point
-constexpr int kTeamLanes = 32 * kTeam;
-constexpr int kThermoPoints = kThermoThreads / kTeamLanes;  // 2 per CTA
-constexpr int kKeep = 12;  // w of a lane's first 12 cells kept for pass 3
+constexpr int kThermoThreads = 256;  // one (h, T) point per CTA, 8 warps
+constexpr int kKeep = 8;  // cells per lane kept in registers (2048 cells)
 constexpr int kMaxBins = (ISD_MAX_SPINS + 1) * (3 * ISD_MAX_SPINS + 1);
 
 struct Cell {
@@ -116,131 +112,120 @@ __global__ void __launch_bounds__(kCompactThreads)
   if (threadIdx.x == kCompactThreads - 1) *n_cells = warp_tot[31];
 }
 
-// K2b: the observables, a team of kTeam warps per (h, T) point.
+// K2b: the observables, one CTA of 256 threads per (h, T) point.  Each lane
+// holds its (up to kKeep) cells' energy, count and weight in registers
+// across the three passes, and every pass ends in one block reduction (a
+// fixed xor-shuffle tree per warp, then the 8 warp partials in a fixed
+// order), so a point's value does not depend on the grid it is in.
+// (History: a four-warp team per point re-read its ~9 cells per lane from
+// L2 in every pass; the whole-CTA point keeps them: 11.4 -> ~4 us on c5.)
 __global__ void __launch_bounds__(kThermoThreads)
     k2_thermo(const Cell* __restrict__ cells, const int* __restrict__ n_cells,
               double scale, const double* __restrict__ fields,
               const double* __restrict__ temps, int n_temps, int n_points,
               double* __restrict__ out) {
+  constexpr int kWarps = kThermoThreads / 32;
+  __shared__ double part[kWarps][4];
   const int nc = *n_cells;
-  // a team of kTeam warps per point; partial results of the team's warps
-  // meet in shared memory in a fixed order (deterministic)
-  __shared__ double part[kThermoThreads / 32][4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int team = warp / kTeam, tw = warp % kTeam;
-  const int tl = tw * 32 + lane;  // lane within the team
-  const int point_raw = blockIdx.x * kThermoPoints + team;
-  const int point = point_raw < n_points ? point_raw : n_points - 1;
+  const int tl = threadIdx.x;
+  const int point = blockIdx.x;
+  if (point >= n_points) return;  // (uniform per CTA)
   const double h = fields[point / n_temps];
   const double t = temps[point % n_temps];
-  auto team_sum = [&](double v, int slot) {
-    v = warp_sum(v);
-    if (lane == 0) part[warp][slot] = v;
+  // block reduction of NV values (sum, or min when `is_min`)
+  auto block_reduce = [&](double* v, int nv, bool is_min) {
+    for (int k = 0; k < nv; ++k)
+      v[k] = is_min ? warp_min(v[k]) : warp_sum(v[k]);
+    if (lane == 0)
+      for (int k = 0; k < nv; ++k) part[warp][k] = v[k];
     __syncthreads();
-    double r = 0.0;
+    for (int k = 0; k < nv; ++k) {
+      double r = part[0][k];
 #pragma unroll
-    for (int w = 0; w < kTeam; ++w) r += part[team * kTeam + w][slot];
-    return r;
+      for (int w = 1; w < kWarps; ++w)
+        r = is_min ? fmin(r, part[w][k]) : r + part[w][k];
+      v[k] = r;
+    }
+    __syncthreads();
   };
 
-  // pass 1: shift = max over occupied cells of x = -H / T.  Division by
-  // T > 0 is monotone, so that max is exactly -H_min / T: one division per
-  // point instead of one per cell.
-  double hmin = INFINITY;
-  for (int i = tl; i < nc; i += kTeamLanes) {
-    const double m = (double)cells[i].m;
-    const double e = (double)cells[i].e * scale;
-    hmin = fmin(hmin, e - h * m);
-  }
-  hmin = warp_min(hmin);
-  if (lane == 0) part[warp][0] = hmin;
-  __syncthreads();
-  double hlo = part[team * kTeam][0];
-#pragma unroll
-  for (int w = 1; w < kTeam; ++w) hlo = fmin(hlo, part[team * kTeam + w][0]);
-  const double shift = -hlo / t;
-  __syncthreads();
-
-  // pass 2: w = g exp(x - shift); s = sum w and the first moments as
-  // w-weighted sums (divided by s afterwards).  A lane keeps the w of its
-  // first kKeep cells in registers for pass 3 (the rest are recomputed).
-  // Two independent accumulators per lane hide the exp latency; they are
-  // combined in a fixed order, then across lanes and warps.
-  double wk[kKeep];
-  double s2[2] = {0, 0}, u2[2] = {0, 0}, m2[2] = {0, 0}, a2[2] = {0, 0};
-  auto weight = [&](int i, double* en_out, double* m_out) {
-    const double m = (double)cells[i].m;
-    const double e = (double)cells[i].e * scale;
-    const double en = e - h * m;
-    *en_out = en;
-    *m_out = m;
-    return cells[i].g * exp(-en / t - shift);
-  };
+  // pass 1: each lane's cells (energy H = E - h M kept), shift = max of
+  // x = -H / T = -H_min / T (division by T > 0 is monotone: one division)
+  double en[kKeep], mm[kKeep], gg[kKeep];
+  double red[4];
+  red[0] = INFINITY;
 #pragma unroll
   for (int j = 0; j < kKeep; ++j) {
-    const int i = tl + kTeamLanes * j;
-    wk[j] = 0.0;
+    const int i = tl + kThermoThreads * j;
+    en[j] = 0.0;
+    mm[j] = 0.0;
+    gg[j] = 0.0;
     if (i < nc) {
-      double en, m;
-      const double w = weight(i, &en, &m);
-      wk[j] = w;
-      s2[j & 1] += w;
-      u2[j & 1] += w * en;
-      m2[j & 1] += w * m;
-      a2[j & 1] += w * fabs(m);
+      const Cell c = cells[i];
+      mm[j] = (double)c.m;
+      en[j] = (double)c.e * scale - h * mm[j];
+      gg[j] = c.g;
+      red[0] = fmin(red[0], en[j]);
     }
   }
-  for (int i0 = tl + kTeamLanes * kKeep; i0 < nc; i0 += 2 * kTeamLanes) {
+  for (int i = tl + kThermoThreads * kKeep; i < nc; i += kThermoThreads) {
+    const double m = (double)cells[i].m;
+    red[0] = fmin(red[0], (double)cells[i].e * scale - h * m);
+  }
+  block_reduce(red, 1, true);
+  const double shift = -red[0] / t;
+
+  // pass 2: w = g exp(x - shift); s = sum w and the first moments as
+  // w-weighted sums (divided by s afterwards)
+  double wk[kKeep];
+  red[0] = red[1] = red[2] = red[3] = 0.0;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int i = i0 + kTeamLanes * j;
-      if (i < nc) {
-        double en, m;
-        const double w = weight(i, &en, &m);
-        s2[j] += w;
-        u2[j] += w * en;
-        m2[j] += w * m;
-        a2[j] += w * fabs(m);
-      }
-    }
+  for (int j = 0; j < kKeep; ++j) {
+    // (off the list: no exp — exp(-shift) alone may overflow)
+    wk[j] = gg[j] != 0.0 ? gg[j] * exp(-en[j] / t - shift) : 0.0;
+    red[0] += wk[j];
+    red[1] += wk[j] * en[j];
+    red[2] += wk[j] * mm[j];
+    red[3] += wk[j] * fabs(mm[j]);
   }
-  const double s = team_sum(s2[0] + s2[1], 0);
-  const double u = team_sum(u2[0] + u2[1], 1) / s;
-  const double mean_m = team_sum(m2[0] + m2[1], 2) / s;
-  const double mean_abs = team_sum(a2[0] + a2[1], 3) / s;
-  __syncthreads();
+  for (int i = tl + kThermoThreads * kKeep; i < nc; i += kThermoThreads) {
+    const double m = (double)cells[i].m;
+    const double e = (double)cells[i].e * scale - h * m;
+    const double w = cells[i].g * exp(-e / t - shift);
+    red[0] += w;
+    red[1] += w * e;
+    red[2] += w * m;
+    red[3] += w * fabs(m);
+  }
+  block_reduce(red, 4, false);
+  const double s = red[0];
+  const double u = red[1] / s;
+  const double mean_m = red[2] / s;
+  const double mean_abs = red[3] / s;
 
   // pass 3: central second moments (the two-pass form of thermo.py:75-77;
   // the raw <H^2> - <H>^2 form cancels catastrophically at low T)
-  double e2[2] = {0, 0}, v2[2] = {0, 0};
+  red[0] = red[1] = 0.0;
 #pragma unroll
   for (int j = 0; j < kKeep; ++j) {
-    const int i = tl + kTeamLanes * j;
-    if (i < nc) {
-      const double m = (double)cells[i].m;
-      const double en = (double)cells[i].e * scale - h * m;
-      const double de = en - u, dm = m - mean_m;
-      e2[j & 1] += wk[j] * (de * de);
-      v2[j & 1] += wk[j] * (dm * dm);
-    }
+    const double de = en[j] - u, dm = mm[j] - mean_m;
+    red[0] += wk[j] * (de * de);
+    red[1] += wk[j] * (dm * dm);
   }
-  for (int i0 = tl + kTeamLanes * kKeep; i0 < nc; i0 += 2 * kTeamLanes) {
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const int i = i0 + kTeamLanes * j;
-      if (i < nc) {
-        double en, m;
-        const double w = weight(i, &en, &m);
-        const double de = en - u, dm = m - mean_m;
-        e2[j] += w * (de * de);
-        v2[j] += w * (dm * dm);
-      }
-    }
+  for (int i = tl + kThermoThreads * kKeep; i < nc; i += kThermoThreads) {
+    const double m = (double)cells[i].m;
+    const double e = (double)cells[i].e * scale - h * m;
+    const double w = cells[i].g * exp(-e / t - shift);
+    const double de = e - u, dm = m - mean_m;
+    red[0] += w * (de * de);
+    red[1] += w * (dm * dm);
   }
-  const double ve = team_sum(e2[0] + e2[1], 0) / s;
-  const double vm = team_sum(v2[0] + v2[1], 1) / s;
+  block_reduce(red, 2, false);
+  const double ve = red[0] / s;
+  const double vm = red[1] / s;
 
-  if (tl == 0 && point_raw < n_points) {
+  if (tl == 0) {
     const double log_z = shift + log(s);
     double* o = out + (size_t)point * ISD_THERMO_FIELDS;
     o[0] = log_z;
@@ -319,7 +304,7 @@ int launch_thermo_set(const TableSet& tabs, unsigned long long* sum,
                                         sizeof(Cell) * bins);
   k2_compact<<<1, kCompactThreads, 0, st>>>(tabs, sum, n_spins, n_bonds,
                                             cells, n_cells);
-  const int grid = (points + kThermoPoints - 1) / kThermoPoints;
+  const int grid = points;
   k2_thermo<<<grid, kThermoThreads, 0, st>>>(cells, n_cells, scale, fields,
                                              temps, n_temps, points, out);
   e = cudaGetLastError();
