@@ -300,8 +300,8 @@ def roofline(wl, cal, clk, sm_count, cfg_per_launch, ms_k1, kernel="k1",
 # multi-GPU projection from one GPU, and cold start
 # --------------------------------------------------------------------------
 
-# NVLink read latency of the root's gather (peer loads of P tables inside
-# K2a), which a one-GPU emulation cannot see: a conservative allowance
+# NVLink read latency of the root's gather (K4: peer loads of the P tables),
+# which a one-GPU emulation cannot see: a conservative allowance
 NVLINK_GATHER_ALLOWANCE_MS = 0.003
 
 

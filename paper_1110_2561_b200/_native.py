@@ -301,7 +301,8 @@ def thermo_gather_device(table_ptrs, sum_ptr, n_spins, n_bonds, scale,
         n_bonds, float(scale), ctypes.c_void_p(fields_ptr or None), n_fields,
         ctypes.c_void_p(temps_ptr or None), n_temps,
         ctypes.c_void_p(out_ptr or None), ctypes.c_void_p(stream_ptr)))
-    return 2 if n_fields * n_temps > 0 else 1
+    gather = 1 if len(table_ptrs) > 1 or sum_ptr else 0  # K4
+    return gather + (1 if n_fields * n_temps > 0 else 0)   # + K2
 
 
 def enumerate_device(lat: Lattice, start: int, end: int, counts_ptr: int,
@@ -340,7 +341,7 @@ def thermo_device(counts_ptr, n_spins, n_bonds, scale, fields_ptr, n_fields,
                                n_fields, ctypes.c_void_p(temps_ptr), n_temps,
                                ctypes.c_void_p(out_ptr),
                                ctypes.c_void_p(stream_ptr)))
-    return 2 if n_fields * n_temps > 0 else 0  # K2a compaction + K2b
+    return 1 if n_fields * n_temps > 0 else 0  # K2
 
 
 def plan(lat: Lattice, n_configs_hint: int) -> tuple:

@@ -9,12 +9,25 @@
 // moments are accumulated as w-weighted sums and divided by s once
 // (sum(w x)/s instead of sum((w/s) x)): same value to ~1e-16 relative.
 //
-// K2a compacts the occupied cells of the table once, in table order (a
-// block prefix scan); K2b gives each (h, T) point one CTA that walks the
-// cell list; each lane takes a fixed strided subset and the partials meet
-// in a fixed xor-shuffle tree.  A point's result therefore does not depend on which other points
-// share the launch (thermo_sweep(...)[0] == partition_point(...) exactly,
+// One kernel, one CTA of 256 threads per (h, T) point, straight from the
+// dense table (no compaction pass: an empty bin has g = 0 and adds 0).  Warp
+// w takes rows m = w, w + 8, ...; lane j takes the columns e = j + 32 c.
+// The Boltzmann weight factorises over the table's axes:
+//     exp(x - shift) = exp(-(E - H_min) / T) * exp(h M / T) = a_e * b_m,
+// so a point needs <= 4 exponentials per lane (its columns) plus one per row
+// instead of one per occupied cell; every bin then costs a few DFMAs.  The
+// factors stay inside fp64 range while |h| N / T <= 300 (a_e, b_m <= e^300);
+// beyond that the kernel takes one exp of the whole argument per occupied
+// bin.  The product differs from exp(x - shift) by a few ulp (the GPU tests
+// hold every field to 1e-12 of the reference).  Each pass ends in a fixed
+// block reduction (xor-shuffle tree per warp, then the 8 warp partials in
+// order), so a point's value does not depend on which other points share
+// the launch (thermo_sweep(...)[0] == partition_point(...) exactly,
 // test_thermo.py:85-87).
+//
+// (History: one CTA per point over the whole table 42 us -> warp per point
+// over a per-CTA compacted cell list 33 us -> separate one-CTA compaction +
+// four-warp teams 16.5 us (c5, 702 points) -> this kernel.)
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -24,15 +37,12 @@
 
 namespace isd {
 
-constexpr int kThermoThreads = 256;  // one (h, T) point per CTA, 8 warps
-constexpr int kKeep = 8;  // cells per lane kept in registers (2048 cells)
-constexpr int kMaxBins = (ISD_MAX_SPINS + 1) * (3 * ISD_MAX_SPINS + 1);
-
-struct Cell {
-  double g;  // count (exact in fp64 below 2^53)
-  float m;   // M = 2 m_idx - N
-  int e;     // 2 e_idx - B (E = e * |J|)
-};
+constexpr int kThermoThreads = 256;  // one (h, T) point per CTA
+constexpr int kThermoWarps = kThermoThreads / 32;
+constexpr int kColSlots = 4;         // columns per lane: B + 1 <= 128
+static_assert(3 * ISD_MAX_SPINS + 1 <= 32 * kColSlots, "columns per lane");
+// weights factorise while every factor stays below e^kSplitMax
+constexpr double kSplitMax = 300.0;
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -47,93 +57,19 @@ __device__ __forceinline__ double warp_min(double v) {
   return v;
 }
 
-// K2a: compact the occupied cells of the table, in table order, into a
-// scratch list (one CTA, <= 5 bins per thread, shuffle scans).
-constexpr int kCompactThreads = 1024;
-static_assert(kMaxBins <= 5 * kCompactThreads, "<= 5 bins per thread");
-
-// K2a sums its input over up to kMaxTables tables (the per-device tables of
-// a multi-GPU walk, read over NVLink peer access) and, when `sum` is set,
-// writes the combined table there: the cross-device reduce is fused into the
-// compaction the thermodynamics needs anyway.
-__global__ void __launch_bounds__(kCompactThreads)
-    k2_compact(const TableSet tabs, unsigned long long* __restrict__ sum,
-               uint32_t n, uint32_t b, Cell* __restrict__ cells,
-               int* __restrict__ n_cells) {
-  __shared__ int warp_tot[kCompactThreads / 32];
-  const uint32_t stride = b + 1;
-  const uint32_t nbins = (n + 1) * stride;
-  const uint32_t per = (nbins + kCompactThreads - 1) / kCompactThreads;  // <= 5
-  const uint32_t lo = threadIdx.x * per;
-  unsigned long long g[5];
-  int mine = 0;
-#pragma unroll
-  for (int j = 0; j < 5; ++j) {
-    const uint32_t i = lo + j;
-    g[j] = 0ull;
-    if (j < (int)per && i < nbins) {
-      for (int t = 0; t < tabs.n; ++t) g[j] += tabs.t[t][i];
-      if (sum) sum[i] = g[j];
-    }
-    mine += g[j] != 0;
-  }
-  // exclusive prefix of `mine` over the CTA: warp shuffle scan, then the
-  // warp totals scanned by warp 0
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = mine;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) warp_tot[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    int t = warp_tot[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += v;
-    }
-    warp_tot[lane] = t;  // inclusive over warps
-  }
-  __syncthreads();
-  int pos = (warp ? warp_tot[warp - 1] : 0) + incl - mine;
-#pragma unroll
-  for (int j = 0; j < 5; ++j) {
-    if (!g[j]) continue;
-    const uint32_t i = lo + j;
-    const int mi = (int)(i / stride), ei = (int)(i - mi * stride);
-    cells[pos].g = (double)g[j];
-    cells[pos].m = (float)(2 * mi - (int)n);
-    cells[pos].e = 2 * ei - (int)b;
-    ++pos;
-  }
-  if (threadIdx.x == kCompactThreads - 1) *n_cells = warp_tot[31];
-}
-
-// K2b: the observables, one CTA of 256 threads per (h, T) point.  Each lane
-// holds its (up to kKeep) cells' energy, count and weight in registers
-// across the three passes, and every pass ends in one block reduction (a
-// fixed xor-shuffle tree per warp, then the 8 warp partials in a fixed
-// order), so a point's value does not depend on the grid it is in.
-// (History: a four-warp team per point re-read its ~9 cells per lane from
-// L2 in every pass; the whole-CTA point keeps them: 11.4 -> ~4 us on c5.)
 __global__ void __launch_bounds__(kThermoThreads)
-    k2_thermo(const Cell* __restrict__ cells, const int* __restrict__ n_cells,
-              double scale, const double* __restrict__ fields,
+    k2_thermo(const unsigned long long* __restrict__ table, uint32_t n,
+              uint32_t b, double scale, const double* __restrict__ fields,
               const double* __restrict__ temps, int n_temps, int n_points,
               double* __restrict__ out) {
-  constexpr int kWarps = kThermoThreads / 32;
-  __shared__ double part[kWarps][4];
-  const int nc = *n_cells;
+  __shared__ double part[kThermoWarps][4];
+  __shared__ double bm_s[ISD_MAX_SPINS + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tl = threadIdx.x;
   const int point = blockIdx.x;
   if (point >= n_points) return;  // (uniform per CTA)
   const double h = fields[point / n_temps];
   const double t = temps[point % n_temps];
-  // block reduction of NV values (sum, or min when `is_min`)
+  const int rows = (int)n + 1, cols = (int)b + 1;
   auto block_reduce = [&](double* v, int nv, bool is_min) {
     for (int k = 0; k < nv; ++k)
       v[k] = is_min ? warp_min(v[k]) : warp_sum(v[k]);
@@ -143,60 +79,67 @@ __global__ void __launch_bounds__(kThermoThreads)
     for (int k = 0; k < nv; ++k) {
       double r = part[0][k];
 #pragma unroll
-      for (int w = 1; w < kWarps; ++w)
+      for (int w = 1; w < kThermoWarps; ++w)
         r = is_min ? fmin(r, part[w][k]) : r + part[w][k];
       v[k] = r;
     }
     __syncthreads();
   };
+  auto count = [&](int r, int e) {
+    return (double)__ldg(table + (size_t)r * cols + e);
+  };
+  double ecol[kColSlots];  // E of this lane's columns
+#pragma unroll
+  for (int c = 0; c < kColSlots; ++c)
+    ecol[c] = (double)(2 * (lane + 32 * c) - (int)b) * scale;
 
-  // pass 1: each lane's cells (energy H = E - h M kept), shift = max of
-  // x = -H / T = -H_min / T (division by T > 0 is monotone: one division)
-  double en[kKeep], mm[kKeep], gg[kKeep];
+  // pass 1: H_min = min over occupied bins of E - h M; shift = -H_min / T
+  // (= max of x = -H / T: division by T > 0 is monotone)
   double red[4];
   red[0] = INFINITY;
+  for (int r = warp; r < rows; r += kThermoWarps) {
+    const double m = (double)(2 * r - (int)n);
 #pragma unroll
-  for (int j = 0; j < kKeep; ++j) {
-    const int i = tl + kThermoThreads * j;
-    en[j] = 0.0;
-    mm[j] = 0.0;
-    gg[j] = 0.0;
-    if (i < nc) {
-      const Cell c = cells[i];
-      mm[j] = (double)c.m;
-      en[j] = (double)c.e * scale - h * mm[j];
-      gg[j] = c.g;
-      red[0] = fmin(red[0], en[j]);
+    for (int c = 0; c < kColSlots; ++c) {
+      const int e = lane + 32 * c;
+      if (e < cols && count(r, e) != 0.0) red[0] = fmin(red[0], ecol[c] - h * m);
     }
   }
-  for (int i = tl + kThermoThreads * kKeep; i < nc; i += kThermoThreads) {
-    const double m = (double)cells[i].m;
-    red[0] = fmin(red[0], (double)cells[i].e * scale - h * m);
-  }
   block_reduce(red, 1, true);
-  const double shift = -red[0] / t;
-
-  // pass 2: w = g exp(x - shift); s = sum w and the first moments as
-  // w-weighted sums (divided by s afterwards)
-  double wk[kKeep];
-  red[0] = red[1] = red[2] = red[3] = 0.0;
+  const double hmin = red[0];
+  const double shift = -hmin / t;
+  const bool split = fabs(h) * (double)n / t <= kSplitMax;
+  // the factors: a_e per lane column, b_m per row (shared)
+  double acol[kColSlots];
 #pragma unroll
-  for (int j = 0; j < kKeep; ++j) {
-    // (off the list: no exp — exp(-shift) alone may overflow)
-    wk[j] = gg[j] != 0.0 ? gg[j] * exp(-en[j] / t - shift) : 0.0;
-    red[0] += wk[j];
-    red[1] += wk[j] * en[j];
-    red[2] += wk[j] * mm[j];
-    red[3] += wk[j] * fabs(mm[j]);
-  }
-  for (int i = tl + kThermoThreads * kKeep; i < nc; i += kThermoThreads) {
-    const double m = (double)cells[i].m;
-    const double e = (double)cells[i].e * scale - h * m;
-    const double w = cells[i].g * exp(-e / t - shift);
-    red[0] += w;
-    red[1] += w * e;
-    red[2] += w * m;
-    red[3] += w * fabs(m);
+  for (int c = 0; c < kColSlots; ++c)
+    acol[c] = split ? exp(-(ecol[c] - hmin) / t) : 0.0;
+  if (split)
+    for (int r = threadIdx.x; r < rows; r += kThermoThreads)
+      bm_s[r] = exp(h * (double)(2 * r - (int)n) / t);
+  __syncthreads();
+  // w of bin (r, e): g a_e b_m, or (beyond the split range) one exp of the
+  // whole argument for an occupied bin
+  auto weight = [&](double g, int c, int r, double en) {
+    if (split) return g * acol[c] * bm_s[r];
+    return g != 0.0 ? g * exp(-(en - hmin) / t) : 0.0;
+  };
+
+  // pass 2: s = sum w and the first moments as w-weighted sums
+  red[0] = red[1] = red[2] = red[3] = 0.0;
+  for (int r = warp; r < rows; r += kThermoWarps) {
+    const double m = (double)(2 * r - (int)n);
+#pragma unroll
+    for (int c = 0; c < kColSlots; ++c) {
+      const int e = lane + 32 * c;
+      if (e >= cols) continue;
+      const double en = ecol[c] - h * m;
+      const double w = weight(count(r, e), c, r, en);
+      red[0] += w;
+      red[1] += w * en;
+      red[2] += w * m;
+      red[3] += w * fabs(m);
+    }
   }
   block_reduce(red, 4, false);
   const double s = red[0];
@@ -207,25 +150,25 @@ __global__ void __launch_bounds__(kThermoThreads)
   // pass 3: central second moments (the two-pass form of thermo.py:75-77;
   // the raw <H^2> - <H>^2 form cancels catastrophically at low T)
   red[0] = red[1] = 0.0;
+  for (int r = warp; r < rows; r += kThermoWarps) {
+    const double m = (double)(2 * r - (int)n);
+    const double dm = m - mean_m;
 #pragma unroll
-  for (int j = 0; j < kKeep; ++j) {
-    const double de = en[j] - u, dm = mm[j] - mean_m;
-    red[0] += wk[j] * (de * de);
-    red[1] += wk[j] * (dm * dm);
-  }
-  for (int i = tl + kThermoThreads * kKeep; i < nc; i += kThermoThreads) {
-    const double m = (double)cells[i].m;
-    const double e = (double)cells[i].e * scale - h * m;
-    const double w = cells[i].g * exp(-e / t - shift);
-    const double de = e - u, dm = m - mean_m;
-    red[0] += w * (de * de);
-    red[1] += w * (dm * dm);
+    for (int c = 0; c < kColSlots; ++c) {
+      const int e = lane + 32 * c;
+      if (e >= cols) continue;
+      const double en = ecol[c] - h * m;
+      const double w = weight(count(r, e), c, r, en);
+      const double de = en - u;
+      red[0] += w * (de * de);
+      red[1] += w * (dm * dm);
+    }
   }
   block_reduce(red, 2, false);
   const double ve = red[0] / s;
   const double vm = red[1] / s;
 
-  if (tl == 0) {
+  if (threadIdx.x == 0) {
     const double log_z = shift + log(s);
     double* o = out + (size_t)point * ISD_THERMO_FIELDS;
     o[0] = log_z;
@@ -270,46 +213,55 @@ int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
                            n_fields, temps, n_temps, out, stream);
 }
 
+// K2 over the sum of a table set: one table is read in place; several are
+// first summed by K4 (each read once, e.g. over NVLink) into `sum`, or into
+// stream-ordered scratch when the caller wants no sum.
 int launch_thermo_set(const TableSet& tabs, unsigned long long* sum,
                       uint32_t n_spins, uint32_t n_bonds, double scale,
                       const double* fields, int n_fields, const double* temps,
                       int n_temps, double* out, void* stream) {
   const int points = n_fields * n_temps;
-  if (points <= 0) {
-    if (sum) return launch_gather(tabs, sum, n_spins, n_bonds, stream);
-    return 0;
-  }
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t bins = (size_t)(n_spins + 1) * (n_bonds + 1);
-  // stream-ordered scratch: safe for concurrent calls on different streams.
-  // Keep freed blocks in the device's default pool (threshold 64 MiB) so a
-  // steady stream of calls does not go back to the driver every time.
-  static std::once_flag pool_ready[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 64)
-    std::call_once(pool_ready[dev], [dev] {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = 64ull << 20;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-      cudaGetLastError();
-    });
+  int launched = 0;
+  const unsigned long long* table = tabs.t[0];
   void* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(&scratch, sizeof(Cell) * bins + 16, st);
-  if (e != cudaSuccess) return -(int)e;
-  Cell* cells = reinterpret_cast<Cell*>(scratch);
-  int* n_cells = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) +
-                                        sizeof(Cell) * bins);
-  k2_compact<<<1, kCompactThreads, 0, st>>>(tabs, sum, n_spins, n_bonds,
-                                            cells, n_cells);
-  const int grid = points;
-  k2_thermo<<<grid, kThermoThreads, 0, st>>>(cells, n_cells, scale, fields,
-                                             temps, n_temps, points, out);
-  e = cudaGetLastError();
-  cudaFreeAsync(scratch, st);
-  return e == cudaSuccess ? 2 : -(int)e;
+  if (tabs.n > 1 || sum) {
+    unsigned long long* dst = sum;
+    if (!dst) {
+      // stream-ordered scratch, kept in the device's default pool
+      // (threshold 64 MiB) so steady calls do not go back to the driver
+      static std::once_flag pool_ready[64];
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (dev < 64)
+        std::call_once(pool_ready[dev], [dev] {
+          cudaMemPool_t pool;
+          if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = 64ull << 20;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold,
+                                    &thr);
+          }
+          cudaGetLastError();
+        });
+      const size_t bytes = (size_t)(n_spins + 1) * (n_bonds + 1) * 8;
+      cudaError_t e = cudaMallocAsync(&scratch, bytes, st);
+      if (e != cudaSuccess) return -(int)e;
+      dst = reinterpret_cast<unsigned long long*>(scratch);
+    }
+    const int r = launch_gather(tabs, dst, n_spins, n_bonds, st);
+    if (r < 0) return r;
+    launched += r;
+    table = dst;
+  }
+  if (points > 0) {
+    k2_thermo<<<points, kThermoThreads, 0, st>>>(table, n_spins, n_bonds,
+                                                 scale, fields, temps, n_temps,
+                                                 points, out);
+    ++launched;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (scratch) cudaFreeAsync(scratch, st);
+  return e == cudaSuccess ? launched : -(int)e;
 }
 
 }  // namespace isd

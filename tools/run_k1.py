@@ -48,7 +48,8 @@ def main():
         if not ok:
             return 1
     from paper_1110_2561_b200.enumeration import native_lattice
-    ok, info = _native.plan(native_lattice(spec), sh.size)
+    ok, info = _native.walk_plan(native_lattice(spec), sh.start_index,
+                                 sh.end_index)
     print(f"  plan: mode={info.e_mode} sites={list(info.copy_site)} "
           f"A,B,P={info.row_words},{info.e_words},{info.plane_words} "
           f"lane_mask={info.lane_mask:#x} est={info.est_wavefronts:.3f}")
