@@ -9,25 +9,30 @@
 // moments are accumulated as w-weighted sums and divided by s once
 // (sum(w x)/s instead of sum((w/s) x)): same value to ~1e-16 relative.
 //
-// One kernel, one CTA of 256 threads per (h, T) point, straight from the
-// dense table (no compaction pass: an empty bin has g = 0 and adds 0).  Warp
-// w takes rows m = w, w + 8, ...; lane j takes the columns e = j + 32 c.
-// The Boltzmann weight factorises over the table's axes:
+// One kernel; a CTA of 256 threads evaluates 8 (h, T) points, one per warp.
+// The CTA first compacts the occupied bins of the table (32 KB, L2-resident)
+// into shared memory — warp w takes rows m = w, w + 8, ..., lane j the
+// columns e = j + 32 c, all loaded at once; one block scan of the per-
+// thread counts places the cells.  Each warp then evaluates its point from
+// that list with warp shuffles only (no further block barrier: the kernel
+// is latency-bound, and a point's critical path is what it costs).  The
+// Boltzmann weight factorises over the table's axes:
 //     exp(x - shift) = exp(-(E - H_min) / T) * exp(h M / T) = a_e * b_m,
-// so a point needs <= 4 exponentials per lane (its columns) plus one per row
-// instead of one per occupied cell; every bin then costs a few DFMAs.  The
-// factors stay inside fp64 range while |h| N / T <= 300 (a_e, b_m <= e^300);
-// beyond that the kernel takes one exp of the whole argument per occupied
-// bin.  The product differs from exp(x - shift) by a few ulp (the GPU tests
-// hold every field to 1e-12 of the reference).  Each pass ends in a fixed
-// block reduction (xor-shuffle tree per warp, then the 8 warp partials in
-// order), so a point's value does not depend on which other points share
-// the launch (thermo_sweep(...)[0] == partition_point(...) exactly,
-// test_thermo.py:85-87).
+// so a point needs one exponential per column and per row instead of one
+// per occupied cell, and a cell costs a few DFMAs in each of the two
+// remaining passes.  The factors stay inside fp64 range while |h| N / T <=
+// 300 (a_e, b_m <= e^300); beyond that a point takes one exp of the whole
+// argument per cell.  The product differs from exp(x - shift) by a few ulp
+// (the GPU tests hold every field to 1e-12 of the reference).  The cell
+// order is fixed and a warp's sums meet in a fixed xor-shuffle tree, so a
+// point's value does not depend on which other points share the launch
+// (thermo_sweep(...)[0] == partition_point(...) exactly, test_thermo.py:
+// 85-87).
 //
-// (History: one CTA per point over the whole table 42 us -> warp per point
-// over a per-CTA compacted cell list 33 us -> separate one-CTA compaction +
-// four-warp teams 16.5 us (c5, 702 points) -> this kernel.)
+// (History, c5's 702-point grid: one CTA per point over the whole table
+// 42 us -> warp per point over a per-CTA compacted cell list 33 us -> one-
+// CTA compaction kernel + four-warp teams 16.5 us -> block-wide passes with
+// factorised weights ~14 us -> this kernel.)
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -57,118 +62,149 @@ __device__ __forceinline__ double warp_min(double v) {
   return v;
 }
 
+// Weight of one cell outside the factorised range (|h| N / T > 300): one
+// exp of the whole argument (rare; out of line to keep the kernel small).
+__device__ __noinline__ double whole_weight(double g, double en, double hmin,
+                                            double t) {
+  return g * exp(-(en - hmin) / t);
+}
+
 __global__ void __launch_bounds__(kThermoThreads)
     k2_thermo(const unsigned long long* __restrict__ table, uint32_t n,
               uint32_t b, double scale, const double* __restrict__ fields,
               const double* __restrict__ temps, int n_temps, int n_points,
               double* __restrict__ out) {
-  __shared__ double part[kThermoWarps][4];
-  __shared__ double bm_s[ISD_MAX_SPINS + 1];
+  extern __shared__ __align__(16) unsigned char cell_mem[];
+  __shared__ int warp_tot[kThermoWarps];
+  __shared__ double a_s[kThermoWarps][32 * kColSlots];
+  __shared__ double b_s[kThermoWarps][ISD_MAX_SPINS + 1];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int point = blockIdx.x;
-  if (point >= n_points) return;  // (uniform per CTA)
+  const int rows = (int)n + 1, cols = (int)b + 1;
+  double* cg = reinterpret_cast<double*>(cell_mem);               // counts
+  uint32_t* cme = reinterpret_cast<uint32_t*>(cg + rows * cols);  // m<<16|e
+
+  // 1. the CTA compacts the occupied bins into shared memory: thread
+  // (warp, lane) takes rows warp + 8 k and columns lane + 32 c, all loaded
+  // before any is used (one L2 round trip); one block scan of the counts
+  // places the cells in (warp, row slot, column slot) order
+  constexpr int kRowSlots =
+      (ISD_MAX_SPINS + 1 + kThermoWarps - 1) / kThermoWarps;
+  unsigned long long gv[kRowSlots][kColSlots];
+#pragma unroll
+  for (int k = 0; k < kRowSlots; ++k) {
+    const int r = warp + kThermoWarps * k;
+#pragma unroll
+    for (int c = 0; c < kColSlots; ++c) {
+      const int e = lane + 32 * c;
+      gv[k][c] = (r < rows && e < cols) ? __ldg(table + r * cols + e) : 0ull;
+    }
+  }
+  int mine = 0;
+#pragma unroll
+  for (int k = 0; k < kRowSlots; ++k)
+#pragma unroll
+    for (int c = 0; c < kColSlots; ++c) mine += gv[k][c] != 0ull;
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  int pos = incl - mine, nc = 0;
+  for (int w = 0; w < kThermoWarps; ++w) {
+    if (w < warp) pos += warp_tot[w];
+    nc += warp_tot[w];
+  }
+#pragma unroll
+  for (int k = 0; k < kRowSlots; ++k) {
+#pragma unroll
+    for (int c = 0; c < kColSlots; ++c) {
+      if (gv[k][c] != 0ull) {
+        cg[pos] = (double)gv[k][c];
+        cme[pos] = ((uint32_t)(warp + kThermoWarps * k) << 16) |
+                   (uint32_t)(lane + 32 * c);
+        ++pos;
+      }
+    }
+  }
+  __syncthreads();
+
+  // 2. each warp evaluates one point from the shared cell list: warp
+  // shuffles only, no further block barrier
+  const int point = (int)blockIdx.x * kThermoWarps + warp;
+  if (point >= n_points) return;
   const double h = fields[point / n_temps];
   const double t = temps[point % n_temps];
-  const int rows = (int)n + 1, cols = (int)b + 1;
-  auto block_reduce = [&](double* v, int nv, bool is_min) {
-    for (int k = 0; k < nv; ++k)
-      v[k] = is_min ? warp_min(v[k]) : warp_sum(v[k]);
-    if (lane == 0)
-      for (int k = 0; k < nv; ++k) part[warp][k] = v[k];
-    __syncthreads();
-    for (int k = 0; k < nv; ++k) {
-      double r = part[0][k];
-#pragma unroll
-      for (int w = 1; w < kThermoWarps; ++w)
-        r = is_min ? fmin(r, part[w][k]) : r + part[w][k];
-      v[k] = r;
-    }
-    __syncthreads();
+  auto cell = [&](int i, double* e, double* m, int* ei, int* mi) {
+    const uint32_t me = cme[i];
+    *mi = (int)(me >> 16);
+    *ei = (int)(me & 0xffffu);
+    *m = (double)(2 * *mi - (int)n);
+    *e = (double)(2 * *ei - (int)b) * scale;
   };
-  auto count = [&](int r, int e) {
-    return (double)__ldg(table + (size_t)r * cols + e);
-  };
-  double ecol[kColSlots];  // E of this lane's columns
-#pragma unroll
-  for (int c = 0; c < kColSlots; ++c)
-    ecol[c] = (double)(2 * (lane + 32 * c) - (int)b) * scale;
-
-  // pass 1: H_min = min over occupied bins of E - h M; shift = -H_min / T
-  // (= max of x = -H / T: division by T > 0 is monotone)
-  double red[4];
-  red[0] = INFINITY;
-  for (int r = warp; r < rows; r += kThermoWarps) {
-    const double m = (double)(2 * r - (int)n);
-#pragma unroll
-    for (int c = 0; c < kColSlots; ++c) {
-      const int e = lane + 32 * c;
-      if (e < cols && count(r, e) != 0.0) red[0] = fmin(red[0], ecol[c] - h * m);
-    }
+  // pass 1: H_min over the cells; shift = -H_min / T (= max of x = -H / T:
+  // division by T > 0 is monotone)
+  double hmin = INFINITY;
+  for (int i = lane; i < nc; i += 32) {
+    double e, m;
+    int ei, mi;
+    cell(i, &e, &m, &ei, &mi);
+    hmin = fmin(hmin, e - h * m);
   }
-  block_reduce(red, 1, true);
-  const double hmin = red[0];
+  hmin = warp_min(hmin);
   const double shift = -hmin / t;
   const bool split = fabs(h) * (double)n / t <= kSplitMax;
-  // the factors: a_e per lane column, b_m per row (shared)
-  double acol[kColSlots];
-#pragma unroll
-  for (int c = 0; c < kColSlots; ++c)
-    acol[c] = split ? exp(-(ecol[c] - hmin) / t) : 0.0;
-  if (split)
-    for (int r = threadIdx.x; r < rows; r += kThermoThreads)
-      bm_s[r] = exp(h * (double)(2 * r - (int)n) / t);
-  __syncthreads();
-  // w of bin (r, e): g a_e b_m, or (beyond the split range) one exp of the
-  // whole argument for an occupied bin
-  auto weight = [&](double g, int c, int r, double en) {
-    if (split) return g * acol[c] * bm_s[r];
-    return g != 0.0 ? g * exp(-(en - hmin) / t) : 0.0;
-  };
-
-  // pass 2: s = sum w and the first moments as w-weighted sums
-  red[0] = red[1] = red[2] = red[3] = 0.0;
-  for (int r = warp; r < rows; r += kThermoWarps) {
-    const double m = (double)(2 * r - (int)n);
+  if (split) {
 #pragma unroll
     for (int c = 0; c < kColSlots; ++c) {
-      const int e = lane + 32 * c;
-      if (e >= cols) continue;
-      const double en = ecol[c] - h * m;
-      const double w = weight(count(r, e), c, r, en);
-      red[0] += w;
-      red[1] += w * en;
-      red[2] += w * m;
-      red[3] += w * fabs(m);
+      const int j = lane + 32 * c;
+      if (j < cols)
+        a_s[warp][j] = exp(-((double)(2 * j - (int)b) * scale - hmin) / t);
     }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int r = lane + 32 * c;
+      if (r < rows) b_s[warp][r] = exp(h * (double)(2 * r - (int)n) / t);
+    }
+    __syncwarp();
   }
-  block_reduce(red, 4, false);
-  const double s = red[0];
-  const double u = red[1] / s;
-  const double mean_m = red[2] / s;
-  const double mean_abs = red[3] / s;
-
+  // pass 2: s = sum w and the first moments as w-weighted sums
+  double s = 0.0, su = 0.0, sm = 0.0, sa = 0.0;
+  for (int i = lane; i < nc; i += 32) {
+    double e, m;
+    int ei, mi;
+    cell(i, &e, &m, &ei, &mi);
+    const double en = e - h * m;
+    const double w = split ? cg[i] * a_s[warp][ei] * b_s[warp][mi]
+                           : whole_weight(cg[i], en, hmin, t);
+    s += w;
+    su += w * en;
+    sm += w * m;
+    sa += w * fabs(m);
+  }
+  s = warp_sum(s);
+  const double u = warp_sum(su) / s;
+  const double mean_m = warp_sum(sm) / s;
+  const double mean_abs = warp_sum(sa) / s;
   // pass 3: central second moments (the two-pass form of thermo.py:75-77;
   // the raw <H^2> - <H>^2 form cancels catastrophically at low T)
-  red[0] = red[1] = 0.0;
-  for (int r = warp; r < rows; r += kThermoWarps) {
-    const double m = (double)(2 * r - (int)n);
-    const double dm = m - mean_m;
-#pragma unroll
-    for (int c = 0; c < kColSlots; ++c) {
-      const int e = lane + 32 * c;
-      if (e >= cols) continue;
-      const double en = ecol[c] - h * m;
-      const double w = weight(count(r, e), c, r, en);
-      const double de = en - u;
-      red[0] += w * (de * de);
-      red[1] += w * (dm * dm);
-    }
+  double ve = 0.0, vm = 0.0;
+  for (int i = lane; i < nc; i += 32) {
+    double e, m;
+    int ei, mi;
+    cell(i, &e, &m, &ei, &mi);
+    const double en = e - h * m;
+    const double w = split ? cg[i] * a_s[warp][ei] * b_s[warp][mi]
+                           : whole_weight(cg[i], en, hmin, t);
+    const double de = en - u, dm = m - mean_m;
+    ve += w * (de * de);
+    vm += w * (dm * dm);
   }
-  block_reduce(red, 2, false);
-  const double ve = red[0] / s;
-  const double vm = red[1] / s;
-
-  if (threadIdx.x == 0) {
+  ve = warp_sum(ve) / s;
+  vm = warp_sum(vm) / s;
+  if (lane == 0) {
     const double log_z = shift + log(s);
     double* o = out + (size_t)point * ISD_THERMO_FIELDS;
     o[0] = log_z;
@@ -254,9 +290,20 @@ int launch_thermo_set(const TableSet& tabs, unsigned long long* sum,
     table = dst;
   }
   if (points > 0) {
-    k2_thermo<<<points, kThermoThreads, 0, st>>>(table, n_spins, n_bonds,
-                                                 scale, fields, temps, n_temps,
-                                                 points, out);
+    // the CTA's cell list: 12 bytes per bin of the table
+    const size_t smem = (size_t)(n_spins + 1) * (n_bonds + 1) * 12;
+    static std::once_flag attr_set[64];  // (a per-device attribute)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::call_once(attr_set[dev & 63], [] {
+      cudaFuncSetAttribute(
+          k2_thermo, cudaFuncAttributeMaxDynamicSharedMemorySize,
+          (int)((ISD_MAX_SPINS + 1) * (3 * ISD_MAX_SPINS + 1) * 12));
+    });
+    const int grid = (points + kThermoWarps - 1) / kThermoWarps;
+    k2_thermo<<<grid, kThermoThreads, smem, st>>>(table, n_spins, n_bonds,
+                                                  scale, fields, temps,
+                                                  n_temps, points, out);
     ++launched;
   }
   cudaError_t e = cudaGetLastError();
