@@ -242,6 +242,12 @@ int isd_walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
 int isd_set_walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
                       const isd_plan_info* plan);
 
+/* The host model's plan for a walk of [start, end) (no GPU): as isd_plan,
+ * but an aligned power-of-two range is planned with its top bits fixed, as
+ * the walk itself is.  The GPU autotuner starts from this model. */
+int isd_plan_range(const isd_lattice* lat, uint64_t start, uint64_t end,
+                   isd_plan_info* out);
+
 /* Generate and NVRTC-compile the lattice's specialised k1 kernel without
  * loading it (no GPU needed); *cubin_bytes = its size.  For tests. */
 int isd_jit_check(const isd_lattice* lat, uint64_t n_configs_hint,
@@ -261,6 +267,15 @@ int isd_band_items(uint32_t free_bits, uint32_t n_target, uint32_t span,
                    const double* seg_cost, uint32_t n_seg, double flush_units,
                    uint64_t* out, uint32_t max_items, uint32_t* n_items,
                    int* exact);
+
+/* The host model's per-segment cost of a banded launch (no GPU; tools and
+ * tests): the 2^F slots of `run_bits` run bits from run_begin, in popcount
+ * order, cut into n_seg segments; out[s] = expected shared wavefronts per
+ * warp RED in segment s (`samples` sampled REDs).  Returns the segment
+ * count written (<= n_seg) or a negative error. */
+int isd_band_costs(const isd_lattice* lat, const isd_plan_info* plan,
+                   uint64_t run_begin, uint32_t run_bits, uint32_t n_seg,
+                   uint32_t samples, double* out);
 
 /* ---- calibration microbenchmarks (K0) -------------------------------- */
 /* which: 0 = POPC, 1 = LOP3, 2 = IADD3, 3 = RED.shared spread,

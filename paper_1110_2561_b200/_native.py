@@ -32,6 +32,7 @@ EXPORTED_SYMBOLS = (
     "isd_jit_check", "isd_band_items", "isd_set_knob", "isd_clear_knobs",
     "isd_set_cache_dirs", "isd_build_id", "isd_enumerate_multi",
     "isd_thermo_gather_async", "isd_walk_plan", "isd_set_walk_plan",
+    "isd_band_costs", "isd_plan_range",
 )
 
 
@@ -144,6 +145,12 @@ def load():
         lib.isd_set_walk_plan.argtypes = [p_lat, u64, u64,
                                           ctypes.POINTER(PlanInfo)]
         lib.isd_set_walk_plan.restype = ctypes.c_int
+        lib.isd_band_costs.argtypes = [p_lat, ctypes.POINTER(PlanInfo), u64,
+                                       ctypes.c_uint32, ctypes.c_uint32,
+                                       ctypes.c_uint32, vp]
+        lib.isd_band_costs.restype = ctypes.c_int
+        lib.isd_plan_range.argtypes = [p_lat, u64, u64, ctypes.POINTER(PlanInfo)]
+        lib.isd_plan_range.restype = ctypes.c_int
         lib.isd_set_cache_dirs.argtypes = [ctypes.c_char_p]
         lib.isd_set_cache_dirs.restype = ctypes.c_int
         lib.isd_build_id.restype = ctypes.c_char_p
@@ -379,6 +386,16 @@ def plan_fingerprint(info: PlanInfo) -> str:
     return hashlib.sha256(bytes(info)).hexdigest()[:16]
 
 
+def plan_range(lat: Lattice, start: int, end: int) -> tuple:
+    """Host model plan of a walk of [start, end) (top bits of an aligned
+    power-of-two range fixed, as the walk holds them): (usable, PlanInfo)."""
+    info = PlanInfo()
+    rc = load().isd_plan_range(ctypes.byref(lat), start, end, ctypes.byref(info))
+    if rc < 0:
+        check(rc)
+    return rc == 0, info
+
+
 def validate(lat: Lattice) -> None:
     check(load().isd_validate(ctypes.byref(lat)))
 
@@ -415,6 +432,18 @@ def jit_check(lat: Lattice, n_configs_hint: int) -> int:
     check(load().isd_jit_check(ctypes.byref(lat), n_configs_hint,
                                ctypes.byref(n)))
     return n.value
+
+
+def band_costs(lat: Lattice, info: PlanInfo, run_begin: int, run_bits: int,
+               n_seg: int, samples: int = 64):
+    """The host model's cost curve of a banded launch (no GPU; tools)."""
+    out = np.zeros(n_seg, dtype=np.float64)
+    n = load().isd_band_costs(ctypes.byref(lat), ctypes.byref(info),
+                              run_begin, run_bits, n_seg, samples,
+                              out.ctypes.data)
+    if n < 0:
+        check(n)
+    return out[:n]
 
 
 def band_items(free_bits: int, n_target: int, span: int, seg_cost=None,

@@ -1372,6 +1372,38 @@ int isd_set_walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
   return ISD_OK;
 }
 
+int isd_band_costs(const isd_lattice* lat, const isd_plan_info* plan,
+                   uint64_t run_begin, uint32_t run_bits, uint32_t n_seg,
+                   uint32_t samples, double* out) {
+  int rc = isd_validate(lat);
+  if (rc) return rc;
+  if (!plan || !out || n_seg < 1 || samples < 1 || run_bits < 6 ||
+      run_bits > 28)
+    return fail(ISD_EINVAL, "bad band cost arguments");
+  std::vector<double> c;
+  band_slot_cost(lat, *plan, run_begin, plan->lane_mask, plan->lane_vec,
+                 (int)run_bits, (int)n_seg, (int)samples, &c);
+  std::memcpy(out, c.data(), c.size() * sizeof(double));
+  return (int)c.size();
+}
+
+int isd_plan_range(const isd_lattice* lat, uint64_t start, uint64_t end,
+                   isd_plan_info* out) {
+  int rc = isd_validate(lat);
+  if (rc) return rc;
+  if (!out) return fail(ISD_EINVAL, "plan pointer is NULL");
+  if (!(start < end && end <= (1ull << lat->n_spins)))
+    return fail(ISD_EINVAL, "range [%llu, %llu) invalid for 2^%u configurations",
+                (unsigned long long)start, (unsigned long long)end,
+                lat->n_spins);
+  const uint64_t len = end - start;
+  const uint64_t top = (!(len & (len - 1)) && start % len == 0 &&
+                        knob_long("ISD_PLAN_TOP", 1) != 0)
+                           ? start
+                           : 0;
+  return cached_plan(lat, len, out, top);
+}
+
 int isd_band_items(uint32_t free_bits, uint32_t n_target, uint32_t span,
                    const double* seg_cost, uint32_t n_seg, double flush_units,
                    uint64_t* out, uint32_t max_items, uint32_t* n_items,
