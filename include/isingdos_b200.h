@@ -119,6 +119,20 @@ int isd_enumerate_multi(const isd_lattice* lat, uint64_t start, uint64_t end,
                         uint64_t* counts_host, double* shard_ms,
                         double* total_ms);
 
+/* The naive cross-check engine (replaces oracle_full_dos's per-index loop,
+ * oracle.py:71-91): per configuration, decode every spin S = +-1 from bit
+ * bit_of_slot[s] of the index, M = sum of spins, and E / |J| =
+ * -sign(J) * sum_b bond_sign[b] S_i S_j over the explicit bond list
+ * (bond_slots[2b], bond_slots[2b + 1]) — one thread per configuration,
+ * nothing shared with the enumeration kernels or the bond-class
+ * descriptor.  Writes the (N+1) x (B+1) table of [start, end) like
+ * isd_enumerate.  Synchronous. */
+int isd_naive_enumerate(uint32_t n_spins, const uint32_t* bit_of_slot,
+                        uint32_t n_bonds, const uint32_t* bond_slots,
+                        const int32_t* bond_sign, int coupling_sign,
+                        uint64_t start, uint64_t end, int device,
+                        uint64_t* counts_host);
+
 /* In-place completion of a half walk: counts[m][e] += counts[N-m][e]
  * pairwise (rows m and N-m both become the sum).  Device buffer, async. */
 int isd_mirror_async(uint64_t* counts_dev, uint32_t n_spins, uint32_t n_bonds,

@@ -19,7 +19,7 @@ LIB = os.path.join(PKG, "libisingdos_b200.so")
 LIB_DEBUG = os.path.join(PKG, "libisingdos_b200_dbg.so")
 
 SOURCES = ["plan.cpp", "enumerate.cu", "thermo.cu", "calibrate.cu", "capi.cu",
-           "jit.cpp", "knobs.cpp", "cache.cpp"]
+           "jit.cpp", "knobs.cpp", "cache.cpp", "naive.cu"]
 HEADERS = ["isd_internal.h", "k1_body.cuh"]
 
 NVCC_FLAGS = [

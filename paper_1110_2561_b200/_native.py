@@ -32,7 +32,7 @@ EXPORTED_SYMBOLS = (
     "isd_jit_check", "isd_band_items", "isd_set_knob", "isd_clear_knobs",
     "isd_set_cache_dirs", "isd_build_id", "isd_enumerate_multi",
     "isd_thermo_gather_async", "isd_walk_plan", "isd_set_walk_plan",
-    "isd_band_costs", "isd_plan_range",
+    "isd_band_costs", "isd_plan_range", "isd_naive_enumerate",
 )
 
 
@@ -151,6 +151,10 @@ def load():
         lib.isd_band_costs.restype = ctypes.c_int
         lib.isd_plan_range.argtypes = [p_lat, u64, u64, ctypes.POINTER(PlanInfo)]
         lib.isd_plan_range.restype = ctypes.c_int
+        lib.isd_naive_enumerate.argtypes = [
+            ctypes.c_uint32, vp, ctypes.c_uint32, vp, vp, i32, u64, u64, i32,
+            vp]
+        lib.isd_naive_enumerate.restype = ctypes.c_int
         lib.isd_set_cache_dirs.argtypes = [ctypes.c_char_p]
         lib.isd_set_cache_dirs.restype = ctypes.c_int
         lib.isd_build_id.restype = ctypes.c_char_p
@@ -310,6 +314,25 @@ def thermo_gather_device(table_ptrs, sum_ptr, n_spins, n_bonds, scale,
         ctypes.c_void_p(out_ptr or None), ctypes.c_void_p(stream_ptr)))
     gather = 1 if len(table_ptrs) > 1 or sum_ptr else 0  # K4
     return gather + (1 if n_fields * n_temps > 0 else 0)   # + K2
+
+
+def naive_enumerate(bit_of_slot, bonds, coupling_sign: int, start: int,
+                    end: int, device=None):
+    """The naive engine (K5): spins decoded per slot, E summed over the
+    explicit bond list `bonds` = [(slot_i, slot_j, sign)]; uint64 table."""
+    lib = load()
+    pos = np.ascontiguousarray(bit_of_slot, dtype=np.uint32)
+    n = len(pos)
+    slots = np.ascontiguousarray([(i, j) for i, j, _ in bonds],
+                                 dtype=np.uint32).reshape(-1)
+    signs = np.ascontiguousarray([s for _, _, s in bonds], dtype=np.int32)
+    out = np.zeros((n + 1) * (len(bonds) + 1), dtype=np.uint64)
+    dev = current_device() if device is None else device
+    check(lib.isd_naive_enumerate(
+        n, pos.ctypes.data, len(bonds), slots.ctypes.data if len(bonds) else None,
+        signs.ctypes.data if len(bonds) else None, int(coupling_sign), start,
+        end, dev, out.ctypes.data))
+    return out.reshape(n + 1, len(bonds) + 1)
 
 
 def enumerate_device(lat: Lattice, start: int, end: int, counts_ptr: int,

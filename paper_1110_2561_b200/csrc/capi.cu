@@ -1542,6 +1542,50 @@ int isd_thermo_gather_async(const uint64_t* const* tables_dev, int n_tables,
   return ISD_OK;
 }
 
+int isd_naive_enumerate(uint32_t n_spins, const uint32_t* bit_of_slot,
+                        uint32_t n_bonds, const uint32_t* bond_slots,
+                        const int32_t* bond_sign, int coupling_sign,
+                        uint64_t start, uint64_t end, int device,
+                        uint64_t* counts_host) {
+  if (!bit_of_slot || (n_bonds && (!bond_slots || !bond_sign)) ||
+      !counts_host)
+    return fail(ISD_EINVAL, "NULL buffer");
+  if (n_spins < 1 || n_spins > ISD_MAX_SPINS || n_bonds > 3 * ISD_MAX_SPINS)
+    return fail(ISD_EINVAL, "bad lattice N=%u B=%u", n_spins, n_bonds);
+  if (!(start <= end && end <= (1ull << n_spins)))
+    return fail(ISD_EINVAL, "range [%llu, %llu) invalid for 2^%u configurations",
+                (unsigned long long)start, (unsigned long long)end, n_spins);
+  DeviceGuard guard;
+  DevState* s = nullptr;
+  std::unique_lock<std::mutex> lock;
+  int rc = get_dev(device, &s, &lock);
+  if (rc) return rc;
+  const size_t bytes = (size_t)(n_spins + 1) * (n_bonds + 1) * 8;
+  rc = ensure_buffer(&s->d_counts, &s->d_counts_bytes, bytes,
+                     "cudaMalloc(counts)");
+  if (rc) return rc;
+  cudaError_t e = cudaMemsetAsync(s->d_counts, 0, bytes, s->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+  std::string why;
+  const int r = naive_enumerate(n_spins, bit_of_slot, n_bonds, bond_slots,
+                                bond_sign, coupling_sign, start, end,
+                                s->d_counts, s->sm_count, s->stream, &why);
+  if (r < 0) {
+    if (!why.empty()) return fail(ISD_EINVAL, "%s", why.c_str());
+    return cuda_fail((cudaError_t)(-r), "k5_naive launch");
+  }
+  bump_launches((uint64_t)r);
+  void* stage = nullptr;
+  rc = stage_buffer(s, bytes, &stage);
+  if (rc) return rc;
+  e = cudaMemcpyAsync(stage, s->d_counts, bytes, cudaMemcpyDeviceToHost,
+                      s->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "naive enumeration");
+  std::memcpy(counts_host, stage, bytes);
+  return ISD_OK;
+}
+
 int isd_mirror_async(uint64_t* counts_dev, uint32_t n_spins, uint32_t n_bonds,
                      void* stream) {
   if (!counts_dev || n_spins < 1 || n_spins > ISD_MAX_SPINS ||

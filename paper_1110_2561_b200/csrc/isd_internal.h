@@ -205,6 +205,13 @@ int launch_thermo(const unsigned long long* counts, uint32_t n_spins,
                   uint32_t n_bonds, double scale, const double* fields,
                   int n_fields, const double* temps, int n_temps, double* out,
                   void* stream);
+// K5, the naive cross-check engine (naive.cu): per-slot bit positions and
+// an explicit bond list (slot pairs, signs); launches or -cudaError_t
+int naive_enumerate(uint32_t n_spins, const uint32_t* bit_of_slot,
+                    uint32_t n_bonds, const uint32_t* bond_slots,
+                    const int32_t* bond_sign, int coupling_sign,
+                    uint64_t start, uint64_t end, unsigned long long* out,
+                    int sm_count, void* stream, std::string* why);
 int run_calibration(int which, int sm_count, double* lanes_per_clk_sm,
                     double* sm_mhz);
 

@@ -431,6 +431,10 @@ __device__ __forceinline__ void k1_hoisted_body(
     }
   };
 
+#ifdef ISD_PROBE
+  unsigned long long probe_enter;  // (probe build) block entry, ns
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(probe_enter));
+#endif
   if (L.band_rows() == 0) {
     // ---- grid-stride walk over the runs; one table for all rows ----
     zero_hist();
@@ -544,6 +548,16 @@ __device__ __forceinline__ void k1_hoisted_body(
 #endif
     }
   }
+#ifdef ISD_PROBE
+  // (probe build) block entry and exit on the global nanosecond clock
+  {
+    unsigned long long probe_exit;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(probe_exit));
+    if (threadIdx.x == 0)
+      printf("ISDBLK blk %u enter %llu exit %llu\n", blockIdx.x, probe_enter,
+             probe_exit);
+  }
+#endif
 }
 
 #endif  // ISD_K1_BODY_CUH

@@ -294,3 +294,88 @@ def test_cli_oracle_check(capsys):
         capsys.readouterr().out
     assert main(["oracle-check", "--rows", "5", "--cols", "5"]) == 1
     assert "oracle cap" in capsys.readouterr().err
+
+
+# -- independence of the shipped cross-check ------------------
+
+def test_crosscheck_bond_pairs_restate_geometry_in_reference_order():
+    # crosscheck.bond_pairs walks the lattice itself (oracle.py:40-58); the
+    # order is the contract bond_signs is defined in, so it must equal the
+    # order of LatticeSpec.bond_list() without being computed from it
+    for dims in [(2, 2, 1), (3, 3, 1), (4, 4, 1), (2, 3, 2), (3, 3, 4),
+                 (2, 2, 2), (4, 3, 3), (2, 5, 4), (6, 6, 1)]:
+        for bd in ("periodic", "free"):
+            spec = isd.LatticeSpec(*dims, boundary=bd)
+            slot = {spec.bit_position(r, c, l): i for i, (r, c, l)
+                    in enumerate(isd.crosscheck.site_order(spec))}
+            want = [(slot[i], slot[j]) for i, j, _, _ in spec.bond_list()]
+            assert isd.crosscheck.bond_pairs(spec) == want
+
+
+def test_crosscheck_never_consults_the_bond_classes(monkeypatch):
+    # the naive route must not read the descriptor K1 runs on: break every
+    # route to it and capture what reaches the naive engine
+    from paper_1110_2561_b200 import _native
+    from oracle import naive
+    seen = {}
+
+    def capture(bits, bonds, sign, start, end, device=None):
+        seen.update(bits=bits, bonds=bonds, sign=sign, range=(start, end))
+        return np.zeros((spec.num_spins + 1, spec.num_bonds + 1),
+                        dtype=np.uint64)
+
+    def boom(*a, **k):
+        raise AssertionError("the cross-check touched the fast path")
+
+    monkeypatch.setattr(isd.LatticeSpec, "bond_classes", boom)
+    monkeypatch.setattr(isd.LatticeSpec, "bond_list", boom)
+    monkeypatch.setattr(_native, "naive_enumerate", capture)
+    monkeypatch.setattr(_native, "enumerate_host", boom)
+    base = isd.LatticeSpec(3, 4, 2)
+    signs = naive.random_signs(base.num_bonds, 11)
+    spec = isd.LatticeSpec(3, 4, 2, -1.5, bond_signs=signs)
+    isd.oracle_full_dos(spec)
+    assert seen["sign"] == -1 and seen["range"] == (0, spec.num_configs)
+    assert sorted(seen["bits"]) == list(range(spec.num_spins))
+    assert len(seen["bonds"]) == spec.num_bonds
+    # the bond list agrees with the test oracle's per-bond restatement
+    pairs = naive.bond_pairs(3, 4, 2, True)
+    assert [(i, j) for i, j, _ in seen["bonds"]] == [tuple(p) for p in pairs]
+
+
+@pytest.mark.gpu
+def test_oracle_check_catches_a_fault_in_the_bond_classes(monkeypatch, capsys):
+    # inject a fault into the descriptor the fast path compiles (one bond's
+    # sign flipped in its class masks): the naive engine must disagree
+    from paper_1110_2561_b200 import enumeration
+    from paper_1110_2561_b200.cli import main
+    good = isd.LatticeSpec.bond_classes
+
+    def faulty(self):
+        classes = list(good(self))
+        s, m, j = classes[0]
+        low = m & -m
+        classes[0] = (s, m, j ^ low)
+        return classes
+
+    monkeypatch.setattr(isd.LatticeSpec, "bond_classes", faulty)
+    monkeypatch.setattr(enumeration, "_DESCRIPTORS", {})
+    assert main(["oracle-check", "--rows", "3", "--cols", "4"]) == 1
+    assert "mismatching cells" in capsys.readouterr().err
+    monkeypatch.setattr(isd.LatticeSpec, "bond_classes", good)
+    monkeypatch.setattr(enumeration, "_DESCRIPTORS", {})
+    assert main(["oracle-check", "--rows", "3", "--cols", "4"]) == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kw", [dict(boundary="free"), dict(coupling=-2),
+                                dict(seed=3)])
+def test_naive_engine_matches_fast_path_on_extended_lattices(kw):
+    kw = dict(kw)
+    seed = kw.pop("seed", None)
+    base = isd.LatticeSpec(3, 4, 2, **kw)
+    spec = base if seed is None else isd.LatticeSpec(
+        3, 4, 2, bond_signs=isd.random_bond_signs(base, seed))
+    got = isd.oracle_full_dos(spec)
+    assert got == isd.full_dos(spec)
+    assert isd.verify_dos(got).passed

@@ -83,6 +83,17 @@ def main():
     for x in recs:
         tot[x["blk"]] += x["flush"]
     vals = list(tot.values())
+    blk = [tuple(int(v) for v in re.findall(r"(\d+)", l)[1:4])
+           for l in out.splitlines() if l.startswith("ISDBLK")]
+    if blk:
+        enter = [e for _, e, _ in blk]
+        leave = [x for _, _, x in blk]
+        span = (max(leave) - min(enter)) / 1e3
+        print(f"kernel span (first block entry -> last block exit) "
+              f"{span:.1f} us; block entry spread "
+              f"{(max(enter) - min(enter)) / 1e3:.1f} us; exit spread "
+              f"{(max(leave) - min(leave)) / 1e3:.1f} us; mean block "
+              f"{sum(x - e for _, e, x in blk) / len(blk) / 1e3:.1f} us")
     print(f"items {len(recs)}; block cycles mean {st.mean(vals):.0f} "
           f"max/mean {max(vals) / st.mean(vals):.4f} min/mean "
           f"{min(vals) / st.mean(vals):.4f}")
