@@ -306,6 +306,13 @@ int jit_compile_check(const HoistParams& P, std::string* why) {
     *why = c.why;
     return 0;
   }
+  std::string dump;  // (ISD_JIT_DUMP: inspect the SASS without a GPU)
+  if (knob_str("ISD_JIT_DUMP", &dump) && !dump.empty()) {
+    if (FILE* f = std::fopen(dump.c_str(), "wb")) {
+      std::fwrite(c.bytes.data(), 1, c.bytes.size(), f);
+      std::fclose(f);
+    }
+  }
   return (int)c.bytes.size();
 }
 

@@ -432,7 +432,8 @@ __device__ __forceinline__ void k1_hoisted_body(
   };
 
 #ifdef ISD_PROBE
-  unsigned long long probe_enter;  // (probe build) block entry, ns
+  // (probe build) block entry and end of its last flush, ns
+  unsigned long long probe_enter, probe_last = 0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(probe_enter));
 #endif
   if (L.band_rows() == 0) {
@@ -537,6 +538,7 @@ __device__ __forceinline__ void k1_hoisted_body(
       flush(row_off, L.band_rows());
       __syncthreads();
 #ifdef ISD_PROBE
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(probe_last));
       // (probe build) per item: first chunk start, this warp's end, last
       // warp's end, flush end, relative to the item start (SM cycles)
       if (threadIdx.x == 0)
@@ -551,8 +553,8 @@ __device__ __forceinline__ void k1_hoisted_body(
 #ifdef ISD_PROBE
   // (probe build) block entry and exit on the global nanosecond clock
   {
-    unsigned long long probe_exit;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(probe_exit));
+    unsigned long long probe_exit = probe_last;
+    if (!probe_exit) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(probe_exit));
     if (threadIdx.x == 0)
       printf("ISDBLK blk %u enter %llu exit %llu\n", blockIdx.x, probe_enter,
              probe_exit);

@@ -83,7 +83,7 @@ def main():
     for x in recs:
         tot[x["blk"]] += x["flush"]
     vals = list(tot.values())
-    blk = [tuple(int(v) for v in re.findall(r"(\d+)", l)[1:4])
+    blk = [tuple(int(v) for v in re.findall(r"(\d+)", l)[0:3])
            for l in out.splitlines() if l.startswith("ISDBLK")]
     if blk:
         enter = [e for _, e, _ in blk]
