@@ -29,6 +29,8 @@ import subprocess
 import sys
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -306,13 +308,16 @@ NVLINK_GATHER_ALLOWANCE_MS = 0.003
 
 
 def shard_emulation(wl, ms_step_1, dev, reps):
-    """Every shard of a P-way split (P = 2, 4, 8) timed on this GPU through
-    the engine's multi-device entry (all shards listed on device 0: each is
-    walked and event-timed alone, exactly as one rank of a P-GPU run walks
-    it), plus the root's tail — the fused peer gather of P tables + K2 on the
-    workload's grid, replayed as a CUDA graph.  Projected P-GPU step = the
-    slowest shard + the tail (+ an NVLink allowance); projected efficiency
-    = one-GPU step / (P x projected step)."""
+    """Every shard of a P-way split (P = 2, 4, 8) timed on this GPU exactly as
+    one rank of a P-GPU run walks it per step: the shard's step work (table
+    memset + K1 over the shard's top-bit range, through the C ABI) captured
+    as a CUDA graph and replayed back to back, CUDA events on the launching
+    stream, `reps` x 10 replays, median per shard.  Plus the root's tail:
+    the fused gather of P tables (K4) + K2 on the workload's grid, also a
+    graph.  Projected P-GPU step = the slowest shard + the tail (+ an NVLink
+    allowance for the gather's peer reads); projected efficiency = one-GPU
+    step / (P x projected step).  The shards also run once through
+    isd_enumerate_multi (all on this GPU) to check the combined table."""
     import statistics as st_
     import torch
     from paper_1110_2561_b200 import _native
@@ -327,23 +332,54 @@ def shard_emulation(wl, ms_step_1, dev, reps):
                       device=dev)
     total = torch.empty(nb, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream(dev)
-    res = {"method": "isd_enumerate_multi with every shard on this GPU "
-                     "(each shard walked and event-timed alone); tail = "
-                     "isd_thermo_gather_async over P tables + K2, CUDA-graph "
-                     f"replay; + {NVLINK_GATHER_ALLOWANCE_MS * 1e3:.0f} us "
-                     "NVLink allowance",
+    whole, _, _ = _native.enumerate_multi(lat, 0, spec.num_configs, [0])
+    res = {"method": "per shard: CUDA graph of (table memset + K1 over the "
+                     "shard) replayed back to back, median of "
+                     f"{reps} x 10 replays; tail: graph of K4 gather of P "
+                     "tables + K2; + "
+                     f"{NVLINK_GATHER_ALLOWANCE_MS * 1e3:.0f} us NVLink "
+                     "allowance",
            "one_gpu_step_ms": ms_step_1}
+
+    def graph_ms(fn, n_rep=10):
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cap):
+            fn(cap.cuda_stream)
+        for _ in range(3):
+            g.replay()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        samples = []
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            e0.record(stream)
+            for _ in range(n_rep):
+                g.replay()
+            e1.record(stream)
+            e1.synchronize()
+            samples.append(e0.elapsed_time(e1) / n_rep)
+        return st_.median(samples), samples
+
     for P in (2, 4, 8):
-        _native.enumerate_multi(lat, 0, spec.num_configs, [0] * P)  # warm
-        runs = [_native.enumerate_multi(lat, 0, spec.num_configs, [0] * P)
-                for _ in range(reps)]
-        per_shard = [st_.median(r[1][i] for r in runs) for i in range(P)]
-        # the root's tail on real shard tables
-        tabs = []
-        for sh in isd.make_shards(spec, P):
+        shards = isd.make_shards(spec, P)
+        # one pass through the engine's multi-device entry: plans, tuning,
+        # and the combined table checked against the one-shard walk
+        table, multi_ms, _ = _native.enumerate_multi(
+            lat, 0, spec.num_configs, [0] * P)
+        tabs, per_shard, samples = [], [], []
+        for sh in shards:
             t = torch.zeros(nb, dtype=torch.int64, device=dev)
-            _native.enumerate_device(lat, sh.start_index, sh.end_index,
-                                     t.data_ptr(), stream.cuda_stream)
+
+            def walk(st, sh=sh, t=t):
+                _native.enumerate_device(lat, sh.start_index, sh.end_index,
+                                         t.data_ptr(), st)
+            walk(stream.cuda_stream)  # (eager: the plan is ready)
+            ms, smp = graph_ms(walk)
+            per_shard.append(ms)
+            samples.append([round(x, 5) for x in smp])
             tabs.append(t)
         ptrs = [t.data_ptr() for t in tabs]
 
@@ -352,33 +388,19 @@ def shard_emulation(wl, ms_step_1, dev, reps):
                 ptrs, total.data_ptr(), spec.num_spins, spec.num_bonds,
                 abs(spec.coupling), fields.data_ptr(), len(wl.fields),
                 temps.data_ptr(), len(wl.temps), out.data_ptr(), st)
+        tail_ms, _ = graph_ms(tail, 50)
         torch.cuda.synchronize(dev)
-        g = torch.cuda.CUDAGraph()
-        cap = torch.cuda.Stream(dev)
-        cap.wait_stream(stream)
-        with torch.cuda.graph(g, stream=cap):
-            tail(cap.cuda_stream)
-        for _ in range(3):
-            g.replay()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        n_rep = 50
-        torch.cuda.synchronize(dev)
-        e0.record(stream)
-        for _ in range(n_rep):
-            g.replay()
-        e1.record(stream)
-        e1.synchronize()
-        tail_ms = e0.elapsed_time(e1) / n_rep
-        ok = bool(torch.equal(total, sum(tabs)))
+        ok = bool(np.array_equal(table, whole)) and bool(torch.equal(
+            total.cpu(), torch.from_numpy(whole.view(np.int64).reshape(-1))))
         step = max(per_shard) + tail_ms + NVLINK_GATHER_ALLOWANCE_MS
         res[f"P{P}"] = {
-            "shard_ms": per_shard, "max_shard_ms": max(per_shard),
-            "min_shard_ms": min(per_shard), "tail_ms": tail_ms,
+            "shard_ms": per_shard, "shard_samples_ms": samples,
+            "max_shard_ms": max(per_shard), "min_shard_ms": min(per_shard),
+            "multi_entry_shard_ms": multi_ms, "tail_ms": tail_ms,
             "projected_step_ms": step,
             "projected_configs_per_s": spec.num_configs / (step / 1e3),
             "projected_efficiency": ms_step_1 / (P * step),
-            "gather_sum_exact": ok}
+            "combined_tables_exact": ok}
     return res
 
 

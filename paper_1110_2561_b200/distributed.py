@@ -7,7 +7,9 @@ does the same with MPI.  Here each rank of a
 backend "nccl") walks `make_shards(spec, world)[rank]` — for a power-of-two
 world exactly the top log2(P) bits of the index — into a device-resident
 uint64 table, and a single `reduce` (sum) over NVLink combines the tables
-on the root.  The table is at most 41 x 121 x 8 B = 39 KB, so the exchange
+on the root.  (Inside one process, `full_dos_timed` drives several GPUs
+through the engine's own multi-device entry instead, which combines the
+tables on the root with one peer-gather kernel.)  The table is at most 41 x 121 x 8 B = 39 KB, so the exchange
 is one latency-bound message per walk (tens of microseconds against
 milliseconds of enumeration); a fused kernel-side exchange would not pay
 for itself here.
@@ -34,17 +36,22 @@ def rank_shard(spec: LatticeSpec, rank: int, world: int) -> Shard:
 
 
 def native_enumerate_into(spec: LatticeSpec, shard: Shard, table) -> int:
-    """K1 over `shard` into the CUDA int64 tensor `table` (current stream)."""
+    """K1 over `shard` into the CUDA int64 tensor `table`, on the current
+    stream of the table's own device (the library launches on the calling
+    thread's current device, so that device is made current first)."""
     import torch
-    stream = torch.cuda.current_stream(table.device).cuda_stream
-    return _native.enumerate_device(native_lattice(spec), shard.start_index,
-                                    shard.end_index, table.data_ptr(), stream,
-                                    accumulate=False)
+    with torch.cuda.device(table.device):
+        stream = torch.cuda.current_stream(table.device).cuda_stream
+        return _native.enumerate_device(native_lattice(spec),
+                                        shard.start_index, shard.end_index,
+                                        table.data_ptr(), stream,
+                                        accumulate=False)
 
 
 def sharded_table(spec: LatticeSpec, group=None, root: int = 0,
                   enumerate_into=None, device=None):
-    """Enumerate this rank's shard and reduce all tables onto `root`.
+    """Enumerate this rank's shard and reduce all tables onto `root` (a rank
+    of `group`).
 
     Returns the reduced table tensor on every rank (only the root's holds
     the full sum).  Collective: every rank of `group` must call it.
@@ -61,7 +68,9 @@ def sharded_table(spec: LatticeSpec, group=None, root: int = 0,
     fn = enumerate_into or native_enumerate_into
     fn(spec, rank_shard(spec, rank, world), table)
     if world > 1:
-        dist.reduce(table, dst=root, group=group)
+        # `root` is a rank of `group`; reduce takes a global rank
+        dst = dist.get_global_rank(group, root) if group is not None else root
+        dist.reduce(table, dst=dst, group=group)
     return table
 
 

@@ -82,3 +82,49 @@ def test_rank_shards_are_top_bits_for_power_of_two():
             assert sh.size == 1 << (36 - bits)
     with pytest.raises(ValueError):
         rank_shard(spec, 2, 2)
+
+
+def _subgroup_worker(rank, world, tcp_port, kw, out_path):
+    # ranks 1 and 2 form a subgroup whose root is its group rank 1 (global
+    # rank 2): the reduce must target the global rank of the group's root
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1110_2561_b200 as isd
+    from paper_1110_2561_b200 import distributed as D
+    from oracle import port
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{tcp_port}",
+                            rank=rank, world_size=world)
+    sub = dist.new_group([1, 2])
+    spec = isd.LatticeSpec(**kw)
+
+    def oracle_into(spec, shard, table):
+        lat = port.Lattice(spec.rows, spec.cols, spec.depth, spec.coupling,
+                           spec.periodic)
+        t = port.enumerate_range(lat, shard.start_index, shard.end_index)
+        table.copy_(torch.from_numpy(t.reshape(-1)))
+        return 0
+
+    if rank in (1, 2):
+        dos = D.sharded_full_dos(spec, group=sub, root=1,
+                                 enumerate_into=oracle_into,
+                                 device=torch.device("cpu"))
+        if rank == 2:
+            np.save(out_path, dos.counts)
+        else:
+            assert dos is None
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_subgroup_root_is_a_group_rank(tmp_path):
+    from oracle import port
+    out = str(tmp_path / "table.npy")
+    kw = dict(rows=3, cols=4)
+    mp.start_processes(_subgroup_worker, args=(3, _free_port(), kw, out),
+                       nprocs=3, join=True, start_method="spawn")
+    lat = port.Lattice(3, 4, 1)
+    assert np.array_equal(np.load(out), port.enumerate_range(lat, 0, 1 << 12))
