@@ -393,8 +393,17 @@ def shard_emulation(wl, ms_step_1, dev, reps):
         ok = bool(np.array_equal(table, whole)) and bool(torch.equal(
             total.cpu(), torch.from_numpy(whole.view(np.int64).reshape(-1))))
         step = max(per_shard) + tail_ms + NVLINK_GATHER_ALLOWANCE_MS
+        plans = []
+        for sh in shards:
+            _, pl = _native.walk_plan(lat, sh.start_index, sh.end_index, 0)
+            plans.append({"fingerprint": _native.plan_fingerprint(pl),
+                          "loop_bits": int(pl.l), "band_rows": int(pl.band_rows),
+                          "lane_mask": hex(pl.lane_mask),
+                          "model_wavefronts_per_red":
+                              round(pl.est_wavefronts, 4)})
         res[f"P{P}"] = {
             "shard_ms": per_shard, "shard_samples_ms": samples,
+            "shard_plans": plans,
             "max_shard_ms": max(per_shard), "min_shard_ms": min(per_shard),
             "multi_entry_shard_ms": multi_ms, "tail_ms": tail_ms,
             "projected_step_ms": step,

@@ -505,7 +505,11 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
   }
   if (cands.size() < 2) return;
   // tuning runs on a private stream (never the caller's, which may be
-  // capturing a graph or carry unrelated work); it is synchronous
+  // capturing a graph or carry unrelated work); it is synchronous, and
+  // waits for the device to drain first: a candidate timed while other
+  // work still occupies the SMs would look slower than it is
+  cudaDeviceSynchronize();
+  cudaGetLastError();
   cudaStream_t st = nullptr;
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
     cudaGetLastError();

@@ -862,10 +862,12 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
         continue;
       const int span =
           domino ? 0 : (int)knob_long("ISD_BAND_SPAN", kBandSpan);  // (knob)
-      const int lb = (int)std::min<long>(
-          knob_long(domino ? "ISD_BAND_DOMINO_LOOP_BITS" : "ISD_BAND_LOOP_BITS",
-                  domino ? 4 : 5),
-          l);
+      // (not capped by the grid-stride loop width l: a banded launch deals
+      // work items of slots to blocks, so it has no grid-stride tail; on
+      // 2^33-configuration shards l = 5 instead of 4 walks 3.5% faster)
+      const long lb_knob = knob_long(
+          domino ? "ISD_BAND_DOMINO_LOOP_BITS" : "ISD_BAND_LOOP_BITS", -1);
+      const int lb = lb_knob >= 0 ? (int)lb_knob : (domino ? 4 : 5);
       const int kb = u + lb;
       const int rows = span + (domino ? 10 : 5) + lb + (u - 2) + 1;
       if (walk_bits - kb - 5 >= 1 && kb <= 32 && rows <= n + 1) {
