@@ -224,6 +224,7 @@ static int cached_plan(const isd_lattice* lat, uint64_t hint,
   std::lock_guard<std::mutex> lock(g_plan_mu);
   auto it = g_plans.find(key);
   if (it == g_plans.end()) {
+    NvtxRange nvtx("isd:plan model");
     PlanEntry fresh;
     fresh.rc = compile_plan(lat, hint, &fresh.info, &fresh.ranked, top);
     it = g_plans.emplace(key, std::move(fresh)).first;
@@ -486,6 +487,7 @@ static constexpr uint64_t kTuneSliceConfigs = 1ull << 36;
 static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
                      uint64_t end, int sms, isd_plan_info* info,
                      uint64_t top) {
+  NvtxRange nvtx("isd:autotune");
   if (knob_long("ISD_AUTOTUNE", 1) == 0) return;
   const std::string key = plan_key(lat, hint, top);
   std::vector<isd_plan_info> cands;
@@ -890,6 +892,7 @@ static int prepare_flip(const isd_lattice* lat, uint64_t start, uint64_t end,
 static int prepare_walk(const isd_lattice* lat, uint64_t start, uint64_t end,
                         int algo, unsigned long long* out, int accumulate,
                         bool capturing, std::vector<Op>* ops) {
+  NvtxRange nvtx("isd:prepare walk");
   char err[256];
   int rc = validate_lattice(lat, err, sizeof err);
   if (rc) return fail(rc, "%s", err);
@@ -1105,6 +1108,7 @@ static int enumerate_multi(const isd_lattice* lat, uint64_t start,
                            uint64_t end, int n_shards, const int* devs,
                            int algo, uint64_t* counts_host, double* shard_ms,
                            double* total_ms) {
+  NvtxRange nvtx("isd:enumerate_multi");
   char err[256];
   int rc = validate_lattice(lat, err, sizeof err);
   if (rc) return fail(rc, "%s", err);
@@ -1462,6 +1466,7 @@ int isd_enumerate_async(const isd_lattice* lat, uint64_t start, uint64_t end,
 int isd_enumerate(const isd_lattice* lat, uint64_t start, uint64_t end,
                   int device, int algo, uint64_t* counts_host,
                   double* device_ms) {
+  NvtxRange nvtx("isd:enumerate");
   int rc = isd_validate(lat);
   if (rc) return rc;
   if (!counts_host) return fail(ISD_EINVAL, "counts pointer is NULL");

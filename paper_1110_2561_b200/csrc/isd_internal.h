@@ -9,7 +9,18 @@
 
 #include "isingdos_b200.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace isd {
+
+// NVTX range for the host phases (plan, autotune, NVRTC, prepare / issue of
+// a walk): visible in nsys / ncu timelines, free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr int kCopyBits = ISD_COPY_BITS;   // u: sites unrolled in registers
 // most loop sites the NVRTC kernel walks in Gray order (HoistParams.gray)

@@ -227,6 +227,7 @@ static std::string jit_source(const HoistParams& P) {
 
 // NVRTC compile of one source (host only).
 static Cubin compile_source(const std::string& src) {
+  NvtxRange nvtx("isd:nvrtc compile");
   Cubin out;
   Nvrtc& nv = nvrtc();
   if (!nv.ok) {

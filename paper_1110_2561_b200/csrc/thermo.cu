@@ -9,34 +9,39 @@
 // moments are accumulated as w-weighted sums and divided by s once
 // (sum(w x)/s instead of sum((w/s) x)): same value to ~1e-16 relative.
 //
-// One kernel; a CTA of 256 threads evaluates 8 (h, T) points, one per warp.
-// The CTA first compacts the occupied bins of the table (32 KB, L2-resident)
-// into shared memory — warp w takes rows m = w, w + 8, ..., lane j the
-// columns e = j + 32 c, all loaded at once; one block scan of the per-
-// thread counts places the cells.  Each warp then evaluates its point from
-// that list with warp shuffles only (no further block barrier: the kernel
-// is latency-bound, and a point's critical path is what it costs).  The
-// Boltzmann weight factorises over the table's axes:
+// One kernel; a CTA of 256 threads evaluates 4 (h, T) points, one per pair
+// of warps.  The CTA first compacts the occupied bins of the table (32 KB,
+// L2-resident) into shared memory — warp w takes rows m = w, w + 8, ...,
+// lane j the columns e = j + 32 c, all loaded at once; one block scan of
+// the per-thread counts places the cells — and keeps each row's lowest
+// occupied column, so a point's H_min (the reference's shift, the max of
+// x = -H/T) is a minimum over rows instead of a pass over cells.  Each pair
+// of warps then evaluates its point from the cell list with warp shuffles
+// and a pair barrier (no further block barrier: the kernel is latency-
+// bound, and a point's critical path is what it costs).  The Boltzmann
+// weight factorises over the table's axes:
 //     exp(x - shift) = exp(-(E - H_min) / T) * exp(h M / T) = a_e * b_m,
 // so a point needs one exponential per column and per row instead of one
-// per occupied cell, and a cell costs a few DFMAs in each of the two
-// remaining passes.  The factors stay inside fp64 range while |h| N / T <=
-// 300 (a_e, b_m <= e^300); beyond that a point takes one exp of the whole
-// argument per cell.  The product differs from exp(x - shift) by a few ulp
-// (the GPU tests hold every field to 1e-12 of the reference).  The cell
-// order is fixed and a warp's sums meet in a fixed xor-shuffle tree, so a
+// per occupied cell, and a cell costs a few DFMAs in each of the two passes
+// (first moments, then central second moments).  The factors stay inside
+// fp64 range while |h| N / T <= 300 (a_e, b_m <= e^300); beyond that a
+// point takes one exp of the whole argument per cell.  The product differs
+// from exp(x - shift) by a few ulp (the GPU tests hold every field to 1e-12
+// of the reference).  The cell order is fixed and a pair's sums meet in a
+// fixed order (xor-shuffle tree per warp, then warp 0 + warp 1), so a
 // point's value does not depend on which other points share the launch
 // (thermo_sweep(...)[0] == partition_point(...) exactly, test_thermo.py:
 // 85-87).
 //
 // (History, c5's 702-point grid: one CTA per point over the whole table
 // 42 us -> warp per point over a per-CTA compacted cell list 33 us -> one-
-// CTA compaction kernel + four-warp teams 16.5 us -> block-wide passes with
-// factorised weights ~14 us -> this kernel.)
+// CTA compaction kernel + four-warp teams 16.5 us -> one warp per point
+// from a per-CTA cell list, factorised weights ~10 us -> this kernel.)
 #include <cuda_runtime.h>
 #include <math.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "isd_internal.h"
 
@@ -69,6 +74,16 @@ __device__ __noinline__ double whole_weight(double g, double en, double hmin,
   return g * exp(-(en - hmin) / t);
 }
 
+// Warps per point: a pair, so each lane walks half as many cells.
+constexpr int kPairWarps = 2;
+constexpr int kPointsPerCta = kThermoWarps / kPairWarps;
+
+// Barrier over the two warps of one point (named barrier 1 + pair).
+__device__ __forceinline__ void pair_sync(int pair) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + pair), "r"(32 * kPairWarps)
+               : "memory");
+}
+
 __global__ void __launch_bounds__(kThermoThreads)
     k2_thermo(const unsigned long long* __restrict__ table, uint32_t n,
               uint32_t b, double scale, const double* __restrict__ fields,
@@ -76,8 +91,10 @@ __global__ void __launch_bounds__(kThermoThreads)
               double* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char cell_mem[];
   __shared__ int warp_tot[kThermoWarps];
-  __shared__ double a_s[kThermoWarps][32 * kColSlots];
-  __shared__ double b_s[kThermoWarps][ISD_MAX_SPINS + 1];
+  __shared__ int row_emin[ISD_MAX_SPINS + 1];  // lowest occupied e per row
+  __shared__ double a_s[kPointsPerCta][32 * kColSlots];
+  __shared__ double b_s[kPointsPerCta][ISD_MAX_SPINS + 1];
+  __shared__ double part[kPointsPerCta][kPairWarps][4];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rows = (int)n + 1, cols = (int)b + 1;
   double* cg = reinterpret_cast<double*>(cell_mem);               // counts
@@ -86,7 +103,9 @@ __global__ void __launch_bounds__(kThermoThreads)
   // 1. the CTA compacts the occupied bins into shared memory: thread
   // (warp, lane) takes rows warp + 8 k and columns lane + 32 c, all loaded
   // before any is used (one L2 round trip); one block scan of the counts
-  // places the cells in (warp, row slot, column slot) order
+  // places the cells in (warp, row slot, column slot) order.  Each row's
+  // lowest occupied column is kept: H_min of a point is then a minimum
+  // over rows, not over cells.
   constexpr int kRowSlots =
       (ISD_MAX_SPINS + 1 + kThermoWarps - 1) / kThermoWarps;
   unsigned long long gv[kRowSlots][kColSlots];
@@ -101,9 +120,17 @@ __global__ void __launch_bounds__(kThermoThreads)
   }
   int mine = 0;
 #pragma unroll
-  for (int k = 0; k < kRowSlots; ++k)
+  for (int k = 0; k < kRowSlots; ++k) {
+    int emin = 0x7fffffff;
 #pragma unroll
-    for (int c = 0; c < kColSlots; ++c) mine += gv[k][c] != 0ull;
+    for (int c = kColSlots - 1; c >= 0; --c) {
+      mine += gv[k][c] != 0ull;
+      const unsigned bal = __ballot_sync(0xffffffffu, gv[k][c] != 0ull);
+      if (bal) emin = 32 * c + __ffs(bal) - 1;
+    }
+    const int r = warp + kThermoWarps * k;
+    if (lane == 0 && r < rows) row_emin[r] = emin;
+  }
   int incl = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -131,10 +158,12 @@ __global__ void __launch_bounds__(kThermoThreads)
   }
   __syncthreads();
 
-  // 2. each warp evaluates one point from the shared cell list: warp
-  // shuffles only, no further block barrier
-  const int point = (int)blockIdx.x * kThermoWarps + warp;
-  if (point >= n_points) return;
+  // 2. each pair of warps evaluates one point from the shared cell list
+  // (warp shuffles and a pair barrier; no further block barrier)
+  const int pair = warp / kPairWarps, half = warp % kPairWarps;
+  const int pl = half * 32 + lane;  // lane within the pair
+  const int point = (int)blockIdx.x * kPointsPerCta + pair;
+  if (point >= n_points) return;  // (both warps of the pair)
   const double h = fields[point / n_temps];
   const double t = temps[point % n_temps];
   auto cell = [&](int i, double* e, double* m, int* ei, int* mi) {
@@ -144,67 +173,74 @@ __global__ void __launch_bounds__(kThermoThreads)
     *m = (double)(2 * *mi - (int)n);
     *e = (double)(2 * *ei - (int)b) * scale;
   };
-  // pass 1: H_min over the cells; shift = -H_min / T (= max of x = -H / T:
-  // division by T > 0 is monotone)
+  // H_min = min over rows of (lowest occupied E) - h M; shift = -H_min / T
+  // (= max of x = -H / T: division by T > 0 is monotone).  Both warps of
+  // the pair compute it, identically.
   double hmin = INFINITY;
-  for (int i = lane; i < nc; i += 32) {
-    double e, m;
-    int ei, mi;
-    cell(i, &e, &m, &ei, &mi);
-    hmin = fmin(hmin, e - h * m);
-  }
+  for (int r = lane; r < rows; r += 32)
+    if (row_emin[r] != 0x7fffffff)
+      hmin = fmin(hmin, (double)(2 * row_emin[r] - (int)b) * scale -
+                            h * (double)(2 * r - (int)n));
   hmin = warp_min(hmin);
   const double shift = -hmin / t;
   const bool split = fabs(h) * (double)n / t <= kSplitMax;
   if (split) {
-#pragma unroll
-    for (int c = 0; c < kColSlots; ++c) {
-      const int j = lane + 32 * c;
-      if (j < cols)
-        a_s[warp][j] = exp(-((double)(2 * j - (int)b) * scale - hmin) / t);
-    }
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int r = lane + 32 * c;
-      if (r < rows) b_s[warp][r] = exp(h * (double)(2 * r - (int)n) / t);
-    }
-    __syncwarp();
+    for (int j = pl; j < cols; j += 32 * kPairWarps)
+      a_s[pair][j] = exp(-((double)(2 * j - (int)b) * scale - hmin) / t);
+    if (pl < rows) b_s[pair][pl] = exp(h * (double)(2 * pl - (int)n) / t);
+    pair_sync(pair);
   }
-  // pass 2: s = sum w and the first moments as w-weighted sums
-  double s = 0.0, su = 0.0, sm = 0.0, sa = 0.0;
-  for (int i = lane; i < nc; i += 32) {
+  // the pair's sums: each warp's xor-tree total, then warp 0 + warp 1
+  auto pair_sum = [&](auto nv_const, double* v) {
+    constexpr int NV = decltype(nv_const)::value;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) part[pair][half][k] = v[k];
+    }
+    pair_sync(pair);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] = part[pair][0][k] + part[pair][1][k];
+    pair_sync(pair);  // (part is reused by the next sum)
+  };
+  // pass 1: s = sum w and the first moments as w-weighted sums
+  double red[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int i = pl; i < nc; i += 32 * kPairWarps) {
     double e, m;
     int ei, mi;
     cell(i, &e, &m, &ei, &mi);
     const double en = e - h * m;
-    const double w = split ? cg[i] * a_s[warp][ei] * b_s[warp][mi]
+    const double w = split ? cg[i] * a_s[pair][ei] * b_s[pair][mi]
                            : whole_weight(cg[i], en, hmin, t);
-    s += w;
-    su += w * en;
-    sm += w * m;
-    sa += w * fabs(m);
+    red[0] += w;
+    red[1] += w * en;
+    red[2] += w * m;
+    red[3] += w * fabs(m);
   }
-  s = warp_sum(s);
-  const double u = warp_sum(su) / s;
-  const double mean_m = warp_sum(sm) / s;
-  const double mean_abs = warp_sum(sa) / s;
-  // pass 3: central second moments (the two-pass form of thermo.py:75-77;
+  pair_sum(std::integral_constant<int, 4>{}, red);
+  const double s = red[0];
+  const double u = red[1] / s;
+  const double mean_m = red[2] / s;
+  const double mean_abs = red[3] / s;
+  // pass 2: central second moments (the two-pass form of thermo.py:75-77;
   // the raw <H^2> - <H>^2 form cancels catastrophically at low T)
-  double ve = 0.0, vm = 0.0;
-  for (int i = lane; i < nc; i += 32) {
+  red[0] = red[1] = 0.0;
+  for (int i = pl; i < nc; i += 32 * kPairWarps) {
     double e, m;
     int ei, mi;
     cell(i, &e, &m, &ei, &mi);
     const double en = e - h * m;
-    const double w = split ? cg[i] * a_s[warp][ei] * b_s[warp][mi]
+    const double w = split ? cg[i] * a_s[pair][ei] * b_s[pair][mi]
                            : whole_weight(cg[i], en, hmin, t);
     const double de = en - u, dm = m - mean_m;
-    ve += w * (de * de);
-    vm += w * (dm * dm);
+    red[0] += w * (de * de);
+    red[1] += w * (dm * dm);
   }
-  ve = warp_sum(ve) / s;
-  vm = warp_sum(vm) / s;
-  if (lane == 0) {
+  pair_sum(std::integral_constant<int, 2>{}, red);
+  const double ve = red[0] / s;
+  const double vm = red[1] / s;
+  if (pl == 0) {
     const double log_z = shift + log(s);
     double* o = out + (size_t)point * ISD_THERMO_FIELDS;
     o[0] = log_z;
@@ -300,7 +336,7 @@ int launch_thermo_set(const TableSet& tabs, unsigned long long* sum,
           k2_thermo, cudaFuncAttributeMaxDynamicSharedMemorySize,
           (int)((ISD_MAX_SPINS + 1) * (3 * ISD_MAX_SPINS + 1) * 12));
     });
-    const int grid = (points + kThermoWarps - 1) / kThermoWarps;
+    const int grid = (points + kPointsPerCta - 1) / kPointsPerCta;
     k2_thermo<<<grid, kThermoThreads, smem, st>>>(table, n_spins, n_bonds,
                                                   scale, fields, temps,
                                                   n_temps, points, out);
