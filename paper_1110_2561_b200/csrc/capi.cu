@@ -615,7 +615,10 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
   const size_t n_final = (size_t)knob_long("ISD_TUNE_FINALISTS", kTuneFinalists);
   for (size_t s2 = 0; s2 < stage1.size() && s2 < n_final; ++s2)
     finalists.push_back(stage1[s2].second);
-  for (size_t b = 0; b < banded.size() && b < 3; ++b)
+  // (banded candidates differ mostly in their lane patterns, which the
+  // model ranks only to a few percent: time more of them)
+  const size_t n_banded = (size_t)knob_long("ISD_TUNE_BANDED", 8);
+  for (size_t b = 0; b < banded.size() && b < n_banded; ++b)
     finalists.push_back(banded[b]);
   // the finalists' NVRTC kernels compile concurrently (or come from the
   // cubin cache) before the first is timed
@@ -653,9 +656,10 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
     hp.run_begin = run0 + off;
     hp.run_end = hp.run_begin + len;
     hp.hi_step = 1;
-    // (equal-size items: the autotuner compares plans, the cost-weighted
-    // cut is computed once for the winner)
-    if (set_band_launch(lat, cands[i], &hp, sms, false)) continue;
+    // (banded candidates are timed with the cost-weighted item cut the walk
+    // will use: equal-size items add a plan-dependent imbalance of a few
+    // percent, enough to rank two lane patterns the wrong way round)
+    if (set_band_launch(lat, cands[i], &hp, sms, true)) continue;
     if (hp.band_claim &&
         cudaMemsetAsync(reinterpret_cast<void*>(hp.band_claim), 0,
                         sizeof(uint32_t), st) != cudaSuccess)

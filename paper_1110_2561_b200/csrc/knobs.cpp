@@ -37,7 +37,7 @@ const char* const kKnownKnobs[] = {
     "ISD_NHIST_MAX",         "ISD_PAIR",
     "ISD_PLAN_TOP",          "ISD_PLAN_WIDE",
     "ISD_PROBE",             "ISD_TUNE_CANDIDATES",
-    "ISD_TUNE_FINALISTS",
+    "ISD_TUNE_FINALISTS",    "ISD_TUNE_BANDED",
 };
 }  // namespace
 
