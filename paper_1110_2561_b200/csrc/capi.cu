@@ -1042,6 +1042,64 @@ static int prepare_walk(const isd_lattice* lat, uint64_t start, uint64_t end,
   return ISD_OK;
 }
 
+// Prepared walks are memoised: a repeated walk (same lattice, range, algo,
+// table and device, same knobs) reuses its operation list instead of
+// rebuilding plan keys, band items and kernel lookups on every call (tens
+// of microseconds of host time on the e2e path).  Only fully tuned walks are
+// kept; knob changes and installed plans clear the memo.
+struct PreparedWalk {
+  std::vector<Op> ops;
+  std::string kernel_info;
+};
+static std::mutex g_prep_mu;
+static std::map<std::string, PreparedWalk> g_prep;
+
+static void forget_prepared() {
+  std::lock_guard<std::mutex> lock(g_prep_mu);
+  g_prep.clear();
+}
+
+static int prepare_walk_cached(const isd_lattice* lat, uint64_t start,
+                               uint64_t end, int algo,
+                               unsigned long long* out, int accumulate,
+                               bool capturing, std::vector<Op>* ops) {
+  int dev = -1;
+  cudaGetDevice(&dev);
+  std::string key(reinterpret_cast<const char*>(lat), sizeof(*lat));
+  char buf[160];
+  std::snprintf(buf, sizeof buf, "|%llu|%llu|%d|%d|%p|%d",
+                (unsigned long long)start, (unsigned long long)end, algo,
+                accumulate, (void*)out, dev);
+  key += buf;
+  key += knob_signature();
+  if (!capturing) {
+    std::lock_guard<std::mutex> lock(g_prep_mu);
+    auto it = g_prep.find(key);
+    if (it != g_prep.end()) {
+      ops->insert(ops->end(), it->second.ops.begin(), it->second.ops.end());
+      g_kernel_info = it->second.kernel_info;
+      return ISD_OK;
+    }
+  }
+  std::vector<Op> mine;
+  const int rc =
+      prepare_walk(lat, start, end, algo, out, accumulate, capturing, &mine);
+  if (rc) return rc;
+  // keep it only when the plan is final: a large walk's plan must be tuned
+  // (not the model's stand-in used while capturing), and no op may depend
+  // on per-launch state (dynamic item claims reset a counter slot)
+  bool keep = !capturing;
+  for (const Op& op : mine)
+    keep = keep && std::strcmp(op.what, "band claim counter reset") != 0;
+  if (keep) {
+    std::lock_guard<std::mutex> lock(g_prep_mu);
+    if (g_prep.size() >= 256) g_prep.clear();
+    g_prep[key] = PreparedWalk{mine, g_kernel_info};
+  }
+  ops->insert(ops->end(), mine.begin(), mine.end());
+  return ISD_OK;
+}
+
 static bool stream_capturing(cudaStream_t st) {
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) {
@@ -1055,8 +1113,8 @@ static int enumerate_impl(const isd_lattice* lat, uint64_t start,
                           uint64_t end, int algo, unsigned long long* out,
                           int accumulate, cudaStream_t st, int* launches) {
   std::vector<Op> ops;
-  const int rc = prepare_walk(lat, start, end, algo, out, accumulate,
-                              stream_capturing(st), &ops);
+  const int rc = prepare_walk_cached(lat, start, end, algo, out, accumulate,
+                                     stream_capturing(st), &ops);
   if (rc) return rc;
   return issue_ops(ops, st, launches);
 }
@@ -1190,8 +1248,9 @@ static int enumerate_multi(const isd_lattice* lat, uint64_t start,
     bool first = true;
     for (int i = 0; i < n_shards && !prc[j]; ++i) {
       if (devs[i] != d) continue;
-      prc[j] = prepare_walk(lat, edge[i], edge[i + 1], algo & 0xff,
-                            g_dev[d].d_counts, first ? 0 : 1, false, &ops[i]);
+      prc[j] = prepare_walk_cached(lat, edge[i], edge[i + 1], algo & 0xff,
+                                   g_dev[d].d_counts, first ? 0 : 1, false,
+                                   &ops[i]);
       first = false;
       if (prc[j]) perr[j] = g_err;
     }
@@ -1254,7 +1313,9 @@ static int enumerate_multi(const isd_lattice* lat, uint64_t start,
   for (size_t j = 0; j < uniq.size(); ++j) {
     const int d = uniq[j];
     if (d != root) cudaStreamWaitEvent(R.stream, done[j], 0);
-    if (peer_access(root, d)) {
+    // (ISD_PEER=0: take the copy path even where the root could read the
+    // table directly — how the one-GPU pool tests it)
+    if (knob_long("ISD_PEER", 1) != 0 && peer_access(root, d)) {
       tabs.t[j] = g_dev[d].d_counts;
     } else {
       unsigned long long* copy = R.d_copies + j * (bytes / 8);
@@ -1381,6 +1442,7 @@ int isd_set_walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
   PlanEntry& pe = g_plans[plan_key(lat, len, top)];
   pe.info = *plan;
   pe.tuned = true;
+  forget_prepared();
   return ISD_OK;
 }
 
@@ -1492,7 +1554,8 @@ int isd_enumerate(const isd_lattice* lat, uint64_t start, uint64_t end,
   // host-side preparation (plan, a first large walk's autotune, work
   // items, NVRTC kernels) happens before the timed region
   std::vector<Op> ops;
-  rc = prepare_walk(lat, start, end, algo, s->d_counts, 0, false, &ops);
+  rc = prepare_walk_cached(lat, start, end, algo, s->d_counts, 0, false,
+                           &ops);
   if (rc) return rc;
   cudaEventRecord(s->ev0, s->stream);
   int nl = 0;
@@ -1725,10 +1788,12 @@ int isd_sm_count(int device) {
 int isd_set_knob(const char* name, const char* value) {
   if (!name || !knob_known(name))
     return fail(ISD_EINVAL, "unknown knob %s", name ? name : "(null)");
+  forget_prepared();
   return set_knob(name, value);
 }
 
 int isd_clear_knobs(void) {
+  forget_prepared();
   clear_knobs();
   return ISD_OK;
 }

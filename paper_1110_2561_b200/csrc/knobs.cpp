@@ -35,6 +35,7 @@ const char* const kKnownKnobs[] = {
     "ISD_JIT",               "ISD_JIT_DUMP",
     "ISD_LAYOUT",            "ISD_LOOP_BITS",
     "ISD_NHIST_MAX",         "ISD_PAIR",
+    "ISD_PEER",
     "ISD_PLAN_TOP",          "ISD_PLAN_WIDE",
     "ISD_PROBE",             "ISD_TUNE_CANDIDATES",
     "ISD_TUNE_FINALISTS",    "ISD_TUNE_BANDED",

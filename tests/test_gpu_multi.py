@@ -37,6 +37,16 @@ def test_multi_walk_of_c5_equals_reference_golden(shards):
     assert total_ms >= sum(shard_ms) * 0.99
 
 
+def test_multi_walk_device_copy_path():
+    # where the root has no peer access it copies each device's table
+    # (cudaMemcpyPeerAsync) before the gather: forced here on one device
+    spec, want = golden("dos_5x5x1_J1.csv")
+    with _native.knobs(ISD_PEER=0):
+        table, _, _ = _native.enumerate_multi(
+            native_lattice(spec), 0, spec.num_configs, [0, 0, 0])
+    assert np.array_equal(table.view(np.int64), want)
+
+
 @pytest.mark.parametrize("shards", [1, 4, 5])
 def test_multi_walk_with_flip_symmetry(shards):
     spec, want = golden("dos_3x3x4_J1.csv")

@@ -1,10 +1,10 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-timeout 1500 python bench.py --steps 10 --warmup 3 --extra-configs "" --no-cold --no-cpu-baseline > gpurun_out/r2p_bench.json 2> gpurun_out/r2p_bench.err
+timeout 1500 python bench.py --steps 10 --warmup 3 --extra-configs "" --no-cold --no-cpu-baseline --knob ISD_CLIMB_STEPS=120 --knob ISD_CLIMB_STARTS=6 --knob ISD_TUNE_BANDED=16 > gpurun_out/r2s_bench.json 2> gpurun_out/r2s_bench.err
 python - <<'PY'
 import json
-for f in ["gpurun_out/r2p_bench.json"]:
+for f in ["gpurun_out/r2s_bench.json"]:
     try:
         d=json.loads(open(f).read().strip().splitlines()[-1])
     except Exception as e:
