@@ -18,7 +18,7 @@ def apply() -> dict:
              "ISD_BAND_SPAN ISD_BAND_WEIGHTS ISD_CLIMB_STARTS ISD_CLIMB_STEPS "
              "ISD_COPY_VARIANT ISD_GPU_CLIMB ISD_GRAY ISD_GRID_SMS "
              "ISD_HIST_BYTES ISD_JIT ISD_JIT_DUMP ISD_LAYOUT ISD_LOOP_BITS "
-             "ISD_NHIST_MAX ISD_PAIR ISD_PLAN_TOP ISD_PLAN_WIDE ISD_PROBE "
+             "ISD_NHIST_MAX ISD_PAIR ISD_PEER ISD_PLAN_TOP ISD_PLAN_WIDE ISD_PROBE "
              "ISD_TUNE_CANDIDATES ISD_TUNE_FINALISTS ISD_TUNE_BANDED").split()
     applied = {}
     for name in names:
