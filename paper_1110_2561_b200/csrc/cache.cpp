@@ -10,7 +10,8 @@
 // Layout: a list of directories (isd_set_cache_dirs); the first is written,
 // the others are read-only seeds.  One file per entry, named by a 128-bit
 // hash of its key; the file stores the full key, so a hash collision is a
-// miss, never a wrong plan.  Writes go to a temporary file and are renamed
+// miss, never a wrong plan, and a checksum of the payload, so a torn or
+// corrupted file is a miss too.  Writes go to a temporary file and are renamed
 // into place (atomic for concurrent processes).  Keys carry ISD_BUILD_ID (a
 // hash of the library sources, set by _build.py), so a rebuilt library never
 // reads another build's entries.
@@ -37,7 +38,7 @@ std::mutex g_cache_mu;
 std::vector<std::string> g_dirs;  // [0] is written, the rest are read-only
 std::atomic<unsigned> g_tmp_seq{0};
 
-constexpr char kMagic[8] = {'I', 'S', 'D', 'C', 'A', 'C', 'H', '1'};
+constexpr char kMagic[8] = {'I', 'S', 'D', 'C', 'A', 'C', 'H', '2'};
 
 uint64_t fnv1a(const std::string& s, uint64_t h) {
   for (unsigned char c : s) {
@@ -102,13 +103,16 @@ bool cache_get(const std::string& kind, const std::string& key,
   for (const std::string& d : dirs) {
     std::string data;
     if (!read_file(d + "/" + name, &data)) continue;
-    // magic | u64 key length | key | blob
-    if (data.size() < 16 || std::memcmp(data.data(), kMagic, 8) != 0)
+    // magic | u64 key length | key | u64 FNV-1a of the blob | blob
+    if (data.size() < 24 || std::memcmp(data.data(), kMagic, 8) != 0)
       continue;
-    uint64_t klen = 0;
+    uint64_t klen = 0, sum = 0;
     std::memcpy(&klen, data.data() + 8, 8);
-    if (data.size() < 16 + klen || data.compare(16, klen, full) != 0) continue;
-    *blob = data.substr(16 + klen);
+    if (data.size() < 24 + klen || data.compare(16, klen, full) != 0) continue;
+    std::memcpy(&sum, data.data() + 16 + klen, 8);
+    std::string b = data.substr(24 + klen);
+    if (fnv1a(b, 1469598103934665603ull) != sum) continue;  // torn / corrupt
+    *blob = std::move(b);
     return true;
   }
   return false;
@@ -133,9 +137,11 @@ void cache_put(const std::string& kind, const std::string& key,
   FILE* f = std::fopen(tmp.c_str(), "wb");
   if (!f) return;  // a read-only or missing cache is not an error
   const uint64_t klen = full.size();
+  const uint64_t sum = fnv1a(blob, 1469598103934665603ull);
   bool ok = std::fwrite(kMagic, 1, 8, f) == 8 &&
             std::fwrite(&klen, 1, 8, f) == 8 &&
             std::fwrite(full.data(), 1, full.size(), f) == full.size() &&
+            std::fwrite(&sum, 1, 8, f) == 8 &&
             std::fwrite(blob.data(), 1, blob.size(), f) == blob.size();
   ok = (std::fclose(f) == 0) && ok;
   if (!ok || std::rename(tmp.c_str(), path.c_str()) != 0)

@@ -59,13 +59,17 @@ def test_second_process_reuses_the_tuned_plan(tmp_path):
     assert second["ms"] < 0.25 * first["ms"], (first, second)
 
 
-def test_corrupt_cache_entries_are_ignored(tmp_path):
+@pytest.mark.parametrize("where", ["key", "payload"])
+def test_corrupt_cache_entries_are_ignored(tmp_path, where):
     cache = str(tmp_path / "cache")
     good = _run(cache)
     for n in os.listdir(cache):
-        with open(os.path.join(cache, n), "r+b") as f:
-            f.seek(20)
-            f.write(b"\xff" * 16)  # inside the stored key: every entry misses
+        path = os.path.join(cache, n)
+        with open(path, "r+b") as f:
+            # inside the stored key (a miss by key), or the last bytes of the
+            # payload (a miss by checksum: never a damaged plan or cubin)
+            f.seek(20 if where == "key" else os.path.getsize(path) - 8)
+            f.write(b"\xff" * 8)
     again = _run(cache)
     assert again["sum"] == good["sum"] == 1 << 34
 
