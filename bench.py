@@ -13,10 +13,11 @@ GPU count grows ("scaling": "strong").
 Timing follows the harness contract: W untimed warm-up steps, then K timed
 steps, each bracketed by CUDA events on the launching stream, with the L2
 flushed (a 256 MiB write) between steps outside the events; max over ranks.
-`e2e` repeats the step through the public API with host buffers
-(`enumerate_shard` -> host table, host -> device -> NCCL reduce for N > 1,
-`thermo_grid` from the host table), host<->device copies inside the timed
-region.  `--impl reference` times the reference algorithm on the host cores
+`e2e` repeats the step through the public API with host buffers, host<->
+device copies inside the timed region: on one GPU `dos_thermo` (walk +
+thermodynamics in one engine call: grid up, table and results down); for
+N > 1 `enumerate_shard` -> host table, host -> device -> NCCL reduce,
+`thermo_grid` on the root.  `--impl reference` times the reference algorithm on the host cores
 (the oracle's numpy restatement of enumeration.py:167-235; the reference
 is pure Python and cannot be installed on the GPU box).
 """
@@ -647,15 +648,17 @@ def run_b200(args, wl):
     h_temps = np.asarray(wl.temps, dtype=np.float64)
 
     def e2e_step():
+        if not use_dist:
+            # one GPU: the public one-call pipeline (walk + thermodynamics,
+            # host grid in, host table and results out)
+            isd.dos_thermo(wl.spec, h_fields, h_temps)
+            return
         shard = isd.make_shards(wl.spec, world)[rank]
         part = isd.enumerate_shard(wl.spec, None, shard)
-        if use_dist:
-            t = torch.from_numpy(part.counts).to(dev)
-            dist.reduce(t, dst=0)
-            counts = t.cpu().numpy() if rank == 0 else None
-            hist = isd.DoSHistogram(wl.spec, counts) if rank == 0 else None
-        else:
-            hist = part
+        t = torch.from_numpy(part.counts).to(dev)
+        dist.reduce(t, dst=0)
+        counts = t.cpu().numpy() if rank == 0 else None
+        hist = isd.DoSHistogram(wl.spec, counts) if rank == 0 else None
         if rank == 0:
             isd.thermo_grid(hist, h_fields, h_temps)
 
@@ -674,10 +677,14 @@ def run_b200(args, wl):
     table_bytes = (wl.spec.num_spins + 1) * (wl.spec.num_bonds + 1) * 8
     npts = len(wl.fields) * len(wl.temps)
     lat_bytes = 208  # sizeof(isd_lattice), passed by value to the kernels
-    h2d = lat_bytes + (table_bytes if use_dist else 0) + \
-        (table_bytes + 8 * (len(wl.fields) + len(wl.temps)) if rank == 0 else 0)
-    d2h = table_bytes + (table_bytes if use_dist and rank == 0 else 0) + \
-        (npts * 7 * 8 if rank == 0 else 0)
+    grid_bytes = 8 * (len(wl.fields) + len(wl.temps))
+    if use_dist:  # enumerate_shard, NCCL reduce, thermo_grid on the root
+        h2d = lat_bytes + table_bytes + \
+            (table_bytes + grid_bytes if rank == 0 else 0)
+        d2h = table_bytes + (table_bytes + npts * 7 * 8 if rank == 0 else 0)
+    else:  # dos_thermo: lattice + grid up, table + results down
+        h2d = lat_bytes + grid_bytes
+        d2h = table_bytes + npts * 7 * 8
 
     # ---- other configs (value only, same protocol, fewer steps) -----------
     extra = {}

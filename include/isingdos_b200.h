@@ -133,6 +133,19 @@ int isd_naive_enumerate(uint32_t n_spins, const uint32_t* bit_of_slot,
                         uint64_t start, uint64_t end, int device,
                         uint64_t* counts_host);
 
+/* The whole pipeline in one call: isd_enumerate_multi, then on the root
+ * the thermodynamic grid of the combined table (as isd_thermo) — host grid
+ * in, host table and results out, one synchronisation.  The table of a
+ * full walk [0, 2^N) is what the grid is evaluated from; the caller checks
+ * completeness (thermo.py:59-63).  out_host: ISD_THERMO_FIELDS doubles per
+ * (field, temperature) point, field-major. */
+int isd_enumerate_thermo(const isd_lattice* lat, uint64_t start, uint64_t end,
+                         int n_shards, const int* devs, int algo,
+                         double energy_scale, const double* fields,
+                         int n_fields, const double* temps, int n_temps,
+                         uint64_t* counts_host, double* out_host,
+                         double* shard_ms, double* total_ms);
+
 /* In-place completion of a half walk: counts[m][e] += counts[N-m][e]
  * pairwise (rows m and N-m both become the sum).  Device buffer, async. */
 int isd_mirror_async(uint64_t* counts_dev, uint32_t n_spins, uint32_t n_bonds,

@@ -69,6 +69,7 @@ from .lattice import (
 )
 from .thermo import (
     ThermoPoint,
+    dos_thermo,
     partition_point,
     temperature_grid,
     thermo_grid,
@@ -89,7 +90,7 @@ __all__ = [
     "encode_words", "enumerate_shard", "full_dos", "full_dos_timed",
     "gpu_count", "make_shards", "merge", "partition_point", "popcount",
     "random_bond_signs", "set_device", "spin_excess", "temperature_grid",
-    "thermo_grid", "thermo_sweep", "total_energy", "unsatisfied_bonds",
+    "thermo_grid", "thermo_sweep", "dos_thermo", "total_energy", "unsatisfied_bonds",
     "verify_dos", "ORACLE_MAX_SPINS", "brute_force_log_z", "decode_spins",
     "oracle_energy", "oracle_full_dos", "oracle_magnetization",
 ]

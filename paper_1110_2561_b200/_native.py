@@ -33,6 +33,7 @@ EXPORTED_SYMBOLS = (
     "isd_set_cache_dirs", "isd_build_id", "isd_enumerate_multi",
     "isd_thermo_gather_async", "isd_walk_plan", "isd_set_walk_plan",
     "isd_band_costs", "isd_plan_range", "isd_naive_enumerate",
+    "isd_enumerate_thermo",
 )
 
 
@@ -155,6 +156,10 @@ def load():
             ctypes.c_uint32, vp, ctypes.c_uint32, vp, vp, i32, u64, u64, i32,
             vp]
         lib.isd_naive_enumerate.restype = ctypes.c_int
+        lib.isd_enumerate_thermo.argtypes = [
+            p_lat, u64, u64, i32, vp, i32, dbl, vp, i32, vp, i32, vp, vp, vp,
+            p_dbl]
+        lib.isd_enumerate_thermo.restype = ctypes.c_int
         lib.isd_set_cache_dirs.argtypes = [ctypes.c_char_p]
         lib.isd_set_cache_dirs.restype = ctypes.c_int
         lib.isd_build_id.restype = ctypes.c_char_p
@@ -298,6 +303,28 @@ def enumerate_multi(lat: Lattice, start: int, end: int, devices,
                                   shard_ms.ctypes.data, ctypes.byref(total)))
     return (out.reshape(lat.n_spins + 1, lat.n_bonds + 1), shard_ms.tolist(),
             total.value)
+
+
+def enumerate_thermo(lat: Lattice, start: int, end: int, devices,
+                     scale: float, fields, temps, algo: int = ALGO_AUTO):
+    """Walk + combine + thermodynamic grid in one engine call
+    (isd_enumerate_thermo).  Returns (uint64 table, float64 [F, T, 7],
+    per-shard device ms, root ms)."""
+    lib = load()
+    devs = np.ascontiguousarray(devices, dtype=np.int32)
+    f = np.ascontiguousarray(fields, dtype=np.float64)
+    t = np.ascontiguousarray(temps, dtype=np.float64)
+    out = np.zeros((lat.n_spins + 1) * (lat.n_bonds + 1), dtype=np.uint64)
+    grid = np.empty((len(f), len(t), ISD_THERMO_FIELDS), dtype=np.float64)
+    shard_ms = np.zeros(len(devs), dtype=np.float64)
+    total = ctypes.c_double(0.0)
+    check(lib.isd_enumerate_thermo(
+        ctypes.byref(lat), start, end, len(devs), devs.ctypes.data, algo,
+        float(scale), f.ctypes.data, len(f), t.ctypes.data, len(t),
+        out.ctypes.data, grid.ctypes.data, shard_ms.ctypes.data,
+        ctypes.byref(total)))
+    return (out.reshape(lat.n_spins + 1, lat.n_bonds + 1), grid,
+            shard_ms.tolist(), total.value)
 
 
 def thermo_gather_device(table_ptrs, sum_ptr, n_spins, n_bonds, scale,

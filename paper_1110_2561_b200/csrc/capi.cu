@@ -1166,10 +1166,21 @@ static void split_range(uint64_t start, uint64_t end, int n,
     (*edge)[i] = start + (uint64_t)i * q + std::min<uint64_t>((uint64_t)i, r);
 }
 
+// The thermodynamic grid a multi-device walk evaluates on the root right
+// after the combine (isd_enumerate_thermo): host inputs and output.
+struct ThermoReq {
+  double scale;
+  const double* fields;
+  int n_fields;
+  const double* temps;
+  int n_temps;
+  double* out_host;
+};
+
 static int enumerate_multi(const isd_lattice* lat, uint64_t start,
                            uint64_t end, int n_shards, const int* devs,
                            int algo, uint64_t* counts_host, double* shard_ms,
-                           double* total_ms) {
+                           double* total_ms, const ThermoReq* thermo = nullptr) {
   NvtxRange nvtx("isd:enumerate_multi");
   char err[256];
   int rc = validate_lattice(lat, err, sizeof err);
@@ -1234,6 +1245,16 @@ static int enumerate_multi(const isd_lattice* lat, uint64_t start,
   rc = ensure_buffer(&R.d_copies, &R.d_copies_bytes, bytes * uniq.size(),
                      "cudaMalloc(table copies)");
   if (rc) return rc;
+  // the grid, if any: [fields | temps | results] in the root's d_buf, the
+  // inputs copied up at the start (they overlap the walks)
+  const size_t n_pts = thermo ? (size_t)thermo->n_fields * thermo->n_temps : 0;
+  const size_t grid_in = thermo ? (size_t)(thermo->n_fields + thermo->n_temps) * 8 : 0;
+  const size_t grid_out = n_pts * ISD_THERMO_FIELDS * 8;
+  if (n_pts) {
+    rc = ensure_buffer(&R.d_buf, &R.d_buf_bytes, grid_in + grid_out,
+                       "cudaMalloc(thermo)");
+    if (rc) return rc;
+  }
   std::vector<uint64_t> edge;
   split_range(wstart, wend, n_shards, &edge);
 
@@ -1282,7 +1303,19 @@ static int enumerate_multi(const isd_lattice* lat, uint64_t start,
   std::fill(ee.begin(), ee.end(), nullptr);
   std::fill(done.begin(), done.end(), nullptr);
   cudaSetDevice(root);
+  void* stage = nullptr;
+  rc = stage_buffer(&R, bytes + grid_in + grid_out, &stage);
+  if (rc) return rc;
+  char* hs = static_cast<char*>(stage);
   cudaEventRecord(R.ev0, R.stream);
+  if (n_pts) {
+    std::memcpy(hs + bytes, thermo->fields, (size_t)thermo->n_fields * 8);
+    std::memcpy(hs + bytes + (size_t)thermo->n_fields * 8, thermo->temps,
+                (size_t)thermo->n_temps * 8);
+    e = cudaMemcpyAsync(R.d_buf, hs + bytes, grid_in, cudaMemcpyHostToDevice,
+                        R.stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(grid)");
+  }
   int nl = 0;
   for (size_t j = 0; j < uniq.size(); ++j) {
     const int d = uniq[j];
@@ -1306,10 +1339,12 @@ static int enumerate_multi(const isd_lattice* lat, uint64_t start,
     cudaEventCreateWithFlags(&done[j], cudaEventDisableTiming);
     cudaEventRecord(done[j], st);
   }
-  // 3. combine on the root: one kernel reads every device's table
+  // 3. combine on the root: one kernel reads every device's table (none
+  // when the root walked everything itself: its table is the result)
   cudaSetDevice(root);
   TableSet tabs;
   tabs.n = (int)uniq.size();
+  unsigned long long* result = R.d_sum;
   for (size_t j = 0; j < uniq.size(); ++j) {
     const int d = uniq[j];
     if (d != root) cudaStreamWaitEvent(R.stream, done[j], 0);
@@ -1328,32 +1363,43 @@ static int enumerate_multi(const isd_lattice* lat, uint64_t start,
       tabs.t[j] = copy;
     }
   }
-  int r = launch_gather(tabs, R.d_sum, lat->n_spins, lat->n_bonds, R.stream);
+  int r = 0;
+  if (tabs.n == 1 && tabs.t[0] == g_dev[root].d_counts)
+    result = g_dev[root].d_counts;
+  else
+    r = launch_gather(tabs, R.d_sum, lat->n_spins, lat->n_bonds, R.stream);
   if (r >= 0 && flip) {
-    const int r2 = launch_mirror(R.d_sum, lat->n_spins, lat->n_bonds, R.stream);
+    const int r2 = launch_mirror(result, lat->n_spins, lat->n_bonds, R.stream);
     r = r2 < 0 ? r2 : r + r2;
+  }
+  if (r >= 0 && n_pts) {
+    const double* d_f = reinterpret_cast<const double*>(R.d_buf);
+    const double* d_t = d_f + thermo->n_fields;
+    double* d_o = R.d_buf + thermo->n_fields + thermo->n_temps;
+    const int r3 = launch_thermo(result, lat->n_spins, lat->n_bonds,
+                                 thermo->scale, d_f, thermo->n_fields, d_t,
+                                 thermo->n_temps, d_o, R.stream);
+    r = r3 < 0 ? r3 : r + r3;
   }
   if (r < 0) {
     destroy_events();
-    return cuda_fail((cudaError_t)(-r), "k4_gather launch");
+    return cuda_fail((cudaError_t)(-r), "k4 / k2 launch");
   }
   nl += r;
   bump_launches((uint64_t)nl);
   cudaEventRecord(R.ev1, R.stream);
-  void* stage = nullptr;
-  rc = stage_buffer(&R, bytes, &stage);
-  if (rc) {
-    destroy_events();
-    return rc;
-  }
-  e = cudaMemcpyAsync(stage, R.d_sum, bytes, cudaMemcpyDeviceToHost,
-                      R.stream);
+  e = cudaMemcpyAsync(stage, result, bytes, cudaMemcpyDeviceToHost, R.stream);
+  if (e == cudaSuccess && n_pts)
+    e = cudaMemcpyAsync(hs + bytes + grid_in,
+                        R.d_buf + thermo->n_fields + thermo->n_temps, grid_out,
+                        cudaMemcpyDeviceToHost, R.stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(R.stream);
   if (e != cudaSuccess) {
     destroy_events();
     return cuda_fail(e, "multi-device enumeration");
   }
   std::memcpy(counts_host, stage, bytes);
+  if (n_pts) std::memcpy(thermo->out_host, hs + bytes + grid_in, grid_out);
   for (int i = 0; i < n_shards; ++i) {
     float ms = 0.f;
     cudaSetDevice(devs[i]);
@@ -1586,6 +1632,24 @@ int isd_enumerate_multi(const isd_lattice* lat, uint64_t start, uint64_t end,
                         double* total_ms) {
   return enumerate_multi(lat, start, end, n_shards, devs, algo, counts_host,
                          shard_ms, total_ms);
+}
+
+int isd_enumerate_thermo(const isd_lattice* lat, uint64_t start, uint64_t end,
+                         int n_shards, const int* devs, int algo,
+                         double energy_scale, const double* fields,
+                         int n_fields, const double* temps, int n_temps,
+                         uint64_t* counts_host, double* out_host,
+                         double* shard_ms, double* total_ms) {
+  if (n_fields < 0 || n_temps < 0)
+    return fail(ISD_EINVAL, "negative grid size");
+  if (!(energy_scale > 0)) return fail(ISD_EINVAL, "energy_scale must be > 0");
+  if (n_fields * n_temps > 0 && (!fields || !temps || !out_host))
+    return fail(ISD_EINVAL, "NULL buffer");
+  for (int i = 0; i < n_temps; ++i)
+    if (!(temps[i] > 0)) return fail(ISD_EINVAL, "temperatures must be > 0");
+  ThermoReq req{energy_scale, fields, n_fields, temps, n_temps, out_host};
+  return enumerate_multi(lat, start, end, n_shards, devs, algo, counts_host,
+                         shard_ms, total_ms, &req);
 }
 
 int isd_thermo_gather_async(const uint64_t* const* tables_dev, int n_tables,

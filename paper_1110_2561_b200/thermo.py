@@ -63,6 +63,40 @@ def thermo_grid(dos: DoSHistogram, fields, temps, *, device=None):
     return out
 
 
+def dos_thermo(spec, fields, temps, workers=None, *, flip_symmetry=False):
+    """Density of states and its thermodynamic grid in one engine call
+    (an extension: `full_dos` + `thermo_grid` without the table's round
+    trip through the host).
+
+    The shards (as `full_dos_timed`: `workers`, default one per GPU) are
+    walked and combined on the root GPU, which then evaluates the
+    (fields x temps) grid from the combined table; one synchronisation.
+    Returns (DoSHistogram, float64 array [len(fields), len(temps), 7]) with
+    the columns of `thermo_grid`.
+    """
+    from .enumeration import (_plan_shards, _signed, gpu_count,
+                              native_lattice)
+    fields = np.asarray(fields, dtype=np.float64).reshape(-1)
+    temps = np.asarray(temps, dtype=np.float64).reshape(-1)
+    if not np.all(temps > 0):  # (NaN fails too)
+        raise ValueError("all temperatures must be > 0")
+    if workers is None:
+        workers = min(max(gpu_count(), 1), spec.num_configs)
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    shards = _plan_shards(spec, workers, flip_symmetry)
+    devices = gpu_count()
+    if devices < 1:
+        raise _native.NativeError("no CUDA device available for enumeration")
+    algo = _native.ALGO_AUTO | (_native.FLAG_FLIP_SYMMETRY if flip_symmetry
+                                else 0)
+    table, grid, _, _ = _native.enumerate_thermo(
+        native_lattice(spec), 0, spec.num_configs,
+        [sh.shard_id % devices for sh in shards], abs(spec.coupling),
+        fields, temps, algo)
+    return DoSHistogram(spec, _signed(table)), grid
+
+
 def _point(h, t, row) -> ThermoPoint:
     return ThermoPoint(field=h, temperature=t, log_z=float(row[0]),
                        free_energy=float(row[1]),

@@ -193,3 +193,26 @@ def test_knobs_are_not_read_from_the_environment(monkeypatch):
     with _native.knobs(ISD_JIT=2):
         isd.full_dos(spec)
         assert _native.kernel_info() == "k1_hoisted_jit"
+
+
+@pytest.mark.parametrize("name,workers,flip", [("c2", 1, False), ("c2", 5, False),
+                                               ("c5", 8, False), ("c5", 4, True),
+                                               ("c1", 3, False)])
+def test_dos_thermo_equals_full_dos_then_thermo_grid(name, workers, flip):
+    w = workloads()[name]
+    dos, grid = isd.dos_thermo(w.spec, w.fields, w.temps, workers,
+                               flip_symmetry=flip)
+    want = isd.full_dos(w.spec)
+    assert dos == want
+    # the same K2 over the same table: identical, not merely close
+    assert np.array_equal(grid, isd.thermo_grid(want, w.fields, w.temps))
+
+
+def test_dos_thermo_validates():
+    spec = isd.LatticeSpec(3, 3)
+    with pytest.raises(ValueError, match="temperature"):
+        isd.dos_thermo(spec, [0.0], [1.0, 0.0])
+    with pytest.raises(ValueError, match="workers"):
+        isd.dos_thermo(spec, [0.0], [1.0], workers=0)
+    dos, grid = isd.dos_thermo(spec, [], [1.0])
+    assert grid.shape == (0, 1, 7) and dos == isd.full_dos(spec)
