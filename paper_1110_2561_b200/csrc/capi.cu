@@ -251,43 +251,13 @@ static bool band_ok(const isd_plan_info& info, uint64_t start, uint64_t end) {
 }
 
 static std::mutex g_items_mu;
-struct DeviceItems {
-  BandItem* items;
-  uint32_t count;
-  const unsigned long long* starts;  // 32 per item (band_starts)
-};
-static std::map<std::string, DeviceItems> g_items;
-
-// The g-th F-bit number in (popcount, value) order and its popcount (the
-// kernel's isd_unrank, k1_body.cuh).
-static uint64_t host_unrank(uint64_t g, int F, int* q) {
-  auto binom = [](int n, int k) -> uint64_t {
-    if (k < 0 || k > n) return 0;
-    uint64_t r = 1;
-    for (int i = 1; i <= k; ++i) r = r * (uint64_t)(n - k + i) / (uint64_t)i;
-    return r;
-  };
-  int qq = 0;
-  while (qq < F && g >= binom(F, qq)) g -= binom(F, qq++);
-  *q = qq;
-  uint64_t v = 0;
-  for (int bit = F - 1; bit >= 0 && qq > 0; --bit) {
-    const uint64_t cb = binom(bit, qq);
-    if (g >= cb) {
-      v |= 1ull << bit;
-      g -= cb;
-      --qq;
-    }
-  }
-  return v;
-}
+static std::map<std::string, std::pair<BandItem*, uint32_t>> g_items;
 
 // Device work items for 2^F slots (uploaded once per device, size and cost
 // curve; `cost_key` identifies w).
 static int band_items(int F, int n_target, int span,
                       const std::vector<double>& w, const std::string& cost_key,
-                      double flush_units, BandItem** ptr, uint32_t* count,
-                      const unsigned long long** starts) {
+                      double flush_units, BandItem** ptr, uint32_t* count) {
   int dev = 0;
   cudaGetDevice(&dev);
   const std::string key = std::to_string(dev) + ":" + std::to_string(F) +
@@ -341,40 +311,16 @@ static int band_items(int F, int n_target, int span,
       if (next != (1ull << F))
         return fail(ISD_EINVAL, "band work items do not tile the slots");
     }
-    // each of the 32 warps' first chunk starts at slot w c0 of its item
-    // (k1_body.cuh): unranked here once instead of in every launch
-    std::vector<unsigned long long> st(host.size() * 32, 0ull);
-    for (size_t i = 0; i < host.size(); ++i) {
-      const uint64_t n = host[i].g1 - host[i].g0;
-      uint64_t c0 = n / 64;
-      c0 = c0 ? c0 : 1;
-      for (uint64_t wv = 0; wv < 32; ++wv) {
-        if (wv * c0 >= n) break;
-        int q = 0;
-        const uint64_t v = host_unrank(host[i].g0 + wv * c0, F, &q);
-        st[i * 32 + wv] = v | ((unsigned long long)q << 32);
-      }
-    }
     const size_t item_bytes = host.size() * sizeof(BandItem);
-    const size_t start_bytes = st.size() * sizeof(unsigned long long);
-    char* d = nullptr;
-    cudaError_t e = cudaMalloc(&d, item_bytes + start_bytes);
+    BandItem* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, item_bytes);
     if (e == cudaSuccess)
       e = cudaMemcpy(d, host.data(), item_bytes, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-      e = cudaMemcpy(d + item_bytes, st.data(), start_bytes,
-                     cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "band work items");
-    it = g_items
-             .emplace(key, DeviceItems{reinterpret_cast<BandItem*>(d),
-                                       (uint32_t)host.size(),
-                                       reinterpret_cast<const unsigned long long*>(
-                                           d + item_bytes)})
-             .first;
+    it = g_items.emplace(key, std::make_pair(d, (uint32_t)host.size())).first;
   }
-  *ptr = it->second.items;
-  *count = it->second.count;
-  *starts = it->second.starts;
+  *ptr = it->second.first;
+  *count = it->second.second;
   return ISD_OK;
 }
 
@@ -488,7 +434,6 @@ static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
   hp->band_items = 0;
   hp->band_n_items = 0;
   hp->band_claim = 0;
-  hp->band_starts = 0;
   if (!hp->band_rows) return ISD_OK;
   const int rb = log2_exact(hp->run_end - hp->run_begin);
   if (rb < 6) return fail(ISD_EINVAL, "banded launch needs 2^r runs");
@@ -513,15 +458,13 @@ static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
   // a flush (~20 K SM cycles) in units of one slot's walk at one wavefront
   // per RED (a slot = 32 lanes x 2^l loop subsets x 32 REDs / 32 lanes)
   const double flush_units = 20000.0 / (double)(32u << hp->l);
-  const unsigned long long* starts = nullptr;
   const int rc = band_items(F, (per_sm < 1 ? 1 : per_sm) * sms,
                             (int)hp->band_span, w ? *w : equal, cost_key,
-                            flush_units, &items, &count, &starts);
+                            flush_units, &items, &count);
   if (rc) return rc;
   hp->band_free_bits = (uint32_t)(rb - 5);
   hp->band_items = (uint64_t)(uintptr_t)items;
   hp->band_n_items = count;
-  hp->band_starts = (uint64_t)(uintptr_t)starts;
   // ISD_BAND_DYNAMIC=1: blocks claim items from a counter (measured no
   // faster than the static round-robin over items in slot order)
   if (knob_long("ISD_BAND_DYNAMIC", 0) != 0) {

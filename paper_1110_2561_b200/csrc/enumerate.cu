@@ -187,8 +187,7 @@ __global__ void __launch_bounds__(PAIR == 2 ? kWideThreads : kThreads)
       L, P.run_begin, P.run_end - P.run_begin, P.hi_step, P.lane_mask, lanes,
       reinterpret_cast<const IsdBandItem*>(P.band_items), P.band_n_items,
       (int)P.band_free_bits,
-      reinterpret_cast<unsigned int*>(P.band_claim),
-      reinterpret_cast<const unsigned long long*>(P.band_starts), hist, out);
+      reinterpret_cast<unsigned int*>(P.band_claim), hist, out);
 }
 
 // ---------------------------------------------------------------------------

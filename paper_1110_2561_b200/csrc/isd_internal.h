@@ -122,10 +122,6 @@ struct HoistParams {
   // banded launches: a zeroed u32 counter the blocks claim items from
   // (dynamic scheduling; 0 = static round-robin)
   uint64_t band_claim;
-  // banded launches: per item, the first slot (value | popcount << 32) of
-  // each of the 32 warps' first chunks, precomputed on the host (0: the
-  // kernel unranks them itself)
-  uint64_t band_starts;
 };
 
 // Largest paired histogram (words): two CTAs of 512 threads per SM fit

@@ -78,20 +78,6 @@ __host__ __device__ constexpr int isd_ctz(int s) {
   return (s & 1) ? 0 : 1 + isd_ctz(s >> 1);
 }
 
-// The it-th subset of `mask` in the order the loop enumerates them
-// (x -> ((x & mask) - mask) & mask): bit j of it goes to the j-th set bit.
-__device__ __forceinline__ unsigned int isd_deposit32(unsigned int it,
-                                                      unsigned int mask) {
-  unsigned int out = 0;
-  while (it && mask) {
-    const unsigned int low = mask & (~mask + 1u);
-    if (it & 1u) out |= low;
-    it >>= 1;
-    mask ^= low;
-  }
-  return out;
-}
-
 // Gray steps S .. 2^G - 1: flip site ctz(S) to its bit in gray(S), emit.
 // Each step is its own call site with constant arguments, so after inlining
 // the site's constants fold (a loop here stays rolled under NVRTC).
@@ -147,8 +133,7 @@ __device__ __forceinline__ void k1_hoisted_body(
     unsigned long long hi_step, unsigned long long lane_mask,
     const IsdLanes lanes, const IsdBandItem* __restrict__ items,
     unsigned int n_items, int free_bits, unsigned int* claim,
-    const unsigned long long* __restrict__ starts, unsigned int* hist,
-    unsigned long long* __restrict__ out) {
+    unsigned int* hist, unsigned long long* __restrict__ out) {
   auto zero_hist = [&]() {
     uint4* h4 = reinterpret_cast<uint4*>(hist);
     const unsigned int n4 = L.n_hist() * L.hist_words() / 4;
@@ -184,8 +169,7 @@ __device__ __forceinline__ void k1_hoisted_body(
     return run_begin + (hi ^ lane_dep);
   };
   // ---- one run: bits [k, N) fixed; table rows are m - row_off ----
-  auto run_body = [&](unsigned long long r, unsigned int row_off,
-                      unsigned int it0, unsigned int it1) {
+  auto run_body = [&](unsigned long long r, unsigned int row_off) {
     // ---- per-run constants (bits [k, N) fixed) ----
     const unsigned long long xt = r << L.k();
     const int m_run = __popcll(xt);
@@ -223,11 +207,9 @@ __device__ __forceinline__ void k1_hoisted_body(
       if (DOUBLE) gpr[g] += __popcll((xt ^ L.g_jn2(g)) & L.g_nm2(g) & above_k);
     }
     // ---- loop over the subsets of the loop sites ----
-    // (iterations [it0, it1) of the 2^(l - G) outer subsets: a banded
-    // walk's last claims split a run between warps)
     const unsigned int outer = L.loop_mask() & ~L.g_mask();
-    unsigned int jb = it0 ? isd_deposit32(it0, outer) : 0u;
-    for (unsigned int it = it0; it < it1; ++it) {
+    unsigned int jb = 0;
+    for (unsigned int it = 0; it < (nloop >> G); ++it) {
       int e = e_run;
 #pragma unroll
       for (int c = 0; c < NC; ++c)
@@ -467,7 +449,7 @@ __device__ __forceinline__ void k1_hoisted_body(
       // non-pivot run bits, so (slot, lane) -> run is a bijection.  Warp w
       // takes slot w * hi_step (1 in a walk; > 1 when the autotuner times a
       // sample of warps spread over the whole range).
-      run_body(slot_run((t >> 5) * hi_step), 0u, 0u, nloop >> T::gray());
+      run_body(slot_run((t >> 5) * hi_step), 0u);
     }
     __syncthreads();
     flush(0u, L.nbins() / L.stride());
@@ -477,13 +459,7 @@ __device__ __forceinline__ void k1_hoisted_body(
     const unsigned int lane = threadIdx.x & 31;
     const unsigned int base_popc =
         (unsigned int)__popcll(run_begin << L.k());
-    // Work is claimed in units of 1/U of a slot (U blocks of the run's
-    // outer loop iterations), so the last claims of an item split slots
-    // between warps and the warps finish within a fraction of a slot.
-    const unsigned int iters = nloop >> T::gray();
-    const unsigned int U = iters >= 4u ? 4u : iters;
-    const unsigned int ipu = iters / U;
-    __shared__ unsigned int next_unit;  // the item's first unclaimed unit
+    __shared__ unsigned int next_slot;  // the item's first unclaimed slot
     __shared__ unsigned int cur_item;
     // Blocks claim items from a zeroed counter (dynamic scheduling), or
     // without one take every gridDim-th item.
@@ -492,13 +468,13 @@ __device__ __forceinline__ void k1_hoisted_body(
         const unsigned int c =
             claim ? atomicAdd(claim, 1u) : blockIdx.x + k * gridDim.x;
         cur_item = c;
-        // warp w's first chunk is slots [w c0, (w + 1) c0) (no claim, no
-        // wait); the rest is claimed from next_unit
+        // warp w's first chunk is [w c0, (w + 1) c0) (no claim, no wait);
+        // the rest is claimed from next_slot
         if (c < n_items) {
           const unsigned int n = (unsigned int)(items[c].g1 - items[c].g0);
           unsigned int c0 = n / (2u * warps);
           c0 = c0 ? c0 : 1u;
-          next_unit = (n < warps * c0 ? n : warps * c0) * U;
+          next_slot = n < warps * c0 ? n : warps * c0;
         }
       }
       zero_hist();
@@ -511,28 +487,26 @@ __device__ __forceinline__ void k1_hoisted_body(
       long long t_first = 0;
 #endif
       const unsigned int row_off = base_popc + item.q0;
-      // Warps then claim chunks of the item's units (guided: a chunk is
-      // 1/(2W) of what is left, down to one unit); a chunk starts at its
-      // first slot's unrank (the first chunks' slots come precomputed from
-      // the host when the table has them) and steps in popcount order.
+      // Warps then claim chunks of the item's slots (guided: a chunk is
+      // 1/(2W) of what is left, down to one slot), so they finish within
+      // about one slot of each other; each chunk starts with an unrank and
+      // steps in popcount order.
       const unsigned int n_slots = (unsigned int)(item.g1 - item.g0);
-      const unsigned int n_units = n_slots * U;
       unsigned int c0 = n_slots / (2u * warps);
       c0 = c0 ? c0 : 1u;
       for (bool first = true;; first = false) {
-        unsigned int start = 0, cnt = 0;  // in units
+        unsigned int start = 0, cnt = 0;
         if (first) {
-          const unsigned int s0 = warp * c0;
-          cnt = s0 < n_slots ? min(c0, n_slots - s0) * U : 0u;
-          start = s0 * U;
+          start = warp * c0;
+          cnt = start < n_slots ? min(c0, n_slots - start) : 0u;
           if (cnt == 0) continue;
         } else {
           if (lane == 0) {
-            unsigned int old = *(volatile unsigned int*)&next_unit;
-            while (old < n_units) {
-              cnt = (n_units - old) / (2u * warps);
+            unsigned int old = *(volatile unsigned int*)&next_slot;
+            while (old < n_slots) {
+              cnt = (n_slots - old) / (2u * warps);
               if (cnt == 0) cnt = 1;
-              const unsigned int seen = atomicCAS(&next_unit, old, old + cnt);
+              const unsigned int seen = atomicCAS(&next_slot, old, old + cnt);
               if (seen == old) break;
               old = seen;
               cnt = 0;
@@ -543,25 +517,14 @@ __device__ __forceinline__ void k1_hoisted_body(
           if (cnt == 0) break;
           start = __shfl_sync(0xffffffffu, start, 0);
         }
-        unsigned int slot = start / U, o = start % U;
         int q = 0;
-        unsigned long long v;
-        if (first && starts && warps == 32) {
-          const unsigned long long packed = starts[it * 32u + warp];
-          v = packed & 0xffffffffull;
-          q = (int)(packed >> 32);
-        } else {
-          v = isd_unrank((unsigned int)item.g0 + slot, free_bits, &q);
-        }
+        unsigned long long v =
+            isd_unrank((unsigned int)item.g0 + start, free_bits, &q);
 #ifdef ISD_PROBE
         if (t_first == 0) t_first = clock64();
 #endif
-        for (unsigned int left = cnt;;) {
-          const unsigned int take = min(left, U - o);
-          run_body(slot_run(v), row_off, o * ipu, (o + take) * ipu);
-          left -= take;
-          if (!left) break;
-          o = 0;
+        for (unsigned int i = 0; i < cnt; ++i) {
+          run_body(slot_run(v), row_off);
           v = isd_next_slot(v, free_bits, &q);
         }
       }
