@@ -356,6 +356,8 @@ static void band_costs(const isd_lattice* lat, const isd_plan_info& info,
     add(info.pair_words[i]);
     add(info.pair_degree[i]);
   }
+  add(info.pair_mode);
+  add((unsigned long long)(long long)info.pair_both);
   for (int t = 0; t < kCopyBits; ++t) add(info.copy_site[t]);
   add(hp.lane_mask);
   for (int v = 0; v < 5; ++v) add(hp.lane_vec[v]);
@@ -457,7 +459,8 @@ static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
   static const std::vector<double> equal;
   // a flush (~20 K SM cycles) in units of one slot's walk at one wavefront
   // per RED (a slot = 32 lanes x 2^l loop subsets x 32 REDs / 32 lanes)
-  const double flush_units = 20000.0 / (double)(32u << hp->l);
+  const double flush_units =
+      20000.0 / (double)((hp->pair == 3 ? 16u : 32u) << hp->l);
   const int rc = band_items(F, (per_sm < 1 ? 1 : per_sm) * sms,
                             (int)hp->band_span, w ? *w : equal, cost_key,
                             flush_units, &items, &count);
@@ -1473,7 +1476,7 @@ int isd_set_walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
                 (unsigned long long)start, (unsigned long long)end,
                 lat->n_spins);
   if (plan->u != ISD_COPY_BITS || plan->k != plan->u + plan->l ||
-      plan->k > lat->n_spins || plan->pair_mode > 2 ||
+      plan->k > lat->n_spins || plan->pair_mode > 3 ||
       (size_t)plan->hist_words * 4 > 227 * 1024)
     return fail(ISD_EINVAL, "not a hoisted-kernel plan of this lattice");
   const uint64_t len = end - start;

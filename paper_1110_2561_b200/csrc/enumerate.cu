@@ -175,7 +175,7 @@ struct RuntimeTraits {
 // (mode-2 histograms can be too large for two blocks per SM: those kernels
 // may run 1024-thread blocks, which caps them at 64 registers)
 template <int NC, bool DOUBLE, int PAIR>
-__global__ void __launch_bounds__(PAIR == 2 ? kWideThreads : kThreads)
+__global__ void __launch_bounds__(PAIR >= 2 ? kWideThreads : kThreads)
     k1_hoisted(const __grid_constant__ HoistParams P,
                unsigned long long* __restrict__ out) {
   extern __shared__ __align__(16) uint32_t hist[];
@@ -299,7 +299,7 @@ static int launch_hoist_t(const HoistParams& p, unsigned long long* out,
   const size_t smem = (size_t)p.n_hist * p.hist_words * 4;
   const void* fn = (const void*)k1_hoisted<NC, D, PR>;
   int grid = 0;
-  const int threads = hoisted_block(fn, smem, sm_count, PR == 2, &grid);
+  const int threads = hoisted_block(fn, smem, sm_count, PR >= 2, &grid);
   const uint64_t runs = p.run_end - p.run_begin;
   const uint64_t need = (runs + threads - 1) / threads;
   if (need < (uint64_t)grid) grid = (int)(need ? need : 1);
@@ -312,12 +312,12 @@ int launch_hoisted(const HoistParams& p, unsigned long long* out, int sm_count,
                    void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   const bool dbl = p.has_double != 0;
-  switch (p.n_classes * 3 + (p.pair > 2 ? 0 : p.pair)) {
+  switch (p.n_classes * 4 + (p.pair > 3 ? 0 : p.pair)) {
 #define CASE1(NC, PR)                                                  \
-  case NC * 3 + PR:                                                    \
+  case NC * 4 + PR:                                                    \
     return dbl ? launch_hoist_t<NC, true, PR>(p, out, sm_count, st)    \
                : launch_hoist_t<NC, false, PR>(p, out, sm_count, st);
-#define CASE(NC) CASE1(NC, 0) CASE1(NC, 1) CASE1(NC, 2)
+#define CASE(NC) CASE1(NC, 0) CASE1(NC, 1) CASE1(NC, 2) CASE1(NC, 3)
     CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
 #undef CASE
 #undef CASE1

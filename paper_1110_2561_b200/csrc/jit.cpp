@@ -172,7 +172,7 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
   o << "    return 0;\n  }\n";
   o << "};\n";
   o << "extern \"C\" __global__ void __launch_bounds__("
-    << (P.pair == 2 ? kWideThreads : kThreads)
+    << (P.pair >= 2 ? kWideThreads : kThreads)
     << ") k1_jit(unsigned long long run_begin, unsigned long long nruns,\n"
        "    unsigned long long hi_step, unsigned long long lane_mask,\n"
        "    const IsdLanes lanes, const IsdBandItem* items,\n"
@@ -342,7 +342,7 @@ static JitKernel build_kernel(const HoistParams& P) {
     cudaGetLastError();
     return jk;
   }
-  jk.threads = hoisted_block((const void*)jk.kern, smem, 1, P.pair == 2,
+  jk.threads = hoisted_block((const void*)jk.kern, smem, 1, P.pair >= 2,
                              &jk.per_sm);
   jk.ok = true;
   return jk;

@@ -117,11 +117,25 @@ __device__ __forceinline__ unsigned int isd_bin_word(const T& L, unsigned int m,
   return m * L.row_words() + e * L.e_words();
 }
 
+// Index of the multiset {a, b, c} (values 0..R) in (largest, middle,
+// smallest) order: C(hi + 2, 3) + C(mid + 1, 2) + lo (plan.cpp tri_index).
+__device__ __forceinline__ unsigned int isd_tri_index(int a, int b, int c) {
+  const int lo = min(a, min(b, c)), hi = max(a, max(b, c));
+  const int mid = a + b + c - lo - hi;
+  return (unsigned int)(hi * (hi + 1) * (hi + 2) / 6 + ((mid * (mid + 1)) >> 1) +
+                        lo);
+}
+
 // PAIR 1: copy bit 6 is not unrolled; one RED counts the configuration
 // with that site down and its partner with it up, in pattern plane p (= the
 // site's unsatisfied bonds while down), and the flush credits the partner
 // to (m + 1, e + D - 2p).  PAIR 2: copy bit 5 as well (4 configurations per
-// RED, planes p0 (bit 6) x p1 (bit 5)).
+// RED, planes p0 (bit 6) x p1 (bit 5)).  PAIR 3: copy bits 4, 5, 6 are a
+// cluster of three like sites (equal degree, pairwise joined alike, no bond
+// to the unpaired copy sites): one RED counts the cluster's 8
+// configurations, in the plane of the multiset of the three sites'
+// unsatisfied external bonds; the flush credits the subset U flipped up to
+// (m + |U|, e + sum_U (R - 2 n_i) + [|U| = 1 or 2] pair_both).
 //
 // Banded tables (L.band_rows() > 0, mode 2): the table holds band_rows rows
 // of m relative to a work item's base row; the launch walks work items
@@ -217,15 +231,22 @@ __device__ __forceinline__ void k1_hoisted_body(
                     L.mvar(c));
       unsigned int d[7];
       unsigned int pair_off = 0;
+      int pn[3] = {0, 0, 0};  // PAIR 3: the cluster sites' unsatisfied bonds
 #pragma unroll
       for (int q = 0; q < 7; ++q) {
         int nq = npr[q] + __popc((jb ^ L.jn1v(q)) & L.nm1v(q));
         if (DOUBLE) nq += __popc((jb ^ L.jn2v(q)) & L.nm2v(q));
         e += nq;
         d[q] = (unsigned int)((int)L.e_bytes() * (L.degree(q) - 2 * nq));
-        if (PAIR >= 1 && q == 6) pair_off += (unsigned int)nq * L.pair_bytes(0);
-        if (PAIR >= 2 && q == 5) pair_off += (unsigned int)nq * L.pair_bytes(1);
+        if (PAIR == 3) {
+          if (q >= 4) pn[q - 4] = nq;
+        } else {
+          if (PAIR >= 1 && q == 6) pair_off += (unsigned int)nq * L.pair_bytes(0);
+          if (PAIR >= 2 && q == 5) pair_off += (unsigned int)nq * L.pair_bytes(1);
+        }
       }
+      if (PAIR == 3)
+        pair_off = isd_tri_index(pn[0], pn[1], pn[2]) * L.pair_bytes(0);
       unsigned int par = (par_run + __popc(jb & odd_loop)) & 1u;
       // a[c] carries no per-copy constant: addr(c) = a[c] + koff(c), where
       // koff(c) = popc(c) row_bytes + e_bytes * (copy-copy unsatisfied
@@ -236,9 +257,10 @@ __device__ __forceinline__ void k1_hoisted_body(
         const unsigned int a0 = a_run + (unsigned int)__popc(jb) * L.row_bytes() +
                                 (unsigned int)e * L.e_bytes() +
                                 par * (unsigned int)L.plane_bytes() + pair_off;
-        unsigned int a[32];
+        constexpr int kTree = PAIR == 3 ? 16 : 32;
+        unsigned int a[kTree];
 #pragma unroll
-        for (int cl = 0; cl < 32; ++cl) {
+        for (int cl = 0; cl < kTree; ++cl) {
           if (cl == 0) {
             a[0] = a0;
           } else {
@@ -247,6 +269,7 @@ __device__ __forceinline__ void k1_hoisted_body(
           }
           ISD_CHECK_ADDR(a[cl] + L.koff(cl), hbase, hbytes);
           isd_red_shared_inc(a[cl] + L.koff(cl));
+          if (PAIR == 3) continue;
           const unsigned int b1 = a[cl] + d[5];
           if (PAIR <= 1) {
             ISD_CHECK_ADDR(b1 + L.koff(cl + 32), hbase, hbytes);
@@ -271,10 +294,18 @@ __device__ __forceinline__ void k1_hoisted_body(
         if (DOUBLE) ng += __popc((jb ^ L.g_jn2v(g)) & L.g_nm2v(g));
         const int sg = up ? 1 : -1;
         e += sg * (L.g_deg(g) - 2 * ng + L.g_csum(g));
+        bool touched = false;  // PAIR 3: a cluster site's count changed
 #pragma unroll
         for (int q = 0; q < 7; ++q)
           if (L.g_cdelta(g, q) != 0) {
             d[q] -= (unsigned int)(sg * 2 * (int)L.e_bytes() * L.g_cdelta(g, q));
+            if (PAIR == 3) {
+              if (q >= 4) {
+                pn[q - 4] += sg * L.g_cdelta(g, q);
+                touched = true;
+              }
+              continue;
+            }
             if (PAIR >= 1 && q == 6)
               pair_off += (unsigned int)(sg * L.g_cdelta(g, q) *
                                          (int)L.pair_bytes(0));
@@ -282,6 +313,8 @@ __device__ __forceinline__ void k1_hoisted_body(
               pair_off += (unsigned int)(sg * L.g_cdelta(g, q) *
                                          (int)L.pair_bytes(1));
           }
+        if (PAIR == 3 && touched)
+          pair_off = isd_tri_index(pn[0], pn[1], pn[2]) * L.pair_bytes(0);
         if (L.g_odd(g)) par ^= 1u;
         jb ^= L.g_bit(g);
       };
@@ -395,6 +428,55 @@ __device__ __forceinline__ void k1_hoisted_body(
             if (ok2 && e_ok((int)e - ft))
               s32 += hh[w0 - 2 * A - de_words(ft) + y_off];     // Y[r-2, ..]
           }
+          s += s32;
+        }
+        if (s) atomicAdd(out + m * L.stride() + e, s);
+      }
+    } else if constexpr (PAIR == 3) {
+      // A bin (m, e) collects, over the multiset planes {a <= b <= c} and the
+      // subsets U of the cluster flipped up, H[r - |U|, e - de(U), plane],
+      // de(U) = sum_U (R - 2 n_i) + [|U| = 1 or 2] I1.
+      const int R = L.pair_deg(0), I1 = L.pair_both();
+      const int S = (int)L.pair_words(0);
+      const unsigned int rot = (blockIdx.x * 97u) % n_units;
+      for (unsigned int v = threadIdx.x; v < n_units; v += blockDim.x) {
+        const unsigned int u = v + rot < n_units ? v + rot : v + rot - n_units;
+        const unsigned int mr = u / per_row;
+        const unsigned int m = m_lo + mr;
+        const unsigned int e = e0 + (u - mr * per_row) * e_step;
+        const int row = (int)(m - row_off);
+        const int gw = (int)isd_bin_word(L, 0u, e);
+        const bool ok0 = row_ok(row), ok1 = row_ok(row - 1),
+                   ok2 = row_ok(row - 2), ok3 = row_ok(row - 3);
+        unsigned long long s = 0;
+        for (unsigned int h = 0; h < L.n_hist(); ++h) {
+          const unsigned int* hh = hist + h * L.hist_words();
+          unsigned int s32 = 0;  // < 2^32: an item holds < 2^32 configurations
+          int w0 = row * A + gw;  // word of (row, e) in the current plane
+          for (int c = 0; c <= R; ++c)
+            for (int b = 0; b <= c; ++b)
+              for (int a = 0; a <= b; ++a, w0 += S) {
+                const int fa = R - 2 * a, fb = R - 2 * b, fc = R - 2 * c;
+                if (ok0) s32 += hh[w0];
+                if (ok1) {
+                  const int w1 = w0 - A;
+                  if (e_ok((int)e - fa - I1)) s32 += hh[w1 - de_words(fa + I1)];
+                  if (e_ok((int)e - fb - I1)) s32 += hh[w1 - de_words(fb + I1)];
+                  if (e_ok((int)e - fc - I1)) s32 += hh[w1 - de_words(fc + I1)];
+                }
+                if (ok2) {
+                  const int w2 = w0 - 2 * A;
+                  const int g0 = fa + fb + I1, g1 = fa + fc + I1,
+                            g2 = fb + fc + I1;
+                  if (e_ok((int)e - g0)) s32 += hh[w2 - de_words(g0)];
+                  if (e_ok((int)e - g1)) s32 += hh[w2 - de_words(g1)];
+                  if (e_ok((int)e - g2)) s32 += hh[w2 - de_words(g2)];
+                }
+                if (ok3) {
+                  const int g = fa + fb + fc;
+                  if (e_ok((int)e - g)) s32 += hh[w0 - 3 * A - de_words(g)];
+                }
+              }
           s += s32;
         }
         if (s) atomicAdd(out + m * L.stride() + e, s);

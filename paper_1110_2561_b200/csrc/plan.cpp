@@ -283,14 +283,69 @@ static int pair_policy() {
   std::string v;
   if (!knob_str("ISD_PAIR", &v) || v.empty()) return -1;
   const int m = std::atoi(v.c_str());
-  return m < 0 ? 0 : (m > 2 ? 2 : m);
+  return m < 0 ? 0 : (m > 3 ? 3 : m);
+}
+
+// Index of the multiset {a, b, c} among the multisets of three values in
+// 0..R, in (largest, middle, smallest) order: C(hi+2, 3) + C(mid+1, 2) + lo.
+static int tri_index(int a, int b, int c) {
+  const int lo = std::min(a, std::min(b, c)), hi = std::max(a, std::max(b, c));
+  const int mid = a + b + c - lo - hi;
+  return hi * (hi + 1) * (hi + 2) / 6 + mid * (mid + 1) / 2 + lo;
+}
+
+// Pair mode 3 ("cluster of three"): copy bits 4, 5, 6 are three
+// sites that the lattice treats alike — equal degree, each pair of them
+// joined by the same number w (0 or 1) of bonds of one sign, and none of
+// them adjacent to an unpaired copy site.  One RED then counts the 8
+// configurations of the cluster, in the pattern plane of the *multiset* of
+// the three sites' unsatisfied external bonds (R = D - 2w external bonds
+// each: (R+1)(R+2)(R+3)/6 planes instead of (R+1)^3).  *i1 = the change of
+// the cluster's internal unsatisfied bonds when one or two of the three
+// sites flip up (2w(1 - 2 neg); 0 when none or all three do).
+static bool cluster_of_three(const isd_lattice* lat, const isd_plan_info* info,
+                             int* R, int* w, int* i1) {
+  const int u = kCopyBits;
+  const int s[3] = {info->copy_site[u - 3], info->copy_site[u - 2],
+                    info->copy_site[u - 1]};
+  auto bonds = [&](int a, int b, int* neg) {
+    int cnt = 0;
+    const int lo = a < b ? a : b, hi = a < b ? b : a;
+    for (uint32_t q = 0; q < lat->n_classes; ++q) {
+      const isd_bond_class& cl = lat->classes[q];
+      if (hi - lo == (int)cl.shift && ((cl.bond_mask >> lo) & 1)) {
+        ++cnt;
+        *neg += (int)((cl.jneg_mask >> lo) & 1);
+      }
+    }
+    return cnt;
+  };
+  int neg01 = 0, neg02 = 0, neg12 = 0;
+  const int c01 = bonds(s[0], s[1], &neg01), c02 = bonds(s[0], s[2], &neg02),
+            c12 = bonds(s[1], s[2], &neg12);
+  if (c01 != c02 || c01 != c12 || c01 > 1) return false;
+  if (c01 == 1 && (neg01 != neg02 || neg01 != neg12)) return false;
+  const int d0 = site_degree(lat, s[0]);
+  if (site_degree(lat, s[1]) != d0 || site_degree(lat, s[2]) != d0) return false;
+  for (int t = 0; t < u - 3; ++t)
+    for (int i = 0; i < 3; ++i) {
+      int ignored = 0;
+      if (bonds(info->copy_site[t], s[i], &ignored)) return false;
+    }
+  const int ext = d0 - 2 * c01;
+  for (int i = 0; i < 3; ++i)
+    if (info->copy_degree[u - 3 + i] != ext) return false;
+  *R = ext;
+  *w = c01;
+  *i1 = 2 * c01 * (1 - 2 * neg01);
+  return true;
 }
 
 static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
                           std::vector<isd_plan_info>* ranked, bool wide,
                           int walk_bits, bool climb, int band_rows = 0,
                           int band_span = kBandSpan, bool band_domino = false,
-                          uint64_t top = 0) {
+                          uint64_t top = 0, int band_pair = 2) {
   // banded tables: lanes flip single sites (lane m span 5), or with
   // band_domino also a neighbour of the pivot (span 10; rows sized for it)
   const bool single_site = band_rows > 0 && !band_domino;
@@ -310,9 +365,14 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   const int psite[2] = {info->copy_site[kCopyBits - 1],
                         info->copy_site[kCopyBits - 2]};
   const int pdeg[2] = {site_degree(lat, psite[0]), site_degree(lat, psite[1])};
+  const int pboth = both_flip_term(lat, psite[0], psite[1]);
   info->pair_degree[0] = pdeg[0];
   info->pair_degree[1] = pdeg[1];
-  info->pair_both = both_flip_term(lat, psite[0], psite[1]);
+  info->pair_both = pboth;
+  // pair mode 3: copy bits 4-6 as a symmetric cluster (when they are one)
+  int tri_r = 0, tri_w = 0, tri_i1 = 0;
+  const bool tri_ok = cluster_of_three(lat, info, &tri_r, &tri_w, &tri_i1);
+  const int tri_planes = (tri_r + 1) * (tri_r + 2) * (tri_r + 3) / 6;
   // candidate layouts (row_words A, e_words B, plane_words P; paired: plane
   // strides s0 (bit 6) and s1 (bit 5) over the pattern planes)
   struct Cand {
@@ -366,11 +426,21 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
         if (c.total <= (int)(band_rows ? kMaxBandWords : kMaxPair2Words))
           cand.push_back(c);
       }
+      // mode 3: one stride over the multiset planes
+      if (tri_ok)
+        for (int r : {1, 3, 5, 9, 11, 13}) {
+          c.pair = 3;
+          c.s0 = ((c.span + 31) & ~31) + r;
+          c.s1 = 0;
+          c.total = c.span + (tri_planes - 1) * c.s0;
+          if (c.total <= (int)(band_rows ? kMaxBandWords : kMaxPair2Words))
+            cand.push_back(c);
+        }
     }
-    if (band_rows) {  // banded tables exist for mode 2 only
+    if (band_rows) {  // banded tables: mode 2, or mode 3 (band_pair)
       std::vector<Cand> keep;
       for (const Cand& c : cand)
-        if (c.pair == 2) keep.push_back(c);
+        if (c.pair == band_pair) keep.push_back(c);
       cand.swap(keep);
       if (cand.empty()) {
         info->est_per_config = 1e30;
@@ -394,6 +464,18 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
     dst->pair_mode = (uint32_t)c.pair;
     dst->pair_words[0] = (uint32_t)c.s0;
     dst->pair_words[1] = (uint32_t)c.s1;
+    if (c.pair == 3) {
+      // mode 3: external degree R, bonds w between two cluster sites, the
+      // internal-bond term, and the plane count
+      dst->pair_degree[0] = tri_r;
+      dst->pair_degree[1] = tri_w;
+      dst->pair_both = tri_i1;
+      dst->pair_words[1] = (uint32_t)tri_planes;
+    } else {
+      dst->pair_degree[0] = pdeg[0];
+      dst->pair_degree[1] = pdeg[1];
+      dst->pair_both = pboth;
+    }
   };
   // default: first candidate
   apply(info, cand[0]);
@@ -415,6 +497,9 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   const int kClimbSteps = (int)knob_long("ISD_CLIMB_STEPS", 40);
   const size_t kClimbStarts = (size_t)knob_long("ISD_CLIMB_STARTS", 3);
   const uint64_t pbit[2] = {1ull << psite[0], 1ull << psite[1]};
+  const uint64_t tbit[3] = {1ull << info->copy_site[kCopyBits - 3],
+                            1ull << info->copy_site[kCopyBits - 2],
+                            1ull << info->copy_site[kCopyBits - 1]};
   std::vector<double> cost(nc);
   // candidates scored by evaluate (the hill climb narrows this to the
   // start pattern's best layouts)
@@ -444,23 +529,33 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
           if ((c >> t) & 1) cbits |= 1ull << info->copy_site[t];
         // distinct bins of the warp instruction for each pairing mode:
         // unpaired (m, e); mode 1 (m, e, p0) of the configuration with the
-        // bit-6 site down; mode 2 (m, e, p0, p1) with both sites down
-        Bin bins[3][32];
-        int pat[3][32];
-        int nb[3] = {0, 0, 0};
+        // bit-6 site down; mode 2 (m, e, p0, p1) with both sites down; mode
+        // 3 (m, e, multiset plane) with the three cluster sites down
+        Bin bins[4][32];
+        int pat[4][32];
+        int nb[4] = {0, 0, 0, 0};
         for (int lane = 0; lane < 32; ++lane) {
           const uint64_t r = hi ^ lane_dep[lane];
           const uint64_t x = (r << k) | jb | cbits | top;
-          for (int mode = 0; mode < 3; ++mode) {
-            const uint64_t xs = mode == 0 ? x
-                                : mode == 1 ? x & ~pbit[0]
-                                            : x & ~(pbit[0] | pbit[1]);
+          for (int mode = 0; mode < (tri_ok ? 4 : 3); ++mode) {
+            const uint64_t xs =
+                mode == 0   ? x
+                : mode == 1 ? x & ~pbit[0]
+                : mode == 2 ? x & ~(pbit[0] | pbit[1])
+                            : x & ~(tbit[0] | tbit[1] | tbit[2]);
             const int e = energy_of(lat, xs);
             int pt = 0;
-            if (mode >= 1)
+            if (mode == 1 || mode == 2)
               pt = (pdeg[0] - (energy_of(lat, xs | pbit[0]) - e)) / 2;
             if (mode == 2)
               pt += 64 * ((pdeg[1] - (energy_of(lat, xs | pbit[1]) - e)) / 2);
+            if (mode == 3) {
+              int nn[3];
+              for (int i = 0; i < 3; ++i)
+                nn[i] = (tri_r + tri_i1 -
+                         (energy_of(lat, xs | tbit[i]) - e)) / 2;
+              pt = tri_index(nn[0], nn[1], nn[2]);
+            }
             const Bin bn{popc64(xs), e, e & 1};
             bool seen = false;
             for (int t = 0; t < nb[mode] && !seen; ++t)
@@ -487,7 +582,10 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
             else
               wd = bb[t].m * cd.a + ((bb[t].e - bb[t].par) >> 1) * cd.b +
                    bb[t].par * cd.p;
-            wd += (pp[t] & 63) * cd.s0 + (pp[t] >> 6) * cd.s1;
+            if (cd.pair == 3)
+              wd += pp[t] * cd.s0;
+            else
+              wd += (pp[t] & 63) * cd.s0 + (pp[t] >> 6) * cd.s1;
             const int v = ++bank[wd & 31];
             if (v > mx) mx = v;
           }
@@ -766,9 +864,92 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
       std::stable_sort(st.begin(), st.end(),
                        [&](int x, int y) { return deg[x] > deg[y]; });
   };
+  // "tri" sets (pair mode 3): copy bits 4-6 = three like sites of the low kk
+  // bits (equal degree, pairwise joined alike: a triangle of a periodic
+  // axis of length 3, or mutually non-adjacent), copy bits 0-3 = four low
+  // sites adjacent to none of them.  Clusters with the fewest external bonds
+  // first (fewest pattern planes); two choices of the unpaired sites each
+  // (the lowest four; greedily non-adjacent ones).
+  auto bond_count = [&](int a, int c, int* negs) {
+    int cnt = 0;
+    const int lo2 = a < c ? a : c, hi2 = a < c ? c : a;
+    for (uint32_t q = 0; q < lat->n_classes; ++q) {
+      const isd_bond_class& cl = lat->classes[q];
+      if (hi2 - lo2 == (int)cl.shift && ((cl.bond_mask >> lo2) & 1)) {
+        ++cnt;
+        *negs += (int)((cl.jneg_mask >> lo2) & 1);
+      }
+    }
+    return cnt;
+  };
+  auto build_tri_sets = [&](int kk, std::vector<std::vector<int>>* sets,
+                            std::vector<const char*>* names) {
+    struct Tri {
+      int s[3], ext;
+      std::vector<int> avail;
+    };
+    std::vector<Tri> tris;
+    for (int a = 0; a < kk; ++a)
+      for (int c = a + 1; c < kk; ++c)
+        for (int h = c + 1; h < kk; ++h) {
+          if (deg[a] != deg[c] || deg[a] != deg[h]) continue;
+          int n1 = 0, n2 = 0, n3 = 0;
+          const int c1 = bond_count(a, c, &n1), c2 = bond_count(a, h, &n2),
+                    c3 = bond_count(c, h, &n3);
+          if (c1 != c2 || c1 != c3 || c1 > 1) continue;
+          if (c1 == 1 && (n1 != n2 || n1 != n3)) continue;
+          Tri t{{a, c, h}, deg[a] - 2 * c1, {}};
+          for (int i = 0; i < kk; ++i) {
+            if (i == a || i == c || i == h) continue;
+            if (adjacent(i, a) || adjacent(i, c) || adjacent(i, h)) continue;
+            t.avail.push_back(i);
+          }
+          if ((int)t.avail.size() >= u - 3) tris.push_back(t);
+        }
+    std::stable_sort(tris.begin(), tris.end(), [](const Tri& x, const Tri& y) {
+      return x.ext < y.ext;
+    });
+    const size_t n_tri = std::min<size_t>(tris.size(), 2);
+    for (size_t ti = 0; ti < n_tri; ++ti) {
+      const Tri& t = tris[ti];
+      std::vector<int> low(t.avail.begin(), t.avail.begin() + (u - 3));
+      std::vector<int> spread;
+      for (int pass = 0; pass < 2 && (int)spread.size() < u - 3; ++pass)
+        for (int i : t.avail) {
+          if ((int)spread.size() >= u - 3) break;
+          if (std::find(spread.begin(), spread.end(), i) != spread.end())
+            continue;
+          bool free_ok = true;
+          for (int j : spread) free_ok = free_ok && !adjacent(i, j);
+          if (free_ok || pass == 1) spread.push_back(i);
+        }
+      std::sort(spread.begin(), spread.end());
+      for (const std::vector<int>* un : {&low, &spread}) {
+        std::vector<int> st(*un);
+        st.insert(st.end(), t.s, t.s + 3);
+        bool dup = false;
+        for (const auto& have_set : *sets) dup = dup || have_set == st;
+        if (dup) continue;
+        sets->push_back(st);
+        names->push_back("tri");
+      }
+    }
+  };
+  const int policy = pair_policy();
   std::vector<std::vector<int>> sets;
   std::vector<const char*> names;
   build_sets(k, &sets, &names);
+  if (policy < 0 || policy == 3) {
+    std::vector<std::vector<int>> tsets;
+    std::vector<const char*> tnames;
+    build_tri_sets(k, &tsets, &tnames);
+    if (policy == 3 && !tsets.empty()) {  // forced: cluster sets only
+      sets.clear();
+      names.clear();
+    }
+    sets.insert(sets.end(), tsets.begin(), tsets.end());
+    names.insert(names.end(), tnames.begin(), tnames.end());
+  }
   isd_plan_info best_info;
   bool have = false;
   std::vector<isd_plan_info> all;
@@ -789,15 +970,16 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
     bool climb;
     int band_rows, band_span;
     bool band_domino;
+    int band_pair;
     isd_plan_info out;
     std::vector<isd_plan_info> all;
   };
   std::vector<Variant> batch;
   auto try_variant = [&](const isd_plan_info& base, const std::vector<int>& set,
                          bool climb, int band_rows, int band_span = kBandSpan,
-                         bool band_domino = false) {
+                         bool band_domino = false, int band_pair = 2) {
     batch.push_back({base, set, climb, band_rows, band_span, band_domino,
-                     base, {}});
+                     band_pair, base, {}});
   };
   auto run_batch = [&]() {
     auto one = [&](Variant& v) {
@@ -806,7 +988,8 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
       for (int site : v.set) all_even = all_even && !((odd >> site) & 1);
       set_copy_sites(lat, &v.out, v.set.data(), all_even ? 1 : 0);
       choose_layout(lat, &v.out, &v.all, wide, walk_bits, v.climb,
-                    v.band_rows, v.band_span, v.band_domino, top);
+                    v.band_rows, v.band_span, v.band_domino, top,
+                    v.band_pair);
     };
     if (batch.size() == 1) {
       one(batch[0]);
@@ -840,11 +1023,11 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
       if (!force || std::strcmp(force, names[v]) == 0)
         try_variant(*info, sets[v], wide, 0);
   run_batch();
-  // Banded mode 2: when no unbanded mode-2 table fits (c5: 49 planes of all
-  // 37 rows), a power-of-two walk can still run mode 2 with a table of
-  // band_rows rows per work item; a shorter loop (l = 5) keeps the band
-  // narrow.  Requires an aligned power-of-two range (checked at launch).
-  const int policy = pair_policy();
+  // Banded modes 2 and 3: when no unbanded table of that mode fits (c5: 49
+  // planes of all 37 rows), a power-of-two walk can still run it with a
+  // table of band_rows rows per work item; a shorter loop (l = 5) keeps the
+  // band narrow.  Requires an aligned power-of-two range (checked at
+  // launch).
   const bool pow2 = n_configs_hint && !(n_configs_hint & (n_configs_hint - 1));
   // Two band shapes: single-site lanes (lane m span 5) with items of up to
   // kBandSpan + 1 popcount classes and l = 5; or domino lanes (span 10)
@@ -853,23 +1036,30 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   // default: on c5 the few layouts that fit 20 rows score 1.24 wavefronts
   // per RED against 1.11 for the single-site shape (the model then picks
   // single-site lanes anyway).  ISD_BAND_DOMINO=1 adds it, 2 keeps only it.
+  // Banded mode 3 (cluster sets only): the same shapes with one row fewer
+  // (u - 3 unpaired copy bits); its multiset planes are few enough that
+  // the domino shape keeps the default span and loop width.
   const long domino_knob = knob_long("ISD_BAND_DOMINO", 0);
-  if (band_knob != 0 && pow2 && (policy < 0 || policy == 2) &&
-      (band_knob == 1 || (wide && (!have || best_info.pair_mode < 2)))) {
+  for (int bp = 2; bp <= 3; ++bp) {
+    if (!(band_knob != 0 && pow2 && (policy < 0 || policy == bp) &&
+          (band_knob == 1 || (wide && (!have || (int)best_info.pair_mode < bp)))))
+      continue;
     for (int shape = 0; shape < 2; ++shape) {
       const bool domino = shape == 1;
       if ((domino && domino_knob == 0) || (!domino && domino_knob == 2))
         continue;
-      const int span =
-          domino ? 0 : (int)knob_long("ISD_BAND_SPAN", kBandSpan);  // (knob)
+      const int span = (domino && bp == 2)
+                           ? 0
+                           : (int)knob_long("ISD_BAND_SPAN", kBandSpan);
       // (not capped by the grid-stride loop width l: a banded launch deals
       // work items of slots to blocks, so it has no grid-stride tail; on
       // 2^33-configuration shards l = 5 instead of 4 walks 3.5% faster)
       const long lb_knob = knob_long(
           domino ? "ISD_BAND_DOMINO_LOOP_BITS" : "ISD_BAND_LOOP_BITS", -1);
-      const int lb = lb_knob >= 0 ? (int)lb_knob : (domino ? 4 : 5);
+      const int lb =
+          lb_knob >= 0 ? (int)lb_knob : ((domino && bp == 2) ? 4 : 5);
       const int kb = u + lb;
-      const int rows = span + (domino ? 10 : 5) + lb + (u - 2) + 1;
+      const int rows = span + (domino ? 10 : 5) + lb + (u - bp) + 1;
       if (walk_bits - kb - 5 >= 1 && kb <= 32 && rows <= n + 1) {
         isd_plan_info base = *info;
         base.l = (uint32_t)lb;
@@ -878,10 +1068,13 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
                                 ~((1ull << kb) - 1);
         std::vector<std::vector<int>> bsets;
         std::vector<const char*> bnames;
-        build_sets(kb, &bsets, &bnames);
+        if (bp == 2)
+          build_sets(kb, &bsets, &bnames);
+        else
+          build_tri_sets(kb, &bsets, &bnames);
         for (size_t v = 0; v < bsets.size(); ++v)
           if (!force || std::strcmp(force, bnames[v]) == 0)
-            try_variant(base, bsets[v], wide, rows, span, domino);
+            try_variant(base, bsets[v], wide, rows, span, domino, bp);
       }
     }
     run_batch();
@@ -896,14 +1089,15 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
                      [](const isd_plan_info& a, const isd_plan_info& b) {
                        return a.est_per_config < b.est_per_config;
                      });
-    std::vector<isd_plan_info> by_mode[4], mixed;
+    std::vector<isd_plan_info> by_mode[6], mixed;
     for (const isd_plan_info& x : all)
       if (x.est_per_config < 1e29)
-        by_mode[x.band_rows ? 3 : x.pair_mode % 3].push_back(x);
+        by_mode[x.band_rows ? (x.pair_mode == 3 ? 5 : 4) : x.pair_mode % 4]
+            .push_back(x);
     size_t total = 0;
     for (const auto& g : by_mode) total += g.size();
     for (size_t i = 0; mixed.size() < total; ++i)
-      for (int mode : {3, 2, 1, 0})
+      for (int mode : {5, 4, 3, 2, 1, 0})
         if (i < by_mode[mode].size()) mixed.push_back(by_mode[mode][i]);
     if (mixed.size() > 256) mixed.resize(256);
     ranked->assign(mixed.begin(), mixed.end());
@@ -1046,7 +1240,8 @@ void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
   // to the copy sites of c left unsatisfied while it is down (the other
   // paired site down too); flipping it changes unsat_cc by (its copy-copy
   // degree) - 2 u(c)
-  for (uint32_t i = 0; i < info->pair_mode; ++i) {
+  // (mode 3: the cluster sites touch no unpaired copy site, u(c) = 0)
+  for (uint32_t i = 0; i < (info->pair_mode == 3 ? 0u : info->pair_mode); ++i) {
     const int slot = kCopyBits - 1 - (int)i;
     const int bit = 1 << slot;
     const int cc_deg = info->pair_degree[i] - info->copy_degree[slot];
@@ -1117,7 +1312,9 @@ void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
   const uint64_t p0bit = 1ull << info.copy_site[kCopyBits - 1];
   const uint64_t p1bit = 1ull << info.copy_site[kCopyBits - 2];
   const int d0 = (int)info.pair_degree[0], d1 = (int)info.pair_degree[1];
-  const int unpaired = kCopyBits - 2;
+  const bool tri = info.pair_mode == 3;
+  const uint64_t p2bit = 1ull << info.copy_site[kCopyBits - 3];
+  const int unpaired = kCopyBits - (tri ? 3 : 2);
   // segments are independent (each with its own seed): spread them over
   // the host's cores
   auto run_segment = [&](int sg) {
@@ -1138,14 +1335,22 @@ void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
         const uint64_t run = run_begin + (slot ^ dep[lane]);
         const uint64_t x = (run << k) | jb | cb;  // paired sites down
         const int e = energy_of(lat, x);
-        const int p0 = (d0 - (energy_of(lat, x | p0bit) - e)) / 2;
-        const int p1 = (d1 - (energy_of(lat, x | p1bit) - e)) / 2;
         const int eh = info.e_mode ? (e - (e & 1)) / 2 : e;
         const int par = info.e_mode ? (e & 1) : 0;
         words[lane] = (int64_t)popc64(x) * info.row_words +
-                      (int64_t)eh * info.e_words + par * info.plane_words +
-                      (int64_t)p0 * info.pair_words[0] +
-                      (int64_t)p1 * info.pair_words[1];
+                      (int64_t)eh * info.e_words + par * info.plane_words;
+        if (tri) {  // d0 = R, pair_both = the internal-bond term
+          const int base = d0 + info.pair_both;
+          const int n0 = (base - (energy_of(lat, x | p0bit) - e)) / 2;
+          const int n1 = (base - (energy_of(lat, x | p1bit) - e)) / 2;
+          const int n2 = (base - (energy_of(lat, x | p2bit) - e)) / 2;
+          words[lane] += (int64_t)tri_index(n0, n1, n2) * info.pair_words[0];
+        } else {
+          const int p0 = (d0 - (energy_of(lat, x | p0bit) - e)) / 2;
+          const int p1 = (d1 - (energy_of(lat, x | p1bit) - e)) / 2;
+          words[lane] += (int64_t)p0 * info.pair_words[0] +
+                         (int64_t)p1 * info.pair_words[1];
+        }
       }
       std::sort(words, words + 32);
       int per_bank[32] = {0};

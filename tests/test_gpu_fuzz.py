@@ -89,7 +89,7 @@ JIT_SPECS = [s for s in WHOLE if s.num_spins >= 14][:8]
 
 
 @pytest.mark.parametrize("gray", ["1", "2", "3", "4", "5"])
-@pytest.mark.parametrize("pair", ["0", "1", "2"])
+@pytest.mark.parametrize("pair", ["0", "1", "2", "3"])
 @pytest.mark.parametrize("spec", JIT_SPECS, ids=repr)
 def test_jit_gray_walk_matches_c_oracle(spec, pair, gray, monkeypatch):
     # Gray widths 3-5 unroll 2^G copies of the RED tree: on 4 lattices, not
@@ -104,6 +104,12 @@ def test_jit_gray_walk_matches_c_oracle(spec, pair, gray, monkeypatch):
     _native.set_knob("ISD_LOOP_BITS", "5" if gray == "5" else "4")
     _native.set_knob("ISD_GRAY", gray)
     _native.set_knob("ISD_PAIR", pair)
+    if pair == "3":  # (a cluster of three needs more low sites: l = 5)
+        from paper_1110_2561_b200.enumeration import native_lattice
+        _native.set_knob("ISD_LOOP_BITS", "5")
+        _, info = _native.plan(native_lattice(spec), spec.num_configs)
+        if info.pair_mode != 3:
+            pytest.skip("no cluster of three like sites in the low bits")
     got = isd.full_dos(spec)
     assert _native_kernel_path().startswith("k1_hoisted_jit")
     assert np.array_equal(got.counts, oracle_table(spec))
@@ -119,16 +125,57 @@ def _native_kernel_path():
 # lattices through both kernel builds, against the C oracle.
 @pytest.mark.parametrize("jit", ["0", "2"])
 @pytest.mark.parametrize("loop_bits", ["1", "3"])
+@pytest.mark.parametrize("pair", ["2", "3"])
 @pytest.mark.parametrize("spec", JIT_SPECS, ids=repr)
-def test_banded_walk_matches_c_oracle(spec, loop_bits, jit, monkeypatch):
+def test_banded_walk_matches_c_oracle(spec, pair, loop_bits, jit, monkeypatch):
     from paper_1110_2561_b200 import _native
     from paper_1110_2561_b200.enumeration import native_lattice
+    if pair == "3":  # (a cluster of three needs more low sites)
+        loop_bits = str(int(loop_bits) + 3)
+    _native.set_knob("ISD_PAIR", pair)
     _native.set_knob("ISD_BAND", "1")
     _native.set_knob("ISD_BAND_LOOP_BITS", loop_bits)
     _native.set_knob("ISD_JIT", jit)
     _native.set_knob("ISD_LOOP_BITS", loop_bits)
     _, info = _native.plan(native_lattice(spec), spec.num_configs)
-    if not info.band_rows or spec.num_spins - info.k < 6:
+    if (not info.band_rows or spec.num_spins - info.k < 6 or
+            info.pair_mode != int(pair)):
         pytest.skip("no banded plan for this lattice")
     got = isd.full_dos(spec)
     assert np.array_equal(got.counts, oracle_table(spec))
+
+
+# Pair mode 3 (a cluster of three like sites: 8 configurations per RED,
+# multiset pattern planes) on lattices with a periodic axis of length 3 (a
+# triangle of mutually adjacent sites, as c5 has) and on ones where the
+# cluster is three non-adjacent sites: both kernel builds, unbanded and
+# banded tables, against the C oracle.
+TRI_SPECS = [
+    isd.LatticeSpec(3, 3, 2), isd.LatticeSpec(3, 6), isd.LatticeSpec(3, 7, 1, -1),
+    isd.LatticeSpec(6, 3), isd.LatticeSpec(3, 3, 2, 1, boundary="free"),
+    isd.LatticeSpec(5, 4), isd.LatticeSpec(4, 5, boundary="free"),
+    isd.LatticeSpec(3, 6, 1, 1, bond_signs=isd.random_bond_signs(
+        isd.LatticeSpec(3, 6), 77)),
+    isd.LatticeSpec(5, 4, 1, 1, bond_signs=isd.random_bond_signs(
+        isd.LatticeSpec(5, 4), 78)),
+]
+
+
+@pytest.mark.parametrize("jit", ["0", "2"])
+@pytest.mark.parametrize("band", ["0", "1"])
+@pytest.mark.parametrize("loop_bits", ["4", "5"])
+@pytest.mark.parametrize("spec", TRI_SPECS, ids=repr)
+def test_cluster_walk_matches_c_oracle(spec, loop_bits, band, jit):
+    from paper_1110_2561_b200.enumeration import native_lattice
+    _native.set_knob("ISD_PAIR", "3")
+    _native.set_knob("ISD_BAND", band)
+    _native.set_knob("ISD_BAND_LOOP_BITS", loop_bits)
+    _native.set_knob("ISD_LOOP_BITS", loop_bits)
+    _native.set_knob("ISD_JIT", jit)
+    _, info = _native.plan(native_lattice(spec), spec.num_configs)
+    if info.pair_mode != 3 or bool(info.band_rows) != (band == "1") or (
+            info.band_rows and spec.num_spins - info.k < 6):
+        pytest.skip("no such cluster plan for this lattice")
+    got = isd.full_dos(spec)
+    assert np.array_equal(got.counts, oracle_table(spec))
+    assert isd.verify_dos(got).passed

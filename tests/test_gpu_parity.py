@@ -174,12 +174,13 @@ def test_baseline_lattice_full_walk(name):
 
 
 @pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
-@pytest.mark.parametrize("pair", ["0", "1", "2"])
+@pytest.mark.parametrize("pair", ["0", "1", "2", "3"])
 def test_paired_and_unpaired_copies(name, pair, monkeypatch):
     # ISD_PAIR forces the pairing mode: 0 = every copy its own RED, 1 = copy
-    # bit 6 paired (2 configurations per RED), 2 = bits 6 and 5 (4 per RED);
-    # every mode must give the golden table (the autotuner then times only
-    # layouts of that mode)
+    # bit 6 paired (2 configurations per RED), 2 = bits 6 and 5 (4 per RED),
+    # 3 = bits 4-6 as a cluster of three like sites (8 per RED, multiset
+    # planes); every mode must give the golden table (the autotuner then
+    # times only layouts of that mode)
     _native.set_knob("ISD_PAIR", pair)
     spec = workloads()[name].spec
     _, info = _native.plan(__import__(
@@ -187,6 +188,8 @@ def test_paired_and_unpaired_copies(name, pair, monkeypatch):
         fromlist=["native_lattice"]).native_lattice(spec), spec.num_configs)
     if pair == "2" and info.pair_mode != 2:
         pytest.skip("mode-2 histogram does not fit shared memory")
+    if pair == "3" and info.pair_mode != 3:
+        pytest.skip("no cluster of three like sites / table does not fit")
     assert info.pair_mode == int(pair)
     assert np.array_equal(full(spec), _golden_c(name))
 

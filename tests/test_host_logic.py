@@ -205,7 +205,7 @@ def _slot_rank(v, F, cum):
 
 
 def replay_hoisted(spec, loop_bits, pair=None, band_items=None,
-                   domino=False):
+                   domino=False, band_pair=2):
     """numpy replay of k1_hoisted's arithmetic and address layout.
 
     Every index is decomposed exactly as the kernel does (run / loop /
@@ -218,7 +218,8 @@ def replay_hoisted(spec, loop_bits, pair=None, band_items=None,
     if pair is not None:
         knobs["ISD_PAIR"] = pair
     if band_items is not None:  # force a banded mode-2 plan
-        knobs.update(ISD_BAND=1, ISD_PAIR=2, ISD_BAND_LOOP_BITS=loop_bits,
+        knobs.update(ISD_BAND=1, ISD_PAIR=band_pair,
+                     ISD_BAND_LOOP_BITS=loop_bits,
                      ISD_BAND_DOMINO_LOOP_BITS=loop_bits,
                      ISD_BAND_DOMINO=2 if domino else 0)
         if domino:  # lane patterns with domino partners need a "wide" plan
@@ -226,9 +227,12 @@ def replay_hoisted(spec, loop_bits, pair=None, band_items=None,
     with _native.knobs(**knobs):
         lat = native_lattice(spec)
         usable, info = _native.plan(lat, spec.num_configs)
-    if band_items is not None and not info.band_rows:
-        return None  # no banded layout for this lattice
+    if band_items is not None and (not usable or not info.band_rows or
+                                   info.pair_mode != band_pair):
+        return None  # no banded layout (of that mode) for this lattice
     assert usable
+    if pair == 3 and info.pair_mode != 3:
+        return None  # no cluster of three among the low sites
     if pair is not None:
         assert info.pair_mode == pair
     u, k = info.u, info.k
@@ -277,8 +281,27 @@ def replay_hoisted(spec, loop_bits, pair=None, band_items=None,
         word = m * A + e * B
     key = m * stride + e
     mode = info.pair_mode
-    slots = [u - 1, u - 2][:mode]  # paired copy bits: 6, then 5
     down = np.ones(x.shape, dtype=bool)
+    if mode == 3:
+        # cluster of three (copy bits 4-6): one RED per configuration with
+        # all three down, in the plane of the multiset of their counts
+        R, planes = info.pair_degree[0], info.pair_words[1]
+        assert planes == (R + 1) * (R + 2) * (R + 3) // 6
+        ns = []
+        for slot in (u - 3, u - 2, u - 1):
+            bit = 1 << slot
+            down &= (c & bit) == 0
+            # no bond to an unpaired copy site: flipping it changes the
+            # copy-copy term only through the cluster's internal bonds
+            assert info.copy_degree[slot] == R
+            ns.append(n_slot[slot])
+        srt = np.sort(np.stack(ns), axis=0)
+        lo, mid, hi = srt[0], srt[1], srt[2]
+        pat = hi * (hi + 1) * (hi + 2) // 6 + mid * (mid + 1) // 2 + lo
+        assert pat[down].min() >= 0 and pat[down].max() < planes
+        word = word + pat * info.pair_words[0]
+        key = key * planes + pat
+    slots = [u - 1, u - 2][:mode] if mode < 3 else []
     for i, slot in enumerate(slots):
         # paired copies: only configurations with the paired copy bits
         # down issue a RED, into pattern plane n + u(c) per paired site
@@ -333,36 +356,57 @@ def replay_hoisted(spec, loop_bits, pair=None, band_items=None,
             return mm * A + ((ee - p2) // 2) * B + p2 * P
         return mm * A + ee * B
 
-    D = list(info.pair_degree) if mode else [0, 0]
-    S = list(info.pair_words) if mode else [0, 0]
+    srcs = _flush_sources(info)
     table = np.zeros((n + 1, stride), dtype=np.int64)
     for mm in range(n + 1):
         for ee in range(stride):
             if info.e_mode and odd == 0 and (ee & 1) != info.e_parity:
                 continue
             tot = 0
-            for p1 in range(D[1] + 1 if mode == 2 else 1):
-                for p0 in range(D[0] + 1 if mode >= 1 else 1):
-                    plane = p0 * S[0] + p1 * S[1]
-                    f0, f1 = D[0] - 2 * p0, D[1] - 2 * p1
-                    srcs = [(mm, ee)]
-                    if mode >= 1:
-                        srcs.append((mm - 1, ee - f0))
-                    if mode == 2:
-                        srcs += [(mm - 1, ee - f1),
-                                 (mm - 2, ee - f0 - f1 - info.pair_both)]
-                    for sm, se in srcs:
-                        if sm >= 0 and 0 <= se < stride:
-                            tot += hist[bin_word(sm, se) + plane]
+            for plane, dr, de in srcs:
+                sm, se = mm - dr, ee - de
+                if sm >= 0 and 0 <= se < stride:
+                    tot += hist[bin_word(sm, se) + plane]
             table[mm, ee] = tot
     return table
+
+
+def _flush_sources(info):
+    """(plane word offset, rows up, e shift) of every source word of a bin:
+    the kernel's flush rule per pairing mode."""
+    mode = info.pair_mode
+    D, S = list(info.pair_degree), list(info.pair_words)
+    if mode == 0:
+        return [(0, 0, 0)]
+    srcs = []
+    if mode == 3:
+        R, i1, idx = D[0], info.pair_both, 0
+        for cc in range(R + 1):
+            for bb in range(cc + 1):
+                for aa in range(bb + 1):
+                    f = [R - 2 * aa, R - 2 * bb, R - 2 * cc]
+                    for sub in range(8):
+                        j = bin(sub).count("1")
+                        de = sum(f[i] for i in range(3) if (sub >> i) & 1)
+                        de += i1 if j in (1, 2) else 0
+                        srcs.append((idx * S[0], j, de))
+                    idx += 1
+        return srcs
+    for p1 in range(D[1] + 1 if mode == 2 else 1):
+        for p0 in range(D[0] + 1):
+            plane = p0 * S[0] + (p1 * S[1] if mode == 2 else 0)
+            f0, f1 = D[0] - 2 * p0, D[1] - 2 * p1
+            srcs += [(plane, 0, 0), (plane, 1, f0)]
+            if mode == 2:
+                srcs += [(plane, 1, f1), (plane, 2, f0 + f1 + info.pair_both)]
+    return srcs
 
 
 def _banded_table(info, spec, word, key, item, q0, n_items, odd, A, B, P):
     """Per-item tables and the kernel's banded mode-2 flush rule."""
     n, stride = spec.num_spins, info.stride
-    D, S = list(info.pair_degree), list(info.pair_words)
     R = info.band_rows
+    srcs = _flush_sources(info)
 
     def bin_word(rr, ee):
         if info.e_mode:
@@ -381,20 +425,15 @@ def _banded_table(info, spec, word, key, item, q0, n_items, odd, A, B, P):
         hist = np.bincount(w, minlength=int(info.hist_words))
         base = int(q0[sel][0])
         assert (q0[sel] == base).all()
-        for mm in range(base, min(n, base + R + 1) + 1):
+        for mm in range(base, min(n, base + R + info.pair_mode - 1) + 1):
             for ee in range(stride):
                 if info.e_mode and odd == 0 and (ee & 1) != info.e_parity:
                     continue
                 tot = 0
-                for p1 in range(D[1] + 1):
-                    for p0 in range(D[0] + 1):
-                        plane = p0 * S[0] + p1 * S[1]
-                        f0, f1 = D[0] - 2 * p0, D[1] - 2 * p1
-                        for dr, de in ((0, 0), (1, f0), (1, f1),
-                                       (2, f0 + f1 + info.pair_both)):
-                            rr, se = mm - base - dr, ee - de
-                            if 0 <= rr < R and 0 <= se < stride:
-                                tot += hist[bin_word(rr, se) + plane]
+                for plane, dr, de in srcs:
+                    rr, se = mm - base - dr, ee - de
+                    if 0 <= rr < R and 0 <= se < stride:
+                        tot += hist[bin_word(rr, se) + plane]
                 table[mm, ee] += tot
     return table
 
@@ -412,7 +451,7 @@ REPLAY = [
 @pytest.mark.parametrize("kw", REPLAY)
 @pytest.mark.parametrize("seed", [None, 11])
 @pytest.mark.parametrize("loop_bits", [0, 3, 7])
-@pytest.mark.parametrize("pair", [0, 1, 2])
+@pytest.mark.parametrize("pair", [0, 1, 2, 3])
 def test_hoisted_plan_replay_matches_oracle(kw, seed, loop_bits, pair):
     spec, (r, c, d, j, per, signs) = _spec_and_oracle(kw, seed)
     if spec.num_spins < 7 + loop_bits + 1:
@@ -420,6 +459,8 @@ def test_hoisted_plan_replay_matches_oracle(kw, seed, loop_bits, pair):
     lat = port.Lattice(r, c, d, j, per, signs)
     want = port.enumerate_range(lat, 0, 1 << lat.n)
     got = replay_hoisted(spec, loop_bits, pair)
+    if got is None:
+        pytest.skip("no cluster of three like sites in the low bits")
     assert np.array_equal(got, want)
 
 
@@ -432,17 +473,59 @@ BAND_REPLAY = [dict(rows=4, cols=4), dict(rows=2, cols=3, depth=3),
 @pytest.mark.parametrize("seed", [None, 11])
 @pytest.mark.parametrize("n_items", [3, 17])
 @pytest.mark.parametrize("domino", [False, True])
-def test_banded_plan_replay_matches_oracle(kw, seed, n_items, domino):
+@pytest.mark.parametrize("band_pair", [2, 3])
+def test_banded_plan_replay_matches_oracle(kw, seed, n_items, domino,
+                                           band_pair):
     # banded mode 2: per-item tables of band_rows rows, the kernel's slot
     # order and item split replayed, flushed per item, against the oracle;
     # both band shapes (single-site lanes; domino lanes, one popcount class
     # per item)
     spec, (r, c, d, j, per, signs) = _spec_and_oracle(kw, seed)
-    got = replay_hoisted(spec, 1, band_items=n_items, domino=domino)
+    # (a cluster of three plus four sites adjacent to none of them needs
+    # more low sites than the 8 of a one-site loop)
+    got = replay_hoisted(spec, 1 if band_pair == 2 else 4,
+                         band_items=n_items, domino=domino,
+                         band_pair=band_pair)
     if got is None:
         pytest.skip("no banded layout")
     lat = port.Lattice(r, c, d, j, per, signs)
     assert np.array_equal(got, port.enumerate_range(lat, 0, 1 << lat.n))
+
+
+TRI_REPLAY = [dict(rows=3, cols=3, depth=2), dict(rows=3, cols=6),
+              dict(rows=3, cols=6, coupling=-1), dict(rows=6, cols=3)]
+
+
+@pytest.mark.parametrize("kw", TRI_REPLAY)
+@pytest.mark.parametrize("seed", [None, 11])
+@pytest.mark.parametrize("banded", [None, 3, 17])
+def test_cluster_plan_replay_matches_oracle(kw, seed, banded):
+    # pair mode 3 on lattices with a periodic axis of length 3 (a triangle of
+    # mutually adjacent sites, as c5 has): multiset planes, 8 configurations
+    # per RED, unbanded and banded, uniform and +-J bonds
+    spec, (r, c, d, j, per, signs) = _spec_and_oracle(kw, seed)
+    if banded is None:
+        got = replay_hoisted(spec, 5, pair=3)
+    else:
+        got = replay_hoisted(spec, 5, band_items=banded, band_pair=3)
+    if got is None:
+        pytest.skip("no cluster plan")
+    lat = port.Lattice(r, c, d, j, per, signs)
+    assert np.array_equal(got, port.enumerate_range(lat, 0, 1 << lat.n))
+
+
+def test_c5_cluster_plan():
+    # c5 (3x3x4): the banded cluster plan pairs the x-row (9, 10, 11) of
+    # layer 1 — four external bonds each, 35 multiset planes — with four
+    # unpaired copy sites among sites 3..8
+    spec = workloads()["c5"].spec
+    with _native.knobs(ISD_PAIR=3, ISD_BAND=1):
+        usable, info = _native.plan(native_lattice(spec), spec.num_configs)
+    assert usable and info.pair_mode == 3 and info.band_rows > 0
+    assert sorted(info.copy_site[4:]) == [9, 10, 11]
+    assert all(3 <= q <= 8 for q in info.copy_site[:4])
+    assert info.pair_degree[0] == 4 and info.pair_words[1] == 35
+    assert info.pair_both == 2 and info.hist_words * 4 <= 227 * 1024
 
 
 def test_plan_copy_site_variants(monkeypatch):
