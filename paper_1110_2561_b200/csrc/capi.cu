@@ -313,9 +313,18 @@ static int band_items(int F, int n_target, int span,
     }
     const size_t item_bytes = host.size() * sizeof(BandItem);
     BandItem* d = nullptr;
+    // (the caller's stream may be capturing a graph: this upload is not part
+    // of the captured work, so this thread steps out of the capture rules)
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
     cudaError_t e = cudaMalloc(&d, item_bytes);
+    cudaStream_t up = nullptr;  // not the legacy stream: it joins blocking ones
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking);
     if (e == cudaSuccess)
-      e = cudaMemcpy(d, host.data(), item_bytes, cudaMemcpyHostToDevice);
+      e = cudaMemcpyAsync(d, host.data(), item_bytes, cudaMemcpyHostToDevice, up);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(up);
+    if (up) cudaStreamDestroy(up);
+    cudaThreadExchangeStreamCaptureMode(&mode);
     if (e != cudaSuccess) return cuda_fail(e, "band work items");
     it = g_items.emplace(key, std::make_pair(d, (uint32_t)host.size())).first;
   }
@@ -616,8 +625,24 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
   const bool jit_ok = knob_long("ISD_JIT", 1) != 0;
   std::vector<size_t> finalists;
   const size_t n_final = (size_t)knob_long("ISD_TUNE_FINALISTS", kTuneFinalists);
-  for (size_t s2 = 0; s2 < stage1.size() && s2 < n_final; ++s2)
-    finalists.push_back(stage1[s2].second);
+  // (stage 1 ran the ahead-of-time kernel, whose plain loop is issue-bound
+  // in the modes with few REDs per loop subset: it ranks layouts within a
+  // pairing mode, not the modes against each other — the best two of every
+  // mode go through, then the best of the rest)
+  {
+    int per_mode[4] = {0, 0, 0, 0};
+    std::vector<char> taken(stage1.size(), 0);
+    for (size_t s2 = 0; s2 < stage1.size(); ++s2) {
+      const uint32_t pm = cands[stage1[s2].second].pair_mode & 3u;
+      if (n_final >= 4 && per_mode[pm] < 2) {
+        ++per_mode[pm];
+        taken[s2] = 1;
+        finalists.push_back(stage1[s2].second);
+      }
+    }
+    for (size_t s2 = 0; s2 < stage1.size() && finalists.size() < n_final; ++s2)
+      if (!taken[s2]) finalists.push_back(stage1[s2].second);
+  }
   // (banded candidates differ mostly in their lane patterns, which the
   // model ranks only to a few percent: time more of them)
   const size_t n_banded = (size_t)knob_long("ISD_TUNE_BANDED", 8);

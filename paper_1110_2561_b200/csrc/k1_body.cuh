@@ -449,34 +449,49 @@ __device__ __forceinline__ void k1_hoisted_body(
         const bool ok0 = row_ok(row), ok1 = row_ok(row - 1),
                    ok2 = row_ok(row - 2), ok3 = row_ok(row - 3);
         unsigned long long s = 0;
+        // One sweep over the planes per number of sites flipped up, the row
+        // test outside it.  In the specialised build R is a constant and
+        // the sweeps unroll: every plane offset and energy shift is then an
+        // immediate, a term costs its range test, a load and an add.
+        // term(dr, de, word): H[row - dr, e - de, plane at word offset]
         for (unsigned int h = 0; h < L.n_hist(); ++h) {
-          const unsigned int* hh = hist + h * L.hist_words();
+          const unsigned int* hh = hist + h * L.hist_words() + row * A + gw;
           unsigned int s32 = 0;  // < 2^32: an item holds < 2^32 configurations
-          int w0 = row * A + gw;  // word of (row, e) in the current plane
-          for (int c = 0; c <= R; ++c)
-            for (int b = 0; b <= c; ++b)
-              for (int a = 0; a <= b; ++a, w0 += S) {
-                const int fa = R - 2 * a, fb = R - 2 * b, fc = R - 2 * c;
-                if (ok0) s32 += hh[w0];
-                if (ok1) {
-                  const int w1 = w0 - A;
-                  if (e_ok((int)e - fa - I1)) s32 += hh[w1 - de_words(fa + I1)];
-                  if (e_ok((int)e - fb - I1)) s32 += hh[w1 - de_words(fb + I1)];
-                  if (e_ok((int)e - fc - I1)) s32 += hh[w1 - de_words(fc + I1)];
+          auto term = [&](int dr, int de, int pw) {
+            if (e_ok((int)e - de)) s32 += hh[pw - dr * A - de_words(de)];
+          };
+          if (ok0) {
+#pragma unroll
+            for (int p = 0; p < (R + 1) * (R + 2) * (R + 3) / 6; ++p)
+              s32 += hh[p * S];
+          }
+          // the planes {a <= b <= c} with n sites of the cluster flipped up
+          auto sweep = [&](const int n) {
+#pragma unroll
+            for (int c = 0; c <= R; ++c)
+#pragma unroll
+              for (int b = 0; b <= c; ++b)
+#pragma unroll
+                for (int a = 0; a <= b; ++a) {
+                  const int pw =
+                      (c * (c + 1) * (c + 2) / 6 + b * (b + 1) / 2 + a) * S;
+                  const int fa = R - 2 * a, fb = R - 2 * b, fc = R - 2 * c;
+                  if (n == 1) {
+                    term(1, fa + I1, pw);
+                    term(1, fb + I1, pw);
+                    term(1, fc + I1, pw);
+                  } else if (n == 2) {
+                    term(2, fa + fb + I1, pw);
+                    term(2, fa + fc + I1, pw);
+                    term(2, fb + fc + I1, pw);
+                  } else {
+                    term(3, fa + fb + fc, pw);
+                  }
                 }
-                if (ok2) {
-                  const int w2 = w0 - 2 * A;
-                  const int g0 = fa + fb + I1, g1 = fa + fc + I1,
-                            g2 = fb + fc + I1;
-                  if (e_ok((int)e - g0)) s32 += hh[w2 - de_words(g0)];
-                  if (e_ok((int)e - g1)) s32 += hh[w2 - de_words(g1)];
-                  if (e_ok((int)e - g2)) s32 += hh[w2 - de_words(g2)];
-                }
-                if (ok3) {
-                  const int g = fa + fb + fc;
-                  if (e_ok((int)e - g)) s32 += hh[w0 - 3 * A - de_words(g)];
-                }
-              }
+          };
+          if (ok1) sweep(1);
+          if (ok2) sweep(2);
+          if (ok3) sweep(3);
           s += s32;
         }
         if (s) atomicAdd(out + m * L.stride() + e, s);

@@ -52,11 +52,15 @@ def main():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--shards", type=int, default=8)
     ap.add_argument("--index", type=int, default=3)
+    ap.add_argument("--raw", default="", help="also write the probe lines here")
     a = ap.parse_args()
     r = subprocess.run([sys.executable, "-c", CHILD, ROOT, a.config,
                         str(a.shards), str(a.index)], capture_output=True,
                        text=True, timeout=900)
     out = r.stdout
+    if a.raw:
+        with open(a.raw, "w") as fh:
+            fh.write(out)
     if r.returncode:
         print(r.stderr[-2000:])
         return 1
@@ -97,6 +101,10 @@ def main():
     print(f"items {len(recs)}; block cycles mean {st.mean(vals):.0f} "
           f"max/mean {max(vals) / st.mean(vals):.4f} min/mean "
           f"{min(vals) / st.mean(vals):.4f}")
+    ph = {k: st.mean(x[k] for x in recs) for k in ("first", "walk", "flush")}
+    print(f"item phases (SM cycles, mean): start {ph['first']:.0f}, walk ends "
+          f"{ph['walk']:.0f}, flush ends {ph['flush']:.0f} "
+          f"(flush {ph['flush'] - ph['walk']:.0f})")
     print(" q  items  slots/item  cyc/slot   model(wavefronts/RED)")
     for q in sorted(byq):
         w = byq[q]
