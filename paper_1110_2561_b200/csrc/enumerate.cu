@@ -156,6 +156,8 @@ struct RuntimeTraits {
   // no Gray sites in the ahead-of-time build (the stubs are never called)
   __device__ uint32_t band_rows() const { return P.band_rows; }
   __host__ __device__ static constexpr int gray() { return 0; }
+  // (mode 3's external degree is a run-time value here: direct flush)
+  __host__ __device__ static constexpr int tri_r() { return -1; }
   __device__ uint32_t g_mask() const { return 0; }
   __device__ uint32_t g_bit(int) const { return 0; }
   __device__ uint64_t g_nm1(int) const { return 0; }

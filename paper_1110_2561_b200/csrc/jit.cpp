@@ -150,6 +150,10 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
   // Gray sites
   o << "  __host__ __device__ static constexpr int gray() { return " << P.gray
     << "; }\n";
+  // mode 3: the cluster's external degree as a compile-time constant (the
+  // two-stage flush sizes register arrays with it)
+  o << "  __host__ __device__ static constexpr int tri_r() { return "
+    << (P.pair == 3 ? (int)P.pair_deg[0] : -1) << "; }\n";
   c32("g_mask", P.g_mask);
   emit_switch(o, "uint32_t", "g_bit", P.g_bit, kMaxGray, "u");
   emit_switch(o, "uint64_t", "g_nm1", P.g_nm1, kMaxGray, "ull");

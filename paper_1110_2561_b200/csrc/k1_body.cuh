@@ -439,6 +439,95 @@ __device__ __forceinline__ void k1_hoisted_body(
       const int R = L.pair_deg(0), I1 = L.pair_both();
       const int S = (int)L.pair_words(0);
       const unsigned int rot = (blockIdx.x * 97u) % n_units;
+      // Specialised build with at least as many planes as folded sums
+      // (R >= 4): a two-stage flush.  The shift a flipped subset U applies
+      // depends on the plane {a, b, c} only through a symmetric function of
+      // it — the value of the one site up, the sum of the two, the sum of
+      // all three — so stage 1 folds the planes of every table cell into
+      //   G0 = sum_p H_p,   G1[v] = sum_p #{i : p_i = v} H_p,
+      //   G2[t] = sum_p #{i < j : p_i + p_j = t} H_p,
+      //   G3[t] = sum_{p : a + b + c = t} H_p
+      // (6R + 4 sums, written in place over the cell's first planes; a
+      // thread owns its cell, the block syncs once), and stage 2 reads
+      //   G0[r, e] + sum_v G1[v][r-1, e - (R-2v) - I1]
+      //            + sum_t G2[t][r-2, e - (2R-2t) - I1]
+      //            + sum_t G3[t][r-3, e - (3R-2t)]:
+      // planes + 2 (6R + 4) shared accesses per cell instead of 8 x planes.
+      constexpr int kR = T::tri_r();
+      constexpr int kNP = kR < 0 ? 0 : (kR + 1) * (kR + 2) * (kR + 3) / 6;
+      constexpr int kNG = 6 * kR + 4;
+      if constexpr (kR >= 0 && kNG <= kNP) {
+        const unsigned int n_cells = rows * per_row;
+        for (unsigned int h = 0; h < L.n_hist(); ++h) {
+          unsigned int* hh0 = hist + h * L.hist_words();
+          for (unsigned int v = threadIdx.x; v < n_cells; v += blockDim.x) {
+            const unsigned int r = v / per_row;
+            const unsigned int e = e0 + (v - r * per_row) * e_step;
+            unsigned int* hh = hh0 + r * A + isd_bin_word(L, 0u, e);
+            unsigned int g0 = 0, g1[kR + 1] = {}, g2[2 * kR + 1] = {},
+                         g3[3 * kR + 1] = {};
+#pragma unroll
+            for (int c = 0; c <= kR; ++c)
+#pragma unroll
+              for (int b = 0; b <= c; ++b)
+#pragma unroll
+                for (int a = 0; a <= b; ++a) {
+                  const unsigned int x =
+                      hh[(c * (c + 1) * (c + 2) / 6 + b * (b + 1) / 2 + a) * S];
+                  g0 += x;
+                  g1[a] += x;
+                  g1[b] += x;
+                  g1[c] += x;
+                  g2[a + b] += x;
+                  g2[a + c] += x;
+                  g2[b + c] += x;
+                  g3[a + b + c] += x;
+                }
+            hh[0] = g0;
+#pragma unroll
+            for (int i = 0; i <= kR; ++i) hh[(1 + i) * S] = g1[i];
+#pragma unroll
+            for (int i = 0; i <= 2 * kR; ++i) hh[(kR + 2 + i) * S] = g2[i];
+#pragma unroll
+            for (int i = 0; i <= 3 * kR; ++i) hh[(3 * kR + 3 + i) * S] = g3[i];
+          }
+        }
+        __syncthreads();
+        for (unsigned int v = threadIdx.x; v < n_units; v += blockDim.x) {
+          const unsigned int u = v + rot < n_units ? v + rot : v + rot - n_units;
+          const unsigned int mr = u / per_row;
+          const unsigned int m = m_lo + mr;
+          const unsigned int e = e0 + (u - mr * per_row) * e_step;
+          const int row = (int)(m - row_off);
+          const int gw = (int)isd_bin_word(L, 0u, e);
+          unsigned long long s = 0;
+          for (unsigned int h = 0; h < L.n_hist(); ++h) {
+            const unsigned int* hh = hist + h * L.hist_words() + row * A + gw;
+            unsigned int s32 = 0;  // (multiplicities <= 3: still < 2^32)
+            auto term = [&](int dr, int de, int j) {
+              if (e_ok((int)e - de)) s32 += hh[j * S - dr * A - de_words(de)];
+            };
+            if (row_ok(row)) s32 += hh[0];
+            if (row_ok(row - 1)) {
+#pragma unroll
+              for (int i = 0; i <= kR; ++i) term(1, kR - 2 * i + I1, 1 + i);
+            }
+            if (row_ok(row - 2)) {
+#pragma unroll
+              for (int i = 0; i <= 2 * kR; ++i)
+                term(2, 2 * kR - 2 * i + I1, kR + 2 + i);
+            }
+            if (row_ok(row - 3)) {
+#pragma unroll
+              for (int i = 0; i <= 3 * kR; ++i)
+                term(3, 3 * kR - 2 * i, 3 * kR + 3 + i);
+            }
+            s += s32;
+          }
+          if (s) atomicAdd(out + m * L.stride() + e, s);
+        }
+        return;
+      }
       for (unsigned int v = threadIdx.x; v < n_units; v += blockDim.x) {
         const unsigned int u = v + rot < n_units ? v + rot : v + rot - n_units;
         const unsigned int mr = u / per_row;

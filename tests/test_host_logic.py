@@ -674,3 +674,55 @@ def test_band_items_valid_for_every_walk_size():
                     for g0, g1, q0 in items:
                         assert bisect_right(cum, g0) - 1 == q0
                         assert bisect_right(cum, g1 - 1) - 1 <= q0 + 2
+
+
+@pytest.mark.parametrize("R,I1", [(4, 2), (4, 0), (5, -2), (6, 0)])
+def test_cluster_flush_folded_sums_equal_direct_gather(R, I1):
+    # k1_body.cuh, PAIR == 3, specialised build: the two-stage flush folds
+    # the multiset planes of a cell into G0, G1[v], G2[t], G3[t] and gathers
+    # 6R + 4 shifted sums per bin; it must equal the direct gather of 8
+    # shifted words per plane (one per subset of the cluster flipped up)
+    rng = np.random.default_rng(R * 10 + I1)
+    rows, ncol = 9, 40
+    planes = [(a, b, c) for c in range(R + 1) for b in range(c + 1)
+              for a in range(b + 1)]
+    H = {p: rng.integers(0, 1000, size=(rows, ncol)) for p in planes}
+
+    def at(arr, r, e):
+        return int(arr[r, e]) if 0 <= r < rows and 0 <= e < ncol else 0
+
+    direct = np.zeros((rows + 3, ncol), dtype=np.int64)
+    for r in range(rows + 3):
+        for e in range(ncol):
+            s = 0
+            for (a, b, c), h in H.items():
+                f = [R - 2 * a, R - 2 * b, R - 2 * c]
+                s += at(h, r, e)
+                for i in range(3):
+                    s += at(h, r - 1, e - f[i] - I1)
+                for i in range(3):
+                    for j in range(i + 1, 3):
+                        s += at(h, r - 2, e - f[i] - f[j] - I1)
+                s += at(h, r - 3, e - sum(f))
+            direct[r, e] = s
+    g0 = sum(H.values())
+    g1 = [sum(h * p.count(v) for p, h in H.items()) for v in range(R + 1)]
+    g2 = [sum(h * sum(1 for i in range(3) for j in range(i + 1, 3)
+                      if p[i] + p[j] == t) for p, h in H.items())
+          for t in range(2 * R + 1)]
+    g3 = [sum((h for p, h in H.items() if sum(p) == t),
+              np.zeros((rows, ncol), dtype=np.int64))
+          for t in range(3 * R + 1)]
+    folded = np.zeros_like(direct)
+    for r in range(rows + 3):
+        for e in range(ncol):
+            s = at(g0, r, e)
+            s += sum(at(g1[v], r - 1, e - (R - 2 * v) - I1)
+                     for v in range(R + 1))
+            s += sum(at(g2[t], r - 2, e - (2 * R - 2 * t) - I1)
+                     for t in range(2 * R + 1))
+            s += sum(at(g3[t], r - 3, e - (3 * R - 2 * t))
+                     for t in range(3 * R + 1))
+            folded[r, e] = s
+    assert np.array_equal(direct, folded)
+    assert 6 * R + 4 <= len(planes)

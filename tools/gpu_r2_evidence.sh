@@ -14,4 +14,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_jit -s 2 -c 1 -o gpurun_out/${T}_k1_c5 python tools/run_k1.py --config c5 --reps 3 > gpurun_out/${T}_ncu_k1.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_jit -s 2 -c 1 -o gpurun_out/${T}_k1_shard3 python tools/run_k1.py --config c5 --shards 8 --index 3 --reps 3 > gpurun_out/${T}_ncu_k1s.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k2_ -c 1 -o gpurun_out/${T}_k2_c5 python tools/k2_time.py --config c5 --reps 2 > gpurun_out/${T}_ncu_k2.log 2>&1
-tail -2 gpurun_out/${T}_gpu.log gpurun_out/${T}_gpu_dbg.log gpurun_out/${T}_smoke.log gpurun_out/${T}_reference_suite.txt gpurun_out/${T}_bench.err
+for f in gpu gpu_dbg smoke; do tail -n 2 gpurun_out/${T}_$f.log; done; tail -n 2 gpurun_out/${T}_reference_suite.txt gpurun_out/${T}_bench.err
