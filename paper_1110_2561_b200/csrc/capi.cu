@@ -627,14 +627,27 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
   const size_t n_final = (size_t)knob_long("ISD_TUNE_FINALISTS", kTuneFinalists);
   // (stage 1 ran the ahead-of-time kernel, whose plain loop is issue-bound
   // in the modes with few REDs per loop subset: it ranks layouts within a
-  // pairing mode, not the modes against each other — the best two of every
-  // mode go through, then the best of the rest)
+  // pairing mode, not the modes against each other, and its order within
+  // the top mode is only a hint for the Gray-walking kernel — the best four
+  // of the highest mode present go through, two of the next, one of each
+  // other, then the best of the rest)
   {
+    int top_mode = -1, next_mode = -1;
+    for (const auto& s1 : stage1) {
+      const int pm = (int)(cands[s1.second].pair_mode & 3u);
+      if (pm > top_mode) {
+        next_mode = top_mode;
+        top_mode = pm;
+      } else if (pm != top_mode && pm > next_mode) {
+        next_mode = pm;
+      }
+    }
     int per_mode[4] = {0, 0, 0, 0};
     std::vector<char> taken(stage1.size(), 0);
     for (size_t s2 = 0; s2 < stage1.size(); ++s2) {
-      const uint32_t pm = cands[stage1[s2].second].pair_mode & 3u;
-      if (n_final >= 4 && per_mode[pm] < 2) {
+      const int pm = (int)(cands[stage1[s2].second].pair_mode & 3u);
+      const int quota = pm == top_mode ? 4 : (pm == next_mode ? 2 : 1);
+      if (n_final >= 4 && per_mode[pm] < quota) {
         ++per_mode[pm];
         taken[s2] = 1;
         finalists.push_back(stage1[s2].second);

@@ -330,8 +330,33 @@ void jit_prefetch(const std::vector<HoistParams>& ps) {
   for (std::thread& t : pool) t.join();
 }
 
-static JitKernel build_kernel(const HoistParams& P) {
+static JitKernel build_kernel(const HoistParams& P0) {
   JitKernel jk;
+  // A Gray walk over many sites is long straight-line code: where it
+  // spills registers to local memory (c4 at five sites: 80 B of stack),
+  // one site fewer is faster (c4: 1.084 -> 1.065 ms) — step down until the
+  // kernel holds its state in registers.
+  HoistParams P = P0;
+  for (;;) {
+    Cubin probe = get_cubin(P);
+    if (!probe.ok || P.gray <= 2) break;
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kern = nullptr;
+    cudaFuncAttributes attr;
+    std::memset(&attr, 0, sizeof attr);
+    cudaError_t pe = cudaLibraryLoadData(&lib, probe.bytes.data(), nullptr,
+                                         nullptr, 0, nullptr, nullptr, 0);
+    if (pe == cudaSuccess) pe = cudaLibraryGetKernel(&kern, lib, "k1_jit");
+    if (pe == cudaSuccess) pe = cudaFuncGetAttributes(&attr, (const void*)kern);
+    if (lib) cudaLibraryUnload(lib);
+    if (pe != cudaSuccess) {
+      cudaGetLastError();
+      break;
+    }
+    if (attr.localSizeBytes == 0) break;
+    P.gray -= 1;
+    P.g_mask &= ~P.g_bit[P.gray];
+  }
   Cubin cubin = get_cubin(P);
   if (!cubin.ok) {
     jk.why = cubin.why;

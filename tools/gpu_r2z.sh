@@ -1,6 +1,7 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-for c in c3 c4; do for g in 3 4 5; do
-  echo "== $c pair 3 gray $g"
-  ISD_PAIR=3 ISD_GRAY=$g timeout 600 python tools/run_k1.py --config $c --reps 3 2>&1 | tail -2
-done; done
+for c in c4 c3 c5; do
+  echo "== $c default"
+  timeout 600 python tools/run_k1.py --config $c --reps 3 2>&1 | tail -2
+done
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -n 2 2>&1 | tail -2
