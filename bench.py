@@ -218,7 +218,8 @@ def ncu_traffic(config, kernel_ms):
         return None, None
     total, dur_ms = 0.0, None
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}
+    tscale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
+              "ns": 1e-6, "us": 1e-3, "ms": 1.0}
     for ln in open(path):
         parts = ln.split()
         if len(parts) < 3:

@@ -234,17 +234,29 @@ typedef struct isd_plan_info {
    * arrays): one RED counts four configurations; the one with both sites
    * up lands at (m + 2, e + D0 - 2p0 + D1 - 2p1 + pair_both).  Each pairing
    * halves the shared-memory REDs per configuration and multiplies the
-   * histogram by D + 1 planes of base_words words. */
-  uint32_t pair_mode;        /* 0, 1 or 2                               */
-  int32_t  pair_degree[2];   /* degree D of the paired sites (bit 6, 5) */
-  uint32_t pair_words[2];    /* pattern-plane strides (bit 6, bit 5)    */
+   * histogram by D + 1 planes of base_words words.
+   * pair_mode 3: copy bits 4, 5, 6 are a cluster of three like sites
+   * (equal degree, each pair joined by the same w = 0 or 1 bonds of one
+   * sign, no bond to the unpaired copy sites): one RED counts the
+   * cluster's 8 configurations, in the plane of the multiset {a, b, c} of
+   * the three sites' unsatisfied external bonds (each 0..R, R = D - 2w):
+   * word = base word + tri(a, b, c)*pair_words[0], (R+1)(R+2)(R+3)/6
+   * planes; the flush credits the subset U flipped up to
+   * (m + |U|, e + sum_U (R - 2 n_i) + [|U| = 1 or 2] pair_both). */
+  uint32_t pair_mode;        /* 0, 1, 2 or 3                            */
+  int32_t  pair_degree[2];   /* degree D of the paired sites (bit 6, 5);
+                                mode 3: {R, w}                          */
+  uint32_t pair_words[2];    /* pattern-plane strides (bit 6, bit 5);
+                                mode 3: {plane stride, plane count}     */
   int32_t  pair_both;        /* mode 2: e change of flipping both sites
-                                beyond the sum of the single flips      */
+                                beyond the sum of the single flips;
+                                mode 3: 2w(1 - 2 neg), the internal-bond
+                                term of one or two cluster sites up     */
   uint32_t base_words;       /* words of the unpaired layout            */
-  /* Banded tables (band_rows > 0, pairing mode 2 only): the table holds
+  /* Banded tables (band_rows > 0, pairing modes 2 and 3): the table holds
    * band_rows rows of m relative to a base row, and a launch is split into
    * work items of run slots ordered by popcount, each item's runs spanning
-   * at most band_span + 5 + l + u - 2 rows — so a mode-2 table that could
+   * at most band_span + 5 + l + u - pair_mode rows — so a table that could
    * not hold all N + 1 rows fits shared memory.  Lanes are then single
    * run sites (lane_vec[i] == pivot i). */
   uint32_t band_rows;

@@ -330,8 +330,18 @@ void jit_prefetch(const std::vector<HoistParams>& ps) {
   for (std::thread& t : pool) t.join();
 }
 
+// The caller's stream may be capturing a graph: loading (and probing) a
+// module is not part of the captured work, so this thread steps out of the
+// capture rules while it builds a kernel.
+struct RelaxedCapture {
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&mode); }
+  ~RelaxedCapture() { cudaThreadExchangeStreamCaptureMode(&mode); }
+};
+
 static JitKernel build_kernel(const HoistParams& P0) {
   JitKernel jk;
+  RelaxedCapture relaxed;
   // A Gray walk over many sites is long straight-line code: where it
   // spills registers to local memory (c4 at five sites: 80 B of stack),
   // one site fewer is faster (c4: 1.084 -> 1.065 ms) — step down until the
