@@ -255,9 +255,21 @@ static std::map<std::string, std::pair<BandItem*, uint32_t>> g_items;
 
 // Device work items for 2^F slots (uploaded once per device, size and cost
 // curve; `cost_key` identifies w).
-static int band_items(int F, int n_target, int span,
-                      const std::vector<double>& w, const std::string& cost_key,
+// Cost curves of a banded launch per segment of its slot order: rows
+// ascending, rows descending (a mirrored item), and the cheaper of the two
+// (ISD_BAND_MIRROR: 0 = never mirror, 1 = per item, 2 = always).
+struct CostCurves {
+  std::vector<double> fwd, mir, best;
+  std::string name;  // short name of `best` for the items cache
+};
+
+static int band_items(int F, int n_target, int span, const CostCurves* cc,
                       double flush_units, BandItem** ptr, uint32_t* count) {
+  static const std::vector<double> equal;
+  const std::vector<double>& w = cc ? cc->best : equal;
+  const long mirror_mode = knob_long("ISD_BAND_MIRROR", 1);
+  const std::string cost_key =
+      (cc ? cc->name : std::string()) + ":m" + std::to_string(mirror_mode);
   int dev = 0;
   cudaGetDevice(&dev);
   const std::string key = std::to_string(dev) + ":" + std::to_string(F) +
@@ -274,14 +286,66 @@ static int band_items(int F, int n_target, int span,
     // (exact: n_target items, block b walks item b, plus the small items
     // of the extreme classes as second items of blocks 0 and 1; otherwise
     // the target is shrunk until the count is a whole number of waves)
-    bool exact = false;
-    std::vector<BandItem> host =
-        band_work_items(F, n_target, span, w, flush_units, &exact);
-    for (int goal = n_target; !exact && (int)host.size() > n_target && goal > 1;) {
-      goal -= (int)host.size() - n_target;
-      bool ignored = false;
-      host = band_work_items(F, goal < 1 ? 1 : goal, span, w, flush_units,
-                             &ignored);
+    auto cut_items = [&](const std::vector<double>& curve) {
+      bool exact = false;
+      std::vector<BandItem> items =
+          band_work_items(F, n_target, span, curve, flush_units, &exact);
+      for (int goal = n_target;
+           !exact && (int)items.size() > n_target && goal > 1;) {
+        goal -= (int)items.size() - n_target;
+        bool ignored = false;
+        items = band_work_items(F, goal < 1 ? 1 : goal, span, curve,
+                                flush_units, &ignored);
+      }
+      return items;
+    };
+    // an item's table holds its rows in descending order where that costs
+    // fewer wavefronts over the item's slots
+    const bool per_item = mirror_mode == 1 && cc && !cc->mir.empty();
+    auto mark = [&](std::vector<BandItem>* items) {
+      const uint64_t total = 1ull << F, n_seg = cc ? cc->fwd.size() : 1;
+      for (BandItem& x : *items) {
+        x.mirror = mirror_mode == 2 ? 1u : 0u;
+        if (!per_item) continue;
+        double cf = 0, cm = 0;
+        for (uint64_t j = x.g0 * n_seg / total;
+             j < n_seg && total * j / n_seg < x.g1; ++j) {
+          const uint64_t lo = std::max<uint64_t>(x.g0, total * j / n_seg);
+          const uint64_t hi = std::min<uint64_t>(x.g1, total * (j + 1) / n_seg);
+          if (hi > lo) {
+            cf += (double)(hi - lo) * cc->fwd[j];
+            cm += (double)(hi - lo) * cc->mir[j];
+          }
+        }
+        x.mirror = cm < cf ? 1u : 0u;
+      }
+    };
+    std::vector<BandItem> host = cut_items(w);
+    mark(&host);
+    // One order of rows serves a whole item, so an item costs the smaller
+    // of its two sums, not the sum of its segments' smaller costs: re-cut
+    // on the curve the items' own choices make (a segment costs what the
+    // item holding its first slot chose) until the choices settle.
+    for (int round = 0; per_item && round < 4; ++round) {
+      const uint64_t total = 1ull << F, n_seg = cc->fwd.size();
+      std::vector<BandItem> by_start(host);
+      std::sort(by_start.begin(), by_start.end(),
+                [](const BandItem& a, const BandItem& b) { return a.g0 < b.g0; });
+      std::vector<double> eff(n_seg);
+      size_t k = 0;
+      for (uint64_t j = 0; j < n_seg; ++j) {
+        const uint64_t lo = total * j / n_seg;
+        while (k + 1 < by_start.size() && by_start[k].g1 <= lo) ++k;
+        eff[j] = by_start[k].mirror ? cc->mir[j] : cc->fwd[j];
+      }
+      std::vector<BandItem> next = cut_items(eff);
+      mark(&next);
+      bool same = next.size() == host.size();
+      for (size_t i = 0; same && i < next.size(); ++i)
+        same = next[i].g0 == host[i].g0 && next[i].g1 == host[i].g1 &&
+               next[i].mirror == host[i].mirror;
+      host.swap(next);
+      if (same) break;
     }
     // the items must tile [0, 2^F) (listed in any order), each within
     // span + 1 popcount classes of its q0
@@ -333,19 +397,17 @@ static int band_items(int F, int n_target, int span,
   return ISD_OK;
 }
 
-// Cost curve of a banded launch (cached: same lattice, plan, lanes and run
-// base give the same curve).  ISD_BAND_WEIGHTS=0: equal costs.
+// Cost curves of a banded launch (cached: same lattice, plan, lanes and run
+// base give the same curves).  ISD_BAND_WEIGHTS=0: equal costs.
 static std::mutex g_cost_mu;
-// key -> (curve, short name of the curve for the items cache)
-static std::map<std::string, std::pair<std::vector<double>, std::string>>
-    g_cost;
+static std::map<std::string, CostCurves> g_cost;
 
 static void band_costs(const isd_lattice* lat, const isd_plan_info& info,
                        const HoistParams& hp, int run_bits,
-                       const std::vector<double>** w, std::string* key) {
-  *w = nullptr;
-  key->clear();
+                       const CostCurves** out) {
+  *out = nullptr;
   if (knob_long("ISD_BAND_WEIGHTS", 1) == 0) return;
+  const long mirror_mode = knob_long("ISD_BAND_MIRROR", 1);
   // (explicit fields: the structs' padding is not initialised)
   std::string k;
   auto add = [&](unsigned long long v) { k += std::to_string(v) + ","; };
@@ -372,41 +434,51 @@ static void band_costs(const isd_lattice* lat, const isd_plan_info& info,
   for (int v = 0; v < 5; ++v) add(hp.lane_vec[v]);
   add(hp.run_begin);
   add((unsigned long long)run_bits);
+  const std::string mem_key = k + "m" + std::to_string(mirror_mode);
   {
     std::lock_guard<std::mutex> lock(g_cost_mu);
-    auto it = g_cost.find(k);
+    auto it = g_cost.find(mem_key);
     if (it == g_cost.end()) {
-      std::vector<double> c;
+      CostCurves cc;
       // ~16 segments per item of a four-items-per-block launch, 64
       // samples each (c5: ~0.3 s once per process and plan; then from the
-      // disk cache)
+      // disk cache, both curves in one entry)
       const int F = run_bits - 5;
       const int n_seg = (int)std::min<uint64_t>(1ull << F, 16ull * 4 * 148);
       std::string blob;
-      if (cache_get("cost", k, &blob) && !blob.empty() &&
-          blob.size() % sizeof(double) == 0) {
-        c.resize(blob.size() / sizeof(double));
-        std::memcpy(c.data(), blob.data(), blob.size());
+      if (cache_get("cost2", k, &blob) && !blob.empty() &&
+          blob.size() % (2 * sizeof(double)) == 0) {
+        const size_t n = blob.size() / (2 * sizeof(double));
+        cc.fwd.resize(n);
+        cc.mir.resize(n);
+        std::memcpy(cc.fwd.data(), blob.data(), n * sizeof(double));
+        std::memcpy(cc.mir.data(), blob.data() + n * sizeof(double),
+                    n * sizeof(double));
       } else {
         band_slot_cost(lat, info, hp.run_begin, hp.lane_mask, hp.lane_vec,
-                       run_bits, n_seg, 64, &c);
-        cache_put("cost", k,
-                  std::string(reinterpret_cast<const char*>(c.data()),
-                              c.size() * sizeof(double)));
+                       run_bits, n_seg, 64, &cc.fwd, &cc.mir);
+        std::string put(reinterpret_cast<const char*>(cc.fwd.data()),
+                        cc.fwd.size() * sizeof(double));
+        put.append(reinterpret_cast<const char*>(cc.mir.data()),
+                   cc.mir.size() * sizeof(double));
+        cache_put("cost2", k, put);
       }
-      // the items cache names the curve by a hash of its rounded values
+      cc.best.resize(cc.fwd.size());
+      for (size_t i = 0; i < cc.fwd.size(); ++i)
+        cc.best[i] = mirror_mode == 0   ? cc.fwd[i]
+                     : mirror_mode == 2 ? cc.mir[i]
+                                        : std::min(cc.fwd[i], cc.mir[i]);
+      // the items cache names the curves by a hash of their rounded values
       uint64_t h = 1469598103934665603ull;
-      for (double x : c) {
-        h ^= (uint64_t)std::llround(x * 1e4);
-        h *= 1099511628211ull;
-      }
-      std::string name = "w" + std::to_string(h) + ":" +
-                         std::to_string(c.size());
-      it = g_cost.emplace(k, std::make_pair(std::move(c), std::move(name)))
-               .first;
+      for (const std::vector<double>* v : {&cc.best, &cc.fwd, &cc.mir})
+        for (double x : *v) {
+          h ^= (uint64_t)std::llround(x * 1e4);
+          h *= 1099511628211ull;
+        }
+      cc.name = "w" + std::to_string(h) + ":" + std::to_string(cc.best.size());
+      it = g_cost.emplace(mem_key, std::move(cc)).first;
     }
-    *w = &it->second.first;  // (map nodes are stable)
-    *key = it->second.second;
+    *out = &it->second;  // (map nodes are stable)
   }
 }
 
@@ -462,17 +534,15 @@ static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
   dflt = dflt < 1 ? 1 : (dflt > 4 ? 4 : dflt);
   if (weighted && knob_long("ISD_BAND_WEIGHTS", 1) != 0) dflt = 1;
   const int per_sm = (int)knob_long("ISD_BAND_ITEMS_PER_SM", dflt);
-  const std::vector<double>* w = nullptr;
-  std::string cost_key;
-  if (weighted) band_costs(lat, info, *hp, rb, &w, &cost_key);
-  static const std::vector<double> equal;
+  const CostCurves* cc = nullptr;
+  if (weighted) band_costs(lat, info, *hp, rb, &cc);
   // a flush (~20 K SM cycles) in units of one slot's walk at one wavefront
   // per RED (a slot = 32 lanes x 2^l loop subsets x 32 REDs / 32 lanes)
   const double flush_units =
       20000.0 / (double)((hp->pair == 3 ? 16u : 32u) << hp->l);
   const int rc = band_items(F, (per_sm < 1 ? 1 : per_sm) * sms,
-                            (int)hp->band_span, w ? *w : equal, cost_key,
-                            flush_units, &items, &count);
+                            (int)hp->band_span, cc, flush_units, &items,
+                            &count);
   if (rc) return rc;
   hp->band_free_bits = (uint32_t)(rb - 5);
   hp->band_items = (uint64_t)(uintptr_t)items;

@@ -135,10 +135,12 @@ constexpr uint32_t kMaxBandWords = 57600;
 // bits + l loop bits + (u - 2) copy bits + 1).
 constexpr int kBandSpan = 2;
 // one work item of a banded launch: slots [g0, g1) of the popcount-ordered
-// free run bits, whose popcounts are >= q0
+// free run bits, whose popcounts are >= q0; mirror != 0: the item's table
+// holds its rows in descending order (row stride -A: the banks its lanes'
+// words fall on are then those of the mirrored popcount class)
 struct BandItem {
   unsigned long long g0, g1;
-  unsigned int q0, pad;
+  unsigned int q0, mirror;
 };
 
 // ---- host side -----------------------------------------------------------
@@ -172,7 +174,8 @@ std::vector<BandItem> band_work_items(int F, int n_target, int span,
 void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
                     uint64_t run_begin, uint64_t lane_mask,
                     const uint64_t* lane_vec, int run_bits, int n_seg,
-                    int samples, std::vector<double>* cost);
+                    int samples, std::vector<double>* cost,
+                    std::vector<double>* cost_mirror = nullptr);
 void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
                 HoistParams* p);
 

@@ -215,8 +215,11 @@ static std::mutex g_jit_mu;
 static std::map<std::string, std::shared_future<Cubin>> g_cubins;
 static std::map<std::string, std::shared_future<JitKernel>> g_jit;
 
+// (-default-device: the body's generic lambdas carry no execution-space
+// annotation, which NVRTC would otherwise read as host functions)
 static const char* const kNvrtcOpts[] = {"--gpu-architecture=sm_100a",
-                                         "-std=c++17", "-lineinfo"};
+                                         "-std=c++17", "-lineinfo",
+                                         "-default-device"};
 
 // The specialised kernel's source (it holds every lattice constant, so it
 // identifies the kernel).
@@ -243,7 +246,8 @@ static Cubin compile_source(const std::string& src) {
     out.why = "nvrtcCreateProgram failed";
     return out;
   }
-  const int rc = nv.compile(prog, 3, kNvrtcOpts);
+  const int rc = nv.compile(
+      prog, (int)(sizeof kNvrtcOpts / sizeof kNvrtcOpts[0]), kNvrtcOpts);
   if (rc != 0) {
     size_t n = 0;
     nv.log_size(prog, &n);
@@ -343,9 +347,11 @@ static JitKernel build_kernel(const HoistParams& P0) {
   JitKernel jk;
   RelaxedCapture relaxed;
   // A Gray walk over many sites is long straight-line code: where it
-  // spills registers to local memory (c4 at five sites: 80 B of stack),
-  // one site fewer is faster (c4: 1.084 -> 1.065 ms) — step down until the
-  // kernel holds its state in registers.
+  // spills more than a few per-run values to local memory (c4 at five
+  // sites: 80 B of stack; at four: 48 B, and 1.084 -> 1.065 ms), one site
+  // fewer is faster — step down until the stack is small (c5's 24 B are
+  // two values saved once per run of 512 REDs).
+  constexpr size_t kSpillBytesOk = 64;
   HoistParams P = P0;
   for (;;) {
     Cubin probe = get_cubin(P);
@@ -363,7 +369,7 @@ static JitKernel build_kernel(const HoistParams& P0) {
       cudaGetLastError();
       break;
     }
-    if (attr.localSizeBytes == 0) break;
+    if (attr.localSizeBytes <= kSpillBytesOk) break;
     P.gray -= 1;
     P.g_mask &= ~P.g_bit[P.gray];
   }

@@ -32,11 +32,41 @@ __device__ __forceinline__ void isd_red_shared_inc(unsigned int addr) {
 }
 
 // A banded launch's work item (mirrors isd::BandItem): slots [g0, g1) of the
-// free run bits in popcount order, popcounts >= q0.
+// free run bits in popcount order, popcounts >= q0; mirror != 0: the item's
+// table holds its rows in descending order.
 struct IsdBandItem {
   unsigned long long g0, g1;
-  unsigned int q0, pad;
+  unsigned int q0, mirror;
 };
+
+// The layout of a mirrored work item: row r of the band lives at row
+// band_rows - 1 - r, i.e. the row stride is -A from an origin at the last
+// row.  Which banks the 32 lanes' words fall on depends on the sign of the
+// row stride (word = +-m A + e' + plane S): the descending order gives a
+// popcount class the conflicts its mirror image has in ascending order, so
+// the host picks per item whichever its cost model scores lower.
+template <class T>
+struct IsdMirror : T {
+  __device__ __forceinline__ explicit IsdMirror(const T& t) : T(t) {}
+  __device__ __forceinline__ unsigned int row_bytes() const {
+    return 0u - T::row_bytes();
+  }
+  __device__ __forceinline__ unsigned int row_words() const {
+    return 0u - T::row_words();
+  }
+  // copy c's offset holds popc(c) row steps
+  __device__ __forceinline__ unsigned int koff(int c) const {
+    return T::koff(c) - 2u * (unsigned int)__popc((unsigned int)c) * T::row_bytes();
+  }
+};
+template <class T>
+__device__ __forceinline__ unsigned int isd_row_origin(const T&) {
+  return 0u;
+}
+template <class T>
+__device__ __forceinline__ unsigned int isd_row_origin(const IsdMirror<T>& M) {
+  return (M.band_rows() - 1u) * M.T::row_words();
+}
 
 // Binomial coefficients C(n, k), n, k < 24, in constant memory: the unrank
 // below reads them with warp-uniform indices (constant-cache broadcasts).
@@ -183,7 +213,8 @@ __device__ __forceinline__ void k1_hoisted_body(
     return run_begin + (hi ^ lane_dep);
   };
   // ---- one run: bits [k, N) fixed; table rows are m - row_off ----
-  auto run_body = [&](unsigned long long r, unsigned int row_off) {
+  auto run_body = [&](const auto& L, unsigned long long r,
+                      unsigned int row_off) {
     // ---- per-run constants (bits [k, N) fixed) ----
     const unsigned long long xt = r << L.k();
     const int m_run = __popcll(xt);
@@ -205,7 +236,8 @@ __device__ __forceinline__ void k1_hoisted_body(
     // byte address of (m_run, e = 0); the e parity of the configurations
     // is par_run ^ parity(loop bits & odd_mask)
     const unsigned int a_run =
-        hbase + (unsigned int)(m_run - (int)row_off) * L.row_bytes();
+        hbase + 4u * isd_row_origin(L) +
+        (unsigned int)(m_run - (int)row_off) * L.row_bytes();
     const unsigned int par_run =
         (unsigned int)(__popcll(xt & L.odd_mask()) + L.e_parity()) & 1u;
     const unsigned int odd_loop =
@@ -330,7 +362,7 @@ __device__ __forceinline__ void k1_hoisted_body(
 #ifdef ISD_PROBE
   long long probe_t1 = 0;  // (probe build) end of the flush's stage 1
 #endif
-  auto flush = [&](unsigned int row_off, unsigned int rows) {
+  auto flush = [&](const auto& L, unsigned int row_off, unsigned int rows) {
     const unsigned int m_lo = row_off;
     unsigned int m_hi = row_off + rows + (PAIR > 0 ? PAIR : 0);  // exclusive
     if (m_hi > L.nbins() / L.stride()) m_hi = L.nbins() / L.stride();
@@ -349,6 +381,7 @@ __device__ __forceinline__ void k1_hoisted_body(
     auto row_ok = [&](int r) { return r >= 0 && r < (int)rows; };
     auto e_ok = [&](int ee) { return ee >= 0 && ee < (int)L.stride(); };
     const int A = (int)L.row_words();
+    const int org = (int)isd_row_origin(L);  // word of row 0
     if constexpr (PAIR == 2) {
       // Separable two-stage flush.  A bin (m, e) collects, over the pattern
       // planes (p0, p1), its own word and its three partners':
@@ -379,7 +412,7 @@ __device__ __forceinline__ void k1_hoisted_body(
           base[j] = 0;
           if (u < per_row) {
             const unsigned int e = e0 + u * e_step;
-            base[j] = r * A + (int)isd_bin_word(L, 0u, e) + p1 * S1;
+            base[j] = org + r * A + (int)isd_bin_word(L, 0u, e) + p1 * S1;
 #pragma unroll
             for (int p0 = 0; p0 <= D0; ++p0) {
               const int f0 = D0 - 2 * p0;
@@ -420,7 +453,7 @@ __device__ __forceinline__ void k1_hoisted_body(
 #pragma unroll
           for (int p1 = 0; p1 <= D1; ++p1) {
             const int f1 = D1 - 2 * p1, ft = f1 + L.pair_both();
-            const int w0 = row * A + gw + p1 * S1;
+            const int w0 = org + row * A + gw + p1 * S1;
             if (ok0) s32 += hh[w0];                             // X[r, e]
             if (ok1) s32 += hh[w0 - A + y_off];                 // Y[r-1, e]
             if (ok1 && e_ok((int)e - f1))
@@ -463,7 +496,7 @@ __device__ __forceinline__ void k1_hoisted_body(
           for (unsigned int v = threadIdx.x; v < n_cells; v += blockDim.x) {
             const unsigned int r = v / per_row;
             const unsigned int e = e0 + (v - r * per_row) * e_step;
-            unsigned int* hh = hh0 + r * A + isd_bin_word(L, 0u, e);
+            unsigned int* hh = hh0 + org + (int)r * A + (int)isd_bin_word(L, 0u, e);
             unsigned int g0 = 0, g1[kR + 1] = {}, g2[2 * kR + 1] = {},
                          g3[3 * kR + 1] = {};
 #pragma unroll
@@ -502,7 +535,8 @@ __device__ __forceinline__ void k1_hoisted_body(
           const int gw = (int)isd_bin_word(L, 0u, e);
           unsigned long long s = 0;
           for (unsigned int h = 0; h < L.n_hist(); ++h) {
-            const unsigned int* hh = hist + h * L.hist_words() + row * A + gw;
+            const unsigned int* hh =
+                hist + h * L.hist_words() + org + row * A + gw;
             unsigned int s32 = 0;  // (multiplicities <= 3: still < 2^32)
             auto term = [&](int dr, int de, int j) {
               if (e_ok((int)e - de)) s32 += hh[j * S - dr * A - de_words(de)];
@@ -544,7 +578,8 @@ __device__ __forceinline__ void k1_hoisted_body(
         // immediate, a term costs its range test, a load and an add.
         // term(dr, de, word): H[row - dr, e - de, plane at word offset]
         for (unsigned int h = 0; h < L.n_hist(); ++h) {
-          const unsigned int* hh = hist + h * L.hist_words() + row * A + gw;
+          const unsigned int* hh =
+              hist + h * L.hist_words() + org + row * A + gw;
           unsigned int s32 = 0;  // < 2^32: an item holds < 2^32 configurations
           auto term = [&](int dr, int de, int pw) {
             if (e_ok((int)e - de)) s32 += hh[pw - dr * A - de_words(de)];
@@ -597,11 +632,11 @@ __device__ __forceinline__ void k1_hoisted_body(
         for (unsigned int h = 0; h < L.n_hist(); ++h) {
           const unsigned int* hh = hist + h * L.hist_words();
           if constexpr (PAIR == 0) {
-            if (row_ok(row)) s += hh[row * A + gw];
+            if (row_ok(row)) s += hh[org + row * A + gw];
           } else {
             const int D0 = L.pair_deg(0);
             const bool ok0 = row_ok(row), ok1 = row_ok(row - 1);
-            const int w0 = row * A + gw, w1 = w0 - A;
+            const int w0 = org + row * A + gw, w1 = w0 - A;
 #pragma unroll
             for (int p = 0; p <= D0; ++p) {
               const int plane = p * (int)L.pair_words(0);
@@ -635,10 +670,10 @@ __device__ __forceinline__ void k1_hoisted_body(
       // non-pivot run bits, so (slot, lane) -> run is a bijection.  Warp w
       // takes slot w * hi_step (1 in a walk; > 1 when the autotuner times a
       // sample of warps spread over the whole range).
-      run_body(slot_run((t >> 5) * hi_step), 0u);
+      run_body(L, slot_run((t >> 5) * hi_step), 0u);
     }
     __syncthreads();
-    flush(0u, L.nbins() / L.stride());
+    flush(L, 0u, L.nbins() / L.stride());
   } else {
     // ---- banded: work items of slots in popcount order ----
     const unsigned int warps = blockDim.x >> 5;
@@ -709,9 +744,18 @@ __device__ __forceinline__ void k1_hoisted_body(
 #ifdef ISD_PROBE
         if (t_first == 0) t_first = clock64();
 #endif
-        for (unsigned int i = 0; i < cnt; ++i) {
-          run_body(slot_run(v), row_off);
-          v = isd_next_slot(v, free_bits, &q);
+        // (block-uniform: the item's table in ascending or descending rows)
+        if (item.mirror) {
+          const IsdMirror<T> M(L);
+          for (unsigned int i = 0; i < cnt; ++i) {
+            run_body(M, slot_run(v), row_off);
+            v = isd_next_slot(v, free_bits, &q);
+          }
+        } else {
+          for (unsigned int i = 0; i < cnt; ++i) {
+            run_body(L, slot_run(v), row_off);
+            v = isd_next_slot(v, free_bits, &q);
+          }
         }
       }
 #ifdef ISD_PROBE
@@ -721,7 +765,10 @@ __device__ __forceinline__ void k1_hoisted_body(
 #ifdef ISD_PROBE
       const long long t_walk = clock64();
 #endif
-      flush(row_off, L.band_rows());
+      if (item.mirror)
+        flush(IsdMirror<T>(L), row_off, L.band_rows());
+      else
+        flush(L, row_off, L.band_rows());
       __syncthreads();
 #ifdef ISD_PROBE
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(probe_last));

@@ -27,7 +27,8 @@ const char* const kKnownKnobs[] = {
     "ISD_AUTOTUNE",          "ISD_BAND",
     "ISD_BAND_DOMINO",       "ISD_BAND_DOMINO_LOOP_BITS",
     "ISD_BAND_DYNAMIC",      "ISD_BAND_ITEMS_PER_SM",
-    "ISD_BAND_LOOP_BITS",    "ISD_BAND_SPAN",
+    "ISD_BAND_LOOP_BITS",    "ISD_BAND_MIRROR",
+    "ISD_BAND_SPAN",
     "ISD_BAND_WEIGHTS",      "ISD_CLIMB_STARTS",
     "ISD_CLIMB_STEPS",       "ISD_COPY_VARIANT",
     "ISD_GPU_CLIMB",         "ISD_GRAY",

@@ -501,6 +501,17 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
                             1ull << info->copy_site[kCopyBits - 2],
                             1ull << info->copy_site[kCopyBits - 1]};
   std::vector<double> cost(nc);
+  // banded tables: a work item may hold its rows in descending order
+  // (capi.cu band_items, ISD_BAND_MIRROR), chosen per item — in effect per
+  // popcount class of the slot — so a banded layout is scored by the
+  // cheaper order of every class: per-class sums for both orders
+  const bool mirror_ok = band_rows > 0 && knob_long("ISD_BAND_MIRROR", 1) == 1;
+  constexpr int kClasses = 40;
+  std::vector<double> cost_f, cost_m;
+  if (mirror_ok) {
+    cost_f.assign((size_t)nc * kClasses, 0.0);
+    cost_m.assign((size_t)nc * kClasses, 0.0);
+  }
   // candidates scored by evaluate (the hill climb narrows this to the
   // start pattern's best layouts)
   std::vector<char> active(nc, 1);
@@ -508,6 +519,8 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
   isd_plan_info best_alt_ = *info;
   auto evaluate = [&](const Lanes& LN, int warps, bool emit) {
     std::fill(cost.begin(), cost.end(), 0.0);
+    std::fill(cost_f.begin(), cost_f.end(), 0.0);
+    std::fill(cost_m.begin(), cost_m.end(), 0.0);
     const uint64_t lane_mask = LN.mask;
     // the same random stream for every candidate (common random numbers:
     // differences between candidates are then not sampling noise)
@@ -521,6 +534,7 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
     }
     for (int w = 0; w < warps; ++w) {
       const uint64_t hi = deposit(rng_next(&seed), free_mask);
+      const int hq = std::min(popc64(hi), kClasses - 1);
       const uint64_t jb = deposit(rng_next(&seed), info->loop_mask);
       for (int cs = 0; cs < kCopySample; ++cs) {
         uint64_t cbits = 0;
@@ -573,29 +587,43 @@ static void choose_layout(const isd_lattice* lat, isd_plan_info* info,
           const Bin* bb = bins[cd.pair];
           const int* pp = pat[cd.pair];
           const int cnt = nb[cd.pair];
-          int bank[32] = {0};
-          int mx = 0;
+          int bank[32] = {0}, bank_m[32] = {0};
+          int mx = 0, mx_m = 0;
           for (int t = 0; t < cnt; ++t) {
-            int wd;
+            int wd;  // the word without its row term
             if (info->e_mode == 0)
-              wd = bb[t].m * cd.a + bb[t].e * cd.b;
+              wd = bb[t].e * cd.b;
             else
-              wd = bb[t].m * cd.a + ((bb[t].e - bb[t].par) >> 1) * cd.b +
-                   bb[t].par * cd.p;
+              wd = ((bb[t].e - bb[t].par) >> 1) * cd.b + bb[t].par * cd.p;
             if (cd.pair == 3)
               wd += pp[t] * cd.s0;
             else
               wd += (pp[t] & 63) * cd.s0 + (pp[t] >> 6) * cd.s1;
-            const int v = ++bank[wd & 31];
+            const int v = ++bank[(wd + bb[t].m * cd.a) & 31];
             if (v > mx) mx = v;
+            if (mirror_ok) {
+              const int vm = ++bank_m[(wd - bb[t].m * cd.a) & 31];
+              if (vm > mx_m) mx_m = vm;
+            }
           }
           cost[ci] += mx;
+          if (mirror_ok) {
+            cost_f[(size_t)ci * kClasses + hq] += mx;
+            cost_m[(size_t)ci * kClasses + hq] += mx_m;
+          }
         }
       }
     }
     double mask_best = 1e30;
     for (int ci = 0; ci < nc; ++ci) {
       if (!active[ci]) continue;
+      if (mirror_ok) {  // every class in its cheaper order
+        double sum = 0;
+        for (int q = 0; q < kClasses; ++q)
+          sum += std::min(cost_f[(size_t)ci * kClasses + q],
+                          cost_m[(size_t)ci * kClasses + q]);
+        cost[ci] = sum;
+      }
       const double per_red = cost[ci] / (warps * kCopySample);
       const double per_cfg = per_red / (double)(1 << cand[ci].pair);
       mask_best = std::min(mask_best, per_cfg);
@@ -1271,11 +1299,14 @@ namespace isd {
 // are up, hence segments rather than classes.  Fixed seed: the same plan
 // gives the same cuts.  Per segment, `samples` warp REDs of a random slot
 // in it, loop subset and unpaired copy: the 32 lanes' words (m, e, pattern
-// planes) counted per bank.
+// planes) counted per bank.  `cost_mirror` (optional): the same samples with
+// the table's rows in descending order (word = -m A + ...), the layout of
+// a mirrored work item.
 void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
                     uint64_t run_begin, uint64_t lane_mask,
                     const uint64_t* lane_vec, int run_bits, int n_seg,
-                    int samples, std::vector<double>* cost) {
+                    int samples, std::vector<double>* cost,
+                    std::vector<double>* cost_mirror) {
   const int k = (int)info.k;
   const uint64_t free_mask =
       ((run_bits >= 64) ? ~0ull : ((1ull << run_bits) - 1)) & ~lane_mask;
@@ -1284,6 +1315,7 @@ void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
   if (n_seg < 1) n_seg = 1;
   if ((uint64_t)n_seg > total) n_seg = (int)total;
   cost->assign((size_t)n_seg, 1.0);
+  if (cost_mirror) cost_mirror->assign((size_t)n_seg, 1.0);
   // binomials C(n, j), n, j <= F
   std::vector<uint64_t> C((size_t)(F + 1) * (F + 1), 0);
   for (int n = 0; n <= F; ++n)
@@ -1324,7 +1356,7 @@ void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
     uint64_t seed = 0x5851F42D4C957F2Dull ^ (0x9E3779B97F4A7C15ull * (sg + 1));
     const uint64_t g0 = total * (uint64_t)sg / (uint64_t)n_seg;
     const uint64_t g1 = total * (uint64_t)(sg + 1) / (uint64_t)n_seg;
-    double tot = 0;
+    double tot = 0, tot_m = 0;
     for (int s = 0; s < samples; ++s) {
       const uint64_t slot =
           deposit(unrank(g0 + rng_next(&seed) % (g1 - g0)), free_mask);
@@ -1333,39 +1365,49 @@ void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
       const uint64_t c = rng_next(&seed);
       for (int t = 0; t < unpaired; ++t)
         if ((c >> t) & 1) cb |= 1ull << info.copy_site[t];
-      int64_t words[32];
+      // a lane's word, without its row term, and its row
+      int64_t rest[32], row[32];
       for (int lane = 0; lane < 32; ++lane) {
         const uint64_t run = run_begin + (slot ^ dep[lane]);
         const uint64_t x = (run << k) | jb | cb;  // paired sites down
         const int e = energy_of(lat, x);
         const int eh = info.e_mode ? (e - (e & 1)) / 2 : e;
         const int par = info.e_mode ? (e & 1) : 0;
-        words[lane] = (int64_t)popc64(x) * info.row_words +
-                      (int64_t)eh * info.e_words + par * info.plane_words;
+        row[lane] = popc64(x);
+        rest[lane] = (int64_t)eh * info.e_words + par * info.plane_words;
         if (tri) {  // d0 = R, pair_both = the internal-bond term
           const int base = d0 + info.pair_both;
           const int n0 = (base - (energy_of(lat, x | p0bit) - e)) / 2;
           const int n1 = (base - (energy_of(lat, x | p1bit) - e)) / 2;
           const int n2 = (base - (energy_of(lat, x | p2bit) - e)) / 2;
-          words[lane] += (int64_t)tri_index(n0, n1, n2) * info.pair_words[0];
+          rest[lane] += (int64_t)tri_index(n0, n1, n2) * info.pair_words[0];
         } else {
           const int p0 = (d0 - (energy_of(lat, x | p0bit) - e)) / 2;
           const int p1 = (d1 - (energy_of(lat, x | p1bit) - e)) / 2;
-          words[lane] += (int64_t)p0 * info.pair_words[0] +
-                         (int64_t)p1 * info.pair_words[1];
+          rest[lane] += (int64_t)p0 * info.pair_words[0] +
+                        (int64_t)p1 * info.pair_words[1];
         }
       }
-      std::sort(words, words + 32);
-      int per_bank[32] = {0};
-      int worst = 0;
-      for (int i = 0; i < 32; ++i)
-        if (i == 0 || words[i] != words[i - 1]) {
-          const int b = (int)(((words[i] % 32) + 32) % 32);
-          worst = std::max(worst, ++per_bank[b]);
-        }
-      tot += worst;
+      // wavefronts of the RED: the most distinct words on one bank
+      auto wavefronts = [&](int64_t row_words) {
+        int64_t words[32];
+        for (int lane = 0; lane < 32; ++lane)
+          words[lane] = row[lane] * row_words + rest[lane];
+        std::sort(words, words + 32);
+        int per_bank[32] = {0};
+        int worst = 0;
+        for (int i = 0; i < 32; ++i)
+          if (i == 0 || words[i] != words[i - 1]) {
+            const int b = (int)(((words[i] % 32) + 32) % 32);
+            worst = std::max(worst, ++per_bank[b]);
+          }
+        return worst;
+      };
+      tot += wavefronts((int64_t)info.row_words);
+      if (cost_mirror) tot_m += wavefronts(-(int64_t)info.row_words);
     }
     (*cost)[(size_t)sg] = tot / samples;
+    if (cost_mirror) (*cost_mirror)[(size_t)sg] = tot_m / samples;
   };
   unsigned nt = std::thread::hardware_concurrency();
   nt = nt < 1 ? 1 : (nt > 32 ? 32 : nt);

@@ -179,3 +179,28 @@ def test_cluster_walk_matches_c_oracle(spec, loop_bits, band, jit):
     got = isd.full_dos(spec)
     assert np.array_equal(got.counts, oracle_table(spec))
     assert isd.verify_dos(got).passed
+
+
+# Mirrored work items (the item's table holds its rows in descending order,
+# chosen per item by the bank-conflict model): forced off, per item, and on
+# for every item, in banded modes 2 and 3 and both kernel builds.
+@pytest.mark.parametrize("jit", ["0", "2"])
+@pytest.mark.parametrize("mirror", ["0", "1", "2"])
+@pytest.mark.parametrize("pair", ["2", "3"])
+@pytest.mark.parametrize("spec", [TRI_SPECS[0], TRI_SPECS[1], TRI_SPECS[5],
+                                  TRI_SPECS[7]], ids=repr)
+def test_mirrored_band_items_match_c_oracle(spec, pair, mirror, jit):
+    from paper_1110_2561_b200.enumeration import native_lattice
+    lb = "5" if pair == "3" else "3"
+    _native.set_knob("ISD_PAIR", pair)
+    _native.set_knob("ISD_BAND", "1")
+    _native.set_knob("ISD_BAND_LOOP_BITS", lb)
+    _native.set_knob("ISD_LOOP_BITS", lb)
+    _native.set_knob("ISD_BAND_MIRROR", mirror)
+    _native.set_knob("ISD_JIT", jit)
+    _, info = _native.plan(native_lattice(spec), spec.num_configs)
+    if (not info.band_rows or spec.num_spins - info.k < 6 or
+            info.pair_mode != int(pair)):
+        pytest.skip("no banded plan for this lattice")
+    got = isd.full_dos(spec)
+    assert np.array_equal(got.counts, oracle_table(spec))

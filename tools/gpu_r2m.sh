@@ -1,15 +1,15 @@
 #!/bin/bash
+# mirrored band items: parity, then c5 full walk and shards with and without
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-timeout 1500 python bench.py --steps 10 --warmup 3 --extra-configs "" --no-cold --no-cpu-baseline --knob ISD_LOOP_BITS=5 > gpurun_out/r2m_bench_l5.json 2> gpurun_out/r2m_bench_l5.err
-python - <<'PY'
-import json
-for f in ["gpurun_out/r2m_bench_l5.json"]:
-    try:
-        d=json.loads(open(f).read().strip().splitlines()[-1])
-    except Exception as e:
-        print(f, "failed", e); continue
-    em=d["extra"]["shard_emulation"]
-    print(f, d["ms_per_step"], {k:(round(v["max_shard_ms"],4), round(v["tail_ms"],4), round(v["projected_efficiency"],4)) for k,v in em.items() if k.startswith("P")})
-    print("  P8 shards", [round(x,4) for x in em["P8"]["shard_ms"]])
-PY
+timeout 1200 python -m pytest tests/test_gpu_fuzz.py -q -m gpu -x -k "mirrored or banded or cluster" -n 2 2>&1 | tail -2
+for m in 0 1; do
+  echo "== c5 full, mirror $m"
+  ISD_BAND_MIRROR=$m timeout 600 python tools/run_k1.py --config c5 --reps 4 2>&1 | tail -3
+  for i in 0 3 5; do
+  echo "== c5 shard $i/8, mirror $m"
+  ISD_BAND_MIRROR=$m timeout 600 python tools/run_k1.py --config c5 --shards 8 --index $i --reps 4 2>&1 | tail -2 | head -1
+  done
+done
+timeout 600 python tools/shard_probe.py --config c5 --shards 1 --index 0 --raw gpurun_out/r2m_probe_full_raw.txt > gpurun_out/r2m_probe_full.txt 2>&1
+tail -24 gpurun_out/r2m_probe_full.txt
