@@ -273,8 +273,12 @@ int launch_canonical(const CanonParams& p, unsigned long long* out,
 // Threads per block of the hoisted kernel: 512, or 1024 when a histogram
 // this large leaves room for one block per SM (twice the warps to hide the
 // issue latency).  The grid is one wave of resident blocks.
+// A banded launch deals one work item to each block: one block of 1024
+// threads per SM even where two of 512 would fit (c3's 95 KB table: the
+// hardware placed consecutive blocks — the ones holding items — in pairs,
+// leaving half the SMs idle).
 int hoisted_block(const void* fn, size_t smem, int sm_count, bool may_widen,
-                  int* grid) {
+                  int* grid, bool banded) {
   int threads = kThreads;
   int per_sm = 0;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -282,12 +286,14 @@ int hoisted_block(const void* fn, size_t smem, int sm_count, bool may_widen,
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads,
                                                     smem) != cudaSuccess)
     per_sm = 1;
-  if (per_sm <= 1 && may_widen) {
+  if ((per_sm <= 1 || banded) && may_widen) {
     int wide = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wide, fn, kWideThreads,
                                                       smem) == cudaSuccess &&
-        wide >= 1)
+        wide >= 1) {
       threads = kWideThreads;
+      per_sm = 1;
+    }
   }
   if (per_sm < 1) per_sm = 1;
   cudaGetLastError();
@@ -301,7 +307,8 @@ static int launch_hoist_t(const HoistParams& p, unsigned long long* out,
   const size_t smem = (size_t)p.n_hist * p.hist_words * 4;
   const void* fn = (const void*)k1_hoisted<NC, D, PR>;
   int grid = 0;
-  const int threads = hoisted_block(fn, smem, sm_count, PR >= 2, &grid);
+  const int threads =
+      hoisted_block(fn, smem, sm_count, PR >= 2, &grid, p.band_rows > 0);
   const uint64_t runs = p.run_end - p.run_begin;
   const uint64_t need = (runs + threads - 1) / threads;
   if (need < (uint64_t)grid) grid = (int)(need ? need : 1);

@@ -187,7 +187,7 @@ int launch_hoisted(const HoistParams& p, unsigned long long* out,
                    int sm_count, void* stream);
 // threads per block (512 or 1024) and grid for a hoisted kernel
 int hoisted_block(const void* fn, size_t smem, int sm_count, bool may_widen,
-                  int* grid);
+                  int* grid, bool banded = false);
 // NVRTC-specialised k1 (jit.cpp): 1 launched, 0 unavailable (*why), <0 error
 int launch_hoisted_jit(const HoistParams& p, unsigned long long* out,
                        int sm_count, void* stream, std::string* why);

@@ -388,7 +388,7 @@ static JitKernel build_kernel(const HoistParams& P0) {
     return jk;
   }
   jk.threads = hoisted_block((const void*)jk.kern, smem, 1, P.pair >= 2,
-                             &jk.per_sm);
+                             &jk.per_sm, P.band_rows > 0);
   jk.ok = true;
   return jk;
 }

@@ -1069,8 +1069,12 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
   // the domino shape keeps the default span and loop width.
   const long domino_knob = knob_long("ISD_BAND_DOMINO", 0);
   for (int bp = 2; bp <= 3; ++bp) {
+    // (mode 2 banded only where no unbanded table of that mode fits; mode 3
+    // banded always: its short loop walks all its sites in Gray order and
+    // its items may mirror their rows — c4 runs 6% faster banded)
     if (!(band_knob != 0 && pow2 && (policy < 0 || policy == bp) &&
-          (band_knob == 1 || (wide && (!have || (int)best_info.pair_mode < bp)))))
+          (band_knob == 1 ||
+           (wide && (!have || (int)best_info.pair_mode < bp || bp == 3)))))
       continue;
     for (int shape = 0; shape < 2; ++shape) {
       const bool domino = shape == 1;

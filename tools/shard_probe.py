@@ -30,6 +30,9 @@ import paper_1110_2561_b200 as isd
 from paper_1110_2561_b200 import _native
 from paper_1110_2561_b200.enumeration import native_lattice
 from paper_1110_2561_b200.workloads import workloads
+sys.path.insert(0, sys.argv[1] + "/tools")
+import knobs_env
+knobs_env.apply()  # (ISD_* variables of the caller: force a plan family)
 spec = workloads()[sys.argv[2]].spec
 P, idx = int(sys.argv[3]), int(sys.argv[4])
 sh = isd.make_shards(spec, P)[idx]
