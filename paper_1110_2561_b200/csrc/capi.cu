@@ -1095,6 +1095,13 @@ static int prepare_walk(const isd_lattice* lat, uint64_t start, uint64_t end,
   }
   HoistParams hp;
   fill_hoist(lat, &info, &hp);
+  // A small walk is bound by what every block does once — zero its tables,
+  // flush them — not by the walk: one table per block instead of up to 16
+  // privatised copies (c2, 2^25 configurations: 30 -> 22 us; c1 25 -> 15)
+  if (end - start <= (1ull << 26))
+    hp.n_hist = 1;
+  else if (end - start <= (1ull << 28) && hp.n_hist > 2)
+    hp.n_hist = 2;
   const uint64_t runs_per_launch = launch_cap(sms) >> k;
   // large walks use the per-lattice NVRTC specialisation (jit.cpp)
   // (ISD_JIT=0: never; ISD_JIT=2: for every hoisted walk — tests)

@@ -1009,6 +1009,19 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
     batch.push_back({base, set, climb, band_rows, band_span, band_domino,
                      band_pair, base, {}});
   };
+  // What a plan is chosen by.  Large walks: modelled wavefronts per
+  // configuration.  Small walks are bound by what every block does once —
+  // zeroing its table, flushing it, adding its bins to the global table —
+  // which grows with the pattern planes: SM cycles of the walk (32 lanes a
+  // clock on each of ~148 SMs) plus about one cycle per table word (two
+  // resident blocks, ~0.5 cycles per word each; measured on c1/c2: the
+  // unpaired table walks 2^25 configurations in 21 us, the 25-plane mode-2
+  // table in 31 us, and the modes cross near 2^27.5 configurations).
+  auto score = [&](const isd_plan_info& x) {
+    if (wide) return x.est_per_config;
+    return x.est_per_config * (double)n_configs_hint / (32.0 * 148.0) +
+           (double)x.hist_words;
+  };
   auto run_batch = [&]() {
     auto one = [&](Variant& v) {
       v.out = v.base;
@@ -1029,7 +1042,7 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
     for (Variant& v : batch) {
       all.insert(all.end(), v.all.begin(), v.all.end());
       if (v.out.est_per_config >= 1e29) continue;  // no layout of that kind
-      if (!have || v.out.est_per_config < best_info.est_per_config - 1e-9) {
+      if (!have || score(v.out) < score(best_info) - 1e-9) {
         best_info = v.out;
         have = true;
       }
@@ -1112,6 +1125,12 @@ int compile_plan(const isd_lattice* lat, uint64_t n_configs_hint,
     run_batch();
   }
   if (!have) return 1;  // forced variant not available for this lattice
+  // (a small walk: every pairing mode of every set competes on the score —
+  // within a set the layout search keeps only the fewest wavefronts)
+  if (!wide)
+    for (const isd_plan_info& x : all)
+      if (x.est_per_config < 1e29 && score(x) < score(best_info) - 1e-9)
+        best_info = x;
   *info = best_info;
   if (ranked) {
     // best first within each pairing mode, the modes interleaved (the model
