@@ -316,6 +316,17 @@ int isd_band_costs(const isd_lattice* lat, const isd_plan_info* plan,
                    uint64_t run_begin, uint32_t run_bits, uint32_t n_seg,
                    uint32_t samples, double* out);
 
+/* The order of a banded launch's slot bits (no GPU; tools and tests): the
+ * F = run_bits - 5 run bits that are not lane pivots, as pos_out[i] = the
+ * run bit that bit i of a slot's popcount-ordered value lands on.  The run
+ * sites that decide whether an item's table is cheaper with ascending or
+ * descending rows take the most significant slot bits (reorder != 0), so
+ * the slots of a work item agree on them; reorder == 0 gives the natural
+ * order.  Returns F or a negative error. */
+int isd_band_slot_order(const isd_lattice* lat, const isd_plan_info* plan,
+                        uint64_t run_begin, uint32_t run_bits, int reorder,
+                        uint8_t* pos_out);
+
 /* ---- calibration microbenchmarks (K0) -------------------------------- */
 /* which: 0 = POPC, 1 = LOP3, 2 = IADD3, 3 = RED.shared spread,
  *        4 = RED.shared realistic bins, 5 = IMAD, 6 = SHF, 7 = RED.shared

@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "isd_set_cache_dirs", "isd_build_id", "isd_enumerate_multi",
     "isd_thermo_gather_async", "isd_walk_plan", "isd_set_walk_plan",
     "isd_band_costs", "isd_plan_range", "isd_naive_enumerate",
-    "isd_enumerate_thermo",
+    "isd_enumerate_thermo", "isd_band_slot_order",
 )
 
 
@@ -150,6 +150,9 @@ def load():
                                        ctypes.c_uint32, ctypes.c_uint32,
                                        ctypes.c_uint32, vp]
         lib.isd_band_costs.restype = ctypes.c_int
+        lib.isd_band_slot_order.argtypes = [p_lat, ctypes.POINTER(PlanInfo),
+                                            u64, ctypes.c_uint32, i32, vp]
+        lib.isd_band_slot_order.restype = ctypes.c_int
         lib.isd_plan_range.argtypes = [p_lat, u64, u64, ctypes.POINTER(PlanInfo)]
         lib.isd_plan_range.restype = ctypes.c_int
         lib.isd_naive_enumerate.argtypes = [
@@ -491,6 +494,18 @@ def band_costs(lat: Lattice, info: PlanInfo, run_begin: int, run_bits: int,
     n = load().isd_band_costs(ctypes.byref(lat), ctypes.byref(info),
                               run_begin, run_bits, n_seg, samples,
                               out.ctypes.data)
+    if n < 0:
+        check(n)
+    return out[:n]
+
+
+def band_slot_order(lat: Lattice, info: PlanInfo, run_begin: int,
+                    run_bits: int, reorder: bool = True):
+    """Run bit of every slot bit of a banded launch (no GPU; tools/tests)."""
+    out = np.zeros(24, dtype=np.uint8)
+    n = load().isd_band_slot_order(ctypes.byref(lat), ctypes.byref(info),
+                                   run_begin, run_bits, 1 if reorder else 0,
+                                   out.ctypes.data)
     if n < 0:
         check(n)
     return out[:n]

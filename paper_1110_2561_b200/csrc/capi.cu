@@ -251,7 +251,12 @@ static bool band_ok(const isd_plan_info& info, uint64_t start, uint64_t end) {
 }
 
 static std::mutex g_items_mu;
-static std::map<std::string, std::pair<BandItem*, uint32_t>> g_items;
+struct ItemSet {
+  BandItem* dev = nullptr;
+  uint32_t count = 0;
+  std::vector<BandItem> host;
+};
+static std::map<std::string, ItemSet> g_items;
 
 // Device work items for 2^F slots (uploaded once per device, size and cost
 // curve; `cost_key` identifies w).
@@ -261,10 +266,45 @@ static std::map<std::string, std::pair<BandItem*, uint32_t>> g_items;
 struct CostCurves {
   std::vector<double> fwd, mir, best;
   std::string name;  // short name of `best` for the items cache
+  uint8_t pos[24];   // slot bit i -> run bit (band_slot_order)
+  std::string disk_key;  // of the "cost3" cache entry
+  long mirror_mode = 1;
+  int calibrated = 0;    // rounds of measured correction applied
 };
 
+// `best`, and the curves' short name, from fwd / mir
+static void finish_curves(CostCurves* cc) {
+  cc->best.resize(cc->fwd.size());
+  for (size_t i = 0; i < cc->fwd.size(); ++i)
+    cc->best[i] = cc->mirror_mode == 0   ? cc->fwd[i]
+                  : cc->mirror_mode == 2 ? cc->mir[i]
+                                         : std::min(cc->fwd[i], cc->mir[i]);
+  // the items cache names the curves by a hash of their rounded values
+  uint64_t h = 1469598103934665603ull;
+  for (const std::vector<double>* v : {&cc->best, &cc->fwd, &cc->mir})
+    for (double x : *v) {
+      h ^= (uint64_t)std::llround(x * 1e4);
+      h *= 1099511628211ull;
+    }
+  for (uint8_t b : cc->pos) {
+    h ^= b;
+    h *= 1099511628211ull;
+  }
+  cc->name = "w" + std::to_string(h) + ":" + std::to_string(cc->best.size());
+}
+
+static std::string curves_blob(const CostCurves& cc) {
+  std::string put(reinterpret_cast<const char*>(cc.fwd.data()),
+                  cc.fwd.size() * sizeof(double));
+  put.append(reinterpret_cast<const char*>(cc.mir.data()),
+             cc.mir.size() * sizeof(double));
+  put.append(reinterpret_cast<const char*>(cc.pos), sizeof cc.pos);
+  return put;
+}
+
 static int band_items(int F, int n_target, int span, const CostCurves* cc,
-                      double flush_units, BandItem** ptr, uint32_t* count) {
+                      double flush_units, BandItem** ptr, uint32_t* count,
+                      std::vector<BandItem>* host_out = nullptr) {
   static const std::vector<double> equal;
   const std::vector<double>& w = cc ? cc->best : equal;
   const long mirror_mode = knob_long("ISD_BAND_MIRROR", 1);
@@ -390,10 +430,15 @@ static int band_items(int F, int n_target, int span, const CostCurves* cc,
     if (up) cudaStreamDestroy(up);
     cudaThreadExchangeStreamCaptureMode(&mode);
     if (e != cudaSuccess) return cuda_fail(e, "band work items");
-    it = g_items.emplace(key, std::make_pair(d, (uint32_t)host.size())).first;
+    ItemSet set;
+    set.dev = d;
+    set.count = (uint32_t)host.size();
+    set.host = host;
+    it = g_items.emplace(key, std::move(set)).first;
   }
-  *ptr = it->second.first;
-  *count = it->second.second;
+  *ptr = it->second.dev;
+  *count = it->second.count;
+  if (host_out) *host_out = it->second.host;
   return ISD_OK;
 }
 
@@ -434,6 +479,10 @@ static void band_costs(const isd_lattice* lat, const isd_plan_info& info,
   for (int v = 0; v < 5; ++v) add(hp.lane_vec[v]);
   add(hp.run_begin);
   add((unsigned long long)run_bits);
+  // slots ordered by the run sites that decide the items' row order
+  // (ISD_BAND_ORDER=0: natural order); only with per-item mirroring
+  const bool reorder = mirror_mode == 1 && knob_long("ISD_BAND_ORDER", 1) != 0;
+  k += reorder ? "o1," : "o0,";
   const std::string mem_key = k + "m" + std::to_string(mirror_mode);
   {
     std::lock_guard<std::mutex> lock(g_cost_mu);
@@ -446,36 +495,27 @@ static void band_costs(const isd_lattice* lat, const isd_plan_info& info,
       const int F = run_bits - 5;
       const int n_seg = (int)std::min<uint64_t>(1ull << F, 16ull * 4 * 148);
       std::string blob;
-      if (cache_get("cost2", k, &blob) && !blob.empty() &&
-          blob.size() % (2 * sizeof(double)) == 0) {
-        const size_t n = blob.size() / (2 * sizeof(double));
+      std::memset(cc.pos, 0, sizeof cc.pos);
+      if (cache_get("cost3", k, &blob) && blob.size() > sizeof cc.pos &&
+          (blob.size() - sizeof cc.pos) % (2 * sizeof(double)) == 0) {
+        const size_t n = (blob.size() - sizeof cc.pos) / (2 * sizeof(double));
         cc.fwd.resize(n);
         cc.mir.resize(n);
         std::memcpy(cc.fwd.data(), blob.data(), n * sizeof(double));
         std::memcpy(cc.mir.data(), blob.data() + n * sizeof(double),
                     n * sizeof(double));
+        std::memcpy(cc.pos, blob.data() + 2 * n * sizeof(double),
+                    sizeof cc.pos);
       } else {
+        band_slot_order(lat, info, hp.run_begin, hp.lane_mask, hp.lane_vec,
+                        run_bits, reorder, cc.pos);
         band_slot_cost(lat, info, hp.run_begin, hp.lane_mask, hp.lane_vec,
-                       run_bits, n_seg, 64, &cc.fwd, &cc.mir);
-        std::string put(reinterpret_cast<const char*>(cc.fwd.data()),
-                        cc.fwd.size() * sizeof(double));
-        put.append(reinterpret_cast<const char*>(cc.mir.data()),
-                   cc.mir.size() * sizeof(double));
-        cache_put("cost2", k, put);
+                       run_bits, n_seg, 64, &cc.fwd, &cc.mir, cc.pos);
+        cache_put("cost3", k, curves_blob(cc));
       }
-      cc.best.resize(cc.fwd.size());
-      for (size_t i = 0; i < cc.fwd.size(); ++i)
-        cc.best[i] = mirror_mode == 0   ? cc.fwd[i]
-                     : mirror_mode == 2 ? cc.mir[i]
-                                        : std::min(cc.fwd[i], cc.mir[i]);
-      // the items cache names the curves by a hash of their rounded values
-      uint64_t h = 1469598103934665603ull;
-      for (const std::vector<double>* v : {&cc.best, &cc.fwd, &cc.mir})
-        for (double x : *v) {
-          h ^= (uint64_t)std::llround(x * 1e4);
-          h *= 1099511628211ull;
-        }
-      cc.name = "w" + std::to_string(h) + ":" + std::to_string(cc.best.size());
+      cc.disk_key = k;
+      cc.mirror_mode = mirror_mode;
+      finish_curves(&cc);
       it = g_cost.emplace(mem_key, std::move(cc)).first;
     }
     *out = &it->second;  // (map nodes are stable)
@@ -512,11 +552,15 @@ static int claim_counter(uint32_t** out) {
 // Fill the banded-launch fields of hp for its run range [run_begin, run_end)
 // (a dynamic-claim counter must be zeroed on the launch's stream first).
 static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
-                           HoistParams* hp, int sms, bool weighted = true) {
+                           HoistParams* hp, int sms, bool weighted = true,
+                           const CostCurves** cc_out = nullptr,
+                           std::vector<BandItem>* host_out = nullptr) {
   hp->band_free_bits = 0;
   hp->band_items = 0;
   hp->band_n_items = 0;
   hp->band_claim = 0;
+  hp->band_clk = 0;
+  if (cc_out) *cc_out = nullptr;
   if (!hp->band_rows) return ISD_OK;
   const int rb = log2_exact(hp->run_end - hp->run_begin);
   if (rb < 6) return fail(ISD_EINVAL, "banded launch needs 2^r runs");
@@ -542,9 +586,20 @@ static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
       20000.0 / (double)((hp->pair == 3 ? 16u : 32u) << hp->l);
   const int rc = band_items(F, (per_sm < 1 ? 1 : per_sm) * sms,
                             (int)hp->band_span, cc, flush_units, &items,
-                            &count);
+                            &count, host_out);
   if (rc) return rc;
+  if (cc_out) *cc_out = cc;
   hp->band_free_bits = (uint32_t)(rb - 5);
+  // the slot map: the cost model's order, else the natural one
+  {
+    uint8_t natural[24];
+    const uint8_t* pos = cc ? cc->pos : natural;
+    if (!cc)
+      band_slot_order(lat, info, hp->run_begin, hp->lane_mask, hp->lane_vec,
+                      rb, false, natural);
+    if (band_slot_fields(pos, rb - 5, hp->slot_mask, hp->slot_rot) < 0)
+      return fail(ISD_EINVAL, "banded launch: slot map needs too many fields");
+  }
   hp->band_items = (uint64_t)(uintptr_t)items;
   hp->band_n_items = count;
   // ISD_BAND_DYNAMIC=1: blocks claim items from a counter (measured no
@@ -556,6 +611,106 @@ static int set_band_launch(const isd_lattice* lat, const isd_plan_info& info,
     hp->band_claim = (uint64_t)(uintptr_t)slot;
   }
   return ISD_OK;
+}
+
+// Correct a banded launch's cost curves by measurement.  The model scores a
+// slot by its expected wavefronts; what a block spends on an item also
+// holds issue-bound stretches and the flush, and the model's estimate of
+// the mirrored order is a few percent off in the upper popcount classes
+// (c5: block totals within -1.5%/+2.5% of their mean).  One launch over the
+// walk's own range writes every item's SM cycles (k1_body.cuh item_clk);
+// each segment's costs are scaled by measured / modelled of the item that
+// held it, the items are cut again, and a second round settles what the
+// moved boundaries changed.  The corrected curves replace the model's in
+// memory and in the disk cache (the plan is tuned once per cache, so they
+// are what later processes cut their items from).
+static void calibrate_items(const isd_lattice* lat, const isd_plan_info& info,
+                            HoistParams hp, int sms, unsigned long long* scratch,
+                            cudaStream_t st, bool jit_ok) {
+  if (!hp.band_rows || knob_long("ISD_BAND_CALIBRATE", 1) == 0 ||
+      knob_long("ISD_BAND_WEIGHTS", 1) == 0 ||
+      knob_long("ISD_BAND_DYNAMIC", 0) != 0)
+    return;
+  NvtxRange nvtx("isd:calibrate items");
+  for (int round = 0; round < 2; ++round) {
+    const CostCurves* cc = nullptr;
+    std::vector<BandItem> items;
+    if (set_band_launch(lat, info, &hp, sms, true, &cc, &items) || !cc ||
+        items.empty() || cc->fwd.empty())
+      return;
+    unsigned long long* clk = nullptr;
+    const size_t bytes = items.size() * sizeof(unsigned long long);
+    if (cudaMalloc(&clk, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    cudaMemsetAsync(clk, 0, bytes, st);
+    hp.band_clk = (uint64_t)(uintptr_t)clk;
+    int x = 0;
+    if (jit_ok) x = launch_hoisted_jit(hp, scratch, sms, st, nullptr);
+    if (x <= 0) x = launch_hoisted(hp, scratch, sms, st);
+    std::vector<unsigned long long> got(items.size(), 0);
+    cudaError_t e = x > 0 ? cudaMemcpyAsync(got.data(), clk, bytes,
+                                            cudaMemcpyDeviceToHost, st)
+                          : cudaErrorUnknown;
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(clk);
+    hp.band_clk = 0;
+    if (x > 0) bump_launches(1);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return;
+    }
+    // modelled cost of every item in the order it chose
+    const uint64_t total = 1ull << hp.band_free_bits;
+    const uint64_t n_seg = cc->fwd.size();
+    std::vector<double> pred(items.size(), 0.0);
+    double sum_pred = 0, sum_meas = 0, slots_main = 0;
+    size_t n_main = 0;
+    for (const BandItem& it : items) slots_main += (double)(it.g1 - it.g0);
+    slots_main /= (double)items.size();
+    for (size_t i = 0; i < items.size(); ++i) {
+      const BandItem& it = items[i];
+      const std::vector<double>& w = it.mirror ? cc->mir : cc->fwd;
+      for (uint64_t j = it.g0 * n_seg / total;
+           j < n_seg && total * j / n_seg < it.g1; ++j) {
+        const uint64_t lo = std::max<uint64_t>(it.g0, total * j / n_seg);
+        const uint64_t hi = std::min<uint64_t>(it.g1, total * (j + 1) / n_seg);
+        if (hi > lo) pred[i] += (double)(hi - lo) * w[j];
+      }
+      // (the small items of the extreme classes carry mostly fixed costs)
+      if ((double)(it.g1 - it.g0) < 0.5 * slots_main || got[i] == 0) continue;
+      sum_pred += pred[i];
+      sum_meas += (double)got[i];
+      ++n_main;
+    }
+    if (n_main < 8 || sum_pred <= 0 || sum_meas <= 0) return;
+    std::vector<double> ratio(items.size(), 1.0);
+    for (size_t i = 0; i < items.size(); ++i) {
+      const BandItem& it = items[i];
+      if ((double)(it.g1 - it.g0) < 0.5 * slots_main || got[i] == 0) continue;
+      double r = ((double)got[i] / sum_meas) / (pred[i] / sum_pred);
+      ratio[i] = std::min(1.15, std::max(0.87, r));
+    }
+    // scale each segment by the item that held its first slot
+    std::vector<size_t> order(items.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+      return items[a].g0 < items[b].g0;
+    });
+    std::lock_guard<std::mutex> lock(g_cost_mu);
+    CostCurves* mut = const_cast<CostCurves*>(cc);
+    size_t kk = 0;
+    for (uint64_t j = 0; j < n_seg; ++j) {
+      const uint64_t lo = total * j / n_seg;
+      while (kk + 1 < order.size() && items[order[kk]].g1 <= lo) ++kk;
+      mut->fwd[j] *= ratio[order[kk]];
+      mut->mir[j] *= ratio[order[kk]];
+    }
+    mut->calibrated += 1;
+    finish_curves(mut);
+    cache_put("cost3", mut->disk_key, curves_blob(*mut));
+  }
 }
 
 static constexpr int kTuneCandidates = 40;
@@ -805,6 +960,21 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
     if (ms < best_ms) {
       best_ms = ms;
       best = i;
+    }
+  }
+  // the winner's work items, balanced by measurement over its own range
+  if (!finalists.empty() && cands[best].band_rows) {
+    HoistParams hp;
+    fill_hoist(lat, &cands[best], &hp);
+    uint64_t run0, run1;
+    run_range(cands[best].k, &run0, &run1);
+    uint64_t len = std::min<uint64_t>(kTuneSliceConfigs >> hp.k, run1 - run0);
+    while (len & (len - 1)) len &= len - 1;
+    if (len) {
+      hp.run_begin = run0;
+      hp.run_end = run0 + len;
+      hp.hi_step = 1;
+      calibrate_items(lat, cands[best], hp, sms, scratch, st, jit_ok);
     }
   }
   cudaEventDestroy(e0);
@@ -1623,6 +1793,24 @@ int isd_band_costs(const isd_lattice* lat, const isd_plan_info* plan,
                  (int)run_bits, (int)n_seg, (int)samples, &c);
   std::memcpy(out, c.data(), c.size() * sizeof(double));
   return (int)c.size();
+}
+
+int isd_band_slot_order(const isd_lattice* lat, const isd_plan_info* plan,
+                        uint64_t run_begin, uint32_t run_bits, int reorder,
+                        uint8_t* pos_out) {
+  int rc = isd_validate(lat);
+  if (rc) return rc;
+  if (!plan || !pos_out || run_bits < 6 || run_bits > 28)
+    return fail(ISD_EINVAL, "bad band order arguments");
+  uint8_t pos[24] = {0};
+  band_slot_order(lat, *plan, run_begin, plan->lane_mask, plan->lane_vec,
+                  (int)run_bits, reorder != 0, pos);
+  const int F = (int)run_bits - 5;
+  uint32_t m[16], r[16];
+  if (band_slot_fields(pos, F, m, r) < 0)
+    return fail(ISD_EINVAL, "slot map needs too many fields");
+  std::memcpy(pos_out, pos, (size_t)F);
+  return F;
 }
 
 int isd_plan_range(const isd_lattice* lat, uint64_t start, uint64_t end,

@@ -185,11 +185,18 @@ __global__ void __launch_bounds__(PAIR >= 2 ? kWideThreads : kThreads)
   IsdLanes lanes;
 #pragma unroll
   for (int i = 0; i < 5; ++i) lanes.v[i] = P.lane_vec[i];
+  IsdSlotMap smap;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    smap.mask[j] = P.slot_mask[j];
+    smap.rot[j] = P.slot_rot[j];
+  }
   k1_hoisted_body<NC, DOUBLE, PAIR>(
       L, P.run_begin, P.run_end - P.run_begin, P.hi_step, P.lane_mask, lanes,
       reinterpret_cast<const IsdBandItem*>(P.band_items), P.band_n_items,
       (int)P.band_free_bits,
-      reinterpret_cast<unsigned int*>(P.band_claim), hist, out);
+      reinterpret_cast<unsigned int*>(P.band_claim), smap,
+      reinterpret_cast<unsigned long long*>(P.band_clk), hist, out);
 }
 
 // ---------------------------------------------------------------------------

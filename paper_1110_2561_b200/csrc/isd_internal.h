@@ -122,6 +122,11 @@ struct HoistParams {
   // banded launches: a zeroed u32 counter the blocks claim items from
   // (dynamic scheduling; 0 = static round-robin)
   uint64_t band_claim;
+  // calibration launches: device array of per-item SM cycles (0 = none)
+  uint64_t band_clk;
+  // banded launches: slot bits -> run bits (k1_body.cuh IsdSlotMap)
+  uint32_t slot_mask[16];
+  uint32_t slot_rot[16];
 };
 
 // Largest paired histogram (words): two CTAs of 512 threads per SM fit
@@ -175,7 +180,15 @@ void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
                     uint64_t run_begin, uint64_t lane_mask,
                     const uint64_t* lane_vec, int run_bits, int n_seg,
                     int samples, std::vector<double>* cost,
-                    std::vector<double>* cost_mirror = nullptr);
+                    std::vector<double>* cost_mirror = nullptr,
+                    const uint8_t* pos = nullptr);
+// order of the free run bits in a banded launch's slots, and the slot map
+// as bit fields (plan.cpp; k1_body.cuh IsdSlotMap)
+void band_slot_order(const isd_lattice* lat, const isd_plan_info& info,
+                     uint64_t run_begin, uint64_t lane_mask,
+                     const uint64_t* lane_vec, int run_bits, bool reorder,
+                     uint8_t* pos);
+int band_slot_fields(const uint8_t* pos, int F, uint32_t* mask, uint32_t* rot);
 void fill_hoist(const isd_lattice* lat, const isd_plan_info* info,
                 HoistParams* p);
 

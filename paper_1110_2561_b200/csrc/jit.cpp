@@ -181,13 +181,14 @@ static std::string generate(const HoistParams& P, int nc, bool dbl,
        "    unsigned long long hi_step, unsigned long long lane_mask,\n"
        "    const IsdLanes lanes, const IsdBandItem* items,\n"
        "    unsigned int n_items, int free_bits, unsigned int* claim,\n"
+       "    const IsdSlotMap smap, unsigned long long* item_clk,\n"
        "    unsigned long long* __restrict__ out) {\n"
        "  extern __shared__ __align__(16) unsigned int hist[];\n"
        "  const JitTraits L;\n"
        "  k1_hoisted_body<"
     << nc << ", " << (dbl ? "true" : "false") << ", "
     << P.pair << ">(L, run_begin, nruns, hi_step, lane_mask, lanes, items,\n"
-       "      n_items, free_bits, claim, hist, out);\n}\n";
+       "      n_items, free_bits, claim, smap, item_clk, hist, out);\n}\n";
   return o.str();
 }
 
@@ -404,6 +405,8 @@ static std::string jit_key(const HoistParams& P, int device) {
   q.band_free_bits = q.band_n_items = 0;  // launch arguments, not constants
   q.band_items = 0;
   q.band_claim = 0;
+  for (int j = 0; j < 16; ++j) q.slot_mask[j] = q.slot_rot[j] = 0;
+  q.band_clk = 0;
   std::string key(reinterpret_cast<const char*>(&q), sizeof q);
   key += std::to_string(device);
   key += knob_long("ISD_PROBE", 0) ? "|probe" : "";
@@ -460,8 +463,16 @@ int launch_hoisted_jit(const HoistParams& P, unsigned long long* out,
   unsigned int n_items = P.band_n_items;
   int free_bits = (int)P.band_free_bits;
   void* claim = reinterpret_cast<void*>(P.band_claim);
-  void* args[] = {&run_begin, &nruns,   &hi_step,   &lane_mask, &lanes,
-                  &items,     &n_items, &free_bits, &claim,     &out};
+  struct {
+    unsigned int mask[16], rot[16];
+  } smap;
+  for (int j = 0; j < 16; ++j) {
+    smap.mask[j] = P.slot_mask[j];
+    smap.rot[j] = P.slot_rot[j];
+  }
+  void* item_clk = reinterpret_cast<void*>(P.band_clk);
+  void* args[] = {&run_begin, &nruns,     &hi_step, &lane_mask, &lanes,    &items,
+                  &n_items,   &free_bits, &claim,   &smap,      &item_clk, &out};
   int grid = jk.per_sm * sm_count;
   const uint64_t need = (nruns + jk.threads - 1) / jk.threads;
   if (need < (uint64_t)grid) grid = (int)(need ? need : 1);

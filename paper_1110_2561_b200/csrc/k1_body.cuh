@@ -39,6 +39,18 @@ struct IsdBandItem {
   unsigned int q0, mirror;
 };
 
+// A banded launch's slot -> run-bit map: free bit i of a slot (the i-th bit
+// of its popcount-ordered value) lands on run bit pos(i), given as up to 16
+// fields of consecutive bits that move together: run bits of the slot =
+// OR_j rotl32(v & mask[j], rot[j]).  The natural order (i-th lowest
+// non-pivot run bit) is one such map; the host may instead put the run
+// sites that decide an item's bank conflicts on top of the order, so that
+// the slots of an item agree on them (capi.cu band_slot_order).
+struct IsdSlotMap {
+  unsigned int mask[16];
+  unsigned int rot[16];
+};
+
 // The layout of a mirrored work item: row r of the band lives at row
 // band_rows - 1 - r, i.e. the row stride is -A from an origin at the last
 // row.  Which banks the 32 lanes' words fall on depends on the sign of the
@@ -177,7 +189,8 @@ __device__ __forceinline__ void k1_hoisted_body(
     unsigned long long hi_step, unsigned long long lane_mask,
     const IsdLanes lanes, const IsdBandItem* __restrict__ items,
     unsigned int n_items, int free_bits, unsigned int* claim,
-    unsigned int* hist, unsigned long long* __restrict__ out) {
+    const IsdSlotMap& smap, unsigned long long* item_clk, unsigned int* hist,
+    unsigned long long* __restrict__ out) {
   auto zero_hist = [&]() {
     uint4* h4 = reinterpret_cast<uint4*>(hist);
     const unsigned int n4 = L.n_hist() * L.hist_words() / 4;
@@ -211,6 +224,15 @@ __device__ __forceinline__ void k1_hoisted_body(
       m ^= low;
     }
     return run_begin + (hi ^ lane_dep);
+  };
+  // banded launches: the slot's bits through the launch's slot map
+  auto band_run = [&](unsigned long long v) {
+    const unsigned int x = (unsigned int)v;
+    unsigned int r = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      r |= __funnelshift_l(x & smap.mask[j], x & smap.mask[j], smap.rot[j]);
+    return run_begin + ((unsigned long long)r ^ lane_dep);
   };
   // ---- one run: bits [k, N) fixed; table rows are m - row_off ----
   auto run_body = [&](const auto& L, unsigned long long r,
@@ -703,6 +725,9 @@ __device__ __forceinline__ void k1_hoisted_body(
       const unsigned int it = cur_item;
       if (it >= n_items) break;
       const IsdBandItem item = items[it];
+      // (calibration launches: SM cycles of this item's walk and flush, for
+      // the host to correct its cost model with — capi.cu calibrate_items)
+      const long long clk0 = item_clk ? clock64() : 0;
 #ifdef ISD_PROBE
       const long long t_item = clock64();
       long long t_first = 0;
@@ -748,12 +773,12 @@ __device__ __forceinline__ void k1_hoisted_body(
         if (item.mirror) {
           const IsdMirror<T> M(L);
           for (unsigned int i = 0; i < cnt; ++i) {
-            run_body(M, slot_run(v), row_off);
+            run_body(M, band_run(v), row_off);
             v = isd_next_slot(v, free_bits, &q);
           }
         } else {
           for (unsigned int i = 0; i < cnt; ++i) {
-            run_body(L, slot_run(v), row_off);
+            run_body(L, band_run(v), row_off);
             v = isd_next_slot(v, free_bits, &q);
           }
         }
@@ -770,6 +795,8 @@ __device__ __forceinline__ void k1_hoisted_body(
       else
         flush(L, row_off, L.band_rows());
       __syncthreads();
+      if (item_clk && threadIdx.x == 0)
+        item_clk[it] = (unsigned long long)(clock64() - clk0);
 #ifdef ISD_PROBE
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(probe_last));
       // (probe build) per item: first chunk start, this warp's end, last

@@ -25,10 +25,11 @@ std::map<std::string, std::string> g_knobs;
 // every knob the library consults (a typo is an error, not a silent no-op)
 const char* const kKnownKnobs[] = {
     "ISD_AUTOTUNE",          "ISD_BAND",
+    "ISD_BAND_CALIBRATE",
     "ISD_BAND_DOMINO",       "ISD_BAND_DOMINO_LOOP_BITS",
     "ISD_BAND_DYNAMIC",      "ISD_BAND_ITEMS_PER_SM",
     "ISD_BAND_LOOP_BITS",    "ISD_BAND_MIRROR",
-    "ISD_BAND_SPAN",
+    "ISD_BAND_ORDER",        "ISD_BAND_SPAN",
     "ISD_BAND_WEIGHTS",      "ISD_CLIMB_STARTS",
     "ISD_CLIMB_STEPS",       "ISD_COPY_VARIANT",
     "ISD_GPU_CLIMB",         "ISD_GRAY",

@@ -1329,7 +1329,7 @@ void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
                     uint64_t run_begin, uint64_t lane_mask,
                     const uint64_t* lane_vec, int run_bits, int n_seg,
                     int samples, std::vector<double>* cost,
-                    std::vector<double>* cost_mirror) {
+                    std::vector<double>* cost_mirror, const uint8_t* pos) {
   const int k = (int)info.k;
   const uint64_t free_mask =
       ((run_bits >= 64) ? ~0ull : ((1ull << run_bits) - 1)) & ~lane_mask;
@@ -1381,8 +1381,14 @@ void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
     const uint64_t g1 = total * (uint64_t)(sg + 1) / (uint64_t)n_seg;
     double tot = 0, tot_m = 0;
     for (int s = 0; s < samples; ++s) {
-      const uint64_t slot =
-          deposit(unrank(g0 + rng_next(&seed) % (g1 - g0)), free_mask);
+      const uint64_t sv = unrank(g0 + rng_next(&seed) % (g1 - g0));
+      uint64_t slot = 0;  // the slot's bits on their run bits
+      if (pos) {
+        for (int i = 0; i < F; ++i)
+          if ((sv >> i) & 1) slot |= 1ull << pos[i];
+      } else {
+        slot = deposit(sv, free_mask);
+      }
       const uint64_t jb = deposit(rng_next(&seed), info.loop_mask);
       uint64_t cb = 0;
       const uint64_t c = rng_next(&seed);
@@ -1441,6 +1447,155 @@ void band_slot_cost(const isd_lattice* lat, const isd_plan_info& info,
       for (int sg; (sg = next.fetch_add(1)) < n_seg;) run_segment(sg);
     });
   for (auto& th : pool) th.join();
+}
+
+// The slot map of a banded launch as fields of consecutive bits that move
+// together (k1_body.cuh IsdSlotMap): free bit i -> run bit pos[i].  Returns
+// the number of fields, or -1 if more than 16 would be needed.
+int band_slot_fields(const uint8_t* pos, int F, uint32_t* mask, uint32_t* rot) {
+  for (int j = 0; j < 16; ++j) mask[j] = rot[j] = 0;
+  int n = 0;
+  for (int i = 0; i < F;) {
+    int j = i;
+    while (j + 1 < F && pos[j + 1] == pos[j] + 1) ++j;
+    if (n == 16) return -1;
+    mask[n] = (uint32_t)(((1ull << (j + 1)) - 1) & ~((1ull << i) - 1));
+    rot[n] = (uint32_t)((pos[i] - i) & 31);
+    ++n;
+    i = j + 1;
+  }
+  return n;
+}
+
+// Order of the free run bits in a banded launch's slots.  Whether an item
+// is cheaper with its rows ascending or descending (band_slot_cost) is
+// decided by a few run sites — the neighbours of the lane sites — and an
+// item is a contiguous range of the (popcount, colex) slot order: with
+// those sites on the most significant slot bits the slots of an item agree
+// on them, and the per-item choice is nearly a per-slot one (c5: modelled
+// wavefronts per RED 1.078 -> ~1.05).  Influence of a free bit = how far
+// the mean of (ascending - descending cost) moves with it, over `slots`
+// random slots; bits above a quarter of the largest influence go on top,
+// strongest last, the rest keep their natural order below.  pos[i] = run
+// bit of slot bit i.  Fixed seed: the same plan gives the same order.
+void band_slot_order(const isd_lattice* lat, const isd_plan_info& info,
+                     uint64_t run_begin, uint64_t lane_mask,
+                     const uint64_t* lane_vec, int run_bits, bool reorder,
+                     uint8_t* pos) {
+  const uint64_t free_mask =
+      ((run_bits >= 64) ? ~0ull : ((1ull << run_bits) - 1)) & ~lane_mask;
+  const int F = popc64(free_mask);
+  std::vector<int> natural;
+  for (int b = 0; b < run_bits; ++b)
+    if ((free_mask >> b) & 1) natural.push_back(b);
+  for (int i = 0; i < F && i < 24; ++i) pos[i] = (uint8_t)natural[(size_t)i];
+  if (!reorder || F < 8 || F > 23 || run_bits > 31) return;
+  const int k = (int)info.k;
+  uint64_t dep[32];
+  for (int lane = 0; lane < 32; ++lane) {
+    dep[lane] = 0;
+    for (int i = 0; i < 5; ++i)
+      if ((lane >> i) & 1) dep[lane] ^= lane_vec[i];
+  }
+  const bool tri = info.pair_mode == 3;
+  const uint64_t p0bit = 1ull << info.copy_site[kCopyBits - 1];
+  const uint64_t p1bit = 1ull << info.copy_site[kCopyBits - 2];
+  const uint64_t p2bit = 1ull << info.copy_site[kCopyBits - 3];
+  const int d0 = (int)info.pair_degree[0], d1 = (int)info.pair_degree[1];
+  const int unpaired = kCopyBits - (tri ? 3 : 2);
+  constexpr int kSlots = 4096, kPer = 6;
+  std::vector<double> sum1((size_t)F, 0.0), sum0((size_t)F, 0.0);
+  std::vector<int> n1((size_t)F, 0), n0((size_t)F, 0);
+  uint64_t seed = 0xD1B54A32D192ED03ull;
+  for (int sidx = 0; sidx < kSlots; ++sidx) {
+    const uint64_t sv = rng_next(&seed) & ((1ull << F) - 1);
+    const uint64_t slot = deposit(sv, free_mask);
+    double d = 0;
+    for (int rep = 0; rep < kPer; ++rep) {
+      const uint64_t jb = deposit(rng_next(&seed), info.loop_mask);
+      uint64_t cb = 0;
+      const uint64_t c = rng_next(&seed);
+      for (int t = 0; t < unpaired; ++t)
+        if ((c >> t) & 1) cb |= 1ull << info.copy_site[t];
+      int64_t rest[32], row[32];
+      for (int lane = 0; lane < 32; ++lane) {
+        const uint64_t run = run_begin + (slot ^ dep[lane]);
+        const uint64_t x = (run << k) | jb | cb;
+        const int e = energy_of(lat, x);
+        const int eh = info.e_mode ? (e - (e & 1)) / 2 : e;
+        const int par = info.e_mode ? (e & 1) : 0;
+        row[lane] = popc64(x);
+        rest[lane] = (int64_t)eh * info.e_words + par * info.plane_words;
+        if (tri) {
+          const int base = d0 + info.pair_both;
+          const int a = (base - (energy_of(lat, x | p0bit) - e)) / 2;
+          const int b = (base - (energy_of(lat, x | p1bit) - e)) / 2;
+          const int cc = (base - (energy_of(lat, x | p2bit) - e)) / 2;
+          rest[lane] += (int64_t)tri_index(a, b, cc) * info.pair_words[0];
+        } else {
+          const int a = (d0 - (energy_of(lat, x | p0bit) - e)) / 2;
+          const int b = (d1 - (energy_of(lat, x | p1bit) - e)) / 2;
+          rest[lane] += (int64_t)a * info.pair_words[0] +
+                        (int64_t)b * info.pair_words[1];
+        }
+      }
+      auto wavefronts = [&](int64_t row_words) {
+        int64_t words[32];
+        for (int lane = 0; lane < 32; ++lane)
+          words[lane] = row[lane] * row_words + rest[lane];
+        std::sort(words, words + 32);
+        int per_bank[32] = {0};
+        int worst = 0;
+        for (int i = 0; i < 32; ++i)
+          if (i == 0 || words[i] != words[i - 1]) {
+            const int b = (int)(((words[i] % 32) + 32) % 32);
+            worst = std::max(worst, ++per_bank[b]);
+          }
+        return worst;
+      };
+      d += wavefronts((int64_t)info.row_words) -
+           wavefronts(-(int64_t)info.row_words);
+    }
+    for (int i = 0; i < F; ++i)
+      if ((sv >> i) & 1) {
+        sum1[(size_t)i] += d;
+        ++n1[(size_t)i];
+      } else {
+        sum0[(size_t)i] += d;
+        ++n0[(size_t)i];
+      }
+  }
+  std::vector<double> infl((size_t)F, 0.0);
+  double top = 0;
+  for (int i = 0; i < F; ++i) {
+    if (n1[(size_t)i] && n0[(size_t)i])
+      infl[(size_t)i] = std::fabs(sum1[(size_t)i] / n1[(size_t)i] -
+                                  sum0[(size_t)i] / n0[(size_t)i]);
+    top = std::max(top, infl[(size_t)i]);
+  }
+  if (top <= 0) return;
+  std::vector<int> low, high;
+  for (int i = 0; i < F; ++i)
+    (infl[(size_t)i] > 0.25 * top ? high : low).push_back(i);
+  if (high.empty() || low.empty()) return;
+  // strongest influence = most significant slot bit; if that breaks the map
+  // into too many fields, the influential bits keep their natural order
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    std::vector<int> hs(high);
+    if (attempt == 0)
+      std::stable_sort(hs.begin(), hs.end(), [&](int a, int b) {
+        return infl[(size_t)a] < infl[(size_t)b];
+      });
+    uint8_t cand[24];
+    int i = 0;
+    for (int b : low) cand[i++] = (uint8_t)natural[(size_t)b];
+    for (int b : hs) cand[i++] = (uint8_t)natural[(size_t)b];
+    uint32_t m[16], r[16];
+    if (band_slot_fields(cand, F, m, r) >= 0) {
+      for (int j = 0; j < F; ++j) pos[j] = cand[j];
+      return;
+    }
+  }
 }
 
 // Work items of a launch over 2^F slots (popcount order): ~n_target items of

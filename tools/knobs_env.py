@@ -13,8 +13,8 @@ import os
 
 def apply() -> dict:
     from paper_1110_2561_b200 import _native
-    names = ("ISD_AUTOTUNE ISD_BAND ISD_BAND_DOMINO ISD_BAND_DOMINO_LOOP_BITS "
-             "ISD_BAND_DYNAMIC ISD_BAND_ITEMS_PER_SM ISD_BAND_LOOP_BITS ISD_BAND_MIRROR "
+    names = ("ISD_AUTOTUNE ISD_BAND ISD_BAND_CALIBRATE ISD_BAND_DOMINO ISD_BAND_DOMINO_LOOP_BITS "
+             "ISD_BAND_DYNAMIC ISD_BAND_ITEMS_PER_SM ISD_BAND_LOOP_BITS ISD_BAND_MIRROR ISD_BAND_ORDER "
              "ISD_BAND_SPAN ISD_BAND_WEIGHTS ISD_CLIMB_STARTS ISD_CLIMB_STEPS "
              "ISD_COPY_VARIANT ISD_GPU_CLIMB ISD_GRAY ISD_GRID_SMS "
              "ISD_HIST_BYTES ISD_JIT ISD_JIT_DUMP ISD_LAYOUT ISD_LOOP_BITS "
