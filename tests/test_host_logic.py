@@ -726,3 +726,30 @@ def test_cluster_flush_folded_sums_equal_direct_gather(R, I1):
             folded[r, e] = s
     assert np.array_equal(direct, folded)
     assert 6 * R + 4 <= len(planes)
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+@pytest.mark.parametrize("log_hint", [33, 36])
+def test_band_slot_order_is_a_permutation_of_the_free_run_bits(name, log_hint):
+    # capi.cu band_slot_order / k1_body.cuh IsdSlotMap: slot bit i lands on
+    # run bit pos[i]; any order must be a bijection onto the run bits that
+    # are not lane pivots (every run is then walked exactly once), and the
+    # natural order is the increasing one
+    from paper_1110_2561_b200 import _native
+    from paper_1110_2561_b200.enumeration import native_lattice
+    from paper_1110_2561_b200.workloads import workloads
+    spec = workloads()[name].spec
+    lat = native_lattice(spec)
+    _native.set_knob("ISD_BAND", "1")
+    _native.set_knob("ISD_PAIR", "3")
+    ok, plan = _native.plan(lat, 1 << log_hint)
+    if not plan.band_rows:
+        pytest.skip("no banded plan")
+    run_bits = log_hint - plan.k
+    free = [b for b in range(run_bits) if not (plan.lane_mask >> b) & 1]
+    natural = list(_native.band_slot_order(lat, plan, 0, run_bits, False))
+    assert natural == free
+    ordered = list(_native.band_slot_order(lat, plan, 0, run_bits, True))
+    assert sorted(ordered) == free
+    # deterministic (fixed seed): the same plan gives the same order
+    assert ordered == list(_native.band_slot_order(lat, plan, 0, run_bits, True))
