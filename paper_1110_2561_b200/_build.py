@@ -84,9 +84,10 @@ def build(force: bool = False, verbose: bool = False,
         h.update(open(f, "rb").read())
     extra.append(f"-DISD_BUILD_ID=\"{h.hexdigest()[:16]}{'-dbg' if debug else ''}\"")
 
-    def compile_one(src):
-        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
-        cmd = [nvcc_path(), *extra, *compile_flags, "-I",
+    def compile_one(unit):
+        src, defines, name = unit
+        obj = os.path.join(objdir, name + ".o")
+        cmd = [nvcc_path(), *extra, *defines, *compile_flags, "-I",
                os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src),
                "-o", obj]
         if verbose:
@@ -94,9 +95,19 @@ def build(force: bool = False, verbose: bool = False,
         subprocess.run(cmd, check=True)
         return obj
 
+    # enumerate.cu holds the hoisted kernel's 64 instantiations: compiled as
+    # four translation units (ISD_HOIST_PART, two class counts each)
+    units = []
+    for src in SOURCES:
+        stem = os.path.splitext(src)[0]
+        if src == "enumerate.cu":
+            units += [(src, [f"-DISD_HOIST_PART={p}"], f"{stem}_{p}")
+                      for p in range(4)]
+        else:
+            units.append((src, [], stem))
     from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
-        objs = list(pool.map(compile_one, SOURCES))
+    with ThreadPoolExecutor(max_workers=len(units)) as pool:
+        objs = list(pool.map(compile_one, units))
     cmd = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a",
            "-shared", *objs, "-ldl", "-o", lib + ".tmp"]
     subprocess.run(cmd, check=True)

@@ -46,7 +46,13 @@
 
 #include "k1_body.cuh"
 
+#ifndef ISD_HOIST_PART
+#define ISD_HOIST_PART 0
+#endif
+
 namespace isd {
+#if ISD_HOIST_PART == 0
+
 
 __device__ __forceinline__ void red_shared_inc(uint32_t addr) {
   isd_red_shared_inc(addr);
@@ -112,6 +118,8 @@ __global__ void __launch_bounds__(kThreads)
   __syncthreads();
   flush_hist(hist, P.n_hist, P.hist_words, P.nbins, out);
 }
+
+#endif  // ISD_HOIST_PART == 0
 
 // ---------------------------------------------------------------------------
 // hoisted kernel (ahead-of-time build; body in k1_body.cuh)
@@ -199,6 +207,7 @@ __global__ void __launch_bounds__(PAIR >= 2 ? kWideThreads : kThreads)
       reinterpret_cast<unsigned long long*>(P.band_clk), hist, out);
 }
 
+#if ISD_HOIST_PART == 0
 // ---------------------------------------------------------------------------
 // flip-symmetry completion: rows m and N-m both become their sum
 // ---------------------------------------------------------------------------
@@ -308,6 +317,8 @@ int hoisted_block(const void* fn, size_t smem, int sm_count, bool may_widen,
   return threads;
 }
 
+#endif  // ISD_HOIST_PART == 0
+
 template <int NC, bool D, int PR>
 static int launch_hoist_t(const HoistParams& p, unsigned long long* out,
                           int sm_count, cudaStream_t st) {
@@ -324,22 +335,49 @@ static int launch_hoist_t(const HoistParams& p, unsigned long long* out,
   return e == cudaSuccess ? 1 : -(int)e;
 }
 
-int launch_hoisted(const HoistParams& p, unsigned long long* out, int sm_count,
-                   void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+// The hoisted kernel's instantiations (8 class counts x double bonds x 4
+// pairing modes) are split over four translation units by class count —
+// the build compiles this file once per ISD_HOIST_PART = 0..3 in parallel;
+// part p holds NC = 2p + 1 and 2p + 2, part 0 also everything else here.
+#define ISD_PART_NAME2(p) launch_hoisted_part##p
+#define ISD_PART_NAME(p) ISD_PART_NAME2(p)
+int ISD_PART_NAME(ISD_HOIST_PART)(const HoistParams& p,
+                                  unsigned long long* out, int sm_count,
+                                  cudaStream_t st) {
   const bool dbl = p.has_double != 0;
   switch (p.n_classes * 4 + (p.pair > 3 ? 0 : p.pair)) {
 #define CASE1(NC, PR)                                                  \
-  case NC * 4 + PR:                                                    \
-    return dbl ? launch_hoist_t<NC, true, PR>(p, out, sm_count, st)    \
-               : launch_hoist_t<NC, false, PR>(p, out, sm_count, st);
+  case (NC) * 4 + PR:                                                  \
+    return dbl ? launch_hoist_t<(NC), true, PR>(p, out, sm_count, st)  \
+               : launch_hoist_t<(NC), false, PR>(p, out, sm_count, st);
 #define CASE(NC) CASE1(NC, 0) CASE1(NC, 1) CASE1(NC, 2) CASE1(NC, 3)
-    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8)
+    CASE(2 * ISD_HOIST_PART + 1) CASE(2 * ISD_HOIST_PART + 2)
 #undef CASE
 #undef CASE1
     default:
       return -(int)cudaErrorInvalidValue;
   }
 }
+
+#if ISD_HOIST_PART == 0
+int launch_hoisted_part1(const HoistParams&, unsigned long long*, int,
+                         cudaStream_t);
+int launch_hoisted_part2(const HoistParams&, unsigned long long*, int,
+                         cudaStream_t);
+int launch_hoisted_part3(const HoistParams&, unsigned long long*, int,
+                         cudaStream_t);
+
+int launch_hoisted(const HoistParams& p, unsigned long long* out, int sm_count,
+                   void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  switch ((p.n_classes - 1) / 2) {
+    case 0: return launch_hoisted_part0(p, out, sm_count, st);
+    case 1: return launch_hoisted_part1(p, out, sm_count, st);
+    case 2: return launch_hoisted_part2(p, out, sm_count, st);
+    case 3: return launch_hoisted_part3(p, out, sm_count, st);
+    default: return -(int)cudaErrorInvalidValue;
+  }
+}
+#endif
 
 }  // namespace isd
