@@ -204,3 +204,33 @@ def test_mirrored_band_items_match_c_oracle(spec, pair, mirror, jit):
         pytest.skip("no banded plan for this lattice")
     got = isd.full_dos(spec)
     assert np.array_equal(got.counts, oracle_table(spec))
+
+
+# Large aligned shards through the default path (autotuned plan, NVRTC
+# kernel, banded mode-3 tables with mirrored items in influence order,
+# calibrated cuts) on lattices outside the BASELINE set: one 2^33-
+# configuration shard each, bit-exact against the C oracle's walk of the
+# same range.
+LARGE_SHARDS = [
+    (isd.LatticeSpec(5, 7), 3),
+    (isd.LatticeSpec(2, 17, boundary="free"), 1),
+    (isd.LatticeSpec(4, 9, 1, -1), 5),
+    (isd.LatticeSpec(3, 4, 3, 1, bond_signs=isd.random_bond_signs(
+        isd.LatticeSpec(3, 4, 3), 4242)), 6),
+    (isd.LatticeSpec(6, 6, 1, 1, boundary="free",
+                     bond_signs=isd.random_bond_signs(
+                         isd.LatticeSpec(6, 6, boundary="free"), 99)), 2),
+    (isd.LatticeSpec(3, 3, 4), 5),
+]
+
+
+@pytest.mark.parametrize("spec,index", LARGE_SHARDS,
+                         ids=[repr(s) for s, _ in LARGE_SHARDS])
+def test_large_aligned_shard_matches_c_oracle(spec, index):
+    size = 1 << 33
+    start = index * size
+    assert start + size <= spec.num_configs
+    got, _ = enumerate_range_timed(spec, start, start + size)
+    assert _native.kernel_info().startswith("k1_hoisted")
+    want = oracle_table(spec, start, start + size)
+    assert np.array_equal(got.view(np.int64), want)
