@@ -179,10 +179,13 @@ __device__ __forceinline__ unsigned int isd_tri_index(int a, int b, int c) {
 // unsatisfied external bonds; the flush credits the subset U flipped up to
 // (m + |U|, e + sum_U (R - 2 n_i) + [|U| = 1 or 2] pair_both).
 //
-// Banded tables (L.band_rows() > 0, mode 2): the table holds band_rows rows
-// of m relative to a work item's base row; the launch walks work items
-// (slots of the free run bits in popcount order, `items`), each zeroed,
-// walked and flushed in turn.
+// Banded tables (L.band_rows() > 0, modes 2 and 3): the table holds
+// band_rows rows of m relative to a work item's base row; the launch walks
+// work items (slots of the free run bits in popcount order, `items`), each
+// zeroed, walked and flushed in turn.  A slot's bits reach their run bits
+// through `smap`; an item marked `mirror` keeps its rows in descending
+// order (IsdMirror); `item_clk`, when given, receives every item's SM
+// cycles (the host's calibration launch).
 template <int NC, bool DOUBLE, int PAIR, class T>
 __device__ __forceinline__ void k1_hoisted_body(
     const T& L, unsigned long long run_begin, unsigned long long nruns,
