@@ -645,13 +645,13 @@ static void calibrate_items(const isd_lattice* lat, const isd_plan_info& info,
     if (x > 0) bump_launches(1);
     return x > 0;
   };
-  // the walk's time with the current curves' items (best of two launches)
+  // the walk's time with the current curves' items (best of three launches)
   auto walk_ms = [&](const CostCurves** cc, std::vector<BandItem>* items) {
     if (set_band_launch(lat, info, &hp, sms, true, cc, items) || !*cc ||
         items->empty() || (*cc)->fwd.empty())
       return -1.f;
     float best = 1e30f;
-    for (int rep = 0; rep < 2; ++rep) {
+    for (int rep = 0; rep < 3; ++rep) {
       float t = 0.f;
       cudaEventRecord(e0, st);
       const bool ok = launch(hp);
@@ -755,14 +755,15 @@ static void calibrate_items(const isd_lattice* lat, const isd_plan_info& info,
       }
       finish_curves(mut);
     }
+    // (the second round starts from the first's cut either way; whichever
+    // of the three cuts measured fastest is restored below)
     const float ms = walk_ms(&cc, &items);
-    if (ms > 0 && ms < best_ms * 0.999f) {
+    if (ms <= 0) break;
+    if (ms < best_ms * 0.999f) {
       best_ms = ms;
       keep_fwd = cc->fwd;
       keep_mir = cc->mir;
       improved = true;
-    } else {
-      break;  // (the curves are restored below)
     }
   }
   if (cc && !keep_fwd.empty()) {
@@ -786,11 +787,14 @@ static constexpr uint64_t kTuneSliceConfigs = 1ull << 36;
 // Time the model's best layouts on `st` and keep the fastest.  Synchronous.
 // Candidates may differ in loop width (banded plans use a shorter loop), so
 // each is timed on its own run range of [start, end).
-static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
+// Returns false when the winner's two timed launches disagreed by more than
+// 15% (another process was using the GPU): the pick then serves this
+// process but is not written to the disk cache.
+static bool autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
                      uint64_t end, int sms, isd_plan_info* info,
                      uint64_t top) {
   NvtxRange nvtx("isd:autotune");
-  if (knob_long("ISD_AUTOTUNE", 1) == 0) return;
+  if (knob_long("ISD_AUTOTUNE", 1) == 0) return true;
   const std::string key = plan_key(lat, hint, top);
   std::vector<isd_plan_info> cands;
   {
@@ -798,7 +802,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
     PlanEntry& pe = g_plans[key];
     if (pe.tuned || pe.rc) {
       *info = pe.info;
-      return;
+      return true;
     }
     pe.tuned = true;
     const int n_cand = (int)knob_long("ISD_TUNE_CANDIDATES", kTuneCandidates);
@@ -807,7 +811,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
       if (!pe.ranked[i].band_rows || band_ok(pe.ranked[i], start, end))
         cands.push_back(pe.ranked[i]);
   }
-  if (cands.size() < 2) return;
+  if (cands.size() < 2) return true;
   // tuning runs on a private stream (never the caller's, which may be
   // capturing a graph or carry unrelated work); it is synchronous, and
   // waits for the device to drain first: a candidate timed while other
@@ -817,7 +821,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
   cudaStream_t st = nullptr;
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
     cudaGetLastError();
-    return;
+    return true;
   }
   const size_t bytes =
       (size_t)(lat->n_spins + 1) * (lat->n_bonds + 1) * sizeof(uint64_t);
@@ -825,7 +829,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
   if (cudaMalloc(&scratch, bytes) != cudaSuccess) {
     cudaGetLastError();
     cudaStreamDestroy(st);
-    return;
+    return true;
   }
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -963,6 +967,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
     jit_prefetch(ps);
   }
   float best_ms = 1e30f;
+  bool steady = true;
   size_t best = finalists.empty() ? 0 : finalists[0];
   for (size_t i : finalists) {
     HoistParams hp;
@@ -1008,6 +1013,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
     // best of two timed launches: one noisy timing picked a plan ~9%
     // slower on c4 once (31.1 vs 33.9e12 configs/s)
     ms = 1e30f;
+    float slowest = 0.f;
     for (int rep = 0; rep < 2; ++rep) {
       float t = 0.f;
       cudaEventRecord(e0, st);
@@ -1020,11 +1026,14 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
       cudaEventElapsedTime(&t, e0, e1);
       bump_launches(1);
       ms = std::min(ms, t);
+      slowest = std::max(slowest, t);
     }
+    const bool unsteady = slowest > 1.15f * ms;
     ms /= (float)len * (float)(1ull << hp.k);  // per configuration
     if (ms < best_ms) {
       best_ms = ms;
       best = i;
+      steady = !unsteady;
     }
   }
   // the winner's work items, balanced by measurement over its own range
@@ -1052,6 +1061,7 @@ static void autotune(const isd_lattice* lat, uint64_t hint, uint64_t start,
   PlanEntry& pe = g_plans[key];
   pe.info = cands[best];
   *info = pe.info;
+  return steady;
 }
 
 // The best plan the model found without a banded table (banded plans need
@@ -1153,7 +1163,7 @@ static int walk_plan(const isd_lattice* lat, uint64_t start, uint64_t end,
   }
   const int rc = cached_plan(lat, len, info, top);
   if (rc || !tune || capturing) return rc;
-  autotune(lat, len, start, end, sms, info, top);
+  if (!autotune(lat, len, start, end, sms, info, top)) return 0;
   // remember the winner (and the best unbanded plan, for unaligned ranges)
   std::string blob(4, '\0');
   uint32_t n = 1;
